@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""Benchmark of the boosted-SFW hot path on B200 (driver contract: one JSON line).
+
+Headline (`metric`): certificate voxel-candidates/s on BASELINE config 4 —
+eta over every voxel of a 512^3 fp32 residual x 16 (sigma, d) candidates
+with the global argmax — one "step" = one full certificate evaluation.
+Secondary (`secondary`): cost+gradient evaluations/s on config 5 (256^3,
+N=1000 atoms, random std-0.1 perturbations).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Multi-GPU (torchrun, one rank per GPU): x-slabs of the output grid per rank
+on the replicated residual; the only collective is the all-gather of the
+16-byte argmax records (and the max-over-ranks timing). scaling = strong.
+`--impl reference` times the reference algorithm (the CPU oracle port of
+sfw3d's FFT eta_field, threads over candidates as the reference's
+map_ordered does) on rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--n", type=int, default=512, help="config-4 grid size (512 = BASELINE)")
+    ap.add_argument("--tap-tol", type=float, default=1e-12)
+    ap.add_argument("--mode", choices=("auto", "direct"), default="auto")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--cg-steps", type=int, default=20)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- clocks
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------ distributed
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text())
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "fallback": True}
+
+
+# ------------------------------------------------------ CPU oracle timing
+def oracle_cert_sample(residual: np.ndarray, kernel: np.ndarray, cands, threads: int, reps: int,
+                       warm: int):
+    """The reference's FFT eta_field (certificate.py:156-172) restated by the
+    oracle, over `len(cands)` candidates mapped on `threads` host threads.
+    Returns (seconds per step list, voxel-candidates per step)."""
+    from concurrent.futures import ThreadPoolExecutor
+    import scipy.fft as sfft
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import sfw3d_oracle as O
+    dims = residual.shape
+    khat = O.psf_hat(kernel)
+    hats = [O.template_hats(khat, dims, [s], [d])[0] for s, d in cands]
+
+    def one(h, rhat):
+        vals = sfft.irfftn(rhat * np.conj(h), s=dims)
+        i = int(np.argmax(vals))
+        return float(vals.flat[i]), i
+
+    times = []
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        for it in range(warm + reps):
+            t0 = time.perf_counter()
+            rhat = sfft.rfftn(residual)
+            res = list(pool.map(lambda h: one(h, rhat), hats))
+            _ = max(res)
+            if it >= warm:
+                times.append(time.perf_counter() - t0)
+    return times, int(np.prod(dims)) * len(cands)
+
+
+def host_residual_cfg4(inst):
+    """Host (numpy) copy of the cfg-4 residual for the CPU arms."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import sfw3d_oracle as O
+    rng = np.random.default_rng(4)
+    r = rng.standard_normal(inst.dims)
+    r += O.conv(O.render(inst.truth, inst.dims), O.psf_hat(inst.kernel))
+    return r.astype(np.float32).astype(np.float64)
+
+
+def reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import psutil
+    from paper_2009_05473_b200 import configs
+    inst = configs.config4(n=args.n)
+    residual = host_residual_cfg4(inst)
+    cands = [(s, d) for s in inst.sigma_grid for d in inst.shape_grid]
+    nproc = os.cpu_count() or 1
+    per_thread = 4.5 * residual.nbytes  # hat + product + field + slack
+    avail = psutil.virtual_memory().available - 3 * residual.nbytes
+    threads = max(1, min(nproc, len(cands), int(avail // per_thread)))
+    sample = cands[-threads:]
+    times, vc = oracle_cert_sample(residual, inst.kernel, sample, threads, args.steps,
+                                   max(0, min(args.warmup, 1)))
+    t = statistics.median(times)
+    value = vc / t
+    line = {
+        "impl": "reference", "metric": "certificate voxel-candidates/s", "value": value,
+        "unit": "voxel-candidates/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cfg4 certificate {args.n}^3 x {len(sample)} of 16 candidates "
+                               "(FFT eta_field, oracle port of sfw3d certificate.py:140-184)"},
+        "cpu_baseline": {"value": value, "unit": "voxel-candidates/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"{len(sample)} candidates x {args.n}^3 per step "
+                                   f"(threads over candidates, median of {len(times)})"},
+        "e2e": {"value": value, "unit": "voxel-candidates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- our arm
+def cert_workload(args, rank, world, dev):
+    import torch
+    import paper_2009_05473_b200 as P
+    from paper_2009_05473_b200 import _native as N, configs
+    from paper_2009_05473_b200.certificate import eta_argmax_dev
+    from paper_2009_05473_b200.forward import psf_apply_dev, render_dev
+
+    P.set_precision("f32")
+    inst = configs.config4(n=args.n)
+    dims = inst.dims
+    psf = P.Psf(P.Volume(inst.kernel), normalize=False)
+    table = P.build_template_table(psf, inst.sigma_grid, inst.shape_grid, tap_tol=args.tap_tol,
+                                   mode=args.mode)
+    info = table.info()
+    g = torch.Generator(device=dev)
+    g.manual_seed(4)
+    residual = torch.randn(dims, generator=g, device=dev, dtype=torch.float32)
+    residual += psf_apply_dev(psf, render_dev(inst.truth, dims, N.F32), False)
+    n = dims[0]
+    x0, x1 = rank * n // world, (rank + 1) * n // world - 1
+    window = ((x0, x1), (0, dims[1] - 1), (0, dims[2] - 1))
+    ctx = N.context(dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        return eta_argmax_dev(residual, 1.0, table, window)[0]
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = Clocks(dev)
+    clocks.start()
+    l0 = ctx.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        best = step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    launches = ctx.launches - l0
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    # global argmax over ranks: all-gather (value, cand, linear index)
+    rec = torch.tensor([best.value, float(best.cand),
+                        float((best.pos[0] * dims[1] + best.pos[1]) * dims[2] + best.pos[2])],
+                       dtype=torch.float64, device=dev)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        allrec = [torch.empty_like(rec) for _ in range(world)]
+        torch.distributed.all_gather(allrec, rec)
+        recs = [tuple(r.tolist()) for r in allrec]
+    else:
+        recs = [tuple(rec.tolist())]
+    gbest = sorted(recs, key=lambda r: (-r[0], r[1], r[2]))[0]
+    ms_step = ms / args.steps
+    vc_step = int(np.prod(dims)) * info["n_cand"]
+    value = vc_step / (ms_step / 1e3)
+
+    # roofline of the dominant kernel: one profiled step
+    ctx.profile(True)
+    step()
+    fam = {f: ctx.profile_read(f) for f in ("eta_direct", "eta_basis", "psf_pass", "pad", "argmax")}
+    ctx.profile(False)
+    step_ms = sum(v[0] for v in fam.values())
+    dom = max(fam, key=lambda f: fam[f][0])
+    fp32_peak = ctx.probe_fp32()
+    win_vox = (x1 - x0 + 1) * dims[1] * dims[2]
+    flops_direct = 2.0 * info["taps_per_voxel"] * win_vox
+    roof = None
+    if fam["eta_direct"][1]:
+        achieved = flops_direct / (fam["eta_direct"][0] / 1e3) / 1e12
+        roof = {"bound": "fp32", "kernel": "eta_direct_kernel", "achieved": achieved,
+                "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
+                "traffic": None,
+                "peak_source": "measured FFMA probe (sfw3d_probe_fp32) on this device",
+                "flops_per_voxel": 2.0 * info["taps_per_voxel"],
+                "avg_launch_ms": fam["eta_direct"][0] / fam["eta_direct"][1],
+                "share_of_step": fam["eta_direct"][0] / step_ms if step_ms else None}
+
+    # end to end through the C ABI with host buffers
+    host = residual.to("cpu").pin_memory()
+    dbuf = torch.empty_like(residual)
+    for _ in range(1):
+        dbuf.copy_(host, non_blocking=True)
+        eta_argmax_dev(dbuf, 1.0, table, window)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        dbuf.copy_(host, non_blocking=True)
+        eta_argmax_dev(dbuf, 1.0, table, window)  # returns after the D2H of the records
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": vc_step / e2e_s, "unit": "voxel-candidates/s",
+           "h2d_bytes_per_step": host.numel() * host.element_size(),
+           "d2h_bytes_per_step": 24 * (info["n_cand"] + 1), "ms_per_step": 1e3 * e2e_s,
+           "path": "pinned host fp32 residual -> H2D -> sfw3d_eta_argmax (C ABI) -> argmax D2H"}
+    out = {
+        "value": value, "ms_per_step": ms_step, "launches": launches, "clocks": clk,
+        "roofline": roof, "e2e": e2e, "kernel_ms": {k: v[0] for k, v in fam.items() if v[1]},
+        "table": info, "best": {"eta": gbest[0], "cand": int(gbest[1]), "lin": int(gbest[2])},
+        "inst": inst, "dims": dims,
+    }
+    return out
+
+
+def costgrad_workload(args, dev):
+    import torch
+    import paper_2009_05473_b200 as P
+    from paper_2009_05473_b200 import _native as N, configs
+    from paper_2009_05473_b200.forward import cost_grad_dev, psf_apply_dev, render_dev
+
+    P.set_precision("f32")
+    inst = configs.config5()
+    psf = P.Psf(P.Volume(inst.kernel), normalize=False)
+    y = psf_apply_dev(psf, render_dev(inst.truth, inst.dims, N.F32), False)
+    perts = configs.perturbations(inst.truth, 100)
+    ctx = N.context(dev)
+    for i in range(3):
+        cost_grad_dev(psf, y, perts[i], 0.1)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for i in range(args.cg_steps):
+        cost_grad_dev(psf, y, perts[i % 100], 0.1)
+    s = (time.perf_counter() - t0) / args.cg_steps
+    ctx.profile(True)
+    cost_grad_dev(psf, y, perts[0], 0.1)
+    fam = {f: ctx.profile_read(f) for f in ("render", "psf_pass", "sumsq", "atom_sums")}
+    ctx.profile(False)
+    hbm = peaks()["hbm_gbs"]
+    nbytes = int(np.prod(inst.dims)) * 4
+    # render writes 1 volume; 6 psf passes read+write; sumsq reads 2 + writes 1
+    psf_bytes = 6 * 2 * nbytes
+    psf_ms = fam["psf_pass"][0]
+    return {"metric": "cost+grad evals/s (cfg5: 256^3 fp32, N=1000, 6000-entry gradient)",
+            "value": 1.0 / s, "unit": "evals/s", "ms_per_eval": 1e3 * s,
+            "kernel_ms": {k: v[0] for k, v in fam.items()},
+            "psf_pass_gbs": psf_bytes / (psf_ms / 1e3) / 1e9 if psf_ms else None,
+            "psf_pass_frac_hbm": (psf_bytes / (psf_ms / 1e3) / 1e9) / hbm if psf_ms else None,
+            "timing": "wall clock per synchronous C-ABI call (host params in, C + gradient out)"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+    import torch
+    rank, world, local = dist_env()
+    dev = local
+    torch.cuda.set_device(dev)
+    if world > 1:
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    res = cert_workload(args, rank, world, dev)
+    secondary = []
+    if rank == 0 and not args.no_secondary:
+        secondary.append(costgrad_workload(args, dev))
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        inst = res["inst"]
+        residual = host_residual_cfg4(inst)
+        cands = [(inst.sigma_grid[-1], inst.shape_grid[0])]
+        times, vc = oracle_cert_sample(residual, inst.kernel, cands, 1, 1, 0)
+        cpu = {"value": vc / times[0], "unit": "voxel-candidates/s", "cores": 1, "kind": "port",
+               "sample": f"1 candidate (sigma=3, d=1.5) x {args.n}^3: rfftn + irfftn + argmax, "
+                         "scipy.fft single thread (the reference never threads its FFTs)"}
+    if rank == 0:
+        line = {
+            "metric": "certificate voxel-candidates/s", "value": res["value"],
+            "unit": "voxel-candidates/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"cfg4 certificate: {args.n}^3 fp32 residual (N(0,1) + 200 "
+                                   "blurred generalized Gaussians) x 16 (sigma,d) candidates, "
+                                   "PSF sigma_h=3 31^3, eta at every voxel + global argmax",
+                       "grid": args.n, "candidates": res["table"]["n_cand"],
+                       "tap_tol": args.tap_tol, "mode": args.mode,
+                       "parallelism": f"x-slabs x{world} (replicated residual)",
+                       "l2": "inputs larger than L2 (512 MiB residual, 0.9 GiB padded copy)"},
+            "gpu_launches": res["launches"], "clocks": res["clocks"], "roofline": res["roofline"],
+            "cpu_baseline": cpu, "e2e": res["e2e"], "kernel_ms_per_step": res["kernel_ms"],
+            "table": res["table"], "argmax": res["best"], "secondary": secondary,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,185 @@
+/*
+ * sfw3d_cuda.h — C ABI of the B200 (sm_100a) hot path of boosted Sliding
+ * Frank-Wolfe 3D deconvolution (drop-in core for the reference `sfw3d` 0.1.0).
+ *
+ * The reference is pure Python/numpy and has no FFI; each entry point below
+ * names the reference function (file:line under pkg/src/sfw3d/) whose
+ * arithmetic it replaces. The Python package `paper_2009_05473_b200` binds
+ * this ABI with ctypes and keeps the reference's public function names,
+ * argument meaning and exceptions (see INTEGRATION.md for the binding a
+ * maintainer of the reference would add).
+ *
+ * Conventions
+ *  - Volumes are dense (nx, ny, nz) arrays in C order (z contiguous), of
+ *    storage type SFW3D_F32 or SFW3D_F64, in DEVICE memory owned by the
+ *    caller (volumes.py:7-16). Host pointers are marked *_host.
+ *  - An atom row is 6 doubles (w, m_x, m_y, m_z, sigma, d): the reference
+ *    gradient-column / _pack order (forward.py:37, solvers.py:183-186).
+ *  - Every call returns an sfw3d_status; sfw3d_last_error() returns a
+ *    thread-local message for the last failure. No C++ exception crosses
+ *    the ABI. SFW3D_EINVAL maps to ValueError, SFW3D_ENONFINITE to
+ *    FloatingPointError (forward.py:225-228, certificate.py:207-208).
+ *  - A context binds one device and one CUDA stream; all work of a call is
+ *    enqueued on that stream. Calls that return values in *_host buffers
+ *    synchronise the stream before returning. Contexts are independent;
+ *    a context must not be used by two threads at once.
+ */
+#ifndef SFW3D_CUDA_H
+#define SFW3D_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFW3D_ABI_VERSION 1
+
+typedef enum {
+  SFW3D_OK = 0,
+  SFW3D_EINVAL = 1,      /* invalid argument (ValueError)               */
+  SFW3D_ENONFINITE = 2,  /* non-finite result (FloatingPointError)       */
+  SFW3D_ECUDA = 3,       /* CUDA runtime failure                         */
+  SFW3D_ENOMEM = 4       /* device allocation failure                    */
+} sfw3d_status;
+
+typedef enum { SFW3D_F32 = 0, SFW3D_F64 = 1 } sfw3d_dtype;
+
+typedef struct sfw3d_ctx sfw3d_ctx;
+typedef struct sfw3d_psf sfw3d_psf;
+typedef struct sfw3d_table sfw3d_table;
+
+/* Discrete argmax record: position (i,j,k), flat candidate index
+ * (sigma-major: i_sigma * n_shape + i_shape) and its eta value. */
+typedef struct {
+  int32_t pos[3];
+  int32_t cand;
+  double value;
+} sfw3d_argmax;
+
+/* ---- library / context ------------------------------------------------ */
+int sfw3d_abi_version(void);
+const char* sfw3d_last_error(void);
+/* stream: a cudaStream_t (NULL = legacy default stream). */
+int sfw3d_ctx_create(int device, void* stream, sfw3d_ctx** out);
+int sfw3d_ctx_destroy(sfw3d_ctx* ctx);
+int sfw3d_ctx_sync(sfw3d_ctx* ctx);
+/* Number of kernels this context has launched (for launch accounting). */
+int64_t sfw3d_ctx_launches(const sfw3d_ctx* ctx);
+
+/* Per-kernel device timing for roofline accounting. When enabled, the
+ * library brackets each of its kernel launches with CUDA events on the
+ * context stream, grouped by kernel family ("eta_direct", "psf_pass",
+ * "render", "atom_sums", "pad", "argmax", "residual", "dots", "cd",
+ * "sumsq", "eta_basis"). enable = 0 disables; any call resets the counters. */
+int sfw3d_ctx_profile(sfw3d_ctx* ctx, int enable);
+/* Total device milliseconds and launch count of one family since the last
+ * reset (synchronises the pending events). */
+int sfw3d_ctx_profile_read(sfw3d_ctx* ctx, const char* family, double* total_ms,
+                           int64_t* launches);
+/* Measured FP32 FMA throughput of this device (a register-resident FFMA
+ * loop over every SM), in TFLOP/s: the roofline denominator for the
+ * correlation kernels (MEASURED_PEAKS.json has no FP32 figure). */
+int sfw3d_probe_fp32(sfw3d_ctx* ctx, double* tflops);
+
+/* Host-only helper (no device work): per-atom support radius and box
+ * geometry exactly as forward.py:97-116 computes them. For each of the k
+ * atom rows writes radius[k] and, per axis, start[3k] (first span value,
+ * may be negative; 0 for a full axis), len[3k] and full[3k]. */
+int sfw3d_atom_geometry(const int dims[3], const double* params_host, int k,
+                        int32_t* radius, int32_t* start, int32_t* len, int32_t* full);
+
+/* ---- PSF (forward.py:40-94) ------------------------------------------- */
+/* kernel_host: dims[0]*dims[1]*dims[2] doubles, centred at n//2 per axis,
+ * already normalised as the caller wants (Psf.__init__, forward.py:49-58).
+ * The library factorises it into three 1-D tap vectors when it is
+ * separable (every BASELINE PSF is), else keeps its non-zero bounding box. */
+int sfw3d_psf_create(sfw3d_ctx* ctx, const int dims[3], const double* kernel_host,
+                     sfw3d_psf** out);
+/* separable flag and the non-zero offset box [lo, hi] per axis */
+int sfw3d_psf_info(const sfw3d_psf* psf, int* separable, int32_t lo[3], int32_t hi[3]);
+int sfw3d_psf_destroy(sfw3d_psf* psf);
+
+/* K4 — out = H * in (adjoint = 0, convolve, forward.py:79-87) or
+ *      out = H^T * in (adjoint = 1, correlate_adjoint, forward.py:90-94).
+ * Circular; in and out are distinct device volumes of `dtype`. */
+int sfw3d_psf_apply(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype,
+                    const void* in_dev, void* out_dev, int adjoint);
+
+/* ---- atoms (forward.py:119-179) --------------------------------------- */
+/* K3 — out = sum_i w_i G_i over each atom's 1e-12 support box, atoms summed
+ * in row order per voxel (_accumulate_atoms, forward.py:165-174). */
+int sfw3d_render(sfw3d_ctx* ctx, int dtype, const int dims[3], const double* params_host,
+                 int k, void* out_dev);
+
+/* K6/K7 — raw per-atom inner products against a device volume `field`:
+ * sums_host[6i + c] = < P_c(atom i), field >, with P = (G, dG/dm_x, dG/dm_y,
+ * dG/dm_z, dG/dsigma, dG/dd) of the UNIT atom (weights are ignored here).
+ * _gradient_rows (forward.py:209-229) and neg_eta (certificate.py:201-209)
+ * finish with row = [s0 + lam, w*s1..w*s5] and [s/lam] respectively.
+ * Returns SFW3D_ENONFINITE if any sum is not finite. */
+int sfw3d_atom_sums(sfw3d_ctx* ctx, int dtype, const int dims[3], const void* field_dev,
+                    const double* params_host, int k, double* sums_host);
+
+/* K3-K6 fused — criterion_and_gradient (forward.py:232-257):
+ *   model = H * sum_i w_i G_i ; C = 1/2 ||model - y||^2 + lam * sum_i w_i ;
+ *   back = H^T * (model - y) ; grad row i = [<G_i,back> + lam, w_i <dG_i,back>].
+ * grad_host may be NULL (criterion only, forward.py:182-190). back_dev, if
+ * not NULL, receives the back-projection (a `dtype` volume). */
+int sfw3d_cost_grad(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* y_dev,
+                    const double* params_host, int k, double lam, double* cost_host,
+                    double* grad_host, void* back_dev);
+
+/* ---- certificate (certificate.py:37-236) ------------------------------ */
+/* K2 — candidate table for the (sigma, d) grid, sigma-major (sorted
+ * ascending, as build_template_table sorts them, certificate.py:72-73).
+ * Spatial unit atoms G_ij(m=0) on the reference's support box
+ * (certificate.py:86-92) are kept on the device; the PSF is applied once to
+ * the residual (factorised eta = G * (H^T * r), exact by associativity).
+ * tap_tol: taps with G < tap_tol are skipped (0 keeps the reference box).
+ * mode: 0 = automatic (separable Gaussian basis where its certified error
+ * bound <= basis_tol, direct correlation otherwise), 1 = direct only. */
+int sfw3d_table_create(sfw3d_ctx* ctx, const sfw3d_psf* psf, int n_sigma,
+                       const double* sigma_host, int n_shape, const double* shape_host,
+                       double tap_tol, int mode, double basis_tol, sfw3d_table** out);
+int sfw3d_table_info(const sfw3d_table* t, int* n_cand, int* n_direct, int* n_basis,
+                     int64_t* taps_per_voxel);
+int sfw3d_table_destroy(sfw3d_table* t);
+
+/* K1 — eta_field (certificate.py:140-184): eta_c(m) = <H*G_c(.-m), r>/lam
+ * for every integer m and candidate c, with the discrete argmax over the
+ * window [window[2a], window[2a+1]] per axis (first C-order maximum per
+ * candidate; global winner by strict '>' over sigma-major candidates).
+ * per_cand_host (n_cand records) and fields_dev (n_cand volumes of dtype,
+ * candidate-major) may be NULL; fields are only produced when given. */
+int sfw3d_eta_argmax(sfw3d_ctx* ctx, const sfw3d_table* t, int dtype,
+                     const void* residual_dev, double lam, const int32_t window[6],
+                     sfw3d_argmax* best_host, sfw3d_argmax* per_cand_host,
+                     void* fields_dev);
+
+/* ---- non-negative LASSO (solvers.py:111-180, 253-266) ----------------- */
+/* K8 — out_host[i] = < vecs[i], v > over n elements, fp64 accumulation,
+ * fixed summation order. vecs_host holds k DEVICE pointers (Gram rows and
+ * the right-hand side b = Phi y, solvers.py:141-143). */
+int sfw3d_dots(sfw3d_ctx* ctx, int dtype, int64_t n, const void* const* vecs_host, int k,
+               const void* v_dev, double* out_host);
+
+/* K9 — cyclic coordinate descent with the reference's update, KKT, stall
+ * and sweep-cap rules (solvers.py:145-180), run in fp64 on the device.
+ * gram_host is k*k row-major, w_host holds w_init on entry and the result
+ * on exit. info_host[0] = sweeps, info_host[1] = 0 kkt / 1 stall / 2 cap,
+ * and the final KKT residual is written to *kkt_host. */
+int sfw3d_nnlasso_cd(sfw3d_ctx* ctx, int k, const double* gram_host, const double* b_host,
+                     double lam, double tol, int max_iter, double* w_host,
+                     int32_t* info_host, double* kkt_host);
+
+/* K5 — out = y - sum_i w_i phi_i in list order (_residual, solvers.py:253-257);
+ * out_dev may be NULL; sumsq_host (may be NULL) receives ||out||^2 in fp64. */
+int sfw3d_residual(sfw3d_ctx* ctx, int dtype, int64_t n, const void* y_dev,
+                   const void* const* phis_host, const double* w_host, int k,
+                   void* out_dev, double* sumsq_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFW3D_CUDA_H */

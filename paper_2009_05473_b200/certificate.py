@@ -1,0 +1,265 @@
+"""Dual certificate on the B200: grid scan fused with argmax, then refinement.
+
+Drop-in for ``sfw3d.certificate`` (certificate.py:1-236). The grid stage
+(eta_field) is the K1 direct-correlation kernel over every voxel x
+(sigma, d) candidate with the fused windowed argmax; only the argmax
+records (and, on request, the fields) leave the device. The continuous
+stage (refine_eta_max) keeps scipy's L-BFGS-B on the host, as the reference
+does, and evaluates eta and its 5-gradient with the K7 device reduction
+against a device-resident back-projection H^T r.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+from scipy.optimize import minimize
+
+from . import _native as N
+from .forward import Psf, atom_sums_dev, psf_apply_dev, to_dev
+from .measures import AtomParams, DomainBounds, clamp_to_domain
+from .volumes import Volume
+
+MODES = {"auto": 0, "direct": 1}
+
+
+def make_parameter_grids(bounds: DomainBounds, n_sigma: int = 8,
+                         n_shape: int = 6) -> tuple[np.ndarray, np.ndarray]:
+    """Geometric sigma samples, linear shape samples (certificate.py:37-49)."""
+    if n_sigma < 1 or n_shape < 1:
+        raise ValueError("grid sizes must be >= 1")
+    return (np.geomspace(bounds.sigma_min, bounds.sigma_max, n_sigma),
+            np.linspace(bounds.shape_min, bounds.shape_max, n_shape))
+
+
+class _TableHandle:
+    def __init__(self, handle):
+        self.handle = handle
+
+    def __del__(self):
+        try:
+            if N._lib is not None and self.handle:
+                N._lib.sfw3d_table_destroy(self.handle)
+        except Exception:
+            pass
+
+
+class AtomTemplateTable:
+    """Per (sigma, d) candidate, the unit atom at the origin, held on the device.
+
+    certificate.py:52-62 stores rfftn(H * G_ij); this build keeps the spatial
+    G_ij and the PSF (the correlation is factorised, see eta.cu), and
+    materialises ``template_hats`` on the host only if someone reads it.
+    """
+
+    def __init__(self, sigma_grid, shape_grid, dims, psf: Psf, tap_tol: float, mode: str,
+                 basis_tol: float):
+        self.sigma_grid = sigma_grid
+        self.shape_grid = shape_grid
+        self.dims = tuple(dims)
+        self.psf = psf
+        self.tap_tol = float(tap_tol)
+        self.mode = mode
+        self.basis_tol = float(basis_tol)
+        self._native = {}
+        self._hats = None
+
+    def native(self, device: int):
+        h = self._native.get(device)
+        if h is None:
+            ctx = N.context(device)
+            hp = C.c_void_p()
+            sg = np.ascontiguousarray(self.sigma_grid, dtype=np.float64)
+            dg = np.ascontiguousarray(self.shape_grid, dtype=np.float64)
+            N.check(N.lib().sfw3d_table_create(ctx.handle, self.psf.native(device), sg.size,
+                                               N.f64_ptr(sg), dg.size, N.f64_ptr(dg),
+                                               self.tap_tol, MODES[self.mode], self.basis_tol,
+                                               C.byref(hp)))
+            h = _TableHandle(hp)
+            self._native[device] = h
+        return h.handle
+
+    def info(self, device=None) -> dict:
+        nc, nd, nb = C.c_int(), C.c_int(), C.c_int()
+        taps = C.c_int64()
+        N.check(N.lib().sfw3d_table_info(self.native(N.device_index(device)), C.byref(nc),
+                                         C.byref(nd), C.byref(nb), C.byref(taps)))
+        return {"n_cand": nc.value, "n_direct": nd.value, "n_basis": nb.value,
+                "taps_per_voxel": taps.value}
+
+    @property
+    def template_hats(self) -> np.ndarray:
+        """Reference representation (n_sigma, n_shape, rfft dims), computed lazily."""
+        if self._hats is None:
+            import scipy.fft as sfft
+            from .forward import render_dev  # device render, then host FFT (compatibility only)
+            out = []
+            for s in self.sigma_grid:
+                for d in self.shape_grid:
+                    atom = render_dev(np.array([[1.0, 0.0, 0.0, 0.0, s, d]]), self.dims, N.F64)
+                    out.append(sfft.rfftn(atom.cpu().numpy()) * self.psf.kernel_hat)
+            self._hats = np.stack(out).reshape(len(self.sigma_grid), len(self.shape_grid),
+                                               *out[0].shape)
+        return self._hats
+
+    def entry(self, i_sigma: int, i_shape: int) -> np.ndarray:
+        return self.template_hats[i_sigma, i_shape]
+
+
+def build_template_table(psf: Psf, sigma_grid, shape_grid, bounds: DomainBounds | None = None,
+                         workers: int | None = None, *, tap_tol: float = 0.0,
+                         mode: str = "auto", basis_tol: float = 1e-9) -> AtomTemplateTable:
+    """Candidate table for the (sigma, d) grid (certificate.py:65-97).
+
+    Keyword-only extras: ``tap_tol`` skips template taps below it (0 keeps
+    the reference's full 1e-12 support box); ``mode`` "auto" lets the
+    library pick the fastest exact-to-``basis_tol`` evaluation per
+    candidate, "direct" forces direct correlation.
+    """
+    sigma_grid = np.sort(np.asarray(sigma_grid, dtype=float))
+    shape_grid = np.sort(np.asarray(shape_grid, dtype=float))
+    if sigma_grid.size == 0 or shape_grid.size == 0:
+        raise ValueError("parameter grids must be non-empty")
+    if bounds is not None:
+        if not (bounds.sigma_min <= sigma_grid[0] and sigma_grid[-1] <= bounds.sigma_max):
+            raise ValueError("sigma grid extends outside the domain bounds")
+        if not (bounds.shape_min <= shape_grid[0] and shape_grid[-1] <= bounds.shape_max):
+            raise ValueError("shape grid extends outside the domain bounds")
+    if not psf.is_centrosymmetric():
+        raise ValueError("template table requires a centro-symmetric kernel")
+    if mode not in MODES:
+        raise ValueError(f"mode must be one of {sorted(MODES)}")
+    table = AtomTemplateTable(sigma_grid, shape_grid, psf.dims, psf, tap_tol, mode, basis_tol)
+    table.native(N.device_index(None))
+    return table
+
+
+def _position_window(bounds: DomainBounds | None, dims):
+    """Integer box [ceil(lo), floor(hi)] clipped to the grid (certificate.py:100-111)."""
+    if bounds is None:
+        return tuple((0, n - 1) for n in dims)
+    out = []
+    for lo, hi, n in zip(bounds.pos_lower, bounds.pos_upper, dims):
+        a, b = max(0, int(np.ceil(lo))), min(n - 1, int(np.floor(hi)))
+        if a > b:
+            raise ValueError("domain position bounds contain no integer grid point")
+        out.append((a, b))
+    return tuple(out)
+
+
+@dataclass(frozen=True, eq=False)
+class CertificateField:
+    """Discrete argmax of eta over positions x (sigma, d), plus optional fields."""
+
+    sigma_grid: np.ndarray
+    shape_grid: np.ndarray
+    argmax_position: tuple[int, int, int]
+    argmax_sigma_index: int
+    argmax_shape_index: int
+    eta_max: float
+    fields: tuple[Volume, ...] | None = None
+
+    @property
+    def argmax_params(self) -> AtomParams:
+        return AtomParams(m=tuple(float(i) for i in self.argmax_position),
+                          sigma=float(self.sigma_grid[self.argmax_sigma_index]),
+                          d=float(self.shape_grid[self.argmax_shape_index]))
+
+
+def eta_argmax_dev(residual, lam: float, table: AtomTemplateTable, window, keep_fields=False):
+    """K1 on a device residual: (best Argmax, per-candidate list, fields tensor|None)."""
+    import torch
+    dev = residual.device.index
+    ctx = N.context(dev)
+    nc = len(table.sigma_grid) * len(table.shape_grid)
+    win = np.array([v for ab in window for v in ab], dtype=np.int32)
+    best = N.Argmax()
+    per = (N.Argmax * nc)()
+    fields = None
+    if keep_fields:
+        fields = torch.empty((nc, *table.dims), dtype=residual.dtype, device=residual.device)
+    from .forward import code_of
+    N.check(N.lib().sfw3d_eta_argmax(ctx.handle, table.native(dev), code_of(residual),
+                                     N.ptr(residual), float(lam), N.i32_ptr(win), C.byref(best),
+                                     per, N.ptr(fields) if fields is not None else None))
+    return best, [per[i] for i in range(nc)], fields
+
+
+def eta_field(residual: Volume, lam: float, table: AtomTemplateTable,
+              bounds: DomainBounds | None = None, keep_fields: bool = True,
+              workers: int | None = None) -> CertificateField:
+    """eta at every integer position for each table entry (certificate.py:140-184)."""
+    if lam <= 0.0:
+        raise ValueError(f"lam must be > 0, got {lam}")
+    if residual.dims != table.dims:
+        raise ValueError(f"dims mismatch: residual {residual.dims} vs table {table.dims}")
+    return eta_field_dev(to_dev(residual), lam, table, bounds, keep_fields)
+
+
+def eta_field_dev(residual, lam: float, table: AtomTemplateTable,
+                  bounds: DomainBounds | None = None, keep_fields: bool = False) -> CertificateField:
+    window = _position_window(bounds, table.dims)
+    best, _, fields = eta_argmax_dev(residual, lam, table, window, keep_fields)
+    i, j = divmod(int(best.cand), len(table.shape_grid))
+    kept = None
+    if keep_fields:
+        host = fields.to("cpu", dtype=__import__("torch").float64).numpy()
+        kept = tuple(Volume(host[c]) for c in range(host.shape[0]))
+    return CertificateField(sigma_grid=table.sigma_grid, shape_grid=table.shape_grid,
+                            argmax_position=tuple(int(p) for p in best.pos),
+                            argmax_sigma_index=i, argmax_shape_index=j,
+                            eta_max=float(best.value), fields=kept)
+
+
+def refine_eta_max(residual: Volume, lam: float, psf: Psf, start: AtomParams,
+                   bounds: DomainBounds, max_iter: int = 200,
+                   gtol: float = 1e-8) -> tuple[AtomParams, float]:
+    """Box-constrained L-BFGS-B ascent of eta from a grid seed (certificate.py:187-224)."""
+    if lam <= 0.0:
+        raise ValueError(f"lam must be > 0, got {lam}")
+    return refine_eta_max_dev(to_dev(residual), lam, psf, start, bounds, max_iter, gtol)
+
+
+def refine_eta_max_dev(residual, lam: float, psf: Psf, start: AtomParams, bounds: DomainBounds,
+                       max_iter: int = 200, gtol: float = 1e-8, back=None):
+    if lam <= 0.0:
+        raise ValueError(f"lam must be > 0, got {lam}")
+    start = clamp_to_domain(start, bounds)
+    if back is None:
+        back = psf_apply_dev(psf, residual, True)
+
+    def neg_eta(vec):
+        row = np.array([[1.0, *np.asarray(vec, dtype=float)]])
+        s = atom_sums_dev(back, row)[0]
+        val = float(s[0]) / lam
+        grad = s[1:] / lam
+        if not (np.isfinite(val) and np.isfinite(grad).all()):
+            raise FloatingPointError(f"non-finite certificate value near {vec}")
+        return -val, -grad
+
+    box = bounds.as_box()
+    start_val = -neg_eta(start.to_array())[0]
+    res = minimize(neg_eta, start.to_array(), jac=True, method="L-BFGS-B", bounds=box,
+                   options={"maxiter": max_iter, "gtol": gtol})
+    if not np.isfinite(res.fun):
+        raise FloatingPointError("certificate ascent diverged to a non-finite value")
+    if -res.fun < start_val:
+        return start, start_val
+    return clamp_to_domain(AtomParams.from_array(res.x), bounds), float(-res.fun)
+
+
+def certificate_max(residual: Volume, lam: float, table: AtomTemplateTable, psf: Psf,
+                    bounds: DomainBounds, workers: int | None = None) -> tuple[AtomParams, float]:
+    """Grid scan then continuous refinement (certificate.py:227-236)."""
+    if lam <= 0.0:
+        raise ValueError(f"lam must be > 0, got {lam}")
+    if residual.dims != table.dims:
+        raise ValueError(f"dims mismatch: residual {residual.dims} vs table {table.dims}")
+    return certificate_max_dev(to_dev(residual), lam, table, psf, bounds)
+
+
+def certificate_max_dev(residual, lam, table, psf, bounds):
+    field = eta_field_dev(residual, lam, table, bounds, keep_fields=False)
+    return refine_eta_max_dev(residual, lam, psf, field.argmax_params, bounds)

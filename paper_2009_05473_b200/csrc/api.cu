@@ -1,0 +1,583 @@
+// C-ABI entry points, context / workspace management, atom geometry and the
+// PSF object. See include/sfw3d_cuda.h for the contract of every function.
+#include <cstdio>
+#include <cstring>
+
+#include "internal.cuh"
+
+namespace sfw3d {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+// 2 * ln(1 / 1e-12) exactly as numpy computes it (forward.py:34)
+const double kTailExponent = 0x1.ba18a998fffa0p+5;
+
+int activate(sfw3d_ctx* ctx) {
+  SFW3D_CUDA_TRY(cudaSetDevice(ctx->device));
+  return SFW3D_OK;
+}
+
+int ensure_device(sfw3d_ctx* ctx, Arena& a, size_t bytes) {
+  if (a.bytes >= bytes) return SFW3D_OK;
+  if (a.ptr) {
+    SFW3D_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    SFW3D_CUDA_TRY(cudaFree(a.ptr));
+    a.ptr = nullptr;
+    a.bytes = 0;
+  }
+  size_t want = bytes + bytes / 8 + 4096;
+  SFW3D_CUDA_TRY(cudaMalloc(&a.ptr, want));
+  a.bytes = want;
+  return SFW3D_OK;
+}
+
+static int ensure_pinned_arena(sfw3d_ctx* ctx, Arena& a, size_t bytes) {
+  if (a.bytes >= bytes) return SFW3D_OK;
+  if (a.ptr) {
+    SFW3D_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    SFW3D_CUDA_TRY(cudaFreeHost(a.ptr));
+    a.ptr = nullptr;
+    a.bytes = 0;
+  }
+  size_t want = bytes * 2 + 65536;
+  SFW3D_CUDA_TRY(cudaMallocHost(&a.ptr, want));
+  a.bytes = want;
+  return SFW3D_OK;
+}
+
+int begin_call(sfw3d_ctx* ctx) {
+  SFW3D_TRY(activate(ctx));
+  if (ctx->pin_off) {
+    // an earlier asynchronous call may still be reading the staging area
+    SFW3D_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    ctx->pin_off = 0;
+  }
+  return SFW3D_OK;
+}
+
+int stage_upload(sfw3d_ctx* ctx, void* dst_dev, const void* src_host, size_t bytes) {
+  if (bytes == 0) return SFW3D_OK;
+  size_t need = ((ctx->pin_off + 255) & ~size_t(255)) + bytes;
+  if (need > ctx->pinned.bytes) {
+    SFW3D_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    ctx->pin_off = 0;
+    SFW3D_TRY(ensure_pinned_arena(ctx, ctx->pinned, bytes + 256));
+  }
+  size_t off = (ctx->pin_off + 255) & ~size_t(255);
+  char* p = static_cast<char*>(ctx->pinned.ptr) + off;
+  memcpy(p, src_host, bytes);
+  SFW3D_CUDA_TRY(cudaMemcpyAsync(dst_dev, p, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->pin_off = off + bytes;
+  return SFW3D_OK;
+}
+
+int download_sync(sfw3d_ctx* ctx, void* dst_host, const void* src_dev, size_t bytes) {
+  SFW3D_TRY(ensure_pinned_arena(ctx, ctx->pinned_out, bytes));
+  SFW3D_CUDA_TRY(cudaMemcpyAsync(ctx->pinned_out.ptr, src_dev, bytes, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+  SFW3D_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  ctx->pin_off = 0;
+  memcpy(dst_host, ctx->pinned_out.ptr, bytes);
+  return SFW3D_OK;
+}
+
+// ------------------------------------------------------------ atom geometry
+static int axis_geometry(int n, double centre, int radius, int& start, int& len, int& full) {
+  if (2LL * radius + 1 >= n) {  // forward.py:107-109
+    start = 0;
+    len = n;
+    full = 1;
+  } else {  // forward.py:111-113: round-half-even centre, unwrapped span
+    const double c = std::nearbyint(centre);
+    start = int(c) - radius;
+    len = 2 * radius + 1;
+    full = 0;
+  }
+  return SFW3D_OK;
+}
+
+int build_atoms(const int dims[3], const double* params, int k, std::vector<AtomGeo>& out) {
+  out.resize(k);
+  for (int i = 0; i < k; ++i) {
+    const double* r = params + 6 * i;
+    for (int c = 0; c < 6; ++c)
+      if (!std::isfinite(r[c])) {
+        set_error("invalid argument: non-finite atom parameters (row " + std::to_string(i) + ")");
+        return SFW3D_EINVAL;
+      }
+    AtomGeo& a = out[i];
+    a.w = r[0];
+    a.m[0] = r[1];
+    a.m[1] = r[2];
+    a.m[2] = r[3];
+    a.sigma = r[4];
+    a.d = r[5];
+    if (!(a.sigma > 0.0 && a.d > 0.0)) {
+      set_error("invalid argument: sigma and d must be positive (row " + std::to_string(i) + ")");
+      return SFW3D_EINVAL;
+    }
+    // forward.py:97-99 support_radius
+    const double rr = std::ceil(a.sigma * std::pow(kTailExponent, 1.0 / a.d));
+    if (!(rr < 1e9)) {
+      set_error("invalid argument: support radius overflow");
+      return SFW3D_EINVAL;
+    }
+    a.radius = int(rr);
+    a.inv2sd = 0.5 / std::pow(a.sigma, a.d);
+    a.half_d = 0.5 * a.d;
+    a.log_sigma = std::log(a.sigma);
+    a.d_over_sigma = a.d / a.sigma;
+    a.d2 = (a.d == 2.0) ? 1 : 0;
+    a.nvox = 1;
+    for (int ax = 0; ax < 3; ++ax) {
+      axis_geometry(dims[ax], a.m[ax], a.radius, a.start[ax], a.len[ax], a.full[ax]);
+      a.nvox *= a.len[ax];
+    }
+  }
+  return SFW3D_OK;
+}
+
+static bool dims_ok(const int dims[3]) {
+  return dims && dims[0] > 0 && dims[1] > 0 && dims[2] > 0;
+}
+
+}  // namespace sfw3d
+
+using namespace sfw3d;
+
+// =========================================================== ABI: library
+extern "C" int sfw3d_abi_version(void) { return SFW3D_ABI_VERSION; }
+
+extern "C" const char* sfw3d_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int sfw3d_ctx_create(int device, void* stream, sfw3d_ctx** out) {
+  SFW3D_CHECK_ARG(out != nullptr, "out is NULL");
+  *out = nullptr;
+  int ndev = 0;
+  SFW3D_CUDA_TRY(cudaGetDeviceCount(&ndev));
+  SFW3D_CHECK_ARG(device >= 0 && device < ndev, "device index out of range");
+  auto* ctx = new sfw3d_ctx();
+  ctx->device = device;
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) {
+    set_error(std::string("CUDA error ") + cudaGetErrorString(e));
+    delete ctx;
+    return SFW3D_ECUDA;
+  }
+  *out = ctx;
+  return SFW3D_OK;
+}
+
+extern "C" int sfw3d_ctx_destroy(sfw3d_ctx* ctx) {
+  if (!ctx) return SFW3D_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->ws.ptr) cudaFree(ctx->ws.ptr);
+  if (ctx->ws_small.ptr) cudaFree(ctx->ws_small.ptr);
+  if (ctx->pinned.ptr) cudaFreeHost(ctx->pinned.ptr);
+  if (ctx->pinned_out.ptr) cudaFreeHost(ctx->pinned_out.ptr);
+  delete ctx;
+  return SFW3D_OK;
+}
+
+extern "C" int sfw3d_ctx_sync(sfw3d_ctx* ctx) {
+  SFW3D_CHECK_ARG(ctx, "ctx is NULL");
+  SFW3D_TRY(activate(ctx));
+  SFW3D_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  ctx->pin_off = 0;
+  return SFW3D_OK;
+}
+
+extern "C" int64_t sfw3d_ctx_launches(const sfw3d_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+extern "C" int sfw3d_atom_geometry(const int dims[3], const double* params_host, int k,
+                                   int32_t* radius, int32_t* start, int32_t* len, int32_t* full) {
+  SFW3D_CHECK_ARG(dims_ok(dims), "dims must be positive");
+  SFW3D_CHECK_ARG(k >= 0 && (k == 0 || params_host), "params");
+  std::vector<AtomGeo> atoms;
+  SFW3D_TRY(build_atoms(dims, params_host, k, atoms));
+  for (int i = 0; i < k; ++i) {
+    if (radius) radius[i] = atoms[i].radius;
+    for (int a = 0; a < 3; ++a) {
+      if (start) start[3 * i + a] = atoms[i].start[a];
+      if (len) len[3 * i + a] = atoms[i].len[a];
+      if (full) full[3 * i + a] = atoms[i].full[a];
+    }
+  }
+  return SFW3D_OK;
+}
+
+// =============================================================== ABI: PSF
+extern "C" int sfw3d_psf_create(sfw3d_ctx* ctx, const int dims[3], const double* kernel_host,
+                                sfw3d_psf** out) {
+  SFW3D_CHECK_ARG(ctx && out && kernel_host, "NULL argument");
+  SFW3D_CHECK_ARG(dims_ok(dims), "dims must be positive");
+  SFW3D_TRY(begin_call(ctx));
+  *out = nullptr;
+  const int nx = dims[0], ny = dims[1], nz = dims[2];
+  auto at = [&](int i, int j, int l) { return kernel_host[((long long)i * ny + j) * nz + l]; };
+  // non-zero bounding box in index space
+  int lo_i[3] = {dims[0], dims[1], dims[2]}, hi_i[3] = {-1, -1, -1};
+  double peak = 0.0;
+  int piv[3] = {0, 0, 0};
+  for (int i = 0; i < nx; ++i)
+    for (int j = 0; j < ny; ++j)
+      for (int l = 0; l < nz; ++l) {
+        const double v = at(i, j, l);
+        if (!std::isfinite(v)) {
+          set_error("invalid argument: kernel contains non-finite values");
+          return SFW3D_EINVAL;
+        }
+        if (v != 0.0) {
+          const int q[3] = {i, j, l};
+          for (int a = 0; a < 3; ++a) {
+            lo_i[a] = std::min(lo_i[a], q[a]);
+            hi_i[a] = std::max(hi_i[a], q[a]);
+          }
+          if (std::fabs(v) > peak) {
+            peak = std::fabs(v);
+            piv[0] = i;
+            piv[1] = j;
+            piv[2] = l;
+          }
+        }
+      }
+  auto* psf = new sfw3d_psf();
+  for (int a = 0; a < 3; ++a) psf->dims[a] = dims[a];
+  psf->device = ctx->device;
+  if (hi_i[0] < 0) {  // all-zero kernel: a single zero tap
+    for (int a = 0; a < 3; ++a) lo_i[a] = hi_i[a] = dims[a] / 2;
+  }
+  for (int a = 0; a < 3; ++a) {
+    psf->lo[a] = lo_i[a] - dims[a] / 2;
+    psf->hi[a] = hi_i[a] - dims[a] / 2;
+  }
+  const int l[3] = {hi_i[0] - lo_i[0] + 1, hi_i[1] - lo_i[1] + 1, hi_i[2] - lo_i[2] + 1};
+  // rank-1 test through the pivot (exact for sampled separable kernels)
+  std::vector<double> f[3];
+  bool sep = peak > 0.0;
+  if (sep) {
+    const double p = at(piv[0], piv[1], piv[2]);
+    f[0].resize(l[0]);
+    f[1].resize(l[1]);
+    f[2].resize(l[2]);
+    for (int i = 0; i < l[0]; ++i) f[0][i] = at(lo_i[0] + i, piv[1], piv[2]);
+    for (int j = 0; j < l[1]; ++j) f[1][j] = at(piv[0], lo_i[1] + j, piv[2]) / p;
+    for (int q = 0; q < l[2]; ++q) f[2][q] = at(piv[0], piv[1], lo_i[2] + q) / p;
+    const double tol = 1e-14 * peak;
+    for (int i = 0; i < l[0] && sep; ++i)
+      for (int j = 0; j < l[1] && sep; ++j)
+        for (int q = 0; q < l[2]; ++q) {
+          const double rec = f[0][i] * f[1][j] * f[2][q];
+          if (std::fabs(rec - at(lo_i[0] + i, lo_i[1] + j, lo_i[2] + q)) > tol) {
+            sep = false;
+            break;
+          }
+        }
+  }
+  psf->separable = sep ? 1 : 0;
+  auto fail = [&](cudaError_t e) {
+    set_error(std::string("CUDA error ") + cudaGetErrorString(e));
+    sfw3d_psf_destroy(psf);
+    return e == cudaErrorMemoryAllocation ? SFW3D_ENOMEM : SFW3D_ECUDA;
+  };
+  if (sep) {
+    for (int a = 0; a < 3; ++a) {
+      std::vector<double> t64(2 * l[a]);
+      std::vector<float> t32(2 * l[a]);
+      for (int q = 0; q < l[a]; ++q) {
+        t64[q] = f[a][q];
+        t64[l[a] + q] = f[a][l[a] - 1 - q];  // reversed: convolution direction
+      }
+      for (int q = 0; q < 2 * l[a]; ++q) t32[q] = float(t64[q]);
+      cudaError_t e = cudaMalloc(&psf->taps64[a], t64.size() * sizeof(double));
+      if (e == cudaSuccess) e = cudaMalloc(&psf->taps32[a], t32.size() * sizeof(float));
+      if (e == cudaSuccess)
+        e = cudaMemcpy(psf->taps64[a], t64.data(), t64.size() * sizeof(double), cudaMemcpyHostToDevice);
+      if (e == cudaSuccess)
+        e = cudaMemcpy(psf->taps32[a], t32.data(), t32.size() * sizeof(float), cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return fail(e);
+    }
+  } else {
+    const size_t nb = size_t(l[0]) * l[1] * l[2];
+    std::vector<double> b64(nb);
+    std::vector<float> b32(nb);
+    for (int i = 0; i < l[0]; ++i)
+      for (int j = 0; j < l[1]; ++j)
+        for (int q = 0; q < l[2]; ++q) {
+          const size_t o = (size_t(i) * l[1] + j) * l[2] + q;
+          b64[o] = at(lo_i[0] + i, lo_i[1] + j, lo_i[2] + q);
+          b32[o] = float(b64[o]);
+        }
+    cudaError_t e = cudaMalloc(&psf->box64, nb * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&psf->box32, nb * sizeof(float));
+    if (e == cudaSuccess) e = cudaMemcpy(psf->box64, b64.data(), nb * sizeof(double), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(psf->box32, b32.data(), nb * sizeof(float), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return fail(e);
+  }
+  *out = psf;
+  return SFW3D_OK;
+}
+
+extern "C" int sfw3d_psf_info(const sfw3d_psf* psf, int* separable, int32_t lo[3], int32_t hi[3]) {
+  SFW3D_CHECK_ARG(psf, "psf is NULL");
+  if (separable) *separable = psf->separable;
+  for (int a = 0; a < 3; ++a) {
+    if (lo) lo[a] = psf->lo[a];
+    if (hi) hi[a] = psf->hi[a];
+  }
+  return SFW3D_OK;
+}
+
+extern "C" int sfw3d_psf_destroy(sfw3d_psf* psf) {
+  if (!psf) return SFW3D_OK;
+  cudaSetDevice(psf->device);
+  for (int a = 0; a < 3; ++a) {
+    if (psf->taps64[a]) cudaFree(psf->taps64[a]);
+    if (psf->taps32[a]) cudaFree(psf->taps32[a]);
+  }
+  if (psf->box64) cudaFree(psf->box64);
+  if (psf->box32) cudaFree(psf->box32);
+  delete psf;
+  return SFW3D_OK;
+}
+
+extern "C" int sfw3d_psf_apply(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* in_dev,
+                               void* out_dev, int adjoint) {
+  SFW3D_CHECK_ARG(ctx && psf && in_dev && out_dev, "NULL argument");
+  SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
+  SFW3D_CHECK_ARG(in_dev != out_dev, "in and out must differ");
+  SFW3D_TRY(begin_call(ctx));
+  const size_t vb = size_t(vol_count(psf->dims)) * dtype_size(dtype);
+  SFW3D_TRY(ensure_device(ctx, ctx->ws, vb));
+  return psf_apply_impl(ctx, psf, dtype, in_dev, out_dev, adjoint, ctx->ws.ptr);
+}
+
+// ============================================================= ABI: atoms
+static int upload_atoms(sfw3d_ctx* ctx, const std::vector<AtomGeo>& atoms, AtomGeo* dst) {
+  return stage_upload(ctx, dst, atoms.data(), atoms.size() * sizeof(AtomGeo));
+}
+
+extern "C" int sfw3d_render(sfw3d_ctx* ctx, int dtype, const int dims[3], const double* params_host,
+                            int k, void* out_dev) {
+  SFW3D_CHECK_ARG(ctx && out_dev, "NULL argument");
+  SFW3D_CHECK_ARG(dims_ok(dims), "dims must be positive");
+  SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
+  SFW3D_CHECK_ARG(k >= 0 && (k == 0 || params_host), "params");
+  SFW3D_TRY(begin_call(ctx));
+  std::vector<AtomGeo> atoms;
+  SFW3D_TRY(build_atoms(dims, params_host, k, atoms));
+  SFW3D_TRY(ensure_device(ctx, ctx->ws_small, (size_t(k) + 1) * sizeof(AtomGeo) + 4096));
+  AtomGeo* ad = static_cast<AtomGeo*>(ctx->ws_small.ptr);
+  SFW3D_TRY(upload_atoms(ctx, atoms, ad));
+  return render_impl(ctx, dtype, dims, ad, k, out_dev);
+}
+
+static int finite_all(const double* x, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(x[i])) return 0;
+  return 1;
+}
+
+extern "C" int sfw3d_atom_sums(sfw3d_ctx* ctx, int dtype, const int dims[3], const void* field_dev,
+                               const double* params_host, int k, double* sums_host) {
+  SFW3D_CHECK_ARG(ctx && field_dev && sums_host, "NULL argument");
+  SFW3D_CHECK_ARG(dims_ok(dims), "dims must be positive");
+  SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
+  SFW3D_CHECK_ARG(k >= 0 && (k == 0 || params_host), "params");
+  SFW3D_TRY(begin_call(ctx));
+  if (k == 0) return SFW3D_OK;
+  std::vector<AtomGeo> atoms;
+  SFW3D_TRY(build_atoms(dims, params_host, k, atoms));
+  const size_t scratch = atom_sums_scratch(atoms);
+  const size_t need = Carver::need({size_t(k) * sizeof(AtomGeo), size_t(k) * 6 * sizeof(double), scratch});
+  SFW3D_TRY(ensure_device(ctx, ctx->ws_small, need));
+  Carver cv(ctx->ws_small.ptr);
+  AtomGeo* ad = cv.take<AtomGeo>(k);
+  double* sums = cv.take<double>(size_t(k) * 6);
+  void* scr = cv.take<char>(scratch);
+  SFW3D_TRY(upload_atoms(ctx, atoms, ad));
+  SFW3D_TRY(atom_sums_impl(ctx, dtype, dims, field_dev, atoms, ad, sums, scr, scratch));
+  SFW3D_TRY(download_sync(ctx, sums_host, sums, size_t(k) * 6 * sizeof(double)));
+  if (!finite_all(sums_host, size_t(k) * 6)) {
+    set_error("non-finite atom inner product; atom parameters left the smooth regime");
+    return SFW3D_ENONFINITE;
+  }
+  return SFW3D_OK;
+}
+
+extern "C" int sfw3d_cost_grad(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* y_dev,
+                               const double* params_host, int k, double lam, double* cost_host,
+                               double* grad_host, void* back_dev) {
+  SFW3D_CHECK_ARG(ctx && psf && y_dev && cost_host, "NULL argument");
+  SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
+  SFW3D_CHECK_ARG(k >= 0 && (k == 0 || params_host), "params");
+  SFW3D_CHECK_ARG(lam > 0.0, "lam must be > 0");
+  SFW3D_TRY(begin_call(ctx));
+  const int* dims = psf->dims;
+  std::vector<AtomGeo> atoms;
+  SFW3D_TRY(build_atoms(dims, params_host, k, atoms));
+  const int64_t n = vol_count(dims);
+  const size_t vb = size_t(n) * dtype_size(dtype);
+  SFW3D_TRY(ensure_device(ctx, ctx->ws, Carver::need({vb, vb})));
+  Carver cw(ctx->ws.ptr);
+  void* A = cw.take<char>(vb);
+  void* B = cw.take<char>(vb);
+  const size_t scratch = atom_sums_scratch(atoms);
+  const int nred = 4 * ctx->num_sms;
+  SFW3D_TRY(ensure_device(ctx, ctx->ws_small,
+                          Carver::need({(size_t(k) + 1) * sizeof(AtomGeo), (size_t(k) * 6 + 1) * sizeof(double),
+                                        size_t(nred) * sizeof(double), scratch})));
+  Carver cs(ctx->ws_small.ptr);
+  AtomGeo* ad = cs.take<AtomGeo>(k + 1);
+  double* res = cs.take<double>(size_t(k) * 6 + 1);  // [sumsq, sums...]
+  double* partials = cs.take<double>(nred);
+  void* scr = cs.take<char>(scratch);
+  SFW3D_TRY(upload_atoms(ctx, atoms, ad));
+  // model = H * sum w G  (A -> B, A used as pass scratch)
+  SFW3D_TRY(render_impl(ctx, dtype, dims, ad, k, A));
+  SFW3D_TRY(psf_apply_impl(ctx, psf, dtype, A, B, 0, A));
+  // resid = model - y -> A ; ||resid||^2
+  SFW3D_TRY(sumsq_diff_impl(ctx, dtype, n, B, y_dev, A, partials, res));
+  if (grad_host) {
+    void* back = back_dev ? back_dev : B;
+    SFW3D_TRY(psf_apply_impl(ctx, psf, dtype, A, back, 1, back == B ? A : B));
+    SFW3D_TRY(atom_sums_impl(ctx, dtype, dims, back, atoms, ad, res + 1, scr, scratch));
+  }
+  std::vector<double> host(size_t(k) * 6 + 1);
+  SFW3D_TRY(download_sync(ctx, host.data(), res, (grad_host ? host.size() : 1) * sizeof(double)));
+  double mass = 0.0;
+  for (int i = 0; i < k; ++i) mass += atoms[i].w;  // total_mass: sum in order
+  *cost_host = 0.5 * host[0] + lam * mass;
+  if (grad_host) {
+    for (int i = 0; i < k; ++i) {
+      const double* s = &host[1 + 6 * i];
+      double* g = grad_host + 6 * i;
+      g[0] = s[0] + lam;                                   // forward.py:218
+      for (int c = 1; c < 6; ++c) g[c] = atoms[i].w * s[c];  // forward.py:219-220
+    }
+    if (!finite_all(grad_host, size_t(k) * 6)) {
+      set_error("non-finite criterion gradient; atom parameters left the smooth regime");
+      return SFW3D_ENONFINITE;
+    }
+  }
+  return SFW3D_OK;
+}
+
+// ========================================================= ABI: profiling
+namespace sfw3d {
+
+ProfScope::ProfScope(sfw3d_ctx* c, const char* f) : ctx(c), family(f) {
+  if (!ctx->profile) return;
+  cudaEvent_t start;
+  if (cudaEventCreate(&start) != cudaSuccess || cudaEventCreate(&stop) != cudaSuccess) {
+    stop = nullptr;
+    return;
+  }
+  cudaEventRecord(start, ctx->stream);
+  ctx->marks.push_back({family, start, nullptr});
+}
+
+ProfScope::~ProfScope() {
+  if (!ctx->profile || !stop) return;
+  cudaEventRecord(stop, ctx->stream);
+  ctx->marks.back().stop = stop;
+}
+
+static void drain_marks(sfw3d_ctx* ctx) {
+  for (auto& m : ctx->marks) {
+    float ms = 0.f;
+    if (m.stop) {
+      cudaEventSynchronize(m.stop);
+      cudaEventElapsedTime(&ms, m.start, m.stop);
+      cudaEventDestroy(m.stop);
+    }
+    cudaEventDestroy(m.start);
+    bool found = false;
+    for (auto& t : ctx->totals)
+      if (t.first == m.family) {
+        t.second.first += ms;
+        t.second.second += 1;
+        found = true;
+      }
+    if (!found) ctx->totals.push_back({m.family, {double(ms), 1LL}});
+  }
+  ctx->marks.clear();
+}
+
+namespace {
+__global__ void __launch_bounds__(256) fma_probe_kernel(float* out, int iters, float seed) {
+  float a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = seed + threadIdx.x * 1e-7f + i;
+  const float m = 0.999999f, c = 1e-7f;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = fmaf(a[i], m, c);
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  if (s == 12345.678f) out[0] = s;  // keep the loop alive
+}
+}  // namespace
+
+}  // namespace sfw3d
+
+extern "C" int sfw3d_ctx_profile(sfw3d_ctx* ctx, int enable) {
+  SFW3D_CHECK_ARG(ctx, "ctx is NULL");
+  SFW3D_TRY(activate(ctx));
+  drain_marks(ctx);
+  ctx->totals.clear();
+  ctx->profile = enable ? 1 : 0;
+  return SFW3D_OK;
+}
+
+extern "C" int sfw3d_ctx_profile_read(sfw3d_ctx* ctx, const char* family, double* total_ms,
+                                      int64_t* launches) {
+  SFW3D_CHECK_ARG(ctx && family, "NULL argument");
+  SFW3D_TRY(activate(ctx));
+  drain_marks(ctx);
+  double ms = 0.0;
+  long long n = 0;
+  for (auto& t : ctx->totals)
+    if (t.first == family) {
+      ms = t.second.first;
+      n = t.second.second;
+    }
+  if (total_ms) *total_ms = ms;
+  if (launches) *launches = n;
+  return SFW3D_OK;
+}
+
+extern "C" int sfw3d_probe_fp32(sfw3d_ctx* ctx, double* tflops) {
+  SFW3D_CHECK_ARG(ctx && tflops, "NULL argument");
+  SFW3D_TRY(begin_call(ctx));
+  SFW3D_TRY(ensure_device(ctx, ctx->ws_small, 4096));
+  float* out = static_cast<float*>(ctx->ws_small.ptr);
+  const int blocks = ctx->num_sms * 8;  // 64 warps per SM
+  const int iters = 4096;
+  cudaEvent_t a, b;
+  SFW3D_CUDA_TRY(cudaEventCreate(&a));
+  SFW3D_CUDA_TRY(cudaEventCreate(&b));
+  fma_probe_kernel<<<blocks, 256, 0, ctx->stream>>>(out, 64, 1.0f);  // warm-up
+  SFW3D_LAUNCH_CHECK(ctx);
+  SFW3D_CUDA_TRY(cudaEventRecord(a, ctx->stream));
+  fma_probe_kernel<<<blocks, 256, 0, ctx->stream>>>(out, iters, 1.0f);
+  SFW3D_LAUNCH_CHECK(ctx);
+  SFW3D_CUDA_TRY(cudaEventRecord(b, ctx->stream));
+  SFW3D_CUDA_TRY(cudaEventSynchronize(b));
+  float ms = 0.f;
+  SFW3D_CUDA_TRY(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  const double flops = 2.0 * double(blocks) * 256.0 * iters * 16.0 * 8.0;
+  *tflops = flops / (double(ms) * 1e-3) / 1e12;
+  return SFW3D_OK;
+}

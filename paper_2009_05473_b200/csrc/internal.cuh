@@ -1,0 +1,192 @@
+// Internal declarations shared by the sfw3d CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "../../include/sfw3d_cuda.h"
+
+namespace sfw3d {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+
+struct Status {
+  int code;
+  Status(int c = SFW3D_OK) : code(c) {}
+};
+
+#define SFW3D_CHECK_ARG(cond, msg)                   \
+  do {                                               \
+    if (!(cond)) {                                   \
+      ::sfw3d::set_error(std::string("invalid argument: ") + (msg)); \
+      return SFW3D_EINVAL;                           \
+    }                                                \
+  } while (0)
+
+#define SFW3D_CUDA_TRY(expr)                                                  \
+  do {                                                                        \
+    cudaError_t _e = (expr);                                                  \
+    if (_e != cudaSuccess) {                                                  \
+      ::sfw3d::set_error(std::string("CUDA error ") + cudaGetErrorString(_e) + \
+                         " at " + __FILE__ + ":" + std::to_string(__LINE__)); \
+      return _e == cudaErrorMemoryAllocation ? SFW3D_ENOMEM : SFW3D_ECUDA;    \
+    }                                                                         \
+  } while (0)
+
+#define SFW3D_LAUNCH_CHECK(ctx)                 \
+  do {                                          \
+    (ctx)->launches++;                          \
+    SFW3D_CUDA_TRY(cudaGetLastError());         \
+  } while (0)
+
+// Records a CUDA event pair around a kernel launch when profiling is on.
+namespace sfw3d {
+struct ProfScope;
+}
+#define SFW3D_PROF(ctx, family) ::sfw3d::ProfScope _prof_scope((ctx), (family))
+
+#define SFW3D_TRY(expr)            \
+  do {                             \
+    int _s = (expr);               \
+    if (_s != SFW3D_OK) return _s; \
+  } while (0)
+
+// ---------------------------------------------------------------- context
+struct Arena {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace sfw3d
+
+struct sfw3d_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  int64_t launches = 0;
+  sfw3d::Arena ws;         // device scratch (grown on demand, reused)
+  sfw3d::Arena pinned;     // pinned host staging for uploads (bump-allocated)
+  size_t pin_off = 0;      // bytes of `pinned` referenced by in-flight copies
+  sfw3d::Arena pinned_out; // pinned host buffer for small downloads
+  sfw3d::Arena ws_small;   // small device scratch (params, partials)
+  // kernel-family timing (sfw3d_ctx_profile)
+  int profile = 0;
+  struct Mark {
+    const char* family;
+    cudaEvent_t start, stop;
+  };
+  std::vector<Mark> marks;
+  std::vector<std::pair<std::string, std::pair<double, long long>>> totals;
+};
+
+namespace sfw3d {
+
+int ensure_device(sfw3d_ctx* ctx, Arena& a, size_t bytes);
+// Host->device upload through the pinned staging area (asynchronous on
+// ctx->stream). The staging area is recycled at the next begin_call or
+// after a synchronising download.
+int stage_upload(sfw3d_ctx* ctx, void* dst_dev, const void* src_host, size_t bytes);
+// Device->host copy through pinned memory; synchronises ctx->stream.
+int download_sync(sfw3d_ctx* ctx, void* dst_host, const void* src_dev, size_t bytes);
+// Called at the top of every ABI entry point.
+int begin_call(sfw3d_ctx* ctx);
+int activate(sfw3d_ctx* ctx);  // cudaSetDevice
+
+struct ProfScope {
+  sfw3d_ctx* ctx;
+  cudaEvent_t stop = nullptr;
+  const char* family;
+  ProfScope(sfw3d_ctx* c, const char* f);
+  ~ProfScope();
+};
+
+// Carves aligned sub-buffers from a workspace arena.
+struct Carver {
+  char* base;
+  size_t off = 0;
+  explicit Carver(void* p) : base(static_cast<char*>(p)) {}
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(base + off);
+    off += count * sizeof(T);
+    return p;
+  }
+  static size_t need(const std::vector<size_t>& sizes) {
+    size_t o = 0;
+    for (size_t s : sizes) o = ((o + 255) & ~size_t(255)) + s;
+    return o + 256;
+  }
+};
+
+// ---------------------------------------------------------------- atoms
+// The reference's tail exponent 2*ln(1/1e-12) (forward.py:34), as the exact
+// double numpy produces.
+extern const double kTailExponent;
+
+// Per-atom descriptor with the support box resolved on the host exactly as
+// forward.py:97-116 does (libm pow/ceil/rint in float64).
+struct AtomGeo {
+  double w, m[3], sigma, d;
+  double inv2sd;     // 0.5 / sigma**d           (forward.py:135)
+  double half_d;     // 0.5 * d                   (forward.py:136)
+  double log_sigma;  // log(sigma)                (forward.py:150)
+  double d_over_sigma;
+  int start[3];      // first span value (unwrapped), 0 for a full axis
+  int len[3];        // box length per axis
+  int full[3];       // 1 when 2R+1 >= n (minimum-image full axis)
+  int d2;            // d == 2.0 exactly          (forward.py:136)
+  int radius;
+  long long nvox;
+};
+
+// Builds AtomGeo rows; returns SFW3D_EINVAL for sigma<=0, d<=0 or
+// non-finite parameters (forward.py:130-131, measures.py:80-82).
+int build_atoms(const int dims[3], const double* params, int k, std::vector<AtomGeo>& out);
+
+// ---------------------------------------------------------------- PSF
+}  // namespace sfw3d
+
+struct sfw3d_psf {
+  int dims[3];
+  int separable;
+  int lo[3], hi[3];              // non-zero offset box (offset = index - n//2)
+  // separable: taps per axis over [lo, hi]; device f64 and f32 copies
+  double* taps64[3] = {nullptr, nullptr, nullptr};
+  float* taps32[3] = {nullptr, nullptr, nullptr};
+  // general: dense box over [lo, hi]^3 (C order)
+  double* box64 = nullptr;
+  float* box32 = nullptr;
+  int device = 0;
+};
+
+namespace sfw3d {
+
+// Applies the PSF (or its adjoint) on ctx->stream. tmp_dev: one scratch
+// volume of the same dtype (may alias nothing else). in != out.
+int psf_apply_impl(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* in,
+                   void* out, int adjoint, void* tmp);
+
+// Launch helpers implemented in the .cu files.
+int render_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const AtomGeo* atoms_dev,
+                int k, void* out);
+int atom_sums_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const void* field,
+                   const std::vector<AtomGeo>& atoms, const AtomGeo* atoms_dev,
+                   double* sums_dev, void* scratch, size_t scratch_bytes);
+size_t atom_sums_scratch(const std::vector<AtomGeo>& atoms);
+
+// fp64 block reductions
+int sumsq_diff_impl(sfw3d_ctx* ctx, int dtype, int64_t n, const void* a, const void* b,
+                    void* diff_out, double* partials, double* result_dev);
+
+inline int64_t vol_count(const int dims[3]) {
+  return int64_t(dims[0]) * dims[1] * dims[2];
+}
+inline size_t dtype_size(int dtype) { return dtype == SFW3D_F64 ? 8 : 4; }
+
+}  // namespace sfw3d

@@ -1,0 +1,303 @@
+// K5 / K8 / K9 — non-negative LASSO weight step on the device.
+//
+// nonneg_lasso (solvers.py:111-180) stacks k full blurred-atom volumes and
+// forms Gram = Phi Phi^T and b = Phi y with one DGEMM (solvers.py:141-143),
+// then runs cyclic coordinate descent in Python. Here:
+//  * sfw3d_dots: k inner products <vec_i, v> in fp64 with a fixed block
+//    partition and fixed-order combine (deterministic); the host solver keeps
+//    the Gram matrix incrementally (one new row per added atom);
+//  * sfw3d_nnlasso_cd: one warp runs the reference's exact update sequence
+//    in fp64 (same rounding: no FMA where numpy rounds twice);
+//  * sfw3d_residual: y - sum_i w_i phi_i in list order (solvers.py:253-257).
+#include <cstring>
+
+#include "internal.cuh"
+
+namespace sfw3d {
+namespace {
+
+constexpr int kDotThreads = 256;
+constexpr int kDotBlocks = 64;  // per vector; fixed so the sum order is fixed
+
+template <typename T>
+__global__ void __launch_bounds__(kDotThreads) dots_kernel(const T* const* __restrict__ vecs,
+                                                           const T* __restrict__ v, long long n,
+                                                           double* __restrict__ partials) {
+  const T* a = vecs[blockIdx.y];
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)kDotThreads + threadIdx.x; i < n;
+       i += (long long)kDotBlocks * kDotThreads)
+    s += double(a[i]) * double(v[i]);
+  __shared__ double red[kDotThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if (lane == 0) red[warp] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0;
+    for (int w = 0; w < kDotThreads / 32; ++w) x += red[w];
+    partials[blockIdx.y * kDotBlocks + blockIdx.x] = x;
+  }
+}
+
+__global__ void dots_combine_kernel(const double* __restrict__ partials, int k,
+                                    double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= k) return;
+  double x = 0.0;
+  for (int b = 0; b < kDotBlocks; ++b) x += partials[i * kDotBlocks + b];
+  out[i] = x;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) residual_kernel(const T* __restrict__ y,
+                                                       const T* const* __restrict__ phis,
+                                                       const double* __restrict__ w, int k,
+                                                       long long n, T* __restrict__ out,
+                                                       double* __restrict__ partials) {
+  double s = 0.0;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+    T r = y[i];
+    for (int j = 0; j < k; ++j) {
+      if constexpr (sizeof(T) == 8)
+        r = __dsub_rn(r, __dmul_rn(w[j], phis[j][i]));  // data -= w * phi
+      else
+        r = T(double(r) - w[j] * double(phis[j][i]));
+    }
+    if (out) out[i] = r;
+    s += double(r) * double(r);
+  }
+  __shared__ double red[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if (lane == 0) red[warp] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0;
+    for (int q = 0; q < 8; ++q) x += red[q];
+    partials[blockIdx.x] = x;
+  }
+}
+
+__global__ void sum_partials_kernel(const double* __restrict__ p, int n, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double x = 0.0;
+    for (int i = 0; i < n; ++i) x += p[i];
+    *out = x;
+  }
+}
+
+// One warp; solvers.py:149-180 step for step. Gram rows are read for the
+// column update: the host assembles the Gram matrix exactly symmetric.
+__global__ void __launch_bounds__(32) cd_kernel(int k, const double* __restrict__ gram,
+                                                const double* __restrict__ b, double lam,
+                                                double tol, int max_iter, double* __restrict__ w_io,
+                                                int* __restrict__ info, double* __restrict__ kkt_out) {
+  extern __shared__ double sm[];
+  double* w = sm;
+  double* gw = sm + k;
+  const int lane = threadIdx.x;
+  for (int i = lane; i < k; i += 32) w[i] = w_io[i];
+  __syncwarp();
+  // gw = gram @ w (row order)
+  for (int i = lane; i < k; i += 32) {
+    double x = 0.0;
+    for (int j = 0; j < k; ++j) x = __dadd_rn(x, __dmul_rn(gram[(long long)i * k + j], w[j]));
+    gw[i] = x;
+  }
+  __syncwarp();
+  double wmax = 0.0;
+  for (int i = 0; i < k; ++i) wmax = (i == 0 || w[i] > wmax) ? w[i] : wmax;
+  double w_scale = wmax > 1.0 ? wmax : 1.0;  // max(1.0, max(w))
+  double kkt = INFINITY;
+  int sweeps = 0, reason = 2;
+  for (int sweep = 1; sweep <= max_iter; ++sweep) {
+    sweeps = sweep;
+    double step = 0.0;
+    for (int i = 0; i < k; ++i) {
+      const double old = w[i];
+      const double gii = gram[(long long)i * k + i];
+      const double x = __dadd_rn(old, __ddiv_rn(__dsub_rn(__dsub_rn(b[i], lam), gw[i]), gii));
+      const double nw = (x > 0.0) ? x : 0.0;  // Python max(0.0, x)
+      __syncwarp();
+      if (nw != old) {
+        const double dlt = __dsub_rn(nw, old);
+        const double* row = gram + (long long)i * k;
+        for (int j = lane; j < k; j += 32) gw[j] = __dadd_rn(gw[j], __dmul_rn(dlt, row[j]));
+        if (lane == 0) w[i] = nw;
+        const double ad = fabs(dlt);
+        step = (ad > step) ? ad : step;
+      }
+      __syncwarp();
+    }
+    // KKT residual (solvers.py:161-169)
+    double ka = 0.0, ki = 0.0;
+    int has_a = 0, has_i = 0;
+    for (int j = lane; j < k; j += 32) {
+      const double slope = __dadd_rn(__dsub_rn(gw[j], b[j]), lam);
+      if (w[j] > 0.0) {
+        has_a = 1;
+        ka = fmax(ka, fabs(slope));
+      } else {
+        has_i = 1;
+        ki = fmax(ki, fmax(0.0, -slope));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ka = fmax(ka, __shfl_xor_sync(0xffffffffu, ka, o));
+      ki = fmax(ki, __shfl_xor_sync(0xffffffffu, ki, o));
+      has_a |= __shfl_xor_sync(0xffffffffu, has_a, o);
+      has_i |= __shfl_xor_sync(0xffffffffu, has_i, o);
+    }
+    kkt = 0.0;
+    if (has_a) kkt = ka;
+    if (has_i) kkt = fmax(kkt, ki);
+    if (kkt <= tol) {
+      reason = 0;
+      break;
+    }
+    double wm = -INFINITY;
+    for (int j = lane; j < k; j += 32) wm = fmax(wm, w[j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wm = fmax(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+    w_scale = (wm > w_scale) ? wm : w_scale;
+    if (step <= 1e-14 * w_scale) {
+      reason = 1;
+      break;
+    }
+  }
+  __syncwarp();
+  for (int i = lane; i < k; i += 32) w_io[i] = w[i];
+  if (lane == 0) {
+    info[0] = sweeps;
+    info[1] = reason;
+    *kkt_out = kkt;
+  }
+}
+
+}  // namespace
+}  // namespace sfw3d
+
+using namespace sfw3d;
+
+extern "C" int sfw3d_dots(sfw3d_ctx* ctx, int dtype, int64_t n, const void* const* vecs_host, int k,
+                          const void* v_dev, double* out_host) {
+  SFW3D_CHECK_ARG(ctx && v_dev && out_host, "NULL argument");
+  SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
+  SFW3D_CHECK_ARG(n >= 0 && k >= 0 && (k == 0 || vecs_host), "sizes");
+  SFW3D_TRY(begin_call(ctx));
+  if (k == 0) return SFW3D_OK;
+  for (int i = 0; i < k; ++i) SFW3D_CHECK_ARG(vecs_host[i] != nullptr, "NULL vector");
+  SFW3D_TRY(ensure_device(ctx, ctx->ws_small,
+                          Carver::need({size_t(k) * sizeof(void*), size_t(k) * kDotBlocks * sizeof(double),
+                                        size_t(k) * sizeof(double)})));
+  Carver cv(ctx->ws_small.ptr);
+  const void** vp = cv.take<const void*>(k);
+  double* part = cv.take<double>(size_t(k) * kDotBlocks);
+  double* out = cv.take<double>(k);
+  SFW3D_TRY(stage_upload(ctx, vp, vecs_host, size_t(k) * sizeof(void*)));
+  dim3 grid(kDotBlocks, k);
+  SFW3D_PROF(ctx, "dots");
+  if (dtype == SFW3D_F64)
+    dots_kernel<double><<<grid, kDotThreads, 0, ctx->stream>>>(
+        reinterpret_cast<const double* const*>(vp), static_cast<const double*>(v_dev), n, part);
+  else
+    dots_kernel<float><<<grid, kDotThreads, 0, ctx->stream>>>(
+        reinterpret_cast<const float* const*>(vp), static_cast<const float*>(v_dev), n, part);
+  SFW3D_LAUNCH_CHECK(ctx);
+  dots_combine_kernel<<<(k + 127) / 128, 128, 0, ctx->stream>>>(part, k, out);
+  SFW3D_LAUNCH_CHECK(ctx);
+  return download_sync(ctx, out_host, out, size_t(k) * sizeof(double));
+}
+
+extern "C" int sfw3d_residual(sfw3d_ctx* ctx, int dtype, int64_t n, const void* y_dev,
+                              const void* const* phis_host, const double* w_host, int k,
+                              void* out_dev, double* sumsq_host) {
+  SFW3D_CHECK_ARG(ctx && y_dev, "NULL argument");
+  SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
+  SFW3D_CHECK_ARG(n >= 0 && k >= 0 && (k == 0 || (phis_host && w_host)), "sizes");
+  SFW3D_TRY(begin_call(ctx));
+  const int nblk = 4 * ctx->num_sms;
+  SFW3D_TRY(ensure_device(ctx, ctx->ws_small,
+                          Carver::need({size_t(k + 1) * sizeof(void*), size_t(k + 1) * sizeof(double),
+                                        size_t(nblk) * sizeof(double), sizeof(double)})));
+  Carver cv(ctx->ws_small.ptr);
+  const void** pp = cv.take<const void*>(k + 1);
+  double* wd = cv.take<double>(k + 1);
+  double* part = cv.take<double>(nblk);
+  double* res = cv.take<double>(1);
+  if (k) {
+    SFW3D_TRY(stage_upload(ctx, pp, phis_host, size_t(k) * sizeof(void*)));
+    SFW3D_TRY(stage_upload(ctx, wd, w_host, size_t(k) * sizeof(double)));
+  }
+  SFW3D_PROF(ctx, "residual");
+  if (dtype == SFW3D_F64)
+    residual_kernel<double><<<nblk, 256, 0, ctx->stream>>>(
+        static_cast<const double*>(y_dev), reinterpret_cast<const double* const*>(pp), wd, k, n,
+        static_cast<double*>(out_dev), part);
+  else
+    residual_kernel<float><<<nblk, 256, 0, ctx->stream>>>(
+        static_cast<const float*>(y_dev), reinterpret_cast<const float* const*>(pp), wd, k, n,
+        static_cast<float*>(out_dev), part);
+  SFW3D_LAUNCH_CHECK(ctx);
+  if (sumsq_host) {
+    sum_partials_kernel<<<1, 32, 0, ctx->stream>>>(part, nblk, res);
+    SFW3D_LAUNCH_CHECK(ctx);
+    return download_sync(ctx, sumsq_host, res, sizeof(double));
+  }
+  return SFW3D_OK;
+}
+
+extern "C" int sfw3d_nnlasso_cd(sfw3d_ctx* ctx, int k, const double* gram_host, const double* b_host,
+                                double lam, double tol, int max_iter, double* w_host,
+                                int32_t* info_host, double* kkt_host) {
+  SFW3D_CHECK_ARG(ctx && w_host, "NULL argument");
+  SFW3D_CHECK_ARG(k >= 0 && (k == 0 || (gram_host && b_host)), "sizes");
+  SFW3D_CHECK_ARG(lam > 0.0, "lam must be > 0");
+  SFW3D_CHECK_ARG(max_iter >= 0, "max_iter must be >= 0");
+  SFW3D_CHECK_ARG(k <= 6000, "k too large for the single-warp solver (<= 6000)");
+  SFW3D_TRY(begin_call(ctx));
+  if (k == 0) {
+    if (info_host) info_host[0] = info_host[1] = 0;
+    if (kkt_host) *kkt_host = 0.0;
+    return SFW3D_OK;
+  }
+  for (int i = 0; i < k; ++i)
+    SFW3D_CHECK_ARG(w_host[i] >= 0.0, "w_init must be non-negative with one entry per atom");
+  const size_t kk = size_t(k) * k;
+  SFW3D_TRY(ensure_device(ctx, ctx->ws_small,
+                          Carver::need({kk * sizeof(double), size_t(k) * sizeof(double),
+                                        size_t(k) * sizeof(double), 4 * sizeof(int), sizeof(double)})));
+  Carver cv(ctx->ws_small.ptr);
+  double* g = cv.take<double>(kk);
+  double* bd = cv.take<double>(k);
+  double* wd = cv.take<double>(k);
+  int* info = cv.take<int>(4);
+  double* kkt = cv.take<double>(1);
+  SFW3D_TRY(stage_upload(ctx, g, gram_host, kk * sizeof(double)));
+  SFW3D_TRY(stage_upload(ctx, bd, b_host, size_t(k) * sizeof(double)));
+  SFW3D_TRY(stage_upload(ctx, wd, w_host, size_t(k) * sizeof(double)));
+  const size_t smem = 2 * size_t(k) * sizeof(double);
+  if (smem > 48 * 1024)
+    SFW3D_CUDA_TRY(cudaFuncSetAttribute(cd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  {
+    SFW3D_PROF(ctx, "cd");
+    cd_kernel<<<1, 32, smem, ctx->stream>>>(k, g, bd, lam, tol, max_iter, wd, info, kkt);
+    SFW3D_LAUNCH_CHECK(ctx);
+  }
+  // results: w, info, kkt in one pinned download each
+  SFW3D_TRY(download_sync(ctx, w_host, wd, size_t(k) * sizeof(double)));
+  int hinfo[4];
+  SFW3D_TRY(download_sync(ctx, hinfo, info, 4 * sizeof(int)));
+  double hk = 0.0;
+  SFW3D_TRY(download_sync(ctx, &hk, kkt, sizeof(double)));
+  if (info_host) {
+    info_host[0] = hinfo[0];
+    info_host[1] = hinfo[1];
+  }
+  if (kkt_host) *kkt_host = hk;
+  return SFW3D_OK;
+}

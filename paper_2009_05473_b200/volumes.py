@@ -1,0 +1,149 @@
+"""Host volume type and ``.vol`` IO — the boundary type of every hot function.
+
+Mirrors the reference's ``sfw3d.volumes`` contract (volumes.py:1-113): an
+immutable float64 C-order (nx, ny, nz) array, z contiguous, validated finite,
+read-only; the ``.vol`` format is ``b"SFW3DV01"``, three little-endian uint32
+dims, then little-endian float64 payload. The B200 build adds one thing: a
+per-(device, storage dtype) cache of the device copy, so a Volume handed to
+several GPU calls (y in the solver loop) is uploaded once. The cache is safe
+because the host array is read-only.
+"""
+
+from __future__ import annotations
+
+import struct
+from pathlib import Path
+
+import numpy as np
+
+MAGIC = b"SFW3DV01"
+_HDR = struct.Struct("<8s3I")
+
+
+class VolumeFormatError(ValueError):
+    """Malformed ``.vol`` file: bad magic, size mismatch or non-finite payload."""
+
+
+def _dims3(dims) -> tuple[int, int, int]:
+    out = tuple(int(n) for n in dims)
+    if len(out) != 3 or min(out) < 1:
+        raise ValueError(f"dims must be three positive integers, got {out}")
+    return out
+
+
+class Volume:
+    """Immutable dense float64 field on an (nx, ny, nz) voxel grid."""
+
+    __slots__ = ("_data", "_dev")
+
+    def __init__(self, data):
+        arr = np.array(data, dtype=np.float64, order="C", copy=True) \
+            if not (isinstance(data, np.ndarray) and data.dtype == np.float64
+                    and data.flags.c_contiguous and not data.flags.writeable) \
+            else data
+        if arr.ndim != 3:
+            raise ValueError(f"volume data must be 3D, got shape {arr.shape}")
+        _dims3(arr.shape)
+        if not np.isfinite(arr).all():
+            raise ValueError("volume data contains non-finite values")
+        if arr.flags.writeable:
+            arr.setflags(write=False)
+        object.__setattr__(self, "_data", arr)
+        object.__setattr__(self, "_dev", {})
+
+    def __setattr__(self, name, value):
+        raise AttributeError("Volume is immutable")
+
+    @property
+    def data(self) -> np.ndarray:
+        return self._data
+
+    @property
+    def dims(self) -> tuple[int, int, int]:
+        return self._data.shape
+
+    def __repr__(self) -> str:
+        return f"Volume(dims={self.dims})"
+
+    # -- device copies (B200 build) -----------------------------------------
+    def device_tensor(self, dtype, device):
+        """Device copy in the given torch dtype, uploaded once and cached."""
+        import torch
+        key = (str(device), dtype)
+        t = self._dev.get(key)
+        if t is None:
+            host = torch.from_numpy(self._data)
+            if dtype != torch.float64:
+                host = host.to(dtype)
+            t = host.pin_memory().to(device, non_blocking=True)
+            self._dev[key] = t
+        return t
+
+    @classmethod
+    def from_device(cls, tensor) -> "Volume":
+        """Host Volume from a device tensor (one D2H copy, float64)."""
+        return cls(tensor.detach().to("cpu", dtype=__import__("torch").float64).numpy())
+
+
+class GridGeometry:
+    """Voxel grid geometry; spacing is one voxel per axis (volumes.py:62-74)."""
+
+    __slots__ = ("_dims",)
+
+    def __init__(self, dims):
+        object.__setattr__(self, "_dims", _dims3(dims))
+
+    def __setattr__(self, name, value):
+        raise AttributeError("GridGeometry is immutable")
+
+    @property
+    def dims(self) -> tuple[int, int, int]:
+        return self._dims
+
+    @property
+    def voxel_count(self) -> int:
+        return self._dims[0] * self._dims[1] * self._dims[2]
+
+    def __eq__(self, other):
+        return isinstance(other, GridGeometry) and other._dims == self._dims
+
+    def __hash__(self):
+        return hash(self._dims)
+
+    def __repr__(self) -> str:
+        return f"GridGeometry(dims={self._dims})"
+
+
+def zero_volume(dims) -> Volume:
+    return Volume(np.zeros(_dims3(dims)))
+
+
+def volume_norms(v: Volume) -> tuple[float, float]:
+    """``(max |v_i|, sqrt(sum v_i^2))``."""
+    flat = v.data.ravel()
+    return (float(np.max(np.abs(flat))) if flat.size else 0.0, float(np.linalg.norm(flat)))
+
+
+def write_volume(v: Volume, path) -> None:
+    with open(Path(path), "wb") as fh:
+        fh.write(_HDR.pack(MAGIC, *v.dims))
+        fh.write(np.ascontiguousarray(v.data, dtype="<f8").tobytes())
+
+
+def read_volume(path) -> Volume:
+    path = Path(path)
+    raw = path.read_bytes()
+    if len(raw) < _HDR.size:
+        raise VolumeFormatError(f"{path}: truncated header")
+    magic, nx, ny, nz = _HDR.unpack_from(raw)
+    if magic != MAGIC:
+        raise VolumeFormatError(f"{path}: bad magic {magic!r}")
+    dims = _dims3((nx, ny, nz))
+    want = _HDR.size + 8 * nx * ny * nz
+    if len(raw) != want:
+        raise VolumeFormatError(
+            f"{path}: payload size mismatch (header says {want} bytes, file has {len(raw)})")
+    data = np.frombuffer(raw, dtype="<f8", offset=_HDR.size).reshape(dims)
+    if not np.isfinite(data).all():
+        raise VolumeFormatError(f"{path}: payload contains non-finite values")
+    return Volume(data.astype(np.float64, copy=True))
