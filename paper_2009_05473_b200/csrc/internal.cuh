@@ -45,9 +45,6 @@ struct Status {
   } while (0)
 
 // Records a CUDA event pair around a kernel launch when profiling is on.
-namespace sfw3d {
-struct ProfScope;
-}
 #define SFW3D_PROF(ctx, family) ::sfw3d::ProfScope _prof_scope((ctx), (family))
 
 #define SFW3D_TRY(expr)            \
