@@ -260,18 +260,46 @@ def cert_workload(args, rank, world, dev):
     step_ms = sum(v[0] for v in fam.values())
     dom = max(fam, key=lambda f: fam[f][0])
     fp32_peak = ctx.probe_fp32()
+    hbm_peak = peaks()["hbm_gbs"]
     win_vox = (x1 - x0 + 1) * dims[1] * dims[2]
-    flops_direct = 2.0 * info["taps_per_voxel"] * win_vox
-    roof = None
+    nvox = int(np.prod(dims))
+    rooflines = {}
     if fam["eta_direct"][1]:
-        achieved = flops_direct / (fam["eta_direct"][0] / 1e3) / 1e12
-        roof = {"bound": "fp32", "kernel": "eta_direct_kernel", "achieved": achieved,
-                "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
-                "traffic": None,
-                "peak_source": "measured FFMA probe (sfw3d_probe_fp32) on this device",
-                "flops_per_voxel": 2.0 * info["taps_per_voxel"],
-                "avg_launch_ms": fam["eta_direct"][0] / fam["eta_direct"][1],
-                "share_of_step": fam["eta_direct"][0] / step_ms if step_ms else None}
+        flops = 2.0 * info["direct_taps_per_voxel"] * win_vox
+        achieved = flops / (fam["eta_direct"][0] / 1e3) / 1e12
+        rooflines["eta_direct"] = {
+            "bound": "fp32", "kernel": "eta_direct_kernel", "achieved": achieved,
+            "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": None,
+            "peak_source": "measured FFMA probe (sfw3d_probe_fp32) on this device",
+            "flops_per_voxel": 2.0 * info["direct_taps_per_voxel"],
+            "launches": fam["eta_direct"][1],
+            "avg_launch_ms": fam["eta_direct"][0] / fam["eta_direct"][1],
+            "share_of_step": fam["eta_direct"][0] / step_ms if step_ms else None}
+    if fam["eta_basis"][1]:
+        n_pass = fam["eta_basis"][1]
+        n_terms = n_pass // 3
+        # per pass: read in + write out (fp32); the x pass also reads its addend
+        nbytes = 4.0 * nvox * (2 * n_pass + n_terms)
+        flops = 2.0 * info["basis_taps_per_voxel"] * nvox
+        t = fam["eta_basis"][0] / 1e3
+        gbs, tfl = nbytes / t / 1e9, flops / t / 1e12
+        rooflines["eta_basis"] = {
+            "bound": "hbm" if gbs / hbm_peak > tfl / fp32_peak else "fp32",
+            "kernel": "pass_strided_kernel / pass_z_kernel (separable basis terms)",
+            "achieved": gbs if gbs / hbm_peak > tfl / fp32_peak else tfl,
+            "peak": hbm_peak if gbs / hbm_peak > tfl / fp32_peak else fp32_peak,
+            "unit": "GB/s" if gbs / hbm_peak > tfl / fp32_peak else "TFLOP/s",
+            "frac": max(gbs / hbm_peak, tfl / fp32_peak), "traffic": None,
+            "achieved_gbs": gbs, "achieved_tflops": tfl, "hbm_peak_gbs": hbm_peak,
+            "fp32_peak_tflops": fp32_peak, "bytes_per_step": nbytes, "flops_per_step": flops,
+            "launches": n_pass, "avg_launch_ms": fam["eta_basis"][0] / n_pass,
+            "share_of_step": fam["eta_basis"][0] / step_ms if step_ms else None}
+    roof = None
+    if rooflines:
+        dom_fam = max(rooflines, key=lambda f: fam[f][0])
+        roof = dict(rooflines[dom_fam])
+        roof["dominant_family"] = dom_fam
+        roof["all"] = rooflines
 
     # end to end through the C ABI with host buffers
     host = residual.to("cpu").pin_memory()

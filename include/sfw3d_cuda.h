@@ -142,8 +142,17 @@ int sfw3d_cost_grad(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void*
 int sfw3d_table_create(sfw3d_ctx* ctx, const sfw3d_psf* psf, int n_sigma,
                        const double* sigma_host, int n_shape, const double* shape_host,
                        double tap_tol, int mode, double basis_tol, sfw3d_table** out);
-int sfw3d_table_info(const sfw3d_table* t, int* n_cand, int* n_direct, int* n_basis,
-                     int64_t* taps_per_voxel);
+/* Evaluator split for a storage dtype: candidates on the direct path and on
+ * the separable basis, and the taps per output voxel each path executes
+ * (summed over its candidates) — the FLOP counts of the roofline. */
+int sfw3d_table_info(const sfw3d_table* t, int dtype, int* n_cand, int* n_direct, int* n_basis,
+                     int64_t* direct_taps, int64_t* basis_taps);
+/* One candidate (flat sigma-major index): evaluator used for `dtype`, basis
+ * term count (incl. the delta term), the basis fit's max absolute error on
+ * the lattice of the support box, and both tap counts. */
+int sfw3d_table_candidate(const sfw3d_table* t, int dtype, int cand, int* uses_basis,
+                          int* n_terms, double* fit_err, int64_t* direct_taps,
+                          int64_t* basis_taps);
 int sfw3d_table_destroy(sfw3d_table* t);
 
 /* K1 — eta_field (certificate.py:140-184): eta_c(m) = <H*G_c(.-m), r>/lam

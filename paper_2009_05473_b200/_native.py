@@ -31,6 +31,7 @@ EXPORTS = (
     "sfw3d_atom_sums", "sfw3d_cost_grad", "sfw3d_table_create", "sfw3d_table_info",
     "sfw3d_table_destroy", "sfw3d_eta_argmax", "sfw3d_dots", "sfw3d_nnlasso_cd",
     "sfw3d_residual", "sfw3d_ctx_profile", "sfw3d_ctx_profile_read", "sfw3d_probe_fp32",
+    "sfw3d_table_candidate",
 )
 
 
@@ -60,7 +61,10 @@ _SIGNATURES = {
     "sfw3d_cost_grad": (C.c_int, [_vp, _vp, C.c_int, _vp, _dp, C.c_int, C.c_double, _dp, _dp, _vp]),
     "sfw3d_table_create": (C.c_int, [_vp, _vp, C.c_int, _dp, C.c_int, _dp, C.c_double, C.c_int,
                                      C.c_double, C.POINTER(_vp)]),
-    "sfw3d_table_info": (C.c_int, [_vp, _ip, _ip, _ip, C.POINTER(C.c_int64)]),
+    "sfw3d_table_info": (C.c_int, [_vp, C.c_int, _ip, _ip, _ip, C.POINTER(C.c_int64),
+                                   C.POINTER(C.c_int64)]),
+    "sfw3d_table_candidate": (C.c_int, [_vp, C.c_int, C.c_int, _ip, _ip, _dp, C.POINTER(C.c_int64),
+                                        C.POINTER(C.c_int64)]),
     "sfw3d_table_destroy": (C.c_int, [_vp]),
     "sfw3d_eta_argmax": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_double, _i32p, C.POINTER(Argmax),
                                    C.POINTER(Argmax), _vp]),

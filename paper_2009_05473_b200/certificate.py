@@ -81,13 +81,27 @@ class AtomTemplateTable:
             self._native[device] = h
         return h.handle
 
-    def info(self, device=None) -> dict:
+    def info(self, device=None, precision: str | None = None) -> dict:
+        """Evaluator split and executed taps per voxel for a storage precision."""
+        code = N.dtype_code(precision)
+        h = self.native(N.device_index(device))
         nc, nd, nb = C.c_int(), C.c_int(), C.c_int()
-        taps = C.c_int64()
-        N.check(N.lib().sfw3d_table_info(self.native(N.device_index(device)), C.byref(nc),
-                                         C.byref(nd), C.byref(nb), C.byref(taps)))
+        dt, bt = C.c_int64(), C.c_int64()
+        N.check(N.lib().sfw3d_table_info(h, code, C.byref(nc), C.byref(nd), C.byref(nb),
+                                         C.byref(dt), C.byref(bt)))
+        cands = []
+        for i in range(nc.value):
+            ub, nt, fe = C.c_int(), C.c_int(), C.c_double()
+            cdt, cbt = C.c_int64(), C.c_int64()
+            N.check(N.lib().sfw3d_table_candidate(h, code, i, C.byref(ub), C.byref(nt),
+                                                  C.byref(fe), C.byref(cdt), C.byref(cbt)))
+            s, d = divmod(i, len(self.shape_grid))
+            cands.append({"sigma": float(self.sigma_grid[s]), "d": float(self.shape_grid[d]),
+                          "path": "basis" if ub.value else "direct", "terms": nt.value,
+                          "fit_err": fe.value, "direct_taps": cdt.value, "basis_taps": cbt.value})
         return {"n_cand": nc.value, "n_direct": nd.value, "n_basis": nb.value,
-                "taps_per_voxel": taps.value}
+                "direct_taps_per_voxel": dt.value, "basis_taps_per_voxel": bt.value,
+                "candidates": cands}
 
     @property
     def template_hats(self) -> np.ndarray:

@@ -2,48 +2,65 @@
 // fused with the windowed argmax.
 //
 // Reference: build_template_table (certificate.py:65-97) stores
-// rfftn(H * G_ij) per candidate and eta_field (certificate.py:140-184) runs
-// one irfftn per candidate, keeps every field, and scans the window for the
+// rfftn(H * G_ij) per candidate; eta_field (certificate.py:140-184) runs one
+// irfftn per candidate, keeps every field, and scans the window for the
 // first C-order maximum; the global winner is the first candidate reaching
 // the maximum (strict '>', sigma-major).
 //
-// Here the certificate is a DIRECT spatial correlation in factorised form
+// Here eta is evaluated in the spatial domain in factorised form
 //     eta_c(m) = (1/lam) * sum_v G_c(v) * b(m + v),   b = H^T * r,
-// exact by associativity (corr(r, H*G) = corr(corr(r, H), G)); the PSF
-// adjoint is the separable K4 pass, applied once and shared by all
-// candidates. b is copied once into a periodically padded volume so the
-// correlation kernel needs no wrap logic.
+// exact by associativity (corr(r, H*G) = corr(corr(r, H), G)); b is one
+// separable K4 pass shared by all candidates. Two evaluators per candidate:
 //
-// Direct kernel (per candidate): a CTA owns 32 (y) x 64 (z) outputs of one
-// x-plane. Warp w handles z-group w (16 consecutive outputs per thread),
-// lane l handles row y0+l, so a warp's shared-memory reads hit 32 different
-// rows (pitch = 4 mod 32 words: conflict-free LDS.128). For every template
-// x-offset a, the residual plane region (32 + template rows - 1) x pitch is
-// staged in shared memory; every template row (a, b) then streams its taps
-// four at a time: one LDS.128 of the sliding register window, one broadcast
-// LDG.128 of taps and 64 FFMA per thread (register window rotated at compile
-// time, no moves). fp32 partial sums are promoted to fp64 once per template
-// slice. The argmax over the window is reduced warp -> CTA -> candidate
-// with the reference's tie rule.
+//  DIRECT — 3-D correlation with the unit atom on the reference's support
+//   box. A CTA owns 32 (y) x 64 (z) outputs of one x-plane: warp w has the
+//   z-group w (16 consecutive outputs per thread), lane l the row y0+l, so
+//   a warp's shared-memory reads hit 32 different rows (pitch = 4 mod 32
+//   words: conflict-free LDS.128). For each template x-offset the residual
+//   plane region is staged in shared memory; every template row streams its
+//   taps four at a time: one LDS.128 of the register window, one broadcast
+//   LDG.128 of taps, 64 FFMA per thread (window rotated at compile time, no
+//   moves). fp32 partial sums are promoted to fp64 once per template slice.
+//
+//  BASIS — the radial profile g(s) = exp(-s^(d/2) / (2 sigma^d)), s = |v|^2,
+//   is written as w_0 delta(s) + sum_k w_k exp(-beta_k s) on the lattice
+//   values s the support box contains (non-negative least squares over 48
+//   geometric beta_k; exact with one term for d = 2). Each term is
+//   separable, (f_k x f_k x f_k)(v) with f_k(t) = exp(-beta_k t^2) truncated
+//   to the same box, so eta_c costs sum_k 3 * (2R+1) taps per voxel instead
+//   of (2R+1)^3. The fit's max absolute error over the box is recorded and
+//   the basis is used only where it is <= basis_tol (fp32 storage) or the
+//   expansion is exact (d == 2, any storage).
 #include <algorithm>
 #include <cstring>
 
 #include "internal.cuh"
 
-struct sfw3d_table;
-
 namespace sfw3d {
+
+struct Term {
+  double beta, w;
+  void* taps64 = nullptr;  // 3 axes x [lo..hi] doubles, contiguous per axis
+  void* taps32 = nullptr;
+};
 
 struct CandHost {
   double sigma, d;
   int lo[3], hi[3];  // template offset box per axis
+  // direct
   int cl, lc4;       // template cols c = cl + col, col in [0, lc4)
   int la, lb;
   std::vector<int2> rows;  // per (a,b): (first step, nsteps), step = 4 cols
-  long long taps;          // executed taps per output voxel
+  long long taps = 0;      // executed direct taps per output voxel
   double* t64 = nullptr;
   float* t32 = nullptr;
   int2* rows_dev = nullptr;
+  // basis
+  bool exact_sep = false;  // d == 2: one exact term
+  double fit_err = INFINITY;
+  double w0 = 0.0;         // delta weight
+  std::vector<Term> terms;
+  long long basis_taps = 0;  // per output voxel
 };
 
 }  // namespace sfw3d
@@ -53,38 +70,39 @@ struct sfw3d_table {
   int n_sigma, n_shape;
   const sfw3d_psf* psf;
   std::vector<sfw3d::CandHost> cands;
-  int pad[3];       // periodic padding (left) per axis of the padded b volume
-  int pdims[3];     // padded dims
+  int pad[3];    // periodic padding (left) per axis of the padded b volume
+  int pdims[3];  // padded dims
   int device;
-  long long taps_per_voxel;
+  int mode;      // 0 auto, 1 direct only
+  double basis_tol;
 };
 
 namespace sfw3d {
 namespace {
 
-constexpr int kTY = 32;              // output rows per CTA (one per lane)
-constexpr int kJ = 16;               // outputs per thread along z
-constexpr int kWarps = 4;            // z-groups per CTA
-constexpr int kTZ = kJ * kWarps;     // 64 outputs along z per CTA
+constexpr int kTY = 32;           // output rows per CTA (one per lane)
+constexpr int kJ = 16;            // outputs per thread along z
+constexpr int kWarps = 4;         // z-groups per CTA
+constexpr int kTZ = kJ * kWarps;  // 64 outputs along z per CTA
 constexpr int kThreads = 32 * kWarps;
 
 struct CandDev {
-  const void* taps;   // dense [la][lb][lc4] of T
-  const int2* rows;   // [la][lb]
+  const void* taps;  // dense [la][lb][lc4] of T
+  const int2* rows;  // [la][lb]
   int lo_a, lo_b, la, lb, cl, lc4;
 };
 
 struct Geo {
   int nx, ny, nz;
-  int px, py, pz;        // padding
-  long long pys, pxs;    // padded strides (y, x) in elements
-  int win[6];            // argmax window (inclusive)
-  int ox0, oy0;          // output tile origin (x plane, y row)
-  int zbase;             // first z tile origin (multiple of 4)
-  int nty, ntz;          // tiles per plane
-  int pitch;             // smem row pitch (elements)
-  int brows;             // template rows per staged chunk
-  double lam;            // eta = sum / lam (certificate.py:160)
+  int px, py, pz;      // padding
+  long long pys, pxs;  // padded strides (y, x) in elements
+  int win[6];          // argmax window (inclusive)
+  int ox0, oy0;        // output tile origin (x plane, y row)
+  int zbase;           // first z tile origin (multiple of 4)
+  int nty, ntz;        // tiles per plane
+  int pitch;           // smem row pitch (elements)
+  int brows;           // template rows per staged chunk
+  double lam;          // eta = sum / lam (certificate.py:160)
 };
 
 struct Best {
@@ -96,17 +114,6 @@ __device__ __forceinline__ bool better(double v, long long i, double bv, long lo
   // larger value wins; ties -> smaller C-order index (first maximum)
   return (v > bv) || (v == bv && i < bi);
 }
-
-template <typename T>
-struct Vec4;
-template <>
-struct Vec4<float> {
-  using type = float4;
-};
-template <>
-struct Vec4<double> {
-  using type = double4;
-};
 
 template <typename T>
 __device__ __forceinline__ void ld4(const T* p, T& a, T& b, T& c, T& d) {
@@ -151,6 +158,25 @@ __device__ __forceinline__ void tap_step(T (&acc)[kJ], T (&buf)[20], const T* tr
 }
 
 template <typename T>
+__device__ __forceinline__ void reduce_store_best(Best best, Best* wbest, Best* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, best.v, o);
+    const long long oi = __shfl_xor_sync(0xffffffffu, best.idx, o);
+    if (better(ov, oi, best.v, best.idx)) best = {ov, oi};
+  }
+  if (lane == 0) wbest[warp] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Best b = wbest[0];
+    for (int w = 1; w < int(blockDim.x / 32); ++w)
+      if (better(wbest[w].v, wbest[w].idx, b.v, b.idx)) b = wbest[w];
+    *out = b;
+  }
+}
+
+template <typename T>
 __global__ void __launch_bounds__(kThreads) eta_direct_kernel(const T* __restrict__ bpad, Geo g,
                                                               CandDev cd, T* __restrict__ field,
                                                               Best* __restrict__ partial) {
@@ -175,12 +201,10 @@ __global__ void __launch_bounds__(kThreads) eta_direct_kernel(const T* __restric
     const T* plane = bpad + (long long)(x + g.px + a) * g.pxs;
     for (int b0 = 0; b0 < cd.lb; b0 += g.brows) {
       const int nb = min(g.brows, cd.lb - b0);
-      // skip chunks without taps (warp-uniform: every thread reads the same rows)
-      bool any = false;
+      bool any = false;  // chunk without taps: skip (uniform over the CTA)
       for (int bi = 0; bi < nb; ++bi) any |= cd.rows[ai * cd.lb + b0 + bi].y > 0;
       if (!any) continue;
       __syncthreads();
-      // stage rows y0 + lo_b + b0 .. + (kTY + nb - 1), cols z0 + cl .. + pitch
       const int nrows = kTY + nb - 1;
       const int nvec = g.pitch / 4;
       const T* src0 = plane + (long long)(y0 + g.py + cd.lo_b + b0) * g.pys + (z0 + g.pz + cd.cl);
@@ -206,7 +230,8 @@ __global__ void __launch_bounds__(kThreads) eta_direct_kernel(const T* __restric
         const T* srow = region + (lane + bi) * g.pitch + warp * kJ + 4 * rr.x;
         T buf[20];
 #pragma unroll
-        for (int q = 0; q < 5; ++q) ld4(srow + 4 * q, buf[4 * q], buf[4 * q + 1], buf[4 * q + 2], buf[4 * q + 3]);
+        for (int q = 0; q < 5; ++q)
+          ld4(srow + 4 * q, buf[4 * q], buf[4 * q + 1], buf[4 * q + 2], buf[4 * q + 3]);
         int s = 0;
         const int ns = rr.y;
         for (; s + 5 <= ns; s += 5) {
@@ -242,20 +267,30 @@ __global__ void __launch_bounds__(kThreads) eta_direct_kernel(const T* __restric
     if (row_win && z >= g.win[4] && z <= g.win[5] && better(eta, lin, best.v, best.idx))
       best = {eta, lin};
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ov = __shfl_xor_sync(0xffffffffu, best.v, o);
-    const long long oi = __shfl_xor_sync(0xffffffffu, best.idx, o);
-    if (better(ov, oi, best.v, best.idx)) best = {ov, oi};
+  reduce_store_best<T>(best, wbest, partial + (long long)blockIdx.y * gridDim.x + blockIdx.x);
+}
+
+// eta = acc / lam over a whole volume (basis path): optional field store and
+// windowed argmax; one partial record per CTA.
+template <typename T>
+__global__ void __launch_bounds__(256) volume_argmax_kernel(const T* __restrict__ acc, int nx, int ny,
+                                                            int nz, const int4 wlo, const int4 whi,
+                                                            double lam, T* __restrict__ field,
+                                                            Best* __restrict__ partial) {
+  __shared__ Best wbest[8];
+  Best best{-INFINITY, 0x7fffffffffffffffLL};
+  const long long n = (long long)nx * ny * nz;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+    const double eta = double(acc[i]) / lam;
+    if (field) field[i] = T(eta);
+    const int z = int(i % nz);
+    const int y = int((i / nz) % ny);
+    const int x = int(i / ((long long)ny * nz));
+    if (x >= wlo.x && x <= whi.x && y >= wlo.y && y <= whi.y && z >= wlo.z && z <= whi.z &&
+        better(eta, i, best.v, best.idx))
+      best = {eta, i};
   }
-  if (lane == 0) wbest[warp] = best;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    Best b = wbest[0];
-    for (int w = 1; w < kWarps; ++w)
-      if (better(wbest[w].v, wbest[w].idx, b.v, b.idx)) b = wbest[w];
-    partial[(long long)blockIdx.y * gridDim.x + blockIdx.x] = b;
-  }
+  reduce_store_best<T>(best, wbest, partial + blockIdx.x);
 }
 
 // periodic padding: dst[X][Y][Z] = src[(X-px) mod nx][(Y-py) mod ny][(Z-pz) mod nz]
@@ -281,30 +316,15 @@ __global__ void best_reduce_kernel(const Best* __restrict__ partial, long long n
     const Best p = partial[i];
     if (better(p.v, p.idx, b.v, b.idx)) b = p;
   }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ov = __shfl_xor_sync(0xffffffffu, b.v, o);
-    const long long oi = __shfl_xor_sync(0xffffffffu, b.idx, o);
-    if (better(ov, oi, b.v, b.idx)) b = {ov, oi};
-  }
-  if (lane == 0) sb[warp] = b;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    Best r = sb[0];
-    for (int w = 1; w < (int)(blockDim.x / 32); ++w)
-      if (better(sb[w].v, sb[w].idx, r.v, r.idx)) r = sb[w];
-    *out = r;
-  }
+  reduce_store_best<double>(b, sb, out);
 }
 
 int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
 // smem row pitch: >= cols needed, and == 4 (mod 32) elements for fp32
-// (conflict-free LDS.128 across 8 consecutive rows); fp64 uses == 2 (mod 16).
+// (conflict-free LDS.128 across 8 consecutive rows); fp64 uses == 4 (mod 16).
 int region_pitch(int lc4, int esize) {
-  int need = lc4 + kTZ + 8;
-  int p = round_up(need, 4);
+  int p = round_up(lc4 + kTZ + 8, 4);
   if (esize == 4) {
     while (p % 32 != 4) p += 4;
   } else {
@@ -313,16 +333,194 @@ int region_pitch(int lc4, int esize) {
   return p;
 }
 
+// ------------------------------------------------------------------ NNLS
+// Lawson-Hanson non-negative least squares min ||A x - g||, x >= 0, with the
+// passive-set subproblems solved by Householder QR. A is column-major M x N.
+void lsq_qr(const std::vector<double>& A, int M, const std::vector<int>& cols,
+            const std::vector<double>& g, std::vector<double>& z) {
+  const int p = int(cols.size());
+  std::vector<double> B(size_t(M) * p), rhs(g);
+  std::vector<double> scale(p);
+  for (int j = 0; j < p; ++j) {
+    double s = 0.0;
+    for (int i = 0; i < M; ++i) s += A[size_t(cols[j]) * M + i] * A[size_t(cols[j]) * M + i];
+    scale[j] = s > 0 ? 1.0 / std::sqrt(s) : 1.0;
+    for (int i = 0; i < M; ++i) B[size_t(j) * M + i] = A[size_t(cols[j]) * M + i] * scale[j];
+  }
+  for (int j = 0; j < p; ++j) {  // Householder on column j, rows j..M-1
+    double* c = &B[size_t(j) * M];
+    double nrm = 0.0;
+    for (int i = j; i < M; ++i) nrm += c[i] * c[i];
+    nrm = std::sqrt(nrm);
+    if (nrm == 0.0) continue;
+    const double alpha = c[j] > 0 ? -nrm : nrm;
+    std::vector<double> v(c + j, c + M);
+    v[0] -= alpha;
+    double vn = 0.0;
+    for (double x : v) vn += x * x;
+    if (vn == 0.0) continue;
+    auto apply = [&](double* col) {
+      double dot = 0.0;
+      for (int i = j; i < M; ++i) dot += v[i - j] * col[i];
+      const double f = 2.0 * dot / vn;
+      for (int i = j; i < M; ++i) col[i] -= f * v[i - j];
+    };
+    for (int k = j; k < p; ++k) apply(&B[size_t(k) * M]);
+    apply(rhs.data());
+  }
+  z.assign(p, 0.0);
+  for (int j = p - 1; j >= 0; --j) {
+    double s = rhs[j];
+    for (int k = j + 1; k < p; ++k) s -= B[size_t(k) * M + j] * z[k];
+    const double r = B[size_t(j) * M + j];
+    z[j] = r != 0.0 ? s / r : 0.0;
+  }
+  for (int j = 0; j < p; ++j) z[j] *= scale[j];
+}
+
+void nnls(const std::vector<double>& A, int M, int N, const std::vector<double>& g,
+          std::vector<double>& x) {
+  x.assign(N, 0.0);
+  std::vector<char> passive(N, 0);
+  std::vector<double> r(g), wgrad(N);
+  double gnorm = 0.0;
+  for (double v : g) gnorm = std::max(gnorm, std::fabs(v));
+  const double tol = 1e-15 * std::max(1.0, gnorm) * M;
+  for (int outer = 0; outer < 3 * N; ++outer) {
+    for (int i = 0; i < M; ++i) {
+      double s = g[i];
+      for (int j = 0; j < N; ++j)
+        if (x[j] != 0.0) s -= A[size_t(j) * M + i] * x[j];
+      r[i] = s;
+    }
+    int jmax = -1;
+    double best = tol;
+    for (int j = 0; j < N; ++j) {
+      if (passive[j]) continue;
+      double s = 0.0;
+      for (int i = 0; i < M; ++i) s += A[size_t(j) * M + i] * r[i];
+      wgrad[j] = s;
+      if (s > best) {
+        best = s;
+        jmax = j;
+      }
+    }
+    if (jmax < 0) break;
+    passive[jmax] = 1;
+    for (int inner = 0; inner < 3 * N; ++inner) {
+      std::vector<int> cols;
+      for (int j = 0; j < N; ++j)
+        if (passive[j]) cols.push_back(j);
+      std::vector<double> z;
+      lsq_qr(A, M, cols, g, z);
+      bool ok = true;
+      for (double v : z) ok &= v > 0.0;
+      if (ok) {
+        std::fill(x.begin(), x.end(), 0.0);
+        for (size_t q = 0; q < cols.size(); ++q) x[cols[q]] = z[q];
+        break;
+      }
+      double alpha = 1.0;
+      for (size_t q = 0; q < cols.size(); ++q)
+        if (z[q] <= 0.0) {
+          const double xv = x[cols[q]];
+          const double a = xv / (xv - z[q]);
+          if (a < alpha) alpha = a;
+        }
+      for (size_t q = 0; q < cols.size(); ++q) {
+        const int j = cols[q];
+        x[j] += alpha * (z[q] - x[j]);
+        if (x[j] <= 1e-300) {
+          x[j] = 0.0;
+          passive[j] = 0;
+        }
+      }
+    }
+  }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ table
-static int build_candidate(const int dims[3], double sigma, double d, double tap_tol, CandHost& c) {
+static int upload(void** dst, const void* src, size_t bytes) {
+  SFW3D_CUDA_TRY(cudaMalloc(dst, bytes));
+  SFW3D_CUDA_TRY(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
+  return SFW3D_OK;
+}
+
+static int fit_basis(CandHost& c) {
+  const double inv2sd = 0.5 / std::pow(c.sigma, c.d);
+  const int l[3] = {c.hi[0] - c.lo[0] + 1, c.hi[1] - c.lo[1] + 1, c.hi[2] - c.lo[2] + 1};
+  if (c.d == 2.0) {  // exp(-inv2sd * (a^2 + b^2 + c^2)) = product of three 1-D Gaussians
+    c.exact_sep = true;
+    c.fit_err = 0.0;
+    c.w0 = 0.0;
+    c.terms.push_back({inv2sd, 1.0});
+  } else {
+    // lattice values s = a^2 + b^2 + c^2 present in the box
+    int smax = 0;
+    for (int a = 0; a < 3; ++a) smax += std::max(c.lo[a] * c.lo[a], c.hi[a] * c.hi[a]);
+    std::vector<char> present(size_t(smax) + 1, 0);
+    std::vector<char> sq[3];
+    for (int ax = 0; ax < 3; ++ax) sq[ax].assign(size_t(smax) + 1, 0);
+    for (int ax = 0; ax < 3; ++ax)
+      for (int t = c.lo[ax]; t <= c.hi[ax]; ++t) sq[ax][size_t(t) * t] = 1;
+    std::vector<int> sv[3];
+    for (int ax = 0; ax < 3; ++ax)
+      for (int s = 0; s <= smax; ++s)
+        if (sq[ax][s]) sv[ax].push_back(s);
+    for (int s0 : sv[0])
+      for (int s1 : sv[1])
+        for (int s2 : sv[2]) present[size_t(s0) + s1 + s2] = 1;
+    std::vector<double> S;
+    for (int s = 0; s <= smax; ++s)
+      if (present[s]) S.push_back(double(s));
+    const int M = int(S.size());
+    const int K = 48;
+    const double rmax = std::max({-c.lo[0], c.hi[0], -c.lo[1], c.hi[1], -c.lo[2], c.hi[2], 1});
+    const double bmin = 0.5 / (rmax * rmax), bmax = 30.0;
+    std::vector<double> betas(K), A(size_t(M) * (K + 1)), g(M);
+    for (int k = 0; k < K; ++k) betas[k] = bmin * std::pow(bmax / bmin, double(k) / (K - 1));
+    for (int i = 0; i < M; ++i) {
+      const double s = S[i];
+      g[i] = std::exp(-inv2sd * std::pow(s, 0.5 * c.d));
+      for (int k = 0; k < K; ++k) A[size_t(k) * M + i] = std::exp(-betas[k] * s);
+      A[size_t(K) * M + i] = s == 0.0 ? 1.0 : 0.0;  // delta term
+    }
+    std::vector<double> x;
+    nnls(A, M, K + 1, g, x);
+    double err = 0.0;
+    for (int i = 0; i < M; ++i) {
+      double v = 0.0;
+      for (int k = 0; k <= K; ++k) v += A[size_t(k) * M + i] * x[k];
+      err = std::max(err, std::fabs(v - g[i]));
+    }
+    c.fit_err = err;
+    c.w0 = x[K];
+    for (int k = 0; k < K; ++k)
+      if (x[k] > 0.0) c.terms.push_back({betas[k], x[k]});
+  }
+  c.basis_taps = (c.w0 != 0.0 ? 1 : 0);
+  for (auto& t : c.terms) {
+    std::vector<double> h64;
+    for (int ax = 0; ax < 3; ++ax)
+      for (int q = c.lo[ax]; q <= c.hi[ax]; ++q) h64.push_back(std::exp(-t.beta * double(q) * q));
+    std::vector<float> h32(h64.begin(), h64.end());
+    SFW3D_TRY(upload(&t.taps64, h64.data(), h64.size() * sizeof(double)));
+    SFW3D_TRY(upload(&t.taps32, h32.data(), h32.size() * sizeof(float)));
+    c.basis_taps += l[0] + l[1] + l[2];
+  }
+  return SFW3D_OK;
+}
+
+static int build_candidate(const int dims[3], double sigma, double d, double tap_tol, bool basis,
+                           CandHost& c) {
   c.sigma = sigma;
   c.d = d;
-  const double rr = std::ceil(sigma * std::pow(kTailExponent, 1.0 / d));
+  const double rr = std::ceil(sigma * std::pow(kTailExponent, 1.0 / d));  // forward.py:97-99
   const int R = int(rr);
   for (int a = 0; a < 3; ++a) {
-    if (2LL * R + 1 >= dims[a]) {
+    if (2LL * R + 1 >= dims[a]) {  // full axis, minimum-image offsets (forward.py:107-109)
       c.lo[a] = -(dims[a] / 2);
       c.hi[a] = c.lo[a] + dims[a] - 1;
     } else {
@@ -347,7 +545,7 @@ static int build_candidate(const int dims[3], double sigma, double d, double tap
       int cmin = 1 << 30, cmax = -(1 << 30);
       double* row = &t[(size_t(ai) * c.lb + bi) * c.lc4];
       for (int cc = c.lo[2]; cc <= c.hi[2]; ++cc) {
-        const double u2 = (a * a + b * b) + double(cc) * cc;
+        const double u2 = (a * a + b * b) + double(cc) * cc;  // forward.py:133
         const double tt = inv2sd * (d2 ? u2 : std::pow(u2, half_d));
         const double v = std::exp(-tt);
         row[cc - c.cl] = v;
@@ -363,18 +561,19 @@ static int build_candidate(const int dims[3], double sigma, double d, double tap
       }
     }
   }
-  cudaError_t e = cudaMalloc(&c.t64, t.size() * sizeof(double));
-  if (e == cudaSuccess) e = cudaMalloc(&c.t32, t.size() * sizeof(float));
-  if (e == cudaSuccess) e = cudaMalloc(&c.rows_dev, c.rows.size() * sizeof(int2));
-  if (e != cudaSuccess) {
-    set_error(std::string("CUDA error ") + cudaGetErrorString(e));
-    return e == cudaErrorMemoryAllocation ? SFW3D_ENOMEM : SFW3D_ECUDA;
-  }
   std::vector<float> t32(t.begin(), t.end());
-  SFW3D_CUDA_TRY(cudaMemcpy(c.t64, t.data(), t.size() * sizeof(double), cudaMemcpyHostToDevice));
-  SFW3D_CUDA_TRY(cudaMemcpy(c.t32, t32.data(), t32.size() * sizeof(float), cudaMemcpyHostToDevice));
-  SFW3D_CUDA_TRY(cudaMemcpy(c.rows_dev, c.rows.data(), c.rows.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  SFW3D_TRY(upload(reinterpret_cast<void**>(&c.t64), t.data(), t.size() * sizeof(double)));
+  SFW3D_TRY(upload(reinterpret_cast<void**>(&c.t32), t32.data(), t32.size() * sizeof(float)));
+  SFW3D_TRY(upload(reinterpret_cast<void**>(&c.rows_dev), c.rows.data(), c.rows.size() * sizeof(int2)));
+  if (basis) SFW3D_TRY(fit_basis(c));
   return SFW3D_OK;
+}
+
+// evaluator choice per candidate and storage type
+static bool use_basis(const sfw3d_table* t, const CandHost& c, int dtype) {
+  if (t->mode == 1 || c.terms.empty()) return false;
+  if (c.exact_sep) return true;
+  return dtype == SFW3D_F32 && c.fit_err <= t->basis_tol && c.basis_taps < c.taps;
 }
 
 }  // namespace sfw3d
@@ -388,6 +587,10 @@ extern "C" int sfw3d_table_destroy(sfw3d_table* t) {
     if (c.t64) cudaFree(c.t64);
     if (c.t32) cudaFree(c.t32);
     if (c.rows_dev) cudaFree(c.rows_dev);
+    for (auto& term : c.terms) {
+      if (term.taps64) cudaFree(term.taps64);
+      if (term.taps32) cudaFree(term.taps32);
+    }
   }
   delete t;
   return SFW3D_OK;
@@ -396,7 +599,6 @@ extern "C" int sfw3d_table_destroy(sfw3d_table* t) {
 extern "C" int sfw3d_table_create(sfw3d_ctx* ctx, const sfw3d_psf* psf, int n_sigma,
                                   const double* sigma_host, int n_shape, const double* shape_host,
                                   double tap_tol, int mode, double basis_tol, sfw3d_table** out) {
-  (void)basis_tol;
   SFW3D_CHECK_ARG(ctx && psf && out, "NULL argument");
   SFW3D_CHECK_ARG(n_sigma > 0 && n_shape > 0 && sigma_host && shape_host,
                   "parameter grids must be non-empty");
@@ -406,7 +608,7 @@ extern "C" int sfw3d_table_create(sfw3d_ctx* ctx, const sfw3d_psf* psf, int n_si
   std::vector<double> sg(sigma_host, sigma_host + n_sigma), dg(shape_host, shape_host + n_shape);
   for (double v : sg) SFW3D_CHECK_ARG(std::isfinite(v) && v > 0.0, "sigma grid values must be > 0");
   for (double v : dg) SFW3D_CHECK_ARG(std::isfinite(v) && v > 0.0, "shape grid values must be > 0");
-  std::sort(sg.begin(), sg.end());
+  std::sort(sg.begin(), sg.end());  // certificate.py:72-73
   std::sort(dg.begin(), dg.end());
   auto* t = new sfw3d_table();
   for (int a = 0; a < 3; ++a) t->dims[a] = psf->dims[a];
@@ -414,18 +616,18 @@ extern "C" int sfw3d_table_create(sfw3d_ctx* ctx, const sfw3d_psf* psf, int n_si
   t->n_shape = n_shape;
   t->psf = psf;
   t->device = ctx->device;
+  t->mode = mode;
+  t->basis_tol = basis_tol;
   t->cands.resize(size_t(n_sigma) * n_shape);
-  t->taps_per_voxel = 0;
   int maxlo[3] = {0, 0, 0}, maxhi[3] = {0, 0, 0}, maxpitch = 0;
   for (int i = 0; i < n_sigma; ++i)
     for (int j = 0; j < n_shape; ++j) {
       CandHost& c = t->cands[size_t(i) * n_shape + j];
-      int s = build_candidate(t->dims, sg[i], dg[j], tap_tol, c);
+      const int s = build_candidate(t->dims, sg[i], dg[j], tap_tol, mode == 0, c);
       if (s != SFW3D_OK) {
         sfw3d_table_destroy(t);
         return s;
       }
-      t->taps_per_voxel += c.taps;
       maxlo[0] = std::max(maxlo[0], -c.lo[0]);
       maxhi[0] = std::max(maxhi[0], c.hi[0]);
       maxlo[1] = std::max(maxlo[1], -c.lo[1]);
@@ -445,13 +647,37 @@ extern "C" int sfw3d_table_create(sfw3d_ctx* ctx, const sfw3d_psf* psf, int n_si
   return SFW3D_OK;
 }
 
-extern "C" int sfw3d_table_info(const sfw3d_table* t, int* n_cand, int* n_direct, int* n_basis,
-                                int64_t* taps_per_voxel) {
+extern "C" int sfw3d_table_info(const sfw3d_table* t, int dtype, int* n_cand, int* n_direct,
+                                int* n_basis, int64_t* direct_taps, int64_t* basis_taps) {
   SFW3D_CHECK_ARG(t, "table is NULL");
+  int nb = 0;
+  long long dt = 0, bt = 0;
+  for (const auto& c : t->cands) {
+    if (use_basis(t, c, dtype)) {
+      ++nb;
+      bt += c.basis_taps;
+    } else {
+      dt += c.taps;
+    }
+  }
   if (n_cand) *n_cand = int(t->cands.size());
-  if (n_direct) *n_direct = int(t->cands.size());
-  if (n_basis) *n_basis = 0;
-  if (taps_per_voxel) *taps_per_voxel = t->taps_per_voxel;
+  if (n_direct) *n_direct = int(t->cands.size()) - nb;
+  if (n_basis) *n_basis = nb;
+  if (direct_taps) *direct_taps = dt;
+  if (basis_taps) *basis_taps = bt;
+  return SFW3D_OK;
+}
+
+extern "C" int sfw3d_table_candidate(const sfw3d_table* t, int dtype, int cand, int* uses_basis,
+                                     int* n_terms, double* fit_err, int64_t* direct_taps,
+                                     int64_t* basis_taps) {
+  SFW3D_CHECK_ARG(t && cand >= 0 && cand < int(t->cands.size()), "candidate index");
+  const CandHost& c = t->cands[cand];
+  if (uses_basis) *uses_basis = use_basis(t, c, dtype) ? 1 : 0;
+  if (n_terms) *n_terms = int(c.terms.size()) + (c.w0 != 0.0 ? 1 : 0);
+  if (fit_err) *fit_err = c.fit_err;
+  if (direct_taps) *direct_taps = c.taps;
+  if (basis_taps) *basis_taps = c.basis_taps;
   return SFW3D_OK;
 }
 
@@ -459,16 +685,17 @@ namespace {
 
 template <typename T>
 int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double lam,
-              const int32_t win_in[6], sfw3d_argmax* best_host, sfw3d_argmax* per_cand_host,
+              const int32_t win[6], sfw3d_argmax* best_host, sfw3d_argmax* per_cand_host,
               void* fields) {
+  const int dtype = sizeof(T) == 8 ? SFW3D_F64 : SFW3D_F32;
   const int* dims = t->dims;
   const int64_t n = vol_count(dims);
   const size_t vb = size_t(n) * sizeof(T);
-  const size_t pb = size_t(t->pdims[0]) * t->pdims[1] * t->pdims[2] * sizeof(T);
   const int nc = int(t->cands.size());
-  // output tiles: the window, or the whole grid when fields are requested
-  int win[6];
-  for (int a = 0; a < 6; ++a) win[a] = win_in[a];
+  bool any_direct = false, any_basis = false;
+  for (const auto& c : t->cands) (use_basis(t, c, dtype) ? any_basis : any_direct) = true;
+  const size_t pb = any_direct ? size_t(t->pdims[0]) * t->pdims[1] * t->pdims[2] * sizeof(T) : 0;
+  // direct output tiles: the window, or the whole grid when fields are requested
   int ow[6];
   if (fields) {
     ow[0] = 0; ow[1] = dims[0] - 1; ow[2] = 0; ow[3] = dims[1] - 1; ow[4] = 0; ow[5] = dims[2] - 1;
@@ -479,26 +706,30 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   const int nty = (ow[3] - ow[2] + 1 + kTY - 1) / kTY;
   const int ntz = (ow[5] - zbase + 1 + kTZ - 1) / kTZ;
   const int nxp = ow[1] - ow[0] + 1;
-  const long long nblocks = (long long)nty * ntz * nxp;
-  SFW3D_TRY(ensure_device(ctx, ctx->ws, Carver::need({vb, vb, pb, size_t(nblocks) * sizeof(Best),
-                                                      size_t(nc) * sizeof(Best)})));
+  const long long nblocks_direct = (long long)nty * ntz * nxp;
+  const int nblocks_vol = 4 * ctx->num_sms;
+  const long long nblocks = std::max<long long>(nblocks_direct, nblocks_vol);
+  SFW3D_TRY(ensure_device(ctx, ctx->ws,
+                          Carver::need({vb, vb, any_basis ? vb : 0, any_basis ? vb : 0, pb,
+                                        size_t(nblocks) * sizeof(Best), size_t(nc) * sizeof(Best)})));
   Carver cv(ctx->ws.ptr);
   T* b = cv.take<T>(n);
   T* tmp = cv.take<T>(n);
-  T* bpad = cv.take<T>(size_t(pb / sizeof(T)));
+  T* t2 = any_basis ? cv.take<T>(n) : nullptr;
+  T* acc = any_basis ? cv.take<T>(n) : nullptr;
+  T* bpad = any_direct ? cv.take<T>(pb / sizeof(T)) : nullptr;
   Best* partial = cv.take<Best>(nblocks);
   Best* cbest = cv.take<Best>(nc);
-  // b = H^T * r, then periodic padding
-  SFW3D_TRY(psf_apply_impl(ctx, t->psf, sizeof(T) == 8 ? SFW3D_F64 : SFW3D_F32, residual, b, 1, tmp));
-  const long long np = (long long)t->pdims[0] * t->pdims[1] * t->pdims[2];
-  {
+  // b = H^T * r (tmp is pass scratch), then the periodic padding for direct
+  SFW3D_TRY(psf_apply_impl(ctx, t->psf, dtype, residual, b, 1, tmp));
+  if (any_direct) {
     SFW3D_PROF(ctx, "pad");
+    const long long np = (long long)t->pdims[0] * t->pdims[1] * t->pdims[2];
     pad_kernel<T><<<unsigned((np + 255) / 256), 256, 0, ctx->stream>>>(
         b, bpad, dims[0], dims[1], dims[2], t->pad[0], t->pad[1], t->pad[2], t->pdims[0],
         t->pdims[1], t->pdims[2]);
     SFW3D_LAUNCH_CHECK(ctx);
   }
-
   Geo g;
   g.nx = dims[0]; g.ny = dims[1]; g.nz = dims[2];
   g.px = t->pad[0]; g.py = t->pad[1]; g.pz = t->pad[2];
@@ -516,36 +747,61 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   const int budget = std::min(smem_max - 2048, 110 * 1024);
   for (int ci = 0; ci < nc; ++ci) {
     const CandHost& c = t->cands[ci];
-    CandDev cd;
-    cd.taps = sizeof(T) == 8 ? static_cast<const void*>(c.t64) : static_cast<const void*>(c.t32);
-    cd.rows = c.rows_dev;
-    cd.lo_a = c.lo[0];
-    cd.lo_b = c.lo[1];
-    cd.la = c.la;
-    cd.lb = c.lb;
-    cd.cl = c.cl;
-    cd.lc4 = c.lc4;
-    Geo gc = g;
-    gc.pitch = region_pitch(c.lc4, sizeof(T));
-    const int row_bytes = gc.pitch * int(sizeof(T));
-    const int brows = budget / row_bytes - (kTY - 1);
-    if (brows < 1) {
-      set_error("certificate template too wide for the shared-memory tile");
-      return SFW3D_EINVAL;
-    }
-    gc.brows = std::min(brows, c.lb);
-    const int smem = (kTY + gc.brows - 1) * row_bytes;
-    SFW3D_CUDA_TRY(cudaFuncSetAttribute(eta_direct_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    dim3 grid(unsigned(nty * ntz), unsigned(nxp));
     T* fld = fields ? static_cast<T*>(fields) + size_t(ci) * n : nullptr;
-    {
+    long long nred = 0;
+    if (use_basis(t, c, dtype)) {
+      // acc = w0 * b + sum_k w_k (f_k x f_k x f_k) * b   (separable passes)
+      const int l[3] = {c.hi[0] - c.lo[0] + 1, c.hi[1] - c.lo[1] + 1, c.hi[2] - c.lo[2] + 1};
+      for (size_t k = 0; k < c.terms.size(); ++k) {
+        const Term& term = c.terms[k];
+        const T* taps = static_cast<const T*>(dtype == SFW3D_F64 ? term.taps64 : term.taps32);
+        SFW3D_TRY(corr_pass_impl(ctx, dtype, b, tmp, dims, 2, taps + l[0] + l[1], c.lo[2], l[2],
+                                 nullptr, 0.0, 1.0, "eta_basis"));
+        SFW3D_TRY(corr_pass_impl(ctx, dtype, tmp, t2, dims, 1, taps + l[0], c.lo[1], l[1], nullptr,
+                                 0.0, 1.0, "eta_basis"));
+        const void* addend = k == 0 ? (c.w0 != 0.0 ? static_cast<const void*>(b) : nullptr)
+                                    : static_cast<const void*>(acc);
+        const double aw = k == 0 ? c.w0 : 1.0;
+        SFW3D_TRY(corr_pass_impl(ctx, dtype, t2, acc, dims, 0, taps, c.lo[0], l[0], addend, aw,
+                                 term.w, "eta_basis"));
+      }
+      SFW3D_PROF(ctx, "argmax");
+      volume_argmax_kernel<T><<<nblocks_vol, 256, 0, ctx->stream>>>(
+          acc, dims[0], dims[1], dims[2], make_int4(win[0], win[2], win[4], 0),
+          make_int4(win[1], win[3], win[5], 0), lam, fld, partial);
+      SFW3D_LAUNCH_CHECK(ctx);
+      nred = nblocks_vol;
+    } else {
+      CandDev cd;
+      cd.taps = sizeof(T) == 8 ? static_cast<const void*>(c.t64) : static_cast<const void*>(c.t32);
+      cd.rows = c.rows_dev;
+      cd.lo_a = c.lo[0];
+      cd.lo_b = c.lo[1];
+      cd.la = c.la;
+      cd.lb = c.lb;
+      cd.cl = c.cl;
+      cd.lc4 = c.lc4;
+      Geo gc = g;
+      gc.pitch = region_pitch(c.lc4, sizeof(T));
+      const int row_bytes = gc.pitch * int(sizeof(T));
+      const int brows = budget / row_bytes - (kTY - 1);
+      if (brows < 1) {
+        set_error("certificate template too wide for the shared-memory tile");
+        return SFW3D_EINVAL;
+      }
+      gc.brows = std::min(brows, c.lb);
+      const int smem = (kTY + gc.brows - 1) * row_bytes;
+      SFW3D_CUDA_TRY(cudaFuncSetAttribute(eta_direct_kernel<T>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      dim3 grid(unsigned(nty * ntz), unsigned(nxp));
       SFW3D_PROF(ctx, "eta_direct");
       eta_direct_kernel<T><<<grid, kThreads, smem, ctx->stream>>>(bpad, gc, cd, fld, partial);
       SFW3D_LAUNCH_CHECK(ctx);
+      nred = nblocks_direct;
     }
     {
       SFW3D_PROF(ctx, "argmax");
-      best_reduce_kernel<<<1, 1024, 0, ctx->stream>>>(partial, nblocks, cbest + ci);
+      best_reduce_kernel<<<1, 1024, 0, ctx->stream>>>(partial, nred, cbest + ci);
       SFW3D_LAUNCH_CHECK(ctx);
     }
   }

@@ -169,6 +169,13 @@ namespace sfw3d {
 int psf_apply_impl(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* in,
                    void* out, int adjoint, void* tmp);
 
+// One circular 1-D correlation pass along `axis`:
+//   out[i] = addend_w * addend[i] + w * sum_q taps[q] * in[i + (lo + q) e_axis]
+// (addend may be NULL or alias out; taps are device pointers of the dtype).
+int corr_pass_impl(sfw3d_ctx* ctx, int dtype, const void* in, void* out, const int dims[3], int axis,
+                   const void* taps, int lo, int ntaps, const void* addend, double addend_w,
+                   double w, const char* family);
+
 // Launch helpers implemented in the .cu files.
 int render_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const AtomGeo* atoms_dev,
                 int k, void* out);

@@ -1,54 +1,124 @@
-// K4 — circular PSF convolution / adjoint correlation, spatial domain.
+// K4 — circular 1-D correlation passes: the PSF (convolve / correlate_adjoint,
+// forward.py:79-94) and the separable Gaussian-basis certificate terms.
 //
-// Replaces convolve / correlate_adjoint (forward.py:79-94), which the
-// reference evaluates as rfftn -> product with kernel_hat -> irfftn. Every
+// The reference applies the PSF as rfftn -> product -> irfftn. Every
 // BASELINE PSF is a box-truncated sampled Gaussian, i.e. exactly separable,
-// so the operator is three 1-D circular passes (one per axis) with
-// (hi - lo + 1) taps each instead of a 3-D FFT pair; a non-separable kernel
-// falls back to a direct 3-D stencil over its non-zero box. Offsets are
-// relative to the kernel origin n//2 (forward.py:43-47, ifftshift at :58).
+// so here the operator is three 1-D circular passes (one per axis) with
+// (hi - lo + 1) taps each; a non-separable kernel falls back to a direct
+// 3-D stencil over its non-zero box. Offsets are relative to the kernel
+// origin n//2 (forward.py:43-47, ifftshift at :58).
+//
+// Pass kernels (out = addend_w * addend + w * sum_q taps[q] * in[i + lo + q]):
+//  * axes 0/1 (strided): one thread per contiguous inner index (coalesced
+//    across the warp) computing J consecutive outputs along the axis with a
+//    register window rotated at compile time (1 load + J FFMA per tap),
+//    taps broadcast from shared memory;
+//  * axis 2 (contiguous): a CTA stages 32 rows x (4J + taps) in shared
+//    memory (odd pitch: lane = row, conflict-free), same rotated window.
 #include "internal.cuh"
 
 namespace sfw3d {
 namespace {
 
-// out[a0 + j] = sum_q taps[q] * in[a0 + j + lo + q]   (circular along `axis`)
-// Thread layout: (outer, a-block, inner) with inner the contiguous block of
-// the axes after `axis`, so a warp reads consecutive addresses for axes 0/1.
+__device__ __forceinline__ int wrap_inc(int i, int n) { return (i + 1 == n) ? 0 : i + 1; }
+
+__device__ __forceinline__ int pmod_i(long long a, int n) {
+  long long r = a % n;
+  return int(r < 0 ? r + n : r);
+}
+
 template <typename T, int J>
-__global__ void __launch_bounds__(256) pass1d_kernel(const T* __restrict__ in, T* __restrict__ out,
-                                                     int n_axis, long long stride, long long n_outer,
-                                                     const T* __restrict__ taps, int lo, int ntaps) {
-  const int nblk = (n_axis + J - 1) / J;
-  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long total = n_outer * nblk * stride;
-  if (t >= total) return;
-  long long inner = t % stride;
-  long long rest = t / stride;
-  int blk = int(rest % nblk);
-  long long outer = rest / nblk;
-  const long long base = outer * (long long)n_axis * stride + inner;
-  const int a0 = blk * J;
-
-  T acc[J];
+__global__ void __launch_bounds__(256) pass_strided_kernel(
+    const T* __restrict__ in, T* out, int n_axis, long long stride, const T* __restrict__ taps_g,
+    int lo, int ntaps, const T* addend, T aw, T w) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* taps = reinterpret_cast<T*>(smem_raw);
+  for (int q = threadIdx.x; q < ntaps; q += blockDim.x) taps[q] = taps_g[q];
+  __syncthreads();
+  const long long inner = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (inner >= stride) return;
+  const int a0 = blockIdx.y * J;
+  const long long base = (long long)blockIdx.z * n_axis * stride + inner;
+  T W[J], acc[J];
+  int idx = pmod_i((long long)a0 + lo, n_axis);
 #pragma unroll
-  for (int j = 0; j < J; ++j) acc[j] = T(0);
-
-  int idx = (a0 + lo) % n_axis;
-  if (idx < 0) idx += n_axis;
-  const int nwin = J - 1 + ntaps;
-  for (int u = 0; u < nwin; ++u) {
-    const T v = in[base + idx * stride];
+  for (int j = 0; j < J; ++j) {
+    W[j] = in[base + idx * stride];
+    idx = wrap_inc(idx, n_axis);
+    acc[j] = T(0);
+  }
+  for (int q0 = 0; q0 < ntaps; q0 += J) {
 #pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const int q = u - j;
-      if (q >= 0 && q < ntaps) acc[j] = fma(taps[q], v, acc[j]);
+    for (int r = 0; r < J; ++r) {
+      if (q0 + r < ntaps) {
+        const T t = taps[q0 + r];
+#pragma unroll
+        for (int j = 0; j < J; ++j) acc[j] = fma(t, W[(r + j) % J], acc[j]);
+        W[r] = in[base + idx * stride];
+        idx = wrap_inc(idx, n_axis);
+      }
     }
-    if (++idx == n_axis) idx = 0;
   }
 #pragma unroll
-  for (int j = 0; j < J; ++j)
-    if (a0 + j < n_axis) out[base + (long long)(a0 + j) * stride] = acc[j];
+  for (int j = 0; j < J; ++j) {
+    if (a0 + j < n_axis) {
+      const long long o = base + (long long)(a0 + j) * stride;
+      out[o] = addend ? T(aw * addend[o] + w * acc[j]) : T(w * acc[j]);
+    }
+  }
+}
+
+constexpr int kZRows = 32;   // rows per CTA (one per lane)
+constexpr int kZWarps = 4;   // z-groups per CTA
+
+template <typename T, int J>
+__global__ void __launch_bounds__(32 * kZWarps) pass_z_kernel(
+    const T* __restrict__ in, T* out, int nz, long long nrows, const T* __restrict__ taps_g, int lo,
+    int ntaps, int pitch, const T* addend, T aw, T w) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* taps = reinterpret_cast<T*>(smem_raw);
+  T* tile = taps + ((ntaps + 3) & ~3);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long row0 = (long long)blockIdx.y * kZRows;
+  const int z0 = blockIdx.x * (J * kZWarps);
+  const int width = J * kZWarps + ntaps - 1 + J;  // staged columns
+  for (int q = threadIdx.x; q < ntaps; q += blockDim.x) taps[q] = taps_g[q];
+  for (int e = threadIdx.x; e < kZRows * width; e += blockDim.x) {
+    const int r = e / width, c = e % width;
+    const long long row = row0 + r;
+    T v = T(0);
+    if (row < nrows) v = in[row * nz + pmod_i((long long)z0 + lo + c, nz)];
+    tile[r * pitch + c] = v;
+  }
+  __syncthreads();
+  const T* src = tile + lane * pitch + warp * J;
+  T W[J], acc[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    W[j] = src[j];
+    acc[j] = T(0);
+  }
+  for (int q0 = 0; q0 < ntaps; q0 += J) {
+#pragma unroll
+    for (int r = 0; r < J; ++r) {
+      if (q0 + r < ntaps) {
+        const T t = taps[q0 + r];
+#pragma unroll
+        for (int j = 0; j < J; ++j) acc[j] = fma(t, W[(r + j) % J], acc[j]);
+        W[r] = src[q0 + r + J];
+      }
+    }
+  }
+  const long long row = row0 + lane;
+  if (row >= nrows) return;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int z = z0 + warp * J + j;
+    if (z < nz) {
+      const long long o = row * nz + z;
+      out[o] = addend ? T(aw * addend[o] + w * acc[j]) : T(w * acc[j]);
+    }
+  }
 }
 
 // General (non-separable) kernel: out[x] = sum_o K(o) in[x + sgn*o] over the
@@ -83,73 +153,108 @@ __global__ void __launch_bounds__(256) stencil3d_kernel(const T* __restrict__ in
   out[t] = acc;
 }
 
-template <typename T>
-int launch_pass(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis, const T* taps,
-                int lo, int ntaps) {
+template <typename T, int J>
+int launch_strided(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis, const T* taps,
+                   int lo, int ntaps, const T* addend, double aw, double w) {
   long long stride = 1;
   for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
   long long outer = 1;
   for (int a = 0; a < axis; ++a) outer *= dims[a];
   const int n = dims[axis];
-  SFW3D_PROF(ctx, "psf_pass");
-  if (axis == 2) {
-    constexpr int J = 1;
-    long long total = outer * ((n + J - 1) / J) * stride;
-    pass1d_kernel<T, J><<<unsigned((total + 255) / 256), 256, 0, ctx->stream>>>(
-        in, out, n, stride, outer, taps, lo, ntaps);
-  } else {
-    constexpr int J = 8;
-    long long total = outer * ((n + J - 1) / J) * stride;
-    pass1d_kernel<T, J><<<unsigned((total + 255) / 256), 256, 0, ctx->stream>>>(
-        in, out, n, stride, outer, taps, lo, ntaps);
-  }
+  dim3 grid(unsigned((stride + 255) / 256), unsigned((n + J - 1) / J), unsigned(outer));
+  pass_strided_kernel<T, J><<<grid, 256, size_t(ntaps) * sizeof(T), ctx->stream>>>(
+      in, out, n, stride, taps, lo, ntaps, addend, T(aw), T(w));
+  SFW3D_LAUNCH_CHECK(ctx);
+  return SFW3D_OK;
+}
+
+template <typename T, int J>
+int launch_z(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* taps, int lo,
+             int ntaps, const T* addend, double aw, double w) {
+  const long long nrows = (long long)dims[0] * dims[1];
+  const int width = J * kZWarps + ntaps - 1 + J;
+  const int pitch = width | 1;  // odd: 32 lanes on 32 rows hit 32 banks
+  const size_t smem = (size_t((ntaps + 3) & ~3) + size_t(kZRows) * pitch) * sizeof(T);
+  if (smem > 48 * 1024)
+    SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_z_kernel<T, J>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  dim3 grid(unsigned((dims[2] + J * kZWarps - 1) / (J * kZWarps)),
+            unsigned((nrows + kZRows - 1) / kZRows));
+  pass_z_kernel<T, J><<<grid, 32 * kZWarps, smem, ctx->stream>>>(in, out, dims[2], nrows, taps, lo,
+                                                                  ntaps, pitch, addend, T(aw), T(w));
   SFW3D_LAUNCH_CHECK(ctx);
   return SFW3D_OK;
 }
 
 template <typename T>
-int apply_typed(sfw3d_ctx* ctx, const sfw3d_psf* psf, const T* in, T* out, int adjoint, T* tmp,
-                const T* const taps[3], const T* box) {
-  const int* dims = psf->dims;
-  if (psf->separable) {
-    // adjoint: correlation with taps over [lo, hi]; forward: convolution =
-    // correlation with reversed taps over [-hi, -lo] (reversed copies are
-    // stored right after the forward taps, see psf_create).
-    int lo[3], nt[3];
-    const T* tp[3];
-    for (int a = 0; a < 3; ++a) {
-      nt[a] = psf->hi[a] - psf->lo[a] + 1;
-      lo[a] = adjoint ? psf->lo[a] : -psf->hi[a];
-      tp[a] = adjoint ? taps[a] : taps[a] + nt[a];
-    }
-    SFW3D_TRY(launch_pass<T>(ctx, in, out, dims, 2, tp[2], lo[2], nt[2]));
-    SFW3D_TRY(launch_pass<T>(ctx, out, tmp, dims, 1, tp[1], lo[1], nt[1]));
-    SFW3D_TRY(launch_pass<T>(ctx, tmp, out, dims, 0, tp[0], lo[0], nt[0]));
-    return SFW3D_OK;
+int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis, const T* taps,
+               int lo, int ntaps, const T* addend, double aw, double w) {
+  if (ntaps > 4096) {
+    set_error("1-D pass with more than 4096 taps");
+    return SFW3D_EINVAL;
   }
-  long long n = vol_count(dims);
-  const int l0 = psf->hi[0] - psf->lo[0] + 1, l1 = psf->hi[1] - psf->lo[1] + 1,
-            l2 = psf->hi[2] - psf->lo[2] + 1;
-  SFW3D_PROF(ctx, "psf_pass");
-  stencil3d_kernel<T><<<unsigned((n + 255) / 256), 256, 0, ctx->stream>>>(
-      in, out, dims[0], dims[1], dims[2], box, psf->lo[0], psf->lo[1], psf->lo[2], l0, l1, l2,
-      adjoint ? 1 : -1);
-  SFW3D_LAUNCH_CHECK(ctx);
-  return SFW3D_OK;
+  const bool wide = ntaps > 24;
+  if (axis == 2)
+    return wide ? launch_z<T, 32>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w)
+                : launch_z<T, 8>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
+  return wide ? launch_strided<T, 32>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w)
+              : launch_strided<T, 8>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
 }
 
 }  // namespace
 
+int corr_pass_impl(sfw3d_ctx* ctx, int dtype, const void* in, void* out, const int dims[3], int axis,
+                   const void* taps, int lo, int ntaps, const void* addend, double addend_w,
+                   double w, const char* family) {
+  SFW3D_PROF(ctx, family);
+  if (dtype == SFW3D_F64)
+    return pass_typed<double>(ctx, static_cast<const double*>(in), static_cast<double*>(out), dims,
+                              axis, static_cast<const double*>(taps), lo, ntaps,
+                              static_cast<const double*>(addend), addend_w, w);
+  return pass_typed<float>(ctx, static_cast<const float*>(in), static_cast<float*>(out), dims, axis,
+                           static_cast<const float*>(taps), lo, ntaps,
+                           static_cast<const float*>(addend), addend_w, w);
+}
+
 int psf_apply_impl(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* in, void* out,
                    int adjoint, void* tmp) {
-  if (dtype == SFW3D_F64) {
-    const double* taps[3] = {psf->taps64[0], psf->taps64[1], psf->taps64[2]};
-    return apply_typed<double>(ctx, psf, static_cast<const double*>(in), static_cast<double*>(out),
-                               adjoint, static_cast<double*>(tmp), taps, psf->box64);
+  const int* dims = psf->dims;
+  if (psf->separable) {
+    // adjoint: correlation with taps over [lo, hi]; forward: convolution =
+    // correlation with reversed taps over [-hi, -lo] (stored after the
+    // forward taps, see sfw3d_psf_create).
+    int lo[3], nt[3];
+    const void* tp[3];
+    for (int a = 0; a < 3; ++a) {
+      nt[a] = psf->hi[a] - psf->lo[a] + 1;
+      lo[a] = adjoint ? psf->lo[a] : -psf->hi[a];
+      if (dtype == SFW3D_F64)
+        tp[a] = adjoint ? psf->taps64[a] : psf->taps64[a] + nt[a];
+      else
+        tp[a] = adjoint ? psf->taps32[a] : psf->taps32[a] + nt[a];
+    }
+    SFW3D_TRY(corr_pass_impl(ctx, dtype, in, out, dims, 2, tp[2], lo[2], nt[2], nullptr, 0.0, 1.0,
+                             "psf_pass"));
+    SFW3D_TRY(corr_pass_impl(ctx, dtype, out, tmp, dims, 1, tp[1], lo[1], nt[1], nullptr, 0.0, 1.0,
+                             "psf_pass"));
+    SFW3D_TRY(corr_pass_impl(ctx, dtype, tmp, out, dims, 0, tp[0], lo[0], nt[0], nullptr, 0.0, 1.0,
+                             "psf_pass"));
+    return SFW3D_OK;
   }
-  const float* taps[3] = {psf->taps32[0], psf->taps32[1], psf->taps32[2]};
-  return apply_typed<float>(ctx, psf, static_cast<const float*>(in), static_cast<float*>(out),
-                            adjoint, static_cast<float*>(tmp), taps, psf->box32);
+  const long long n = vol_count(dims);
+  const int l0 = psf->hi[0] - psf->lo[0] + 1, l1 = psf->hi[1] - psf->lo[1] + 1,
+            l2 = psf->hi[2] - psf->lo[2] + 1;
+  SFW3D_PROF(ctx, "psf_pass");
+  if (dtype == SFW3D_F64)
+    stencil3d_kernel<double><<<unsigned((n + 255) / 256), 256, 0, ctx->stream>>>(
+        static_cast<const double*>(in), static_cast<double*>(out), dims[0], dims[1], dims[2],
+        psf->box64, psf->lo[0], psf->lo[1], psf->lo[2], l0, l1, l2, adjoint ? 1 : -1);
+  else
+    stencil3d_kernel<float><<<unsigned((n + 255) / 256), 256, 0, ctx->stream>>>(
+        static_cast<const float*>(in), static_cast<float*>(out), dims[0], dims[1], dims[2],
+        psf->box32, psf->lo[0], psf->lo[1], psf->lo[2], l0, l1, l2, adjoint ? 1 : -1);
+  SFW3D_LAUNCH_CHECK(ctx);
+  return SFW3D_OK;
 }
 
 }  // namespace sfw3d

@@ -1,0 +1,99 @@
+"""GPU tests of the certificate evaluators (direct correlation vs separable
+Gaussian basis) against the oracle's FFT eta_field.
+
+Bars: fp32 storage — eta within 1e-5 of eta_max (north-star bar) and the
+argmax identical unless the top two differ by < 1e-6 relative; fp64 — the
+direct path and the exact d = 2 separable path within 1e-10 of eta_max.
+"""
+import numpy as np
+import pytest
+
+import sfw3d_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2009_05473_b200 as pkg
+    pkg.set_precision("f64")
+    return pkg
+
+
+def cfg4_like(n, seed=0):
+    rng = np.random.default_rng(seed)
+    dims = (n, n, n)
+    kernel = O.box_gaussian_psf(dims, (3.0, 3.0, 3.0), (15, 15, 15))
+    rows = np.column_stack([rng.uniform(5, 10, 12), rng.uniform(0, n, (12, 3)),
+                            rng.uniform(1, 3, 12), rng.uniform(1.5, 3, 12)])
+    r = rng.standard_normal(dims) + O.conv(O.render(rows, dims), O.psf_hat(kernel))
+    return dims, kernel, r.astype(np.float32).astype(np.float64)
+
+
+def test_table_fits(P):
+    dims = (96, 96, 96)
+    psf = P.Psf(P.Volume(O.box_gaussian_psf(dims, (3, 3, 3), (15, 15, 15))), normalize=False)
+    table = P.build_template_table(psf, [1.0, 1.5, 2.0, 3.0], [1.5, 2.0, 2.5, 3.0])
+    with P.precision("f32"):
+        info = table.info()
+    for c in info["candidates"]:
+        if c["d"] == 2.0:
+            assert c["path"] == "basis" and c["fit_err"] == 0.0 and c["terms"] == 1
+        elif c["d"] < 2.0:
+            assert c["path"] == "basis" and c["fit_err"] <= 1e-9
+            assert c["basis_taps"] * 10 < c["direct_taps"]
+    with P.precision("f64"):
+        info64 = table.info()
+    for c in info64["candidates"]:
+        assert c["path"] == ("basis" if c["d"] == 2.0 else "direct")
+
+
+@pytest.mark.parametrize("n", [64, 80])
+def test_eta_f32_basis_vs_oracle(P, n):
+    dims, kernel, r = cfg4_like(n)
+    sg, dg = np.array([1.0, 1.5, 2.0, 3.0]), np.array([1.5, 2.0, 2.5, 3.0])
+    hats = O.template_hats(O.psf_hat(kernel), dims, sg, dg)
+    pos, flat, val, per, fields = O.eta_field(r, 1.0, hats, 4, None, keep_fields=True)
+    ref = np.stack(fields)
+    psf = P.Psf(P.Volume(kernel), normalize=False)
+    with P.precision("f32"):
+        for mode in ("auto", "direct"):
+            table = P.build_template_table(psf, sg, dg, mode=mode, tap_tol=1e-12)
+            f = P.eta_field(P.Volume(r), 1.0, table, keep_fields=True)
+            got = np.stack([v.data for v in f.fields])
+            err = np.max(np.abs(got - ref)) / abs(val)
+            assert err <= 1e-5, (mode, err)
+            assert abs(f.eta_max - val) <= 1e-5 * abs(val)
+            top = np.sort(np.array([v for _, v in per]))[::-1]
+            if top[0] - top[1] > 1e-6 * abs(top[0]):
+                assert f.argmax_sigma_index * 4 + f.argmax_shape_index == flat
+            assert f.argmax_position == pos or abs(ref.ravel()[np.ravel_multi_index(
+                f.argmax_position, dims) + flat * r.size] - val) <= 1e-6 * abs(val)
+
+
+def test_eta_f64_separable_exact(P):
+    dims, kernel, r = cfg4_like(48, seed=3)
+    sg, dg = np.array([1.2, 2.4]), np.array([2.0])
+    hats = O.template_hats(O.psf_hat(kernel), dims, sg, dg)
+    _, _, val, _, fields = O.eta_field(r, 0.5, hats, 1, None, keep_fields=True)
+    psf = P.Psf(P.Volume(kernel), normalize=False)
+    table = P.build_template_table(psf, sg, dg)
+    assert table.info()["n_basis"] == 2
+    f = P.eta_field(P.Volume(r), 0.5, table, keep_fields=True)
+    got = np.stack([v.data for v in f.fields])
+    assert np.max(np.abs(got - np.stack(fields))) <= 1e-10 * abs(val)
+
+
+def test_eta_linearity(P):
+    """eta(a r1 + b r2) = a eta(r1) + b eta(r2)."""
+    dims, kernel, r1 = cfg4_like(40, seed=5)
+    r2 = np.random.default_rng(9).standard_normal(dims)
+    psf = P.Psf(P.Volume(kernel), normalize=False)
+    table = P.build_template_table(psf, [1.5, 2.5], [1.6, 2.0, 2.7])
+    f1 = np.stack([v.data for v in P.eta_field(P.Volume(r1), 1.0, table).fields])
+    f2 = np.stack([v.data for v in P.eta_field(P.Volume(r2), 1.0, table).fields])
+    f3 = np.stack([v.data for v in P.eta_field(P.Volume(2.0 * r1 - 0.5 * r2), 1.0, table).fields])
+    assert np.max(np.abs(f3 - (2.0 * f1 - 0.5 * f2))) <= 1e-10 * np.max(np.abs(f3))
