@@ -147,6 +147,13 @@ int sfw3d_table_create(sfw3d_ctx* ctx, const sfw3d_psf* psf, int n_sigma,
  * (summed over its candidates) — the FLOP counts of the roofline. */
 int sfw3d_table_info(const sfw3d_table* t, int dtype, int* n_cand, int* n_direct, int* n_basis,
                      int64_t* direct_taps, int64_t* basis_taps);
+/* Host-only (no device work): the separable-basis fit the table uses for a
+ * (sigma, d) candidate on the offset box [lo, hi]: g(s) ~ w0 [s == 0] +
+ * sum_k weights[k] exp(-betas[k] s) with non-negative weights; writes up to
+ * max_terms terms, the term count and the max abs error on the lattice. */
+int sfw3d_basis_fit(const int32_t lo[3], const int32_t hi[3], double sigma, double d,
+                    int max_terms, double* betas, double* weights, double* w0, int* n_terms,
+                    double* fit_err);
 /* One candidate (flat sigma-major index): evaluator used for `dtype`, basis
  * term count (incl. the delta term), the basis fit's max absolute error on
  * the lattice of the support box, and both tap counts. */

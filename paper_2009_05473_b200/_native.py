@@ -31,7 +31,7 @@ EXPORTS = (
     "sfw3d_atom_sums", "sfw3d_cost_grad", "sfw3d_table_create", "sfw3d_table_info",
     "sfw3d_table_destroy", "sfw3d_eta_argmax", "sfw3d_dots", "sfw3d_nnlasso_cd",
     "sfw3d_residual", "sfw3d_ctx_profile", "sfw3d_ctx_profile_read", "sfw3d_probe_fp32",
-    "sfw3d_table_candidate",
+    "sfw3d_table_candidate", "sfw3d_basis_fit",
 )
 
 
@@ -73,6 +73,8 @@ _SIGNATURES = {
                                    _i32p, _dp]),
     "sfw3d_residual": (C.c_int, [_vp, C.c_int, C.c_int64, _vp, C.POINTER(_vp), _dp, C.c_int, _vp,
                                  _dp]),
+    "sfw3d_basis_fit": (C.c_int, [_i32p, _i32p, C.c_double, C.c_double, C.c_int, _dp, _dp, _dp,
+                                  _ip, _dp]),
     "sfw3d_ctx_profile": (C.c_int, [_vp, C.c_int]),
     "sfw3d_ctx_profile_read": (C.c_int, [_vp, C.c_char_p, _dp, C.POINTER(C.c_int64)]),
     "sfw3d_probe_fp32": (C.c_int, [_vp, _dp]),
@@ -141,6 +143,21 @@ def atom_geometry(dims, params: np.ndarray):
     check(lib().sfw3d_atom_geometry(dims_arg(dims), f64_ptr(p), k, i32_ptr(radius),
                                     i32_ptr(start), i32_ptr(length), i32_ptr(full)))
     return radius, start, length, full
+
+
+def basis_fit(lo, hi, sigma: float, d: float):
+    """Host-only: (betas, weights, w0, max abs error) of the certificate basis fit."""
+    lo = np.ascontiguousarray(lo, dtype=np.int32)
+    hi = np.ascontiguousarray(hi, dtype=np.int32)
+    betas = np.zeros(64)
+    weights = np.zeros(64)
+    w0, err = C.c_double(), C.c_double()
+    nt = C.c_int()
+    check(lib().sfw3d_basis_fit(i32_ptr(lo), i32_ptr(hi), float(sigma), float(d), 64,
+                                f64_ptr(betas), f64_ptr(weights), C.byref(w0), C.byref(nt),
+                                C.byref(err)))
+    k = min(nt.value, 64)
+    return betas[:k], weights[:k], w0.value, err.value
 
 
 # ------------------------------------------------------------------ devices

@@ -336,70 +336,80 @@ int region_pitch(int lc4, int esize) {
 // ------------------------------------------------------------------ NNLS
 // Lawson-Hanson non-negative least squares min ||A x - g||, x >= 0, with the
 // passive-set subproblems solved by Householder QR. A is column-major M x N.
-void lsq_qr(const std::vector<double>& A, int M, const std::vector<int>& cols,
-            const std::vector<double>& g, std::vector<double>& z) {
+// Extended precision (x86 long double, 64-bit mantissa) keeps the passive-set
+// least-squares solves accurate on the nearly collinear exponential columns.
+using ld = long double;
+
+void lsq_qr(const std::vector<ld>& A, int M, const std::vector<int>& cols, const std::vector<ld>& g,
+            std::vector<ld>& z) {
   const int p = int(cols.size());
-  std::vector<double> B(size_t(M) * p), rhs(g);
-  std::vector<double> scale(p);
+  std::vector<ld> B(size_t(M) * p), rhs(g), scale(p), v(M);
   for (int j = 0; j < p; ++j) {
-    double s = 0.0;
+    ld s = 0.0L;
     for (int i = 0; i < M; ++i) s += A[size_t(cols[j]) * M + i] * A[size_t(cols[j]) * M + i];
-    scale[j] = s > 0 ? 1.0 / std::sqrt(s) : 1.0;
+    scale[j] = s > 0 ? 1.0L / std::sqrt(s) : 1.0L;
     for (int i = 0; i < M; ++i) B[size_t(j) * M + i] = A[size_t(cols[j]) * M + i] * scale[j];
   }
   for (int j = 0; j < p; ++j) {  // Householder on column j, rows j..M-1
-    double* c = &B[size_t(j) * M];
-    double nrm = 0.0;
+    ld* c = &B[size_t(j) * M];
+    ld nrm = 0.0L;
     for (int i = j; i < M; ++i) nrm += c[i] * c[i];
     nrm = std::sqrt(nrm);
-    if (nrm == 0.0) continue;
-    const double alpha = c[j] > 0 ? -nrm : nrm;
-    std::vector<double> v(c + j, c + M);
-    v[0] -= alpha;
-    double vn = 0.0;
-    for (double x : v) vn += x * x;
-    if (vn == 0.0) continue;
-    auto apply = [&](double* col) {
-      double dot = 0.0;
-      for (int i = j; i < M; ++i) dot += v[i - j] * col[i];
-      const double f = 2.0 * dot / vn;
-      for (int i = j; i < M; ++i) col[i] -= f * v[i - j];
+    if (nrm == 0.0L) continue;
+    const ld alpha = c[j] > 0 ? -nrm : nrm;
+    for (int i = j; i < M; ++i) v[i] = c[i];
+    v[j] -= alpha;
+    ld vn = 0.0L;
+    for (int i = j; i < M; ++i) vn += v[i] * v[i];
+    if (vn == 0.0L) continue;
+    auto apply = [&](ld* col) {
+      ld dot = 0.0L;
+      for (int i = j; i < M; ++i) dot += v[i] * col[i];
+      const ld f = 2.0L * dot / vn;
+      for (int i = j; i < M; ++i) col[i] -= f * v[i];
     };
     for (int k = j; k < p; ++k) apply(&B[size_t(k) * M]);
     apply(rhs.data());
   }
-  z.assign(p, 0.0);
+  z.assign(p, 0.0L);
   for (int j = p - 1; j >= 0; --j) {
-    double s = rhs[j];
+    ld s = rhs[j];
     for (int k = j + 1; k < p; ++k) s -= B[size_t(k) * M + j] * z[k];
-    const double r = B[size_t(j) * M + j];
-    z[j] = r != 0.0 ? s / r : 0.0;
+    const ld r = B[size_t(j) * M + j];
+    z[j] = r != 0.0L ? s / r : 0.0L;
   }
   for (int j = 0; j < p; ++j) z[j] *= scale[j];
 }
 
-void nnls(const std::vector<double>& A, int M, int N, const std::vector<double>& g,
-          std::vector<double>& x) {
-  x.assign(N, 0.0);
-  std::vector<char> passive(N, 0);
-  std::vector<double> r(g), wgrad(N);
-  double gnorm = 0.0;
-  for (double v : g) gnorm = std::max(gnorm, std::fabs(v));
-  const double tol = 1e-15 * std::max(1.0, gnorm) * M;
-  for (int outer = 0; outer < 3 * N; ++outer) {
+// Lawson-Hanson: add the column with the largest (scaled) gradient, solve the
+// passive least-squares problem, step back to feasibility when needed.
+void nnls(const std::vector<double>& Ad, int M, int N, const std::vector<double>& gd,
+          std::vector<double>& xd) {
+  std::vector<ld> A(Ad.begin(), Ad.end()), g(gd.begin(), gd.end()), x(N, 0.0L), r(M);
+  std::vector<char> passive(N, 0), banned(N, 0);
+  std::vector<ld> cn(N);
+  for (int j = 0; j < N; ++j) {
+    ld s = 0.0L;
+    for (int i = 0; i < M; ++i) s += A[size_t(j) * M + i] * A[size_t(j) * M + i];
+    cn[j] = s > 0.0L ? std::sqrt(s) : 1.0L;
+  }
+  ld gn = 0.0L;
+  for (ld v : g) gn += v * v;
+  const ld tol = 1e-17L * std::sqrt(gn);
+  for (int outer = 0; outer < 8 * N; ++outer) {
     for (int i = 0; i < M; ++i) {
-      double s = g[i];
+      ld s = g[i];
       for (int j = 0; j < N; ++j)
-        if (x[j] != 0.0) s -= A[size_t(j) * M + i] * x[j];
+        if (x[j] != 0.0L) s -= A[size_t(j) * M + i] * x[j];
       r[i] = s;
     }
     int jmax = -1;
-    double best = tol;
+    ld best = tol;
     for (int j = 0; j < N; ++j) {
-      if (passive[j]) continue;
-      double s = 0.0;
+      if (passive[j] || banned[j]) continue;
+      ld s = 0.0L;
       for (int i = 0; i < M; ++i) s += A[size_t(j) * M + i] * r[i];
-      wgrad[j] = s;
+      s /= cn[j];
       if (s > best) {
         best = s;
         jmax = j;
@@ -407,36 +417,54 @@ void nnls(const std::vector<double>& A, int M, int N, const std::vector<double>&
     }
     if (jmax < 0) break;
     passive[jmax] = 1;
+    bool first = true, added = true;
     for (int inner = 0; inner < 3 * N; ++inner) {
       std::vector<int> cols;
       for (int j = 0; j < N; ++j)
         if (passive[j]) cols.push_back(j);
-      std::vector<double> z;
+      std::vector<ld> z;
       lsq_qr(A, M, cols, g, z);
       bool ok = true;
-      for (double v : z) ok &= v > 0.0;
+      for (ld v : z) ok &= v > 0.0L;
       if (ok) {
-        std::fill(x.begin(), x.end(), 0.0);
+        std::fill(x.begin(), x.end(), 0.0L);
         for (size_t q = 0; q < cols.size(); ++q) x[cols[q]] = z[q];
         break;
       }
-      double alpha = 1.0;
+      if (first) {  // the entering column itself came out non-positive: skip it
+        size_t qn = 0;
+        while (cols[qn] != jmax) ++qn;
+        if (z[qn] <= 0.0L) {
+          passive[jmax] = 0;
+          banned[jmax] = 1;
+          added = false;
+          break;
+        }
+      }
+      first = false;
+      ld alpha = 2.0L;
+      int qmin = -1;
       for (size_t q = 0; q < cols.size(); ++q)
-        if (z[q] <= 0.0) {
-          const double xv = x[cols[q]];
-          const double a = xv / (xv - z[q]);
-          if (a < alpha) alpha = a;
+        if (z[q] <= 0.0L) {
+          const ld xv = x[cols[q]];
+          const ld a = xv / (xv - z[q]);
+          if (a < alpha) {
+            alpha = a;
+            qmin = int(q);
+          }
         }
       for (size_t q = 0; q < cols.size(); ++q) {
         const int j = cols[q];
         x[j] += alpha * (z[q] - x[j]);
-        if (x[j] <= 1e-300) {
-          x[j] = 0.0;
+        if (int(q) == qmin || x[j] <= 0.0L) {
+          x[j] = 0.0L;
           passive[j] = 0;
         }
       }
     }
+    if (added) std::fill(banned.begin(), banned.end(), 0);
   }
+  xd.assign(x.begin(), x.end());
 }
 
 }  // namespace
@@ -448,58 +476,90 @@ static int upload(void** dst, const void* src, size_t bytes) {
   return SFW3D_OK;
 }
 
-static int fit_basis(CandHost& c) {
-  const double inv2sd = 0.5 / std::pow(c.sigma, c.d);
-  const int l[3] = {c.hi[0] - c.lo[0] + 1, c.hi[1] - c.lo[1] + 1, c.hi[2] - c.lo[2] + 1};
-  if (c.d == 2.0) {  // exp(-inv2sd * (a^2 + b^2 + c^2)) = product of three 1-D Gaussians
-    c.exact_sep = true;
-    c.fit_err = 0.0;
-    c.w0 = 0.0;
-    c.terms.push_back({inv2sd, 1.0});
-  } else {
-    // lattice values s = a^2 + b^2 + c^2 present in the box
-    int smax = 0;
-    for (int a = 0; a < 3; ++a) smax += std::max(c.lo[a] * c.lo[a], c.hi[a] * c.hi[a]);
-    std::vector<char> present(size_t(smax) + 1, 0);
-    std::vector<char> sq[3];
-    for (int ax = 0; ax < 3; ++ax) sq[ax].assign(size_t(smax) + 1, 0);
-    for (int ax = 0; ax < 3; ++ax)
-      for (int t = c.lo[ax]; t <= c.hi[ax]; ++t) sq[ax][size_t(t) * t] = 1;
-    std::vector<int> sv[3];
-    for (int ax = 0; ax < 3; ++ax)
-      for (int s = 0; s <= smax; ++s)
-        if (sq[ax][s]) sv[ax].push_back(s);
-    for (int s0 : sv[0])
-      for (int s1 : sv[1])
-        for (int s2 : sv[2]) present[size_t(s0) + s1 + s2] = 1;
-    std::vector<double> S;
+// Fits g(s) = exp(-s^(d/2) / (2 sigma^d)) on the lattice values s = a^2 + b^2
+// + c^2 of the offset box [lo, hi] by w0 * [s == 0] + sum_k w_k exp(-beta_k s)
+// (non-negative weights, 48 geometric beta_k). Host-only.
+static void fit_profile(const int lo[3], const int hi[3], double sigma, double d, double& w0,
+                        std::vector<std::pair<double, double>>& terms, double& err, bool& exact) {
+  const double inv2sd = 0.5 / std::pow(sigma, d);
+  terms.clear();
+  if (d == 2.0) {  // exp(-inv2sd * (a^2 + b^2 + c^2)) = product of three 1-D Gaussians
+    exact = true;
+    err = 0.0;
+    w0 = 0.0;
+    terms.push_back({inv2sd, 1.0});
+    return;
+  }
+  exact = false;
+  int smax = 0;
+  for (int a = 0; a < 3; ++a) smax += std::max(lo[a] * lo[a], hi[a] * hi[a]);
+  std::vector<char> present(size_t(smax) + 1, 0);
+  std::vector<int> sv[3];
+  for (int ax = 0; ax < 3; ++ax) {
+    std::vector<char> sq(size_t(smax) + 1, 0);
+    for (int t = lo[ax]; t <= hi[ax]; ++t) sq[size_t(t) * t] = 1;
     for (int s = 0; s <= smax; ++s)
-      if (present[s]) S.push_back(double(s));
-    const int M = int(S.size());
-    const int K = 48;
-    const double rmax = std::max({-c.lo[0], c.hi[0], -c.lo[1], c.hi[1], -c.lo[2], c.hi[2], 1});
-    const double bmin = 0.5 / (rmax * rmax), bmax = 30.0;
+      if (sq[s]) sv[ax].push_back(s);
+  }
+  for (int s0 : sv[0])
+    for (int s1 : sv[1])
+      for (int s2 : sv[2]) present[size_t(s0) + s1 + s2] = 1;
+  std::vector<double> S;
+  for (int s = 0; s <= smax; ++s)
+    if (present[s]) S.push_back(double(s));
+  const int Mfull = int(S.size());
+  // fit on all s <= 256 plus a geometric subsample of the rest (the profile
+  // is smooth there); the error is then measured on every lattice value
+  std::vector<double> Sfit;
+  {
+    double next = 256.0;
+    for (double s : S) {
+      if (s <= 256.0 || s >= next) {
+        Sfit.push_back(s);
+        if (s > 256.0) next = s * 1.004;
+      }
+    }
+  }
+  const int M = int(Sfit.size());
+  const double rmax = std::max({-lo[0], hi[0], -lo[1], hi[1], -lo[2], hi[2], 1});
+  const double bmin = 0.5 / (rmax * rmax), bmax = 30.0;
+  std::vector<double> gfull(Mfull);
+  for (int i = 0; i < Mfull; ++i) gfull[i] = std::exp(-inv2sd * std::pow(S[i], 0.5 * d));
+  err = INFINITY;
+  for (const int K : {48, 96}) {  // denser dictionary only when the first misses 1e-10
     std::vector<double> betas(K), A(size_t(M) * (K + 1)), g(M);
     for (int k = 0; k < K; ++k) betas[k] = bmin * std::pow(bmax / bmin, double(k) / (K - 1));
     for (int i = 0; i < M; ++i) {
-      const double s = S[i];
-      g[i] = std::exp(-inv2sd * std::pow(s, 0.5 * c.d));
+      const double s = Sfit[i];
+      g[i] = std::exp(-inv2sd * std::pow(s, 0.5 * d));
       for (int k = 0; k < K; ++k) A[size_t(k) * M + i] = std::exp(-betas[k] * s);
       A[size_t(K) * M + i] = s == 0.0 ? 1.0 : 0.0;  // delta term
     }
     std::vector<double> x;
     nnls(A, M, K + 1, g, x);
-    double err = 0.0;
-    for (int i = 0; i < M; ++i) {
-      double v = 0.0;
-      for (int k = 0; k <= K; ++k) v += A[size_t(k) * M + i] * x[k];
-      err = std::max(err, std::fabs(v - g[i]));
+    double e = 0.0;
+    for (int i = 0; i < Mfull; ++i) {
+      double v = S[i] == 0.0 ? x[K] : 0.0;
+      for (int k = 0; k < K; ++k)
+        if (x[k] > 0.0) v += std::exp(-betas[k] * S[i]) * x[k];
+      e = std::max(e, std::fabs(v - gfull[i]));
     }
-    c.fit_err = err;
-    c.w0 = x[K];
-    for (int k = 0; k < K; ++k)
-      if (x[k] > 0.0) c.terms.push_back({betas[k], x[k]});
+    if (e < err) {
+      err = e;
+      w0 = x[K];
+      terms.clear();
+      for (int k = 0; k < K; ++k)
+        if (x[k] > 0.0) terms.push_back({betas[k], x[k]});
+    }
+    if (err <= 1e-10) break;
   }
+}
+
+static int fit_basis(CandHost& c) {
+  const int l[3] = {c.hi[0] - c.lo[0] + 1, c.hi[1] - c.lo[1] + 1, c.hi[2] - c.lo[2] + 1};
+  std::vector<std::pair<double, double>> bw;
+  fit_profile(c.lo, c.hi, c.sigma, c.d, c.w0, bw, c.fit_err, c.exact_sep);
+  for (auto& p : bw) c.terms.push_back({p.first, p.second});
   c.basis_taps = (c.w0 != 0.0 ? 1 : 0);
   for (auto& t : c.terms) {
     std::vector<double> h64;
@@ -579,6 +639,28 @@ static bool use_basis(const sfw3d_table* t, const CandHost& c, int dtype) {
 }  // namespace sfw3d
 
 using namespace sfw3d;
+
+extern "C" int sfw3d_basis_fit(const int32_t lo[3], const int32_t hi[3], double sigma, double d,
+                               int max_terms, double* betas, double* weights, double* w0,
+                               int* n_terms, double* fit_err) {
+  SFW3D_CHECK_ARG(lo && hi && w0 && n_terms && fit_err, "NULL argument");
+  SFW3D_CHECK_ARG(sigma > 0.0 && d > 0.0, "sigma and d must be positive");
+  int l[3], h[3];
+  for (int a = 0; a < 3; ++a) {
+    SFW3D_CHECK_ARG(lo[a] <= 0 && hi[a] >= 0, "box must contain the origin");
+    l[a] = lo[a];
+    h[a] = hi[a];
+  }
+  std::vector<std::pair<double, double>> bw;
+  bool exact = false;
+  fit_profile(l, h, sigma, d, *w0, bw, *fit_err, exact);
+  *n_terms = int(bw.size());
+  for (int k = 0; k < int(bw.size()) && k < max_terms; ++k) {
+    if (betas) betas[k] = bw[k].first;
+    if (weights) weights[k] = bw[k].second;
+  }
+  return SFW3D_OK;
+}
 
 extern "C" int sfw3d_table_destroy(sfw3d_table* t) {
   if (!t) return SFW3D_OK;
