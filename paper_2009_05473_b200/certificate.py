@@ -19,7 +19,7 @@ from scipy.optimize import minimize
 
 from . import _native as N
 from .forward import Psf, atom_sums_dev, psf_apply_dev, to_dev
-from .measures import AtomParams, DomainBounds, clamp_to_domain
+from .measures import AtomParams, DomainBounds, bounds_box, clamp_to_domain
 from .volumes import Volume
 
 MODES = {"auto": 0, "direct": 1}
@@ -253,7 +253,7 @@ def refine_eta_max_dev(residual, lam: float, psf: Psf, start: AtomParams, bounds
             raise FloatingPointError(f"non-finite certificate value near {vec}")
         return -val, -grad
 
-    box = bounds.as_box()
+    box = bounds_box(bounds)
     start_val = -neg_eta(start.to_array())[0]
     res = minimize(neg_eta, start.to_array(), jac=True, method="L-BFGS-B", bounds=box,
                    options={"maxiter": max_iter, "gtol": gtol})

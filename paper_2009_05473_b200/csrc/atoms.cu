@@ -23,9 +23,16 @@ constexpr int kBX = 4, kBY = 8, kBZ = 16;  // render brick (512 voxels)
 constexpr int kChunk = 4096;               // atom-sum chunk (voxels)
 constexpr int kSumThreads = 256;
 
-__device__ __forceinline__ int pmod(long long a, int n) {
-  long long r = a % n;
-  return int(r < 0 ? r + n : r);
+// a mod n in [0, n) without a 64-bit division on the common path (|a| < 2n)
+__device__ __forceinline__ int pmod(int a, int n) {
+  if (a < 0) {
+    a += n;
+    if (a < 0) a = (a % n + n) % n;
+  } else if (a >= n) {
+    a -= n;
+    if (a >= n) a %= n;
+  }
+  return a;
 }
 
 // Minimum-image offset of voxel i from centre m on a full axis
@@ -45,7 +52,7 @@ __device__ __forceinline__ bool axis_offset(const AtomGeo& a, int axis, int g, i
     off = min_image(g, a.m[axis], n);
     return true;
   }
-  int il = pmod((long long)g - a.start[axis], n);
+  int il = pmod(g - a.start[axis], n);
   if (il >= a.len[axis]) return false;
   off = __dsub_rn(double(a.start[axis] + il), a.m[axis]);
   return true;
@@ -156,15 +163,16 @@ __global__ void __launch_bounds__(kSumThreads) atom_sums_kernel(
   const Chunk ch = chunks[blockIdx.x];
   const AtomGeo& a = atoms[ch.atom];
   const int dims[3] = {nx, ny, nz};
-  const long long vend = min((long long)ch.first + kChunk, a.nvox);
+  const int vend = int(min((long long)ch.first + kChunk, a.nvox));
+  const int l2 = a.len[2], l1 = a.len[1];
 
   double s[6] = {0, 0, 0, 0, 0, 0};
   float sf[6] = {0, 0, 0, 0, 0, 0};
-  for (long long v = ch.first + threadIdx.x; v < vend; v += kSumThreads) {
-    const int ic = int(v % a.len[2]);
-    const long long rest = v / a.len[2];
-    const int ib = int(rest % a.len[1]);
-    const int ia = int(rest / a.len[1]);
+  for (int v = ch.first + threadIdx.x; v < vend; v += kSumThreads) {
+    const int rest = v / l2;  // 32-bit index math (boxes hold < 2^31 voxels)
+    const int ic = v - rest * l2;
+    const int ia = rest / l1;
+    const int ib = rest - ia * l1;
     int g[3];
     double off[3];
     const int il[3] = {ia, ib, ic};

@@ -40,7 +40,8 @@ namespace sfw3d {
 
 struct Term {
   double beta, w;
-  void* taps64 = nullptr;  // 3 axes x [lo..hi] doubles, contiguous per axis
+  int tlo[3], tlen[3];     // per-axis tap range (the box clipped where f_k < eps)
+  void* taps64 = nullptr;  // 3 axes, contiguous per axis, tlen[a] each
   void* taps32 = nullptr;
 };
 
@@ -559,16 +560,35 @@ static int fit_basis(CandHost& c) {
   const int l[3] = {c.hi[0] - c.lo[0] + 1, c.hi[1] - c.lo[1] + 1, c.hi[2] - c.lo[2] + 1};
   std::vector<std::pair<double, double>> bw;
   fit_profile(c.lo, c.hi, c.sigma, c.d, c.w0, bw, c.fit_err, c.exact_sep);
-  for (auto& p : bw) c.terms.push_back({p.first, p.second});
+  (void)l;
+  double wsum = 0.0;
+  for (auto& p : bw) wsum += p.second;
+  // A term's 1-D factor exp(-beta t^2) is dropped where it is below
+  // eps = 1e-12 / max(1, sum w): every dropped product is then < w_k * eps,
+  // so the truncation adds at most 1e-12 to the recorded fit error.
+  const double eps = 1e-12 / std::max(1.0, wsum);
+  for (auto& p : bw) {
+    Term t{};
+    t.beta = p.first;
+    t.w = p.second;
+    const int r = c.exact_sep ? (1 << 29) : int(std::ceil(std::sqrt(std::log(1.0 / eps) / t.beta)));
+    for (int ax = 0; ax < 3; ++ax) {
+      t.tlo[ax] = std::max(c.lo[ax], -r);
+      t.tlen[ax] = std::min(c.hi[ax], r) - t.tlo[ax] + 1;
+    }
+    c.terms.push_back(t);
+  }
+  if (!c.exact_sep) c.fit_err += 1e-12;
   c.basis_taps = (c.w0 != 0.0 ? 1 : 0);
   for (auto& t : c.terms) {
     std::vector<double> h64;
     for (int ax = 0; ax < 3; ++ax)
-      for (int q = c.lo[ax]; q <= c.hi[ax]; ++q) h64.push_back(std::exp(-t.beta * double(q) * q));
+      for (int q = t.tlo[ax]; q < t.tlo[ax] + t.tlen[ax]; ++q)
+        h64.push_back(std::exp(-t.beta * double(q) * q));
     std::vector<float> h32(h64.begin(), h64.end());
     SFW3D_TRY(upload(&t.taps64, h64.data(), h64.size() * sizeof(double)));
     SFW3D_TRY(upload(&t.taps32, h32.data(), h32.size() * sizeof(float)));
-    c.basis_taps += l[0] + l[1] + l[2];
+    c.basis_taps += t.tlen[0] + t.tlen[1] + t.tlen[2];
   }
   return SFW3D_OK;
 }
@@ -833,19 +853,19 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
     long long nred = 0;
     if (use_basis(t, c, dtype)) {
       // acc = w0 * b + sum_k w_k (f_k x f_k x f_k) * b   (separable passes)
-      const int l[3] = {c.hi[0] - c.lo[0] + 1, c.hi[1] - c.lo[1] + 1, c.hi[2] - c.lo[2] + 1};
       for (size_t k = 0; k < c.terms.size(); ++k) {
         const Term& term = c.terms[k];
         const T* taps = static_cast<const T*>(dtype == SFW3D_F64 ? term.taps64 : term.taps32);
-        SFW3D_TRY(corr_pass_impl(ctx, dtype, b, tmp, dims, 2, taps + l[0] + l[1], c.lo[2], l[2],
+        const int* tl = term.tlen;
+        SFW3D_TRY(corr_pass_impl(ctx, dtype, b, tmp, dims, 2, taps + tl[0] + tl[1], term.tlo[2],
+                                 tl[2], nullptr, 0.0, 1.0, "eta_basis"));
+        SFW3D_TRY(corr_pass_impl(ctx, dtype, tmp, t2, dims, 1, taps + tl[0], term.tlo[1], tl[1],
                                  nullptr, 0.0, 1.0, "eta_basis"));
-        SFW3D_TRY(corr_pass_impl(ctx, dtype, tmp, t2, dims, 1, taps + l[0], c.lo[1], l[1], nullptr,
-                                 0.0, 1.0, "eta_basis"));
         const void* addend = k == 0 ? (c.w0 != 0.0 ? static_cast<const void*>(b) : nullptr)
                                     : static_cast<const void*>(acc);
         const double aw = k == 0 ? c.w0 : 1.0;
-        SFW3D_TRY(corr_pass_impl(ctx, dtype, t2, acc, dims, 0, taps, c.lo[0], l[0], addend, aw,
-                                 term.w, "eta_basis"));
+        SFW3D_TRY(corr_pass_impl(ctx, dtype, t2, acc, dims, 0, taps, term.tlo[0], tl[0], addend,
+                                 aw, term.w, "eta_basis"));
       }
       SFW3D_PROF(ctx, "argmax");
       volume_argmax_kernel<T><<<nblocks_vol, 256, 0, ctx->stream>>>(

@@ -22,9 +22,16 @@ namespace {
 
 __device__ __forceinline__ int wrap_inc(int i, int n) { return (i + 1 == n) ? 0 : i + 1; }
 
-__device__ __forceinline__ int pmod_i(long long a, int n) {
-  long long r = a % n;
-  return int(r < 0 ? r + n : r);
+// a mod n in [0, n) without a division on the common path (|a| < 2n)
+__device__ __forceinline__ int pmod_i(int a, int n) {
+  if (a < 0) {
+    a += n;
+    if (a < 0) a = (a % n + n) % n;
+  } else if (a >= n) {
+    a -= n;
+    if (a >= n) a %= n;
+  }
+  return a;
 }
 
 template <typename T, int J>
@@ -35,12 +42,14 @@ __global__ void __launch_bounds__(256) pass_strided_kernel(
   T* taps = reinterpret_cast<T*>(smem_raw);
   for (int q = threadIdx.x; q < ntaps; q += blockDim.x) taps[q] = taps_g[q];
   __syncthreads();
-  const long long inner = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  // blockIdx.x runs over the a-blocks so CTAs that share input planes are
+  // resident together (L2 reuse of the (J + taps - 1)/J overlap)
+  const long long inner = blockIdx.y * (long long)blockDim.x + threadIdx.x;
   if (inner >= stride) return;
-  const int a0 = blockIdx.y * J;
+  const int a0 = blockIdx.x * J;
   const long long base = (long long)blockIdx.z * n_axis * stride + inner;
   T W[J], acc[J];
-  int idx = pmod_i((long long)a0 + lo, n_axis);
+  int idx = pmod_i(a0 + lo, n_axis);
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     W[j] = in[base + idx * stride];
@@ -83,12 +92,14 @@ __global__ void __launch_bounds__(32 * kZWarps) pass_z_kernel(
   const int z0 = blockIdx.x * (J * kZWarps);
   const int width = J * kZWarps + ntaps - 1 + J;  // staged columns
   for (int q = threadIdx.x; q < ntaps; q += blockDim.x) taps[q] = taps_g[q];
-  for (int e = threadIdx.x; e < kZRows * width; e += blockDim.x) {
-    const int r = e / width, c = e % width;
-    const long long row = row0 + r;
-    T v = T(0);
-    if (row < nrows) v = in[row * nz + pmod_i((long long)z0 + lo + c, nz)];
-    tile[r * pitch + c] = v;
+  // rows of the tile are read by consecutive threads along z (coalesced);
+  // the wrapped column index is computed once per column, not per element
+  for (int c = threadIdx.x; c < width; c += blockDim.x) {
+    const int zc = pmod_i(z0 + lo + c, nz);
+    for (int r = 0; r < kZRows; ++r) {
+      const long long row = row0 + r;
+      tile[r * pitch + c] = row < nrows ? in[row * nz + zc] : T(0);
+    }
   }
   __syncthreads();
   const T* src = tile + lane * pitch + warp * J;
@@ -161,7 +172,7 @@ int launch_strided(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int a
   long long outer = 1;
   for (int a = 0; a < axis; ++a) outer *= dims[a];
   const int n = dims[axis];
-  dim3 grid(unsigned((stride + 255) / 256), unsigned((n + J - 1) / J), unsigned(outer));
+  dim3 grid(unsigned((n + J - 1) / J), unsigned((stride + 255) / 256), unsigned(outer));
   pass_strided_kernel<T, J><<<grid, 256, size_t(ntaps) * sizeof(T), ctx->stream>>>(
       in, out, n, stride, taps, lo, ntaps, addend, T(aw), T(w));
   SFW3D_LAUNCH_CHECK(ctx);
