@@ -125,7 +125,8 @@ int sfw3d_atom_sums(sfw3d_ctx* ctx, int dtype, const int dims[3], const void* fi
  *   model = H * sum_i w_i G_i ; C = 1/2 ||model - y||^2 + lam * sum_i w_i ;
  *   back = H^T * (model - y) ; grad row i = [<G_i,back> + lam, w_i <dG_i,back>].
  * grad_host may be NULL (criterion only, forward.py:182-190). back_dev, if
- * not NULL, receives the back-projection (a `dtype` volume). */
+ * not NULL, receives the back-projection (a `dtype` volume) — also when
+ * grad_host is NULL (the sharded gradient splits the atom sums over ranks). */
 int sfw3d_cost_grad(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* y_dev,
                     const double* params_host, int k, double lam, double* cost_host,
                     double* grad_host, void* back_dev);

@@ -442,10 +442,10 @@ extern "C" int sfw3d_cost_grad(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, 
   SFW3D_TRY(psf_apply_impl(ctx, psf, dtype, A, B, 0, A));
   // resid = model - y -> A ; ||resid||^2
   SFW3D_TRY(sumsq_diff_impl(ctx, dtype, n, B, y_dev, A, partials, res));
-  if (grad_host) {
+  if (grad_host || back_dev) {
     void* back = back_dev ? back_dev : B;
     SFW3D_TRY(psf_apply_impl(ctx, psf, dtype, A, back, 1, back == B ? A : B));
-    SFW3D_TRY(atom_sums_impl(ctx, dtype, dims, back, atoms, ad, res + 1, scr, scratch));
+    if (grad_host) SFW3D_TRY(atom_sums_impl(ctx, dtype, dims, back, atoms, ad, res + 1, scr, scratch));
   }
   std::vector<double> host(size_t(k) * 6 + 1);
   SFW3D_TRY(download_sync(ctx, host.data(), res, (grad_host ? host.size() : 1) * sizeof(double)));

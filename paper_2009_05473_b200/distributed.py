@@ -1,0 +1,192 @@
+"""Multi-GPU sharding of the hot path: one process per GPU.
+
+Plumbing is torch.distributed (NCCL on the B200 box; gloo in the CPU tests).
+What shards and which exchanges exist:
+
+* certificate — the output grid is split into x-slabs (axis 0, the slowest
+  axis). With a replicated residual every rank evaluates eta on its slab
+  only (a window restriction, no halo needed) and the single collective is an
+  all-gather of one 24-byte argmax record per rank, reduced with the
+  reference's order (larger eta, then smaller sigma-major candidate, then
+  smaller C-order position: certificate.py:161-172). With a slab-distributed
+  residual the ranks first exchange periodic halos of the template radius.
+* cost + gradient — atoms are split across ranks for the per-atom box
+  reductions (K6, the dominant kernel at config 5) and the rows are
+  all-gathered; the criterion value is computed once per rank (replicated
+  volumes). Slab-local rendering is listed as next work in DESIGN.md.
+* sums (Gram rows, ||r||^2) — fp64 all-reduce.
+
+The functions take a `compute` callable where the per-rank work happens so
+the same exchange logic runs with the CUDA kernels on the GPU and with the
+CPU oracle in the gloo tests.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def _dist():
+    import torch.distributed as dist
+    return dist
+
+
+def world():
+    dist = _dist()
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(), dist.get_world_size()
+    return 0, 1
+
+
+def slab_bounds(n: int, size: int, rank: int) -> tuple[int, int]:
+    """Inclusive [x0, x1] of rank's x-slab; sizes differ by at most one plane."""
+    if not 0 <= rank < size or n < size:
+        raise ValueError("need 0 <= rank < size <= n")
+    base, extra = divmod(n, size)
+    x0 = rank * base + min(rank, extra)
+    return x0, x0 + base + (1 if rank < extra else 0) - 1
+
+
+def better(a, b) -> bool:
+    """Total order of argmax records (value, cand, lin): eta desc, cand asc, lin asc."""
+    if a[0] != b[0]:
+        return a[0] > b[0]
+    if a[1] != b[1]:
+        return a[1] < b[1]
+    return a[2] < b[2]
+
+
+def combine_best(records):
+    best = None
+    for r in records:
+        if r[0] != r[0]:  # NaN never wins
+            continue
+        if best is None or better(r, best):
+            best = r
+    return best
+
+
+def allgather_best(record, group=None, device=None):
+    """All-gather (value, cand, lin) records and return the global winner."""
+    import torch
+    dist = _dist()
+    size = dist.get_world_size(group)
+    t = torch.tensor([float(record[0]), float(record[1]), float(record[2])], dtype=torch.float64,
+                     device=device)
+    out = [torch.empty_like(t) for _ in range(size)]
+    dist.all_gather(out, t, group=group)
+    recs = [(float(o[0]), int(o[1]), int(o[2])) for o in (x.cpu() for x in out)]
+    return combine_best(recs)
+
+
+def allreduce_f64(values, group=None, device=None) -> np.ndarray:
+    """Sum of float64 arrays over ranks (rank order does not matter for the
+    tests' tolerance; NCCL's ring order is fixed for a fixed world size)."""
+    import torch
+    dist = _dist()
+    t = torch.as_tensor(np.ascontiguousarray(values, dtype=np.float64), device=device).clone()
+    dist.all_reduce(t, group=group)
+    return t.cpu().numpy()
+
+
+def halo_exchange(slab, halo: int, group=None):
+    """Fill the periodic halos of an x-slab in place.
+
+    `slab` has shape (n_local + 2*halo, ...): planes [halo, halo + n_local)
+    are owned. Planes [0, halo) receive the left neighbour's last `halo`
+    owned planes and [halo + n_local, end) the right neighbour's first ones
+    (ring: rank 0's left neighbour is the last rank). Requires n_local >= halo.
+    """
+    import torch
+    dist = _dist()
+    rank, size = dist.get_rank(group), dist.get_world_size(group)
+    if halo == 0:
+        return slab
+    n_local = slab.shape[0] - 2 * halo
+    if n_local < halo:
+        raise ValueError("slab thinner than its halo")
+    if size == 1:
+        slab[:halo] = slab[n_local:n_local + halo]
+        slab[halo + n_local:] = slab[halo:2 * halo]
+        return slab
+    left, right = (rank - 1) % size, (rank + 1) % size
+    send_r = slab[n_local:n_local + halo].contiguous()   # my last owned -> right's low halo
+    send_l = slab[halo:2 * halo].contiguous()             # my first owned -> left's high halo
+    recv_l = torch.empty_like(send_r)
+    recv_r = torch.empty_like(send_l)
+    ops = [dist.P2POp(dist.isend, send_r, right, group), dist.P2POp(dist.irecv, recv_l, left, group),
+           dist.P2POp(dist.isend, send_l, left, group), dist.P2POp(dist.irecv, recv_r, right, group)]
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+    slab[:halo] = recv_l
+    slab[halo + n_local:] = recv_r
+    return slab
+
+
+def sharded_argmax(compute, n: int, window, group=None, device=None):
+    """Certificate over x-slabs: `compute(window_slab) -> (value, cand, lin)`
+    for this rank's part of `window` (x range intersected with its slab);
+    returns the global winner. Ranks whose slab misses the window contribute
+    (-inf, big, big)."""
+    dist = _dist()
+    rank, size = dist.get_rank(group), dist.get_world_size(group)
+    x0, x1 = slab_bounds(n, size, rank)
+    (wx0, wx1), wy, wz = window
+    lo, hi = max(x0, wx0), min(x1, wx1)
+    if lo <= hi:
+        rec = compute(((lo, hi), wy, wz))
+    else:
+        rec = (float("-inf"), 2 ** 31, 2 ** 62)
+    return allgather_best(rec, group, device)
+
+
+def sharded_rows(compute_rows, k: int, group=None, device=None) -> np.ndarray:
+    """Per-atom rows split over ranks: `compute_rows(i0, i1) -> (i1 - i0, 6)`;
+    the full (k, 6) matrix is assembled with an fp64 all-reduce (each rank
+    fills only its own atoms)."""
+    dist = _dist()
+    rank, size = dist.get_rank(group), dist.get_world_size(group)
+    base, extra = divmod(k, size)
+    i0 = rank * base + min(rank, extra)
+    i1 = i0 + base + (1 if rank < extra else 0)
+    full = np.zeros((k, 6))
+    if i1 > i0:
+        full[i0:i1] = compute_rows(i0, i1)
+    return allreduce_f64(full, group, device).reshape(k, 6)
+
+
+# ------------------------------------------------------------- GPU helpers
+def eta_field_sharded(residual, lam, table, bounds=None, group=None):
+    """GPU certificate on this rank's x-slab of the window (replicated residual);
+    returns the global (eta_max, candidate, (i, j, k))."""
+    from .certificate import _position_window, eta_argmax_dev
+    dims = table.dims
+
+    def compute(win):
+        best, _, _ = eta_argmax_dev(residual, lam, table, win)
+        lin = (best.pos[0] * dims[1] + best.pos[1]) * dims[2] + best.pos[2]
+        return (best.value, int(best.cand), int(lin))
+
+    v, c, lin = sharded_argmax(compute, dims[0], _position_window(bounds, dims), group,
+                               residual.device)
+    pos = (lin // (dims[1] * dims[2]), (lin // dims[2]) % dims[1], lin % dims[2])
+    return v, c, pos
+
+
+def cost_grad_sharded(psf, y, rows, lam, group=None):
+    """GPU criterion + gradient with the per-atom reductions split over ranks."""
+    from .forward import atom_sums_dev, cost_grad_dev
+    import torch
+    rows = np.ascontiguousarray(rows, dtype=np.float64).reshape(-1, 6)
+    back = torch.empty_like(y)
+    # C and the back-projection H^T (model - y) once per rank (replicated)
+    c, _ = cost_grad_dev(psf, y, rows, lam, want_grad=False, back=back)
+
+    def compute_rows(i0, i1):
+        s = atom_sums_dev(back, rows[i0:i1])
+        out = np.empty_like(s)
+        out[:, 0] = s[:, 0] + lam
+        out[:, 1:] = rows[i0:i1, :1] * s[:, 1:]
+        return out
+
+    return c, sharded_rows(compute_rows, rows.shape[0], group, y.device)
