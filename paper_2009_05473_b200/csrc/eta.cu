@@ -142,20 +142,27 @@ __device__ __forceinline__ void ldg4(const T* p, T& a, T& b, T& c, T& d) {
 
 // One 4-tap step with compile-time window rotation R (0..4): the window
 // value at relative column u lives in buf[(4R + u) % 20].
+// `tc` holds this step's 4 taps; the next step's taps are fetched from
+// `tnext` before the FFMAs so the L1 latency is hidden behind them.
 template <typename T, int R>
-__device__ __forceinline__ void tap_step(T (&acc)[kJ], T (&buf)[20], const T* trow, const T* srow) {
-  T t0, t1, t2, t3;
-  ldg4(trow, t0, t1, t2, t3);
+__device__ __forceinline__ void tap_step(T (&acc)[kJ], T (&buf)[20], T (&tc)[4], const T* tnext,
+                                         const T* srow) {
+  T n0, n1, n2, n3;
+  ldg4(tnext, n0, n1, n2, n3);
 #pragma unroll
   for (int j = 0; j < kJ; ++j) {
-    acc[j] = fma(t0, buf[(4 * R + j + 0) % 20], acc[j]);
-    acc[j] = fma(t1, buf[(4 * R + j + 1) % 20], acc[j]);
-    acc[j] = fma(t2, buf[(4 * R + j + 2) % 20], acc[j]);
-    acc[j] = fma(t3, buf[(4 * R + j + 3) % 20], acc[j]);
+    acc[j] = fma(tc[0], buf[(4 * R + j + 0) % 20], acc[j]);
+    acc[j] = fma(tc[1], buf[(4 * R + j + 1) % 20], acc[j]);
+    acc[j] = fma(tc[2], buf[(4 * R + j + 2) % 20], acc[j]);
+    acc[j] = fma(tc[3], buf[(4 * R + j + 3) % 20], acc[j]);
   }
   // slots of columns 0..3 are free now: load columns 20..23
   ld4(srow + 20, buf[(4 * R) % 20], buf[(4 * R + 1) % 20], buf[(4 * R + 2) % 20],
       buf[(4 * R + 3) % 20]);
+  tc[0] = n0;
+  tc[1] = n1;
+  tc[2] = n2;
+  tc[3] = n3;
 }
 
 template <typename T>
@@ -224,29 +231,32 @@ __global__ void __launch_bounds__(kThreads) eta_direct_kernel(const T* __restric
       T acc[kJ];
 #pragma unroll
       for (int j = 0; j < kJ; ++j) acc[j] = T(0);
+      int2 rr_next = cd.rows[ai * cd.lb + b0];
       for (int bi = 0; bi < nb; ++bi) {
-        const int2 rr = cd.rows[ai * cd.lb + b0 + bi];
+        const int2 rr = rr_next;
+        if (bi + 1 < nb) rr_next = cd.rows[ai * cd.lb + b0 + bi + 1];  // prefetch
         if (rr.y <= 0) continue;
         const T* trow = taps + ((long long)ai * cd.lb + b0 + bi) * cd.lc4 + 4 * rr.x;
         const T* srow = region + (lane + bi) * g.pitch + warp * kJ + 4 * rr.x;
-        T buf[20];
+        T buf[20], tc[4];
+        ldg4(trow, tc[0], tc[1], tc[2], tc[3]);
 #pragma unroll
         for (int q = 0; q < 5; ++q)
           ld4(srow + 4 * q, buf[4 * q], buf[4 * q + 1], buf[4 * q + 2], buf[4 * q + 3]);
         int s = 0;
         const int ns = rr.y;
         for (; s + 5 <= ns; s += 5) {
-          tap_step<T, 0>(acc, buf, trow + 4 * s, srow + 4 * s);
-          tap_step<T, 1>(acc, buf, trow + 4 * s + 4, srow + 4 * s + 4);
-          tap_step<T, 2>(acc, buf, trow + 4 * s + 8, srow + 4 * s + 8);
-          tap_step<T, 3>(acc, buf, trow + 4 * s + 12, srow + 4 * s + 12);
-          tap_step<T, 4>(acc, buf, trow + 4 * s + 16, srow + 4 * s + 16);
+          tap_step<T, 0>(acc, buf, tc, trow + 4 * s + 4, srow + 4 * s);
+          tap_step<T, 1>(acc, buf, tc, trow + 4 * s + 8, srow + 4 * s + 4);
+          tap_step<T, 2>(acc, buf, tc, trow + 4 * s + 12, srow + 4 * s + 8);
+          tap_step<T, 3>(acc, buf, tc, trow + 4 * s + 16, srow + 4 * s + 12);
+          tap_step<T, 4>(acc, buf, tc, trow + 4 * s + 20, srow + 4 * s + 16);
         }
         const int rem = ns - s;
-        if (rem > 0) tap_step<T, 0>(acc, buf, trow + 4 * s, srow + 4 * s);
-        if (rem > 1) tap_step<T, 1>(acc, buf, trow + 4 * s + 4, srow + 4 * s + 4);
-        if (rem > 2) tap_step<T, 2>(acc, buf, trow + 4 * s + 8, srow + 4 * s + 8);
-        if (rem > 3) tap_step<T, 3>(acc, buf, trow + 4 * s + 12, srow + 4 * s + 12);
+        if (rem > 0) tap_step<T, 0>(acc, buf, tc, trow + 4 * s + 4, srow + 4 * s);
+        if (rem > 1) tap_step<T, 1>(acc, buf, tc, trow + 4 * s + 8, srow + 4 * s + 4);
+        if (rem > 2) tap_step<T, 2>(acc, buf, tc, trow + 4 * s + 12, srow + 4 * s + 8);
+        if (rem > 3) tap_step<T, 3>(acc, buf, tc, trow + 4 * s + 16, srow + 4 * s + 12);
       }
 #pragma unroll
       for (int j = 0; j < kJ; ++j) accd[j] += double(acc[j]);
@@ -616,7 +626,8 @@ static int build_candidate(const int dims[3], double sigma, double d, double tap
   const double half_d = 0.5 * d;
   const bool d2 = d == 2.0;
   c.rows.assign(size_t(c.la) * c.lb, make_int2(0, 0));
-  std::vector<double> t(size_t(c.la) * c.lb * c.lc4, 0.0);
+  // +8: the kernel prefetches one 4-tap group past the end of each row
+  std::vector<double> t(size_t(c.la) * c.lb * c.lc4 + 8, 0.0);
   c.taps = 0;
   for (int ai = 0; ai < c.la; ++ai) {
     const double a = c.lo[0] + ai;

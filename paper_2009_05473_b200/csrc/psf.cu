@@ -34,13 +34,23 @@ __device__ __forceinline__ int pmod_i(int a, int n) {
   return a;
 }
 
+// Taps are zero-padded to a multiple of J in shared memory; each block of J
+// taps is read into registers at once, so the inner loop is J x (J FFMA +
+// one window load) with no tap-load latency on the critical path.
 template <typename T, int J>
-__global__ void __launch_bounds__(256) pass_strided_kernel(
+__device__ __forceinline__ void load_taps_padded(T* taps, const T* __restrict__ taps_g, int ntaps,
+                                                 int npad) {
+  for (int q = threadIdx.x; q < npad; q += blockDim.x) taps[q] = q < ntaps ? taps_g[q] : T(0);
+}
+
+template <typename T, int J>
+__global__ void __launch_bounds__(256, 2) pass_strided_kernel(
     const T* __restrict__ in, T* out, int n_axis, long long stride, const T* __restrict__ taps_g,
     int lo, int ntaps, const T* addend, T aw, T w) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* taps = reinterpret_cast<T*>(smem_raw);
-  for (int q = threadIdx.x; q < ntaps; q += blockDim.x) taps[q] = taps_g[q];
+  const int npad = (ntaps + J - 1) / J * J;
+  load_taps_padded<T, J>(taps, taps_g, ntaps, npad);
   __syncthreads();
   // blockIdx.x runs over the a-blocks so CTAs that share input planes are
   // resident together (L2 reuse of the (J + taps - 1)/J overlap)
@@ -56,16 +66,16 @@ __global__ void __launch_bounds__(256) pass_strided_kernel(
     idx = wrap_inc(idx, n_axis);
     acc[j] = T(0);
   }
-  for (int q0 = 0; q0 < ntaps; q0 += J) {
+  for (int q0 = 0; q0 < npad; q0 += J) {
+    T tq[J];
+#pragma unroll
+    for (int r = 0; r < J; ++r) tq[r] = taps[q0 + r];
 #pragma unroll
     for (int r = 0; r < J; ++r) {
-      if (q0 + r < ntaps) {
-        const T t = taps[q0 + r];
 #pragma unroll
-        for (int j = 0; j < J; ++j) acc[j] = fma(t, W[(r + j) % J], acc[j]);
-        W[r] = in[base + idx * stride];
-        idx = wrap_inc(idx, n_axis);
-      }
+      for (int j = 0; j < J; ++j) acc[j] = fma(tq[r], W[(r + j) % J], acc[j]);
+      W[r] = in[base + idx * stride];
+      idx = wrap_inc(idx, n_axis);
     }
   }
 #pragma unroll
@@ -80,20 +90,23 @@ __global__ void __launch_bounds__(256) pass_strided_kernel(
 constexpr int kZRows = 32;   // rows per CTA (one per lane)
 constexpr int kZWarps = 4;   // z-groups per CTA
 
+// Contiguous axis: the CTA stages 32 rows x (4J + taps + J) in shared memory
+// (odd pitch: lane = row is conflict-free), computes J consecutive outputs
+// per thread with the rotated register window, then transposes the results
+// through shared memory so the global stores are coalesced along z.
 template <typename T, int J>
 __global__ void __launch_bounds__(32 * kZWarps) pass_z_kernel(
     const T* __restrict__ in, T* out, int nz, long long nrows, const T* __restrict__ taps_g, int lo,
     int ntaps, int pitch, const T* addend, T aw, T w) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int npad = (ntaps + J - 1) / J * J;
   T* taps = reinterpret_cast<T*>(smem_raw);
-  T* tile = taps + ((ntaps + 3) & ~3);
+  T* tile = taps + npad;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long row0 = (long long)blockIdx.y * kZRows;
   const int z0 = blockIdx.x * (J * kZWarps);
-  const int width = J * kZWarps + ntaps - 1 + J;  // staged columns
-  for (int q = threadIdx.x; q < ntaps; q += blockDim.x) taps[q] = taps_g[q];
-  // rows of the tile are read by consecutive threads along z (coalesced);
-  // the wrapped column index is computed once per column, not per element
+  const int width = J * kZWarps + npad;  // staged columns (incl. the padded-tap overrun)
+  load_taps_padded<T, J>(taps, taps_g, ntaps, npad);
   for (int c = threadIdx.x; c < width; c += blockDim.x) {
     const int zc = pmod_i(z0 + lo + c, nz);
     for (int r = 0; r < kZRows; ++r) {
@@ -109,25 +122,31 @@ __global__ void __launch_bounds__(32 * kZWarps) pass_z_kernel(
     W[j] = src[j];
     acc[j] = T(0);
   }
-  for (int q0 = 0; q0 < ntaps; q0 += J) {
+  for (int q0 = 0; q0 < npad; q0 += J) {
+    T tq[J];
+#pragma unroll
+    for (int r = 0; r < J; ++r) tq[r] = taps[q0 + r];
 #pragma unroll
     for (int r = 0; r < J; ++r) {
-      if (q0 + r < ntaps) {
-        const T t = taps[q0 + r];
 #pragma unroll
-        for (int j = 0; j < J; ++j) acc[j] = fma(t, W[(r + j) % J], acc[j]);
-        W[r] = src[q0 + r + J];
-      }
+      for (int j = 0; j < J; ++j) acc[j] = fma(tq[r], W[(r + j) % J], acc[j]);
+      W[r] = src[q0 + r + J];
     }
   }
-  const long long row = row0 + lane;
-  if (row >= nrows) return;
+  __syncthreads();  // every thread is done reading the staged input
+  T* res = tile + lane * pitch + warp * J;
 #pragma unroll
-  for (int j = 0; j < J; ++j) {
-    const int z = z0 + warp * J + j;
-    if (z < nz) {
+  for (int j = 0; j < J; ++j) res[j] = acc[j];
+  __syncthreads();
+  const int ncols = J * kZWarps;
+  for (int e = threadIdx.x; e < kZRows * ncols; e += blockDim.x) {
+    const int r = e / ncols, c = e % ncols;
+    const long long row = row0 + r;
+    const int z = z0 + c;
+    if (row < nrows && z < nz) {
       const long long o = row * nz + z;
-      out[o] = addend ? T(aw * addend[o] + w * acc[j]) : T(w * acc[j]);
+      const T v = tile[r * pitch + c];
+      out[o] = addend ? T(aw * addend[o] + w * v) : T(w * v);
     }
   }
 }
@@ -173,7 +192,11 @@ int launch_strided(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int a
   for (int a = 0; a < axis; ++a) outer *= dims[a];
   const int n = dims[axis];
   dim3 grid(unsigned((n + J - 1) / J), unsigned((stride + 255) / 256), unsigned(outer));
-  pass_strided_kernel<T, J><<<grid, 256, size_t(ntaps) * sizeof(T), ctx->stream>>>(
+  const size_t smem = size_t((ntaps + J - 1) / J * J) * sizeof(T);
+  if (smem > 48 * 1024)
+    SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_strided_kernel<T, J>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  pass_strided_kernel<T, J><<<grid, 256, smem, ctx->stream>>>(
       in, out, n, stride, taps, lo, ntaps, addend, T(aw), T(w));
   SFW3D_LAUNCH_CHECK(ctx);
   return SFW3D_OK;
@@ -183,9 +206,10 @@ template <typename T, int J>
 int launch_z(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* taps, int lo,
              int ntaps, const T* addend, double aw, double w) {
   const long long nrows = (long long)dims[0] * dims[1];
-  const int width = J * kZWarps + ntaps - 1 + J;
+  const int npad = (ntaps + J - 1) / J * J;
+  const int width = J * kZWarps + npad;
   const int pitch = width | 1;  // odd: 32 lanes on 32 rows hit 32 banks
-  const size_t smem = (size_t((ntaps + 3) & ~3) + size_t(kZRows) * pitch) * sizeof(T);
+  const size_t smem = (size_t(npad) + size_t(kZRows) * pitch) * sizeof(T);
   if (smem > 48 * 1024)
     SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_z_kernel<T, J>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
