@@ -5,25 +5,30 @@
 // (forward.py:209-229) / neg_eta (certificate.py:201-209).
 //
 //  * render: deterministic GATHER. One CTA owns a 4x8x16 brick, compacts
-//    (in row order) the atoms whose wrapped box meets the brick, and each
-//    thread sums w*G for its voxel in that order — the reference's per-voxel
-//    summation order (acc[box] += w*values, atom by atom), no float atomics.
-//  * atom sums: each atom box is cut into fixed 4096-voxel chunks; one CTA
-//    per chunk reduces the six products <P_c, field> in fp64, then a second
-//    kernel adds the chunk partials of each atom in chunk order.
+//    (in row order) the atoms whose wrapped box meets the brick, tabulates
+//    each listed atom's per-axis offsets for the brick's 4 + 8 + 16
+//    coordinates once in shared memory, and each thread sums w*G for its
+//    voxel in atom order — the reference's per-voxel summation order
+//    (acc[box] += w*values, atom by atom), no float atomics.
+//  * atom sums: each atom box is cut into fixed 4096-voxel chunks; a CTA
+//    tabulates the atom's per-axis (wrapped index, offset) once, then reduces
+//    the six products <P_c, field> over its chunk (fp64 across threads); a
+//    second kernel adds the chunk partials of each atom in chunk order.
 // fp64 volumes use fp64 math with products/sums rounded exactly as numpy
 // does (no FMA contraction where the reference rounds twice); fp32 volumes
-// use fp32 math (MUFU exp2/log2) with fp64 accumulation.
+// use fp32 math on the MUFU (ex2/lg2/rcp) with fp64 accumulation.
 #include "internal.cuh"
 
 namespace sfw3d {
 namespace {
 
 constexpr int kBX = 4, kBY = 8, kBZ = 16;  // render brick (512 voxels)
+constexpr int kSub = 16;                   // listed atoms tabulated per pass
 constexpr int kChunk = 4096;               // atom-sum chunk (voxels)
 constexpr int kSumThreads = 256;
+constexpr int kMaxAxis = 1024;             // tabulated axis length in atom sums
 
-// a mod n in [0, n) without a 64-bit division on the common path (|a| < 2n)
+// a mod n in [0, n) without a division on the common path (|a| < 2n)
 __device__ __forceinline__ int pmod(int a, int n) {
   if (a < 0) {
     a += n;
@@ -46,7 +51,7 @@ __device__ __forceinline__ double min_image(int i, double m, int n) {
 }
 
 // Offset of global voxel index g from the atom centre along one axis, or
-// false when g is outside the atom's box.
+// false when g is outside the atom's box (forward.py:102-116).
 __device__ __forceinline__ bool axis_offset(const AtomGeo& a, int axis, int g, int n, double& off) {
   if (a.full[axis]) {
     off = min_image(g, a.m[axis], n);
@@ -66,30 +71,35 @@ __device__ __forceinline__ bool box_meets(const AtomGeo& a, int axis, int b0, in
   return (b1 >= s) || (b0 <= e - n);
 }
 
-// unit profile value, fp64 (forward.py:133-137)
+__device__ __forceinline__ double u2_exact(double dx, double dy, double dz) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+
+// unit profile, fp64 (forward.py:133-137)
 __device__ __forceinline__ double profile64(const AtomGeo& a, double u2, double& t) {
   const double p = a.d2 ? u2 : pow(u2, a.half_d);
   t = __dmul_rn(a.inv2sd, p);
   return exp(-t);
 }
 
-__device__ __forceinline__ float profile32(const AtomGeo& a, float u2, float& t) {
-  const float p = a.d2 ? u2 : exp2f(float(a.half_d) * log2f(u2));
-  t = float(a.inv2sd) * p;
-  return expf(-t);
-}
-
-__device__ __forceinline__ double u2_exact(double dx, double dy, double dz) {
-  return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+// unit profile, fp32 on the MUFU; lg2u2 returns log2(u2) for reuse
+__device__ __forceinline__ float profile32(float inv2sd, float half_d, bool d2, float u2, float& t,
+                                           float& lg2u2) {
+  lg2u2 = __log2f(u2);
+  const float p = d2 ? u2 : exp2f(half_d * lg2u2);
+  t = inv2sd * p;
+  return __expf(-t);
 }
 
 // ------------------------------------------------------------------ render
 template <typename T>
 __global__ void __launch_bounds__(512) render_kernel(const AtomGeo* __restrict__ atoms, int k,
                                                      int nx, int ny, int nz, T* __restrict__ out) {
+  using Off = T;  // offsets tabulated in the storage precision (exact for fp64)
   __shared__ int list[512];
   __shared__ int warp_cnt[16];
   __shared__ int list_n;
+  __shared__ Off tx[kSub][kBX], ty[kSub][kBY], tz[kSub][kBZ];
 
   const int nbz = (nz + kBZ - 1) / kBZ, nby = (ny + kBY - 1) / kBY;
   const int bz = blockIdx.x % nbz, by = (blockIdx.x / nbz) % nby, bx = blockIdx.x / (nbz * nby);
@@ -100,6 +110,7 @@ __global__ void __launch_bounds__(512) render_kernel(const AtomGeo* __restrict__
   const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
   const bool live = gx < nx && gy < ny && gz < nz;
   const int lane = tid & 31, warp = tid >> 5;
+  const Off kOut = Off(INFINITY);
 
   double acc = 0.0;
   for (int base = 0; base < k; base += 512) {
@@ -126,26 +137,41 @@ __global__ void __launch_bounds__(512) render_kernel(const AtomGeo* __restrict__
     if (hit) list[warp_cnt[warp] + __popc(mask & ((1u << lane) - 1u))] = ai;
     __syncthreads();
     const int cnt = list_n;
-    if (live) {
-      for (int q = 0; q < cnt; ++q) {
-        const AtomGeo& a = atoms[list[q]];
-        double dx, dy, dz;
-        if (!axis_offset(a, 0, gx, nx, dx)) continue;
-        if (!axis_offset(a, 1, gy, ny, dy)) continue;
-        if (!axis_offset(a, 2, gz, nz, dz)) continue;
-        if constexpr (sizeof(T) == 8) {
-          double t;
-          const double v = profile64(a, u2_exact(dx, dy, dz), t);
-          acc = __dadd_rn(acc, __dmul_rn(a.w, v));
-        } else {
-          const float fx = float(dx), fy = float(dy), fz = float(dz);
-          float t;
-          const float v = profile32(a, fx * fx + fy * fy + fz * fz, t);
-          acc += a.w * double(v);
+    for (int q0 = 0; q0 < cnt; q0 += kSub) {
+      const int nq = min(kSub, cnt - q0);
+      // tabulate offsets of the brick coordinates (inf = outside the box)
+      if (tid < nq * (kBX + kBY + kBZ)) {
+        const int q = tid / (kBX + kBY + kBZ), e = tid % (kBX + kBY + kBZ);
+        const AtomGeo& a = atoms[list[q0 + q]];
+        int axis, li, g, n;
+        if (e < kBX) { axis = 0; li = e; g = x0 + e; n = nx; }
+        else if (e < kBX + kBY) { axis = 1; li = e - kBX; g = y0 + li; n = ny; }
+        else { axis = 2; li = e - kBX - kBY; g = z0 + li; n = nz; }
+        double off = 0.0;
+        const bool in = g < n && axis_offset(a, axis, g, n, off);
+        const Off v = in ? Off(off) : kOut;
+        if (axis == 0) tx[q][li] = v; else if (axis == 1) ty[q][li] = v; else tz[q][li] = v;
+      }
+      __syncthreads();
+      if (live) {
+        for (int q = 0; q < nq; ++q) {
+          const Off ox = tx[q][lx], oy = ty[q][ly], oz = tz[q][lz];
+          if (ox == kOut || oy == kOut || oz == kOut) continue;
+          const AtomGeo& a = atoms[list[q0 + q]];
+          if constexpr (sizeof(T) == 8) {
+            double t;
+            const double v = profile64(a, u2_exact(ox, oy, oz), t);
+            acc = __dadd_rn(acc, __dmul_rn(a.w, v));
+          } else {
+            float t, lg;
+            const float v = profile32(float(a.inv2sd), float(a.half_d), a.d2, ox * ox + oy * oy + oz * oz,
+                                      t, lg);
+            acc += a.w * double(v);
+          }
         }
       }
+      __syncthreads();
     }
-    __syncthreads();
   }
   if (live) out[((long long)gx * ny + gy) * nz + gz] = T(acc);
 }
@@ -160,31 +186,60 @@ template <typename T>
 __global__ void __launch_bounds__(kSumThreads) atom_sums_kernel(
     const AtomGeo* __restrict__ atoms, const Chunk* __restrict__ chunks, int nx, int ny, int nz,
     const T* __restrict__ field, double* __restrict__ partials) {
+  using Off = T;
+  __shared__ Off toff[3][kMaxAxis];
+  __shared__ int tidx[3][kMaxAxis];
   const Chunk ch = chunks[blockIdx.x];
   const AtomGeo& a = atoms[ch.atom];
   const int dims[3] = {nx, ny, nz};
   const int vend = int(min((long long)ch.first + kChunk, a.nvox));
   const int l2 = a.len[2], l1 = a.len[1];
+  const bool tab = a.len[0] <= kMaxAxis && l1 <= kMaxAxis && l2 <= kMaxAxis;
+  if (tab) {
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax)
+      for (int il = threadIdx.x; il < a.len[ax]; il += kSumThreads) {
+        if (a.full[ax]) {
+          tidx[ax][il] = il;
+          toff[ax][il] = Off(min_image(il, a.m[ax], dims[ax]));
+        } else {
+          const int p = a.start[ax] + il;
+          tidx[ax][il] = pmod(p, dims[ax]);
+          toff[ax][il] = Off(__dsub_rn(double(p), a.m[ax]));
+        }
+      }
+  }
+  __syncthreads();
 
   double s[6] = {0, 0, 0, 0, 0, 0};
   float sf[6] = {0, 0, 0, 0, 0, 0};
+  const float inv2sd = float(a.inv2sd), half_d = float(a.half_d), dd = float(a.d),
+              dos = float(a.d_over_sigma), lsig = float(a.log_sigma);
   for (int v = ch.first + threadIdx.x; v < vend; v += kSumThreads) {
     const int rest = v / l2;  // 32-bit index math (boxes hold < 2^31 voxels)
     const int ic = v - rest * l2;
     const int ia = rest / l1;
     const int ib = rest - ia * l1;
     int g[3];
-    double off[3];
+    Off off[3];
     const int il[3] = {ia, ib, ic};
+    if (tab) {
 #pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-      if (a.full[ax]) {
-        g[ax] = il[ax];
-        off[ax] = min_image(il[ax], a.m[ax], dims[ax]);
-      } else {
-        const int p = a.start[ax] + il[ax];
-        g[ax] = pmod(p, dims[ax]);
-        off[ax] = __dsub_rn(double(p), a.m[ax]);
+      for (int ax = 0; ax < 3; ++ax) {
+        g[ax] = tidx[ax][il[ax]];
+        off[ax] = toff[ax][il[ax]];
+      }
+    } else {
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        if (a.full[ax]) {
+          g[ax] = il[ax];
+          off[ax] = Off(min_image(il[ax], a.m[ax], dims[ax]));
+        } else {
+          const int p = a.start[ax] + il[ax];
+          g[ax] = pmod(p, dims[ax]);
+          off[ax] = Off(__dsub_rn(double(p), a.m[ax]));
+        }
       }
     }
     const T b = field[((long long)g[0] * ny + g[1]) * nz + g[2]];
@@ -205,22 +260,23 @@ __global__ void __launch_bounds__(kSumThreads) atom_sums_kernel(
       s[4] += __dmul_rn(vt, a.d_over_sigma) * b;
       s[5] += __dmul_rn(-vt, lr) * b;
     } else {
-      const float fx = float(off[0]), fy = float(off[1]), fz = float(off[2]);
+      const float fx = off[0], fy = off[1], fz = off[2];
       const float u2 = fx * fx + fy * fy + fz * fz;
-      float t;
-      const float val = profile32(a, u2, t);
+      float t, lg;
+      const float val = profile32(inv2sd, half_d, a.d2, u2, t, lg);
       float ampl = 0.f, lr = 0.f;
       if (u2 > 0.f) {
-        ampl = float(a.d) * val * t / u2;
-        lr = 0.5f * logf(u2) - float(a.log_sigma);
+        ampl = dd * val * t * __frcp_rn(u2);
+        lr = 0.34657359027997264f * lg - lsig;  // 0.5 ln(u2) = 0.5 ln2 log2(u2)
       }
       const float vt = val * t;
       const float bf = float(b);
+      const float ab = ampl * bf;
       sf[0] += val * bf;
-      sf[1] += ampl * fx * bf;
-      sf[2] += ampl * fy * bf;
-      sf[3] += ampl * fz * bf;
-      sf[4] += vt * float(a.d_over_sigma) * bf;
+      sf[1] += ab * fx;
+      sf[2] += ab * fy;
+      sf[3] += ab * fz;
+      sf[4] += vt * dos * bf;
       sf[5] -= vt * lr * bf;
     }
   }

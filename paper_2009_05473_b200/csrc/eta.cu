@@ -231,15 +231,24 @@ __global__ void __launch_bounds__(kThreads) eta_direct_kernel(const T* __restric
       T acc[kJ];
 #pragma unroll
       for (int j = 0; j < kJ; ++j) acc[j] = T(0);
+      // software pipeline over template rows: the next row's extent and its
+      // first 4 taps are fetched while the current row computes
+      const T* trow_base = taps + ((long long)ai * cd.lb + b0) * cd.lc4;
       int2 rr_next = cd.rows[ai * cd.lb + b0];
+      T tn[4];
+      ldg4(trow_base + 4 * max(rr_next.x, 0), tn[0], tn[1], tn[2], tn[3]);
       for (int bi = 0; bi < nb; ++bi) {
         const int2 rr = rr_next;
-        if (bi + 1 < nb) rr_next = cd.rows[ai * cd.lb + b0 + bi + 1];  // prefetch
+        T tc[4] = {tn[0], tn[1], tn[2], tn[3]};
+        if (bi + 1 < nb) {
+          rr_next = cd.rows[ai * cd.lb + b0 + bi + 1];
+          ldg4(trow_base + (long long)(bi + 1) * cd.lc4 + 4 * max(rr_next.x, 0), tn[0], tn[1], tn[2],
+               tn[3]);
+        }
         if (rr.y <= 0) continue;
-        const T* trow = taps + ((long long)ai * cd.lb + b0 + bi) * cd.lc4 + 4 * rr.x;
+        const T* trow = trow_base + (long long)bi * cd.lc4 + 4 * rr.x;
         const T* srow = region + (lane + bi) * g.pitch + warp * kJ + 4 * rr.x;
-        T buf[20], tc[4];
-        ldg4(trow, tc[0], tc[1], tc[2], tc[3]);
+        T buf[20];
 #pragma unroll
         for (int q = 0; q < 5; ++q)
           ld4(srow + 4 * q, buf[4 * q], buf[4 * q + 1], buf[4 * q + 2], buf[4 * q + 3]);

@@ -44,7 +44,7 @@ __device__ __forceinline__ void load_taps_padded(T* taps, const T* __restrict__ 
 }
 
 template <typename T, int J>
-__global__ void __launch_bounds__(256, 2) pass_strided_kernel(
+__global__ void __launch_bounds__(256) pass_strided_kernel(
     const T* __restrict__ in, T* out, int n_axis, long long stride, const T* __restrict__ taps_g,
     int lo, int ntaps, const T* addend, T aw, T w) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -66,14 +66,14 @@ __global__ void __launch_bounds__(256, 2) pass_strided_kernel(
     idx = wrap_inc(idx, n_axis);
     acc[j] = T(0);
   }
+  // (taps stay in shared memory here: the strided window loads need the
+  // registers more than the broadcast taps do)
   for (int q0 = 0; q0 < npad; q0 += J) {
-    T tq[J];
-#pragma unroll
-    for (int r = 0; r < J; ++r) tq[r] = taps[q0 + r];
 #pragma unroll
     for (int r = 0; r < J; ++r) {
+      const T t = taps[q0 + r];
 #pragma unroll
-      for (int j = 0; j < J; ++j) acc[j] = fma(tq[r], W[(r + j) % J], acc[j]);
+      for (int j = 0; j < J; ++j) acc[j] = fma(t, W[(r + j) % J], acc[j]);
       W[r] = in[base + idx * stride];
       idx = wrap_inc(idx, n_axis);
     }
@@ -82,6 +82,61 @@ __global__ void __launch_bounds__(256, 2) pass_strided_kernel(
   for (int j = 0; j < J; ++j) {
     if (a0 + j < n_axis) {
       const long long o = base + (long long)(a0 + j) * stride;
+      out[o] = addend ? T(aw * addend[o] + w * acc[j]) : T(w * acc[j]);
+    }
+  }
+}
+
+// Strided axes, shared-memory tiled: a CTA owns 64 consecutive inner
+// (contiguous) indices x 4J outputs along the axis; the (4J + taps) input
+// rows are staged once with coalesced 256-byte row loads, so each input is
+// read ~ (4J + taps) / 4J times instead of (J + taps) / J. Lanes run over the
+// inner index: conflict-free smem, coalesced stores.
+constexpr int kTInner = 64;
+constexpr int kTGroups = 4;
+
+template <typename T, int J>
+__global__ void __launch_bounds__(256) pass_tiled_kernel(
+    const T* __restrict__ in, T* out, int n_axis, long long stride, const T* __restrict__ taps_g,
+    int lo, int ntaps, const T* addend, T aw, T w) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int npad = (ntaps + J - 1) / J * J;
+  T* taps = reinterpret_cast<T*>(smem_raw);
+  T* tile = taps + npad;
+  constexpr int To = J * kTGroups;
+  const int a0 = blockIdx.x * To;
+  const long long inner0 = (long long)blockIdx.y * kTInner;
+  const long long base0 = (long long)blockIdx.z * n_axis * stride + inner0;
+  const int rows = To + npad;
+  load_taps_padded<T, J>(taps, taps_g, ntaps, npad);
+  for (int e = threadIdx.x; e < rows * kTInner; e += blockDim.x) {
+    const int r = e / kTInner, c = e % kTInner;
+    const int a = pmod_i(a0 + lo + r, n_axis);
+    tile[e] = in[base0 + (long long)a * stride + c];
+  }
+  __syncthreads();
+  const int il = threadIdx.x % kTInner, ag = threadIdx.x / kTInner;
+  const T* src = tile + (ag * J) * kTInner + il;
+  T W[J], acc[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    W[j] = src[j * kTInner];
+    acc[j] = T(0);
+  }
+  for (int q0 = 0; q0 < npad; q0 += J) {
+#pragma unroll
+    for (int r = 0; r < J; ++r) {
+      const T t = taps[q0 + r];
+#pragma unroll
+      for (int j = 0; j < J; ++j) acc[j] = fma(t, W[(r + j) % J], acc[j]);
+      W[r] = src[(q0 + r + J) * kTInner];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int a = a0 + ag * J + j;
+    if (a < n_axis) {
+      const long long o = base0 + (long long)a * stride + il;
       out[o] = addend ? T(aw * addend[o] + w * acc[j]) : T(w * acc[j]);
     }
   }
@@ -203,6 +258,27 @@ int launch_strided(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int a
 }
 
 template <typename T, int J>
+int launch_tiled(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis, const T* taps,
+                 int lo, int ntaps, const T* addend, double aw, double w) {
+  long long stride = 1;
+  for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
+  long long outer = 1;
+  for (int a = 0; a < axis; ++a) outer *= dims[a];
+  const int n = dims[axis];
+  constexpr int To = J * kTGroups;
+  const int npad = (ntaps + J - 1) / J * J;
+  const size_t smem = (size_t(npad) + size_t(To + npad) * kTInner) * sizeof(T);
+  if (smem > 48 * 1024)
+    SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_tiled_kernel<T, J>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  dim3 grid(unsigned((n + To - 1) / To), unsigned(stride / kTInner), unsigned(outer));
+  pass_tiled_kernel<T, J><<<grid, 256, smem, ctx->stream>>>(in, out, n, stride, taps, lo, ntaps,
+                                                              addend, T(aw), T(w));
+  SFW3D_LAUNCH_CHECK(ctx);
+  return SFW3D_OK;
+}
+
+template <typename T, int J>
 int launch_z(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* taps, int lo,
              int ntaps, const T* addend, double aw, double w) {
   const long long nrows = (long long)dims[0] * dims[1];
@@ -231,7 +307,11 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
   const bool wide = ntaps > 24;
   if (axis == 2)
     return wide ? launch_z<T, 32>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w)
-                : launch_z<T, 8>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
+                : launch_z<T, 16>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
+  long long stride = 1;
+  for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
+  if (stride % kTInner == 0 && ntaps <= 512)
+    return launch_tiled<T, 16>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
   return wide ? launch_strided<T, 32>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w)
               : launch_strided<T, 8>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
 }
