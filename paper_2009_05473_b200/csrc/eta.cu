@@ -220,13 +220,10 @@ __global__ void __launch_bounds__(kThreads) eta_direct_kernel(const T* __restric
         const int r = e / nvec, c4 = e % nvec;
         const T* s = src0 + (long long)r * g.pys + 4 * c4;
         T* d = region + r * g.pitch + 4 * c4;
-        if constexpr (sizeof(T) == 4) {
-          *reinterpret_cast<float4*>(d) = __ldg(reinterpret_cast<const float4*>(s));
-        } else {
-          *reinterpret_cast<double2*>(d) = __ldg(reinterpret_cast<const double2*>(s));
-          *reinterpret_cast<double2*>(d + 2) = __ldg(reinterpret_cast<const double2*>(s + 2));
-        }
+        cp_async16(d, s);
+        if constexpr (sizeof(T) == 8) cp_async16(d + 2, s + 2);
       }
+      cp_async_wait_all();
       __syncthreads();
       T acc[kJ];
 #pragma unroll
@@ -399,14 +396,11 @@ __global__ void __launch_bounds__(kThreads) eta_sym_kernel(const T* __restrict__
         const int r = e / nvec, c4 = e % nvec;
         const T* s = src0 + (long long)r * g.pys + 4 * c4;
         T* d = dst0 + r * g.pitch + 4 * c4;
-        if constexpr (sizeof(T) == 4) {
-          *reinterpret_cast<float4*>(d) = __ldg(reinterpret_cast<const float4*>(s));
-        } else {
-          *reinterpret_cast<double2*>(d) = __ldg(reinterpret_cast<const double2*>(s));
-          *reinterpret_cast<double2*>(d + 2) = __ldg(reinterpret_cast<const double2*>(s + 2));
-        }
+        cp_async16(d, s);
+        if constexpr (sizeof(T) == 8) cp_async16(d + 2, s + 2);
       }
     }
+    cp_async_wait_all();
     __syncthreads();
     T acc[kJ];
 #pragma unroll

@@ -109,11 +109,14 @@ __global__ void __launch_bounds__(256) pass_tiled_kernel(
   const long long base0 = (long long)blockIdx.z * n_axis * stride + inner0;
   const int rows = To + npad;
   load_taps_padded<T, J>(taps, taps_g, ntaps, npad);
-  for (int e = threadIdx.x; e < rows * kTInner; e += blockDim.x) {
-    const int r = e / kTInner, c = e % kTInner;
+  constexpr int kVec = 16 / sizeof(T);  // elements per 16-byte async copy
+  constexpr int kRowVecs = kTInner / kVec;
+  for (int e = threadIdx.x; e < rows * kRowVecs; e += blockDim.x) {
+    const int r = e / kRowVecs, c = (e % kRowVecs) * kVec;
     const int a = pmod_i(a0 + lo + r, n_axis);
-    tile[e] = in[base0 + (long long)a * stride + c];
+    cp_async16(tile + r * kTInner + c, in + base0 + (long long)a * stride + c);
   }
+  cp_async_wait_all();
   __syncthreads();
   const int il = threadIdx.x % kTInner, ag = threadIdx.x / kTInner;
   const T* src = tile + (ag * J) * kTInner + il;
@@ -166,9 +169,17 @@ __global__ void __launch_bounds__(32 * kZWarps) pass_z_kernel(
     const int zc = pmod_i(z0 + lo + c, nz);
     for (int r = 0; r < kZRows; ++r) {
       const long long row = row0 + r;
-      tile[r * pitch + c] = row < nrows ? in[row * nz + zc] : T(0);
+      if (row < nrows) {
+        if constexpr (sizeof(T) == 8)
+          cp_async8(tile + r * pitch + c, in + row * nz + zc);
+        else
+          cp_async4(tile + r * pitch + c, in + row * nz + zc);
+      } else {
+        tile[r * pitch + c] = T(0);
+      }
     }
   }
+  cp_async_wait_all();
   __syncthreads();
   const T* src = tile + lane * pitch + warp * J;
   T W[J], acc[J];
