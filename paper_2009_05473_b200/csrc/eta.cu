@@ -298,6 +298,11 @@ __device__ __forceinline__ void sym_step(T (&acc)[kJ], T (&buf)[20], T (&tc)[4],
                                          const T* const (&src)[4], int col) {
   T n0, n1, n2, n3;
   ldg4(tnext, n0, n1, n2, n3);
+  // issue the next window columns of all NR rows before the FFMAs so their
+  // shared-memory latency is hidden; sum them afterwards
+  T u[NR][4];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) ld4(src[q] + col, u[q][0], u[q][1], u[q][2], u[q][3]);
 #pragma unroll
   for (int j = 0; j < kJ; ++j) {
     acc[j] = fma(tc[0], buf[(4 * R + j + 0) % 20], acc[j]);
@@ -305,13 +310,10 @@ __device__ __forceinline__ void sym_step(T (&acc)[kJ], T (&buf)[20], T (&tc)[4],
     acc[j] = fma(tc[2], buf[(4 * R + j + 2) % 20], acc[j]);
     acc[j] = fma(tc[3], buf[(4 * R + j + 3) % 20], acc[j]);
   }
-  T s0, s1, s2, s3;
-  ld4(src[0] + col, s0, s1, s2, s3);
+  T s0 = u[0][0], s1 = u[0][1], s2 = u[0][2], s3 = u[0][3];
 #pragma unroll
   for (int q = 1; q < NR; ++q) {
-    T u0, u1, u2, u3;
-    ld4(src[q] + col, u0, u1, u2, u3);
-    s0 += u0; s1 += u1; s2 += u2; s3 += u3;
+    s0 += u[q][0]; s1 += u[q][1]; s2 += u[q][2]; s3 += u[q][3];
   }
   buf[(4 * R) % 20] = s0;
   buf[(4 * R + 1) % 20] = s1;

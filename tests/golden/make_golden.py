@@ -227,6 +227,42 @@ def case_solve(rng):
     np.savez(OUT / "solve.npz", **out)
 
 
+def case_config1(seed=2):
+    """BASELINE config 1 end to end: 64^3 f64, N=5 atoms (m ~ U[8,56]^3,
+    sigma ~ U[1.5,3], d ~ U[1.5,2.5], w ~ U[1,2]), PSF sigma_h=2 on 15^3, white
+    noise at 20 dB power SNR, lam = 0.1 max Phi*y over the certificate grid
+    sigma {1.5,2,2.5,3} x d {1.5,2,2.5} (injected by rebinding
+    solvers.make_parameter_grids), BSFW with 20 outer
+    iterations. The truth is drawn exactly as paper_2009_05473_b200.configs
+    .config1(seed) draws it."""
+    rng = np.random.default_rng(seed)
+    dims = (64, 64, 64)
+    m = rng.uniform(8.0, 56.0, size=(5, 3))
+    truth = np.column_stack([rng.uniform(1, 2, 5), m, rng.uniform(1.5, 3, 5),
+                             rng.uniform(1.5, 2.5, 5)])
+    psf = Psf(Volume(box_psf(dims, (2, 2, 2), (7, 7, 7))))
+    clean = sfw3d.forward(measure_from_rows(truth), psf).data
+    noise = np.sqrt(np.mean(clean ** 2) / 10 ** (20 / 10))
+    y = clean + noise * np.random.default_rng(seed + 1000).standard_normal(dims)
+    bounds = DomainBounds(pos_lower=(8.0,) * 3, pos_upper=(56.0,) * 3, sigma_min=1.5,
+                          sigma_max=3.0, shape_min=1.5, shape_max=2.5)
+    sg, dg = np.array([1.5, 2.0, 2.5, 3.0]), np.array([1.5, 2.0, 2.5])
+    table = rcert.build_template_table(psf, sg, dg, bounds=bounds)
+    lam = 0.1 * rcert.eta_field(Volume(y), 1.0, table, bounds=bounds, keep_fields=False).eta_max
+    orig = rsolv.make_parameter_grids
+    rsolv.make_parameter_grids = lambda b, ns, nd: (sg, dg)
+    try:
+        res = sfw3d.bsfw(Volume(y), psf, SolverOptions(lam=lam, max_outer_iterations=20), bounds)
+    finally:
+        rsolv.make_parameter_grids = orig
+    np.savez_compressed(OUT / "config1.npz", y=y, truth=truth, lam=np.array(lam),
+                        noise=np.array(noise), rows=rows_from_measure(res.measure),
+                        C=np.array(res.criterion), term=np.array(res.termination),
+                        eta=np.array([r.eta_max for r in res.trace.records]),
+                        atoms=np.array([r.atom_count for r in res.trace.records]),
+                        t_total=np.array(res.trace.t_total))
+
+
 def main():
     rng = np.random.default_rng(20090547)
     case_kats()
@@ -236,6 +272,8 @@ def main():
     case_certificate(rng)
     case_lasso(rng)
     case_solve(rng)
+    if "--with-config1" in sys.argv:
+        case_config1()
     print("golden fixtures written to", OUT)
 
 
