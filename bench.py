@@ -366,6 +366,46 @@ def costgrad_workload(args, dev):
             "timing": "wall clock per synchronous C-ABI call (host params in, C + gradient out)"}
 
 
+def solve_workload(dev):
+    """Config 1 BSFW end to end (64^3 f64) on the reference-generated
+    observation in tests/golden/config1.npz (the GPU parity test compares the
+    result with the reference's own solve of it)."""
+    import paper_2009_05473_b200 as P
+    from paper_2009_05473_b200 import solvers
+    g = np.load(ROOT / "tests" / "golden" / "config1.npz")
+    P.set_precision("f64")
+    from paper_2009_05473_b200.configs import box_psf_kernel
+    dims = (64, 64, 64)
+    psf = P.Psf(P.Volume(box_psf_kernel(dims, (2, 2, 2), (7, 7, 7))), normalize=False)
+    bounds = P.DomainBounds((8.0,) * 3, (56.0,) * 3, 1.5, 3.0, 1.5, 2.5)
+    sg, dg = np.array([1.5, 2.0, 2.5, 3.0]), np.array([1.5, 2.0, 2.5])
+    orig = solvers.make_parameter_grids
+    solvers.make_parameter_grids = lambda b, ns, nd: (sg, dg)
+    try:
+        y = P.Volume(g["y"])
+        opts = P.SolverOptions(lam=float(g["lam"]), max_outer_iterations=20)
+        P.bsfw(y, psf, opts, bounds)  # warm-up (as experiment.py:487-492 does)
+        t0 = time.perf_counter()
+        res = P.bsfw(P.Volume(g["y"]), psf, opts, bounds)
+        t = time.perf_counter() - t0
+    finally:
+        solvers.make_parameter_grids = orig
+    rows = res.measure.to_rows()
+    ref = g["rows"]
+    return {"metric": "BSFW solve time, config 1 (64^3 f64, N=5, 12 candidates)",
+            "value": t, "unit": "s", "higher_is_better": False,
+            "outer_iterations": len(res.trace.records), "atoms": len(res.measure),
+            "criterion": res.criterion, "reference_atoms": int(ref.shape[0]),
+            "reference_criterion": float(g["C"]),
+            "reference_cpu_s": float(g["t_total"]),
+            "reference_cpu_note": "sfw3d 0.1.0 bsfw on the same observation, timed in the build "
+                                  "container (8-core VM) when the golden was generated",
+            "split_s": {"certificate": res.trace.step_time("certificate"),
+                        "lasso": res.trace.step_time("lasso"),
+                        "descent": res.trace.step_time("descent"),
+                        "table": res.trace.t_table}}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -381,6 +421,7 @@ def main():
     secondary = []
     if rank == 0 and not args.no_secondary:
         secondary.append(costgrad_workload(args, dev))
+        secondary.append(solve_workload(dev))
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         inst = res["inst"]

@@ -95,88 +95,54 @@ __global__ void __launch_bounds__(256) pass_strided_kernel(
 constexpr int kTInner = 64;
 constexpr int kTGroups = 4;
 
-// Persistent and double-buffered: each CTA walks tiles t = blockIdx.x,
-// blockIdx.x + gridDim.x, ... and prefetches tile t+1 with cp.async while it
-// computes tile t, so HBM stays busy through the FFMA phases.
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait_group() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
 template <typename T, int J>
 __global__ void __launch_bounds__(256) pass_tiled_kernel(
-    const T* __restrict__ in, T* out, int n_axis, long long stride, long long outer,
-    const T* __restrict__ taps_g, int lo, int ntaps, const T* addend, T aw, T w) {
+    const T* __restrict__ in, T* out, int n_axis, long long stride, const T* __restrict__ taps_g,
+    int lo, int ntaps, const T* addend, T aw, T w) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int npad = (ntaps + J - 1) / J * J;
   T* taps = reinterpret_cast<T*>(smem_raw);
+  T* tile = taps + npad;
   constexpr int To = J * kTGroups;
+  const int a0 = blockIdx.x * To;
+  const long long inner0 = (long long)blockIdx.y * kTInner;
+  const long long base0 = (long long)blockIdx.z * n_axis * stride + inner0;
   const int rows = To + npad;
-  T* buf[2] = {taps + npad, taps + npad + rows * kTInner};
-  const int n_ablk = (n_axis + To - 1) / To;
-  const long long n_inner = stride / kTInner;
-  const long long n_tiles = (long long)n_ablk * n_inner * outer;
+  load_taps_padded<T, J>(taps, taps_g, ntaps, npad);
   constexpr int kVec = 16 / sizeof(T);  // elements per 16-byte async copy
   constexpr int kRowVecs = kTInner / kVec;
-  load_taps_padded<T, J>(taps, taps_g, ntaps, npad);
-
-  auto tile_origin = [&](long long t, int& a0, long long& base0) {
-    a0 = int(t % n_ablk) * To;  // a-blocks fastest: neighbours share input rows in L2
-    const long long rest = t / n_ablk;
-    base0 = (rest / n_inner) * n_axis * stride + (rest % n_inner) * kTInner;
-  };
-  auto stage = [&](long long t, T* dst) {
-    int a0;
-    long long base0;
-    tile_origin(t, a0, base0);
-    for (int e = threadIdx.x; e < rows * kRowVecs; e += blockDim.x) {
-      const int r = e / kRowVecs, c = (e % kRowVecs) * kVec;
-      const int a = pmod_i(a0 + lo + r, n_axis);
-      cp_async16(dst + r * kTInner + c, in + base0 + (long long)a * stride + c);
-    }
-  };
-
-  const int il = threadIdx.x % kTInner, ag = threadIdx.x / kTInner;
-  long long t = blockIdx.x;
-  if (t < n_tiles) stage(t, buf[0]);
-  cp_async_commit();
-  for (int it = 0; t < n_tiles; t += gridDim.x, ++it) {
-    const long long tn = t + gridDim.x;
-    if (tn < n_tiles) stage(tn, buf[(it + 1) & 1]);
-    cp_async_commit();
-    cp_async_wait_group<1>();  // tile t has landed (tn may still be in flight)
-    __syncthreads();
-    const T* src = buf[it & 1] + (ag * J) * kTInner + il;
-    T W[J], acc[J];
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      W[j] = src[j * kTInner];
-      acc[j] = T(0);
-    }
-    for (int q0 = 0; q0 < npad; q0 += J) {
-#pragma unroll
-      for (int r = 0; r < J; ++r) {
-        const T tp = taps[q0 + r];
-#pragma unroll
-        for (int j = 0; j < J; ++j) acc[j] = fma(tp, W[(r + j) % J], acc[j]);
-        W[r] = src[(q0 + r + J) * kTInner];
-      }
-    }
-    int a0;
-    long long base0;
-    tile_origin(t, a0, base0);
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const int a = a0 + ag * J + j;
-      if (a < n_axis) {
-        const long long o = base0 + (long long)a * stride + il;
-        out[o] = addend ? T(aw * addend[o] + w * acc[j]) : T(w * acc[j]);
-      }
-    }
-    __syncthreads();  // buffer it&1 is free for the prefetch two tiles ahead
+  for (int e = threadIdx.x; e < rows * kRowVecs; e += blockDim.x) {
+    const int r = e / kRowVecs, c = (e % kRowVecs) * kVec;
+    const int a = pmod_i(a0 + lo + r, n_axis);
+    cp_async16(tile + r * kTInner + c, in + base0 + (long long)a * stride + c);
   }
-  cp_async_wait_group<0>();
+  cp_async_wait_all();
+  __syncthreads();
+  const int il = threadIdx.x % kTInner, ag = threadIdx.x / kTInner;
+  const T* src = tile + (ag * J) * kTInner + il;
+  T W[J], acc[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    W[j] = src[j * kTInner];
+    acc[j] = T(0);
+  }
+  for (int q0 = 0; q0 < npad; q0 += J) {
+#pragma unroll
+    for (int r = 0; r < J; ++r) {
+      const T t = taps[q0 + r];
+#pragma unroll
+      for (int j = 0; j < J; ++j) acc[j] = fma(t, W[(r + j) % J], acc[j]);
+      W[r] = src[(q0 + r + J) * kTInner];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int a = a0 + ag * J + j;
+    if (a < n_axis) {
+      const long long o = base0 + (long long)a * stride + il;
+      out[o] = addend ? T(aw * addend[o] + w * acc[j]) : T(w * acc[j]);
+    }
+  }
 }
 
 constexpr int kZRows = 32;   // rows per CTA (one per lane)
@@ -193,81 +159,62 @@ __global__ void __launch_bounds__(32 * kZWarps) pass_z_kernel(
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int npad = (ntaps + J - 1) / J * J;
   T* taps = reinterpret_cast<T*>(smem_raw);
-  T* buf[2] = {taps + npad, taps + npad + kZRows * pitch};
+  T* tile = taps + npad;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int ncols = J * kZWarps;
-  const int width = ncols + npad;  // staged columns (incl. the padded-tap overrun)
-  const int nzb = (nz + ncols - 1) / ncols;
-  const long long n_tiles = (long long)nzb * ((nrows + kZRows - 1) / kZRows);
+  const long long row0 = (long long)blockIdx.y * kZRows;
+  const int z0 = blockIdx.x * (J * kZWarps);
+  const int width = J * kZWarps + npad;  // staged columns (incl. the padded-tap overrun)
   load_taps_padded<T, J>(taps, taps_g, ntaps, npad);
-
-  auto stage = [&](long long t, T* tile) {
-    const int z0 = int(t % nzb) * ncols;
-    const long long row0 = (t / nzb) * kZRows;
-    for (int c = threadIdx.x; c < width; c += blockDim.x) {
-      const int zc = pmod_i(z0 + lo + c, nz);
-      for (int r = 0; r < kZRows; ++r) {
-        const long long row = row0 + r;
-        if (row < nrows) {
-          if constexpr (sizeof(T) == 8)
-            cp_async8(tile + r * pitch + c, in + row * nz + zc);
-          else
-            cp_async4(tile + r * pitch + c, in + row * nz + zc);
-        } else {
-          tile[r * pitch + c] = T(0);
-        }
-      }
-    }
-  };
-
-  long long t = blockIdx.x;
-  if (t < n_tiles) stage(t, buf[0]);
-  cp_async_commit();
-  for (int it = 0; t < n_tiles; t += gridDim.x, ++it) {
-    const long long tn = t + gridDim.x;
-    if (tn < n_tiles) stage(tn, buf[(it + 1) & 1]);
-    cp_async_commit();
-    cp_async_wait_group<1>();
-    __syncthreads();
-    T* tile = buf[it & 1];
-    const T* src = tile + lane * pitch + warp * J;
-    T W[J], acc[J];
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      W[j] = src[j];
-      acc[j] = T(0);
-    }
-    for (int q0 = 0; q0 < npad; q0 += J) {
-      T tq[J];
-#pragma unroll
-      for (int r = 0; r < J; ++r) tq[r] = taps[q0 + r];
-#pragma unroll
-      for (int r = 0; r < J; ++r) {
-#pragma unroll
-        for (int j = 0; j < J; ++j) acc[j] = fma(tq[r], W[(r + j) % J], acc[j]);
-        W[r] = src[q0 + r + J];
-      }
-    }
-    __syncthreads();  // every thread is done reading the staged input
-    T* res = tile + lane * pitch + warp * J;
-#pragma unroll
-    for (int j = 0; j < J; ++j) res[j] = acc[j];
-    __syncthreads();
-    const int z0 = int(t % nzb) * ncols;
-    const long long row0 = (t / nzb) * kZRows;
-    for (int e = threadIdx.x; e < kZRows * ncols; e += blockDim.x) {
-      const int r = e / ncols, c = e % ncols;
+  for (int c = threadIdx.x; c < width; c += blockDim.x) {
+    const int zc = pmod_i(z0 + lo + c, nz);
+    for (int r = 0; r < kZRows; ++r) {
       const long long row = row0 + r;
-      const int z = z0 + c;
-      if (row < nrows && z < nz) {
-        const long long o = row * nz + z;
-        const T v = tile[r * pitch + c];
-        out[o] = addend ? T(aw * addend[o] + w * v) : T(w * v);
+      if (row < nrows) {
+        if constexpr (sizeof(T) == 8)
+          cp_async8(tile + r * pitch + c, in + row * nz + zc);
+        else
+          cp_async4(tile + r * pitch + c, in + row * nz + zc);
+      } else {
+        tile[r * pitch + c] = T(0);
       }
     }
-    __syncthreads();  // the tile buffer is reused by the prefetch two tiles ahead
   }
-  cp_async_wait_group<0>();
+  cp_async_wait_all();
+  __syncthreads();
+  const T* src = tile + lane * pitch + warp * J;
+  T W[J], acc[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    W[j] = src[j];
+    acc[j] = T(0);
+  }
+  for (int q0 = 0; q0 < npad; q0 += J) {
+    T tq[J];
+#pragma unroll
+    for (int r = 0; r < J; ++r) tq[r] = taps[q0 + r];
+#pragma unroll
+    for (int r = 0; r < J; ++r) {
+#pragma unroll
+      for (int j = 0; j < J; ++j) acc[j] = fma(tq[r], W[(r + j) % J], acc[j]);
+      W[r] = src[q0 + r + J];
+    }
+  }
+  __syncthreads();  // every thread is done reading the staged input
+  T* res = tile + lane * pitch + warp * J;
+#pragma unroll
+  for (int j = 0; j < J; ++j) res[j] = acc[j];
+  __syncthreads();
+  const int ncols = J * kZWarps;
+  for (int e = threadIdx.x; e < kZRows * ncols; e += blockDim.x) {
+    const int r = e / ncols, c = e % ncols;
+    const long long row = row0 + r;
+    const int z = z0 + c;
+    if (row < nrows && z < nz) {
+      const long long o = row * nz + z;
+      const T v = tile[r * pitch + c];
+      out[o] = addend ? T(aw * addend[o] + w * v) : T(w * v);
+    }
+  }
 }
 
 // General (non-separable) kernel: out[x] = sum_o K(o) in[x + sgn*o] over the
@@ -331,17 +278,13 @@ int launch_tiled(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axi
   const int n = dims[axis];
   constexpr int To = J * kTGroups;
   const int npad = (ntaps + J - 1) / J * J;
-  const size_t smem = (size_t(npad) + 2 * size_t(To + npad) * kTInner) * sizeof(T);
+  const size_t smem = (size_t(npad) + size_t(To + npad) * kTInner) * sizeof(T);
   if (smem > 48 * 1024)
     SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_tiled_kernel<T, J>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  const long long n_tiles = (long long)((n + To - 1) / To) * (stride / kTInner) * outer;
-  int per_sm = 1;
-  SFW3D_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pass_tiled_kernel<T, J>,
-                                                               256, smem));
-  const long long grid = std::min<long long>(n_tiles, (long long)std::max(per_sm, 1) * ctx->num_sms);
-  pass_tiled_kernel<T, J><<<unsigned(grid), 256, smem, ctx->stream>>>(
-      in, out, n, stride, outer, taps, lo, ntaps, addend, T(aw), T(w));
+  dim3 grid(unsigned((n + To - 1) / To), unsigned(stride / kTInner), unsigned(outer));
+  pass_tiled_kernel<T, J><<<grid, 256, smem, ctx->stream>>>(in, out, n, stride, taps, lo, ntaps,
+                                                              addend, T(aw), T(w));
   SFW3D_LAUNCH_CHECK(ctx);
   return SFW3D_OK;
 }
@@ -353,16 +296,12 @@ int launch_z(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* ta
   const int npad = (ntaps + J - 1) / J * J;
   const int width = J * kZWarps + npad;
   const int pitch = width | 1;  // odd: 32 lanes on 32 rows hit 32 banks
-  const size_t smem = (size_t(npad) + 2 * size_t(kZRows) * pitch) * sizeof(T);
+  const size_t smem = (size_t(npad) + size_t(kZRows) * pitch) * sizeof(T);
   if (smem > 48 * 1024)
     SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_z_kernel<T, J>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  const long long n_tiles = (long long)((dims[2] + J * kZWarps - 1) / (J * kZWarps)) *
-                            ((nrows + kZRows - 1) / kZRows);
-  int per_sm = 1;
-  SFW3D_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pass_z_kernel<T, J>,
-                                                               32 * kZWarps, smem));
-  const unsigned grid = unsigned(std::min<long long>(n_tiles, (long long)std::max(per_sm, 1) * ctx->num_sms));
+  dim3 grid(unsigned((dims[2] + J * kZWarps - 1) / (J * kZWarps)),
+            unsigned((nrows + kZRows - 1) / kZRows));
   pass_z_kernel<T, J><<<grid, 32 * kZWarps, smem, ctx->stream>>>(in, out, dims[2], nrows, taps, lo,
                                                                   ntaps, pitch, addend, T(aw), T(w));
   SFW3D_LAUNCH_CHECK(ctx);
