@@ -15,6 +15,8 @@
 //    taps broadcast from shared memory;
 //  * axis 2 (contiguous): a CTA stages 32 rows x (4J + taps) in shared
 //    memory (odd pitch: lane = row, conflict-free), same rotated window.
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace sfw3d {
@@ -92,13 +94,12 @@ __global__ void __launch_bounds__(256) pass_strided_kernel(
 // rows are staged once with coalesced 256-byte row loads, so each input is
 // read ~ (4J + taps) / 4J times instead of (J + taps) / J. Lanes run over the
 // inner index: conflict-free smem, coalesced stores.
-constexpr int kTInner = 64;
-constexpr int kTGroups = 4;
 
-template <typename T, int J>
-__global__ void __launch_bounds__(256) pass_tiled_kernel(
+template <typename T, int J, int kTInner, int NT>
+__global__ void __launch_bounds__(NT) pass_tiled_kernel(
     const T* __restrict__ in, T* out, int n_axis, long long stride, const T* __restrict__ taps_g,
     int lo, int ntaps, const T* addend, T aw, T w) {
+  constexpr int kTGroups = NT / kTInner;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int npad = (ntaps + J - 1) / J * J;
   T* taps = reinterpret_cast<T*>(smem_raw);
@@ -268,9 +269,10 @@ int launch_strided(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int a
   return SFW3D_OK;
 }
 
-template <typename T, int J>
+template <typename T, int J, int kTInner, int NT>
 int launch_tiled(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis, const T* taps,
                  int lo, int ntaps, const T* addend, double aw, double w) {
+  constexpr int kTGroups = NT / kTInner;
   long long stride = 1;
   for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
   long long outer = 1;
@@ -280,11 +282,11 @@ int launch_tiled(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axi
   const int npad = (ntaps + J - 1) / J * J;
   const size_t smem = (size_t(npad) + size_t(To + npad) * kTInner) * sizeof(T);
   if (smem > 48 * 1024)
-    SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_tiled_kernel<T, J>,
+    SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_tiled_kernel<T, J, kTInner, NT>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   dim3 grid(unsigned((n + To - 1) / To), unsigned(stride / kTInner), unsigned(outer));
-  pass_tiled_kernel<T, J><<<grid, 256, smem, ctx->stream>>>(in, out, n, stride, taps, lo, ntaps,
-                                                              addend, T(aw), T(w));
+  pass_tiled_kernel<T, J, kTInner, NT><<<grid, NT, smem, ctx->stream>>>(
+      in, out, n, stride, taps, lo, ntaps, addend, T(aw), T(w));
   SFW3D_LAUNCH_CHECK(ctx);
   return SFW3D_OK;
 }
@@ -321,8 +323,34 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
                 : launch_z<T, 16>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
   long long stride = 1;
   for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
-  if (stride % kTInner == 0 && ntaps <= 512)
-    return launch_tiled<T, 16>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
+  // tile shape variants (SFW3D_PASS_VARIANT, for tuning; default 0)
+  static const int variant = [] {
+    const char* e = getenv("SFW3D_PASS_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  if (ntaps <= 512) {
+    switch (variant) {
+      case 1:
+        if (stride % 128 == 0)
+          return launch_tiled<T, 16, 128, 512>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
+        break;
+      case 2:
+        if (stride % 256 == 0)
+          return launch_tiled<T, 16, 256, 256>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
+        break;
+      case 3:
+        if (stride % 64 == 0)
+          return launch_tiled<T, 32, 64, 256>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
+        break;
+      case 4:
+        if (stride % 128 == 0)
+          return launch_tiled<T, 32, 128, 256>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
+        break;
+      default:
+        if (stride % 64 == 0)
+          return launch_tiled<T, 16, 64, 256>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
+    }
+  }
   return wide ? launch_strided<T, 32>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w)
               : launch_strided<T, 8>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
 }
