@@ -265,13 +265,14 @@ def cert_workload(args, rank, world, dev):
     nvox = int(np.prod(dims))
     rooflines = {}
     if fam["eta_direct"][1]:
-        flops = 2.0 * info["direct_taps_per_voxel"] * win_vox
+        flops = info["direct_flops_per_voxel"] * win_vox  # executed FP32 ops (FMA = 2)
         achieved = flops / (fam["eta_direct"][0] / 1e3) / 1e12
         rooflines["eta_direct"] = {
-            "bound": "fp32", "kernel": "eta_direct_kernel", "achieved": achieved,
+            "bound": "fp32", "kernel": "eta_sym_kernel / eta_direct_kernel", "achieved": achieved,
             "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": None,
             "peak_source": "measured FFMA probe (sfw3d_probe_fp32) on this device",
-            "flops_per_voxel": 2.0 * info["direct_taps_per_voxel"],
+            "flops_per_voxel": info["direct_flops_per_voxel"],
+            "reference_box_taps_per_voxel": info["direct_taps_per_voxel"],
             "launches": fam["eta_direct"][1],
             "avg_launch_ms": fam["eta_direct"][0] / fam["eta_direct"][1],
             "share_of_step": fam["eta_direct"][0] / step_ms if step_ms else None}
@@ -280,7 +281,7 @@ def cert_workload(args, rank, world, dev):
         n_terms = n_pass // 3
         # per pass: read in + write out (fp32); the x pass also reads its addend
         nbytes = 4.0 * nvox * (2 * n_pass + n_terms)
-        flops = 2.0 * info["basis_taps_per_voxel"] * nvox
+        flops = info["basis_flops_per_voxel"] * nvox
         t = fam["eta_basis"][0] / 1e3
         gbs, tfl = nbytes / t / 1e9, flops / t / 1e12
         rooflines["eta_basis"] = {

@@ -144,10 +144,12 @@ int sfw3d_table_create(sfw3d_ctx* ctx, const sfw3d_psf* psf, int n_sigma,
                        const double* sigma_host, int n_shape, const double* shape_host,
                        double tap_tol, int mode, double basis_tol, sfw3d_table** out);
 /* Evaluator split for a storage dtype: candidates on the direct path and on
- * the separable basis, and the taps per output voxel each path executes
- * (summed over its candidates) — the FLOP counts of the roofline. */
+ * the separable basis, the taps per output voxel each path's table holds,
+ * and the FP32/FP64 flops per output voxel each path EXECUTES (summed over
+ * its candidates; FMA = 2, add = 1) — the FLOP counts of the roofline. */
 int sfw3d_table_info(const sfw3d_table* t, int dtype, int* n_cand, int* n_direct, int* n_basis,
-                     int64_t* direct_taps, int64_t* basis_taps);
+                     int64_t* direct_taps, int64_t* basis_taps, double* direct_flops,
+                     double* basis_flops);
 /* Host-only (no device work): the separable-basis fit the table uses for a
  * (sigma, d) candidate on the offset box [lo, hi]: g(s) ~ w0 [s == 0] +
  * sum_k weights[k] exp(-betas[k] s) with non-negative weights; writes up to
@@ -160,7 +162,7 @@ int sfw3d_basis_fit(const int32_t lo[3], const int32_t hi[3], double sigma, doub
  * the lattice of the support box, and both tap counts. */
 int sfw3d_table_candidate(const sfw3d_table* t, int dtype, int cand, int* uses_basis,
                           int* n_terms, double* fit_err, int64_t* direct_taps,
-                          int64_t* basis_taps);
+                          int64_t* basis_taps, double* flops);
 int sfw3d_table_destroy(sfw3d_table* t);
 
 /* K1 — eta_field (certificate.py:140-184): eta_c(m) = <H*G_c(.-m), r>/lam

@@ -62,9 +62,9 @@ _SIGNATURES = {
     "sfw3d_table_create": (C.c_int, [_vp, _vp, C.c_int, _dp, C.c_int, _dp, C.c_double, C.c_int,
                                      C.c_double, C.POINTER(_vp)]),
     "sfw3d_table_info": (C.c_int, [_vp, C.c_int, _ip, _ip, _ip, C.POINTER(C.c_int64),
-                                   C.POINTER(C.c_int64)]),
+                                   C.POINTER(C.c_int64), _dp, _dp]),
     "sfw3d_table_candidate": (C.c_int, [_vp, C.c_int, C.c_int, _ip, _ip, _dp, C.POINTER(C.c_int64),
-                                        C.POINTER(C.c_int64)]),
+                                        C.POINTER(C.c_int64), _dp]),
     "sfw3d_table_destroy": (C.c_int, [_vp]),
     "sfw3d_eta_argmax": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_double, _i32p, C.POINTER(Argmax),
                                    C.POINTER(Argmax), _vp]),

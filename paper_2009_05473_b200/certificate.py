@@ -87,20 +87,24 @@ class AtomTemplateTable:
         h = self.native(N.device_index(device))
         nc, nd, nb = C.c_int(), C.c_int(), C.c_int()
         dt, bt = C.c_int64(), C.c_int64()
+        df, bf = C.c_double(), C.c_double()
         N.check(N.lib().sfw3d_table_info(h, code, C.byref(nc), C.byref(nd), C.byref(nb),
-                                         C.byref(dt), C.byref(bt)))
+                                         C.byref(dt), C.byref(bt), C.byref(df), C.byref(bf)))
         cands = []
         for i in range(nc.value):
-            ub, nt, fe = C.c_int(), C.c_int(), C.c_double()
+            ub, nt, fe, fl = C.c_int(), C.c_int(), C.c_double(), C.c_double()
             cdt, cbt = C.c_int64(), C.c_int64()
             N.check(N.lib().sfw3d_table_candidate(h, code, i, C.byref(ub), C.byref(nt),
-                                                  C.byref(fe), C.byref(cdt), C.byref(cbt)))
+                                                  C.byref(fe), C.byref(cdt), C.byref(cbt),
+                                                  C.byref(fl)))
             s, d = divmod(i, len(self.shape_grid))
             cands.append({"sigma": float(self.sigma_grid[s]), "d": float(self.shape_grid[d]),
                           "path": "basis" if ub.value else "direct", "terms": nt.value,
-                          "fit_err": fe.value, "direct_taps": cdt.value, "basis_taps": cbt.value})
+                          "fit_err": fe.value, "direct_taps": cdt.value, "basis_taps": cbt.value,
+                          "flops_per_voxel": fl.value})
         return {"n_cand": nc.value, "n_direct": nd.value, "n_basis": nb.value,
                 "direct_taps_per_voxel": dt.value, "basis_taps_per_voxel": bt.value,
+                "direct_flops_per_voxel": df.value, "basis_flops_per_voxel": bf.value,
                 "candidates": cands}
 
     @property

@@ -62,6 +62,7 @@ struct CandHost {
   double w0 = 0.0;         // delta weight
   std::vector<Term> terms;
   long long basis_taps = 0;  // per output voxel
+  double fold_flops = 0.0;   // FP32 flops per voxel of the folded direct kernel
 };
 
 }  // namespace sfw3d
@@ -76,6 +77,7 @@ struct sfw3d_table {
   int device;
   int mode;      // 0 auto, 1 direct only
   double basis_tol;
+  int smem_max;  // opt-in shared memory per block of the device
 };
 
 namespace sfw3d {
@@ -817,6 +819,19 @@ static int build_candidate(const int dims[3], double sigma, double d, double tap
       }
     }
   }
+  // executed flops of the folded kernel (eta_sym_kernel): per (a >= 0, b >= 0)
+  // tap row, 4 FMA per step and (NR - 1) window sums per 4 columns, where NR
+  // rows (+-a, +-b) share the row; each thread owns 16 outputs
+  if (c.lo[0] == -c.hi[0] && c.lo[1] == -c.hi[1]) {
+    const int Ra = c.hi[0], Rb = c.hi[1];
+    for (int a = 0; a <= Ra; ++a)
+      for (int b = 0; b <= Rb; ++b) {
+        const int2 rr = c.rows[size_t(a + Ra) * c.lb + (b + Rb)];
+        if (rr.y <= 0) continue;
+        const int nr = (a ? 2 : 1) * (b ? 2 : 1);
+        c.fold_flops += 2.0 * 4.0 * rr.y + double(nr - 1) * (4.0 * rr.y + 20.0) / 16.0;
+      }
+  }
   std::vector<float> t32(t.begin(), t.end());
   SFW3D_TRY(upload(reinterpret_cast<void**>(&c.t64), t.data(), t.size() * sizeof(double)));
   SFW3D_TRY(upload(reinterpret_cast<void**>(&c.t32), t32.data(), t32.size() * sizeof(float)));
@@ -830,6 +845,18 @@ static bool use_basis(const sfw3d_table* t, const CandHost& c, int dtype) {
   if (t->mode == 1 || c.terms.empty()) return false;
   if (c.exact_sep) return true;
   return dtype == SFW3D_F32 && c.fit_err <= t->basis_tol && c.basis_taps < c.taps;
+}
+
+static bool use_sym(const sfw3d_table* t, const CandHost& c, int dtype) {
+  const int esize = dtype == SFW3D_F64 ? 8 : 4;
+  const bool sym = c.lo[0] == -c.hi[0] && c.lo[1] == -c.hi[1];
+  const int smem_sym = 2 * (kTY + c.lb - 1) * region_pitch(c.lc4, esize) * esize;
+  return sym && smem_sym <= std::min(t->smem_max - 2048, 160 * 1024);
+}
+
+static double cand_flops(const sfw3d_table* t, const CandHost& c, int dtype) {
+  if (use_basis(t, c, dtype)) return 2.0 * double(c.basis_taps) + 2.0 * double(c.terms.size());
+  return use_sym(t, c, dtype) ? c.fold_flops : 2.0 * double(c.taps);
 }
 
 }  // namespace sfw3d
@@ -896,6 +923,8 @@ extern "C" int sfw3d_table_create(sfw3d_ctx* ctx, const sfw3d_psf* psf, int n_si
   t->device = ctx->device;
   t->mode = mode;
   t->basis_tol = basis_tol;
+  t->smem_max = 48 * 1024;
+  cudaDeviceGetAttribute(&t->smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
   t->cands.resize(size_t(n_sigma) * n_shape);
   int maxlo[3] = {0, 0, 0}, maxhi[3] = {0, 0, 0}, maxpitch = 0;
   for (int i = 0; i < n_sigma; ++i)
@@ -926,16 +955,20 @@ extern "C" int sfw3d_table_create(sfw3d_ctx* ctx, const sfw3d_psf* psf, int n_si
 }
 
 extern "C" int sfw3d_table_info(const sfw3d_table* t, int dtype, int* n_cand, int* n_direct,
-                                int* n_basis, int64_t* direct_taps, int64_t* basis_taps) {
+                                int* n_basis, int64_t* direct_taps, int64_t* basis_taps,
+                                double* direct_flops, double* basis_flops) {
   SFW3D_CHECK_ARG(t, "table is NULL");
   int nb = 0;
   long long dt = 0, bt = 0;
+  double df = 0.0, bf = 0.0;
   for (const auto& c : t->cands) {
     if (use_basis(t, c, dtype)) {
       ++nb;
       bt += c.basis_taps;
+      bf += cand_flops(t, c, dtype);
     } else {
       dt += c.taps;
+      df += cand_flops(t, c, dtype);
     }
   }
   if (n_cand) *n_cand = int(t->cands.size());
@@ -943,12 +976,14 @@ extern "C" int sfw3d_table_info(const sfw3d_table* t, int dtype, int* n_cand, in
   if (n_basis) *n_basis = nb;
   if (direct_taps) *direct_taps = dt;
   if (basis_taps) *basis_taps = bt;
+  if (direct_flops) *direct_flops = df;
+  if (basis_flops) *basis_flops = bf;
   return SFW3D_OK;
 }
 
 extern "C" int sfw3d_table_candidate(const sfw3d_table* t, int dtype, int cand, int* uses_basis,
                                      int* n_terms, double* fit_err, int64_t* direct_taps,
-                                     int64_t* basis_taps) {
+                                     int64_t* basis_taps, double* flops) {
   SFW3D_CHECK_ARG(t && cand >= 0 && cand < int(t->cands.size()), "candidate index");
   const CandHost& c = t->cands[cand];
   if (uses_basis) *uses_basis = use_basis(t, c, dtype) ? 1 : 0;
@@ -956,6 +991,7 @@ extern "C" int sfw3d_table_candidate(const sfw3d_table* t, int dtype, int cand, 
   if (fit_err) *fit_err = c.fit_err;
   if (direct_taps) *direct_taps = c.taps;
   if (basis_taps) *basis_taps = c.basis_taps;
+  if (flops) *flops = cand_flops(t, c, dtype);
   return SFW3D_OK;
 }
 
@@ -1063,9 +1099,8 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
       gc.pitch = region_pitch(c.lc4, sizeof(T));
       const int row_bytes = gc.pitch * int(sizeof(T));
       dim3 grid(unsigned(nty * ntz), unsigned(nxp));
-      const bool sym = c.lo[0] == -c.hi[0] && c.lo[1] == -c.hi[1];
       const int smem_sym = 2 * (kTY + c.lb - 1) * row_bytes;
-      if (sym && smem_sym <= std::min(smem_max - 2048, 160 * 1024)) {
+      if (use_sym(t, c, dtype)) {
         gc.brows = c.lb;
         SFW3D_CUDA_TRY(cudaFuncSetAttribute(eta_sym_kernel<T>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem_sym));
