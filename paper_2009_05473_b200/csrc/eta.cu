@@ -202,9 +202,9 @@ __global__ void __launch_bounds__(kThreads) eta_direct_kernel(const T* __restric
   const int z0 = g.zbase + tz * kTZ;
   const T* taps = static_cast<const T*>(cd.taps);
 
-  double accd[kJ];
+  T accd[kJ];  // slice partials summed in the storage precision (fp32 error << 1e-5 bar)
 #pragma unroll
-  for (int j = 0; j < kJ; ++j) accd[j] = 0.0;
+  for (int j = 0; j < kJ; ++j) accd[j] = T(0);
 
   for (int ai = 0; ai < cd.la; ++ai) {
     const int a = cd.lo_a + ai;
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kThreads) eta_direct_kernel(const T* __restric
         if (rem > 3) tap_step<T, 3>(acc, buf, tc, trow + 4 * s + 16, srow + 4 * s + 12);
       }
 #pragma unroll
-      for (int j = 0; j < kJ; ++j) accd[j] += double(acc[j]);
+      for (int j = 0; j < kJ; ++j) accd[j] += acc[j];
     }
   }
 
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(kThreads) eta_direct_kernel(const T* __restric
   for (int j = 0; j < kJ; ++j) {
     const int z = z0 + warp * kJ + j;
     if (!row_ok || z >= g.nz) continue;
-    const double eta = accd[j] / g.lam;
+    const double eta = double(accd[j]) / g.lam;
     const long long lin = ((long long)x * g.ny + y) * g.nz + z;
     if (field) field[lin] = T(eta);
     if (row_win && z >= g.win[4] && z <= g.win[5] && better(eta, lin, best.v, best.idx))
@@ -381,9 +381,9 @@ __global__ void __launch_bounds__(kThreads) eta_sym_kernel(const T* __restrict__
   const T* taps = static_cast<const T*>(cd.taps);
   const int Ra = cd.la / 2, Rb = cd.lb / 2;  // symmetric boxes: lo = -R
 
-  double accd[kJ];
+  T accd[kJ];  // slice partials summed in the storage precision (fp32 error << 1e-5 bar)
 #pragma unroll
-  for (int j = 0; j < kJ; ++j) accd[j] = 0.0;
+  for (int j = 0; j < kJ; ++j) accd[j] = T(0);
 
   for (int a = 0; a <= Ra; ++a) {
     const int ai = a + Ra;  // template slice index of +a (same taps as -a)
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(kThreads) eta_sym_kernel(const T* __restrict__
       }
     }
 #pragma unroll
-    for (int j = 0; j < kJ; ++j) accd[j] += double(acc[j]);
+    for (int j = 0; j < kJ; ++j) accd[j] += acc[j];
   }
 
   const int y = y0 + lane;
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(kThreads) eta_sym_kernel(const T* __restrict__
   for (int j = 0; j < kJ; ++j) {
     const int z = z0 + warp * kJ + j;
     if (!row_ok || z >= g.nz) continue;
-    const double eta = accd[j] / g.lam;
+    const double eta = double(accd[j]) / g.lam;
     const long long lin = ((long long)x * g.ny + y) * g.nz + z;
     if (field) field[lin] = T(eta);
     if (row_win && z >= g.win[4] && z <= g.win[5] && better(eta, lin, best.v, best.idx))
