@@ -56,13 +56,17 @@ struct CandHost {
   double* t64 = nullptr;
   float* t32 = nullptr;
   int2* rows_dev = nullptr;
-  // basis
-  bool exact_sep = false;  // d == 2: one exact term
-  double fit_err = INFINITY;
-  double w0 = 0.0;         // delta weight
-  std::vector<Term> terms;
-  long long basis_taps = 0;  // per output voxel
-  double fold_flops = 0.0;   // FP32 flops per voxel of the folded direct kernel
+  // separable bases: one fitted for fp32 storage (stop at 1e-10) and one for
+  // fp64 storage (stop at 1e-13); identical and exact for d == 2
+  struct Basis {
+    bool exact = false;     // d == 2: one exact term
+    double fit_err = INFINITY;
+    double w0 = 0.0;        // delta weight
+    std::vector<Term> terms;
+    long long taps = 0;     // per output voxel
+  } b32, b64;
+  double fold_flops = 0.0;  // FP32 flops per voxel of the folded direct kernel
+  const Basis& basis(int dtype) const { return dtype == SFW3D_F64 ? b64 : b32; }
 };
 
 }  // namespace sfw3d
@@ -657,8 +661,9 @@ static int upload(void** dst, const void* src, size_t bytes) {
 // Fits g(s) = exp(-s^(d/2) / (2 sigma^d)) on the lattice values s = a^2 + b^2
 // + c^2 of the offset box [lo, hi] by w0 * [s == 0] + sum_k w_k exp(-beta_k s)
 // (non-negative weights, 48 geometric beta_k). Host-only.
-static void fit_profile(const int lo[3], const int hi[3], double sigma, double d, double& w0,
-                        std::vector<std::pair<double, double>>& terms, double& err, bool& exact) {
+static void fit_profile(const int lo[3], const int hi[3], double sigma, double d, double target,
+                        double& w0, std::vector<std::pair<double, double>>& terms, double& err,
+                        bool& exact) {
   const double inv2sd = 0.5 / std::pow(sigma, d);
   terms.clear();
   if (d == 2.0) {  // exp(-inv2sd * (a^2 + b^2 + c^2)) = product of three 1-D Gaussians
@@ -729,15 +734,13 @@ static void fit_profile(const int lo[3], const int hi[3], double sigma, double d
       for (int k = 0; k < K; ++k)
         if (x[k] > 0.0) terms.push_back({betas[k], x[k]});
     }
-    if (err <= 1e-10) break;
+    if (err <= target) break;
   }
 }
 
-static int fit_basis(CandHost& c) {
-  const int l[3] = {c.hi[0] - c.lo[0] + 1, c.hi[1] - c.lo[1] + 1, c.hi[2] - c.lo[2] + 1};
+static int fit_basis(CandHost& c, CandHost::Basis& B, double target) {
   std::vector<std::pair<double, double>> bw;
-  fit_profile(c.lo, c.hi, c.sigma, c.d, c.w0, bw, c.fit_err, c.exact_sep);
-  (void)l;
+  fit_profile(c.lo, c.hi, c.sigma, c.d, target, B.w0, bw, B.fit_err, B.exact);
   double wsum = 0.0;
   for (auto& p : bw) wsum += p.second;
   // A term's 1-D factor exp(-beta t^2) is dropped where it is below
@@ -748,16 +751,16 @@ static int fit_basis(CandHost& c) {
     Term t{};
     t.beta = p.first;
     t.w = p.second;
-    const int r = c.exact_sep ? (1 << 29) : int(std::ceil(std::sqrt(std::log(1.0 / eps) / t.beta)));
+    const int r = B.exact ? (1 << 29) : int(std::ceil(std::sqrt(std::log(1.0 / eps) / t.beta)));
     for (int ax = 0; ax < 3; ++ax) {
       t.tlo[ax] = std::max(c.lo[ax], -r);
       t.tlen[ax] = std::min(c.hi[ax], r) - t.tlo[ax] + 1;
     }
-    c.terms.push_back(t);
+    B.terms.push_back(t);
   }
-  if (!c.exact_sep) c.fit_err += 1e-12;
-  c.basis_taps = (c.w0 != 0.0 ? 1 : 0);
-  for (auto& t : c.terms) {
+  if (!B.exact) B.fit_err += 1e-12;
+  B.taps = (B.w0 != 0.0 ? 1 : 0);
+  for (auto& t : B.terms) {
     std::vector<double> h64;
     for (int ax = 0; ax < 3; ++ax)
       for (int q = t.tlo[ax]; q < t.tlo[ax] + t.tlen[ax]; ++q)
@@ -765,7 +768,7 @@ static int fit_basis(CandHost& c) {
     std::vector<float> h32(h64.begin(), h64.end());
     SFW3D_TRY(upload(&t.taps64, h64.data(), h64.size() * sizeof(double)));
     SFW3D_TRY(upload(&t.taps32, h32.data(), h32.size() * sizeof(float)));
-    c.basis_taps += t.tlen[0] + t.tlen[1] + t.tlen[2];
+    B.taps += t.tlen[0] + t.tlen[1] + t.tlen[2];
   }
   return SFW3D_OK;
 }
@@ -836,15 +839,23 @@ static int build_candidate(const int dims[3], double sigma, double d, double tap
   SFW3D_TRY(upload(reinterpret_cast<void**>(&c.t64), t.data(), t.size() * sizeof(double)));
   SFW3D_TRY(upload(reinterpret_cast<void**>(&c.t32), t32.data(), t32.size() * sizeof(float)));
   SFW3D_TRY(upload(reinterpret_cast<void**>(&c.rows_dev), c.rows.data(), c.rows.size() * sizeof(int2)));
-  if (basis) SFW3D_TRY(fit_basis(c));
+  if (basis) {
+    SFW3D_TRY(fit_basis(c, c.b32, 1e-10));
+    SFW3D_TRY(fit_basis(c, c.b64, 1e-13));
+  }
   return SFW3D_OK;
 }
 
+// fp64 storage (reference-parity configs) accepts a basis only this close
+constexpr double kBasisTol64 = 1e-12;
+
 // evaluator choice per candidate and storage type
 static bool use_basis(const sfw3d_table* t, const CandHost& c, int dtype) {
-  if (t->mode == 1 || c.terms.empty()) return false;
-  if (c.exact_sep) return true;
-  return dtype == SFW3D_F32 && c.fit_err <= t->basis_tol && c.basis_taps < c.taps;
+  const CandHost::Basis& B = c.basis(dtype);
+  if (t->mode == 1 || B.terms.empty()) return false;
+  if (B.exact) return true;
+  const double tol = dtype == SFW3D_F64 ? std::min(t->basis_tol, kBasisTol64) : t->basis_tol;
+  return B.fit_err <= tol && B.taps < c.taps;
 }
 
 static bool use_sym(const sfw3d_table* t, const CandHost& c, int dtype) {
@@ -855,7 +866,8 @@ static bool use_sym(const sfw3d_table* t, const CandHost& c, int dtype) {
 }
 
 static double cand_flops(const sfw3d_table* t, const CandHost& c, int dtype) {
-  if (use_basis(t, c, dtype)) return 2.0 * double(c.basis_taps) + 2.0 * double(c.terms.size());
+  if (use_basis(t, c, dtype))
+    return 2.0 * double(c.basis(dtype).taps) + 2.0 * double(c.basis(dtype).terms.size());
   return use_sym(t, c, dtype) ? c.fold_flops : 2.0 * double(c.taps);
 }
 
@@ -876,7 +888,7 @@ extern "C" int sfw3d_basis_fit(const int32_t lo[3], const int32_t hi[3], double 
   }
   std::vector<std::pair<double, double>> bw;
   bool exact = false;
-  fit_profile(l, h, sigma, d, *w0, bw, *fit_err, exact);
+  fit_profile(l, h, sigma, d, 1e-10, *w0, bw, *fit_err, exact);
   *n_terms = int(bw.size());
   for (int k = 0; k < int(bw.size()) && k < max_terms; ++k) {
     if (betas) betas[k] = bw[k].first;
@@ -892,10 +904,11 @@ extern "C" int sfw3d_table_destroy(sfw3d_table* t) {
     if (c.t64) cudaFree(c.t64);
     if (c.t32) cudaFree(c.t32);
     if (c.rows_dev) cudaFree(c.rows_dev);
-    for (auto& term : c.terms) {
-      if (term.taps64) cudaFree(term.taps64);
-      if (term.taps32) cudaFree(term.taps32);
-    }
+    for (auto* B : {&c.b32, &c.b64})
+      for (auto& term : B->terms) {
+        if (term.taps64) cudaFree(term.taps64);
+        if (term.taps32) cudaFree(term.taps32);
+      }
   }
   delete t;
   return SFW3D_OK;
@@ -964,7 +977,7 @@ extern "C" int sfw3d_table_info(const sfw3d_table* t, int dtype, int* n_cand, in
   for (const auto& c : t->cands) {
     if (use_basis(t, c, dtype)) {
       ++nb;
-      bt += c.basis_taps;
+      bt += c.basis(dtype).taps;
       bf += cand_flops(t, c, dtype);
     } else {
       dt += c.taps;
@@ -987,10 +1000,11 @@ extern "C" int sfw3d_table_candidate(const sfw3d_table* t, int dtype, int cand, 
   SFW3D_CHECK_ARG(t && cand >= 0 && cand < int(t->cands.size()), "candidate index");
   const CandHost& c = t->cands[cand];
   if (uses_basis) *uses_basis = use_basis(t, c, dtype) ? 1 : 0;
-  if (n_terms) *n_terms = int(c.terms.size()) + (c.w0 != 0.0 ? 1 : 0);
-  if (fit_err) *fit_err = c.fit_err;
+  const CandHost::Basis& B = c.basis(dtype);
+  if (n_terms) *n_terms = int(B.terms.size()) + (B.w0 != 0.0 ? 1 : 0);
+  if (fit_err) *fit_err = B.fit_err;
   if (direct_taps) *direct_taps = c.taps;
-  if (basis_taps) *basis_taps = c.basis_taps;
+  if (basis_taps) *basis_taps = B.taps;
   if (flops) *flops = cand_flops(t, c, dtype);
   return SFW3D_OK;
 }
@@ -1065,17 +1079,18 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
     long long nred = 0;
     if (use_basis(t, c, dtype)) {
       // acc = w0 * b + sum_k w_k (f_k x f_k x f_k) * b   (separable passes)
-      for (size_t k = 0; k < c.terms.size(); ++k) {
-        const Term& term = c.terms[k];
+      const CandHost::Basis& B = c.basis(dtype);
+      for (size_t k = 0; k < B.terms.size(); ++k) {
+        const Term& term = B.terms[k];
         const T* taps = static_cast<const T*>(dtype == SFW3D_F64 ? term.taps64 : term.taps32);
         const int* tl = term.tlen;
         SFW3D_TRY(corr_pass_impl(ctx, dtype, b, tmp, dims, 2, taps + tl[0] + tl[1], term.tlo[2],
                                  tl[2], nullptr, 0.0, 1.0, "eta_basis"));
         SFW3D_TRY(corr_pass_impl(ctx, dtype, tmp, t2, dims, 1, taps + tl[0], term.tlo[1], tl[1],
                                  nullptr, 0.0, 1.0, "eta_basis"));
-        const void* addend = k == 0 ? (c.w0 != 0.0 ? static_cast<const void*>(b) : nullptr)
+        const void* addend = k == 0 ? (B.w0 != 0.0 ? static_cast<const void*>(b) : nullptr)
                                     : static_cast<const void*>(acc);
-        const double aw = k == 0 ? c.w0 : 1.0;
+        const double aw = k == 0 ? B.w0 : 1.0;
         SFW3D_TRY(corr_pass_impl(ctx, dtype, t2, acc, dims, 0, taps, term.tlo[0], tl[0], addend,
                                  aw, term.w, "eta_basis"));
       }

@@ -48,7 +48,34 @@ def test_table_fits(P):
     with P.precision("f64"):
         info64 = table.info()
     for c in info64["candidates"]:
-        assert c["path"] == ("basis" if c["d"] == 2.0 else "direct")
+        if c["d"] == 2.0:
+            assert c["path"] == "basis" and c["fit_err"] == 0.0
+        elif c["d"] > 2.0:
+            assert c["path"] == "direct"
+        else:  # fp64 storage accepts the (tighter) fp64 fit only below 1e-12
+            assert (c["path"] == "basis") == (c["fit_err"] <= 1e-12)
+
+
+def test_eta_config2_f64_vs_oracle(P):
+    """BASELINE config 2 geometry: 128^3 f64, anisotropic 17x17x33 PSF, 6 x 5
+    candidates incl. d = 1.2 (full-axis boxes, R up to 85) — fp64 storage with
+    the fp64 basis / direct split, against the FFT oracle."""
+    rng = np.random.default_rng(12)
+    dims = (128, 128, 128)
+    kernel = O.box_gaussian_psf(dims, (1.5, 1.5, 4.0), (8, 8, 16))
+    rows = np.column_stack([rng.uniform(0.5, 2, 20), rng.uniform(9, 118, (20, 3)),
+                            rng.uniform(1, 3, 20), rng.uniform(1.2, 2.8, 20)])
+    y = O.conv(O.render(rows, dims), O.psf_hat(kernel)) + 0.05 * rng.standard_normal(dims)
+    sg, dg = np.geomspace(1, 3, 6), np.linspace(1.2, 2.8, 5)
+    hats = O.template_hats(O.psf_hat(kernel), dims, sg, dg)
+    win = ((9, 118), (9, 118), (9, 118))
+    pos, flat, val, per, _ = O.eta_field(y, 0.7, hats, 5, win)
+    psf = P.Psf(P.Volume(kernel), normalize=False)
+    table = P.build_template_table(psf, sg, dg)
+    bounds = P.DomainBounds((9.0,) * 3, (118.0,) * 3, 1.0, 3.0, 1.2, 2.8)
+    f = P.eta_field(P.Volume(y), 0.7, table, bounds=bounds, keep_fields=False)
+    assert abs(f.eta_max - val) <= 1e-9 * abs(val)
+    assert f.argmax_position == pos and f.argmax_sigma_index * 5 + f.argmax_shape_index == flat
 
 
 @pytest.mark.parametrize("n", [64, 80])
