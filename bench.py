@@ -255,7 +255,8 @@ def cert_workload(args, rank, world, dev):
     # roofline of the dominant kernel: one profiled step
     ctx.profile(True)
     step()
-    fam = {f: ctx.profile_read(f) for f in ("eta_direct", "eta_basis", "psf_pass", "pad", "argmax")}
+    fam = {f: ctx.profile_read(f) for f in ("eta_direct", "eta_basis", "eta_mix", "psf_pass", "pad",
+                                           "argmax")}
     ctx.profile(False)
     step_ms = sum(v[0] for v in fam.values())
     dom = max(fam, key=lambda f: fam[f][0])
@@ -279,22 +280,35 @@ def cert_workload(args, rank, world, dev):
     if fam["eta_basis"][1]:
         n_pass = fam["eta_basis"][1]
         n_terms = n_pass // 3
-        # per pass: read in + write out (fp32); the x pass also reads its addend
-        nbytes = 4.0 * nvox * (2 * n_pass + n_terms)
-        flops = info["basis_flops_per_voxel"] * nvox
+        # per pass: read in + write out (fp32), one z/y/x triple per shared term
+        nbytes = 4.0 * nvox * 2 * n_pass
+        flops = 2.0 * info["basis_taps_per_voxel"] * nvox
         t = fam["eta_basis"][0] / 1e3
         gbs, tfl = nbytes / t / 1e9, flops / t / 1e12
+        hbm = gbs / hbm_peak > tfl / fp32_peak
         rooflines["eta_basis"] = {
-            "bound": "hbm" if gbs / hbm_peak > tfl / fp32_peak else "fp32",
-            "kernel": "pass_strided_kernel / pass_z_kernel (separable basis terms)",
-            "achieved": gbs if gbs / hbm_peak > tfl / fp32_peak else tfl,
-            "peak": hbm_peak if gbs / hbm_peak > tfl / fp32_peak else fp32_peak,
-            "unit": "GB/s" if gbs / hbm_peak > tfl / fp32_peak else "TFLOP/s",
+            "bound": "hbm" if hbm else "fp32",
+            "kernel": "pass_tiled_kernel / pass_z_kernel (shared separable basis terms)",
+            "achieved": gbs if hbm else tfl, "peak": hbm_peak if hbm else fp32_peak,
+            "unit": "GB/s" if hbm else "TFLOP/s",
             "frac": max(gbs / hbm_peak, tfl / fp32_peak), "traffic": None,
             "achieved_gbs": gbs, "achieved_tflops": tfl, "hbm_peak_gbs": hbm_peak,
             "fp32_peak_tflops": fp32_peak, "bytes_per_step": nbytes, "flops_per_step": flops,
-            "launches": n_pass, "avg_launch_ms": fam["eta_basis"][0] / n_pass,
+            "shared_terms": n_terms, "launches": n_pass,
+            "avg_launch_ms": fam["eta_basis"][0] / n_pass,
             "share_of_step": fam["eta_basis"][0] / step_ms if step_ms else None}
+    if fam["eta_mix"][1]:
+        n_terms = fam["eta_basis"][1] // 3
+        # reads b and every shared term once, forms every member candidate
+        nbytes = 4.0 * nvox * (n_terms + 1)
+        t = fam["eta_mix"][0] / 1e3
+        gbs = nbytes / t / 1e9
+        rooflines["eta_mix"] = {
+            "bound": "hbm", "kernel": "mix_argmax_kernel (members x shared terms + argmax)",
+            "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
+            "traffic": None, "bytes_per_step": nbytes, "members": info["n_basis"],
+            "launches": fam["eta_mix"][1], "avg_launch_ms": fam["eta_mix"][0] / fam["eta_mix"][1],
+            "share_of_step": fam["eta_mix"][0] / step_ms if step_ms else None}
     roof = None
     if rooflines:
         dom_fam = max(rooflines, key=lambda f: fam[f][0])

@@ -157,9 +157,24 @@ int sfw3d_table_info(const sfw3d_table* t, int dtype, int* n_cand, int* n_direct
 int sfw3d_basis_fit(const int32_t lo[3], const int32_t hi[3], double sigma, double d,
                     int max_terms, double* betas, double* weights, double* w0, int* n_terms,
                     double* fit_err);
-/* One candidate (flat sigma-major index): evaluator used for `dtype`, basis
- * term count (incl. the delta term), the basis fit's max absolute error on
- * the lattice of the support box, and both tap counts. */
+/* Host-only (no device work): the SHARED separable basis a table builds for
+ * the candidate grid sigma x shape (sigma-major) at storage `dtype` with
+ * acceptance tolerance `tol` (the table uses basis_tol for SFW3D_F32 and
+ * min(basis_tol, 1e-12) for SFW3D_F64). Every d <= 2 candidate is fitted on one
+ * dictionary over the union of the candidates' support boxes:
+ * g_c(s) ~ w0[c] [s == 0] + sum_t weights[c*max_terms + t] exp(-betas[t] s).
+ * Writes the shared term count, up to max_terms betas, the member rows of
+ * weights (zero rows elsewhere), w0, fit_err (max abs error on the common
+ * box's lattice incl. the 1e-12 factor truncation; +inf for d > 2) and
+ * member (1 = certificate takes the basis path) per candidate. */
+int sfw3d_basis_set_fit(const int32_t dims[3], int n_sigma, const double* sigma_host,
+                        int n_shape, const double* shape_host, int dtype, double tol,
+                        int max_terms, int* n_terms, double* betas, double* weights, double* w0,
+                        double* fit_err, int32_t* member);
+/* One candidate (flat sigma-major index): evaluator used for `dtype`, the
+ * table's SHARED basis term count, the candidate's shared-basis fit error
+ * (max abs on the common box lattice, +inf when not fitted), its direct tap
+ * count, the shared basis taps per voxel, and its executed flops per voxel. */
 int sfw3d_table_candidate(const sfw3d_table* t, int dtype, int cand, int* uses_basis,
                           int* n_terms, double* fit_err, int64_t* direct_taps,
                           int64_t* basis_taps, double* flops);

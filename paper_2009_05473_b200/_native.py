@@ -31,7 +31,7 @@ EXPORTS = (
     "sfw3d_atom_sums", "sfw3d_cost_grad", "sfw3d_table_create", "sfw3d_table_info",
     "sfw3d_table_destroy", "sfw3d_eta_argmax", "sfw3d_dots", "sfw3d_nnlasso_cd",
     "sfw3d_residual", "sfw3d_ctx_profile", "sfw3d_ctx_profile_read", "sfw3d_probe_fp32",
-    "sfw3d_table_candidate", "sfw3d_basis_fit",
+    "sfw3d_table_candidate", "sfw3d_basis_fit", "sfw3d_basis_set_fit",
 )
 
 
@@ -75,6 +75,8 @@ _SIGNATURES = {
                                  _dp]),
     "sfw3d_basis_fit": (C.c_int, [_i32p, _i32p, C.c_double, C.c_double, C.c_int, _dp, _dp, _dp,
                                   _ip, _dp]),
+    "sfw3d_basis_set_fit": (C.c_int, [_ip, C.c_int, _dp, C.c_int, _dp, C.c_int, C.c_double,
+                                      C.c_int, _ip, _dp, _dp, _dp, _dp, _i32p]),
     "sfw3d_ctx_profile": (C.c_int, [_vp, C.c_int]),
     "sfw3d_ctx_profile_read": (C.c_int, [_vp, C.c_char_p, _dp, C.POINTER(C.c_int64)]),
     "sfw3d_probe_fp32": (C.c_int, [_vp, _dp]),
@@ -158,6 +160,29 @@ def basis_fit(lo, hi, sigma: float, d: float):
                                 C.byref(err)))
     k = min(nt.value, 64)
     return betas[:k], weights[:k], w0.value, err.value
+
+
+def basis_set_fit(dims, sigmas, shapes, dtype: int, tol: float, max_terms: int = 256):
+    """Host-only: the shared separable basis a table fits for the candidate
+    grid (sigma-major): dict(betas [T], weights [C, T], w0 [C], fit_err [C],
+    member [C] bool)."""
+    sg = np.ascontiguousarray(sigmas, dtype=np.float64)
+    sh = np.ascontiguousarray(shapes, dtype=np.float64)
+    nc = sg.size * sh.size
+    betas = np.zeros(max_terms)
+    weights = np.zeros((nc, max_terms))
+    w0, err = np.zeros(nc), np.zeros(nc)
+    member = np.zeros(nc, np.int32)
+    nt = C.c_int()
+    check(lib().sfw3d_basis_set_fit(dims_arg(dims), sg.size, f64_ptr(sg), sh.size, f64_ptr(sh),
+                                    int(dtype), float(tol), max_terms, C.byref(nt),
+                                    f64_ptr(betas), f64_ptr(weights), f64_ptr(w0), f64_ptr(err),
+                                    i32_ptr(member)))
+    if nt.value > max_terms:
+        raise ValueError(f"shared basis has {nt.value} terms > max_terms={max_terms}")
+    k = nt.value
+    return {"betas": betas[:k], "weights": weights[:, :k], "w0": w0, "fit_err": err,
+            "member": member.astype(bool)}
 
 
 # ------------------------------------------------------------------ devices

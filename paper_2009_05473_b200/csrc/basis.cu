@@ -1,0 +1,772 @@
+// Shared separable Gaussian basis for the dual certificate (K1 fast path).
+//
+// Every certificate candidate is a unit atom G_c(v) = g_c(|v|^2) with
+// g_c(s) = exp(-s^(d/2) / (2 sigma^d)) on the reference's support box
+// (_unit_atom, forward.py:119-137; certificate.py:86-92). For d <= 2, g_c is
+// completely monotone in s, so it is a positive mixture of Gaussians
+// exp(-beta s) — and a Gaussian of |v|^2 is separable, f(a) f(b) f(c). Here
+// all basis candidates of a table share ONE dictionary of betas (geometric
+// over the common box, plus the exact 1/(2 sigma^2) of every d == 2
+// candidate) and are fitted on it by non-negative least squares on the
+// lattice values s of the common box:
+//     G_c(v) ~ w0_c [v == 0] + sum_k W[c][k] exp(-beta_k |v|^2).
+// The certificate then costs, per voxel,
+//   * one separable pass triple per SHARED term k:  T_k = f_k^(x,y,z) * b,
+//   * one fused kernel that reads b and every T_k once and forms
+//     eta_c = (w0_c b + sum_k W[c][k] T_k) / lam for every member c, with the
+//     windowed argmax per member (and the fields when requested),
+// instead of (2R+1)^3 taps per candidate. Candidates whose fit error on the
+// common box exceeds the tolerance stay on the direct kernels (eta.cu).
+// Factors are truncated where exp(-beta t^2) < 1e-12 / max_c(sum_k W[c][k]),
+// which adds at most 1e-12 to every member's recorded error.
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <thread>
+
+#include "basis.cuh"
+
+namespace sfw3d {
+
+// ------------------------------------------------------------------ NNLS
+// Lawson-Hanson non-negative least squares min ||A x - g||, x >= 0, with the
+// passive-set subproblems solved by Householder QR in extended precision
+// (x86 long double): the exponential columns are nearly collinear.
+namespace {
+using ld = long double;
+
+void lsq_qr(const std::vector<ld>& A, int M, const std::vector<int>& cols, const std::vector<ld>& g,
+            std::vector<ld>& z) {
+  const int p = int(cols.size());
+  std::vector<ld> B(size_t(M) * p), rhs(g), scale(p), v(M);
+  for (int j = 0; j < p; ++j) {
+    ld s = 0.0L;
+    for (int i = 0; i < M; ++i) s += A[size_t(cols[j]) * M + i] * A[size_t(cols[j]) * M + i];
+    scale[j] = s > 0 ? 1.0L / std::sqrt(s) : 1.0L;
+    for (int i = 0; i < M; ++i) B[size_t(j) * M + i] = A[size_t(cols[j]) * M + i] * scale[j];
+  }
+  for (int j = 0; j < p; ++j) {
+    ld* c = &B[size_t(j) * M];
+    ld nrm = 0.0L;
+    for (int i = j; i < M; ++i) nrm += c[i] * c[i];
+    nrm = std::sqrt(nrm);
+    if (nrm == 0.0L) continue;
+    const ld alpha = c[j] > 0 ? -nrm : nrm;
+    for (int i = j; i < M; ++i) v[i] = c[i];
+    v[j] -= alpha;
+    ld vn = 0.0L;
+    for (int i = j; i < M; ++i) vn += v[i] * v[i];
+    if (vn == 0.0L) continue;
+    auto apply = [&](ld* col) {
+      ld dot = 0.0L;
+      for (int i = j; i < M; ++i) dot += v[i] * col[i];
+      const ld f = 2.0L * dot / vn;
+      for (int i = j; i < M; ++i) col[i] -= f * v[i];
+    };
+    for (int k = j; k < p; ++k) apply(&B[size_t(k) * M]);
+    apply(rhs.data());
+  }
+  z.assign(p, 0.0L);
+  for (int j = p - 1; j >= 0; --j) {
+    ld s = rhs[j];
+    for (int k = j + 1; k < p; ++k) s -= B[size_t(k) * M + j] * z[k];
+    const ld r = B[size_t(j) * M + j];
+    z[j] = r != 0.0L ? s / r : 0.0L;
+  }
+  for (int j = 0; j < p; ++j) z[j] *= scale[j];
+}
+
+void nnls(const std::vector<double>& Ad, int M, int N, const std::vector<double>& gd,
+          std::vector<double>& xd) {
+  std::vector<ld> A(Ad.begin(), Ad.end()), g(gd.begin(), gd.end()), x(N, 0.0L), r(M), cn(N);
+  std::vector<char> passive(N, 0), banned(N, 0);
+  for (int j = 0; j < N; ++j) {
+    ld s = 0.0L;
+    for (int i = 0; i < M; ++i) s += A[size_t(j) * M + i] * A[size_t(j) * M + i];
+    cn[j] = s > 0.0L ? std::sqrt(s) : 1.0L;
+  }
+  ld gn = 0.0L;
+  for (ld v : g) gn += v * v;
+  const ld tol = 1e-17L * std::sqrt(gn);
+  for (int outer = 0; outer < 8 * N; ++outer) {
+    for (int i = 0; i < M; ++i) {
+      ld s = g[i];
+      for (int j = 0; j < N; ++j)
+        if (x[j] != 0.0L) s -= A[size_t(j) * M + i] * x[j];
+      r[i] = s;
+    }
+    int jmax = -1;
+    ld best = tol;
+    for (int j = 0; j < N; ++j) {
+      if (passive[j] || banned[j]) continue;
+      ld s = 0.0L;
+      for (int i = 0; i < M; ++i) s += A[size_t(j) * M + i] * r[i];
+      s /= cn[j];
+      if (s > best) {
+        best = s;
+        jmax = j;
+      }
+    }
+    if (jmax < 0) break;
+    passive[jmax] = 1;
+    bool first = true, added = true;
+    for (int inner = 0; inner < 3 * N; ++inner) {
+      std::vector<int> cols;
+      for (int j = 0; j < N; ++j)
+        if (passive[j]) cols.push_back(j);
+      std::vector<ld> z;
+      lsq_qr(A, M, cols, g, z);
+      bool ok = true;
+      for (ld v : z) ok &= v > 0.0L;
+      if (ok) {
+        std::fill(x.begin(), x.end(), 0.0L);
+        for (size_t q = 0; q < cols.size(); ++q) x[cols[q]] = z[q];
+        break;
+      }
+      if (first) {  // the entering column itself came out non-positive: skip it
+        size_t qn = 0;
+        while (cols[qn] != jmax) ++qn;
+        if (z[qn] <= 0.0L) {
+          passive[jmax] = 0;
+          banned[jmax] = 1;
+          added = false;
+          break;
+        }
+      }
+      first = false;
+      ld alpha = 2.0L;
+      int qmin = -1;
+      for (size_t q = 0; q < cols.size(); ++q)
+        if (z[q] <= 0.0L) {
+          const ld xv = x[cols[q]];
+          const ld a = xv / (xv - z[q]);
+          if (a < alpha) {
+            alpha = a;
+            qmin = int(q);
+          }
+        }
+      for (size_t q = 0; q < cols.size(); ++q) {
+        const int j = cols[q];
+        x[j] += alpha * (z[q] - x[j]);
+        if (int(q) == qmin || x[j] <= 0.0L) {
+          x[j] = 0.0L;
+          passive[j] = 0;
+        }
+      }
+    }
+    if (added) std::fill(banned.begin(), banned.end(), 0);
+  }
+  xd.assign(x.begin(), x.end());
+}
+
+// lattice values s = a^2 + b^2 + c^2 of an offset box, and the fitting subset
+// (every s <= 256, then geometric 0.4% steps: the profile is smooth there)
+void box_lattice(const int lo[3], const int hi[3], std::vector<double>& S, std::vector<double>& Sfit) {
+  int smax = 0;
+  for (int a = 0; a < 3; ++a) smax += std::max(lo[a] * lo[a], hi[a] * hi[a]);
+  std::vector<char> present(size_t(smax) + 1, 0);
+  std::vector<int> sv[3];
+  for (int ax = 0; ax < 3; ++ax) {
+    std::vector<char> sq(size_t(smax) + 1, 0);
+    for (int t = lo[ax]; t <= hi[ax]; ++t) sq[size_t(t) * t] = 1;
+    for (int s = 0; s <= smax; ++s)
+      if (sq[s]) sv[ax].push_back(s);
+  }
+  for (int s0 : sv[0])
+    for (int s1 : sv[1])
+      for (int s2 : sv[2]) present[size_t(s0) + s1 + s2] = 1;
+  S.clear();
+  for (int s = 0; s <= smax; ++s)
+    if (present[s]) S.push_back(double(s));
+  Sfit.clear();
+  double next = 256.0;
+  for (double s : S)
+    if (s <= 256.0 || s >= next) {
+      Sfit.push_back(s);
+      if (s > 256.0) next = s * 1.01;
+    }
+}
+
+double profile(double s, double sigma, double d) {
+  return std::exp(-(0.5 / std::pow(sigma, d)) * std::pow(s, 0.5 * d));
+}
+
+// NNLS fit of one profile on a dictionary; returns weights (dict order), w0
+// and the max abs error over all lattice values S.
+double fit_on(const std::vector<double>& dict, const std::vector<double>& S,
+              const std::vector<double>& Sfit, double sigma, double d, std::vector<double>& w,
+              double& w0) {
+  const int K = int(dict.size()), M = int(Sfit.size());
+  std::vector<double> A(size_t(M) * (K + 1)), g(M);
+  for (int i = 0; i < M; ++i) {
+    const double s = Sfit[i];
+    g[i] = profile(s, sigma, d);
+    for (int k = 0; k < K; ++k) A[size_t(k) * M + i] = std::exp(-dict[k] * s);
+    A[size_t(K) * M + i] = s == 0.0 ? 1.0 : 0.0;  // delta term
+  }
+  std::vector<double> x;
+  nnls(A, M, K + 1, g, x);
+  w.assign(x.begin(), x.begin() + K);
+  w0 = x[K];
+  double err = 0.0;
+  for (double s : S) {
+    double v = s == 0.0 ? w0 : 0.0;
+    for (int k = 0; k < K; ++k)
+      if (w[k] > 0.0) v += std::exp(-dict[k] * s) * w[k];
+    err = std::max(err, std::fabs(v - profile(s, sigma, d)));
+  }
+  return err;
+}
+
+std::vector<double> geometric(double lo, double hi, int K) {
+  std::vector<double> out(K);
+  for (int k = 0; k < K; ++k) out[k] = lo * std::pow(hi / lo, double(k) / (K - 1));
+  return out;
+}
+
+int upload(void** dst, const void* src, size_t bytes) {
+  SFW3D_CUDA_TRY(cudaMalloc(dst, bytes));
+  SFW3D_CUDA_TRY(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
+  return SFW3D_OK;
+}
+
+}  // namespace
+
+void fit_profile(const int lo[3], const int hi[3], double sigma, double d, double target,
+                 double& w0, std::vector<std::pair<double, double>>& terms, double& err,
+                 bool& exact) {
+  terms.clear();
+  if (d == 2.0) {  // exp(-s / (2 sigma^2)): one exact separable term
+    exact = true;
+    err = 0.0;
+    w0 = 0.0;
+    terms.push_back({0.5 / (sigma * sigma), 1.0});
+    return;
+  }
+  exact = false;
+  std::vector<double> S, Sfit;
+  box_lattice(lo, hi, S, Sfit);
+  const double rmax = std::max({-lo[0], hi[0], -lo[1], hi[1], -lo[2], hi[2], 1});
+  err = INFINITY;
+  for (const int K : {48, 96}) {
+    std::vector<double> dict = geometric(0.5 / (rmax * rmax), 30.0, K), w;
+    double z0;
+    const double e = fit_on(dict, S, Sfit, sigma, d, w, z0);
+    if (e < err) {
+      err = e;
+      w0 = z0;
+      terms.clear();
+      for (int k = 0; k < K; ++k)
+        if (w[k] > 0.0) terms.push_back({dict[k], w[k]});
+    }
+    if (err <= target) break;
+  }
+}
+
+// ------------------------------------------------------------------ set
+struct BasisSet {
+  int dtype;
+  int lo[3], hi[3];                 // common offset box
+  std::vector<double> betas;        // shared terms
+  std::vector<int> tlo[3], tlen[3];  // per term, per axis tap range
+  std::vector<void*> taps;          // per term: 3 axes contiguous, storage dtype
+  std::vector<int> members;         // candidate ids on the basis path
+  std::vector<double> W, w0;        // [member][term], [member]
+  std::vector<double> fit_err;      // per candidate (inf when not fitted)
+  std::vector<char> is_member;      // per candidate
+  void* W_dev = nullptr;            // storage dtype, [member][term]
+  void* w0_dev = nullptr;
+  int* cid_dev = nullptr;           // member -> candidate id
+  long long taps_per_voxel = 0;
+  int device = 0;
+};
+
+// coarse dictionary size (the fine one has 2 * kDictCoarse - 1 points)
+constexpr int kDictCoarse = 49;
+// no fit is accepted below this bound (double-precision evaluation floor)
+constexpr double kFitFloor = 1e-11;
+
+int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands, int dtype,
+                    double tol, BasisSet** out, bool on_device) {
+  auto* s = new BasisSet();
+  s->dtype = dtype;
+  cudaGetDevice(&s->device);
+  const int nc = int(cands.size());
+  s->fit_err.assign(nc, INFINITY);
+  s->is_member.assign(nc, 0);
+  // candidates that can have a positive Gaussian mixture (d <= 2)
+  std::vector<int> pool;
+  for (int c = 0; c < nc; ++c)
+    if (cands[c].d <= 2.0) pool.push_back(c);
+  *out = s;
+  if (pool.empty()) return SFW3D_OK;
+  // common box: union of the pool's boxes
+  for (int a = 0; a < 3; ++a) {
+    s->lo[a] = 0;
+    s->hi[a] = 0;
+    for (int c : pool) {
+      s->lo[a] = std::min(s->lo[a], cands[c].lo[a]);
+      s->hi[a] = std::max(s->hi[a], cands[c].hi[a]);
+    }
+    if (s->hi[a] - s->lo[a] + 1 > dims[a]) {  // never wider than the axis
+      s->lo[a] = -(dims[a] / 2);
+      s->hi[a] = s->lo[a] + dims[a] - 1;
+    }
+  }
+  std::vector<double> S, Sfit;
+  box_lattice(s->lo, s->hi, S, Sfit);
+  const double rmax = std::max({-s->lo[0], s->hi[0], -s->lo[1], s->hi[1], -s->lo[2], s->hi[2], 1});
+  // nested geometric dictionaries over [0.5 / rmax^2, 30] (the coarse one is
+  // every other point of the fine one) plus the exact 1/(2 sigma^2) of every
+  // d == 2 candidate
+  std::vector<double> dict = geometric(0.5 / (rmax * rmax), 30.0, 2 * kDictCoarse - 1);
+  for (int c : pool)
+    if (cands[c].d == 2.0) dict.push_back(0.5 / (cands[c].sigma * cands[c].sigma));
+  std::sort(dict.begin(), dict.end());
+  dict.erase(std::unique(dict.begin(), dict.end()), dict.end());
+  const int K = int(dict.size());
+  std::vector<double> coarse = geometric(0.5 / (rmax * rmax), 30.0, kDictCoarse);
+  std::vector<int> coarse_idx;  // positions of the coarse points in dict
+  for (double b : coarse) {
+    const auto it = std::min_element(dict.begin(), dict.end(), [&](double x, double y) {
+      return std::fabs(x - b) < std::fabs(y - b);
+    });
+    coarse_idx.push_back(int(it - dict.begin()));
+  }
+  // fit every pool candidate over the COMMON box: outside its own box the
+  // target is its true profile (< 1e-12 there), so the mixture stays
+  // controlled on the whole box the passes use. Coarse dictionary first, the
+  // fine one where that misses tol. Below kFitFloor no NNLS fit can certify
+  // the bound in double arithmetic: only the exact d == 2 candidates join.
+  // Independent problems: one host thread each. A d == 2 candidate is
+  // exactly its own dictionary term, weight 1.
+  std::vector<std::vector<double>> wfit(nc);
+  std::vector<double> w0fit(nc, 0.0);
+  std::vector<double> err(nc, INFINITY);
+  auto fit_one = [&](int c) {
+    wfit[c].assign(K, 0.0);
+    if (cands[c].d == 2.0) {
+      const double beta = 0.5 / (cands[c].sigma * cands[c].sigma);
+      wfit[c][std::lower_bound(dict.begin(), dict.end(), beta) - dict.begin()] = 1.0;
+      err[c] = 0.0;
+      return;
+    }
+    if (tol < kFitFloor) return;
+    std::vector<double> sub, w;
+    for (int k : coarse_idx) sub.push_back(dict[k]);
+    double e = fit_on(sub, S, Sfit, cands[c].sigma, cands[c].d, w, w0fit[c]) + 1e-12;
+    for (size_t q = 0; q < coarse_idx.size(); ++q) wfit[c][coarse_idx[q]] = w[q];
+    if (e > tol) {
+      double z0;
+      const double e2 = fit_on(dict, S, Sfit, cands[c].sigma, cands[c].d, w, z0) + 1e-12;
+      if (e2 < e) {
+        e = e2;
+        wfit[c] = w;
+        w0fit[c] = z0;
+      }
+    }
+    err[c] = e;  // (+ 1e-12: factor truncation below)
+  };
+  {
+    const int nthreads =
+        std::max(1, std::min<int>(int(pool.size()), int(std::thread::hardware_concurrency())));
+    std::atomic<int> next{0};
+    std::vector<std::thread> workers;
+    for (int w = 0; w < nthreads; ++w)
+      workers.emplace_back([&] {
+        for (int q = next++; q < int(pool.size()); q = next++) fit_one(pool[q]);
+      });
+    for (auto& th : workers) th.join();
+  }
+  for (int c : pool) {
+    s->fit_err[c] = err[c];
+    if (err[c] <= tol) {
+      s->is_member[c] = 1;
+      s->members.push_back(c);
+    }
+  }
+  // union of the members' terms
+  std::vector<char> used(K, 0);
+  double wsum_max = 1.0;
+  for (int c : s->members) {
+    double ws = 0.0;
+    for (int k = 0; k < K; ++k)
+      if (wfit[c][k] > 0.0) {
+        used[k] = 1;
+        ws += wfit[c][k];
+      }
+    wsum_max = std::max(wsum_max, ws);
+  }
+  const double eps = 1e-12 / wsum_max;
+  std::vector<int> kmap;
+  for (int k = 0; k < K; ++k)
+    if (used[k]) kmap.push_back(k);
+  const int nt = int(kmap.size()), nm = int(s->members.size());
+  for (int a = 0; a < 3; ++a) {
+    s->tlo[a].resize(nt);
+    s->tlen[a].resize(nt);
+  }
+  for (int t = 0; t < nt; ++t) {
+    const double beta = dict[kmap[t]];
+    s->betas.push_back(beta);
+    const int r = int(std::ceil(std::sqrt(std::log(1.0 / eps) / beta)));
+    std::vector<double> h;
+    for (int a = 0; a < 3; ++a) {
+      s->tlo[a][t] = std::max(s->lo[a], -r);
+      s->tlen[a][t] = std::min(s->hi[a], r) - s->tlo[a][t] + 1;
+      for (int q = s->tlo[a][t]; q < s->tlo[a][t] + s->tlen[a][t]; ++q)
+        h.push_back(std::exp(-beta * double(q) * q));
+      s->taps_per_voxel += s->tlen[a][t];
+    }
+    if (!on_device) continue;
+    void* dev = nullptr;
+    int st;
+    if (dtype == SFW3D_F64) {
+      st = upload(&dev, h.data(), h.size() * sizeof(double));
+    } else {
+      std::vector<float> hf(h.begin(), h.end());
+      st = upload(&dev, hf.data(), hf.size() * sizeof(float));
+    }
+    if (st != SFW3D_OK) return st;
+    s->taps.push_back(dev);
+  }
+  s->W.assign(size_t(nm) * nt, 0.0);
+  s->w0.assign(nm, 0.0);
+  for (int m = 0; m < nm; ++m) {
+    const int c = s->members[m];
+    for (int t = 0; t < nt; ++t) s->W[size_t(m) * nt + t] = wfit[c][kmap[t]];
+    s->w0[m] = w0fit[c];
+  }
+  if (nm && on_device) {
+    if (dtype == SFW3D_F64) {
+      SFW3D_TRY(upload(&s->W_dev, s->W.data(), s->W.size() * sizeof(double) + 8));
+      SFW3D_TRY(upload(&s->w0_dev, s->w0.data(), s->w0.size() * sizeof(double)));
+    } else {
+      std::vector<float> Wf(s->W.begin(), s->W.end()), w0f(s->w0.begin(), s->w0.end());
+      Wf.push_back(0.f);
+      SFW3D_TRY(upload(&s->W_dev, Wf.data(), Wf.size() * sizeof(float)));
+      SFW3D_TRY(upload(&s->w0_dev, w0f.data(), w0f.size() * sizeof(float)));
+    }
+    SFW3D_TRY(upload(reinterpret_cast<void**>(&s->cid_dev), s->members.data(),
+                     s->members.size() * sizeof(int)));
+  }
+  return SFW3D_OK;
+}
+
+void basis_set_destroy(BasisSet* s) {
+  if (!s) return;
+  cudaSetDevice(s->device);
+  for (void* p : s->taps) cudaFree(p);
+  if (s->W_dev) cudaFree(s->W_dev);
+  if (s->w0_dev) cudaFree(s->w0_dev);
+  if (s->cid_dev) cudaFree(s->cid_dev);
+  delete s;
+}
+
+void basis_set_export(const BasisSet* s, int max_terms, int* n_terms, double* betas,
+                      double* weights, double* w0, double* fit_err, int32_t* member) {
+  const int nt = int(s->betas.size()), nc = int(s->is_member.size());
+  if (n_terms) *n_terms = nt;
+  for (int t = 0; t < nt && t < max_terms; ++t)
+    if (betas) betas[t] = s->betas[t];
+  for (int c = 0; c < nc; ++c) {
+    if (fit_err) fit_err[c] = s->fit_err[c];
+    if (member) member[c] = s->is_member[c];
+    if (w0) w0[c] = 0.0;
+    if (weights)
+      for (int t = 0; t < max_terms; ++t) weights[size_t(c) * max_terms + t] = 0.0;
+  }
+  for (int m = 0; m < int(s->members.size()); ++m) {
+    const int c = s->members[m];
+    if (w0) w0[c] = s->w0[m];
+    if (weights)
+      for (int t = 0; t < nt && t < max_terms; ++t)
+        weights[size_t(c) * max_terms + t] = s->W[size_t(m) * nt + t];
+  }
+}
+
+bool basis_set_member(const BasisSet* s, int cand, double* fit_err) {
+  if (!s || cand < 0 || cand >= int(s->is_member.size())) return false;
+  if (fit_err) *fit_err = s->fit_err[cand];
+  return s->is_member[cand] != 0;
+}
+int basis_set_n_terms(const BasisSet* s) { return s ? int(s->betas.size()) : 0; }
+int basis_set_n_members(const BasisSet* s) { return s ? int(s->members.size()) : 0; }
+long long basis_set_taps(const BasisSet* s) { return s ? s->taps_per_voxel : 0; }
+double basis_set_member_flops(const BasisSet* s) {
+  return s ? 2.0 * double(s->betas.size()) + 2.0 : 0.0;
+}
+double basis_set_flops(const BasisSet* s) {
+  if (!s || s->members.empty()) return 0.0;
+  return 2.0 * double(s->taps_per_voxel) + double(s->members.size()) * basis_set_member_flops(s);
+}
+
+// ------------------------------------------------------------------ eval
+namespace {
+
+constexpr int kMixMax = 32;  // members mixed per launch
+constexpr int kMixThreads = 256;
+
+// V consecutive elements of one volume as one vector load/store (16 B max)
+template <typename T, int V>
+struct Vec {
+  T v[V];
+};
+template <typename T, int V>
+__device__ __forceinline__ Vec<T, V> ld_stream(const T* p) {
+  Vec<T, V> r;
+  if constexpr (sizeof(T) * V == 16) {
+    const float4 q = __ldcs(reinterpret_cast<const float4*>(p));
+    memcpy(&r, &q, 16);
+  } else if constexpr (sizeof(T) * V == 8) {
+    const float2 q = __ldcs(reinterpret_cast<const float2*>(p));
+    memcpy(&r, &q, 8);
+  } else {
+    r.v[0] = __ldcs(p);
+  }
+  return r;
+}
+template <typename T, int V>
+__device__ __forceinline__ void st_stream(T* p, const Vec<T, V>& r) {
+  if constexpr (sizeof(T) * V == 16) {
+    float4 q;
+    memcpy(&q, &r, 16);
+    __stcs(reinterpret_cast<float4*>(p), q);
+  } else if constexpr (sizeof(T) * V == 8) {
+    float2 q;
+    memcpy(&q, &r, 8);
+    __stcs(reinterpret_cast<float2*>(p), q);
+  } else {
+    __stcs(p, r.v[0]);
+  }
+}
+
+// eta_c = (w0_c b + sum_k W[c][k] T_k) / lam for members [m0, m0 + nm) at
+// every voxel; windowed argmax per member (one partial per CTA); optional
+// field store. HBM-bound: each thread owns V consecutive voxels of one z row
+// (vector loads), KU term loads in flight; the running maximum is kept on the
+// raw accumulator (eta = acc / lam with lam > 0 is monotone in acc).
+template <typename T, int NM, int V>
+__global__ void __launch_bounds__(kMixThreads) mix_argmax_kernel(
+    const T* __restrict__ b, const T* __restrict__ terms, long long n, int K, int nm, int m0,
+    const T* __restrict__ W, const T* __restrict__ w0, const int* __restrict__ cid, int nx, int ny,
+    int nz, int4 wlo, int4 whi, double lam, T* __restrict__ fields, Best* __restrict__ partial) {
+  constexpr int KU = V == 4 ? 8 : (V == 2 ? 12 : 16);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sW = reinterpret_cast<T*>(smem_raw);  // [K][NM], zero-padded members
+  T* sw0 = sW + K * NM;
+  __shared__ Best red[NM][kMixThreads / 32];
+  for (int e = threadIdx.x; e < K * NM; e += kMixThreads) {
+    const int k = e / NM, m = e % NM;
+    sW[e] = m < nm ? W[size_t(m0 + m) * K + k] : T(0);
+  }
+  for (int e = threadIdx.x; e < NM; e += kMixThreads) sw0[e] = e < nm ? w0[m0 + e] : T(0);
+  __syncthreads();
+  T bacc[NM];
+  int bidx[NM];
+#pragma unroll
+  for (int m = 0; m < NM; ++m) {
+    bacc[m] = T(-INFINITY);
+    bidx[m] = 0x7fffffff;
+  }
+  const long long nv = n / V;
+  for (long long q = blockIdx.x * (long long)kMixThreads + threadIdx.x; q < nv;
+       q += (long long)gridDim.x * kMixThreads) {
+    const long long i0 = q * V;
+    const Vec<T, V> bv = ld_stream<T, V>(b + i0);
+    T acc[NM][V];
+#pragma unroll
+    for (int m = 0; m < NM; ++m)
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc[m][j] = sw0[m] * bv.v[j];
+    int k = 0;
+    for (; k + KU <= K; k += KU) {
+      Vec<T, V> tv[KU];
+#pragma unroll
+      for (int u = 0; u < KU; ++u) tv[u] = ld_stream<T, V>(terms + (long long)(k + u) * n + i0);
+#pragma unroll
+      for (int u = 0; u < KU; ++u)
+#pragma unroll
+        for (int m = 0; m < NM; ++m) {
+          const T w = sW[(k + u) * NM + m];
+#pragma unroll
+          for (int j = 0; j < V; ++j) acc[m][j] = fma(w, tv[u].v[j], acc[m][j]);
+        }
+    }
+    for (; k < K; ++k) {
+      const Vec<T, V> tv = ld_stream<T, V>(terms + (long long)k * n + i0);
+#pragma unroll
+      for (int m = 0; m < NM; ++m) {
+        const T w = sW[k * NM + m];
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[m][j] = fma(w, tv.v[j], acc[m][j]);
+      }
+    }
+    // the V voxels share one (x, y) row (nz % V == 0)
+    const int z0 = int(i0 % nz);
+    const long long row = i0 / nz;
+    const int y = int(row % ny), x = int(row / ny);
+    const bool row_win = x >= wlo.x && x <= whi.x && y >= wlo.y && y <= whi.y;
+#pragma unroll
+    for (int m = 0; m < NM; ++m) {
+      if (m >= nm) break;
+      if (fields) {
+        Vec<T, V> f;
+#pragma unroll
+        for (int j = 0; j < V; ++j) f.v[j] = T(double(acc[m][j]) / lam);
+        st_stream<T, V>(fields + (long long)cid[m0 + m] * n + i0, f);
+      }
+      if (row_win) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          const int z = z0 + j;
+          // ascending i within the thread: strict '>' keeps the first maximum
+          if (z >= wlo.z && z <= whi.z && acc[m][j] > bacc[m]) {
+            bacc[m] = acc[m][j];
+            bidx[m] = int(i0 + j);
+          }
+        }
+      }
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int m = 0; m < NM; ++m) {
+    if (m >= nm) break;
+    Best bm = {bidx[m] == 0x7fffffff ? -INFINITY : double(bacc[m]) / lam,
+               bidx[m] == 0x7fffffff ? 0x7fffffffffffffffLL : (long long)bidx[m]};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bm.v, o);
+      const long long oi = __shfl_xor_sync(0xffffffffu, bm.idx, o);
+      if (better(ov, oi, bm.v, bm.idx)) bm = {ov, oi};
+    }
+    if (lane == 0) red[m][warp] = bm;
+  }
+  __syncthreads();
+  if (threadIdx.x < nm) {
+    Best bm = red[threadIdx.x][0];
+    for (int w = 1; w < kMixThreads / 32; ++w)
+      if (better(red[threadIdx.x][w].v, red[threadIdx.x][w].idx, bm.v, bm.idx))
+        bm = red[threadIdx.x][w];
+    partial[(long long)(m0 + threadIdx.x) * gridDim.x + blockIdx.x] = bm;
+  }
+}
+
+__global__ void member_reduce_kernel(const Best* __restrict__ partial, int nblocks,
+                                     const int* __restrict__ cid, Best* __restrict__ best_dev) {
+  __shared__ Best sb[32];
+  const int m = blockIdx.x;
+  Best b{-INFINITY, 0x7fffffffffffffffLL};
+  for (int i = threadIdx.x; i < nblocks; i += blockDim.x) {
+    const Best p = partial[(long long)m * nblocks + i];
+    if (better(p.v, p.idx, b.v, b.idx)) b = p;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, b.v, o);
+    const long long oi = __shfl_xor_sync(0xffffffffu, b.idx, o);
+    if (better(ov, oi, b.v, b.idx)) b = {ov, oi};
+  }
+  if (lane == 0) sb[warp] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Best r = sb[0];
+    for (int w = 1; w < int(blockDim.x / 32); ++w)
+      if (better(sb[w].v, sb[w].idx, r.v, r.idx)) r = sb[w];
+    best_dev[cid[m]] = r;
+  }
+}
+
+}  // namespace
+
+size_t basis_set_scratch(const BasisSet* s, long long n, int dtype) {
+  if (!s || s->members.empty()) return 0;
+  const size_t es = dtype == SFW3D_F64 ? 8 : 4;
+  return Carver::need({size_t(n) * es, size_t(n) * es, size_t(n) * es * s->betas.size(),
+                       s->members.size() * 4096 * sizeof(Best)});
+}
+
+template <typename T, int NM, int V>
+static int launch_mix_nm(sfw3d_ctx* ctx, int nblocks, const void* b, const void* terms,
+                         long long n, int nt, int nmm, int m0, const BasisSet* s, const int dims[3],
+                         int4 wlo, int4 whi, double lam, void* fields, Best* partial) {
+  const size_t smem = (size_t(nt) * NM + NM) * sizeof(T);
+  if (smem > 48 * 1024)
+    SFW3D_CUDA_TRY(cudaFuncSetAttribute(mix_argmax_kernel<T, NM, V>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  mix_argmax_kernel<T, NM, V><<<nblocks, kMixThreads, smem, ctx->stream>>>(
+      static_cast<const T*>(b), static_cast<const T*>(terms), n, nt, nmm, m0,
+      static_cast<const T*>(s->W_dev), static_cast<const T*>(s->w0_dev), s->cid_dev, dims[0],
+      dims[1], dims[2], wlo, whi, lam, static_cast<T*>(fields), partial);
+  return SFW3D_OK;
+}
+
+// member-count buckets keep the accumulators in registers: V voxels per
+// thread x NM members <= 32 accumulators (16-byte loads where z allows)
+template <typename T>
+static int launch_mix(sfw3d_ctx* ctx, int nblocks, const void* b, const void* terms, long long n,
+                      int nt, int nmm, int m0, const BasisSet* s, const int dims[3], int4 wlo,
+                      int4 whi, double lam, void* fields, Best* partial) {
+  constexpr int V4 = 16 / sizeof(T);  // 4 floats / 2 doubles
+  const int nz = dims[2];
+#define SFW3D_MIX(NM, V)                                                                        \
+  return launch_mix_nm<T, NM, V>(ctx, nblocks, b, terms, n, nt, nmm, m0, s, dims, wlo, whi, lam, \
+                                 fields, partial)
+  if (nmm <= 8 && nz % V4 == 0) SFW3D_MIX(8, V4);
+  if (nmm <= 16 && nz % 2 == 0) SFW3D_MIX(16, 2);
+  if (nmm <= 8) SFW3D_MIX(8, 1);
+  if (nmm <= 16) SFW3D_MIX(16, 1);
+  SFW3D_MIX(kMixMax, 1);
+#undef SFW3D_MIX
+}
+
+int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[3], const void* b,
+                   double lam, const int32_t win[6], void* fields, Best* best_dev, void* scratch) {
+  const int nm = int(s->members.size()), nt = int(s->betas.size());
+  if (nm == 0) return SFW3D_OK;
+  const long long n = vol_count(dims);
+  if (n >= (1LL << 31)) {  // (n_terms volumes of that size exceed any HBM anyway)
+    set_error("volume too large for the separable basis path (>= 2^31 voxels)");
+    return SFW3D_EINVAL;
+  }
+  const size_t es = dtype == SFW3D_F64 ? 8 : 4;
+  Carver cv(scratch);
+  char* t1 = cv.take<char>(size_t(n) * es);
+  char* t2 = cv.take<char>(size_t(n) * es);
+  char* terms = cv.take<char>(size_t(n) * es * nt);
+  const int nblocks = std::min<long long>(4096, (long long)ctx->num_sms * 8);
+  Best* partial = cv.take<Best>(size_t(nm) * nblocks);
+  // T_k = (f_k x f_k x f_k) * b for every shared term
+  for (int t = 0; t < nt; ++t) {
+    const char* tp = static_cast<const char*>(s->taps[t]);
+    const int l0 = s->tlen[0][t], l1 = s->tlen[1][t], l2 = s->tlen[2][t];
+    SFW3D_TRY(corr_pass_impl(ctx, dtype, b, t1, dims, 2, tp + es * (l0 + l1), s->tlo[2][t], l2,
+                             nullptr, 0.0, 1.0, "eta_basis"));
+    SFW3D_TRY(corr_pass_impl(ctx, dtype, t1, t2, dims, 1, tp + es * l0, s->tlo[1][t], l1, nullptr,
+                             0.0, 1.0, "eta_basis"));
+    SFW3D_TRY(corr_pass_impl(ctx, dtype, t2, terms + size_t(t) * n * es, dims, 0, tp, s->tlo[0][t],
+                             l0, nullptr, 0.0, 1.0, "eta_basis"));
+  }
+  const int4 wlo = make_int4(win[0], win[2], win[4], 0), whi = make_int4(win[1], win[3], win[5], 0);
+  for (int m0 = 0; m0 < nm; m0 += kMixMax) {
+    const int nmm = std::min(kMixMax, nm - m0);
+    SFW3D_PROF(ctx, "eta_mix");
+    if (dtype == SFW3D_F64)
+      SFW3D_TRY(launch_mix<double>(ctx, nblocks, b, terms, n, nt, nmm, m0, s, dims, wlo, whi, lam,
+                                   fields, partial));
+    else
+      SFW3D_TRY(launch_mix<float>(ctx, nblocks, b, terms, n, nt, nmm, m0, s, dims, wlo, whi, lam,
+                                  fields, partial));
+    SFW3D_LAUNCH_CHECK(ctx);
+  }
+  {
+    SFW3D_PROF(ctx, "argmax");
+    member_reduce_kernel<<<nm, 256, 0, ctx->stream>>>(partial, nblocks, s->cid_dev, best_dev);
+    SFW3D_LAUNCH_CHECK(ctx);
+  }
+  return SFW3D_OK;
+}
+
+}  // namespace sfw3d

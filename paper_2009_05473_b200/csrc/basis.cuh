@@ -1,0 +1,60 @@
+// Shared separable Gaussian basis for the certificate (see basis.cu).
+#pragma once
+
+#include <utility>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace sfw3d {
+
+// argmax record shared by the certificate kernels: larger value wins, ties
+// go to the smaller C-order index (first maximum, certificate.py:161-163)
+struct Best {
+  double v;
+  long long idx;
+};
+
+__device__ __forceinline__ bool better(double v, long long i, double bv, long long bi) {
+  return (v > bv) || (v == bv && i < bi);
+}
+
+struct BasisCandidate {
+  double sigma, d;
+  int lo[3], hi[3];   // the candidate's reference support box (offsets)
+  long long direct_taps;
+};
+
+struct BasisSet;
+
+// Fits every candidate on one shared dictionary of Gaussians (see basis.cu)
+// and keeps those whose max abs error on the common box is <= tol.
+// on_device = false fits on the host only (no device buffers; eval unusable).
+int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands, int dtype,
+                    double tol, BasisSet** out, bool on_device = true);
+// host copy of the fit: betas[n_terms], weights[n_cand][max_terms] (member rows,
+// zero elsewhere), w0[n_cand], fit_err[n_cand], member[n_cand]; NULLs skipped
+void basis_set_export(const BasisSet* s, int max_terms, int* n_terms, double* betas,
+                      double* weights, double* w0, double* fit_err, int32_t* member);
+void basis_set_destroy(BasisSet* s);
+// candidate -> (is member, fit error of its shared-dictionary fit)
+bool basis_set_member(const BasisSet* s, int cand, double* fit_err);
+int basis_set_n_terms(const BasisSet* s);
+int basis_set_n_members(const BasisSet* s);
+long long basis_set_taps(const BasisSet* s);        // per voxel, all shared terms
+double basis_set_flops(const BasisSet* s);          // executed flops per voxel (all members)
+double basis_set_member_flops(const BasisSet* s);   // mix flops per voxel per member
+
+// Scratch (bytes) basis_set_eval needs for a volume of n elements.
+size_t basis_set_scratch(const BasisSet* s, long long n, int dtype);
+// eta for all members: best_dev[cand] receives each member's windowed
+// argmax; fields (n_cand volumes, candidate-major) are written when non-NULL.
+int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[3], const void* b,
+                   double lam, const int32_t win[6], void* fields, Best* best_dev, void* scratch);
+
+// Host-only single-candidate fit (the sfw3d_basis_fit ABI helper).
+void fit_profile(const int lo[3], const int hi[3], double sigma, double d, double target,
+                 double& w0, std::vector<std::pair<double, double>>& terms, double& err,
+                 bool& exact);
+
+}  // namespace sfw3d

@@ -34,16 +34,9 @@
 #include <algorithm>
 #include <cstring>
 
-#include "internal.cuh"
+#include "basis.cuh"
 
 namespace sfw3d {
-
-struct Term {
-  double beta, w;
-  int tlo[3], tlen[3];     // per-axis tap range (the box clipped where f_k < eps)
-  void* taps64 = nullptr;  // 3 axes, contiguous per axis, tlen[a] each
-  void* taps32 = nullptr;
-};
 
 struct CandHost {
   double sigma, d;
@@ -56,17 +49,7 @@ struct CandHost {
   double* t64 = nullptr;
   float* t32 = nullptr;
   int2* rows_dev = nullptr;
-  // separable bases: one fitted for fp32 storage (stop at 1e-10) and one for
-  // fp64 storage (stop at 1e-13); identical and exact for d == 2
-  struct Basis {
-    bool exact = false;     // d == 2: one exact term
-    double fit_err = INFINITY;
-    double w0 = 0.0;        // delta weight
-    std::vector<Term> terms;
-    long long taps = 0;     // per output voxel
-  } b32, b64;
   double fold_flops = 0.0;  // FP32 flops per voxel of the folded direct kernel
-  const Basis& basis(int dtype) const { return dtype == SFW3D_F64 ? b64 : b32; }
 };
 
 }  // namespace sfw3d
@@ -82,6 +65,12 @@ struct sfw3d_table {
   int mode;      // 0 auto, 1 direct only
   double basis_tol;
   int smem_max;  // opt-in shared memory per block of the device
+  // shared separable bases (basis.cu), one per storage precision, fitted on
+  // first use of that precision (a solve only ever touches one)
+  std::vector<sfw3d::BasisCandidate> bcands;
+  mutable sfw3d::BasisSet* set32 = nullptr;
+  mutable sfw3d::BasisSet* set64 = nullptr;
+  const sfw3d::BasisSet* set(int dtype) const { return dtype == SFW3D_F64 ? set64 : set32; }
 };
 
 namespace sfw3d {
@@ -111,16 +100,6 @@ struct Geo {
   int brows;           // template rows per staged chunk
   double lam;          // eta = sum / lam (certificate.py:160)
 };
-
-struct Best {
-  double v;
-  long long idx;
-};
-
-__device__ __forceinline__ bool better(double v, long long i, double bv, long long bi) {
-  // larger value wins; ties -> smaller C-order index (first maximum)
-  return (v > bv) || (v == bv && i < bi);
-}
 
 template <typename T>
 __device__ __forceinline__ void ld4(const T* p, T& a, T& b, T& c, T& d) {
@@ -452,29 +431,6 @@ __global__ void __launch_bounds__(kThreads) eta_sym_kernel(const T* __restrict__
   reduce_store_best<T>(best, wbest, partial + (long long)blockIdx.y * gridDim.x + blockIdx.x);
 }
 
-// eta = acc / lam over a whole volume (basis path): optional field store and
-// windowed argmax; one partial record per CTA.
-template <typename T>
-__global__ void __launch_bounds__(256) volume_argmax_kernel(const T* __restrict__ acc, int nx, int ny,
-                                                            int nz, const int4 wlo, const int4 whi,
-                                                            double lam, T* __restrict__ field,
-                                                            Best* __restrict__ partial) {
-  __shared__ Best wbest[8];
-  Best best{-INFINITY, 0x7fffffffffffffffLL};
-  const long long n = (long long)nx * ny * nz;
-  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
-    const double eta = double(acc[i]) / lam;
-    if (field) field[i] = T(eta);
-    const int z = int(i % nz);
-    const int y = int((i / nz) % ny);
-    const int x = int(i / ((long long)ny * nz));
-    if (x >= wlo.x && x <= whi.x && y >= wlo.y && y <= whi.y && z >= wlo.z && z <= whi.z &&
-        better(eta, i, best.v, best.idx))
-      best = {eta, i};
-  }
-  reduce_store_best<T>(best, wbest, partial + blockIdx.x);
-}
-
 // periodic padding: dst[X][Y][Z] = src[(X-px) mod nx][(Y-py) mod ny][(Z-pz) mod nz]
 template <typename T>
 __global__ void pad_kernel(const T* __restrict__ src, T* __restrict__ dst, int nx, int ny, int nz,
@@ -515,140 +471,6 @@ int region_pitch(int lc4, int esize) {
   return p;
 }
 
-// ------------------------------------------------------------------ NNLS
-// Lawson-Hanson non-negative least squares min ||A x - g||, x >= 0, with the
-// passive-set subproblems solved by Householder QR. A is column-major M x N.
-// Extended precision (x86 long double, 64-bit mantissa) keeps the passive-set
-// least-squares solves accurate on the nearly collinear exponential columns.
-using ld = long double;
-
-void lsq_qr(const std::vector<ld>& A, int M, const std::vector<int>& cols, const std::vector<ld>& g,
-            std::vector<ld>& z) {
-  const int p = int(cols.size());
-  std::vector<ld> B(size_t(M) * p), rhs(g), scale(p), v(M);
-  for (int j = 0; j < p; ++j) {
-    ld s = 0.0L;
-    for (int i = 0; i < M; ++i) s += A[size_t(cols[j]) * M + i] * A[size_t(cols[j]) * M + i];
-    scale[j] = s > 0 ? 1.0L / std::sqrt(s) : 1.0L;
-    for (int i = 0; i < M; ++i) B[size_t(j) * M + i] = A[size_t(cols[j]) * M + i] * scale[j];
-  }
-  for (int j = 0; j < p; ++j) {  // Householder on column j, rows j..M-1
-    ld* c = &B[size_t(j) * M];
-    ld nrm = 0.0L;
-    for (int i = j; i < M; ++i) nrm += c[i] * c[i];
-    nrm = std::sqrt(nrm);
-    if (nrm == 0.0L) continue;
-    const ld alpha = c[j] > 0 ? -nrm : nrm;
-    for (int i = j; i < M; ++i) v[i] = c[i];
-    v[j] -= alpha;
-    ld vn = 0.0L;
-    for (int i = j; i < M; ++i) vn += v[i] * v[i];
-    if (vn == 0.0L) continue;
-    auto apply = [&](ld* col) {
-      ld dot = 0.0L;
-      for (int i = j; i < M; ++i) dot += v[i] * col[i];
-      const ld f = 2.0L * dot / vn;
-      for (int i = j; i < M; ++i) col[i] -= f * v[i];
-    };
-    for (int k = j; k < p; ++k) apply(&B[size_t(k) * M]);
-    apply(rhs.data());
-  }
-  z.assign(p, 0.0L);
-  for (int j = p - 1; j >= 0; --j) {
-    ld s = rhs[j];
-    for (int k = j + 1; k < p; ++k) s -= B[size_t(k) * M + j] * z[k];
-    const ld r = B[size_t(j) * M + j];
-    z[j] = r != 0.0L ? s / r : 0.0L;
-  }
-  for (int j = 0; j < p; ++j) z[j] *= scale[j];
-}
-
-// Lawson-Hanson: add the column with the largest (scaled) gradient, solve the
-// passive least-squares problem, step back to feasibility when needed.
-void nnls(const std::vector<double>& Ad, int M, int N, const std::vector<double>& gd,
-          std::vector<double>& xd) {
-  std::vector<ld> A(Ad.begin(), Ad.end()), g(gd.begin(), gd.end()), x(N, 0.0L), r(M);
-  std::vector<char> passive(N, 0), banned(N, 0);
-  std::vector<ld> cn(N);
-  for (int j = 0; j < N; ++j) {
-    ld s = 0.0L;
-    for (int i = 0; i < M; ++i) s += A[size_t(j) * M + i] * A[size_t(j) * M + i];
-    cn[j] = s > 0.0L ? std::sqrt(s) : 1.0L;
-  }
-  ld gn = 0.0L;
-  for (ld v : g) gn += v * v;
-  const ld tol = 1e-17L * std::sqrt(gn);
-  for (int outer = 0; outer < 8 * N; ++outer) {
-    for (int i = 0; i < M; ++i) {
-      ld s = g[i];
-      for (int j = 0; j < N; ++j)
-        if (x[j] != 0.0L) s -= A[size_t(j) * M + i] * x[j];
-      r[i] = s;
-    }
-    int jmax = -1;
-    ld best = tol;
-    for (int j = 0; j < N; ++j) {
-      if (passive[j] || banned[j]) continue;
-      ld s = 0.0L;
-      for (int i = 0; i < M; ++i) s += A[size_t(j) * M + i] * r[i];
-      s /= cn[j];
-      if (s > best) {
-        best = s;
-        jmax = j;
-      }
-    }
-    if (jmax < 0) break;
-    passive[jmax] = 1;
-    bool first = true, added = true;
-    for (int inner = 0; inner < 3 * N; ++inner) {
-      std::vector<int> cols;
-      for (int j = 0; j < N; ++j)
-        if (passive[j]) cols.push_back(j);
-      std::vector<ld> z;
-      lsq_qr(A, M, cols, g, z);
-      bool ok = true;
-      for (ld v : z) ok &= v > 0.0L;
-      if (ok) {
-        std::fill(x.begin(), x.end(), 0.0L);
-        for (size_t q = 0; q < cols.size(); ++q) x[cols[q]] = z[q];
-        break;
-      }
-      if (first) {  // the entering column itself came out non-positive: skip it
-        size_t qn = 0;
-        while (cols[qn] != jmax) ++qn;
-        if (z[qn] <= 0.0L) {
-          passive[jmax] = 0;
-          banned[jmax] = 1;
-          added = false;
-          break;
-        }
-      }
-      first = false;
-      ld alpha = 2.0L;
-      int qmin = -1;
-      for (size_t q = 0; q < cols.size(); ++q)
-        if (z[q] <= 0.0L) {
-          const ld xv = x[cols[q]];
-          const ld a = xv / (xv - z[q]);
-          if (a < alpha) {
-            alpha = a;
-            qmin = int(q);
-          }
-        }
-      for (size_t q = 0; q < cols.size(); ++q) {
-        const int j = cols[q];
-        x[j] += alpha * (z[q] - x[j]);
-        if (int(q) == qmin || x[j] <= 0.0L) {
-          x[j] = 0.0L;
-          passive[j] = 0;
-        }
-      }
-    }
-    if (added) std::fill(banned.begin(), banned.end(), 0);
-  }
-  xd.assign(x.begin(), x.end());
-}
-
 }  // namespace
 
 // ------------------------------------------------------------------ table
@@ -658,136 +480,26 @@ static int upload(void** dst, const void* src, size_t bytes) {
   return SFW3D_OK;
 }
 
-// Fits g(s) = exp(-s^(d/2) / (2 sigma^d)) on the lattice values s = a^2 + b^2
-// + c^2 of the offset box [lo, hi] by w0 * [s == 0] + sum_k w_k exp(-beta_k s)
-// (non-negative weights, 48 geometric beta_k). Host-only.
-static void fit_profile(const int lo[3], const int hi[3], double sigma, double d, double target,
-                        double& w0, std::vector<std::pair<double, double>>& terms, double& err,
-                        bool& exact) {
-  const double inv2sd = 0.5 / std::pow(sigma, d);
-  terms.clear();
-  if (d == 2.0) {  // exp(-inv2sd * (a^2 + b^2 + c^2)) = product of three 1-D Gaussians
-    exact = true;
-    err = 0.0;
-    w0 = 0.0;
-    terms.push_back({inv2sd, 1.0});
-    return;
-  }
-  exact = false;
-  int smax = 0;
-  for (int a = 0; a < 3; ++a) smax += std::max(lo[a] * lo[a], hi[a] * hi[a]);
-  std::vector<char> present(size_t(smax) + 1, 0);
-  std::vector<int> sv[3];
-  for (int ax = 0; ax < 3; ++ax) {
-    std::vector<char> sq(size_t(smax) + 1, 0);
-    for (int t = lo[ax]; t <= hi[ax]; ++t) sq[size_t(t) * t] = 1;
-    for (int s = 0; s <= smax; ++s)
-      if (sq[s]) sv[ax].push_back(s);
-  }
-  for (int s0 : sv[0])
-    for (int s1 : sv[1])
-      for (int s2 : sv[2]) present[size_t(s0) + s1 + s2] = 1;
-  std::vector<double> S;
-  for (int s = 0; s <= smax; ++s)
-    if (present[s]) S.push_back(double(s));
-  const int Mfull = int(S.size());
-  // fit on all s <= 256 plus a geometric subsample of the rest (the profile
-  // is smooth there); the error is then measured on every lattice value
-  std::vector<double> Sfit;
-  {
-    double next = 256.0;
-    for (double s : S) {
-      if (s <= 256.0 || s >= next) {
-        Sfit.push_back(s);
-        if (s > 256.0) next = s * 1.004;
-      }
+// the reference's support box of a unit atom: radius R = ceil(sigma * 36^(1/d)),
+// full axis with minimum-image offsets when 2R + 1 >= n (forward.py:97-109)
+static void candidate_box(const int dims[3], double sigma, double d, int lo[3], int hi[3]) {
+  const int R = int(std::ceil(sigma * std::pow(kTailExponent, 1.0 / d)));
+  for (int a = 0; a < 3; ++a) {
+    if (2LL * R + 1 >= dims[a]) {
+      lo[a] = -(dims[a] / 2);
+      hi[a] = lo[a] + dims[a] - 1;
+    } else {
+      lo[a] = -R;
+      hi[a] = R;
     }
-  }
-  const int M = int(Sfit.size());
-  const double rmax = std::max({-lo[0], hi[0], -lo[1], hi[1], -lo[2], hi[2], 1});
-  const double bmin = 0.5 / (rmax * rmax), bmax = 30.0;
-  std::vector<double> gfull(Mfull);
-  for (int i = 0; i < Mfull; ++i) gfull[i] = std::exp(-inv2sd * std::pow(S[i], 0.5 * d));
-  err = INFINITY;
-  for (const int K : {48, 96}) {  // denser dictionary only when the first misses 1e-10
-    std::vector<double> betas(K), A(size_t(M) * (K + 1)), g(M);
-    for (int k = 0; k < K; ++k) betas[k] = bmin * std::pow(bmax / bmin, double(k) / (K - 1));
-    for (int i = 0; i < M; ++i) {
-      const double s = Sfit[i];
-      g[i] = std::exp(-inv2sd * std::pow(s, 0.5 * d));
-      for (int k = 0; k < K; ++k) A[size_t(k) * M + i] = std::exp(-betas[k] * s);
-      A[size_t(K) * M + i] = s == 0.0 ? 1.0 : 0.0;  // delta term
-    }
-    std::vector<double> x;
-    nnls(A, M, K + 1, g, x);
-    double e = 0.0;
-    for (int i = 0; i < Mfull; ++i) {
-      double v = S[i] == 0.0 ? x[K] : 0.0;
-      for (int k = 0; k < K; ++k)
-        if (x[k] > 0.0) v += std::exp(-betas[k] * S[i]) * x[k];
-      e = std::max(e, std::fabs(v - gfull[i]));
-    }
-    if (e < err) {
-      err = e;
-      w0 = x[K];
-      terms.clear();
-      for (int k = 0; k < K; ++k)
-        if (x[k] > 0.0) terms.push_back({betas[k], x[k]});
-    }
-    if (err <= target) break;
   }
 }
 
-static int fit_basis(CandHost& c, CandHost::Basis& B, double target) {
-  std::vector<std::pair<double, double>> bw;
-  fit_profile(c.lo, c.hi, c.sigma, c.d, target, B.w0, bw, B.fit_err, B.exact);
-  double wsum = 0.0;
-  for (auto& p : bw) wsum += p.second;
-  // A term's 1-D factor exp(-beta t^2) is dropped where it is below
-  // eps = 1e-12 / max(1, sum w): every dropped product is then < w_k * eps,
-  // so the truncation adds at most 1e-12 to the recorded fit error.
-  const double eps = 1e-12 / std::max(1.0, wsum);
-  for (auto& p : bw) {
-    Term t{};
-    t.beta = p.first;
-    t.w = p.second;
-    const int r = B.exact ? (1 << 29) : int(std::ceil(std::sqrt(std::log(1.0 / eps) / t.beta)));
-    for (int ax = 0; ax < 3; ++ax) {
-      t.tlo[ax] = std::max(c.lo[ax], -r);
-      t.tlen[ax] = std::min(c.hi[ax], r) - t.tlo[ax] + 1;
-    }
-    B.terms.push_back(t);
-  }
-  if (!B.exact) B.fit_err += 1e-12;
-  B.taps = (B.w0 != 0.0 ? 1 : 0);
-  for (auto& t : B.terms) {
-    std::vector<double> h64;
-    for (int ax = 0; ax < 3; ++ax)
-      for (int q = t.tlo[ax]; q < t.tlo[ax] + t.tlen[ax]; ++q)
-        h64.push_back(std::exp(-t.beta * double(q) * q));
-    std::vector<float> h32(h64.begin(), h64.end());
-    SFW3D_TRY(upload(&t.taps64, h64.data(), h64.size() * sizeof(double)));
-    SFW3D_TRY(upload(&t.taps32, h32.data(), h32.size() * sizeof(float)));
-    B.taps += t.tlen[0] + t.tlen[1] + t.tlen[2];
-  }
-  return SFW3D_OK;
-}
-
-static int build_candidate(const int dims[3], double sigma, double d, double tap_tol, bool basis,
+static int build_candidate(const int dims[3], double sigma, double d, double tap_tol,
                            CandHost& c) {
   c.sigma = sigma;
   c.d = d;
-  const double rr = std::ceil(sigma * std::pow(kTailExponent, 1.0 / d));  // forward.py:97-99
-  const int R = int(rr);
-  for (int a = 0; a < 3; ++a) {
-    if (2LL * R + 1 >= dims[a]) {  // full axis, minimum-image offsets (forward.py:107-109)
-      c.lo[a] = -(dims[a] / 2);
-      c.hi[a] = c.lo[a] + dims[a] - 1;
-    } else {
-      c.lo[a] = -R;
-      c.hi[a] = R;
-    }
-  }
+  candidate_box(dims, sigma, d, c.lo, c.hi);
   c.la = c.hi[0] - c.lo[0] + 1;
   c.lb = c.hi[1] - c.lo[1] + 1;
   c.cl = -round_up(-c.lo[2], 4);  // lo[2] rounded down to a multiple of 4
@@ -839,23 +551,36 @@ static int build_candidate(const int dims[3], double sigma, double d, double tap
   SFW3D_TRY(upload(reinterpret_cast<void**>(&c.t64), t.data(), t.size() * sizeof(double)));
   SFW3D_TRY(upload(reinterpret_cast<void**>(&c.t32), t32.data(), t32.size() * sizeof(float)));
   SFW3D_TRY(upload(reinterpret_cast<void**>(&c.rows_dev), c.rows.data(), c.rows.size() * sizeof(int2)));
-  if (basis) {
-    SFW3D_TRY(fit_basis(c, c.b32, 1e-10));
-    SFW3D_TRY(fit_basis(c, c.b64, 1e-13));
-  }
   return SFW3D_OK;
 }
 
 // fp64 storage (reference-parity configs) accepts a basis only this close
 constexpr double kBasisTol64 = 1e-12;
 
-// evaluator choice per candidate and storage type
-static bool use_basis(const sfw3d_table* t, const CandHost& c, int dtype) {
-  const CandHost::Basis& B = c.basis(dtype);
-  if (t->mode == 1 || B.terms.empty()) return false;
-  if (B.exact) return true;
+// builds the shared basis of one storage precision on first use; fp64
+// storage (the reference-parity configs) accepts fits <= min(basis_tol, 1e-12)
+static int ensure_basis(const sfw3d_table* t, int dtype) {
+  if (t->mode != 0) return SFW3D_OK;
+  BasisSet*& s = dtype == SFW3D_F64 ? t->set64 : t->set32;
+  if (s) return SFW3D_OK;
   const double tol = dtype == SFW3D_F64 ? std::min(t->basis_tol, kBasisTol64) : t->basis_tol;
-  return B.fit_err <= tol && B.taps < c.taps;
+  int dev = 0;
+  SFW3D_CUDA_TRY(cudaGetDevice(&dev));
+  SFW3D_CUDA_TRY(cudaSetDevice(t->device));
+  BasisSet* built = nullptr;
+  const int st = basis_set_build(t->dims, t->bcands, dtype, tol, &built);
+  cudaSetDevice(dev);
+  if (st != SFW3D_OK) {
+    basis_set_destroy(built);
+    return st;
+  }
+  s = built;
+  return SFW3D_OK;
+}
+
+// evaluator choice per candidate and storage type
+static bool use_basis(const sfw3d_table* t, int ci, int dtype) {
+  return t->mode == 0 && basis_set_member(t->set(dtype), ci, nullptr);
 }
 
 static bool use_sym(const sfw3d_table* t, const CandHost& c, int dtype) {
@@ -865,9 +590,14 @@ static bool use_sym(const sfw3d_table* t, const CandHost& c, int dtype) {
   return sym && smem_sym <= std::min(t->smem_max - 2048, 160 * 1024);
 }
 
-static double cand_flops(const sfw3d_table* t, const CandHost& c, int dtype) {
-  if (use_basis(t, c, dtype))
-    return 2.0 * double(c.basis(dtype).taps) + 2.0 * double(c.basis(dtype).terms.size());
+// executed flops per voxel attributed to one candidate (basis members share
+// the term passes equally and each pays its own mix)
+static double cand_flops(const sfw3d_table* t, int ci, int dtype) {
+  const CandHost& c = t->cands[ci];
+  if (use_basis(t, ci, dtype)) {
+    const BasisSet* s = t->set(dtype);
+    return 2.0 * double(basis_set_taps(s)) / basis_set_n_members(s) + basis_set_member_flops(s);
+  }
   return use_sym(t, c, dtype) ? c.fold_flops : 2.0 * double(c.taps);
 }
 
@@ -897,6 +627,34 @@ extern "C" int sfw3d_basis_fit(const int32_t lo[3], const int32_t hi[3], double 
   return SFW3D_OK;
 }
 
+extern "C" int sfw3d_basis_set_fit(const int32_t dims[3], int n_sigma, const double* sigmas,
+                                   int n_shape, const double* shapes, int dtype, double tol,
+                                   int max_terms, int* n_terms, double* betas, double* weights,
+                                   double* w0, double* fit_err, int32_t* member) {
+  SFW3D_CHECK_ARG(dims && sigmas && shapes && n_terms, "NULL argument");
+  SFW3D_CHECK_ARG(n_sigma > 0 && n_shape > 0, "empty candidate grid");
+  SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
+  int dm[3];
+  for (int a = 0; a < 3; ++a) {
+    SFW3D_CHECK_ARG(dims[a] > 0, "dims must be positive");
+    dm[a] = dims[a];
+  }
+  std::vector<BasisCandidate> bc;
+  for (int i = 0; i < n_sigma; ++i)
+    for (int j = 0; j < n_shape; ++j) {
+      SFW3D_CHECK_ARG(sigmas[i] > 0.0 && shapes[j] > 0.0, "sigma and d must be positive");
+      BasisCandidate c{sigmas[i], shapes[j], {0, 0, 0}, {0, 0, 0}, 0};
+      candidate_box(dm, c.sigma, c.d, c.lo, c.hi);
+      bc.push_back(c);
+    }
+  BasisSet* s = nullptr;
+  const int st = basis_set_build(dm, bc, dtype, tol, &s, /*on_device=*/false);
+  if (st == SFW3D_OK)
+    basis_set_export(s, max_terms, n_terms, betas, weights, w0, fit_err, member);
+  basis_set_destroy(s);
+  return st;
+}
+
 extern "C" int sfw3d_table_destroy(sfw3d_table* t) {
   if (!t) return SFW3D_OK;
   cudaSetDevice(t->device);
@@ -904,12 +662,9 @@ extern "C" int sfw3d_table_destroy(sfw3d_table* t) {
     if (c.t64) cudaFree(c.t64);
     if (c.t32) cudaFree(c.t32);
     if (c.rows_dev) cudaFree(c.rows_dev);
-    for (auto* B : {&c.b32, &c.b64})
-      for (auto& term : B->terms) {
-        if (term.taps64) cudaFree(term.taps64);
-        if (term.taps32) cudaFree(term.taps32);
-      }
   }
+  basis_set_destroy(t->set32);
+  basis_set_destroy(t->set64);
   delete t;
   return SFW3D_OK;
 }
@@ -943,7 +698,7 @@ extern "C" int sfw3d_table_create(sfw3d_ctx* ctx, const sfw3d_psf* psf, int n_si
   for (int i = 0; i < n_sigma; ++i)
     for (int j = 0; j < n_shape; ++j) {
       CandHost& c = t->cands[size_t(i) * n_shape + j];
-      const int s = build_candidate(t->dims, sg[i], dg[j], tap_tol, mode == 0, c);
+      const int s = build_candidate(t->dims, sg[i], dg[j], tap_tol, c);
       if (s != SFW3D_OK) {
         sfw3d_table_destroy(t);
         return s;
@@ -963,6 +718,9 @@ extern "C" int sfw3d_table_create(sfw3d_ctx* ctx, const sfw3d_psf* psf, int n_si
   t->pdims[0] = t->pad[0] + t->dims[0] + maxhi[0];
   t->pdims[1] = t->pad[1] + round_up(t->dims[1], kTY) + maxhi[1] + kTY;
   t->pdims[2] = round_up(t->pad[2] + round_up(t->dims[2], kTZ) + 4 + maxpitch, 4);
+  for (const auto& c : t->cands)
+    t->bcands.push_back(
+        {c.sigma, c.d, {c.lo[0], c.lo[1], c.lo[2]}, {c.hi[0], c.hi[1], c.hi[2]}, c.taps});
   *out = t;
   return SFW3D_OK;
 }
@@ -971,18 +729,22 @@ extern "C" int sfw3d_table_info(const sfw3d_table* t, int dtype, int* n_cand, in
                                 int* n_basis, int64_t* direct_taps, int64_t* basis_taps,
                                 double* direct_flops, double* basis_flops) {
   SFW3D_CHECK_ARG(t, "table is NULL");
+  SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
+  SFW3D_TRY(ensure_basis(t, dtype));
   int nb = 0;
   long long dt = 0, bt = 0;
   double df = 0.0, bf = 0.0;
-  for (const auto& c : t->cands) {
-    if (use_basis(t, c, dtype)) {
+  for (int ci = 0; ci < int(t->cands.size()); ++ci) {
+    if (use_basis(t, ci, dtype)) {
       ++nb;
-      bt += c.basis(dtype).taps;
-      bf += cand_flops(t, c, dtype);
     } else {
-      dt += c.taps;
-      df += cand_flops(t, c, dtype);
+      dt += t->cands[ci].taps;
+      df += cand_flops(t, ci, dtype);
     }
+  }
+  if (nb) {
+    bt = basis_set_taps(t->set(dtype));
+    bf = basis_set_flops(t->set(dtype));
   }
   if (n_cand) *n_cand = int(t->cands.size());
   if (n_direct) *n_direct = int(t->cands.size()) - nb;
@@ -998,14 +760,17 @@ extern "C" int sfw3d_table_candidate(const sfw3d_table* t, int dtype, int cand, 
                                      int* n_terms, double* fit_err, int64_t* direct_taps,
                                      int64_t* basis_taps, double* flops) {
   SFW3D_CHECK_ARG(t && cand >= 0 && cand < int(t->cands.size()), "candidate index");
+  SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
+  SFW3D_TRY(ensure_basis(t, dtype));
   const CandHost& c = t->cands[cand];
-  if (uses_basis) *uses_basis = use_basis(t, c, dtype) ? 1 : 0;
-  const CandHost::Basis& B = c.basis(dtype);
-  if (n_terms) *n_terms = int(B.terms.size()) + (B.w0 != 0.0 ? 1 : 0);
-  if (fit_err) *fit_err = B.fit_err;
+  if (uses_basis) *uses_basis = use_basis(t, cand, dtype) ? 1 : 0;
+  double fe = INFINITY;
+  basis_set_member(t->set(dtype), cand, &fe);
+  if (n_terms) *n_terms = basis_set_n_terms(t->set(dtype));  // shared terms of the table
+  if (fit_err) *fit_err = fe;
   if (direct_taps) *direct_taps = c.taps;
-  if (basis_taps) *basis_taps = B.taps;
-  if (flops) *flops = cand_flops(t, c, dtype);
+  if (basis_taps) *basis_taps = basis_set_taps(t->set(dtype));
+  if (flops) *flops = cand_flops(t, cand, dtype);
   return SFW3D_OK;
 }
 
@@ -1021,7 +786,9 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   const size_t vb = size_t(n) * sizeof(T);
   const int nc = int(t->cands.size());
   bool any_direct = false, any_basis = false;
-  for (const auto& c : t->cands) (use_basis(t, c, dtype) ? any_basis : any_direct) = true;
+  for (int ci = 0; ci < nc; ++ci) (use_basis(t, ci, dtype) ? any_basis : any_direct) = true;
+  const BasisSet* bset = t->set(dtype);
+  const size_t sb = any_basis ? basis_set_scratch(bset, n, dtype) : 0;
   const size_t pb = any_direct ? size_t(t->pdims[0]) * t->pdims[1] * t->pdims[2] * sizeof(T) : 0;
   // direct output tiles: the window, or the whole grid when fields are requested
   int ow[6];
@@ -1035,16 +802,14 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   const int ntz = (ow[5] - zbase + 1 + kTZ - 1) / kTZ;
   const int nxp = ow[1] - ow[0] + 1;
   const long long nblocks_direct = (long long)nty * ntz * nxp;
-  const int nblocks_vol = 4 * ctx->num_sms;
-  const long long nblocks = std::max<long long>(nblocks_direct, nblocks_vol);
+  const long long nblocks = nblocks_direct;
   SFW3D_TRY(ensure_device(ctx, ctx->ws,
-                          Carver::need({vb, vb, any_basis ? vb : 0, any_basis ? vb : 0, pb,
-                                        size_t(nblocks) * sizeof(Best), size_t(nc) * sizeof(Best)})));
+                          Carver::need({vb, vb, sb, pb, size_t(nblocks) * sizeof(Best),
+                                        size_t(nc) * sizeof(Best)})));
   Carver cv(ctx->ws.ptr);
   T* b = cv.take<T>(n);
   T* tmp = cv.take<T>(n);
-  T* t2 = any_basis ? cv.take<T>(n) : nullptr;
-  T* acc = any_basis ? cv.take<T>(n) : nullptr;
+  void* bscratch = sb ? cv.take<char>(sb) : nullptr;
   T* bpad = any_direct ? cv.take<T>(pb / sizeof(T)) : nullptr;
   Best* partial = cv.take<Best>(nblocks);
   Best* cbest = cv.take<Best>(nc);
@@ -1073,34 +838,16 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   int smem_max = 0;
   SFW3D_CUDA_TRY(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
   const int budget = std::min(smem_max - 2048, 110 * 1024);
+  // every basis member at once: shared separable terms + fused mix/argmax,
+  // writing cbest[cand] (and the member fields) directly
+  if (any_basis)
+    SFW3D_TRY(basis_set_eval(ctx, bset, dtype, dims, b, lam, win, fields, cbest, bscratch));
   for (int ci = 0; ci < nc; ++ci) {
+    if (use_basis(t, ci, dtype)) continue;
     const CandHost& c = t->cands[ci];
     T* fld = fields ? static_cast<T*>(fields) + size_t(ci) * n : nullptr;
     long long nred = 0;
-    if (use_basis(t, c, dtype)) {
-      // acc = w0 * b + sum_k w_k (f_k x f_k x f_k) * b   (separable passes)
-      const CandHost::Basis& B = c.basis(dtype);
-      for (size_t k = 0; k < B.terms.size(); ++k) {
-        const Term& term = B.terms[k];
-        const T* taps = static_cast<const T*>(dtype == SFW3D_F64 ? term.taps64 : term.taps32);
-        const int* tl = term.tlen;
-        SFW3D_TRY(corr_pass_impl(ctx, dtype, b, tmp, dims, 2, taps + tl[0] + tl[1], term.tlo[2],
-                                 tl[2], nullptr, 0.0, 1.0, "eta_basis"));
-        SFW3D_TRY(corr_pass_impl(ctx, dtype, tmp, t2, dims, 1, taps + tl[0], term.tlo[1], tl[1],
-                                 nullptr, 0.0, 1.0, "eta_basis"));
-        const void* addend = k == 0 ? (B.w0 != 0.0 ? static_cast<const void*>(b) : nullptr)
-                                    : static_cast<const void*>(acc);
-        const double aw = k == 0 ? B.w0 : 1.0;
-        SFW3D_TRY(corr_pass_impl(ctx, dtype, t2, acc, dims, 0, taps, term.tlo[0], tl[0], addend,
-                                 aw, term.w, "eta_basis"));
-      }
-      SFW3D_PROF(ctx, "argmax");
-      volume_argmax_kernel<T><<<nblocks_vol, 256, 0, ctx->stream>>>(
-          acc, dims[0], dims[1], dims[2], make_int4(win[0], win[2], win[4], 0),
-          make_int4(win[1], win[3], win[5], 0), lam, fld, partial);
-      SFW3D_LAUNCH_CHECK(ctx);
-      nred = nblocks_vol;
-    } else {
+    {
       CandDev cd;
       cd.taps = sizeof(T) == 8 ? static_cast<const void*>(c.t64) : static_cast<const void*>(c.t32);
       cd.rows = c.rows_dev;
@@ -1187,6 +934,7 @@ extern "C" int sfw3d_eta_argmax(sfw3d_ctx* ctx, const sfw3d_table* t, int dtype,
                         window[2 * a + 1] < t->dims[a],
                     "window must be a non-empty box inside the grid");
   SFW3D_TRY(begin_call(ctx));
+  SFW3D_TRY(ensure_basis(t, dtype));
   if (dtype == SFW3D_F64)
     return eta_typed<double>(ctx, t, residual_dev, lam, window, best_host, per_cand_host, fields_dev);
   return eta_typed<float>(ctx, t, residual_dev, lam, window, best_host, per_cand_host, fields_dev);

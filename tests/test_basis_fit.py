@@ -46,3 +46,71 @@ def test_fit_reports_failure_for_d_above_2():
     R = O.support_radius(2.0, 2.5)
     _, _, _, err = N.basis_fit([-R] * 3, [R] * 3, 2.0, 2.5)
     assert err > 1e-3
+
+
+def common_box(dims, sigmas, shapes):
+    """Union of the d <= 2 candidates' support boxes, clipped to the axis."""
+    lo, hi = [0, 0, 0], [0, 0, 0]
+    for s in sigmas:
+        for d in shapes:
+            if d > 2.0:
+                continue
+            R = O.support_radius(s, d)
+            for a in range(3):
+                if 2 * R + 1 >= dims[a]:
+                    l, h = -(dims[a] // 2), dims[a] - 1 - dims[a] // 2
+                else:
+                    l, h = -R, R
+                lo[a], hi[a] = min(lo[a], l), max(hi[a], h)
+    for a in range(3):
+        if hi[a] - lo[a] + 1 > dims[a]:
+            lo[a], hi[a] = -(dims[a] // 2), dims[a] - 1 - dims[a] // 2
+    return lo, hi
+
+
+@pytest.mark.parametrize("name,dims,sigmas,shapes", [
+    ("cfg1", (64,) * 3, [1.5, 2.0, 2.5, 3.0], [1.5, 2.0, 2.5]),
+    ("cfg4", (512,) * 3, [1.0, 1.5, 2.0, 3.0], [1.5, 2.0, 2.5, 3.0]),
+    ("cfg2", (128,) * 3, list(np.geomspace(1, 3, 6)), list(np.linspace(1.2, 2.8, 5))),
+    ("cfg3", (256,) * 3, list(np.geomspace(1, 3, 8)), list(np.linspace(1.5, 2.5, 6))),
+])
+def test_shared_basis_set(name, dims, sigmas, shapes):
+    """The table's shared dictionary fit (f32 storage, basis_tol 1e-9): every
+    member's mixture reproduces its profile on the COMMON box lattice within
+    the reported error (which includes the 1e-12 factor truncation), members
+    are exactly the candidates with fit_err <= tol, d = 2 candidates are one
+    exact term of weight 1 and d > 2 candidates are never members."""
+    tol = 1e-9
+    r = N.basis_set_fit(dims, sigmas, shapes, 0, tol)
+    lo, hi = common_box(dims, sigmas, shapes)
+    s = lattice(lo, hi).astype(float)
+    E = np.exp(-np.outer(s, r["betas"]))
+    assert len(r["betas"]) <= 64 and np.all(np.diff(r["betas"]) > 0)
+    for c, (sg, d) in enumerate([(a, b) for a in sigmas for b in shapes]):
+        err, member, w = r["fit_err"][c], r["member"][c], r["weights"][c]
+        assert member == (err <= tol)
+        if d > 2.0:
+            assert not member and np.isinf(err)
+            continue
+        if d == 2.0:
+            assert member and err == 0.0 and r["w0"][c] == 0.0
+            k = np.flatnonzero(w)
+            assert len(k) == 1 and w[k[0]] == 1.0 and r["betas"][k[0]] == 0.5 / sg ** 2
+            continue
+        if not member:
+            assert np.all(w == 0.0)
+            continue
+        g = np.exp(-0.5 * s ** (d / 2) / sg ** d)
+        approx = r["w0"][c] * (s == 0) + E @ w
+        assert np.all(w >= 0.0) and r["w0"][c] >= 0.0
+        assert abs(np.max(np.abs(approx - g)) + 1e-12 - err) <= 2e-13, (sg, d)
+    # the (cfg) members this grid is expected to route to the basis path
+    n_expected = {"cfg1": 8, "cfg4": 8, "cfg2": 18, "cfg3": 21}[name]
+    assert r["member"].sum() == n_expected
+
+
+def test_shared_basis_set_f64_exact_only():
+    """fp64 storage accepts only fits <= 1e-12: just the exact d = 2 terms."""
+    r = N.basis_set_fit((64,) * 3, [1.5, 2.0, 3.0], [1.5, 2.0, 2.5], 1, 1e-12)
+    assert list(r["member"]) == [False, True, False] * 3
+    assert len(r["betas"]) == 3

@@ -39,12 +39,17 @@ def test_table_fits(P):
     table = P.build_template_table(psf, [1.0, 1.5, 2.0, 3.0], [1.5, 2.0, 2.5, 3.0])
     with P.precision("f32"):
         info = table.info()
+    members = [c for c in info["candidates"] if c["path"] == "basis"]
     for c in info["candidates"]:
-        if c["d"] == 2.0:
-            assert c["path"] == "basis" and c["fit_err"] == 0.0 and c["terms"] == 1
+        if c["d"] == 2.0:  # exactly one shared term (its own beta), weight 1
+            assert c["path"] == "basis" and c["fit_err"] == 0.0
         elif c["d"] < 2.0:
             assert c["path"] == "basis" and c["fit_err"] <= 1e-9
-            assert c["basis_taps"] * 10 < c["direct_taps"]
+        else:
+            assert c["path"] == "direct"
+    # the shared terms' passes cost far less than the members' direct taps
+    assert members[0]["basis_taps"] * 10 < sum(c["direct_taps"] for c in members)
+    assert all(c["terms"] == members[0]["terms"] < 64 for c in members)
     with P.precision("f64"):
         info64 = table.info()
     for c in info64["candidates"]:

@@ -36,8 +36,8 @@ g.manual_seed(1000 + a.seed)
 y_dev = clean + noise * torch.randn(inst.dims, generator=g, device="cuda", dtype=clean.dtype)
 y = P.Volume(y_dev.double().cpu().numpy())
 table = P.build_template_table(psf, inst.sigma_grid, inst.shape_grid, bounds=inst.bounds)
-lam = inst.lam_factor * eta_field_dev(P.forward.to_dev(y) if False else y.device_tensor(
-    y_dev.dtype, y_dev.device), 1.0, table, inst.bounds).eta_max
+lam = inst.lam_factor * eta_field_dev(y.device_tensor(y_dev.dtype, y_dev.device), 1.0, table,
+                                     inst.bounds).eta_max
 orig = solvers.make_parameter_grids
 solvers.make_parameter_grids = lambda b, ns, nd: (inst.sigma_grid, inst.shape_grid)
 opts = P.SolverOptions(lam=lam, max_outer_iterations=a.max_outer or 3 * len(inst.truth))
