@@ -32,7 +32,10 @@
 //   the basis is used only where it is <= basis_tol (fp32 storage) or the
 //   expansion is exact (d == 2, any storage).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <type_traits>
+#include <utility>
 
 #include "basis.cuh"
 
@@ -49,7 +52,7 @@ struct CandHost {
   double* t64 = nullptr;
   float* t32 = nullptr;
   int2* rows_dev = nullptr;
-  double fold_flops = 0.0;  // FP32 flops per voxel of the folded direct kernel
+  double fold_flops[2] = {0.0, 0.0};  // flops per voxel of the folded kernel (f32, f64)
 };
 
 }  // namespace sfw3d
@@ -81,6 +84,10 @@ constexpr int kJ = 16;            // outputs per thread along z
 constexpr int kWarps = 4;         // z-groups per CTA
 constexpr int kTZ = kJ * kWarps;  // 64 outputs along z per CTA
 constexpr int kThreads = 32 * kWarps;
+// folded kernel: outputs per thread along z (fp32 / fp64) and the widest tile
+template <typename T>
+constexpr int fold_kj() { return sizeof(T) == 4 ? 32 : 16; }
+constexpr int kFoldTZMax = 32 * kWarps;
 
 struct CandDev {
   const void* taps;  // dense [la][lb][lc4] of T
@@ -274,99 +281,162 @@ __global__ void __launch_bounds__(kThreads) eta_direct_kernel(const T* __restric
 
 // ---------------------------------------------------------- direct, folded
 // The unit atom is radial: G(a, b, c) = G(+-a, +-b, c). For a box symmetric
-// on axes 0 and 1 the four rows (+-a, +-b) share one tap row, so their
-// inputs are summed first (3 FADD per window element) and correlated once:
-// ~4x fewer FP32-pipe instructions than the plain kernel. The CTA stages the
-// two planes x + a and x - a; everything else mirrors eta_direct_kernel.
-template <typename T, int NR, int R>
-__device__ __forceinline__ void sym_step(T (&acc)[kJ], T (&buf)[20], T (&tc)[4], const T* tnext,
-                                         const T* const (&src)[4], int col) {
-  T n0, n1, n2, n3;
-  ldg4(tnext, n0, n1, n2, n3);
-  // issue the next window columns of all NR rows before the FFMAs so their
-  // shared-memory latency is hidden; sum them afterwards
-  T u[NR][4];
-#pragma unroll
-  for (int q = 0; q < NR; ++q) ld4(src[q] + col, u[q][0], u[q][1], u[q][2], u[q][3]);
-#pragma unroll
-  for (int j = 0; j < kJ; ++j) {
-    acc[j] = fma(tc[0], buf[(4 * R + j + 0) % 20], acc[j]);
-    acc[j] = fma(tc[1], buf[(4 * R + j + 1) % 20], acc[j]);
-    acc[j] = fma(tc[2], buf[(4 * R + j + 2) % 20], acc[j]);
-    acc[j] = fma(tc[3], buf[(4 * R + j + 3) % 20], acc[j]);
-  }
-  T s0 = u[0][0], s1 = u[0][1], s2 = u[0][2], s3 = u[0][3];
-#pragma unroll
-  for (int q = 1; q < NR; ++q) {
-    s0 += u[q][0]; s1 += u[q][1]; s2 += u[q][2]; s3 += u[q][3];
-  }
-  buf[(4 * R) % 20] = s0;
-  buf[(4 * R + 1) % 20] = s1;
-  buf[(4 * R + 2) % 20] = s2;
-  buf[(4 * R + 3) % 20] = s3;
-  tc[0] = n0;
-  tc[1] = n1;
-  tc[2] = n2;
-  tc[3] = n3;
-}
+// on axes 0 and 1 the four rows (x +- a, y +- b) share one tap row. A CTA owns
+// 32 (y) x 4 KJ (z) outputs of one x-plane; per template x-offset a >= 0 it
+// stages the SUMMED plane S_a = P(x + a) + P(x - a) once (one smem plane,
+// one FADD per staged element), and per b >= 0 the thread sums the rows
+// y + b and y - b of S_a (NR = 2) and correlates them with the tap row:
+// ~4x fewer FFMA than the unfolded kernel, one LDS.128 + 4 FADD per 4 KJ
+// FFMA. lane = output row (pitch = 4 mod 8 words: conflict-free LDS.128);
+// each thread slides a (KJ + 4)-register window along z, 4 taps per step:
+//   sum the NR rows' next 4 columns (loaded one step earlier) into the slots
+//   freed by the previous step, issue the loads for the following step and
+//   the next 4 taps, then 4 KJ FFMA (tap-major, KJ independent chains).
+// The window rotation is resolved at compile time (no register moves).
+// Per-slice fp32 partials are added into a shared-memory accumulator.
+template <typename T, int KJ, int NR>
+struct Fold {
+  static constexpr int W = KJ + 4;  // window registers
+  static constexpr int NS = W / 4;  // steps per full rotation
 
-template <typename T, int NR>
-__device__ __forceinline__ void sym_row(T (&acc)[kJ], const T* trow, const T* const (&src)[4],
-                                        int c0, int ns) {
-  T buf[20], tc[4];
-  ldg4(trow, tc[0], tc[1], tc[2], tc[3]);
+  template <int R>
+  static __device__ __forceinline__ void step(T (&acc)[KJ], T (&buf)[W], T (&tc)[4], T (&u)[NR][4],
+                                              const T* __restrict__ tnext,
+                                              const T* const (&q)[NR], int col) {
+    // columns KJ..KJ+3 of this window (loaded last step) into freed slots
 #pragma unroll
-  for (int q = 0; q < 5; ++q) {
-    T s0, s1, s2, s3;
-    ld4(src[0] + c0 + 4 * q, s0, s1, s2, s3);
+    for (int i = 0; i < 4; ++i) buf[(4 * R + KJ + i) % W] = NR == 2 ? u[0][i] + u[NR - 1][i] : u[0][i];
+    // next step's new columns and taps
 #pragma unroll
-    for (int r = 1; r < NR; ++r) {
-      T u0, u1, u2, u3;
-      ld4(src[r] + c0 + 4 * q, u0, u1, u2, u3);
-      s0 += u0; s1 += u1; s2 += u2; s3 += u3;
+    for (int r = 0; r < NR; ++r) ld4(q[r] + col + KJ + 4, u[r][0], u[r][1], u[r][2], u[r][3]);
+    T n0, n1, n2, n3;
+    ldg4(tnext, n0, n1, n2, n3);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int j = 0; j < KJ; ++j) acc[j] = fma(tc[k], buf[(4 * R + j + k) % W], acc[j]);
+    tc[0] = n0;
+    tc[1] = n1;
+    tc[2] = n2;
+    tc[3] = n3;
+  }
+
+  // acc[j] += sum_{c < 4 ns} trow[c] * (sum_r q_r[j + c]),  j < KJ
+  static __device__ __forceinline__ void row(T (&acc)[KJ], const T* __restrict__ trow,
+                                             const T* const (&q)[NR], int ns) {
+    T buf[W], tc[4], u[NR][4];
+    ldg4(trow, tc[0], tc[1], tc[2], tc[3]);
+#pragma unroll
+    for (int g = 0; g < KJ / 4; ++g) {
+      T s0, s1, s2, s3;
+      ld4(q[0] + 4 * g, s0, s1, s2, s3);
+      if constexpr (NR == 2) {
+        T v0, v1, v2, v3;
+        ld4(q[1] + 4 * g, v0, v1, v2, v3);
+        s0 += v0; s1 += v1; s2 += v2; s3 += v3;
+      }
+      buf[4 * g] = s0;
+      buf[4 * g + 1] = s1;
+      buf[4 * g + 2] = s2;
+      buf[4 * g + 3] = s3;
     }
-    buf[4 * q] = s0;
-    buf[4 * q + 1] = s1;
-    buf[4 * q + 2] = s2;
-    buf[4 * q + 3] = s3;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) ld4(q[r] + KJ, u[r][0], u[r][1], u[r][2], u[r][3]);
+    int s = 0;
+    for (; s + NS <= ns; s += NS) unrolled(acc, buf, tc, u, trow, q, s, std::make_integer_sequence<int, NS>{});
+    const int rem = ns - s;
+    tail(acc, buf, tc, u, trow, q, s, rem, std::make_integer_sequence<int, NS - 1>{});
   }
-  int s = 0;
-  for (; s + 5 <= ns; s += 5) {
-    const int c = c0 + 4 * s + 20;
-    sym_step<T, NR, 0>(acc, buf, tc, trow + 4 * s + 4, src, c);
-    sym_step<T, NR, 1>(acc, buf, tc, trow + 4 * s + 8, src, c + 4);
-    sym_step<T, NR, 2>(acc, buf, tc, trow + 4 * s + 12, src, c + 8);
-    sym_step<T, NR, 3>(acc, buf, tc, trow + 4 * s + 16, src, c + 12);
-    sym_step<T, NR, 4>(acc, buf, tc, trow + 4 * s + 20, src, c + 16);
+
+  template <int... R>
+  static __device__ __forceinline__ void unrolled(T (&acc)[KJ], T (&buf)[W], T (&tc)[4],
+                                                  T (&u)[NR][4], const T* trow,
+                                                  const T* const (&q)[NR], int s,
+                                                  std::integer_sequence<int, R...>) {
+    (step<R>(acc, buf, tc, u, trow + 4 * (s + R) + 4, q, 4 * (s + R)), ...);
   }
-  const int rem = ns - s;
-  const int c = c0 + 4 * s + 20;
-  if (rem > 0) sym_step<T, NR, 0>(acc, buf, tc, trow + 4 * s + 4, src, c);
-  if (rem > 1) sym_step<T, NR, 1>(acc, buf, tc, trow + 4 * s + 8, src, c + 4);
-  if (rem > 2) sym_step<T, NR, 2>(acc, buf, tc, trow + 4 * s + 12, src, c + 8);
-  if (rem > 3) sym_step<T, NR, 3>(acc, buf, tc, trow + 4 * s + 16, src, c + 12);
+  template <int... R>
+  static __device__ __forceinline__ void tail(T (&acc)[KJ], T (&buf)[W], T (&tc)[4], T (&u)[NR][4],
+                                              const T* trow, const T* const (&q)[NR], int s,
+                                              int rem, std::integer_sequence<int, R...>) {
+    ((rem > R ? step<R>(acc, buf, tc, u, trow + 4 * (s + R) + 4, q, 4 * (s + R)) : void()), ...);
+  }
+};
+
+// 16-byte vector of 4 fp32 / 2 fp64 (global read-only load, shared store)
+template <typename T>
+struct V16 {
+  using type = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+};
+template <typename T>
+__device__ __forceinline__ typename V16<T>::type vadd(typename V16<T>::type a,
+                                                      typename V16<T>::type b) {
+  if constexpr (sizeof(T) == 4)
+    return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+  else
+    return make_double2(a.x + b.x, a.y + b.y);
 }
 
+// S = P(x + a) [+ P(x - a)]: nrows x pitch elements of two padded planes into
+// one smem plane; batches of kB 16-byte vectors per thread in flight
 template <typename T>
-__global__ void __launch_bounds__(kThreads) eta_sym_kernel(const T* __restrict__ bpad, Geo g,
-                                                           CandDev cd, T* __restrict__ field,
-                                                           Best* __restrict__ partial) {
+__device__ __forceinline__ void stage_sum(T* __restrict__ S, const T* __restrict__ sp,
+                                          const T* __restrict__ sm, int nrows, int pitch,
+                                          long long pys) {
+  using V = typename V16<T>::type;
+  constexpr int kE = 16 / sizeof(T);  // elements per vector
+  constexpr int kB = 4;
+  const int nvec = pitch / kE;
+  const int total = nrows * nvec;
+  // (row, vec) of this thread's first element, advanced by kThreads
+  const int dr = kThreads / nvec, dc = kThreads % nvec;
+  int r = threadIdx.x / nvec, c = threadIdx.x % nvec;
+  for (int e0 = threadIdx.x; e0 < total; e0 += kB * kThreads) {
+    V vp[kB], vm[kB];
+    int off[kB];
+#pragma unroll
+    for (int k = 0; k < kB; ++k) {
+      off[k] = -1;
+      if (e0 + k * kThreads < total) {
+        const long long go = (long long)r * pys + kE * c;
+        off[k] = r * pitch + kE * c;
+        vp[k] = __ldg(reinterpret_cast<const V*>(sp + go));
+        if (sm) vm[k] = __ldg(reinterpret_cast<const V*>(sm + go));
+      }
+      c += dc;
+      r += dr;
+      if (c >= nvec) {
+        c -= nvec;
+        ++r;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kB; ++k)
+      if (off[k] >= 0)
+        *reinterpret_cast<V*>(S + off[k]) = sm ? vadd<T>(vp[k], vm[k]) : vp[k];
+  }
+}
+
+template <typename T, int KJ>
+__global__ void __launch_bounds__(kThreads) eta_fold_kernel(const T* __restrict__ bpad, Geo g,
+                                                            CandDev cd, T* __restrict__ field,
+                                                            Best* __restrict__ partial) {
+  constexpr int TZ = KJ * kWarps;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Best wbest[kWarps];
-  const int nrows = kTY + cd.lb - 1;  // rows of one staged plane (whole b range)
-  T* plane_p = reinterpret_cast<T*>(smem_raw);
-  T* plane_m = plane_p + nrows * g.pitch;
+  const int nrows = kTY + cd.lb - 1;  // rows of the staged plane (whole b range)
+  T* accd = reinterpret_cast<T*>(smem_raw);  // [KJ][kThreads] slice sums
+  T* plane = accd + KJ * kThreads;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ty = blockIdx.x / g.ntz, tz = blockIdx.x % g.ntz;
   const int x = g.ox0 + blockIdx.y;
   const int y0 = g.oy0 + ty * kTY;
-  const int z0 = g.zbase + tz * kTZ;
+  const int z0 = g.zbase + tz * TZ;
   const T* taps = static_cast<const T*>(cd.taps);
   const int Ra = cd.la / 2, Rb = cd.lb / 2;  // symmetric boxes: lo = -R
-
-  T accd[kJ];  // slice partials summed in the storage precision (fp32 error << 1e-5 bar)
 #pragma unroll
-  for (int j = 0; j < kJ; ++j) accd[j] = T(0);
+  for (int j = 0; j < KJ; ++j) accd[j * kThreads + threadIdx.x] = T(0);
+  const long long corner = (long long)(y0 + g.py + cd.lo_b) * g.pys + (z0 + g.pz + cd.cl);
 
   for (int a = 0; a <= Ra; ++a) {
     const int ai = a + Ra;  // template slice index of +a (same taps as -a)
@@ -374,44 +444,29 @@ __global__ void __launch_bounds__(kThreads) eta_sym_kernel(const T* __restrict__
     for (int bi = Rb; bi < cd.lb; ++bi) any |= cd.rows[ai * cd.lb + bi].y > 0;
     if (!any) continue;
     __syncthreads();
-    const int nvec = g.pitch / 4;
-    for (int pl = 0; pl < (a ? 2 : 1); ++pl) {
-      const T* src0 = bpad + (long long)(x + g.px + (pl ? -a : a)) * g.pxs +
-                      (long long)(y0 + g.py + cd.lo_b) * g.pys + (z0 + g.pz + cd.cl);
-      T* dst0 = pl ? plane_m : plane_p;
-      for (int e = threadIdx.x; e < nrows * nvec; e += kThreads) {
-        const int r = e / nvec, c4 = e % nvec;
-        const T* s = src0 + (long long)r * g.pys + 4 * c4;
-        T* d = dst0 + r * g.pitch + 4 * c4;
-        cp_async16(d, s);
-        if constexpr (sizeof(T) == 8) cp_async16(d + 2, s + 2);
-      }
-    }
-    cp_async_wait_all();
+    stage_sum<T>(plane, bpad + (long long)(x + g.px + a) * g.pxs + corner,
+                 a ? bpad + (long long)(x + g.px - a) * g.pxs + corner : nullptr, nrows, g.pitch,
+                 g.pys);
     __syncthreads();
-    T acc[kJ];
+    T acc[KJ];
 #pragma unroll
-    for (int j = 0; j < kJ; ++j) acc[j] = T(0);
+    for (int j = 0; j < KJ; ++j) acc[j] = T(0);
     for (int b = 0; b <= Rb; ++b) {
       const int2 rr = cd.rows[ai * cd.lb + b + Rb];
       if (rr.y <= 0) continue;
       const T* trow = taps + ((long long)ai * cd.lb + b + Rb) * cd.lc4 + 4 * rr.x;
-      const int c0 = warp * kJ + 4 * rr.x;
-      const T* src[4] = {plane_p + (lane + Rb + b) * g.pitch, plane_p + (lane + Rb - b) * g.pitch,
-                         plane_m + (lane + Rb + b) * g.pitch, plane_m + (lane + Rb - b) * g.pitch};
-      if (a == 0 && b == 0) {
-        sym_row<T, 1>(acc, trow, src, c0, rr.y);
-      } else if (a == 0) {
-        sym_row<T, 2>(acc, trow, src, c0, rr.y);
-      } else if (b == 0) {
-        const T* s2[4] = {src[0], src[2], src[0], src[0]};
-        sym_row<T, 2>(acc, trow, s2, c0, rr.y);
+      const int c0 = warp * KJ + 4 * rr.x;
+      const T* pp = plane + (lane + Rb + b) * g.pitch + c0;
+      if (b == 0) {
+        const T* const q[1] = {pp};
+        Fold<T, KJ, 1>::row(acc, trow, q, rr.y);
       } else {
-        sym_row<T, 4>(acc, trow, src, c0, rr.y);
+        const T* const q[2] = {pp, plane + (lane + Rb - b) * g.pitch + c0};
+        Fold<T, KJ, 2>::row(acc, trow, q, rr.y);
       }
     }
 #pragma unroll
-    for (int j = 0; j < kJ; ++j) accd[j] += acc[j];
+    for (int j = 0; j < KJ; ++j) accd[j * kThreads + threadIdx.x] += acc[j];
   }
 
   const int y = y0 + lane;
@@ -419,10 +474,10 @@ __global__ void __launch_bounds__(kThreads) eta_sym_kernel(const T* __restrict__
   const bool row_ok = y < g.ny;
   const bool row_win = x >= g.win[0] && x <= g.win[1] && y >= g.win[2] && y <= g.win[3];
 #pragma unroll
-  for (int j = 0; j < kJ; ++j) {
-    const int z = z0 + warp * kJ + j;
+  for (int j = 0; j < KJ; ++j) {
+    const int z = z0 + warp * KJ + j;
     if (!row_ok || z >= g.nz) continue;
-    const double eta = double(accd[j]) / g.lam;
+    const double eta = double(accd[j * kThreads + threadIdx.x]) / g.lam;
     const long long lin = ((long long)x * g.ny + y) * g.nz + z;
     if (field) field[lin] = T(eta);
     if (row_win && z >= g.win[4] && z <= g.win[5] && better(eta, lin, best.v, best.idx))
@@ -459,14 +514,16 @@ __global__ void best_reduce_kernel(const Best* __restrict__ partial, long long n
 
 int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
-// smem row pitch: >= cols needed, and == 4 (mod 32) elements for fp32
-// (conflict-free LDS.128 across 8 consecutive rows); fp64 uses == 4 (mod 16).
-int region_pitch(int lc4, int esize) {
-  int p = round_up(lc4 + kTZ + 8, 4);
+// smem row pitch (elements): >= cols needed, and the 16-byte chunk index of
+// consecutive rows advances by an odd number, so the 8 lanes of one LDS.128
+// wavefront (lane = row) hit 8 distinct 4-bank groups: fp32 pitch == 4 (mod 8),
+// fp64 pitch == 2 (mod 4). (Rows stay 16-byte aligned for cp.async.)
+int region_pitch(int lc4, int esize, int tz = kTZ) {
+  int p = round_up(lc4 + tz + 8, 4);
   if (esize == 4) {
-    while (p % 32 != 4) p += 4;
+    if (p % 8 != 4) p += 4;
   } else {
-    while (p % 16 != 4) p += 4;
+    p += 2;
   }
   return p;
 }
@@ -534,9 +591,10 @@ static int build_candidate(const int dims[3], double sigma, double d, double tap
       }
     }
   }
-  // executed flops of the folded kernel (eta_sym_kernel): per (a >= 0, b >= 0)
-  // tap row, 4 FMA per step and (NR - 1) window sums per 4 columns, where NR
-  // rows (+-a, +-b) share the row; each thread owns 16 outputs
+  // executed flops of the folded kernel (eta_fold_kernel): per (a >= 0, b >= 0)
+  // tap row, 4 FMA per step and (NR - 1) sums per window column, where NR
+  // rows (+-a, +-b) share the row; each thread owns KJ outputs and its window
+  // spans KJ + 4 * nsteps columns
   if (c.lo[0] == -c.hi[0] && c.lo[1] == -c.hi[1]) {
     const int Ra = c.hi[0], Rb = c.hi[1];
     for (int a = 0; a <= Ra; ++a)
@@ -544,7 +602,10 @@ static int build_candidate(const int dims[3], double sigma, double d, double tap
         const int2 rr = c.rows[size_t(a + Ra) * c.lb + (b + Rb)];
         if (rr.y <= 0) continue;
         const int nr = (a ? 2 : 1) * (b ? 2 : 1);
-        c.fold_flops += 2.0 * 4.0 * rr.y + double(nr - 1) * (4.0 * rr.y + 20.0) / 16.0;
+        for (int k = 0; k < 2; ++k) {
+          const double kj = k == 0 ? fold_kj<float>() : fold_kj<double>();
+          c.fold_flops[k] += 2.0 * 4.0 * rr.y + double(nr - 1) * (4.0 * rr.y + kj) / kj;
+        }
       }
   }
   std::vector<float> t32(t.begin(), t.end());
@@ -583,11 +644,25 @@ static bool use_basis(const sfw3d_table* t, int ci, int dtype) {
   return t->mode == 0 && basis_set_member(t->set(dtype), ci, nullptr);
 }
 
+// folded kernel tile: outputs per thread (fp32 default 32, SFW3D_FOLD_KJ=16
+// for tuning; fp64 16), z extent, smem row pitch and dynamic smem bytes
+static int fold_kj_rt(int esize) {
+  static const int kj32 = [] {
+    const char* e = getenv("SFW3D_FOLD_KJ");
+    return e && atoi(e) == 16 ? 16 : 32;
+  }();
+  return esize == 8 ? 16 : kj32;
+}
+static int fold_tz(int esize) { return fold_kj_rt(esize) * kWarps; }
+static int fold_smem(const CandHost& c, int esize) {
+  const int kj = fold_tz(esize) / kWarps;
+  return (kj * kThreads + (kTY + c.lb - 1) * region_pitch(c.lc4, esize, fold_tz(esize))) * esize;
+}
+
 static bool use_sym(const sfw3d_table* t, const CandHost& c, int dtype) {
   const int esize = dtype == SFW3D_F64 ? 8 : 4;
   const bool sym = c.lo[0] == -c.hi[0] && c.lo[1] == -c.hi[1];
-  const int smem_sym = 2 * (kTY + c.lb - 1) * region_pitch(c.lc4, esize) * esize;
-  return sym && smem_sym <= std::min(t->smem_max - 2048, 160 * 1024);
+  return sym && fold_smem(c, esize) <= std::min(t->smem_max - 2048, 200 * 1024);
 }
 
 // executed flops per voxel attributed to one candidate (basis members share
@@ -598,7 +673,7 @@ static double cand_flops(const sfw3d_table* t, int ci, int dtype) {
     const BasisSet* s = t->set(dtype);
     return 2.0 * double(basis_set_taps(s)) / basis_set_n_members(s) + basis_set_member_flops(s);
   }
-  return use_sym(t, c, dtype) ? c.fold_flops : 2.0 * double(c.taps);
+  return use_sym(t, c, dtype) ? c.fold_flops[dtype == SFW3D_F64 ? 1 : 0] : 2.0 * double(c.taps);
 }
 
 }  // namespace sfw3d
@@ -708,7 +783,8 @@ extern "C" int sfw3d_table_create(sfw3d_ctx* ctx, const sfw3d_psf* psf, int n_si
       maxlo[1] = std::max(maxlo[1], -c.lo[1]);
       maxhi[1] = std::max(maxhi[1], c.hi[1]);
       maxlo[2] = std::max(maxlo[2], -c.cl);
-      maxpitch = std::max(maxpitch, std::max(region_pitch(c.lc4, 8), region_pitch(c.lc4, 4)));
+      maxpitch = std::max(maxpitch, std::max(region_pitch(c.lc4, 8, kFoldTZMax),
+                                             region_pitch(c.lc4, 4, kFoldTZMax)));
     }
   // padded b: x/y pads cover the template offsets (+ the last partial tile
   // in y), z covers the aligned template start and the widest staged row.
@@ -717,7 +793,7 @@ extern "C" int sfw3d_table_create(sfw3d_ctx* ctx, const sfw3d_psf* psf, int n_si
   t->pad[2] = round_up(maxlo[2], 4);
   t->pdims[0] = t->pad[0] + t->dims[0] + maxhi[0];
   t->pdims[1] = t->pad[1] + round_up(t->dims[1], kTY) + maxhi[1] + kTY;
-  t->pdims[2] = round_up(t->pad[2] + round_up(t->dims[2], kTZ) + 4 + maxpitch, 4);
+  t->pdims[2] = round_up(t->pad[2] + round_up(t->dims[2], kFoldTZMax) + 4 + maxpitch, 4);
   for (const auto& c : t->cands)
     t->bcands.push_back(
         {c.sigma, c.d, {c.lo[0], c.lo[1], c.lo[2]}, {c.hi[0], c.hi[1], c.hi[2]}, c.taps});
@@ -858,18 +934,32 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
       cd.cl = c.cl;
       cd.lc4 = c.lc4;
       Geo gc = g;
-      gc.pitch = region_pitch(c.lc4, sizeof(T));
-      const int row_bytes = gc.pitch * int(sizeof(T));
-      dim3 grid(unsigned(nty * ntz), unsigned(nxp));
-      const int smem_sym = 2 * (kTY + c.lb - 1) * row_bytes;
       if (use_sym(t, c, dtype)) {
+        const int kj = fold_kj_rt(sizeof(T));
+        const int TZ = kj * kWarps;
+        gc.pitch = region_pitch(c.lc4, sizeof(T), TZ);
+        gc.ntz = (ow[5] - zbase + 1 + TZ - 1) / TZ;
         gc.brows = c.lb;
-        SFW3D_CUDA_TRY(cudaFuncSetAttribute(eta_sym_kernel<T>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem_sym));
+        const int smem = fold_smem(c, sizeof(T));
         SFW3D_PROF(ctx, "eta_direct");
-        eta_sym_kernel<T><<<grid, kThreads, smem_sym, ctx->stream>>>(bpad, gc, cd, fld, partial);
+        dim3 grid(unsigned(nty * gc.ntz), unsigned(nxp));
+        if constexpr (sizeof(T) == 4) {
+          if (kj == 32) {
+            SFW3D_CUDA_TRY(cudaFuncSetAttribute(eta_fold_kernel<T, 32>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            eta_fold_kernel<T, 32><<<grid, kThreads, smem, ctx->stream>>>(bpad, gc, cd, fld, partial);
+          }
+        }
+        if (kj == 16) {
+          SFW3D_CUDA_TRY(cudaFuncSetAttribute(eta_fold_kernel<T, 16>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+          eta_fold_kernel<T, 16><<<grid, kThreads, smem, ctx->stream>>>(bpad, gc, cd, fld, partial);
+        }
         SFW3D_LAUNCH_CHECK(ctx);
+        nred = (long long)nty * gc.ntz * nxp;
       } else {
+        gc.pitch = region_pitch(c.lc4, sizeof(T));
+        const int row_bytes = gc.pitch * int(sizeof(T));
         const int brows = budget / row_bytes - (kTY - 1);
         if (brows < 1) {
           set_error("certificate template too wide for the shared-memory tile");
@@ -880,10 +970,11 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
         SFW3D_CUDA_TRY(cudaFuncSetAttribute(eta_direct_kernel<T>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         SFW3D_PROF(ctx, "eta_direct");
+        dim3 grid(unsigned(nty * ntz), unsigned(nxp));
         eta_direct_kernel<T><<<grid, kThreads, smem, ctx->stream>>>(bpad, gc, cd, fld, partial);
         SFW3D_LAUNCH_CHECK(ctx);
+        nred = nblocks_direct;
       }
-      nred = nblocks_direct;
     }
     {
       SFW3D_PROF(ctx, "argmax");
