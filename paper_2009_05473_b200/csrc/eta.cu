@@ -120,6 +120,22 @@ __device__ __forceinline__ void ld4(const T* p, T& a, T& b, T& c, T& d) {
   }
 }
 
+// shared-memory 4-vector load as a volatile asm statement: ptxas keeps the
+// program order of these loads, so the folded kernel's loads stay exactly one
+// step ahead of their use instead of being hoisted (register pressure)
+template <typename T>
+__device__ __forceinline__ void lds4v(const T* p, T& a, T& b, T& c, T& d) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(p));
+  if constexpr (sizeof(T) == 4) {
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(a), "=f"(b), "=f"(c), "=f"(d)
+                 : "r"(sa));
+  } else {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(sa));
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(c), "=d"(d) : "r"(sa + 16));
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ void ldg4(const T* p, T& a, T& b, T& c, T& d) {
   if constexpr (sizeof(T) == 4) {
@@ -308,9 +324,9 @@ struct Fold {
     for (int i = 0; i < 4; ++i) buf[(4 * R + KJ + i) % W] = NR == 2 ? u[0][i] + u[NR - 1][i] : u[0][i];
     // next step's new columns and taps
 #pragma unroll
-    for (int r = 0; r < NR; ++r) ld4(q[r] + col + KJ + 4, u[r][0], u[r][1], u[r][2], u[r][3]);
+    for (int r = 0; r < NR; ++r) lds4v(q[r] + col + KJ + 4, u[r][0], u[r][1], u[r][2], u[r][3]);
     T n0, n1, n2, n3;
-    ldg4(tnext, n0, n1, n2, n3);
+    lds4v(tnext, n0, n1, n2, n3);  // shared-memory tap row (broadcast)
 #pragma unroll
     for (int k = 0; k < 4; ++k)
 #pragma unroll
@@ -325,7 +341,7 @@ struct Fold {
   static __device__ __forceinline__ void row(T (&acc)[KJ], const T* __restrict__ trow,
                                              const T* const (&q)[NR], int ns) {
     T buf[W], tc[4], u[NR][4];
-    ldg4(trow, tc[0], tc[1], tc[2], tc[3]);
+    ld4(trow, tc[0], tc[1], tc[2], tc[3]);
 #pragma unroll
     for (int g = 0; g < KJ / 4; ++g) {
       T s0, s1, s2, s3;
@@ -379,7 +395,7 @@ __device__ __forceinline__ typename V16<T>::type vadd(typename V16<T>::type a,
 
 // S = P(x + a) [+ P(x - a)]: nrows x pitch elements of two padded planes into
 // one smem plane; batches of kB 16-byte vectors per thread in flight
-template <typename T>
+template <typename T, int NT>
 __device__ __forceinline__ void stage_sum(T* __restrict__ S, const T* __restrict__ sp,
                                           const T* __restrict__ sm, int nrows, int pitch,
                                           long long pys) {
@@ -388,16 +404,16 @@ __device__ __forceinline__ void stage_sum(T* __restrict__ S, const T* __restrict
   constexpr int kB = 4;
   const int nvec = pitch / kE;
   const int total = nrows * nvec;
-  // (row, vec) of this thread's first element, advanced by kThreads
-  const int dr = kThreads / nvec, dc = kThreads % nvec;
+  // (row, vec) of this thread's first element, advanced by NT
+  const int dr = NT / nvec, dc = NT % nvec;
   int r = threadIdx.x / nvec, c = threadIdx.x % nvec;
-  for (int e0 = threadIdx.x; e0 < total; e0 += kB * kThreads) {
+  for (int e0 = threadIdx.x; e0 < total; e0 += kB * NT) {
     V vp[kB], vm[kB];
     int off[kB];
 #pragma unroll
     for (int k = 0; k < kB; ++k) {
       off[k] = -1;
-      if (e0 + k * kThreads < total) {
+      if (e0 + k * NT < total) {
         const long long go = (long long)r * pys + kE * c;
         off[k] = r * pitch + kE * c;
         vp[k] = __ldg(reinterpret_cast<const V*>(sp + go));
@@ -417,25 +433,34 @@ __device__ __forceinline__ void stage_sum(T* __restrict__ S, const T* __restrict
   }
 }
 
-template <typename T, int KJ>
-__global__ void __launch_bounds__(kThreads) eta_fold_kernel(const T* __restrict__ bpad, Geo g,
-                                                            CandDev cd, T* __restrict__ field,
-                                                            Best* __restrict__ partial) {
-  constexpr int TZ = KJ * kWarps;
+// resident CTAs per SM the register budget is sized for (fp32 tiles)
+template <typename T, int KJ, int NWY>
+constexpr int fold_min_blocks() {
+  return sizeof(T) == 8 ? 1 : (NWY == 2 ? 2 : (KJ == 32 ? 3 : 4));
+}
+
+template <typename T, int KJ, int NWY>
+__global__ void __launch_bounds__(kThreads * NWY, (fold_min_blocks<T, KJ, NWY>())) eta_fold_kernel(const T* __restrict__ bpad, Geo g,
+                                                                  CandDev cd, T* __restrict__ field,
+                                                                  Best* __restrict__ partial) {
+  constexpr int NT = kThreads * NWY, TY = kTY * NWY, TZ = KJ * kWarps;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ Best wbest[kWarps];
-  const int nrows = kTY + cd.lb - 1;  // rows of the staged plane (whole b range)
-  T* accd = reinterpret_cast<T*>(smem_raw);  // [KJ][kThreads] slice sums
-  T* plane = accd + KJ * kThreads;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ Best wbest[kWarps * NWY];
+  const int nrows = TY + cd.lb - 1;  // rows of the staged plane (whole b range)
+  T* accd = reinterpret_cast<T*>(smem_raw);  // [KJ][NT] slice sums
+  T* stap = accd + KJ * NT;                   // [Rb + 1][lc4] tap rows b >= 0 (+8)
+  const int ntap = (cd.lb / 2 + 1) * cd.lc4;
+  T* plane = stap + ((ntap + 8 + 3) & ~3);
+  const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) % kWarps;
+  const int ylane = (threadIdx.x >> 5) / kWarps * kTY + lane;  // output row in the tile
   const int ty = blockIdx.x / g.ntz, tz = blockIdx.x % g.ntz;
   const int x = g.ox0 + blockIdx.y;
-  const int y0 = g.oy0 + ty * kTY;
+  const int y0 = g.oy0 + ty * TY;
   const int z0 = g.zbase + tz * TZ;
   const T* taps = static_cast<const T*>(cd.taps);
   const int Ra = cd.la / 2, Rb = cd.lb / 2;  // symmetric boxes: lo = -R
 #pragma unroll
-  for (int j = 0; j < KJ; ++j) accd[j * kThreads + threadIdx.x] = T(0);
+  for (int j = 0; j < KJ; ++j) accd[j * NT + threadIdx.x] = T(0);
   const long long corner = (long long)(y0 + g.py + cd.lo_b) * g.pys + (z0 + g.pz + cd.cl);
 
   for (int a = 0; a <= Ra; ++a) {
@@ -444,9 +469,13 @@ __global__ void __launch_bounds__(kThreads) eta_fold_kernel(const T* __restrict_
     for (int bi = Rb; bi < cd.lb; ++bi) any |= cd.rows[ai * cd.lb + bi].y > 0;
     if (!any) continue;
     __syncthreads();
-    stage_sum<T>(plane, bpad + (long long)(x + g.px + a) * g.pxs + corner,
-                 a ? bpad + (long long)(x + g.px - a) * g.pxs + corner : nullptr, nrows, g.pitch,
-                 g.pys);
+    {
+      const T* tsrc = taps + ((long long)ai * cd.lb + Rb) * cd.lc4;
+      for (int e = threadIdx.x; e < ntap + 8; e += NT) stap[e] = e < ntap ? tsrc[e] : T(0);
+    }
+    stage_sum<T, NT>(plane, bpad + (long long)(x + g.px + a) * g.pxs + corner,
+                     a ? bpad + (long long)(x + g.px - a) * g.pxs + corner : nullptr, nrows,
+                     g.pitch, g.pys);
     __syncthreads();
     T acc[KJ];
 #pragma unroll
@@ -454,22 +483,22 @@ __global__ void __launch_bounds__(kThreads) eta_fold_kernel(const T* __restrict_
     for (int b = 0; b <= Rb; ++b) {
       const int2 rr = cd.rows[ai * cd.lb + b + Rb];
       if (rr.y <= 0) continue;
-      const T* trow = taps + ((long long)ai * cd.lb + b + Rb) * cd.lc4 + 4 * rr.x;
+      const T* trow = stap + b * cd.lc4 + 4 * rr.x;
       const int c0 = warp * KJ + 4 * rr.x;
-      const T* pp = plane + (lane + Rb + b) * g.pitch + c0;
+      const T* pp = plane + (ylane + Rb + b) * g.pitch + c0;
       if (b == 0) {
         const T* const q[1] = {pp};
         Fold<T, KJ, 1>::row(acc, trow, q, rr.y);
       } else {
-        const T* const q[2] = {pp, plane + (lane + Rb - b) * g.pitch + c0};
+        const T* const q[2] = {pp, plane + (ylane + Rb - b) * g.pitch + c0};
         Fold<T, KJ, 2>::row(acc, trow, q, rr.y);
       }
     }
 #pragma unroll
-    for (int j = 0; j < KJ; ++j) accd[j * kThreads + threadIdx.x] += acc[j];
+    for (int j = 0; j < KJ; ++j) accd[j * NT + threadIdx.x] += acc[j];
   }
 
-  const int y = y0 + lane;
+  const int y = y0 + ylane;
   Best best{-INFINITY, 0x7fffffffffffffffLL};
   const bool row_ok = y < g.ny;
   const bool row_win = x >= g.win[0] && x <= g.win[1] && y >= g.win[2] && y <= g.win[3];
@@ -477,7 +506,7 @@ __global__ void __launch_bounds__(kThreads) eta_fold_kernel(const T* __restrict_
   for (int j = 0; j < KJ; ++j) {
     const int z = z0 + warp * KJ + j;
     if (!row_ok || z >= g.nz) continue;
-    const double eta = double(accd[j * kThreads + threadIdx.x]) / g.lam;
+    const double eta = double(accd[j * NT + threadIdx.x]) / g.lam;
     const long long lin = ((long long)x * g.ny + y) * g.nz + z;
     if (field) field[lin] = T(eta);
     if (row_win && z >= g.win[4] && z <= g.win[5] && better(eta, lin, best.v, best.idx))
@@ -644,19 +673,37 @@ static bool use_basis(const sfw3d_table* t, int ci, int dtype) {
   return t->mode == 0 && basis_set_member(t->set(dtype), ci, nullptr);
 }
 
-// folded kernel tile: outputs per thread (fp32 default 32, SFW3D_FOLD_KJ=16
-// for tuning; fp64 16), z extent, smem row pitch and dynamic smem bytes
+// folded kernel tile: outputs per thread along z (fp32 32, fp64 16) and
+// y rows (32 x NWY, fp32 NWY = 2); SFW3D_FOLD_KJ / SFW3D_FOLD_NWY override
+// the fp32 choice for tuning. z extent, smem row pitch, dynamic smem bytes.
+static int env_int(const char* name, int def) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : def;
+}
 static int fold_kj_rt(int esize) {
-  static const int kj32 = [] {
-    const char* e = getenv("SFW3D_FOLD_KJ");
-    return e && atoi(e) == 16 ? 16 : 32;
-  }();
+  static const int kj32 = env_int("SFW3D_FOLD_KJ", 32) == 16 ? 16 : 32;
   return esize == 8 ? 16 : kj32;
+}
+static int fold_nwy_rt(int esize) {
+  static const int nwy32 = env_int("SFW3D_FOLD_NWY", 1) == 2 ? 2 : 1;
+  return esize == 8 ? 1 : nwy32;
 }
 static int fold_tz(int esize) { return fold_kj_rt(esize) * kWarps; }
 static int fold_smem(const CandHost& c, int esize) {
-  const int kj = fold_tz(esize) / kWarps;
-  return (kj * kThreads + (kTY + c.lb - 1) * region_pitch(c.lc4, esize, fold_tz(esize))) * esize;
+  const int kj = fold_kj_rt(esize), nwy = fold_nwy_rt(esize);
+  const int ntap = ((c.lb / 2 + 1) * c.lc4 + 8 + 3) & ~3;
+  return (kj * kThreads * nwy + ntap +
+          (kTY * nwy + c.lb - 1) * region_pitch(c.lc4, esize, fold_tz(esize))) * esize;
+}
+
+template <typename T, int KJ, int NWY>
+static int launch_fold(sfw3d_ctx* ctx, dim3 grid, int smem, const T* bpad, const Geo& g,
+                       const CandDev& cd, T* fld, Best* partial) {
+  SFW3D_CUDA_TRY(cudaFuncSetAttribute(eta_fold_kernel<T, KJ, NWY>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  eta_fold_kernel<T, KJ, NWY><<<grid, kThreads * NWY, smem, ctx->stream>>>(bpad, g, cd, fld, partial);
+  SFW3D_LAUNCH_CHECK(ctx);
+  return SFW3D_OK;
 }
 
 static bool use_sym(const sfw3d_table* t, const CandHost& c, int dtype) {
@@ -935,28 +982,28 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
       cd.lc4 = c.lc4;
       Geo gc = g;
       if (use_sym(t, c, dtype)) {
-        const int kj = fold_kj_rt(sizeof(T));
-        const int TZ = kj * kWarps;
+        const int kj = fold_kj_rt(sizeof(T)), nwy = fold_nwy_rt(sizeof(T));
+        const int TZ = kj * kWarps, TY = kTY * nwy;
         gc.pitch = region_pitch(c.lc4, sizeof(T), TZ);
         gc.ntz = (ow[5] - zbase + 1 + TZ - 1) / TZ;
+        gc.nty = (ow[3] - ow[2] + 1 + TY - 1) / TY;
         gc.brows = c.lb;
         const int smem = fold_smem(c, sizeof(T));
         SFW3D_PROF(ctx, "eta_direct");
-        dim3 grid(unsigned(nty * gc.ntz), unsigned(nxp));
+        dim3 grid(unsigned(gc.nty * gc.ntz), unsigned(nxp));
         if constexpr (sizeof(T) == 4) {
-          if (kj == 32) {
-            SFW3D_CUDA_TRY(cudaFuncSetAttribute(eta_fold_kernel<T, 32>,
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            eta_fold_kernel<T, 32><<<grid, kThreads, smem, ctx->stream>>>(bpad, gc, cd, fld, partial);
-          }
+          if (kj == 32 && nwy == 2)
+            SFW3D_TRY((launch_fold<T, 32, 2>(ctx, grid, smem, bpad, gc, cd, fld, partial)));
+          else if (kj == 32)
+            SFW3D_TRY((launch_fold<T, 32, 1>(ctx, grid, smem, bpad, gc, cd, fld, partial)));
+          else if (nwy == 2)
+            SFW3D_TRY((launch_fold<T, 16, 2>(ctx, grid, smem, bpad, gc, cd, fld, partial)));
+          else
+            SFW3D_TRY((launch_fold<T, 16, 1>(ctx, grid, smem, bpad, gc, cd, fld, partial)));
+        } else {
+          SFW3D_TRY((launch_fold<T, 16, 1>(ctx, grid, smem, bpad, gc, cd, fld, partial)));
         }
-        if (kj == 16) {
-          SFW3D_CUDA_TRY(cudaFuncSetAttribute(eta_fold_kernel<T, 16>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-          eta_fold_kernel<T, 16><<<grid, kThreads, smem, ctx->stream>>>(bpad, gc, cd, fld, partial);
-        }
-        SFW3D_LAUNCH_CHECK(ctx);
-        nred = (long long)nty * gc.ntz * nxp;
+        nred = (long long)gc.nty * gc.ntz * nxp;
       } else {
         gc.pitch = region_pitch(c.lc4, sizeof(T));
         const int row_bytes = gc.pitch * int(sizeof(T));
