@@ -341,14 +341,14 @@ struct Fold {
   static __device__ __forceinline__ void row(T (&acc)[KJ], const T* __restrict__ trow,
                                              const T* const (&q)[NR], int ns) {
     T buf[W], tc[4], u[NR][4];
-    ld4(trow, tc[0], tc[1], tc[2], tc[3]);
+    lds4v(trow, tc[0], tc[1], tc[2], tc[3]);
 #pragma unroll
     for (int g = 0; g < KJ / 4; ++g) {
       T s0, s1, s2, s3;
-      ld4(q[0] + 4 * g, s0, s1, s2, s3);
+      lds4v(q[0] + 4 * g, s0, s1, s2, s3);
       if constexpr (NR == 2) {
         T v0, v1, v2, v3;
-        ld4(q[1] + 4 * g, v0, v1, v2, v3);
+        lds4v(q[1] + 4 * g, v0, v1, v2, v3);
         s0 += v0; s1 += v1; s2 += v2; s3 += v3;
       }
       buf[4 * g] = s0;
@@ -357,7 +357,7 @@ struct Fold {
       buf[4 * g + 3] = s3;
     }
 #pragma unroll
-    for (int r = 0; r < NR; ++r) ld4(q[r] + KJ, u[r][0], u[r][1], u[r][2], u[r][3]);
+    for (int r = 0; r < NR; ++r) lds4v(q[r] + KJ, u[r][0], u[r][1], u[r][2], u[r][3]);
     int s = 0;
     for (; s + NS <= ns; s += NS) unrolled(acc, buf, tc, u, trow, q, s, std::make_integer_sequence<int, NS>{});
     const int rem = ns - s;
