@@ -18,6 +18,7 @@
 #include <cstdlib>
 
 #include "internal.cuh"
+#include "window.cuh"
 
 namespace sfw3d {
 namespace {
@@ -136,12 +137,19 @@ __global__ void __launch_bounds__(NT) pass_tiled_kernel(
       W[r] = src[(q0 + r + J) * kTInner];
     }
   }
+  {
+    const int a1 = a0 + ag * J;
+    const long long o0 = base0 + (long long)a1 * stride + il;
+    T* po = out + o0;
+    if (addend) {
+      const T* pa = addend + o0;
 #pragma unroll
-  for (int j = 0; j < J; ++j) {
-    const int a = a0 + ag * J + j;
-    if (a < n_axis) {
-      const long long o = base0 + (long long)a * stride + il;
-      out[o] = addend ? T(aw * addend[o] + w * acc[j]) : T(w * acc[j]);
+      for (int j = 0; j < J; ++j, po += stride, pa += stride)
+        if (a1 + j < n_axis) *po = T(aw * *pa + w * acc[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < J; ++j, po += stride)
+        if (a1 + j < n_axis) *po = T(w * acc[j]);
     }
   }
 }
@@ -208,6 +216,181 @@ __global__ void __launch_bounds__(32 * kZWarps) pass_z_kernel(
   const int ncols = J * kZWarps;
   for (int e = threadIdx.x; e < kZRows * ncols; e += blockDim.x) {
     const int r = e / ncols, c = e % ncols;
+    const long long row = row0 + r;
+    const int z = z0 + c;
+    if (row < nrows && z < nz) {
+      const long long o = row * nz + z;
+      const T v = tile[r * pitch + c];
+      out[o] = addend ? T(aw * addend[o] + w * v) : T(w * v);
+    }
+  }
+}
+
+// ------------------------------------------------------------ v2 passes
+// Register-window passes with ~94% FFMA issue density: taps padded only to a
+// multiple of 4 (the window consumes 4 taps per step), the staged tile reused
+// by J outputs per thread, incremental wrap arithmetic in the staging loops.
+
+// Strided axes (0, 1): a CTA owns TI consecutive inner (contiguous) indices
+// x G groups of J consecutive outputs along the axis. Rows a0 + lo + r
+// (wrapped) are staged with 16-byte cp.async; lane = inner index (conflict-
+// free scalar smem reads, coalesced 128-byte stores). Per tap: one LDS of the
+// next window row + J FFMA (taps read four at a time, broadcast).
+template <typename T, int J, int TI, int NT>
+__global__ void __launch_bounds__(NT) pass_tile2_kernel(
+    const T* __restrict__ in, T* __restrict__ out, int n_axis, long long stride,
+    const T* __restrict__ taps_g, int lo, int ntaps, const T* addend, T aw, T w) {
+  constexpr int G = NT / TI, To = J * G;
+  constexpr int kVec = 16 / sizeof(T), kRowVecs = TI / kVec;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int nt4 = (ntaps + 3) & ~3;
+  T* taps = reinterpret_cast<T*>(smem_raw);
+  T* tile = taps + nt4;
+  const int rows = To + nt4;
+  const int a0 = blockIdx.x * To;
+  const long long base0 = (long long)blockIdx.z * n_axis * stride + (long long)blockIdx.y * TI;
+  for (int q = threadIdx.x; q < nt4; q += NT) taps[q] = q < ntaps ? taps_g[q] : T(0);
+  {
+    static_assert(NT % kRowVecs == 0, "row vectors");
+    constexpr int dr = NT / kRowVecs;
+    const int c = (threadIdx.x % kRowVecs) * kVec;
+    int r = threadIdx.x / kRowVecs;
+    int a = (a0 + lo + r) % n_axis;
+    if (a < 0) a += n_axis;
+    const T* src = in + base0 + c;
+    T* dst = tile + r * TI + c;
+    if (n_axis >= dr) {  // at most one wrap per step
+      for (; r < rows; r += dr, dst += dr * TI) {
+        cp_async16(dst, src + (long long)a * stride);
+        a += dr;
+        a = a >= n_axis ? a - n_axis : a;
+      }
+    } else {
+      for (; r < rows; r += dr, dst += dr * TI) {
+        cp_async16(dst, src + (long long)a * stride);
+        a = (a + dr) % n_axis;
+      }
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const int il = threadIdx.x % TI, ag = threadIdx.x / TI;
+  const T* src = tile + (ag * J) * TI + il;
+  T W[J], acc[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    W[j] = src[j * TI];
+    acc[j] = T(0);
+  }
+  int q0 = 0;
+  for (; q0 + J <= nt4; q0 += J) {
+#pragma unroll
+    for (int r = 0; r < J; r += 4) {
+      T t4[4];
+      ld4(taps + q0 + r, t4[0], t4[1], t4[2], t4[3]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+#pragma unroll
+        for (int j = 0; j < J; ++j) acc[j] = fma(t4[k], W[(r + k + j) % J], acc[j]);
+        W[r + k] = src[(q0 + r + k + J) * TI];
+      }
+    }
+  }
+  // remaining taps (< J, a multiple of 4): same rotation, guarded 4-tap steps
+#pragma unroll
+  for (int r = 0; r < J; r += 4) {
+    if (q0 + r >= nt4) break;
+    T t4[4];
+    ld4(taps + q0 + r, t4[0], t4[1], t4[2], t4[3]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+      for (int j = 0; j < J; ++j) acc[j] = fma(t4[k], W[(r + k + j) % J], acc[j]);
+      W[r + k] = src[(q0 + r + k + J) * TI];
+    }
+  }
+  {
+    const int a1 = a0 + ag * J;
+    const long long o0 = base0 + (long long)a1 * stride + il;
+    T* po = out + o0;
+    if (addend) {
+      const T* pa = addend + o0;
+#pragma unroll
+      for (int j = 0; j < J; ++j, po += stride, pa += stride)
+        if (a1 + j < n_axis) *po = T(aw * *pa + w * acc[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < J; ++j, po += stride)
+        if (a1 + j < n_axis) *po = T(w * acc[j]);
+    }
+  }
+}
+
+// Contiguous axis (2), nz % 4 == 0: a CTA owns 32 rows (lane = row) x 4 J
+// outputs (warp = J-column group). The staged row span starts at the aligned
+// column floor4(z0 + lo); the misalignment sh = lo mod 4 is absorbed by sh
+// leading zero taps, so the window is the shared Fold<T, J, 1> register
+// window (LDS.128 per 4 taps, pitch = 4 mod 8 words: conflict-free). Results
+// go back through shared memory for coalesced stores.
+template <typename T, int J>
+__global__ void __launch_bounds__(128) pass_z2_kernel(
+    const T* __restrict__ in, T* __restrict__ out, int nz, long long nrows,
+    const T* __restrict__ taps_g, int lo, int ntaps, int pitch, const T* addend, T aw, T w) {
+  constexpr int kVec = 16 / sizeof(T);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int sh = ((lo % 4) + 4) % 4;
+  const int nt4 = (ntaps + sh + 3) & ~3;
+  T* taps = reinterpret_cast<T*>(smem_raw);  // [nt4 + 8]: sh zeros, taps, zeros
+  T* tile = taps + nt4 + 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long row0 = (long long)blockIdx.y * 32;
+  const int z0 = blockIdx.x * (4 * J);
+  for (int q = threadIdx.x; q < nt4 + 8; q += 128)
+    taps[q] = (q >= sh && q - sh < ntaps) ? taps_g[q - sh] : T(0);
+  // staged columns [zs, zs + width), zs = z0 + lo - sh (aligned), wrapped
+  const int width = 4 * J + nt4 + 4;
+  const int nv = width / kVec;
+  {
+    int zs = (z0 + lo - sh) % nz;
+    if (zs < 0) zs += nz;
+    // lanes over 16-byte vectors of a row (wrapped column per lane is fixed
+    // across rows), warps over rows
+    for (int v = lane; v < nv; v += 32) {
+      int z = (zs + v * kVec) % nz;
+      for (int r = warp; r < 32; r += 4) {
+        const long long row = row0 + r;
+        T* d = tile + r * pitch + v * kVec;
+        if (row < nrows)
+          cp_async16(d, in + row * nz + z);
+        else
+          for (int k = 0; k < kVec; ++k) d[k] = T(0);
+      }
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  T acc[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) acc[j] = T(0);
+  {
+    const T* const q[1] = {tile + lane * pitch + warp * J};
+    Fold<T, J, 1>::row(acc, taps, q, nt4 / 4);
+  }
+  __syncthreads();  // every thread is done reading the staged input
+  T* res = tile + lane * pitch + warp * J;
+#pragma unroll
+  for (int j = 0; j < J; j += 4) {
+    if constexpr (sizeof(T) == 4) {
+      *reinterpret_cast<float4*>(res + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+    } else {
+      *reinterpret_cast<double2*>(res + j) = make_double2(acc[j], acc[j + 1]);
+      *reinterpret_cast<double2*>(res + j + 2) = make_double2(acc[j + 2], acc[j + 3]);
+    }
+  }
+  __syncthreads();
+  const int ncols = 4 * J;
+  for (int e = threadIdx.x; e < 32 * ncols; e += 128) {
+    const int r = e / ncols, c = e - r * ncols;
     const long long row = row0 + r;
     const int z = z0 + c;
     if (row < nrows && z < nz) {
@@ -310,6 +493,52 @@ int launch_z(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* ta
   return SFW3D_OK;
 }
 
+template <typename T, int J>
+int launch_tile2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis, const T* taps,
+                 int lo, int ntaps, const T* addend, double aw, double w) {
+  constexpr int TI = 64, NT = 256, To = J * (NT / TI);
+  long long stride = 1;
+  for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
+  long long outer = 1;
+  for (int a = 0; a < axis; ++a) outer *= dims[a];
+  const int n = dims[axis];
+  const int nt4 = (ntaps + 3) & ~3;
+  const size_t smem = (size_t(nt4) + size_t(To + nt4) * TI) * sizeof(T);
+  if (smem > 48 * 1024)
+    SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_tile2_kernel<T, J, TI, NT>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  dim3 grid(unsigned((n + To - 1) / To), unsigned(stride / TI), unsigned(outer));
+  pass_tile2_kernel<T, J, TI, NT><<<grid, NT, smem, ctx->stream>>>(in, out, n, stride, taps, lo,
+                                                                   ntaps, addend, T(aw), T(w));
+  SFW3D_LAUNCH_CHECK(ctx);
+  return SFW3D_OK;
+}
+
+template <typename T, int J>
+int launch_z2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* taps, int lo,
+              int ntaps, const T* addend, double aw, double w) {
+  const long long nrows = (long long)dims[0] * dims[1];
+  const int sh = ((lo % 4) + 4) % 4;
+  const int nt4 = (ntaps + sh + 3) & ~3;
+  const int width = 4 * J + nt4 + 4;
+  // 16-byte rows whose 16-byte chunk index advances by an odd number per row
+  int pitch = (width + 3) & ~3;
+  if (sizeof(T) == 4) {
+    if (pitch % 8 != 4) pitch += 4;
+  } else {
+    if (pitch % 4 != 2) pitch += 2;
+  }
+  const size_t smem = (size_t(nt4) + 8 + size_t(32) * pitch) * sizeof(T);
+  if (smem > 48 * 1024)
+    SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_z2_kernel<T, J>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  dim3 grid(unsigned((dims[2] + 4 * J - 1) / (4 * J)), unsigned((nrows + 31) / 32));
+  pass_z2_kernel<T, J><<<grid, 128, smem, ctx->stream>>>(in, out, dims[2], nrows, taps, lo, ntaps,
+                                                         pitch, addend, T(aw), T(w));
+  SFW3D_LAUNCH_CHECK(ctx);
+  return SFW3D_OK;
+}
+
 template <typename T>
 int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis, const T* taps,
                int lo, int ntaps, const T* addend, double aw, double w) {
@@ -318,16 +547,27 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
     return SFW3D_EINVAL;
   }
   const bool wide = ntaps > 24;
-  if (axis == 2)
-    return wide ? launch_z<T, 32>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w)
-                : launch_z<T, 16>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
-  long long stride = 1;
-  for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
-  // tile shape variants (SFW3D_PASS_VARIANT, for tuning; default 0)
+  // kernel generation (SFW3D_PASS_VARIANT, for tuning; default 0 = v2)
   static const int variant = [] {
     const char* e = getenv("SFW3D_PASS_VARIANT");
     return e ? atoi(e) : 0;
   }();
+  if (axis == 2) {
+    if (variant == 0 && dims[2] % 4 == 0 && ntaps <= 1024) {
+      if (dims[2] >= 128)
+        return launch_z2<T, 32>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
+      return launch_z2<T, 16>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
+    }
+    return wide ? launch_z<T, 32>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w)
+                : launch_z<T, 16>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
+  }
+  long long stride = 1;
+  for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
+  if (variant == 0 && stride % 64 == 0 && ntaps <= 512) {
+    if (dims[axis] >= 128)
+      return launch_tile2<T, 32>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
+    return launch_tile2<T, 16>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
+  }
   if (ntaps <= 512) {
     switch (variant) {
       case 1:
@@ -346,7 +586,7 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
         if (stride % 128 == 0)
           return launch_tiled<T, 32, 128, 256>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
         break;
-      default:
+      default:  // (variant 5: v1 default)
         if (stride % 64 == 0)
           return launch_tiled<T, 16, 64, 256>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
     }
