@@ -327,7 +327,8 @@ __global__ void __launch_bounds__(kThreads * NWY, (fold_min_blocks<T, KJ, NWY>()
   T* accd = reinterpret_cast<T*>(smem_raw);  // [KJ][NT] slice sums
   T* stap = accd + KJ * NT;                   // [Rb + 1][lc4] tap rows b >= 0 (+8)
   const int ntap = (cd.lb / 2 + 1) * cd.lc4;
-  T* plane = stap + ((ntap + 8 + 3) & ~3);
+  int2* srows = reinterpret_cast<int2*>(stap + ((ntap + 8 + 3) & ~3));  // [Rb + 1] (+pad)
+  T* plane = reinterpret_cast<T*>(srows + ((cd.lb / 2 + 1 + 1) & ~1));
   const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) % kWarps;
   const int ylane = (threadIdx.x >> 5) / kWarps * kTY + lane;  // output row in the tile
   const int ty = blockIdx.x / g.ntz, tz = blockIdx.x % g.ntz;
@@ -342,14 +343,17 @@ __global__ void __launch_bounds__(kThreads * NWY, (fold_min_blocks<T, KJ, NWY>()
 
   for (int a = 0; a <= Ra; ++a) {
     const int ai = a + Ra;  // template slice index of +a (same taps as -a)
-    bool any = false;
-    for (int bi = Rb; bi < cd.lb; ++bi) any |= cd.rows[ai * cd.lb + bi].y > 0;
-    if (!any) continue;
-    __syncthreads();
+    __syncthreads();        // previous slice fully consumed
+    // this slice's tap rows b >= 0 and their (first step, nsteps) extents
     {
       const T* tsrc = taps + ((long long)ai * cd.lb + Rb) * cd.lc4;
       for (int e = threadIdx.x; e < ntap + 8; e += NT) stap[e] = e < ntap ? tsrc[e] : T(0);
+      for (int e = threadIdx.x; e <= Rb; e += NT) srows[e] = cd.rows[ai * cd.lb + Rb + e];
     }
+    __syncthreads();
+    bool any = false;
+    for (int b = 0; b <= Rb; ++b) any |= srows[b].y > 0;
+    if (!any) continue;  // (uniform over the CTA)
     stage_sum<T, NT>(plane, bpad + (long long)(x + g.px + a) * g.pxs + corner,
                      a ? bpad + (long long)(x + g.px - a) * g.pxs + corner : nullptr, nrows,
                      g.pitch, g.pys);
@@ -358,7 +362,7 @@ __global__ void __launch_bounds__(kThreads * NWY, (fold_min_blocks<T, KJ, NWY>()
 #pragma unroll
     for (int j = 0; j < KJ; ++j) acc[j] = T(0);
     for (int b = 0; b <= Rb; ++b) {
-      const int2 rr = cd.rows[ai * cd.lb + b + Rb];
+      const int2 rr = srows[b];
       if (rr.y <= 0) continue;
       const T* trow = stap + b * cd.lc4 + 4 * rr.x;
       const int c0 = warp * KJ + 4 * rr.x;
@@ -569,7 +573,8 @@ static int fold_tz(int esize) { return fold_kj_rt(esize) * kWarps; }
 static int fold_smem(const CandHost& c, int esize) {
   const int kj = fold_kj_rt(esize), nwy = fold_nwy_rt(esize);
   const int ntap = ((c.lb / 2 + 1) * c.lc4 + 8 + 3) & ~3;
-  return (kj * kThreads * nwy + ntap +
+  const int nrow2 = ((c.lb / 2 + 2) & ~1) * (8 / esize);  // int2 rows in elements
+  return (kj * kThreads * nwy + ntap + nrow2 +
           (kTY * nwy + c.lb - 1) * region_pitch(c.lc4, esize, fold_tz(esize))) * esize;
 }
 
