@@ -171,7 +171,9 @@ int sfw3d_basis_set_fit(const int32_t dims[3], int n_sigma, const double* sigma_
                         int n_shape, const double* shape_host, int dtype, double tol,
                         int max_terms, int* n_terms, double* betas, double* weights, double* w0,
                         double* fit_err, int32_t* member);
-/* One candidate (flat sigma-major index): evaluator used for `dtype`, the
+/* One candidate (flat sigma-major index): evaluator used for `dtype`
+ * (uses_basis: 0 direct, 1 shared separable basis, 2 basis with exact
+ * refinement of its maxima — fp64 storage, inexact fit), the
  * table's SHARED basis term count, the candidate's shared-basis fit error
  * (max abs on the common box lattice, +inf when not fitted), its direct tap
  * count, the shared basis taps per voxel, and its executed flops per voxel. */

@@ -99,7 +99,8 @@ class AtomTemplateTable:
                                                   C.byref(fl)))
             s, d = divmod(i, len(self.shape_grid))
             cands.append({"sigma": float(self.sigma_grid[s]), "d": float(self.shape_grid[d]),
-                          "path": "basis" if ub.value else "direct", "terms": nt.value,
+                          "path": ("direct", "basis", "basis+refine")[ub.value],
+                          "terms": nt.value,
                           "fit_err": fe.value, "direct_taps": cdt.value, "basis_taps": cbt.value,
                           "flops_per_voxel": fl.value})
         return {"n_cand": nc.value, "n_direct": nd.value, "n_basis": nb.value,

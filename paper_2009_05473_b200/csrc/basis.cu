@@ -546,11 +546,23 @@ __device__ __forceinline__ void st_stream(T* p, const Vec<T, V>& r) {
 // field store. HBM-bound: each thread owns V consecutive voxels of one z row
 // (vector loads), KU term loads in flight; the running maximum is kept on the
 // raw accumulator (eta = acc / lam with lam > 0 is monotone in acc).
-template <typename T, int NM, int V>
+// COLLECT: instead of the argmax, append every windowed voxel whose eta is
+// >= thr[member] to the item list (candidate id, voxel) — capped at col.cap,
+// the counter keeps counting past the cap.
+struct Collect {
+  const double* thr;  // [members]
+  int* cand;          // [cap] member index
+  long long* idx;     // [cap] voxel
+  int* count;
+  int cap;
+};
+
+template <typename T, int NM, int V, bool COLLECT = false>
 __global__ void __launch_bounds__(kMixThreads) mix_argmax_kernel(
     const T* __restrict__ b, const T* __restrict__ terms, long long n, int K, int nm, int m0,
     const T* __restrict__ W, const T* __restrict__ w0, const int* __restrict__ cid, int nx, int ny,
-    int nz, int4 wlo, int4 whi, double lam, T* __restrict__ fields, Best* __restrict__ partial) {
+    int nz, int4 wlo, int4 whi, double lam, T* __restrict__ fields, Best* __restrict__ partial,
+    Collect col = {}) {
   constexpr int KU = V == 4 ? 8 : (V == 2 ? 12 : 16);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sW = reinterpret_cast<T*>(smem_raw);  // [K][NM], zero-padded members
@@ -607,6 +619,26 @@ __global__ void __launch_bounds__(kMixThreads) mix_argmax_kernel(
     const long long row = i0 / nz;
     const int y = int(row % ny), x = int(row / ny);
     const bool row_win = x >= wlo.x && x <= whi.x && y >= wlo.y && y <= whi.y;
+    if constexpr (COLLECT) {
+      if (row_win) {
+#pragma unroll
+        for (int m = 0; m < NM; ++m) {
+          if (m >= nm) break;
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            const int z = z0 + j;
+            if (z >= wlo.z && z <= whi.z && double(acc[m][j]) / lam >= col.thr[m0 + m]) {
+              const int slot = atomicAdd(col.count, 1);
+              if (slot < col.cap) {
+                col.cand[slot] = cid[m0 + m];
+                col.idx[slot] = i0 + j;
+              }
+            }
+          }
+        }
+      }
+      continue;
+    }
 #pragma unroll
     for (int m = 0; m < NM; ++m) {
       if (m >= nm) break;
@@ -629,6 +661,7 @@ __global__ void __launch_bounds__(kMixThreads) mix_argmax_kernel(
       }
     }
   }
+  if constexpr (COLLECT) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int m = 0; m < NM; ++m) {
@@ -691,8 +724,19 @@ size_t basis_set_scratch(const BasisSet* s, long long n, int dtype) {
 template <typename T, int NM, int V>
 static int launch_mix_nm(sfw3d_ctx* ctx, int nblocks, const void* b, const void* terms,
                          long long n, int nt, int nmm, int m0, const BasisSet* s, const int dims[3],
-                         int4 wlo, int4 whi, double lam, void* fields, Best* partial) {
+                         int4 wlo, int4 whi, double lam, void* fields, Best* partial,
+                         const Collect* col) {
   const size_t smem = (size_t(nt) * NM + NM) * sizeof(T);
+  if (col) {
+    if (smem > 48 * 1024)
+      SFW3D_CUDA_TRY(cudaFuncSetAttribute(mix_argmax_kernel<T, NM, V, true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    mix_argmax_kernel<T, NM, V, true><<<nblocks, kMixThreads, smem, ctx->stream>>>(
+        static_cast<const T*>(b), static_cast<const T*>(terms), n, nt, nmm, m0,
+        static_cast<const T*>(s->W_dev), static_cast<const T*>(s->w0_dev), s->cid_dev, dims[0],
+        dims[1], dims[2], wlo, whi, lam, nullptr, partial, *col);
+    return SFW3D_OK;
+  }
   if (smem > 48 * 1024)
     SFW3D_CUDA_TRY(cudaFuncSetAttribute(mix_argmax_kernel<T, NM, V>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -708,12 +752,12 @@ static int launch_mix_nm(sfw3d_ctx* ctx, int nblocks, const void* b, const void*
 template <typename T>
 static int launch_mix(sfw3d_ctx* ctx, int nblocks, const void* b, const void* terms, long long n,
                       int nt, int nmm, int m0, const BasisSet* s, const int dims[3], int4 wlo,
-                      int4 whi, double lam, void* fields, Best* partial) {
+                      int4 whi, double lam, void* fields, Best* partial, const Collect* col) {
   constexpr int V4 = 16 / sizeof(T);  // 4 floats / 2 doubles
   const int nz = dims[2];
 #define SFW3D_MIX(NM, V)                                                                        \
   return launch_mix_nm<T, NM, V>(ctx, nblocks, b, terms, n, nt, nmm, m0, s, dims, wlo, whi, lam, \
-                                 fields, partial)
+                                 fields, partial, col)
   if (nmm <= 8 && nz % V4 == 0) SFW3D_MIX(8, V4);
   if (nmm <= 16 && nz % 2 == 0) SFW3D_MIX(16, 2);
   if (nmm <= 8) SFW3D_MIX(8, 1);
@@ -755,10 +799,10 @@ int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[
     SFW3D_PROF(ctx, "eta_mix");
     if (dtype == SFW3D_F64)
       SFW3D_TRY(launch_mix<double>(ctx, nblocks, b, terms, n, nt, nmm, m0, s, dims, wlo, whi, lam,
-                                   fields, partial));
+                                   fields, partial, nullptr));
     else
       SFW3D_TRY(launch_mix<float>(ctx, nblocks, b, terms, n, nt, nmm, m0, s, dims, wlo, whi, lam,
-                                  fields, partial));
+                                  fields, partial, nullptr));
     SFW3D_LAUNCH_CHECK(ctx);
   }
   {
@@ -768,5 +812,42 @@ int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[
   }
   return SFW3D_OK;
 }
+
+int basis_set_collect(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[3],
+                      const void* b, double lam, const int32_t win[6], const double* thr_dev,
+                      int cap, int* cand_dev, long long* idx_dev, int* count_dev, void* scratch) {
+  const int nm = int(s->members.size()), nt = int(s->betas.size());
+  if (nm == 0) return SFW3D_OK;
+  const long long n = vol_count(dims);
+  const size_t es = dtype == SFW3D_F64 ? 8 : 4;
+  Carver cv(scratch);
+  cv.take<char>(size_t(n) * es);
+  cv.take<char>(size_t(n) * es);
+  const char* terms = cv.take<char>(size_t(n) * es * nt);  // left by basis_set_eval
+  const int nblocks = std::min<long long>(4096, (long long)ctx->num_sms * 8);
+  const int4 wlo = make_int4(win[0], win[2], win[4], 0), whi = make_int4(win[1], win[3], win[5], 0);
+  SFW3D_CUDA_TRY(cudaMemsetAsync(count_dev, 0, sizeof(int), ctx->stream));
+  const Collect col{thr_dev, cand_dev, idx_dev, count_dev, cap};
+  for (int m0 = 0; m0 < nm; m0 += kMixMax) {
+    const int nmm = std::min(kMixMax, nm - m0);
+    SFW3D_PROF(ctx, "eta_refine");
+    if (dtype == SFW3D_F64)
+      SFW3D_TRY(launch_mix<double>(ctx, nblocks, b, terms, n, nt, nmm, m0, s, dims, wlo, whi, lam,
+                                   nullptr, nullptr, &col));
+    else
+      SFW3D_TRY(launch_mix<float>(ctx, nblocks, b, terms, n, nt, nmm, m0, s, dims, wlo, whi, lam,
+                                  nullptr, nullptr, &col));
+    SFW3D_LAUNCH_CHECK(ctx);
+  }
+  return SFW3D_OK;
+}
+
+int basis_set_member_index(const BasisSet* s, int cand) {
+  if (!s) return -1;
+  for (int m = 0; m < int(s->members.size()); ++m)
+    if (s->members[m] == cand) return m;
+  return -1;
+}
+int basis_set_member_cand(const BasisSet* s, int m) { return s->members[m]; }
 
 }  // namespace sfw3d

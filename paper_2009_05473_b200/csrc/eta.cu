@@ -74,6 +74,7 @@ struct sfw3d_table {
   std::vector<sfw3d::BasisCandidate> bcands;
   mutable sfw3d::BasisSet* set32 = nullptr;
   mutable sfw3d::BasisSet* set64 = nullptr;
+  void* refcand_dev = nullptr;  // RefCand per candidate (fp64 exact refinement)
   const sfw3d::BasisSet* set(int dtype) const { return dtype == SFW3D_F64 ? set64 : set32; }
 };
 
@@ -422,6 +423,76 @@ __global__ void best_reduce_kernel(const Best* __restrict__ partial, long long n
   reduce_store_best<double>(b, sb, out);
 }
 
+// ---------------------------------------------------------- exact refinement
+// fp64 basis members are approximate (fit error e_c per tap); the voxels
+// whose approximate eta is within 2 E_c of the member's approximate maximum
+// (E_c = (e_c + 2e-12) ||b||_1 / lam bounds |eta~ - eta| everywhere) are
+// re-evaluated exactly here, with the candidate's direct taps on the
+// reference box, so the reported maxima and argmaxima are the direct ones.
+struct RefCand {
+  const double* taps;  // dense [la][lb][lc4]
+  const int2* rows;    // [la][lb] (first step, nsteps), step = 4 columns
+  int lo_a, lo_b, cl, la, lb, lc4;
+};
+
+// sum |b| over the volume (fp64), one atomicAdd per block
+template <typename T>
+__global__ void abs_sum_kernel(const T* __restrict__ b, long long n, double* __restrict__ out) {
+  __shared__ double red[8];
+  double sacc = 0.0;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256)
+    sacc += fabs(double(b[i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sacc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    atomicAdd(out, t);
+  }
+}
+
+// one CTA per item: eta = sum_v G_c(v) b(m + v) / lam over the candidate's
+// box (periodic indexing), warps over template rows, lanes over taps
+__global__ void __launch_bounds__(256) refine_kernel(const double* __restrict__ b, int nx, int ny,
+                                                     int nz, const RefCand* __restrict__ rc,
+                                                     const int* __restrict__ item_cand,
+                                                     const long long* __restrict__ item_idx,
+                                                     double lam, double* __restrict__ out) {
+  __shared__ double red[8];
+  const RefCand c = rc[item_cand[blockIdx.x]];
+  const long long lin = item_idx[blockIdx.x];
+  const int z = int(lin % nz), y = int((lin / nz) % ny), x = int(lin / ((long long)ny * nz));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc = 0.0;
+  for (int r = warp; r < c.la * c.lb; r += 8) {
+    const int2 rr = c.rows[r];
+    if (rr.y <= 0) continue;
+    const int ai = r / c.lb, bi = r - ai * c.lb;
+    int xa = (x + c.lo_a + ai) % nx;
+    if (xa < 0) xa += nx;
+    int yb = (y + c.lo_b + bi) % ny;
+    if (yb < 0) yb += ny;
+    const double* brow = b + ((long long)xa * ny + yb) * nz;
+    const double* trow = c.taps + (long long)r * c.lc4;
+    for (int col = 4 * rr.x + lane; col < 4 * (rr.x + rr.y); col += 32) {
+      int zc = (z + c.cl + col) % nz;
+      if (zc < 0) zc += nz;
+      acc = fma(trow[col], brow[zc], acc);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    out[blockIdx.x] = t / lam;
+  }
+}
+
 int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
 // smem row pitch (elements): >= cols needed, and the 16-byte chunk index of
@@ -525,16 +596,14 @@ static int build_candidate(const int dims[3], double sigma, double d, double tap
   return SFW3D_OK;
 }
 
-// fp64 storage (reference-parity configs) accepts a basis only this close
-constexpr double kBasisTol64 = 1e-12;
-
-// builds the shared basis of one storage precision on first use; fp64
-// storage (the reference-parity configs) accepts fits <= min(basis_tol, 1e-12)
+// builds the shared basis of one storage precision on first use (fits
+// accepted at basis_tol; fp64 members with inexact fits get their maxima
+// refined exactly, see refine_kernel)
 static int ensure_basis(const sfw3d_table* t, int dtype) {
   if (t->mode != 0) return SFW3D_OK;
   BasisSet*& s = dtype == SFW3D_F64 ? t->set64 : t->set32;
   if (s) return SFW3D_OK;
-  const double tol = dtype == SFW3D_F64 ? std::min(t->basis_tol, kBasisTol64) : t->basis_tol;
+  const double tol = t->basis_tol;
   int dev = 0;
   SFW3D_CUDA_TRY(cudaGetDevice(&dev));
   SFW3D_CUDA_TRY(cudaSetDevice(t->device));
@@ -552,6 +621,12 @@ static int ensure_basis(const sfw3d_table* t, int dtype) {
 // evaluator choice per candidate and storage type
 static bool use_basis(const sfw3d_table* t, int ci, int dtype) {
   return t->mode == 0 && basis_set_member(t->set(dtype), ci, nullptr);
+}
+
+// fp64 storage: basis members whose fit is not exact get an exact refinement
+static bool use_refine(const sfw3d_table* t, int ci, int dtype) {
+  double fe = 0.0;
+  return dtype == SFW3D_F64 && t->mode == 0 && basis_set_member(t->set(dtype), ci, &fe) && fe > 0.0;
 }
 
 // folded kernel tile: outputs per thread along z (fp32 32, fp64 16) and
@@ -669,6 +744,7 @@ extern "C" int sfw3d_table_destroy(sfw3d_table* t) {
   }
   basis_set_destroy(t->set32);
   basis_set_destroy(t->set64);
+  if (t->refcand_dev) cudaFree(t->refcand_dev);
   delete t;
   return SFW3D_OK;
 }
@@ -726,6 +802,15 @@ extern "C" int sfw3d_table_create(sfw3d_ctx* ctx, const sfw3d_psf* psf, int n_si
   for (const auto& c : t->cands)
     t->bcands.push_back(
         {c.sigma, c.d, {c.lo[0], c.lo[1], c.lo[2]}, {c.hi[0], c.hi[1], c.hi[2]}, c.taps});
+  {
+    std::vector<RefCand> rc;
+    for (const auto& c : t->cands) rc.push_back({c.t64, c.rows_dev, c.lo[0], c.lo[1], c.cl, c.la, c.lb, c.lc4});
+    const int st = upload(&t->refcand_dev, rc.data(), rc.size() * sizeof(RefCand));
+    if (st != SFW3D_OK) {
+      sfw3d_table_destroy(t);
+      return st;
+    }
+  }
   *out = t;
   return SFW3D_OK;
 }
@@ -768,7 +853,7 @@ extern "C" int sfw3d_table_candidate(const sfw3d_table* t, int dtype, int cand, 
   SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
   SFW3D_TRY(ensure_basis(t, dtype));
   const CandHost& c = t->cands[cand];
-  if (uses_basis) *uses_basis = use_basis(t, cand, dtype) ? 1 : 0;
+  if (uses_basis) *uses_basis = use_basis(t, cand, dtype) ? (use_refine(t, cand, dtype) ? 2 : 1) : 0;
   double fe = INFINITY;
   basis_set_member(t->set(dtype), cand, &fe);
   if (n_terms) *n_terms = basis_set_n_terms(t->set(dtype));  // shared terms of the table
@@ -790,11 +875,20 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   const int64_t n = vol_count(dims);
   const size_t vb = size_t(n) * sizeof(T);
   const int nc = int(t->cands.size());
-  bool any_direct = false, any_basis = false;
-  for (int ci = 0; ci < nc; ++ci) (use_basis(t, ci, dtype) ? any_basis : any_direct) = true;
+  bool any_direct = false, any_basis = false, any_refine = false;
+  for (int ci = 0; ci < nc; ++ci) {
+    (use_basis(t, ci, dtype) ? any_basis : any_direct) = true;
+    any_refine |= use_refine(t, ci, dtype);
+  }
+  // direct evaluation per candidate (refined members fall back to it when
+  // their candidate list overflows)
+  std::vector<char> direct(nc, 0);
+  for (int ci = 0; ci < nc; ++ci) direct[ci] = !use_basis(t, ci, dtype);
   const BasisSet* bset = t->set(dtype);
   const size_t sb = any_basis ? basis_set_scratch(bset, n, dtype) : 0;
-  const size_t pb = any_direct ? size_t(t->pdims[0]) * t->pdims[1] * t->pdims[2] * sizeof(T) : 0;
+  const size_t pb = (any_direct || any_refine)
+                        ? size_t(t->pdims[0]) * t->pdims[1] * t->pdims[2] * sizeof(T) : 0;
+  constexpr int kRefCap = 1 << 16;  // refinement items per call
   // direct output tiles: the window, or the whole grid when fields are requested
   int ow[6];
   if (fields) {
@@ -808,19 +902,27 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   const int nxp = ow[1] - ow[0] + 1;
   const long long nblocks_direct = (long long)nty * ntz * nxp;
   const long long nblocks = nblocks_direct;
+  const size_t rb = any_refine ? size_t(kRefCap) * (4 + 8 + 8) + size_t(nc) * 8 + 64 : 0;
   SFW3D_TRY(ensure_device(ctx, ctx->ws,
                           Carver::need({vb, vb, sb, pb, size_t(nblocks) * sizeof(Best),
-                                        size_t(nc) * sizeof(Best)})));
+                                        size_t(nc) * sizeof(Best), rb})));
   Carver cv(ctx->ws.ptr);
   T* b = cv.take<T>(n);
   T* tmp = cv.take<T>(n);
   void* bscratch = sb ? cv.take<char>(sb) : nullptr;
-  T* bpad = any_direct ? cv.take<T>(pb / sizeof(T)) : nullptr;
+  T* bpad = pb ? cv.take<T>(pb / sizeof(T)) : nullptr;
   Best* partial = cv.take<Best>(nblocks);
   Best* cbest = cv.take<Best>(nc);
+  int* ref_cand = any_refine ? cv.take<int>(kRefCap) : nullptr;
+  long long* ref_idx = any_refine ? cv.take<long long>(kRefCap) : nullptr;
+  double* ref_val = any_refine ? cv.take<double>(kRefCap) : nullptr;
+  double* ref_thr = any_refine ? cv.take<double>(nc) : nullptr;
+  double* ref_l1 = any_refine ? cv.take<double>(1) : nullptr;
+  int* ref_count = any_refine ? cv.take<int>(1) : nullptr;
+  std::vector<Best> refined(nc, Best{NAN, -1});  // exact maxima of refined members
   // b = H^T * r (tmp is pass scratch), then the periodic padding for direct
   SFW3D_TRY(psf_apply_impl(ctx, t->psf, dtype, residual, b, 1, tmp));
-  if (any_direct) {
+  if (pb) {
     SFW3D_PROF(ctx, "pad");
     const long long np = (long long)t->pdims[0] * t->pdims[1] * t->pdims[2];
     pad_kernel<T><<<unsigned((np + 255) / 256), 256, 0, ctx->stream>>>(
@@ -847,8 +949,58 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   // writing cbest[cand] (and the member fields) directly
   if (any_basis)
     SFW3D_TRY(basis_set_eval(ctx, bset, dtype, dims, b, lam, win, fields, cbest, bscratch));
+  if constexpr (sizeof(T) == 8) {
+    if (any_refine) {
+      // E_c = (e_c + 2e-12) ||b||_1 / lam bounds |eta~_c - eta_c| at every voxel:
+      // the true maximum lies among the voxels with eta~ >= max eta~ - 2 E_c
+      SFW3D_PROF(ctx, "eta_refine");
+      SFW3D_CUDA_TRY(cudaMemsetAsync(ref_l1, 0, sizeof(double), ctx->stream));
+      abs_sum_kernel<T><<<4 * ctx->num_sms, 256, 0, ctx->stream>>>(b, n, ref_l1);
+      SFW3D_LAUNCH_CHECK(ctx);
+      std::vector<Best> hb0(nc);
+      double l1 = 0.0;
+      SFW3D_TRY(download_sync(ctx, hb0.data(), cbest, size_t(nc) * sizeof(Best)));
+      SFW3D_TRY(download_sync(ctx, &l1, ref_l1, sizeof(double)));
+      const int nm = basis_set_n_members(bset);
+      std::vector<double> thr(nm, INFINITY);
+      for (int m = 0; m < nm; ++m) {
+        const int ci = basis_set_member_cand(bset, m);
+        double fe = 0.0;
+        basis_set_member(bset, ci, &fe);
+        if (!use_refine(t, ci, dtype) || !std::isfinite(hb0[ci].v)) continue;
+        const double E = (fe + 2e-12) * l1 / lam;
+        thr[m] = hb0[ci].v - 2.0 * E - 1e-12 * std::fabs(hb0[ci].v);
+      }
+      SFW3D_TRY(stage_upload(ctx, ref_thr, thr.data(), size_t(nm) * sizeof(double)));
+      SFW3D_TRY(basis_set_collect(ctx, bset, dtype, dims, b, lam, win, ref_thr, kRefCap, ref_cand,
+                                  ref_idx, ref_count, bscratch));
+      int count = 0;
+      SFW3D_TRY(download_sync(ctx, &count, ref_count, sizeof(int)));
+      if (count > kRefCap) {  // too many near-maximal voxels: exact direct evaluation
+        for (int ci = 0; ci < nc; ++ci)
+          if (use_refine(t, ci, dtype)) direct[ci] = 1;
+      } else if (count > 0) {
+        SFW3D_PROF(ctx, "eta_refine");
+        refine_kernel<<<count, 256, 0, ctx->stream>>>(
+            reinterpret_cast<const double*>(b), dims[0], dims[1], dims[2],
+            static_cast<const RefCand*>(t->refcand_dev), ref_cand, ref_idx, lam, ref_val);
+        SFW3D_LAUNCH_CHECK(ctx);
+        std::vector<int> hc(count);
+        std::vector<long long> hi(count);
+        std::vector<double> hv(count);
+        SFW3D_TRY(download_sync(ctx, hc.data(), ref_cand, size_t(count) * sizeof(int)));
+        SFW3D_TRY(download_sync(ctx, hi.data(), ref_idx, size_t(count) * sizeof(long long)));
+        SFW3D_TRY(download_sync(ctx, hv.data(), ref_val, size_t(count) * sizeof(double)));
+        for (int i = 0; i < count; ++i) {
+          Best& r = refined[hc[i]];
+          // larger value wins, ties to the smaller C-order index
+          if (std::isnan(r.v) || hv[i] > r.v || (hv[i] == r.v && hi[i] < r.idx)) r = {hv[i], hi[i]};
+        }
+      }
+    }
+  }
   for (int ci = 0; ci < nc; ++ci) {
-    if (use_basis(t, ci, dtype)) continue;
+    if (!direct[ci]) continue;
     const CandHost& c = t->cands[ci];
     T* fld = fields ? static_cast<T*>(fields) + size_t(ci) * n : nullptr;
     long long nred = 0;
@@ -913,6 +1065,8 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   }
   std::vector<Best> hb(nc);
   SFW3D_TRY(download_sync(ctx, hb.data(), cbest, size_t(nc) * sizeof(Best)));
+  for (int ci = 0; ci < nc; ++ci)
+    if (!direct[ci] && !std::isnan(refined[ci].v)) hb[ci] = refined[ci];
   int bi = 0;
   double bv = -INFINITY;
   for (int ci = 0; ci < nc; ++ci) {

@@ -53,12 +53,12 @@ def test_table_fits(P):
     with P.precision("f64"):
         info64 = table.info()
     for c in info64["candidates"]:
-        if c["d"] == 2.0:
+        if c["d"] == 2.0:  # exact: no refinement needed
             assert c["path"] == "basis" and c["fit_err"] == 0.0
         elif c["d"] > 2.0:
             assert c["path"] == "direct"
-        else:  # fp64 storage accepts the (tighter) fp64 fit only below 1e-12
-            assert (c["path"] == "basis") == (c["fit_err"] <= 1e-12)
+        else:  # fp64: approximate basis, maxima refined exactly
+            assert c["path"] == "basis+refine" and c["fit_err"] <= 1e-9
 
 
 def test_eta_config2_f64_vs_oracle(P):
@@ -129,3 +129,34 @@ def test_eta_linearity(P):
     f2 = np.stack([v.data for v in P.eta_field(P.Volume(r2), 1.0, table).fields])
     f3 = np.stack([v.data for v in P.eta_field(P.Volume(2.0 * r1 - 0.5 * r2), 1.0, table).fields])
     assert np.max(np.abs(f3 - (2.0 * f1 - 0.5 * f2))) <= 1e-10 * np.max(np.abs(f3))
+
+
+def test_eta_f64_refined_maxima(P):
+    """fp64 storage, d < 2 candidates on the shared basis with exact
+    refinement: every candidate's windowed maximum and its position equal the
+    oracle's (direct-equivalent) ones to 1e-10, and the approximate fields
+    stay within the refinement bound E_c = (e_c + 2e-12) ||b||_1 / lam."""
+    import torch
+    dims, kernel, r = cfg4_like(56, seed=7)
+    sg, dg = np.array([1.0, 1.7, 2.6]), np.array([1.3, 1.6, 1.9, 2.0])
+    hats = O.template_hats(O.psf_hat(kernel), dims, sg, dg)
+    win = ((4, 51), (6, 49), (3, 52))
+    _, _, val, per, fields = O.eta_field(r, 0.8, hats, len(dg), win, keep_fields=True)
+    psf = P.Psf(P.Volume(kernel), normalize=False)
+    table = P.build_template_table(psf, sg, dg)
+    info = table.info()
+    assert sum(c["path"] == "basis+refine" for c in info["candidates"]) == 9
+    rd = torch.tensor(r, device="cuda")
+    best, recs, fl = P.certificate.eta_argmax_dev(rd, 0.8, table, win, keep_fields=True)
+    assert abs(best.value - val) <= 1e-10 * abs(val)
+    for c, rec in enumerate(recs):
+        pos, v = per[c]
+        assert abs(rec.value - v) <= 1e-10 * abs(val), (c, rec.value, v)
+        assert tuple(rec.pos) == tuple(pos), (c, tuple(rec.pos), pos)
+    b = O.corr(r, O.psf_hat(kernel))  # H^T r
+    l1 = np.abs(b).sum()
+    got = fl.cpu().numpy()
+    for c, cinfo in enumerate(info["candidates"]):
+        if cinfo["path"] == "basis+refine":
+            E = (cinfo["fit_err"] + 2e-12) * l1 / 0.8
+            assert np.max(np.abs(got[c] - fields[c])) <= E
