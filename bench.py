@@ -309,6 +309,15 @@ def cert_workload(args, rank, world, dev):
             "traffic": None, "bytes_per_step": nbytes, "members": info["n_basis"],
             "launches": fam["eta_mix"][1], "avg_launch_ms": fam["eta_mix"][0] / fam["eta_mix"][1],
             "share_of_step": fam["eta_mix"][0] / step_ms if step_ms else None}
+    # measured DRAM bytes per launch (ncu capture of the same workload,
+    # profiles/round1/traffic_cert512.json) where available
+    tpath = ROOT / "profiles" / "round1" / "traffic_cert512.json"
+    if tpath.exists() and n == 512 and world == 1:
+        fams = json.loads(tpath.read_text())["families"]
+        for f, rl in rooflines.items():
+            if f in fams:
+                rl["traffic"] = fams[f]["dram_bytes_per_launch"]
+                rl["traffic_source"] = "profiles/round1/traffic_cert512.json (ncu dram__bytes_read+write)"
     roof = None
     if rooflines:
         dom_fam = max(rooflines, key=lambda f: fam[f][0])
