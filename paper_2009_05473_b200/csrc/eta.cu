@@ -10,27 +10,19 @@
 // Here eta is evaluated in the spatial domain in factorised form
 //     eta_c(m) = (1/lam) * sum_v G_c(v) * b(m + v),   b = H^T * r,
 // exact by associativity (corr(r, H*G) = corr(corr(r, H), G)); b is one
-// separable K4 pass shared by all candidates. Two evaluators per candidate:
+// separable K4 pass shared by all candidates. Evaluators per candidate:
 //
-//  DIRECT — 3-D correlation with the unit atom on the reference's support
-//   box. A CTA owns 32 (y) x 64 (z) outputs of one x-plane: warp w has the
-//   z-group w (16 consecutive outputs per thread), lane l the row y0+l, so
-//   a warp's shared-memory reads hit 32 different rows (pitch = 4 mod 32
-//   words: conflict-free LDS.128). For each template x-offset the residual
-//   plane region is staged in shared memory; every template row streams its
-//   taps four at a time: one LDS.128 of the register window, one broadcast
-//   LDG.128 of taps, 64 FFMA per thread (window rotated at compile time, no
-//   moves). fp32 partial sums are promoted to fp64 once per template slice.
-//
-//  BASIS — the radial profile g(s) = exp(-s^(d/2) / (2 sigma^d)), s = |v|^2,
-//   is written as w_0 delta(s) + sum_k w_k exp(-beta_k s) on the lattice
-//   values s the support box contains (non-negative least squares over 48
-//   geometric beta_k; exact with one term for d = 2). Each term is
-//   separable, (f_k x f_k x f_k)(v) with f_k(t) = exp(-beta_k t^2) truncated
-//   to the same box, so eta_c costs sum_k 3 * (2R+1) taps per voxel instead
-//   of (2R+1)^3. The fit's max absolute error over the box is recorded and
-//   the basis is used only where it is <= basis_tol (fp32 storage) or the
-//   expansion is exact (d == 2, any storage).
+//  FOLDED DIRECT (eta_fold_kernel) — symmetric boxes: the radial atom's rows
+//   (x +- a, y +- b) share one tap row; per a the CTA stages the summed plane
+//   P(x+a) + P(x-a), per b each thread sums rows y +- b and correlates with
+//   the tap row through a compile-time-rotated register window (window.cuh).
+//  DIRECT (eta_direct_kernel) — any box (full-axis, asymmetric offsets).
+//  SHARED BASIS (basis.cu) — d <= 2 candidates as positive Gaussian
+//   mixtures on one dictionary shared by the table: separable passes once
+//   per shared term, one fused mix + argmax kernel for all members.
+//  EXACT REFINEMENT (refine_kernel) — fp64 storage, inexact members: the
+//   voxels within 2 E_c of the member's approximate maximum are re-evaluated
+//   with the direct taps, so maxima / argmaxima are the direct ones.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
