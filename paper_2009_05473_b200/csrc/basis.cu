@@ -287,7 +287,7 @@ constexpr int kDictCoarse = 49;
 constexpr double kFitFloor = 1e-11;
 
 int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands, int dtype,
-                    double tol, BasisSet** out, bool on_device) {
+                    double tol, BasisSet** out, bool on_device, bool prune) {
   auto* s = new BasisSet();
   s->dtype = dtype;
   cudaGetDevice(&s->device);
@@ -383,6 +383,62 @@ int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands,
     if (err[c] <= tol) {
       s->is_member[c] = 1;
       s->members.push_back(c);
+    }
+  }
+  // Greedy pruning of the shared term set (large volumes, where each term
+  // costs three full-volume passes per certificate): try dropping terms from
+  // the most expensive (widest) down; a drop is kept when every member using
+  // the term refits on the remaining terms within tol.
+  if (prune && !s->members.empty()) {
+    std::vector<char> in(K, 0), pinned(K, 0);
+    for (int c : s->members)
+      for (int k = 0; k < K; ++k)
+        if (wfit[c][k] > 0.0) {
+          in[k] = 1;
+          if (cands[c].d == 2.0) pinned[k] = 1;  // exact members need their term
+        }
+    const double rbox = rmax;
+    auto cost = [&](int k) {
+      return std::min(2.0 * std::ceil(std::sqrt(27.7 / dict[k])) + 1.0, 2.0 * rbox + 1.0);
+    };
+    std::vector<int> order;
+    for (int k = 0; k < K; ++k)
+      if (in[k] && !pinned[k]) order.push_back(k);
+    std::sort(order.begin(), order.end(), [&](int x, int y) { return cost(x) > cost(y); });
+    for (int k : order) {
+      std::vector<int> users;
+      for (int c : s->members)
+        if (wfit[c][k] > 0.0 && cands[c].d != 2.0) users.push_back(c);
+      in[k] = 0;
+      std::vector<double> sub;
+      std::vector<int> subk;
+      for (int q = 0; q < K; ++q)
+        if (in[q]) {
+          sub.push_back(dict[q]);
+          subk.push_back(q);
+        }
+      std::vector<std::vector<double>> nw(users.size());
+      std::vector<double> nw0(users.size()), ne(users.size());
+      std::vector<std::thread> th;
+      for (size_t u = 0; u < users.size(); ++u)
+        th.emplace_back([&, u] {
+          const int c = users[u];
+          ne[u] = fit_on(sub, S, Sfit, cands[c].sigma, cands[c].d, nw[u], nw0[u]) + 1e-12;
+        });
+      for (auto& x : th) x.join();
+      bool ok = true;
+      for (size_t u = 0; u < users.size(); ++u) ok &= ne[u] <= tol;
+      if (!ok) {
+        in[k] = 1;
+        continue;
+      }
+      for (size_t u = 0; u < users.size(); ++u) {
+        const int c = users[u];
+        wfit[c].assign(K, 0.0);
+        for (size_t q = 0; q < subk.size(); ++q) wfit[c][subk[q]] = nw[u][q];
+        w0fit[c] = nw0[u];
+        s->fit_err[c] = ne[u];
+      }
     }
   }
   // union of the members' terms

@@ -1,6 +1,7 @@
 // Shared separable Gaussian basis for the certificate (see basis.cu).
 #pragma once
 
+#include <cstdlib>
 #include <utility>
 #include <vector>
 
@@ -29,14 +30,23 @@ struct BasisSet;
 
 // Fits every candidate on one shared dictionary of Gaussians (see basis.cu)
 // and keeps those whose max abs error on the common box is <= tol.
-// on_device = false fits on the host only (no device buffers; eval unusable).
+// on_device = false fits on the host only (no device buffers; eval unusable);
+// prune = greedily drop shared terms while every member stays within tol.
 int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands, int dtype,
-                    double tol, BasisSet** out, bool on_device = true);
+                    double tol, BasisSet** out, bool on_device = true, bool prune = false);
 // host copy of the fit: betas[n_terms], weights[n_cand][max_terms] (member rows,
 // zero elsewhere), w0[n_cand], fit_err[n_cand], member[n_cand]; NULLs skipped
 void basis_set_export(const BasisSet* s, int max_terms, int* n_terms, double* betas,
                       double* weights, double* w0, double* fit_err, int32_t* member);
 void basis_set_destroy(BasisSet* s);
+// tables prune their shared terms for volumes of >= 2^26 voxels (~406^3):
+// there a term's three full-volume passes per certificate outweigh the
+// seconds of host NNLS refits the pruning costs once per table
+// (SFW3D_BASIS_PRUNE=0/1 overrides, for measurements)
+inline bool basis_prune_rule(const int dims[3]) {
+  if (const char* e = getenv("SFW3D_BASIS_PRUNE")) return atoi(e) != 0;
+  return (long long)dims[0] * dims[1] * dims[2] >= (1LL << 26);
+}
 // candidate -> (is member, fit error of its shared-dictionary fit)
 bool basis_set_member(const BasisSet* s, int cand, double* fit_err);
 int basis_set_n_terms(const BasisSet* s);
