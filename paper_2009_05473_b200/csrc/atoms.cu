@@ -17,13 +17,14 @@
 // fp64 volumes use fp64 math with products/sums rounded exactly as numpy
 // does (no FMA contraction where the reference rounds twice); fp32 volumes
 // use fp32 math on the MUFU (ex2/lg2/rcp) with fp64 accumulation.
+#include <algorithm>
+#include <type_traits>
+
 #include "internal.cuh"
 
 namespace sfw3d {
 namespace {
 
-constexpr int kBX = 4, kBY = 8, kBZ = 16;  // render brick (512 voxels)
-constexpr int kSub = 16;                   // listed atoms tabulated per pass
 constexpr int kChunk = 4096;               // atom-sum chunk (voxels)
 constexpr int kSumThreads = 256;
 constexpr int kMaxAxis = 1024;             // tabulated axis length in atom sums
@@ -82,16 +83,39 @@ __device__ __forceinline__ double profile64(const AtomGeo& a, double u2, double&
   return exp(-t);
 }
 
+// single-instruction MUFU transcendentals (flush-to-zero approximations;
+// the fp32 storage path's own rounding dominates their error)
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // unit profile, fp32 on the MUFU; lg2u2 returns log2(u2) for reuse
+// (u2 = 0: lg2 = -inf, ex2(-inf) = 0, so p = 0 and the profile is 1)
 __device__ __forceinline__ float profile32(float inv2sd, float half_d, bool d2, float u2, float& t,
                                            float& lg2u2) {
-  lg2u2 = __log2f(u2);
-  const float p = d2 ? u2 : exp2f(half_d * lg2u2);
+  lg2u2 = lg2_approx(u2);
+  const float p = d2 ? u2 : ex2_approx(half_d * lg2u2);
   t = inv2sd * p;
-  return __expf(-t);
+  return ex2_approx(-1.4426950408889634f * t);
 }
 
 // ------------------------------------------------------------------ render
+// One CTA per 16 (x) x 16 (y) x 32 (z) superbrick; thread (y, z) owns the
+// 16-voxel column along x. The CTA scans the atoms in row order (512 per
+// pass), ballot-compacts those whose wrapped box meets the superbrick, and
+// per group of kGroup listed atoms tabulates each atom's per-axis offsets
+// over the superbrick (inf = outside the box) and its profile parameters in
+// shared memory. Threads skip atoms missing their (y, z) at once; the x loop
+// accumulates w * G in the reference's per-voxel atom order.
+constexpr int kSX = 16, kSY = 16, kSZ = 32, kGroup = 32;
+
 template <typename T>
 __global__ void __launch_bounds__(512) render_kernel(const AtomGeo* __restrict__ atoms, int k,
                                                      int nx, int ny, int nz, T* __restrict__ out) {
@@ -99,20 +123,27 @@ __global__ void __launch_bounds__(512) render_kernel(const AtomGeo* __restrict__
   __shared__ int list[512];
   __shared__ int warp_cnt[16];
   __shared__ int list_n;
-  __shared__ Off tx[kSub][kBX], ty[kSub][kBY], tz[kSub][kBZ];
+  __shared__ Off tx[kGroup][kSX], ty[kGroup][kSY], tz[kGroup][kSZ];
+  __shared__ float pw[kGroup], pinv[kGroup], phd[kGroup];
+  __shared__ int pd2[kGroup];
 
-  const int nbz = (nz + kBZ - 1) / kBZ, nby = (ny + kBY - 1) / kBY;
+  const int nbz = (nz + kSZ - 1) / kSZ, nby = (ny + kSY - 1) / kSY;
   const int bz = blockIdx.x % nbz, by = (blockIdx.x / nbz) % nby, bx = blockIdx.x / (nbz * nby);
-  const int x0 = bx * kBX, y0 = by * kBY, z0 = bz * kBZ;
-  const int x1 = min(x0 + kBX, nx) - 1, y1 = min(y0 + kBY, ny) - 1, z1 = min(z0 + kBZ, nz) - 1;
+  const int x0 = bx * kSX, y0 = by * kSY, z0 = bz * kSZ;
+  const int x1 = min(x0 + kSX, nx) - 1, y1 = min(y0 + kSY, ny) - 1, z1 = min(z0 + kSZ, nz) - 1;
   const int tid = threadIdx.x;
-  const int lz = tid % kBZ, ly = (tid / kBZ) % kBY, lx = tid / (kBZ * kBY);
-  const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
-  const bool live = gx < nx && gy < ny && gz < nz;
+  const int lz = tid % kSZ, ly = tid / kSZ;
+  const int gy = y0 + ly, gz = z0 + lz;
+  const bool live = gy < ny && gz < nz;
   const int lane = tid & 31, warp = tid >> 5;
   const Off kOut = Off(INFINITY);
 
-  double acc = 0.0;
+  // fp64 storage: fp64 sums with the reference's rounding; fp32 storage:
+  // fp32 sums (the result is stored in fp32)
+  using Acc = typename std::conditional<sizeof(T) == 8, double, float>::type;
+  Acc acc[kSX];
+#pragma unroll
+  for (int i = 0; i < kSX; ++i) acc[i] = Acc(0);
   for (int base = 0; base < k; base += 512) {
     const int ai = base + tid;
     bool hit = false;
@@ -125,62 +156,129 @@ __global__ void __launch_bounds__(512) render_kernel(const AtomGeo* __restrict__
     if (lane == 0) warp_cnt[warp] = __popc(mask);
     __syncthreads();
     if (tid == 0) {
-      int s = 0;
+      int sacc = 0;
       for (int w = 0; w < 16; ++w) {
-        int c = warp_cnt[w];
-        warp_cnt[w] = s;
-        s += c;
+        const int c = warp_cnt[w];
+        warp_cnt[w] = sacc;
+        sacc += c;
       }
-      list_n = s;
+      list_n = sacc;
     }
     __syncthreads();
     if (hit) list[warp_cnt[warp] + __popc(mask & ((1u << lane) - 1u))] = ai;
     __syncthreads();
     const int cnt = list_n;
-    for (int q0 = 0; q0 < cnt; q0 += kSub) {
-      const int nq = min(kSub, cnt - q0);
-      // tabulate offsets of the brick coordinates (inf = outside the box)
-      if (tid < nq * (kBX + kBY + kBZ)) {
-        const int q = tid / (kBX + kBY + kBZ), e = tid % (kBX + kBY + kBZ);
+    for (int q0 = 0; q0 < cnt; q0 += kGroup) {
+      const int nq = min(kGroup, cnt - q0);
+      // tabulate the group's offsets over the superbrick (inf = outside)
+      for (int e = tid; e < nq * (kSX + kSY + kSZ); e += 512) {
+        const int q = e / (kSX + kSY + kSZ), r = e % (kSX + kSY + kSZ);
         const AtomGeo& a = atoms[list[q0 + q]];
         int axis, li, g, n;
-        if (e < kBX) { axis = 0; li = e; g = x0 + e; n = nx; }
-        else if (e < kBX + kBY) { axis = 1; li = e - kBX; g = y0 + li; n = ny; }
-        else { axis = 2; li = e - kBX - kBY; g = z0 + li; n = nz; }
+        if (r < kSX) { axis = 0; li = r; g = x0 + r; n = nx; }
+        else if (r < kSX + kSY) { axis = 1; li = r - kSX; g = y0 + li; n = ny; }
+        else { axis = 2; li = r - kSX - kSY; g = z0 + li; n = nz; }
         double off = 0.0;
         const bool in = g < n && axis_offset(a, axis, g, n, off);
         const Off v = in ? Off(off) : kOut;
         if (axis == 0) tx[q][li] = v; else if (axis == 1) ty[q][li] = v; else tz[q][li] = v;
       }
+      if (tid < nq) {
+        const AtomGeo& a = atoms[list[q0 + tid]];
+        pw[tid] = float(a.w);
+        pinv[tid] = float(a.inv2sd);
+        phd[tid] = float(a.half_d);
+        pd2[tid] = a.d2;
+      }
       __syncthreads();
       if (live) {
         for (int q = 0; q < nq; ++q) {
-          const Off ox = tx[q][lx], oy = ty[q][ly], oz = tz[q][lz];
-          if (ox == kOut || oy == kOut || oz == kOut) continue;
-          const AtomGeo& a = atoms[list[q0 + q]];
+          const Off oy = ty[q][ly], oz = tz[q][lz];
+          if (oy == kOut || oz == kOut) continue;
           if constexpr (sizeof(T) == 8) {
-            double t;
-            const double v = profile64(a, u2_exact(ox, oy, oz), t);
-            acc = __dadd_rn(acc, __dmul_rn(a.w, v));
+            const AtomGeo& a = atoms[list[q0 + q]];
+#pragma unroll
+            for (int i = 0; i < kSX; ++i) {
+              const Off ox = tx[q][i];
+              if (ox == kOut) continue;
+              double t;
+              const double v = profile64(a, u2_exact(ox, oy, oz), t);
+              acc[i] = __dadd_rn(acc[i], __dmul_rn(a.w, v));
+            }
           } else {
-            float t, lg;
-            const float v = profile32(float(a.inv2sd), float(a.half_d), a.d2, ox * ox + oy * oy + oz * oz,
-                                      t, lg);
-            acc += a.w * double(v);
+            const float yz = oy * oy + oz * oz;
+            const float inv = pinv[q], hd = phd[q], w = pw[q];
+            const bool d2 = pd2[q] != 0;
+#pragma unroll
+            for (int i = 0; i < kSX; ++i) {
+              const Off ox = tx[q][i];
+              if (ox == kOut) continue;
+              float t, lg;
+              const float v = profile32(inv, hd, d2, ox * ox + yz, t, lg);
+              acc[i] = fmaf(w, v, acc[i]);
+            }
           }
         }
       }
       __syncthreads();
     }
   }
-  if (live) out[((long long)gx * ny + gy) * nz + gz] = T(acc);
+  if (live) {
+#pragma unroll
+    for (int i = 0; i < kSX; ++i)
+      if (x0 + i < nx) out[((long long)(x0 + i) * ny + gy) * nz + gz] = T(acc[i]);
+  }
 }
 
 // -------------------------------------------------------------- atom sums
+// A chunk is a run of whole z-rows (a, b) of one atom box, ~4096 voxels.
+// Warps take rows; lanes run along z (coalesced field loads, tabulated
+// per-axis wrapped index / offset, one integer division per row).
 struct Chunk {
   int atom;
-  int first;  // first voxel (linear in the atom box, z fastest)
+  int row0;   // first row (a * len[1] + b)
+  int nrows;
 };
+
+template <typename T>
+__device__ __forceinline__ void atom_terms(const AtomGeo& a, T ox, T oy, T oz, T b, double (&s)[6],
+                                           float (&sf)[6], float inv2sd, float half_d, float dd,
+                                           float dos, float lsig) {
+  if constexpr (sizeof(T) == 8) {
+    const double u2 = u2_exact(ox, oy, oz);
+    double t;
+    const double val = profile64(a, u2, t);
+    double ampl = 0.0, lr = 0.0;
+    if (u2 > 0.0) {
+      ampl = __ddiv_rn(__dmul_rn(__dmul_rn(a.d, val), t), u2);
+      lr = __dsub_rn(__dmul_rn(0.5, log(u2)), a.log_sigma);
+    }
+    const double vt = __dmul_rn(val, t);
+    s[0] += val * b;
+    s[1] += __dmul_rn(ampl, ox) * b;
+    s[2] += __dmul_rn(ampl, oy) * b;
+    s[3] += __dmul_rn(ampl, oz) * b;
+    s[4] += __dmul_rn(vt, a.d_over_sigma) * b;
+    s[5] += __dmul_rn(-vt, lr) * b;
+  } else {
+    const float u2 = ox * ox + oy * oy + oz * oz;
+    float t, lg;
+    const float val = profile32(inv2sd, half_d, a.d2, u2, t, lg);
+    float ampl = 0.f, lr = 0.f;
+    if (u2 > 0.f) {
+      ampl = __fdividef(dd * val * t, u2);
+      lr = 0.34657359027997264f * lg - lsig;  // 0.5 ln(u2) = 0.5 ln2 log2(u2)
+    }
+    const float vt = val * t;
+    const float ab = ampl * b;
+    sf[0] += val * b;
+    sf[1] += ab * ox;
+    sf[2] += ab * oy;
+    sf[3] += ab * oz;
+    sf[4] += vt * dos * b;
+    sf[5] -= vt * lr * b;
+  }
+}
 
 template <typename T>
 __global__ void __launch_bounds__(kSumThreads) atom_sums_kernel(
@@ -188,96 +286,53 @@ __global__ void __launch_bounds__(kSumThreads) atom_sums_kernel(
     const T* __restrict__ field, double* __restrict__ partials) {
   using Off = T;
   __shared__ Off toff[3][kMaxAxis];
-  __shared__ int tidx[3][kMaxAxis];
+  __shared__ int tlin[3][kMaxAxis];  // wrapped index x axis stride (volumes < 2^31 voxels)
   const Chunk ch = chunks[blockIdx.x];
   const AtomGeo& a = atoms[ch.atom];
   const int dims[3] = {nx, ny, nz};
-  const int vend = int(min((long long)ch.first + kChunk, a.nvox));
-  const int l2 = a.len[2], l1 = a.len[1];
-  const bool tab = a.len[0] <= kMaxAxis && l1 <= kMaxAxis && l2 <= kMaxAxis;
-  if (tab) {
+  const int strides[3] = {ny * nz, nz, 1};
+  const int l1 = a.len[1], l2 = a.len[2];
+  // the planner only emits these chunks for boxes with every axis <= kMaxAxis
 #pragma unroll
-    for (int ax = 0; ax < 3; ++ax)
-      for (int il = threadIdx.x; il < a.len[ax]; il += kSumThreads) {
-        if (a.full[ax]) {
-          tidx[ax][il] = il;
-          toff[ax][il] = Off(min_image(il, a.m[ax], dims[ax]));
-        } else {
-          const int p = a.start[ax] + il;
-          tidx[ax][il] = pmod(p, dims[ax]);
-          toff[ax][il] = Off(__dsub_rn(double(p), a.m[ax]));
-        }
+  for (int ax = 0; ax < 3; ++ax)
+    for (int il = threadIdx.x; il < a.len[ax]; il += kSumThreads) {
+      if (a.full[ax]) {
+        tlin[ax][il] = il * strides[ax];
+        toff[ax][il] = Off(min_image(il, a.m[ax], dims[ax]));
+      } else {
+        const int p = a.start[ax] + il;
+        tlin[ax][il] = pmod(p, dims[ax]) * strides[ax];
+        toff[ax][il] = Off(__dsub_rn(double(p), a.m[ax]));
       }
-  }
+    }
   __syncthreads();
 
   double s[6] = {0, 0, 0, 0, 0, 0};
   float sf[6] = {0, 0, 0, 0, 0, 0};
   const float inv2sd = float(a.inv2sd), half_d = float(a.half_d), dd = float(a.d),
               dos = float(a.d_over_sigma), lsig = float(a.log_sigma);
-  for (int v = ch.first + threadIdx.x; v < vend; v += kSumThreads) {
-    const int rest = v / l2;  // 32-bit index math (boxes hold < 2^31 voxels)
-    const int ic = v - rest * l2;
-    const int ia = rest / l1;
-    const int ib = rest - ia * l1;
-    int g[3];
-    Off off[3];
-    const int il[3] = {ia, ib, ic};
-    if (tab) {
-#pragma unroll
-      for (int ax = 0; ax < 3; ++ax) {
-        g[ax] = tidx[ax][il[ax]];
-        off[ax] = toff[ax][il[ax]];
-      }
-    } else {
-#pragma unroll
-      for (int ax = 0; ax < 3; ++ax) {
-        if (a.full[ax]) {
-          g[ax] = il[ax];
-          off[ax] = Off(min_image(il[ax], a.m[ax], dims[ax]));
-        } else {
-          const int p = a.start[ax] + il[ax];
-          g[ax] = pmod(p, dims[ax]);
-          off[ax] = Off(__dsub_rn(double(p), a.m[ax]));
-        }
-      }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // flat voxels of the chunk (z fastest), one per thread per step of
+  // kSumThreads; (row, z) and (a, b) advance incrementally
+  const int nv = ch.nrows * l2;
+  int ic = threadIdx.x % l2, q = threadIdx.x / l2;
+  int ib = (ch.row0 + q) % l1, ia = (ch.row0 + q) / l1;
+  const int dq = kSumThreads / l2, dc = kSumThreads % l2;
+  const int da = dq / l1, db = dq % l1;
+  for (int v = threadIdx.x; v < nv; v += kSumThreads) {
+    const T b = field[tlin[0][ia] + tlin[1][ib] + tlin[2][ic]];
+    atom_terms<T>(a, toff[0][ia], toff[1][ib], toff[2][ic], b, s, sf, inv2sd, half_d, dd, dos, lsig);
+    ic += dc;
+    int carry = 0;
+    if (ic >= l2) {
+      ic -= l2;
+      carry = 1;
     }
-    const T b = field[((long long)g[0] * ny + g[1]) * nz + g[2]];
-    if constexpr (sizeof(T) == 8) {
-      const double u2 = u2_exact(off[0], off[1], off[2]);
-      double t;
-      const double val = profile64(a, u2, t);
-      double ampl = 0.0, lr = 0.0;
-      if (u2 > 0.0) {
-        ampl = __ddiv_rn(__dmul_rn(__dmul_rn(a.d, val), t), u2);
-        lr = __dsub_rn(__dmul_rn(0.5, log(u2)), a.log_sigma);
-      }
-      const double vt = __dmul_rn(val, t);
-      s[0] += val * b;
-      s[1] += __dmul_rn(ampl, off[0]) * b;
-      s[2] += __dmul_rn(ampl, off[1]) * b;
-      s[3] += __dmul_rn(ampl, off[2]) * b;
-      s[4] += __dmul_rn(vt, a.d_over_sigma) * b;
-      s[5] += __dmul_rn(-vt, lr) * b;
-    } else {
-      const float fx = off[0], fy = off[1], fz = off[2];
-      const float u2 = fx * fx + fy * fy + fz * fz;
-      float t, lg;
-      const float val = profile32(inv2sd, half_d, a.d2, u2, t, lg);
-      float ampl = 0.f, lr = 0.f;
-      if (u2 > 0.f) {
-        ampl = dd * val * t * __frcp_rn(u2);
-        lr = 0.34657359027997264f * lg - lsig;  // 0.5 ln(u2) = 0.5 ln2 log2(u2)
-      }
-      const float vt = val * t;
-      const float bf = float(b);
-      const float ab = ampl * bf;
-      sf[0] += val * bf;
-      sf[1] += ab * fx;
-      sf[2] += ab * fy;
-      sf[3] += ab * fz;
-      sf[4] += vt * dos * bf;
-      sf[5] -= vt * lr * bf;
+    ib += db + carry;
+    ia += da;
+    if (ib >= l1) {
+      ib -= l1;
+      ++ia;
     }
   }
   if constexpr (sizeof(T) != 8) {
@@ -286,7 +341,70 @@ __global__ void __launch_bounds__(kSumThreads) atom_sums_kernel(
   }
   // block reduction in fp64 (fixed order: warp tree, then warps in order)
   __shared__ double red[6][kSumThreads / 32];
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    double x = s[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (lane == 0) red[c][warp] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    double x = 0.0;
+    for (int w = 0; w < kSumThreads / 32; ++w) x += red[threadIdx.x][w];
+    partials[(long long)blockIdx.x * 6 + threadIdx.x] = x;
+  }
+}
+
+// Boxes with an axis longer than kMaxAxis (huge sigma on a huge grid): one
+// voxel per thread with the offsets computed on the fly (rare fallback).
+template <typename T>
+__global__ void __launch_bounds__(kSumThreads) atom_sums_big_kernel(
+    const AtomGeo* __restrict__ atoms, const Chunk* __restrict__ chunks, int nx, int ny, int nz,
+    const T* __restrict__ field, double* __restrict__ partials) {
+  const Chunk ch = chunks[blockIdx.x];
+  const AtomGeo& a = atoms[ch.atom];
+  const int dims[3] = {nx, ny, nz};
+  const int l1 = a.len[1], l2 = a.len[2];
+  double s[6] = {0, 0, 0, 0, 0, 0};
+  float sf[6] = {0, 0, 0, 0, 0, 0};
+  const float inv2sd = float(a.inv2sd), half_d = float(a.half_d), dd = float(a.d),
+              dos = float(a.d_over_sigma), lsig = float(a.log_sigma);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int r = ch.row0 + warp; r < ch.row0 + ch.nrows; r += kSumThreads / 32) {
+    const int il[2] = {r / l1, r - (r / l1) * l1};
+    int g[2];
+    T o[2];
+    for (int ax = 0; ax < 2; ++ax) {
+      if (a.full[ax]) {
+        g[ax] = il[ax];
+        o[ax] = T(min_image(il[ax], a.m[ax], dims[ax]));
+      } else {
+        const int p = a.start[ax] + il[ax];
+        g[ax] = pmod(p, dims[ax]);
+        o[ax] = T(__dsub_rn(double(p), a.m[ax]));
+      }
+    }
+    const T* frow = field + ((long long)g[0] * ny + g[1]) * nz;
+    for (int ic = lane; ic < l2; ic += 32) {
+      int gz;
+      T oz;
+      if (a.full[2]) {
+        gz = ic;
+        oz = T(min_image(ic, a.m[2], nz));
+      } else {
+        const int p = a.start[2] + ic;
+        gz = pmod(p, nz);
+        oz = T(__dsub_rn(double(p), a.m[2]));
+      }
+      atom_terms<T>(a, o[0], o[1], oz, frow[gz], s, sf, inv2sd, half_d, dd, dos, lsig);
+    }
+  }
+  if constexpr (sizeof(T) != 8) {
+#pragma unroll
+    for (int c = 0; c < 6; ++c) s[c] = double(sf[c]);
+  }
+  __shared__ double red[6][kSumThreads / 32];
 #pragma unroll
   for (int c = 0; c < 6; ++c) {
     double x = s[c];
@@ -361,8 +479,8 @@ __global__ void final_sum_kernel(const double* __restrict__ partials, int n, dou
 
 int render_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const AtomGeo* atoms_dev, int k,
                 void* out) {
-  const int nb = ((dims[0] + kBX - 1) / kBX) * ((dims[1] + kBY - 1) / kBY) *
-                 ((dims[2] + kBZ - 1) / kBZ);
+  const int nb = ((dims[0] + kSX - 1) / kSX) * ((dims[1] + kSY - 1) / kSY) *
+                 ((dims[2] + kSZ - 1) / kSZ);
   SFW3D_PROF(ctx, "render");
   if (dtype == SFW3D_F64)
     render_kernel<double><<<nb, 512, 0, ctx->stream>>>(atoms_dev, k, dims[0], dims[1], dims[2],
@@ -374,20 +492,34 @@ int render_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const AtomGeo* ato
   return SFW3D_OK;
 }
 
+// Row chunks (~kChunk voxels of whole z-rows) per atom, in atom order; the
+// atom's chunks are contiguous and first[i]..first[i+1] delimits them.
 static void chunk_plan(const std::vector<AtomGeo>& atoms, std::vector<Chunk>& chunks,
                        std::vector<int>& first) {
   chunks.clear();
   first.assign(atoms.size() + 1, 0);
   for (size_t i = 0; i < atoms.size(); ++i) {
     first[i] = int(chunks.size());
-    for (long long v = 0; v < atoms[i].nvox; v += kChunk) chunks.push_back({int(i), int(v)});
+    const AtomGeo& a = atoms[i];
+    const int rows = a.len[0] * a.len[1];
+    const int per = std::max(1, kChunk / std::max(1, a.len[2]));
+    for (int r = 0; r < rows; r += per) chunks.push_back({int(i), r, std::min(per, rows - r)});
   }
   first[atoms.size()] = int(chunks.size());
 }
 
+static bool small_boxes(const std::vector<AtomGeo>& atoms, const int dims[3]) {
+  if ((long long)dims[0] * dims[1] * dims[2] >= (1LL << 31)) return false;  // int32 offsets
+  for (const auto& a : atoms)
+    if (a.len[0] > kMaxAxis || a.len[1] > kMaxAxis || a.len[2] > kMaxAxis) return false;
+  return true;
+}
+
 size_t atom_sums_scratch(const std::vector<AtomGeo>& atoms) {
-  size_t nch = 0;
-  for (auto& a : atoms) nch += size_t((a.nvox + kChunk - 1) / kChunk);
+  std::vector<Chunk> chunks;
+  std::vector<int> first;
+  chunk_plan(atoms, chunks, first);
+  const size_t nch = chunks.size();
   return Carver::need({nch * sizeof(Chunk), (atoms.size() + 1) * sizeof(int), nch * 6 * sizeof(double)});
 }
 
@@ -411,12 +543,22 @@ int atom_sums_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const void* fie
   SFW3D_TRY(stage_upload(ctx, first_dev, first.data(), first.size() * sizeof(int)));
   const unsigned nch = unsigned(chunks.size());
   SFW3D_PROF(ctx, "atom_sums");
-  if (dtype == SFW3D_F64)
-    atom_sums_kernel<double><<<nch, kSumThreads, 0, ctx->stream>>>(
-        atoms_dev, ch_dev, dims[0], dims[1], dims[2], static_cast<const double*>(field), part);
-  else
-    atom_sums_kernel<float><<<nch, kSumThreads, 0, ctx->stream>>>(
-        atoms_dev, ch_dev, dims[0], dims[1], dims[2], static_cast<const float*>(field), part);
+  const bool small = small_boxes(atoms, dims);
+  if (dtype == SFW3D_F64) {
+    if (small)
+      atom_sums_kernel<double><<<nch, kSumThreads, 0, ctx->stream>>>(
+          atoms_dev, ch_dev, dims[0], dims[1], dims[2], static_cast<const double*>(field), part);
+    else
+      atom_sums_big_kernel<double><<<nch, kSumThreads, 0, ctx->stream>>>(
+          atoms_dev, ch_dev, dims[0], dims[1], dims[2], static_cast<const double*>(field), part);
+  } else {
+    if (small)
+      atom_sums_kernel<float><<<nch, kSumThreads, 0, ctx->stream>>>(
+          atoms_dev, ch_dev, dims[0], dims[1], dims[2], static_cast<const float*>(field), part);
+    else
+      atom_sums_big_kernel<float><<<nch, kSumThreads, 0, ctx->stream>>>(
+          atoms_dev, ch_dev, dims[0], dims[1], dims[2], static_cast<const float*>(field), part);
+  }
   SFW3D_LAUNCH_CHECK(ctx);
   chunk_combine_kernel<<<(k * 6 + 255) / 256, 256, 0, ctx->stream>>>(first_dev, k, part, sums_dev);
   SFW3D_LAUNCH_CHECK(ctx);
