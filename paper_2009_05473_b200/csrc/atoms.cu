@@ -28,6 +28,7 @@ namespace {
 constexpr int kChunk = 4096;               // atom-sum chunk (voxels)
 constexpr int kSumThreads = 256;
 constexpr int kMaxAxis = 1024;             // tabulated axis length in atom sums
+constexpr int kMaxRows = 512;              // rows per chunk
 
 // a mod n in [0, n) without a division on the common path (|a| < 2n)
 __device__ __forceinline__ int pmod(int a, int n) {
@@ -280,31 +281,45 @@ __device__ __forceinline__ void atom_terms(const AtomGeo& a, T ox, T oy, T oz, T
   }
 }
 
+// per-row record of a chunk: offsets (x, y) from the atom centre and the
+// linear offset of the row's first z in the volume (int32: < 2^31 voxels)
+template <typename T>
+struct RowRec {
+  T ox, oy;
+  int lin;
+};
+
 template <typename T>
 __global__ void __launch_bounds__(kSumThreads) atom_sums_kernel(
     const AtomGeo* __restrict__ atoms, const Chunk* __restrict__ chunks, int nx, int ny, int nz,
     const T* __restrict__ field, double* __restrict__ partials) {
-  using Off = T;
-  __shared__ Off toff[3][kMaxAxis];
-  __shared__ int tlin[3][kMaxAxis];  // wrapped index x axis stride (volumes < 2^31 voxels)
+  __shared__ RowRec<T> rows[kMaxRows];
+  __shared__ T tzo[kMaxAxis];   // z offsets (full z axes only)
   const Chunk ch = chunks[blockIdx.x];
   const AtomGeo& a = atoms[ch.atom];
-  const int dims[3] = {nx, ny, nz};
-  const int strides[3] = {ny * nz, nz, 1};
   const int l1 = a.len[1], l2 = a.len[2];
-  // the planner only emits these chunks for boxes with every axis <= kMaxAxis
+  for (int q = threadIdx.x; q < ch.nrows; q += kSumThreads) {
+    const int r = ch.row0 + q;
+    const int il[2] = {r / l1, r - (r / l1) * l1};
+    const int dims2[2] = {nx, ny};
+    int g[2];
+    T o[2];
 #pragma unroll
-  for (int ax = 0; ax < 3; ++ax)
-    for (int il = threadIdx.x; il < a.len[ax]; il += kSumThreads) {
+    for (int ax = 0; ax < 2; ++ax) {
       if (a.full[ax]) {
-        tlin[ax][il] = il * strides[ax];
-        toff[ax][il] = Off(min_image(il, a.m[ax], dims[ax]));
+        g[ax] = il[ax];
+        o[ax] = T(min_image(il[ax], a.m[ax], dims2[ax]));
       } else {
-        const int p = a.start[ax] + il;
-        tlin[ax][il] = pmod(p, dims[ax]) * strides[ax];
-        toff[ax][il] = Off(__dsub_rn(double(p), a.m[ax]));
+        const int p = a.start[ax] + il[ax];
+        g[ax] = pmod(p, dims2[ax]);
+        o[ax] = T(__dsub_rn(double(p), a.m[ax]));
       }
     }
+    rows[q] = {o[0], o[1], (g[0] * ny + g[1]) * nz};
+  }
+  const bool zfull = a.full[2] != 0;
+  if (zfull)
+    for (int ic = threadIdx.x; ic < l2; ic += kSumThreads) tzo[ic] = T(min_image(ic, a.m[2], nz));
   __syncthreads();
 
   double s[6] = {0, 0, 0, 0, 0, 0};
@@ -312,27 +327,34 @@ __global__ void __launch_bounds__(kSumThreads) atom_sums_kernel(
   const float inv2sd = float(a.inv2sd), half_d = float(a.half_d), dd = float(a.d),
               dos = float(a.d_over_sigma), lsig = float(a.log_sigma);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // flat voxels of the chunk (z fastest), one per thread per step of
-  // kSumThreads; (row, z) and (a, b) advance incrementally
+  // z of box column ic: volume index zs + ic (wrapped once), offset oz0 + ic
+  const int zs = zfull ? 0 : pmod(a.start[2], nz);
+  const T oz0 = zfull ? T(0) : T(__dsub_rn(double(a.start[2]), a.m[2]));
+  // flat voxels of the chunk (z fastest), one per thread per kSumThreads step
   const int nv = ch.nrows * l2;
   int ic = threadIdx.x % l2, q = threadIdx.x / l2;
-  int ib = (ch.row0 + q) % l1, ia = (ch.row0 + q) / l1;
   const int dq = kSumThreads / l2, dc = kSumThreads % l2;
-  const int da = dq / l1, db = dq % l1;
   for (int v = threadIdx.x; v < nv; v += kSumThreads) {
-    const T b = field[tlin[0][ia] + tlin[1][ib] + tlin[2][ic]];
-    atom_terms<T>(a, toff[0][ia], toff[1][ib], toff[2][ic], b, s, sf, inv2sd, half_d, dd, dos, lsig);
+    const RowRec<T> rr = rows[q];
+    int gz;
+    T oz;
+    if (zfull) {
+      gz = ic;
+      oz = tzo[ic];
+    } else {
+      gz = zs + ic;
+      gz = gz >= nz ? gz - nz : gz;
+      if constexpr (sizeof(T) == 8)
+        oz = __dsub_rn(double(a.start[2] + ic), a.m[2]);  // the reference's span - m
+      else
+        oz = oz0 + float(ic);
+    }
+    atom_terms<T>(a, rr.ox, rr.oy, oz, field[rr.lin + gz], s, sf, inv2sd, half_d, dd, dos, lsig);
     ic += dc;
-    int carry = 0;
+    q += dq;
     if (ic >= l2) {
       ic -= l2;
-      carry = 1;
-    }
-    ib += db + carry;
-    ia += da;
-    if (ib >= l1) {
-      ib -= l1;
-      ++ia;
+      ++q;
     }
   }
   if constexpr (sizeof(T) != 8) {
@@ -502,7 +524,7 @@ static void chunk_plan(const std::vector<AtomGeo>& atoms, std::vector<Chunk>& ch
     first[i] = int(chunks.size());
     const AtomGeo& a = atoms[i];
     const int rows = a.len[0] * a.len[1];
-    const int per = std::max(1, kChunk / std::max(1, a.len[2]));
+    const int per = std::min(kMaxRows, std::max(1, kChunk / std::max(1, a.len[2])));
     for (int r = 0; r < rows; r += per) chunks.push_back({int(i), r, std::min(per, rows - r)});
   }
   first[atoms.size()] = int(chunks.size());
