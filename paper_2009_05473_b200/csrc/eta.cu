@@ -100,6 +100,7 @@ struct Geo {
   int pitch;           // smem row pitch (elements)
   int brows;           // template rows per staged chunk
   double lam;          // eta = sum / lam (certificate.py:160)
+  void* accd_g;        // folded kernel: slice sums in global scratch (or NULL: smem)
 };
 
 // One 4-tap step with compile-time window rotation R (0..4): the window
@@ -304,21 +305,23 @@ __device__ __forceinline__ void stage_sum(T* __restrict__ S, const T* __restrict
 }
 
 // resident CTAs per SM the register budget is sized for (fp32 tiles)
-template <typename T, int KJ, int NWY>
+template <typename T, int KJ, int NWY, bool AG>
 constexpr int fold_min_blocks() {
-  return sizeof(T) == 8 ? 1 : (NWY == 2 ? 2 : (KJ == 32 ? 3 : 4));
+  return sizeof(T) == 8 ? 1 : (NWY == 2 ? 2 : (KJ == 32 ? (AG ? 4 : 3) : 4));
 }
 
-template <typename T, int KJ, int NWY>
-__global__ void __launch_bounds__(kThreads * NWY, (fold_min_blocks<T, KJ, NWY>())) eta_fold_kernel(const T* __restrict__ bpad, Geo g,
+// AG: slice sums in a global scratch slab per CTA instead of shared memory
+template <typename T, int KJ, int NWY, bool AG = false>
+__global__ void __launch_bounds__(kThreads * NWY, (fold_min_blocks<T, KJ, NWY, AG>())) eta_fold_kernel(const T* __restrict__ bpad, Geo g,
                                                                   CandDev cd, T* __restrict__ field,
                                                                   Best* __restrict__ partial) {
   constexpr int NT = kThreads * NWY, TY = kTY * NWY, TZ = KJ * kWarps;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Best wbest[kWarps * NWY];
   const int nrows = TY + cd.lb - 1;  // rows of the staged plane (whole b range)
-  T* accd = reinterpret_cast<T*>(smem_raw);  // [KJ][NT] slice sums
-  T* stap = accd + KJ * NT;                   // [Rb + 1][lc4] tap rows b >= 0 (+8)
+  T* accd = AG ? static_cast<T*>(g.accd_g) + ((long long)blockIdx.y * gridDim.x + blockIdx.x) * KJ * NT
+               : reinterpret_cast<T*>(smem_raw);  // [KJ][NT] slice sums
+  T* stap = AG ? reinterpret_cast<T*>(smem_raw) : accd + KJ * NT;  // [Rb + 1][lc4] tap rows b >= 0 (+8)
   const int ntap = (cd.lb / 2 + 1) * cd.lc4;
   int2* srows = reinterpret_cast<int2*>(stap + ((ntap + 8 + 3) & ~3));  // [Rb + 1] (+pad)
   T* plane = reinterpret_cast<T*>(srows + ((cd.lb / 2 + 1 + 1) & ~1));
@@ -638,20 +641,33 @@ static int fold_nwy_rt(int esize) {
   return esize == 8 ? 1 : nwy32;
 }
 static int fold_tz(int esize) { return fold_kj_rt(esize) * kWarps; }
+// fp32 KJ = 32 tiles keep the per-slice sums in a global scratch slab per
+// CTA (L2-resident traffic of 2 x 16 KB per slice): the freed 16 KB of shared
+// memory and a 128-register budget give 4 resident CTAs instead of 3
+// (SFW3D_FOLD_ACCD_GLOBAL=0: shared-memory sums, for comparison)
+static bool fold_accd_global(int esize) {
+  static const int ag = env_int("SFW3D_FOLD_ACCD_GLOBAL", 1);
+  return esize == 4 && ag != 0 && fold_kj_rt(esize) == 32 && fold_nwy_rt(esize) == 1;
+}
 static int fold_smem(const CandHost& c, int esize) {
   const int kj = fold_kj_rt(esize), nwy = fold_nwy_rt(esize);
+  if (fold_accd_global(esize)) {
+    const int ntap = ((c.lb / 2 + 1) * c.lc4 + 8 + 3) & ~3;
+    const int nrow2 = ((c.lb / 2 + 2) & ~1) * (8 / esize);
+    return (ntap + nrow2 + (kTY * nwy + c.lb - 1) * region_pitch(c.lc4, esize, fold_tz(esize))) * esize;
+  }
   const int ntap = ((c.lb / 2 + 1) * c.lc4 + 8 + 3) & ~3;
   const int nrow2 = ((c.lb / 2 + 2) & ~1) * (8 / esize);  // int2 rows in elements
   return (kj * kThreads * nwy + ntap + nrow2 +
           (kTY * nwy + c.lb - 1) * region_pitch(c.lc4, esize, fold_tz(esize))) * esize;
 }
 
-template <typename T, int KJ, int NWY>
+template <typename T, int KJ, int NWY, bool AG = false>
 static int launch_fold(sfw3d_ctx* ctx, dim3 grid, int smem, const T* bpad, const Geo& g,
                        const CandDev& cd, T* fld, Best* partial) {
-  SFW3D_CUDA_TRY(cudaFuncSetAttribute(eta_fold_kernel<T, KJ, NWY>,
+  SFW3D_CUDA_TRY(cudaFuncSetAttribute(eta_fold_kernel<T, KJ, NWY, AG>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  eta_fold_kernel<T, KJ, NWY><<<grid, kThreads * NWY, smem, ctx->stream>>>(bpad, g, cd, fld, partial);
+  eta_fold_kernel<T, KJ, NWY, AG><<<grid, kThreads * NWY, smem, ctx->stream>>>(bpad, g, cd, fld, partial);
   SFW3D_LAUNCH_CHECK(ctx);
   return SFW3D_OK;
 }
@@ -896,9 +912,17 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   const long long nblocks_direct = (long long)nty * ntz * nxp;
   const long long nblocks = nblocks_direct;
   const size_t rb = any_refine ? size_t(kRefCap) * (4 + 8 + 8) + size_t(nc) * 8 + 64 : 0;
+  // folded kernel slice sums in global memory (tuning variant)
+  size_t ab = 0;
+  if (fold_accd_global(sizeof(T))) {
+    const int tzf = fold_tz(sizeof(T));
+    const long long nctas = (long long)((ow[3] - ow[2] + 1 + kTY - 1) / kTY) *
+                            ((ow[5] - zbase + 1 + tzf - 1) / tzf) * nxp;
+    ab = size_t(nctas) * fold_kj_rt(sizeof(T)) * kThreads * sizeof(T);
+  }
   SFW3D_TRY(ensure_device(ctx, ctx->ws,
                           Carver::need({vb, vb, sb, pb, size_t(nblocks) * sizeof(Best),
-                                        size_t(nc) * sizeof(Best), rb})));
+                                        size_t(nc) * sizeof(Best), rb, ab})));
   Carver cv(ctx->ws.ptr);
   T* b = cv.take<T>(n);
   T* tmp = cv.take<T>(n);
@@ -913,6 +937,7 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   double* ref_l1 = any_refine ? cv.take<double>(1) : nullptr;
   int* ref_count = any_refine ? cv.take<int>(1) : nullptr;
   std::vector<Best> refined(nc, Best{NAN, -1});  // exact maxima of refined members
+  void* accd_g = ab ? cv.take<char>(ab) : nullptr;
   // b = H^T * r (tmp is pass scratch), then the periodic padding for direct
   SFW3D_TRY(psf_apply_impl(ctx, t->psf, dtype, residual, b, 1, tmp));
   if (pb) {
@@ -935,6 +960,7 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   g.nty = nty;
   g.ntz = ntz;
   g.lam = lam;
+  g.accd_g = accd_g;
   int smem_max = 0;
   SFW3D_CUDA_TRY(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
   const int budget = std::min(smem_max - 2048, 110 * 1024);
@@ -1019,7 +1045,9 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
         SFW3D_PROF(ctx, "eta_direct");
         dim3 grid(unsigned(gc.nty * gc.ntz), unsigned(nxp));
         if constexpr (sizeof(T) == 4) {
-          if (kj == 32 && nwy == 2)
+          if (kj == 32 && nwy == 1 && fold_accd_global(4))
+            SFW3D_TRY((launch_fold<T, 32, 1, true>(ctx, grid, smem, bpad, gc, cd, fld, partial)));
+          else if (kj == 32 && nwy == 2)
             SFW3D_TRY((launch_fold<T, 32, 2>(ctx, grid, smem, bpad, gc, cd, fld, partial)));
           else if (kj == 32)
             SFW3D_TRY((launch_fold<T, 32, 1>(ctx, grid, smem, bpad, gc, cd, fld, partial)));
