@@ -539,6 +539,15 @@ int launch_z2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* t
   return SFW3D_OK;
 }
 
+// taps at or below which a pass takes the J = 16 tile (SFW3D_NARROW_TAPS)
+static int narrow_taps() {
+  static const int v = [] {
+    const char* e = getenv("SFW3D_NARROW_TAPS");
+    return e ? atoi(e) : 24;
+  }();
+  return v;
+}
+
 template <typename T>
 int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis, const T* taps,
                int lo, int ntaps, const T* addend, double aw, double w) {
@@ -554,7 +563,8 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
   }();
   if (axis == 2) {
     if (variant == 0 && dims[2] % 4 == 0 && ntaps <= 1024) {
-      if (dims[2] >= 128)
+      // narrow filters are HBM-bound: the smaller tile keeps more CTAs resident
+      if (dims[2] >= 128 && ntaps > narrow_taps())
         return launch_z2<T, 32>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
       return launch_z2<T, 16>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
     }
@@ -564,7 +574,7 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
   long long stride = 1;
   for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
   if (variant == 0 && stride % 64 == 0 && ntaps <= 512) {
-    if (dims[axis] >= 128)
+    if (dims[axis] >= 128 && ntaps > narrow_taps())
       return launch_tile2<T, 32>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
     return launch_tile2<T, 16>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
   }
