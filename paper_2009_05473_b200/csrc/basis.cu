@@ -283,6 +283,8 @@ struct BasisSet {
 
 // coarse dictionary size (the fine one has 2 * kDictCoarse - 1 points)
 constexpr int kDictCoarse = 49;
+// tangent betas per d < 2 candidate (s = 1, 2, 4, ..., 2^(kTangents-1))
+constexpr int kTangents = 10;
 // no fit is accepted below this bound (double-precision evaluation floor)
 constexpr double kFitFloor = 1e-11;
 
@@ -319,20 +321,37 @@ int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands,
   // nested geometric dictionaries over [0.5 / rmax^2, 30] (the coarse one is
   // every other point of the fine one) plus the exact 1/(2 sigma^2) of every
   // d == 2 candidate
-  std::vector<double> dict = geometric(0.5 / (rmax * rmax), 30.0, 2 * kDictCoarse - 1);
+  const double bmin = 0.5 / (rmax * rmax);
+  std::vector<double> fine = geometric(bmin, 30.0, 2 * kDictCoarse - 1);
   for (int c : pool)
-    if (cands[c].d == 2.0) dict.push_back(0.5 / (cands[c].sigma * cands[c].sigma));
+    if (cands[c].d == 2.0) fine.push_back(0.5 / (cands[c].sigma * cands[c].sigma));
+  // tangent betas of a d < 2 candidate: the Gaussian matching the profile's
+  // log-slope at s = 2^j (d/2 s^(d/2-1) / (2 sigma^d)); they let the fine fit
+  // of a near-Gaussian profile (d close to 2) reach tol where the geometric
+  // grid alone stalls at a few 1e-9
+  std::vector<std::vector<double>> tangents(nc);
+  for (int c : pool) {
+    if (cands[c].d >= 2.0) continue;
+    const double a0 = 0.5 / std::pow(cands[c].sigma, cands[c].d) * 0.5 * cands[c].d;
+    for (int j = 0; j < kTangents; ++j) {
+      const double b = a0 * std::pow(double(1 << j), 0.5 * cands[c].d - 1.0);
+      if (b >= 0.5 * bmin && b <= 30.0) tangents[c].push_back(b);
+    }
+  }
+  std::vector<double> dict(fine);
+  for (int c : pool) dict.insert(dict.end(), tangents[c].begin(), tangents[c].end());
   std::sort(dict.begin(), dict.end());
   dict.erase(std::unique(dict.begin(), dict.end()), dict.end());
   const int K = int(dict.size());
-  std::vector<double> coarse = geometric(0.5 / (rmax * rmax), 30.0, kDictCoarse);
-  std::vector<int> coarse_idx;  // positions of the coarse points in dict
-  for (double b : coarse) {
+  auto index_of = [&](double b) {
     const auto it = std::min_element(dict.begin(), dict.end(), [&](double x, double y) {
       return std::fabs(x - b) < std::fabs(y - b);
     });
-    coarse_idx.push_back(int(it - dict.begin()));
-  }
+    return int(it - dict.begin());
+  };
+  std::vector<int> coarse_idx, fine_idx;  // positions of the grid points in dict
+  for (double b : geometric(bmin, 30.0, kDictCoarse)) coarse_idx.push_back(index_of(b));
+  for (double b : fine) fine_idx.push_back(index_of(b));
   // fit every pool candidate over the COMMON box: outside its own box the
   // target is its true profile (< 1e-12 there), so the mixture stays
   // controlled on the whole box the passes use. Coarse dictionary first, the
@@ -356,12 +375,22 @@ int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands,
     for (int k : coarse_idx) sub.push_back(dict[k]);
     double e = fit_on(sub, S, Sfit, cands[c].sigma, cands[c].d, w, w0fit[c]) + 1e-12;
     for (size_t q = 0; q < coarse_idx.size(); ++q) wfit[c][coarse_idx[q]] = w[q];
-    if (e > tol) {
+    // fine grid, then fine grid + the candidate's own tangent betas (each only
+    // when the previous level misses tol: extra betas are extra shared terms)
+    for (int level = 0; level < 2 && e > tol; ++level) {
+      std::vector<int> idx(fine_idx);
+      if (level == 1)
+        for (double b : tangents[c]) idx.push_back(index_of(b));
+      std::sort(idx.begin(), idx.end());
+      idx.erase(std::unique(idx.begin(), idx.end()), idx.end());
+      sub.clear();
+      for (int k : idx) sub.push_back(dict[k]);
       double z0;
-      const double e2 = fit_on(dict, S, Sfit, cands[c].sigma, cands[c].d, w, z0) + 1e-12;
+      const double e2 = fit_on(sub, S, Sfit, cands[c].sigma, cands[c].d, w, z0) + 1e-12;
       if (e2 < e) {
         e = e2;
-        wfit[c] = w;
+        wfit[c].assign(K, 0.0);
+        for (size_t q = 0; q < idx.size(); ++q) wfit[c][idx[q]] = w[q];
         w0fit[c] = z0;
       }
     }

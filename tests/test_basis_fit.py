@@ -105,7 +105,7 @@ def test_shared_basis_set(name, dims, sigmas, shapes):
         assert np.all(w >= 0.0) and r["w0"][c] >= 0.0
         assert abs(np.max(np.abs(approx - g)) + 1e-12 - err) <= 2e-13, (sg, d)
     # the (cfg) members this grid is expected to route to the basis path
-    n_expected = {"cfg1": 8, "cfg4": 8, "cfg2": 18, "cfg3": 21}[name]  # (cfg4 pruned: 512^3)
+    n_expected = {"cfg1": 8, "cfg4": 8, "cfg2": 18, "cfg3": 24}[name]  # (cfg4 pruned: 512^3)
     assert r["member"].sum() == n_expected
 
 
