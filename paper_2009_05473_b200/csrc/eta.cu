@@ -598,10 +598,7 @@ static int ensure_basis(const sfw3d_table* t, int dtype) {
   if (t->mode != 0) return SFW3D_OK;
   BasisSet*& s = dtype == SFW3D_F64 ? t->set64 : t->set32;
   if (s) return SFW3D_OK;
-  // small fp64 volumes: the direct kernels are cheap and the NNLS fits would
-  // dominate a solve — only the exact (d == 2) members join there
-  const bool small64 = dtype == SFW3D_F64 && vol_count(t->dims) < (1LL << 20);
-  const double tol = small64 ? std::min(t->basis_tol, 1e-12) : t->basis_tol;
+  const double tol = t->basis_tol;
   int dev = 0;
   SFW3D_CUDA_TRY(cudaGetDevice(&dev));
   SFW3D_CUDA_TRY(cudaSetDevice(t->device));
