@@ -255,9 +255,10 @@ def cert_workload(args, rank, world, dev):
     # roofline of the dominant kernel: one profiled step
     ctx.profile(True)
     step()
-    fam = {f: ctx.profile_read(f) for f in ("eta_direct", "eta_basis", "eta_mix", "psf_pass", "pad",
-                                           "argmax")}
+    fam = {f: ctx.profile_read(f) for f in ("eta_direct", "eta_basis", "eta_mix", "eta_refine",
+                                           "psf_pass", "pad", "argmax")}
     ctx.profile(False)
+    refine_count = N.last_refine_count()
     step_ms = sum(v[0] for v in fam.values())
     dom = max(fam, key=lambda f: fam[f][0])
     fp32_peak = ctx.probe_fp32()
@@ -349,6 +350,7 @@ def cert_workload(args, rank, world, dev):
         "value": value, "ms_per_step": ms_step, "launches": launches, "clocks": clk,
         "roofline": roof, "e2e": e2e, "kernel_ms": {k: v[0] for k, v in fam.items() if v[1]},
         "table": info, "best": {"eta": gbest[0], "cand": int(gbest[1]), "lin": int(gbest[2])},
+        "refined_voxels": refine_count,
         "inst": inst, "dims": dims,
     }
     return out
@@ -470,7 +472,8 @@ def main():
                        "l2": "inputs larger than L2 (512 MiB residual, 0.9 GiB padded copy)"},
             "gpu_launches": res["launches"], "clocks": res["clocks"], "roofline": res["roofline"],
             "cpu_baseline": cpu, "e2e": res["e2e"], "kernel_ms_per_step": res["kernel_ms"],
-            "table": res["table"], "argmax": res["best"], "secondary": secondary,
+            "table": res["table"], "argmax": res["best"], "refined_voxels": res["refined_voxels"],
+            "secondary": secondary,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -171,16 +171,24 @@ int sfw3d_basis_set_fit(const int32_t dims[3], int n_sigma, const double* sigma_
                         int n_shape, const double* shape_host, int dtype, double tol,
                         int max_terms, int* n_terms, double* betas, double* weights, double* w0,
                         double* fit_err, int32_t* member);
-/* One candidate (flat sigma-major index): evaluator used for `dtype`
- * (uses_basis: 0 direct, 1 shared separable basis, 2 basis with exact
- * refinement of its maxima — fp64 storage, inexact fit), the
- * table's SHARED basis term count, the candidate's shared-basis fit error
- * (max abs on the common box lattice, +inf when not fitted), its direct tap
- * count, the shared basis taps per voxel, and its executed flops per voxel. */
+/* One candidate (flat sigma-major index): evaluator used for `dtype` by an
+ * argmax-only evaluation (uses_basis: 0 direct, 1 shared separable basis,
+ * 2 basis with exact refinement of its maxima — fp64 non-negative members
+ * with an inexact fit, and the SIGNED members: candidates outside the
+ * non-negative pool, e.g. d > 2, fitted with signed weights; calls that keep
+ * the eta fields evaluate signed members directly), the table's SHARED basis
+ * term count, the candidate's shared-basis fit error (max abs on the common
+ * box lattice; for signed members the certified bound factor E, with
+ * |eta~ - eta| <= E ||b||_inf / lam at every voxel; +inf when not fitted),
+ * its direct tap count, the shared basis taps per voxel, and its executed
+ * flops per voxel. */
 int sfw3d_table_candidate(const sfw3d_table* t, int dtype, int cand, int* uses_basis,
                           int* n_terms, double* fit_err, int64_t* direct_taps,
                           int64_t* basis_taps, double* flops);
 int sfw3d_table_destroy(sfw3d_table* t);
+/* Diagnostics: voxels the calling thread's last sfw3d_eta_argmax re-evaluated
+ * exactly (refined basis members; > 65536 means it fell back to direct). */
+int sfw3d_last_refine_count(void);
 
 /* K1 — eta_field (certificate.py:140-184): eta_c(m) = <H*G_c(.-m), r>/lam
  * for every integer m and candidate c, with the discrete argmax over the

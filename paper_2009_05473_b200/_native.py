@@ -32,6 +32,7 @@ EXPORTS = (
     "sfw3d_table_destroy", "sfw3d_eta_argmax", "sfw3d_dots", "sfw3d_nnlasso_cd",
     "sfw3d_residual", "sfw3d_ctx_profile", "sfw3d_ctx_profile_read", "sfw3d_probe_fp32",
     "sfw3d_table_candidate", "sfw3d_basis_fit", "sfw3d_basis_set_fit",
+    "sfw3d_last_refine_count",
 )
 
 
@@ -47,6 +48,7 @@ _dp = C.POINTER(C.c_double)
 _SIGNATURES = {
     "sfw3d_abi_version": (C.c_int, []),
     "sfw3d_last_error": (C.c_char_p, []),
+    "sfw3d_last_refine_count": (C.c_int, []),
     "sfw3d_ctx_create": (C.c_int, [C.c_int, _vp, C.POINTER(_vp)]),
     "sfw3d_ctx_destroy": (C.c_int, [_vp]),
     "sfw3d_ctx_sync": (C.c_int, [_vp]),
@@ -182,7 +184,7 @@ def basis_set_fit(dims, sigmas, shapes, dtype: int, tol: float, max_terms: int =
         raise ValueError(f"shared basis has {nt.value} terms > max_terms={max_terms}")
     k = nt.value
     return {"betas": betas[:k], "weights": weights[:, :k], "w0": w0, "fit_err": err,
-            "member": member.astype(bool)}
+            "member": member.astype(bool), "signed": member == 2}
 
 
 # ------------------------------------------------------------------ devices
@@ -261,6 +263,11 @@ def context(device=None) -> Context:
         ctx = Context(dev, stream)
         _contexts[key] = ctx
     return ctx
+
+
+def last_refine_count() -> int:
+    """Voxels this thread's last certificate evaluation re-evaluated exactly."""
+    return int(lib().sfw3d_last_refine_count())
 
 
 def total_launches() -> int:

@@ -21,6 +21,8 @@
 // which adds at most 1e-12 to every member's recorded error.
 #include <algorithm>
 #include <atomic>
+#include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <thread>
 
@@ -273,7 +275,9 @@ struct BasisSet {
   std::vector<int> members;         // candidate ids on the basis path
   std::vector<double> W, w0;        // [member][term], [member]
   std::vector<double> fit_err;      // per candidate (inf when not fitted)
-  std::vector<char> is_member;      // per candidate
+  std::vector<char> is_member;      // per candidate: 1 non-negative fit, 2 signed
+  int n_nnls = 0;                   // members [0, n_nnls) non-negative, then signed
+  std::vector<double> ebound;       // per candidate: signed members' bound factor
   void* W_dev = nullptr;            // storage dtype, [member][term]
   void* w0_dev = nullptr;
   int* cid_dev = nullptr;           // member -> candidate id
@@ -287,6 +291,201 @@ constexpr int kDictCoarse = 49;
 constexpr int kTangents = 10;
 // no fit is accepted below this bound (double-precision evaluation floor)
 constexpr double kFitFloor = 1e-11;
+
+// ------------------------------------------------------------ signed members
+// A candidate outside the non-negative pool (d > 2: g_c is not completely
+// monotone) is fitted on the SHARED terms by weighted-ridge least squares with
+// signed weights. Its basis value eta~ then differs from the direct value at
+// EVERY voxel m by at most
+//   lam |eta~(m) - eta(m)| <= ||b||_inf (D1 + R),
+//   D1 = sum_{v in C} |G~(v) - G_dir(v)| + tap_tol |B_c|
+//        (the exact mixture with the stored factors and weights against the
+//        candidate's direct template g_c(|v|^2) on its box B_c, over the
+//        common box C that the passes cover),
+//   R  = sum_k |W_k| S_k (rho_k + g_mix (1 + rho_k)) + |w0| g_mix
+//        (floating-point rounding: a pass of L taps is an L-term FMA chain,
+//        rho_k = 1.01 u (Lx + Ly + Lz) for the three passes of term k, S_k the
+//        factor mass over C, g_mix = 1.01 u (K + 2) for the (K + 1)-term mix).
+// The ridge weight trades D1 against R (large signed weights amplify the
+// rounding) and is picked to minimise D1 + R. eta.cu collects every voxel
+// within 2 E of the approximate maximum and re-evaluates it directly.
+namespace {
+
+constexpr int kRidgeMin = -34, kRidgeMax = -6;  // ridge weights 10^e (and 0)
+
+double env_double(const char* name, double def) {
+  const char* e = getenv(name);
+  return e ? atof(e) : def;
+}
+
+void fit_signed_members(BasisSet* s, const std::vector<BasisCandidate>& cands, int dtype,
+                        const std::vector<double>& Sfit,
+                        const std::vector<std::vector<double>>& hstore) {
+  if (env_double("SFW3D_SIGNED", 1.0) == 0.0) return;
+  const int nc = int(cands.size()), nt = int(s->betas.size());
+  const double u = dtype == SFW3D_F64 ? 0x1p-53 : 0x1p-24;
+  const double accept = env_double("SFW3D_SIGNED_ACCEPT", 0.01);
+  const bool debug = env_double("SFW3D_SIGNED_DEBUG", 0.0) != 0.0;
+  // per term: factor mass over C and the three passes' rounding factor
+  std::vector<double> Sk(nt), rho(nt);
+  std::vector<size_t> aoff[3];
+  for (int a = 0; a < 3; ++a) aoff[a].resize(nt);
+  for (int t = 0; t < nt; ++t) {
+    double prod = 1.0;
+    int L = 0;
+    size_t off = 0;
+    for (int a = 0; a < 3; ++a) {
+      aoff[a][t] = off;
+      double sa = 0.0;
+      for (int q = 0; q < s->tlen[a][t]; ++q) sa += std::fabs(hstore[t][off + q]);
+      off += s->tlen[a][t];
+      prod *= sa;
+      L += s->tlen[a][t];
+    }
+    Sk[t] = prod;
+    rho[t] = 1.01 * u * L;
+  }
+  const double gmix = 1.01 * u * (nt + 2);
+  // axis representatives: offsets +t and -t share one (multiplicity 2) when
+  // both lie in C and every factor is defined at both
+  struct Rep {
+    int t;
+    double w;
+  };
+  std::vector<Rep> reps[3];
+  std::vector<std::vector<double>> fval[3];  // [a][rep][term]
+  for (int a = 0; a < 3; ++a) {
+    const int lo = s->lo[a], hi = s->hi[a];
+    auto in_term = [&](int t, int k) { return t >= s->tlo[a][k] && t < s->tlo[a][k] + s->tlen[a][k]; };
+    for (int t = 0; t <= std::max(-lo, hi); ++t) {
+      const bool pos = t >= lo && t <= hi, neg = t > 0 && -t >= lo && -t <= hi;
+      bool same = pos && neg;
+      for (int k = 0; same && k < nt; ++k) same = in_term(t, k) == in_term(-t, k);
+      if (same) {
+        reps[a].push_back({t, 2.0});
+      } else {
+        if (pos) reps[a].push_back({t, 1.0});
+        if (neg) reps[a].push_back({-t, 1.0});
+      }
+    }
+    for (const Rep& r : reps[a]) {
+      std::vector<double> f(nt, 0.0);
+      for (int k = 0; k < nt; ++k)
+        if (in_term(r.t, k)) f[k] = hstore[k][aoff[a][k] + (r.t - s->tlo[a][k])];
+      fval[a].push_back(std::move(f));
+    }
+  }
+  std::vector<int> todo;
+  for (int c = 0; c < nc; ++c) {
+    if (s->is_member[c]) continue;
+    bool ok = true;
+    for (int a = 0; a < 3; ++a)
+      ok &= cands[c].lo[a] == -cands[c].hi[a] && cands[c].lo[a] >= s->lo[a] &&
+            cands[c].hi[a] <= s->hi[a];
+    if (ok) todo.push_back(c);
+  }
+  if (todo.empty()) return;
+  const int M = int(Sfit.size()), ncol = nt + 1, Mt = M + ncol;
+  std::vector<std::vector<double>> wsig(nc);
+  std::vector<double> w0sig(nc, 0.0), esig(nc, INFINITY), dsig(nc, INFINITY), mass(nc, 0.0);
+  auto fit_one = [&](int c) {
+    const BasisCandidate& bc = cands[c];
+    std::vector<ld> A(size_t(Mt) * ncol, 0.0L), g(Mt, 0.0L);
+    for (int i = 0; i < M; ++i) {
+      g[i] = profile(Sfit[i], bc.sigma, bc.d);
+      for (int k = 0; k < nt; ++k) A[size_t(k) * Mt + i] = std::exp(-(ld)s->betas[k] * Sfit[i]);
+      A[size_t(nt) * Mt + i] = Sfit[i] == 0.0 ? 1.0L : 0.0L;
+    }
+    std::vector<double> pen(ncol);
+    for (int k = 0; k < nt; ++k) pen[k] = Sk[k] * (rho[k] + gmix * (1.0 + rho[k]));
+    pen[nt] = gmix;
+    std::vector<int> cols(ncol);
+    for (int k = 0; k < ncol; ++k) cols[k] = k;
+    // the direct template on its box, per representative triple
+    double m = 0.0;
+    for (int x = bc.lo[0]; x <= bc.hi[0]; ++x)
+      for (int y = bc.lo[1]; y <= bc.hi[1]; ++y)
+        for (int z = bc.lo[2]; z <= bc.hi[2]; ++z)
+          m += profile(double(x) * x + double(y) * y + double(z) * z, bc.sigma, bc.d);
+    mass[c] = m;
+    const double box_taps = double(bc.hi[0] - bc.lo[0] + 1) * (bc.hi[1] - bc.lo[1] + 1) *
+                            (bc.hi[2] - bc.lo[2] + 1);
+    std::vector<double> P(nt);
+    for (int e = kRidgeMin - 1; e <= kRidgeMax; ++e) {
+      const ld mu = e < kRidgeMin ? 0.0L : std::pow(10.0L, (ld)e);
+      for (int k = 0; k < ncol; ++k) A[size_t(k) * Mt + M + k] = std::sqrt(mu) * (ld)pen[k];
+      std::vector<ld> z;
+      lsq_qr(A, Mt, cols, g, z);
+      std::vector<double> w(nt);
+      bool finite = true;
+      for (int k = 0; k < nt; ++k) {
+        w[k] = dtype == SFW3D_F64 ? double(z[k]) : double(float(z[k]));
+        finite &= std::isfinite(w[k]);
+      }
+      double w0 = dtype == SFW3D_F64 ? double(z[nt]) : double(float(z[nt]));
+      if (!finite || !std::isfinite(w0)) continue;
+      double R = std::fabs(w0) * gmix;
+      for (int k = 0; k < nt; ++k) R += std::fabs(w[k]) * pen[k];
+      if (R >= esig[c]) continue;
+      double D1 = bc.tap_tol * box_taps;
+      for (size_t ix = 0; ix < reps[0].size(); ++ix) {
+        const Rep rx = reps[0][ix];
+        for (size_t iy = 0; iy < reps[1].size(); ++iy) {
+          const Rep ry = reps[1][iy];
+          for (int k = 0; k < nt; ++k) P[k] = w[k] * fval[0][ix][k] * fval[1][iy][k];
+          const bool in_xy = std::abs(rx.t) <= bc.hi[0] && std::abs(ry.t) <= bc.hi[1];
+          const double sxy = double(rx.t) * rx.t + double(ry.t) * ry.t;
+          double acc = 0.0;
+          for (size_t iz = 0; iz < reps[2].size(); ++iz) {
+            const Rep rz = reps[2][iz];
+            const std::vector<double>& fz = fval[2][iz];
+            double gv = (rx.t == 0 && ry.t == 0 && rz.t == 0) ? w0 : 0.0;
+            for (int k = 0; k < nt; ++k) gv += P[k] * fz[k];
+            const double gd = in_xy && std::abs(rz.t) <= bc.hi[2]
+                                  ? profile(sxy + double(rz.t) * rz.t, bc.sigma, bc.d)
+                                  : 0.0;
+            acc += rz.w * std::fabs(gv - gd);
+          }
+          D1 += rx.w * ry.w * acc;
+        }
+        if (D1 + R >= esig[c]) break;
+      }
+      if (D1 + R < esig[c]) {
+        esig[c] = D1 + R;
+        dsig[c] = D1;
+        wsig[c] = w;
+        w0sig[c] = w0;
+      }
+    }
+  };
+  {
+    const int nthreads =
+        std::max(1, std::min<int>(int(todo.size()), int(std::thread::hardware_concurrency())));
+    std::atomic<int> next{0};
+    std::vector<std::thread> workers;
+    for (int w = 0; w < nthreads; ++w)
+      workers.emplace_back([&] {
+        for (int q = next++; q < int(todo.size()); q = next++) fit_one(todo[q]);
+      });
+    for (auto& th : workers) th.join();
+  }
+  for (int c : todo) {
+    const bool ok = std::isfinite(esig[c]) && esig[c] <= accept * mass[c];
+    if (debug)
+      fprintf(stderr, "[signed] cand %d sigma %.3f d %.3f: D1 %.3e R %.3e E/mass %.3e -> %s\n", c,
+              cands[c].sigma, cands[c].d, dsig[c], esig[c] - dsig[c], esig[c] / mass[c],
+              ok ? "member" : "direct");
+    if (!ok) continue;
+    s->is_member[c] = 2;
+    s->ebound[c] = esig[c];
+    s->fit_err[c] = esig[c];  // (signed members report their bound factor)
+    s->members.push_back(c);
+    s->W.insert(s->W.end(), wsig[c].begin(), wsig[c].end());
+    s->w0.push_back(w0sig[c]);
+  }
+}
+
+}  // namespace
 
 int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands, int dtype,
                     double tol, BasisSet** out, bool on_device, bool prune) {
@@ -491,16 +690,21 @@ int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands,
     s->tlo[a].resize(nt);
     s->tlen[a].resize(nt);
   }
+  // stored factor values (rounded to the storage precision) per term, axes
+  // 0, 1, 2 contiguous: what the passes multiply by
+  std::vector<std::vector<double>> hstore(nt);
   for (int t = 0; t < nt; ++t) {
     const double beta = dict[kmap[t]];
     s->betas.push_back(beta);
     const int r = int(std::ceil(std::sqrt(std::log(1.0 / eps) / beta)));
-    std::vector<double> h;
+    std::vector<double>& h = hstore[t];
     for (int a = 0; a < 3; ++a) {
       s->tlo[a][t] = std::max(s->lo[a], -r);
       s->tlen[a][t] = std::min(s->hi[a], r) - s->tlo[a][t] + 1;
-      for (int q = s->tlo[a][t]; q < s->tlo[a][t] + s->tlen[a][t]; ++q)
-        h.push_back(std::exp(-beta * double(q) * q));
+      for (int q = s->tlo[a][t]; q < s->tlo[a][t] + s->tlen[a][t]; ++q) {
+        const double v = std::exp(-beta * double(q) * q);
+        h.push_back(dtype == SFW3D_F64 ? v : double(float(v)));
+      }
       s->taps_per_voxel += s->tlen[a][t];
     }
     if (!on_device) continue;
@@ -522,9 +726,15 @@ int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands,
     for (int t = 0; t < nt; ++t) s->W[size_t(m) * nt + t] = wfit[c][kmap[t]];
     s->w0[m] = w0fit[c];
   }
-  if (nm && on_device) {
+  s->n_nnls = nm;
+  s->ebound.assign(nc, 0.0);
+  if (nt > 0) fit_signed_members(s, cands, dtype, Sfit, hstore);
+  const int nmt = int(s->members.size());
+  if (nmt && on_device) {
     if (dtype == SFW3D_F64) {
-      SFW3D_TRY(upload(&s->W_dev, s->W.data(), s->W.size() * sizeof(double) + 8));
+      std::vector<double> Wd(s->W);
+      Wd.push_back(0.0);
+      SFW3D_TRY(upload(&s->W_dev, Wd.data(), Wd.size() * sizeof(double)));
       SFW3D_TRY(upload(&s->w0_dev, s->w0.data(), s->w0.size() * sizeof(double)));
     } else {
       std::vector<float> Wf(s->W.begin(), s->W.end()), w0f(s->w0.begin(), s->w0.end());
@@ -574,6 +784,12 @@ bool basis_set_member(const BasisSet* s, int cand, double* fit_err) {
   if (!s || cand < 0 || cand >= int(s->is_member.size())) return false;
   if (fit_err) *fit_err = s->fit_err[cand];
   return s->is_member[cand] != 0;
+}
+bool basis_set_signed(const BasisSet* s, int cand) {
+  return s && cand >= 0 && cand < int(s->is_member.size()) && s->is_member[cand] == 2;
+}
+double basis_set_ebound(const BasisSet* s, int cand) {
+  return basis_set_signed(s, cand) ? s->ebound[cand] : 0.0;
 }
 int basis_set_n_terms(const BasisSet* s) { return s ? int(s->betas.size()) : 0; }
 int basis_set_n_members(const BasisSet* s) { return s ? int(s->members.size()) : 0; }
@@ -853,7 +1069,7 @@ static int launch_mix(sfw3d_ctx* ctx, int nblocks, const void* b, const void* te
 
 int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[3], const void* b,
                    double lam, const int32_t win[6], void* fields, Best* best_dev, void* scratch) {
-  const int nm = int(s->members.size()), nt = int(s->betas.size());
+  const int nm = fields ? s->n_nnls : int(s->members.size()), nt = int(s->betas.size());
   if (nm == 0) return SFW3D_OK;
   const long long n = vol_count(dims);
   if (n >= (1LL << 31)) {  // (n_terms volumes of that size exceed any HBM anyway)

@@ -24,6 +24,7 @@ struct BasisCandidate {
   double sigma, d;
   int lo[3], hi[3];   // the candidate's reference support box (offsets)
   long long direct_taps;
+  double tap_tol = 0.0;  // direct taps below this are dropped (eta.cu build_candidate)
 };
 
 struct BasisSet;
@@ -49,6 +50,14 @@ inline bool basis_prune_rule(const int dims[3]) {
 }
 // candidate -> (is member, fit error of its shared-dictionary fit)
 bool basis_set_member(const BasisSet* s, int cand, double* fit_err);
+// Signed members: candidates outside the non-negative pool (d > 2, or d <= 2
+// fits missing tol) fitted by weighted-ridge least squares on the SHARED terms.
+// Their eta is only certified to within ebound * ||b||_inf / lam at every
+// voxel (fit + rounding, see basis.cu), so they are used for argmax-only
+// evaluations and always refined exactly (eta.cu); never for fields.
+bool basis_set_signed(const BasisSet* s, int cand);
+// per-candidate bound factor E (0 for non-signed): |eta~ - eta| <= E ||b||_inf / lam
+double basis_set_ebound(const BasisSet* s, int cand);
 int basis_set_n_terms(const BasisSet* s);
 int basis_set_n_members(const BasisSet* s);
 long long basis_set_taps(const BasisSet* s);        // per voxel, all shared terms
@@ -58,7 +67,8 @@ double basis_set_member_flops(const BasisSet* s);   // mix flops per voxel per m
 // Scratch (bytes) basis_set_eval needs for a volume of n elements.
 size_t basis_set_scratch(const BasisSet* s, long long n, int dtype);
 // eta for all members: best_dev[cand] receives each member's windowed
-// argmax; fields (n_cand volumes, candidate-major) are written when non-NULL.
+// argmax; fields (n_cand volumes, candidate-major) are written when non-NULL
+// (then the signed members are skipped: their values are not certified).
 int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[3], const void* b,
                    double lam, const int32_t win[6], void* fields, Best* best_dev, void* scratch);
 

@@ -430,27 +430,44 @@ struct RefCand {
   int lo_a, lo_b, cl, la, lb, lc4;
 };
 
-// sum |b| over the volume (fp64), one atomicAdd per block
+// sum |b| (fp64, one atomicAdd per block) and max |b| (bit pattern of a
+// non-negative double: integer order = value order) over the volume
 template <typename T>
-__global__ void abs_sum_kernel(const T* __restrict__ b, long long n, double* __restrict__ out) {
+__global__ void abs_sum_kernel(const T* __restrict__ b, long long n, double* __restrict__ out,
+                               unsigned long long* __restrict__ amax) {
   __shared__ double red[8];
-  double sacc = 0.0;
-  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256)
-    sacc += fabs(double(b[i]));
+  __shared__ double redm[8];
+  double sacc = 0.0, m = 0.0;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+    const double v = fabs(double(b[i]));
+    sacc += v;
+    m = fmax(m, v);
+  }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sacc;
+  for (int o = 16; o > 0; o >>= 1) {
+    sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = sacc;
+    redm[threadIdx.x >> 5] = m;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < 8; ++w) t += red[w];
+    double t = 0.0, mm = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      t += red[w];
+      mm = fmax(mm, redm[w]);
+    }
     atomicAdd(out, t);
+    atomicMax(amax, static_cast<unsigned long long>(__double_as_longlong(mm)));
   }
 }
 
 // one CTA per item: eta = sum_v G_c(v) b(m + v) / lam over the candidate's
 // box (periodic indexing), warps over template rows, lanes over taps
-__global__ void __launch_bounds__(256) refine_kernel(const double* __restrict__ b, int nx, int ny,
+template <typename T>
+__global__ void __launch_bounds__(256) refine_kernel(const T* __restrict__ b, int nx, int ny,
                                                      int nz, const RefCand* __restrict__ rc,
                                                      const int* __restrict__ item_cand,
                                                      const long long* __restrict__ item_idx,
@@ -469,12 +486,12 @@ __global__ void __launch_bounds__(256) refine_kernel(const double* __restrict__ 
     if (xa < 0) xa += nx;
     int yb = (y + c.lo_b + bi) % ny;
     if (yb < 0) yb += ny;
-    const double* brow = b + ((long long)xa * ny + yb) * nz;
+    const T* brow = b + ((long long)xa * ny + yb) * nz;
     const double* trow = c.taps + (long long)r * c.lc4;
     for (int col = 4 * rr.x + lane; col < 4 * (rr.x + rr.y); col += 32) {
       int zc = (z + c.cl + col) % nz;
       if (zc < 0) zc += nz;
-      acc = fma(trow[col], brow[zc], acc);
+      acc = fma(trow[col], double(brow[zc]), acc);
     }
   }
 #pragma unroll
@@ -614,15 +631,21 @@ static int ensure_basis(const sfw3d_table* t, int dtype) {
   return SFW3D_OK;
 }
 
-// evaluator choice per candidate and storage type
-static bool use_basis(const sfw3d_table* t, int ci, int dtype) {
-  return t->mode == 0 && basis_set_member(t->set(dtype), ci, nullptr);
+// evaluator choice per candidate and storage type (fields: the call keeps
+// every eta volume, which signed members cannot certify)
+static bool use_basis(const sfw3d_table* t, int ci, int dtype, bool fields = false) {
+  return t->mode == 0 && basis_set_member(t->set(dtype), ci, nullptr) &&
+         !(fields && basis_set_signed(t->set(dtype), ci));
 }
 
-// fp64 storage: basis members whose fit is not exact get an exact refinement
-static bool use_refine(const sfw3d_table* t, int ci, int dtype) {
+// exact refinement of the maxima: signed members always; in fp64 storage
+// also the non-negative members whose fit is not exact
+static bool use_refine(const sfw3d_table* t, int ci, int dtype, bool fields = false) {
+  if (t->mode != 0) return false;
+  const BasisSet* s = t->set(dtype);
+  if (basis_set_signed(s, ci)) return !fields;
   double fe = 0.0;
-  return dtype == SFW3D_F64 && t->mode == 0 && basis_set_member(t->set(dtype), ci, &fe) && fe > 0.0;
+  return dtype == SFW3D_F64 && basis_set_member(s, ci, &fe) && fe > 0.0;
 }
 
 // folded kernel tile: outputs per thread along z (fp32 32, fp64 16) and
@@ -810,7 +833,7 @@ extern "C" int sfw3d_table_create(sfw3d_ctx* ctx, const sfw3d_psf* psf, int n_si
   t->pdims[2] = round_up(t->pad[2] + round_up(t->dims[2], kFoldTZMax) + 4 + maxpitch, 4);
   for (const auto& c : t->cands)
     t->bcands.push_back(
-        {c.sigma, c.d, {c.lo[0], c.lo[1], c.lo[2]}, {c.hi[0], c.hi[1], c.hi[2]}, c.taps});
+        {c.sigma, c.d, {c.lo[0], c.lo[1], c.lo[2]}, {c.hi[0], c.hi[1], c.hi[2]}, c.taps, tap_tol});
   {
     std::vector<RefCand> rc;
     for (const auto& c : t->cands) rc.push_back({c.t64, c.rows_dev, c.lo[0], c.lo[1], c.cl, c.la, c.lb, c.lc4});
@@ -875,6 +898,12 @@ extern "C" int sfw3d_table_candidate(const sfw3d_table* t, int dtype, int cand, 
 
 namespace {
 
+// voxels the last exact refinement re-evaluated (diagnostics)
+int& last_refine_count() {
+  static thread_local int c = 0;
+  return c;
+}
+
 template <typename T>
 int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double lam,
               const int32_t win[6], sfw3d_argmax* best_host, sfw3d_argmax* per_cand_host,
@@ -885,14 +914,15 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   const size_t vb = size_t(n) * sizeof(T);
   const int nc = int(t->cands.size());
   bool any_direct = false, any_basis = false, any_refine = false;
+  const bool fl = fields != nullptr;
   for (int ci = 0; ci < nc; ++ci) {
-    (use_basis(t, ci, dtype) ? any_basis : any_direct) = true;
-    any_refine |= use_refine(t, ci, dtype);
+    (use_basis(t, ci, dtype, fl) ? any_basis : any_direct) = true;
+    any_refine |= use_refine(t, ci, dtype, fl);
   }
   // direct evaluation per candidate (refined members fall back to it when
   // their candidate list overflows)
   std::vector<char> direct(nc, 0);
-  for (int ci = 0; ci < nc; ++ci) direct[ci] = !use_basis(t, ci, dtype);
+  for (int ci = 0; ci < nc; ++ci) direct[ci] = !use_basis(t, ci, dtype, fl);
   const BasisSet* bset = t->set(dtype);
   const size_t sb = any_basis ? basis_set_scratch(bset, n, dtype) : 0;
   const size_t pb = (any_direct || any_refine)
@@ -911,7 +941,7 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   const int nxp = ow[1] - ow[0] + 1;
   const long long nblocks_direct = (long long)nty * ntz * nxp;
   const long long nblocks = nblocks_direct;
-  const size_t rb = any_refine ? size_t(kRefCap) * (4 + 8 + 8) + size_t(nc) * 8 + 64 : 0;
+  const size_t rb = any_refine ? size_t(kRefCap) * (4 + 8 + 8) + size_t(nc) * 8 + 96 : 0;
   // folded kernel slice sums in global memory (tuning variant)
   size_t ab = 0;
   if (fold_accd_global(sizeof(T))) {
@@ -934,7 +964,7 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   long long* ref_idx = any_refine ? cv.take<long long>(kRefCap) : nullptr;
   double* ref_val = any_refine ? cv.take<double>(kRefCap) : nullptr;
   double* ref_thr = any_refine ? cv.take<double>(nc) : nullptr;
-  double* ref_l1 = any_refine ? cv.take<double>(1) : nullptr;
+  double* ref_l1 = any_refine ? cv.take<double>(2) : nullptr;  // [sum |b|, max |b| bits]
   int* ref_count = any_refine ? cv.take<int>(1) : nullptr;
   std::vector<Best> refined(nc, Best{NAN, -1});  // exact maxima of refined members
   void* accd_g = ab ? cv.take<char>(ab) : nullptr;
@@ -968,55 +998,66 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   // writing cbest[cand] (and the member fields) directly
   if (any_basis)
     SFW3D_TRY(basis_set_eval(ctx, bset, dtype, dims, b, lam, win, fields, cbest, bscratch));
-  if constexpr (sizeof(T) == 8) {
-    if (any_refine) {
-      // E_c = (e_c + 2e-12) ||b||_1 / lam bounds |eta~_c - eta_c| at every voxel:
-      // the true maximum lies among the voxels with eta~ >= max eta~ - 2 E_c
-      SFW3D_PROF(ctx, "eta_refine");
-      SFW3D_CUDA_TRY(cudaMemsetAsync(ref_l1, 0, sizeof(double), ctx->stream));
-      abs_sum_kernel<T><<<4 * ctx->num_sms, 256, 0, ctx->stream>>>(b, n, ref_l1);
-      SFW3D_LAUNCH_CHECK(ctx);
-      std::vector<Best> hb0(nc);
-      double l1 = 0.0;
-      SFW3D_TRY(download_sync(ctx, hb0.data(), cbest, size_t(nc) * sizeof(Best)));
-      SFW3D_TRY(download_sync(ctx, &l1, ref_l1, sizeof(double)));
-      const int nm = basis_set_n_members(bset);
-      std::vector<double> thr(nm, INFINITY);
-      for (int m = 0; m < nm; ++m) {
-        const int ci = basis_set_member_cand(bset, m);
+  if (any_refine) {
+    // Every refined member's approximate eta~ is within E_c of its direct
+    // value at every voxel: signed members E_c = ebound_c ||b||_inf / lam
+    // (basis.cu), fp64 non-negative members E_c = (e_c + 2e-12) ||b||_1 / lam.
+    // The true maximum lies among the voxels with eta~ >= max eta~ - 2 E_c.
+    SFW3D_PROF(ctx, "eta_refine");
+    SFW3D_CUDA_TRY(cudaMemsetAsync(ref_l1, 0, 2 * sizeof(double), ctx->stream));
+    abs_sum_kernel<T><<<4 * ctx->num_sms, 256, 0, ctx->stream>>>(
+        b, n, ref_l1, reinterpret_cast<unsigned long long*>(ref_l1 + 1));
+    SFW3D_LAUNCH_CHECK(ctx);
+    std::vector<Best> hb0(nc);
+    double l1[2] = {0.0, 0.0};
+    SFW3D_TRY(download_sync(ctx, hb0.data(), cbest, size_t(nc) * sizeof(Best)));
+    SFW3D_TRY(download_sync(ctx, l1, ref_l1, 2 * sizeof(double)));
+    const int nm = basis_set_n_members(bset);
+    std::vector<double> thr(nm, INFINITY);
+    for (int m = 0; m < nm; ++m) {
+      const int ci = basis_set_member_cand(bset, m);
+      if (!use_refine(t, ci, dtype, fl) || !std::isfinite(hb0[ci].v)) continue;
+      double E;
+      if (basis_set_signed(bset, ci)) {
+        E = basis_set_ebound(bset, ci) * l1[1] / lam * (1.0 + 1e-6);
+      } else {
         double fe = 0.0;
         basis_set_member(bset, ci, &fe);
-        if (!use_refine(t, ci, dtype) || !std::isfinite(hb0[ci].v)) continue;
-        const double E = (fe + 2e-12) * l1 / lam;
-        thr[m] = hb0[ci].v - 2.0 * E - 1e-12 * std::fabs(hb0[ci].v);
+        E = (fe + 2e-12) * l1[0] / lam;
       }
-      SFW3D_TRY(stage_upload(ctx, ref_thr, thr.data(), size_t(nm) * sizeof(double)));
-      SFW3D_TRY(basis_set_collect(ctx, bset, dtype, dims, b, lam, win, ref_thr, kRefCap, ref_cand,
-                                  ref_idx, ref_count, bscratch));
-      int count = 0;
-      SFW3D_TRY(download_sync(ctx, &count, ref_count, sizeof(int)));
-      if (count > kRefCap) {  // too many near-maximal voxels: exact direct evaluation
-        for (int ci = 0; ci < nc; ++ci)
-          if (use_refine(t, ci, dtype)) direct[ci] = 1;
-      } else if (count > 0) {
-        SFW3D_PROF(ctx, "eta_refine");
-        refine_kernel<<<count, 256, 0, ctx->stream>>>(
-            reinterpret_cast<const double*>(b), dims[0], dims[1], dims[2],
-            static_cast<const RefCand*>(t->refcand_dev), ref_cand, ref_idx, lam, ref_val);
-        SFW3D_LAUNCH_CHECK(ctx);
-        std::vector<int> hc(count);
-        std::vector<long long> hi(count);
-        std::vector<double> hv(count);
-        SFW3D_TRY(download_sync(ctx, hc.data(), ref_cand, size_t(count) * sizeof(int)));
-        SFW3D_TRY(download_sync(ctx, hi.data(), ref_idx, size_t(count) * sizeof(long long)));
-        SFW3D_TRY(download_sync(ctx, hv.data(), ref_val, size_t(count) * sizeof(double)));
-        for (int i = 0; i < count; ++i) {
-          Best& r = refined[hc[i]];
-          // larger value wins, ties to the smaller C-order index
-          if (std::isnan(r.v) || hv[i] > r.v || (hv[i] == r.v && hi[i] < r.idx)) r = {hv[i], hi[i]};
-        }
+      thr[m] = hb0[ci].v - 2.0 * E - 1e-12 * std::fabs(hb0[ci].v);
+    }
+    SFW3D_TRY(stage_upload(ctx, ref_thr, thr.data(), size_t(nm) * sizeof(double)));
+    SFW3D_TRY(basis_set_collect(ctx, bset, dtype, dims, b, lam, win, ref_thr, kRefCap, ref_cand,
+                                ref_idx, ref_count, bscratch));
+    int count = 0;
+    SFW3D_TRY(download_sync(ctx, &count, ref_count, sizeof(int)));
+    last_refine_count() = count;
+    if (count > kRefCap) {  // too many near-maximal voxels: exact direct evaluation
+      for (int ci = 0; ci < nc; ++ci)
+        if (use_refine(t, ci, dtype, fl)) direct[ci] = 1;
+    } else if (count > 0) {
+      SFW3D_PROF(ctx, "eta_refine");
+      refine_kernel<T><<<count, 256, 0, ctx->stream>>>(
+          b, dims[0], dims[1], dims[2], static_cast<const RefCand*>(t->refcand_dev), ref_cand,
+          ref_idx, lam, ref_val);
+      SFW3D_LAUNCH_CHECK(ctx);
+      std::vector<int> hc(count);
+      std::vector<long long> hi(count);
+      std::vector<double> hv(count);
+      SFW3D_TRY(download_sync(ctx, hc.data(), ref_cand, size_t(count) * sizeof(int)));
+      SFW3D_TRY(download_sync(ctx, hi.data(), ref_idx, size_t(count) * sizeof(long long)));
+      SFW3D_TRY(download_sync(ctx, hv.data(), ref_val, size_t(count) * sizeof(double)));
+      for (int i = 0; i < count; ++i) {
+        Best& r = refined[hc[i]];
+        // larger value wins, ties to the smaller C-order index
+        if (std::isnan(r.v) || hv[i] > r.v || (hv[i] == r.v && hi[i] < r.idx)) r = {hv[i], hi[i]};
       }
     }
+    // (a refined member always collects its own approximate maximum; if not,
+    // evaluate it directly rather than report an uncertified value)
+    for (int ci = 0; ci < nc; ++ci)
+      if (use_refine(t, ci, dtype, fl) && !direct[ci] && std::isnan(refined[ci].v)) direct[ci] = 1;
   }
   for (int ci = 0; ci < nc; ++ci) {
     if (!direct[ci]) continue;
@@ -1117,6 +1158,8 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
 }
 
 }  // namespace
+
+extern "C" int sfw3d_last_refine_count(void) { return last_refine_count(); }
 
 extern "C" int sfw3d_eta_argmax(sfw3d_ctx* ctx, const sfw3d_table* t, int dtype,
                                 const void* residual_dev, double lam, const int32_t window[6],

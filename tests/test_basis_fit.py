@@ -79,7 +79,8 @@ def test_shared_basis_set(name, dims, sigmas, shapes):
     member's mixture reproduces its profile on the COMMON box lattice within
     the reported error (which includes the 1e-12 factor truncation), members
     are exactly the candidates with fit_err <= tol, d = 2 candidates are one
-    exact term of weight 1 and d > 2 candidates are never members."""
+    exact term of weight 1 and d > 2 candidates are never non-negative
+    members (they join as signed members, test_signed_members)."""
     tol = 1e-9
     r = N.basis_set_fit(dims, sigmas, shapes, 0, tol)
     lo, hi = common_box(dims, sigmas, shapes)
@@ -88,6 +89,8 @@ def test_shared_basis_set(name, dims, sigmas, shapes):
     assert len(r["betas"]) <= 64 and np.all(np.diff(r["betas"]) > 0)
     for c, (sg, d) in enumerate([(a, b) for a in sigmas for b in shapes]):
         err, member, w = r["fit_err"][c], r["member"][c], r["weights"][c]
+        if r["signed"][c]:
+            continue
         assert member == (err <= tol)
         if d > 2.0:
             assert not member and np.isinf(err)
@@ -106,11 +109,45 @@ def test_shared_basis_set(name, dims, sigmas, shapes):
         assert abs(np.max(np.abs(approx - g)) + 1e-12 - err) <= 2e-13, (sg, d)
     # the (cfg) members this grid is expected to route to the basis path
     n_expected = {"cfg1": 8, "cfg4": 8, "cfg2": 18, "cfg3": 24}[name]  # (cfg4 pruned: 512^3)
-    assert r["member"].sum() == n_expected
+    assert (r["member"] & ~r["signed"]).sum() == n_expected
 
 
 def test_shared_basis_set_f64_exact_only():
     """fp64 storage accepts only fits <= 1e-12: just the exact d = 2 terms."""
     r = N.basis_set_fit((64,) * 3, [1.5, 2.0, 3.0], [1.5, 2.0, 2.5], 1, 1e-12)
-    assert list(r["member"]) == [False, True, False] * 3
+    assert list(r["member"] & ~r["signed"]) == [False, True, False] * 3
     assert len(r["betas"]) == 3
+
+
+@pytest.mark.parametrize("name,dims,sigmas,shapes", [
+    ("cfg1", (64,) * 3, [1.5, 2.0, 2.5, 3.0], [1.5, 2.0, 2.5]),
+    ("cfg4", (512,) * 3, [1.0, 1.5, 2.0, 3.0], [1.5, 2.0, 2.5, 3.0]),
+    ("cfg3", (256,) * 3, list(np.geomspace(1, 3, 8)), list(np.linspace(1.5, 2.5, 6))),
+])
+@pytest.mark.parametrize("dtype", [0, 1])
+def test_signed_members(name, dims, sigmas, shapes, dtype):
+    """d > 2 candidates join the shared basis as SIGNED members: weighted-ridge
+    least squares on the shared terms, certified by a bound factor E with
+    |eta~ - eta| <= E ||b||_inf / lam at every voxel (basis.cu). Independent
+    check: E covers the summed error of the mixture (storage-rounded factors
+    and weights) against the direct template over the candidate's own box,
+    and stays <= 1% of the template mass (the table's acceptance rule)."""
+    r = N.basis_set_fit(dims, sigmas, shapes, dtype, 1e-9)
+    rnd = (lambda a: np.asarray(a, np.float32).astype(np.float64)) if dtype == 0 else np.asarray
+    betas = r["betas"]
+    for c, (sg, d) in enumerate([(a, b) for a in sigmas for b in shapes]):
+        if d <= 2.0:
+            assert not r["signed"][c]
+            continue
+        assert r["signed"][c] and r["member"][c], (sg, d)
+        E, w, w0 = r["fit_err"][c], rnd(r["weights"][c]), r["w0"][c]
+        assert np.isfinite(E) and E > 0.0
+        R = O.support_radius(sg, d)
+        t = np.arange(-R, R + 1, dtype=np.float64)
+        f = rnd(np.exp(-np.outer(t * t, betas)))  # [offset, term] stored factors
+        mix = np.einsum("k,xk,yk,zk->xyz", w, f, f, f)
+        mix[R, R, R] += w0
+        s3 = t[:, None, None] ** 2 + t[None, :, None] ** 2 + t[None, None, :] ** 2
+        g = np.exp(-0.5 * s3 ** (d / 2) / sg ** d)
+        assert np.sum(np.abs(mix - g)) <= E, (sg, d)
+        assert E <= 0.01 * g.sum(), (sg, d)

@@ -45,8 +45,8 @@ def test_table_fits(P):
             assert c["path"] == "basis" and c["fit_err"] == 0.0
         elif c["d"] < 2.0:
             assert c["path"] == "basis" and c["fit_err"] <= 1e-9
-        else:
-            assert c["path"] == "direct"
+        else:  # signed members: maxima refined exactly
+            assert c["path"] == "basis+refine" and 0.0 < c["fit_err"] < 1.0
     # the shared terms' passes cost far less than the members' direct taps
     assert members[0]["basis_taps"] * 10 < sum(c["direct_taps"] for c in members)
     assert all(c["terms"] == members[0]["terms"] < 64 for c in members)
@@ -55,8 +55,8 @@ def test_table_fits(P):
     for c in info64["candidates"]:
         if c["d"] == 2.0:  # exact: no refinement needed
             assert c["path"] == "basis" and c["fit_err"] == 0.0
-        elif c["d"] > 2.0:
-            assert c["path"] == "direct"
+        elif c["d"] > 2.0:  # signed members
+            assert c["path"] == "basis+refine" and 0.0 < c["fit_err"] < 1e-3
         else:  # fp64: approximate basis, maxima refined exactly
             assert c["path"] == "basis+refine" and c["fit_err"] <= 1e-9
 
@@ -160,3 +160,37 @@ def test_eta_f64_refined_maxima(P):
         if cinfo["path"] == "basis+refine":
             E = (cinfo["fit_err"] + 2e-12) * l1 / 0.8
             assert np.max(np.abs(got[c] - fields[c])) <= E
+
+
+@pytest.mark.parametrize("prec,tol", [("f32", 1e-5), ("f64", 1e-10)])
+def test_signed_members_refined_maxima(P, prec, tol):
+    """d > 2 candidates on the shared basis with signed weights: an argmax-only
+    evaluation refines every voxel within 2 E_c of each member's approximate
+    maximum exactly, so each candidate's maximum and position equal the FFT
+    oracle's (and the direct path's) to the storage bar; the refined set is
+    small. With fields kept, the same candidates run on the direct kernels."""
+    import torch
+    from paper_2009_05473_b200 import _native as N
+    dims, kernel, r = cfg4_like(72, seed=11)
+    sg, dg = np.array([1.0, 1.5, 2.0, 3.0]), np.array([1.5, 2.0, 2.5, 3.0])
+    hats = O.template_hats(O.psf_hat(kernel), dims, sg, dg)
+    win = ((3, 68), (0, 71), (5, 66))
+    _, _, val, per, _ = O.eta_field(r, 0.9, hats, len(dg), win)
+    psf = P.Psf(P.Volume(kernel), normalize=False)
+    with P.precision(prec):
+        table = P.build_template_table(psf, sg, dg, tap_tol=1e-12)
+        paths = [c["path"] for c in table.info()["candidates"]]
+        assert all(p == "basis+refine" for p, (s, d) in zip(paths, [(a, b) for a in sg for b in dg])
+                   if d > 2.0)
+        rd = torch.tensor(r, device="cuda", dtype=torch.float32 if prec == "f32" else torch.float64)
+        best, recs, _ = P.certificate.eta_argmax_dev(rd, 0.9, table, win)
+        count = N.last_refine_count()
+        assert 0 < count <= 65536
+        dtab = P.build_template_table(psf, sg, dg, tap_tol=1e-12, mode="direct")
+        _, drecs, _ = P.certificate.eta_argmax_dev(rd, 0.9, dtab, win)
+    assert abs(best.value - val) <= tol * abs(val)
+    for c, (rec, drec) in enumerate(zip(recs, drecs)):
+        pos, v = per[c]
+        assert abs(rec.value - v) <= tol * abs(val), (c, rec.value, v)
+        assert abs(rec.value - drec.value) <= tol * abs(val), (c, rec.value, drec.value)
+        assert tuple(rec.pos) == tuple(pos), (c, tuple(rec.pos), pos)
