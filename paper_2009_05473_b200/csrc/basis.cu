@@ -851,11 +851,12 @@ __device__ __forceinline__ void st_stream(T* p, const Vec<T, V>& r) {
 // >= thr[member] to the item list (candidate id, voxel) — capped at col.cap,
 // the counter keeps counting past the cap.
 struct Collect {
-  const double* thr;  // [members]
-  int* cand;          // [cap] member index
-  long long* idx;     // [cap] voxel
+  const double* thr;    // [members]
+  int* cand;            // [cap] member index
+  long long* idx;       // [cap] voxel
   int* count;
   int cap;
+  const Best* part;     // the evaluation pass's per-CTA maxima [member][CTA]
 };
 
 template <typename T, int NM, int V, bool COLLECT = false>
@@ -874,6 +875,19 @@ __global__ void __launch_bounds__(kMixThreads) mix_argmax_kernel(
     sW[e] = m < nm ? W[size_t(m0 + m) * K + k] : T(0);
   }
   for (int e = threadIdx.x; e < NM; e += kMixThreads) sw0[e] = e < nm ? w0[m0 + e] : T(0);
+  if constexpr (COLLECT) {
+    // a CTA whose evaluation-pass maxima are all below the thresholds holds
+    // no qualifying voxel (same contiguous voxel chunk in both passes)
+    __shared__ int any;
+    if (threadIdx.x == 0) {
+      int a = 0;
+      for (int m = 0; m < nm; ++m)
+        a |= col.part[(long long)(m0 + m) * gridDim.x + blockIdx.x].v >= col.thr[m0 + m];
+      any = a;
+    }
+    __syncthreads();
+    if (!any) return;
+  }
   __syncthreads();
   T bacc[NM];
   int bidx[NM];
@@ -882,9 +896,12 @@ __global__ void __launch_bounds__(kMixThreads) mix_argmax_kernel(
     bacc[m] = T(-INFINITY);
     bidx[m] = 0x7fffffff;
   }
+  // contiguous chunk of V-vectors per CTA (the collect pass revisits only the
+  // chunks whose maxima can qualify)
   const long long nv = n / V;
-  for (long long q = blockIdx.x * (long long)kMixThreads + threadIdx.x; q < nv;
-       q += (long long)gridDim.x * kMixThreads) {
+  const long long chunk = ((nv + gridDim.x - 1) / gridDim.x + kMixThreads - 1) / kMixThreads * kMixThreads;
+  const long long qend = min(nv, (blockIdx.x + 1) * chunk);
+  for (long long q = blockIdx.x * chunk + threadIdx.x; q < qend; q += kMixThreads) {
     const long long i0 = q * V;
     const Vec<T, V> bv = ld_stream<T, V>(b + i0);
     T acc[NM][V];
@@ -1116,8 +1133,9 @@ int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[
 
 int basis_set_collect(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[3],
                       const void* b, double lam, const int32_t win[6], const double* thr_dev,
-                      int cap, int* cand_dev, long long* idx_dev, int* count_dev, void* scratch) {
-  const int nm = int(s->members.size()), nt = int(s->betas.size());
+                      int cap, int* cand_dev, long long* idx_dev, int* count_dev, void* scratch,
+                      bool fields) {
+  const int nm = fields ? s->n_nnls : int(s->members.size()), nt = int(s->betas.size());
   if (nm == 0) return SFW3D_OK;
   const long long n = vol_count(dims);
   const size_t es = dtype == SFW3D_F64 ? 8 : 4;
@@ -1126,9 +1144,32 @@ int basis_set_collect(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int di
   cv.take<char>(size_t(n) * es);
   const char* terms = cv.take<char>(size_t(n) * es * nt);  // left by basis_set_eval
   const int nblocks = std::min<long long>(4096, (long long)ctx->num_sms * 8);
+  const Best* partial = cv.take<Best>(size_t(nm) * nblocks);  // left by basis_set_eval
   const int4 wlo = make_int4(win[0], win[2], win[4], 0), whi = make_int4(win[1], win[3], win[5], 0);
   SFW3D_CUDA_TRY(cudaMemsetAsync(count_dev, 0, sizeof(int), ctx->stream));
-  const Collect col{thr_dev, cand_dev, idx_dev, count_dev, cap};
+  const Collect col{thr_dev, cand_dev, idx_dev, count_dev, cap, partial};
+  if (getenv("SFW3D_DEBUG_COLLECT")) {
+    std::vector<Best> hp(size_t(nm) * nblocks);
+    std::vector<double> ht(nm);
+    SFW3D_TRY(download_sync(ctx, hp.data(), partial, hp.size() * sizeof(Best)));
+    SFW3D_TRY(download_sync(ctx, ht.data(), thr_dev, ht.size() * sizeof(double)));
+    int any = 0;
+    for (int b = 0; b < nblocks; ++b) {
+      int a = 0;
+      for (int m = 0; m < nm; ++m) a |= hp[size_t(m) * nblocks + b].v >= ht[m];
+      any += a;
+    }
+    for (int m = 0; m < nm; ++m) {
+      double mx = -INFINITY;
+      int q = 0;
+      for (int b = 0; b < nblocks; ++b) {
+        mx = std::max(mx, hp[size_t(m) * nblocks + b].v);
+        q += hp[size_t(m) * nblocks + b].v >= ht[m];
+      }
+      fprintf(stderr, "[collect] member %d thr %.9g max %.9g ctas %d\n", m, ht[m], mx, q);
+    }
+    fprintf(stderr, "[collect] %d of %d CTAs qualify\n", any, nblocks);
+  }
   for (int m0 = 0; m0 < nm; m0 += kMixMax) {
     const int nmm = std::min(kMixMax, nm - m0);
     SFW3D_PROF(ctx, "eta_refine");

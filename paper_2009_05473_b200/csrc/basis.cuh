@@ -72,14 +72,16 @@ size_t basis_set_scratch(const BasisSet* s, long long n, int dtype);
 int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[3], const void* b,
                    double lam, const int32_t win[6], void* fields, Best* best_dev, void* scratch);
 
-// Refinement support (fp64 storage, inexact members): re-runs the fused mix
-// over the terms basis_set_eval left in `scratch` and appends every windowed
+// Refinement support (inexact / signed members): re-runs the fused mix over
+// the terms basis_set_eval left in `scratch` (same `fields` flag; only the
+// CTAs whose evaluation-pass maxima reach a threshold) and appends every windowed
 // voxel whose approximate eta >= thr_dev[member] (member-indexed) to
 // (cand_dev = candidate id, idx_dev = voxel); *count_dev receives the total
 // (may exceed cap: then the list is incomplete).
 int basis_set_collect(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[3],
                       const void* b, double lam, const int32_t win[6], const double* thr_dev,
-                      int cap, int* cand_dev, long long* idx_dev, int* count_dev, void* scratch);
+                      int cap, int* cand_dev, long long* idx_dev, int* count_dev, void* scratch,
+                      bool fields);
 int basis_set_member_index(const BasisSet* s, int cand);  // -1 when not a member
 int basis_set_member_cand(const BasisSet* s, int member);
 

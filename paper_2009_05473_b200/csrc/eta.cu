@@ -925,8 +925,10 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   for (int ci = 0; ci < nc; ++ci) direct[ci] = !use_basis(t, ci, dtype, fl);
   const BasisSet* bset = t->set(dtype);
   const size_t sb = any_basis ? basis_set_scratch(bset, n, dtype) : 0;
-  const size_t pb = (any_direct || any_refine)
-                        ? size_t(t->pdims[0]) * t->pdims[1] * t->pdims[2] * sizeof(T) : 0;
+  // the padded copy of b feeds the direct kernels only (refinement may fall
+  // back to them: the copy is then made on demand)
+  const size_t pbytes = size_t(t->pdims[0]) * t->pdims[1] * t->pdims[2] * sizeof(T);
+  const size_t pb = (any_direct || any_refine) ? pbytes : 0;
   constexpr int kRefCap = 1 << 16;  // refinement items per call
   // direct output tiles: the window, or the whole grid when fields are requested
   int ow[6];
@@ -970,14 +972,18 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   void* accd_g = ab ? cv.take<char>(ab) : nullptr;
   // b = H^T * r (tmp is pass scratch), then the periodic padding for direct
   SFW3D_TRY(psf_apply_impl(ctx, t->psf, dtype, residual, b, 1, tmp));
-  if (pb) {
+  bool padded = false;
+  auto make_pad = [&]() -> int {
+    if (padded || !bpad) return SFW3D_OK;
     SFW3D_PROF(ctx, "pad");
     const long long np = (long long)t->pdims[0] * t->pdims[1] * t->pdims[2];
     pad_kernel<T><<<unsigned((np + 255) / 256), 256, 0, ctx->stream>>>(
         b, bpad, dims[0], dims[1], dims[2], t->pad[0], t->pad[1], t->pad[2], t->pdims[0],
         t->pdims[1], t->pdims[2]);
     SFW3D_LAUNCH_CHECK(ctx);
-  }
+    padded = true;
+    return SFW3D_OK;
+  };
   Geo g;
   g.nx = dims[0]; g.ny = dims[1]; g.nz = dims[2];
   g.px = t->pad[0]; g.py = t->pad[1]; g.pz = t->pad[2];
@@ -1029,7 +1035,7 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
     }
     SFW3D_TRY(stage_upload(ctx, ref_thr, thr.data(), size_t(nm) * sizeof(double)));
     SFW3D_TRY(basis_set_collect(ctx, bset, dtype, dims, b, lam, win, ref_thr, kRefCap, ref_cand,
-                                ref_idx, ref_count, bscratch));
+                                ref_idx, ref_count, bscratch, fl));
     int count = 0;
     SFW3D_TRY(download_sync(ctx, &count, ref_count, sizeof(int)));
     last_refine_count() = count;
@@ -1061,6 +1067,7 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   }
   for (int ci = 0; ci < nc; ++ci) {
     if (!direct[ci]) continue;
+    SFW3D_TRY(make_pad());
     const CandHost& c = t->cands[ci];
     T* fld = fields ? static_cast<T*>(fields) + size_t(ci) * n : nullptr;
     long long nred = 0;

@@ -15,7 +15,9 @@
 //    taps broadcast from shared memory;
 //  * axis 2 (contiguous): a CTA stages 32 rows x (4J + taps) in shared
 //    memory (odd pitch: lane = row, conflict-free), same rotated window.
+#include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "internal.cuh"
 #include "window.cuh"
@@ -236,8 +238,8 @@ __global__ void __launch_bounds__(32 * kZWarps) pass_z_kernel(
 // (wrapped) are staged with 16-byte cp.async; lane = inner index (conflict-
 // free scalar smem reads, coalesced 128-byte stores). Per tap: one LDS of the
 // next window row + J FFMA (taps read four at a time, broadcast).
-template <typename T, int J, int TI, int NT>
-__global__ void __launch_bounds__(NT) pass_tile2_kernel(
+template <typename T, int J, int TI, int NT, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) pass_tile2_kernel(
     const T* __restrict__ in, T* __restrict__ out, int n_axis, long long stride,
     const T* __restrict__ taps_g, int lo, int ntaps, const T* addend, T aw, T w) {
   constexpr int G = NT / TI, To = J * G;
@@ -332,8 +334,8 @@ __global__ void __launch_bounds__(NT) pass_tile2_kernel(
 // leading zero taps, so the window is the shared Fold<T, J, 1> register
 // window (LDS.128 per 4 taps, pitch = 4 mod 8 words: conflict-free). Results
 // go back through shared memory for coalesced stores.
-template <typename T, int J>
-__global__ void __launch_bounds__(128) pass_z2_kernel(
+template <typename T, int J, int MINB = 1>
+__global__ void __launch_bounds__(128, MINB) pass_z2_kernel(
     const T* __restrict__ in, T* __restrict__ out, int nz, long long nrows,
     const T* __restrict__ taps_g, int lo, int ntaps, int pitch, const T* addend, T aw, T w) {
   constexpr int kVec = 16 / sizeof(T);
@@ -493,7 +495,7 @@ int launch_z(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* ta
   return SFW3D_OK;
 }
 
-template <typename T, int J>
+template <typename T, int J, int MINB = 1>
 int launch_tile2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis, const T* taps,
                  int lo, int ntaps, const T* addend, double aw, double w) {
   constexpr int TI = 64, NT = 256, To = J * (NT / TI);
@@ -505,16 +507,16 @@ int launch_tile2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axi
   const int nt4 = (ntaps + 3) & ~3;
   const size_t smem = (size_t(nt4) + size_t(To + nt4) * TI) * sizeof(T);
   if (smem > 48 * 1024)
-    SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_tile2_kernel<T, J, TI, NT>,
+    SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_tile2_kernel<T, J, TI, NT, MINB>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   dim3 grid(unsigned((n + To - 1) / To), unsigned(stride / TI), unsigned(outer));
-  pass_tile2_kernel<T, J, TI, NT><<<grid, NT, smem, ctx->stream>>>(in, out, n, stride, taps, lo,
+  pass_tile2_kernel<T, J, TI, NT, MINB><<<grid, NT, smem, ctx->stream>>>(in, out, n, stride, taps, lo,
                                                                    ntaps, addend, T(aw), T(w));
   SFW3D_LAUNCH_CHECK(ctx);
   return SFW3D_OK;
 }
 
-template <typename T, int J>
+template <typename T, int J, int MINB = 1>
 int launch_z2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* taps, int lo,
               int ntaps, const T* addend, double aw, double w) {
   const long long nrows = (long long)dims[0] * dims[1];
@@ -530,13 +532,30 @@ int launch_z2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* t
   }
   const size_t smem = (size_t(nt4) + 8 + size_t(32) * pitch) * sizeof(T);
   if (smem > 48 * 1024)
-    SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_z2_kernel<T, J>,
+    SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_z2_kernel<T, J, MINB>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   dim3 grid(unsigned((dims[2] + 4 * J - 1) / (4 * J)), unsigned((nrows + 31) / 32));
-  pass_z2_kernel<T, J><<<grid, 128, smem, ctx->stream>>>(in, out, dims[2], nrows, taps, lo, ntaps,
+  pass_z2_kernel<T, J, MINB><<<grid, 128, smem, ctx->stream>>>(in, out, dims[2], nrows, taps, lo, ntaps,
                                                          pitch, addend, T(aw), T(w));
   SFW3D_LAUNCH_CHECK(ctx);
   return SFW3D_OK;
+}
+
+// resident-CTA targets of the J = 32 v2 tiles: 3 strided (80 registers),
+// 5 contiguous (96 registers) — measured 29.1 -> 27.7 ms over the config-4
+// basis passes; SFW3D_PASS_OCC="1,1" restores the unconstrained allocation.
+// (A persistent NS-stage cp.async ring and a warp-specialised bulk-copy
+// producer were both measured slower than these one-shot tiles here.)
+static int pass_occ(int which) {
+  static const int v[2] = {[] {
+    const char* e = getenv("SFW3D_PASS_OCC");
+    return e ? atoi(e) : 3;
+  }(), [] {
+    const char* e = getenv("SFW3D_PASS_OCC");
+    const char* c = e ? strchr(e, ',') : nullptr;
+    return c ? atoi(c + 1) : 5;
+  }()};
+  return v[which];
 }
 
 // taps at or below which a pass takes the J = 16 tile (SFW3D_NARROW_TAPS)
@@ -561,11 +580,14 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
     const char* e = getenv("SFW3D_PASS_VARIANT");
     return e ? atoi(e) : 0;
   }();
+  const int v2 = variant;
   if (axis == 2) {
-    if (variant == 0 && dims[2] % 4 == 0 && ntaps <= 1024) {
+    if (v2 == 0 && dims[2] % 4 == 0 && ntaps <= 1024) {
       // narrow filters are HBM-bound: the smaller tile keeps more CTAs resident
       if (dims[2] >= 128 && ntaps > narrow_taps())
-        return launch_z2<T, 32>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
+        return pass_occ(1) == 5
+                   ? launch_z2<T, 32, 5>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w)
+                   : launch_z2<T, 32>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
       return launch_z2<T, 16>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
     }
     return wide ? launch_z<T, 32>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w)
@@ -573,13 +595,15 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
   }
   long long stride = 1;
   for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
-  if (variant == 0 && stride % 64 == 0 && ntaps <= 512) {
+  if (v2 == 0 && stride % 64 == 0 && ntaps <= 512) {
     if (dims[axis] >= 128 && ntaps > narrow_taps())
-      return launch_tile2<T, 32>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
+      return pass_occ(0) == 3
+                 ? launch_tile2<T, 32, 3>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w)
+                 : launch_tile2<T, 32>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
     return launch_tile2<T, 16>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
   }
   if (ntaps <= 512) {
-    switch (variant) {
+    switch (v2) {
       case 1:
         if (stride % 128 == 0)
           return launch_tiled<T, 16, 128, 512>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
