@@ -411,7 +411,9 @@ void fit_signed_members(BasisSet* s, const std::vector<BasisCandidate>& cands, i
     const double box_taps = double(bc.hi[0] - bc.lo[0] + 1) * (bc.hi[1] - bc.lo[1] + 1) *
                             (bc.hi[2] - bc.lo[2] + 1);
     std::vector<double> P(nt);
-    for (int e = kRidgeMin - 1; e <= kRidgeMax; ++e) {
+    int best_e = kRidgeMin - 1;
+    // one ridge weight 10^e (e < kRidgeMin: none): solve, bound, keep the best
+    auto try_ridge = [&](int e) {
       const ld mu = e < kRidgeMin ? 0.0L : std::pow(10.0L, (ld)e);
       for (int k = 0; k < ncol; ++k) A[size_t(k) * Mt + M + k] = std::sqrt(mu) * (ld)pen[k];
       std::vector<ld> z;
@@ -423,10 +425,10 @@ void fit_signed_members(BasisSet* s, const std::vector<BasisCandidate>& cands, i
         finite &= std::isfinite(w[k]);
       }
       double w0 = dtype == SFW3D_F64 ? double(z[nt]) : double(float(z[nt]));
-      if (!finite || !std::isfinite(w0)) continue;
+      if (!finite || !std::isfinite(w0)) return;
       double R = std::fabs(w0) * gmix;
       for (int k = 0; k < nt; ++k) R += std::fabs(w[k]) * pen[k];
-      if (R >= esig[c]) continue;
+      if (R >= esig[c]) return;
       double D1 = bc.tap_tol * box_taps;
       for (size_t ix = 0; ix < reps[0].size(); ++ix) {
         const Rep rx = reps[0][ix];
@@ -455,8 +457,16 @@ void fit_signed_members(BasisSet* s, const std::vector<BasisCandidate>& cands, i
         dsig[c] = D1;
         wsig[c] = w;
         w0sig[c] = w0;
+        best_e = e;
       }
-    }
+    };
+    // coarse scan (every 3 decades, and no ridge), then the neighbours of the best
+    try_ridge(kRidgeMin - 1);
+    for (int e = kRidgeMin; e <= kRidgeMax; e += 3) try_ridge(e);
+    const int e0 = best_e;
+    if (e0 >= kRidgeMin)
+      for (int e : {e0 - 2, e0 - 1, e0 + 1, e0 + 2})
+        if (e >= kRidgeMin && e <= kRidgeMax) try_ridge(e);
   };
   {
     const int nthreads =
@@ -857,6 +867,8 @@ struct Collect {
   int* count;
   int cap;
   const Best* part;     // the evaluation pass's per-CTA maxima [member][CTA]
+  int parents;          // evaluation grid (CTA chunks)
+  int split;            // collect CTAs per evaluation chunk
 };
 
 template <typename T, int NM, int V, bool COLLECT = false>
@@ -875,18 +887,23 @@ __global__ void __launch_bounds__(kMixThreads) mix_argmax_kernel(
     sW[e] = m < nm ? W[size_t(m0 + m) * K + k] : T(0);
   }
   for (int e = threadIdx.x; e < NM; e += kMixThreads) sw0[e] = e < nm ? w0[m0 + e] : T(0);
+  // contiguous chunk of V-vectors per evaluation CTA; the collect pass splits
+  // each chunk over col.split CTAs and revisits only the chunks whose
+  // evaluation-pass maxima reach a threshold
+  const long long nv = n / V;
+  const int parents = COLLECT ? col.parents : int(gridDim.x);
+  const int parent = COLLECT ? int(blockIdx.x) / col.split : int(blockIdx.x);
+  const long long chunk =
+      ((nv + parents - 1) / parents + kMixThreads - 1) / kMixThreads * kMixThreads;
+  long long qbeg = parent * chunk, qend = min(nv, (parent + 1) * chunk);
   if constexpr (COLLECT) {
-    // a CTA whose evaluation-pass maxima are all below the thresholds holds
-    // no qualifying voxel (same contiguous voxel chunk in both passes)
-    __shared__ int any;
-    if (threadIdx.x == 0) {
-      int a = 0;
-      for (int m = 0; m < nm; ++m)
-        a |= col.part[(long long)(m0 + m) * gridDim.x + blockIdx.x].v >= col.thr[m0 + m];
-      any = a;
-    }
-    __syncthreads();
-    if (!any) return;
+    const int q = threadIdx.x < nm &&
+                  col.part[(long long)(m0 + threadIdx.x) * parents + parent].v >= col.thr[m0 + threadIdx.x];
+    if (!__syncthreads_or(q)) return;
+    const int sub = int(blockIdx.x) % col.split;
+    const long long sc = ((chunk + col.split - 1) / col.split + kMixThreads - 1) / kMixThreads * kMixThreads;
+    qbeg += sub * sc;
+    qend = min(qend, qbeg + sc);
   }
   __syncthreads();
   T bacc[NM];
@@ -896,12 +913,7 @@ __global__ void __launch_bounds__(kMixThreads) mix_argmax_kernel(
     bacc[m] = T(-INFINITY);
     bidx[m] = 0x7fffffff;
   }
-  // contiguous chunk of V-vectors per CTA (the collect pass revisits only the
-  // chunks whose maxima can qualify)
-  const long long nv = n / V;
-  const long long chunk = ((nv + gridDim.x - 1) / gridDim.x + kMixThreads - 1) / kMixThreads * kMixThreads;
-  const long long qend = min(nv, (blockIdx.x + 1) * chunk);
-  for (long long q = blockIdx.x * chunk + threadIdx.x; q < qend; q += kMixThreads) {
+  for (long long q = qbeg + threadIdx.x; q < qend; q += kMixThreads) {
     const long long i0 = q * V;
     const Vec<T, V> bv = ld_stream<T, V>(b + i0);
     T acc[NM][V];
@@ -946,6 +958,7 @@ __global__ void __launch_bounds__(kMixThreads) mix_argmax_kernel(
           for (int j = 0; j < V; ++j) {
             const int z = z0 + j;
             if (z >= wlo.z && z <= whi.z && double(acc[m][j]) / lam >= col.thr[m0 + m]) {
+              atomicAdd(col.count + 1 + m0 + m, 1);
               const int slot = atomicAdd(col.count, 1);
               if (slot < col.cap) {
                 col.cand[slot] = cid[m0 + m];
@@ -1146,8 +1159,9 @@ int basis_set_collect(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int di
   const int nblocks = std::min<long long>(4096, (long long)ctx->num_sms * 8);
   const Best* partial = cv.take<Best>(size_t(nm) * nblocks);  // left by basis_set_eval
   const int4 wlo = make_int4(win[0], win[2], win[4], 0), whi = make_int4(win[1], win[3], win[5], 0);
-  SFW3D_CUDA_TRY(cudaMemsetAsync(count_dev, 0, sizeof(int), ctx->stream));
-  const Collect col{thr_dev, cand_dev, idx_dev, count_dev, cap, partial};
+  SFW3D_CUDA_TRY(cudaMemsetAsync(count_dev, 0, sizeof(int) * (1 + nm), ctx->stream));
+  constexpr int kSplit = 32;
+  const Collect col{thr_dev, cand_dev, idx_dev, count_dev, cap, partial, nblocks, kSplit};
   if (getenv("SFW3D_DEBUG_COLLECT")) {
     std::vector<Best> hp(size_t(nm) * nblocks);
     std::vector<double> ht(nm);
@@ -1174,11 +1188,11 @@ int basis_set_collect(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int di
     const int nmm = std::min(kMixMax, nm - m0);
     SFW3D_PROF(ctx, "eta_refine");
     if (dtype == SFW3D_F64)
-      SFW3D_TRY(launch_mix<double>(ctx, nblocks, b, terms, n, nt, nmm, m0, s, dims, wlo, whi, lam,
-                                   nullptr, nullptr, &col));
+      SFW3D_TRY(launch_mix<double>(ctx, nblocks * kSplit, b, terms, n, nt, nmm, m0, s, dims, wlo,
+                                   whi, lam, nullptr, nullptr, &col));
     else
-      SFW3D_TRY(launch_mix<float>(ctx, nblocks, b, terms, n, nt, nmm, m0, s, dims, wlo, whi, lam,
-                                  nullptr, nullptr, &col));
+      SFW3D_TRY(launch_mix<float>(ctx, nblocks * kSplit, b, terms, n, nt, nmm, m0, s, dims, wlo,
+                                  whi, lam, nullptr, nullptr, &col));
     SFW3D_LAUNCH_CHECK(ctx);
   }
   return SFW3D_OK;

@@ -76,8 +76,8 @@ int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[
 // the terms basis_set_eval left in `scratch` (same `fields` flag; only the
 // CTAs whose evaluation-pass maxima reach a threshold) and appends every windowed
 // voxel whose approximate eta >= thr_dev[member] (member-indexed) to
-// (cand_dev = candidate id, idx_dev = voxel); *count_dev receives the total
-// (may exceed cap: then the list is incomplete).
+// (cand_dev = candidate id, idx_dev = voxel); count_dev[0] receives the total
+// (may exceed cap: then the list is incomplete), count_dev[1 + m] member m's.
 int basis_set_collect(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[3],
                       const void* b, double lam, const int32_t win[6], const double* thr_dev,
                       int cap, int* cand_dev, long long* idx_dev, int* count_dev, void* scratch,

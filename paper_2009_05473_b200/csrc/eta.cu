@@ -929,7 +929,11 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   // back to them: the copy is then made on demand)
   const size_t pbytes = size_t(t->pdims[0]) * t->pdims[1] * t->pdims[2] * sizeof(T);
   const size_t pb = (any_direct || any_refine) ? pbytes : 0;
-  constexpr int kRefCap = 1 << 16;  // refinement items per call
+  // refinement items per call (SFW3D_REFINE_CAP overrides, for tests)
+  const int kRefCap = [] {
+    const char* e = getenv("SFW3D_REFINE_CAP");
+    return e ? std::max(1, atoi(e)) : (1 << 16);
+  }();
   // direct output tiles: the window, or the whole grid when fields are requested
   int ow[6];
   if (fields) {
@@ -943,7 +947,7 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   const int nxp = ow[1] - ow[0] + 1;
   const long long nblocks_direct = (long long)nty * ntz * nxp;
   const long long nblocks = nblocks_direct;
-  const size_t rb = any_refine ? size_t(kRefCap) * (4 + 8 + 8) + size_t(nc) * 8 + 96 : 0;
+  const size_t rb = any_refine ? size_t(kRefCap) * (4 + 8 + 8) + size_t(nc) * 12 + 352 : 0;
   // folded kernel slice sums in global memory (tuning variant)
   size_t ab = 0;
   if (fold_accd_global(sizeof(T))) {
@@ -967,7 +971,7 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   double* ref_val = any_refine ? cv.take<double>(kRefCap) : nullptr;
   double* ref_thr = any_refine ? cv.take<double>(nc) : nullptr;
   double* ref_l1 = any_refine ? cv.take<double>(2) : nullptr;  // [sum |b|, max |b| bits]
-  int* ref_count = any_refine ? cv.take<int>(1) : nullptr;
+  int* ref_count = any_refine ? cv.take<int>(1 + nc) : nullptr;  // [total, per member]
   std::vector<Best> refined(nc, Best{NAN, -1});  // exact maxima of refined members
   void* accd_g = ab ? cv.take<char>(ab) : nullptr;
   // b = H^T * r (tmp is pass scratch), then the periodic padding for direct
@@ -1036,12 +1040,35 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
     SFW3D_TRY(stage_upload(ctx, ref_thr, thr.data(), size_t(nm) * sizeof(double)));
     SFW3D_TRY(basis_set_collect(ctx, bset, dtype, dims, b, lam, win, ref_thr, kRefCap, ref_cand,
                                 ref_idx, ref_count, bscratch, fl));
-    int count = 0;
-    SFW3D_TRY(download_sync(ctx, &count, ref_count, sizeof(int)));
+    std::vector<int> counts(1 + nm, 0);
+    SFW3D_TRY(download_sync(ctx, counts.data(), ref_count, counts.size() * sizeof(int)));
+    int count = counts[0];
+    if (count > kRefCap) {
+      // keep refining the members with the fewest near-maximal voxels (within
+      // the cap), evaluate the others directly, and collect again
+      std::vector<int> order;
+      for (int m = 0; m < nm; ++m)
+        if (std::isfinite(thr[m])) order.push_back(m);
+      std::sort(order.begin(), order.end(), [&](int x, int y) { return counts[1 + x] < counts[1 + y]; });
+      long long used = 0;
+      for (int m : order) {
+        if (used + counts[1 + m] <= kRefCap) {
+          used += counts[1 + m];
+        } else {
+          thr[m] = INFINITY;
+          direct[basis_set_member_cand(bset, m)] = 1;
+        }
+      }
+      SFW3D_TRY(stage_upload(ctx, ref_thr, thr.data(), size_t(nm) * sizeof(double)));
+      SFW3D_TRY(basis_set_collect(ctx, bset, dtype, dims, b, lam, win, ref_thr, kRefCap, ref_cand,
+                                  ref_idx, ref_count, bscratch, fl));
+      SFW3D_TRY(download_sync(ctx, &count, ref_count, sizeof(int)));
+    }
     last_refine_count() = count;
-    if (count > kRefCap) {  // too many near-maximal voxels: exact direct evaluation
+    if (count > kRefCap) {  // (cannot happen after the split above; kept as a guard)
       for (int ci = 0; ci < nc; ++ci)
         if (use_refine(t, ci, dtype, fl)) direct[ci] = 1;
+      count = 0;
     } else if (count > 0) {
       SFW3D_PROF(ctx, "eta_refine");
       refine_kernel<T><<<count, 256, 0, ctx->stream>>>(

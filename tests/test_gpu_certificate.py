@@ -162,14 +162,19 @@ def test_eta_f64_refined_maxima(P):
             assert np.max(np.abs(got[c] - fields[c])) <= E
 
 
-@pytest.mark.parametrize("prec,tol", [("f32", 1e-5), ("f64", 1e-10)])
-def test_signed_members_refined_maxima(P, prec, tol):
+@pytest.mark.parametrize("prec,tol,cap", [("f32", 1e-5, None), ("f64", 1e-10, None),
+                                          ("f32", 1e-5, "6")])
+def test_signed_members_refined_maxima(P, prec, tol, cap, monkeypatch):
     """d > 2 candidates on the shared basis with signed weights: an argmax-only
     evaluation refines every voxel within 2 E_c of each member's approximate
     maximum exactly, so each candidate's maximum and position equal the FFT
     oracle's (and the direct path's) to the storage bar; the refined set is
-    small. With fields kept, the same candidates run on the direct kernels."""
+    small. With a refinement cap below the collected count (cap = 6), the
+    members with the most near-maximal voxels fall back to the direct
+    kernels and the rest are still refined."""
     import torch
+    if cap:
+        monkeypatch.setenv("SFW3D_REFINE_CAP", cap)
     from paper_2009_05473_b200 import _native as N
     dims, kernel, r = cfg4_like(72, seed=11)
     sg, dg = np.array([1.0, 1.5, 2.0, 3.0]), np.array([1.5, 2.0, 2.5, 3.0])
@@ -185,7 +190,7 @@ def test_signed_members_refined_maxima(P, prec, tol):
         rd = torch.tensor(r, device="cuda", dtype=torch.float32 if prec == "f32" else torch.float64)
         best, recs, _ = P.certificate.eta_argmax_dev(rd, 0.9, table, win)
         count = N.last_refine_count()
-        assert 0 < count <= 65536
+        assert 0 < count <= (int(cap) if cap else 65536)
         dtab = P.build_template_table(psf, sg, dg, tap_tol=1e-12, mode="direct")
         _, drecs, _ = P.certificate.eta_argmax_dev(rd, 0.9, dtab, win)
     assert abs(best.value - val) <= tol * abs(val)
