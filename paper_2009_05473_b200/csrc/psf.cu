@@ -378,6 +378,28 @@ __global__ void __launch_bounds__(128, MINB) pass_z2_kernel(
     const T* const q[1] = {tile + lane * pitch + warp * J};
     Fold<T, J, 1>::row(acc, taps, q, nt4 / 4);
   }
+  const long long row = row0 + lane;
+  const int zc = z0 + warp * J;
+  if (!addend) {
+    // straight from registers: J consecutive outputs per thread as 16-byte
+    // vector stores (the two halves of each 32-byte sector come from the
+    // same thread's consecutive stores)
+    if (row < nrows) {
+      T* po = out + row * nz + zc;
+#pragma unroll
+      for (int j = 0; j < J; j += 4) {
+        if (zc + j >= nz) break;
+        if constexpr (sizeof(T) == 4) {
+          __stcs(reinterpret_cast<float4*>(po + j),
+                 make_float4(w * acc[j], w * acc[j + 1], w * acc[j + 2], w * acc[j + 3]));
+        } else {
+          __stcs(reinterpret_cast<double2*>(po + j), make_double2(w * acc[j], w * acc[j + 1]));
+          __stcs(reinterpret_cast<double2*>(po + j + 2), make_double2(w * acc[j + 2], w * acc[j + 3]));
+        }
+      }
+    }
+    return;
+  }
   __syncthreads();  // every thread is done reading the staged input
   T* res = tile + lane * pitch + warp * J;
 #pragma unroll
@@ -393,12 +415,11 @@ __global__ void __launch_bounds__(128, MINB) pass_z2_kernel(
   const int ncols = 4 * J;
   for (int e = threadIdx.x; e < 32 * ncols; e += 128) {
     const int r = e / ncols, c = e - r * ncols;
-    const long long row = row0 + r;
+    const long long rw = row0 + r;
     const int z = z0 + c;
-    if (row < nrows && z < nz) {
-      const long long o = row * nz + z;
-      const T v = tile[r * pitch + c];
-      out[o] = addend ? T(aw * addend[o] + w * v) : T(w * v);
+    if (rw < nrows && z < nz) {
+      const long long o = rw * nz + z;
+      out[o] = T(aw * addend[o] + w * tile[r * pitch + c]);
     }
   }
 }
