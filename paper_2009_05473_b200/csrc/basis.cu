@@ -27,6 +27,7 @@
 #include <thread>
 
 #include "basis.cuh"
+#include "window.cuh"
 
 namespace sfw3d {
 
@@ -281,6 +282,12 @@ struct BasisSet {
   void* W_dev = nullptr;            // storage dtype, [member][term]
   void* w0_dev = nullptr;
   int* cid_dev = nullptr;           // member -> candidate id
+  // fp32 fused x pass + mix (xmix_kernel): every term's axis-0 taps, each
+  // padded with zeros to a multiple of 4, concatenated; per term {offset, lo,
+  // padded length, 0}
+  float* xtaps_dev = nullptr;
+  int4* xmeta_dev = nullptr;
+  int max_nt4x = 0, xtaps_total = 0;
   long long taps_per_voxel = 0;
   int device = 0;
 };
@@ -754,6 +761,19 @@ int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands,
     }
     SFW3D_TRY(upload(reinterpret_cast<void**>(&s->cid_dev), s->members.data(),
                      s->members.size() * sizeof(int)));
+    if (dtype == SFW3D_F32) {
+      std::vector<float> xt;
+      std::vector<int4> meta;
+      for (int t = 0; t < nt; ++t) {
+        const int len = s->tlen[0][t], nt4 = (len + 3) & ~3;
+        meta.push_back(make_int4(int(xt.size()), s->tlo[0][t], nt4, 0));
+        for (int q = 0; q < nt4; ++q) xt.push_back(q < len ? float(hstore[t][q]) : 0.f);
+        s->max_nt4x = std::max(s->max_nt4x, nt4);
+      }
+      s->xtaps_total = int(xt.size());
+      SFW3D_TRY(upload(reinterpret_cast<void**>(&s->xtaps_dev), xt.data(), xt.size() * sizeof(float)));
+      SFW3D_TRY(upload(reinterpret_cast<void**>(&s->xmeta_dev), meta.data(), meta.size() * sizeof(int4)));
+    }
   }
   return SFW3D_OK;
 }
@@ -765,6 +785,8 @@ void basis_set_destroy(BasisSet* s) {
   if (s->W_dev) cudaFree(s->W_dev);
   if (s->w0_dev) cudaFree(s->w0_dev);
   if (s->cid_dev) cudaFree(s->cid_dev);
+  if (s->xtaps_dev) cudaFree(s->xtaps_dev);
+  if (s->xmeta_dev) cudaFree(s->xmeta_dev);
   delete s;
 }
 
@@ -1017,6 +1039,319 @@ __global__ void __launch_bounds__(kMixThreads) mix_argmax_kernel(
   }
 }
 
+// ------------------------------------------------ fused x pass + member mix
+// fp32 storage. `U` holds, per shared term k, U_k = f_k^(y) f_k^(z) * b (the
+// two in-plane passes). This kernel forms T_k = f_k^(x) * U_k for a tile of
+// kXTo x-outputs x kXTI consecutive inner (y, z) indices in registers and
+// folds it straight into every member's accumulator,
+//     acc_m = w0_m b + sum_k W[m][k] T_k      (k ascending, one FMA each),
+// so T_k never goes to HBM and the (K + 1)-volume mix read disappears. The
+// arithmetic is the same FMA chains as pass + mix_argmax_kernel (same
+// rounding bound, basis.cu signed members).
+//   Packed fp32x2 (FFMA2): lane l owns the inner pair (2l, 2l + 1), so a
+//   staged row gives the pair with one 8-byte LDS, and every FMA of the pass
+//   and of the mix is one FFMA2 on (inner 2l, inner 2l + 1) — half the
+//   issue slots of scalar FFMA at the same FP32 pipe rate, which leaves room
+//   for the loads at 8 warps per SM (the 16 x J accumulator pairs take 128
+//   registers). Taps and weights are stored as duplicated pairs (t, t).
+//   CTA = kXW persistent warps; warp w owns x-outputs a0 + w J .. + J - 1.
+//   The (tile, term) sequence streams rows a0 + lo_k .. a0 + kXTo + nt4_k - 2
+//   (wrapped) of the 64-wide inner column through a kXNS-deep cp.async ring
+//   (one commit group per entry, one barrier per entry).
+constexpr int kXJ = 4;                 // x-outputs per thread
+constexpr int kXP = 4;                 // window prefetch (steps)
+constexpr int kXW = 8;                 // warps per CTA
+constexpr int kXTo = kXJ * kXW;        // x-outputs per tile
+constexpr int kXTI = 64;               // inner indices per tile (2 per lane)
+constexpr int kXNS = 4;                // ring depth
+
+typedef unsigned long long f2;  // packed fp32 pair (low = first)
+
+__device__ __forceinline__ void ffma2(f2& c, f2 a, f2 b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ f2 lds2v(const float* p) {
+  f2 v;
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(p));
+  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(sa));
+  return v;
+}
+__device__ __forceinline__ void lds22v(const f2* p, f2& a, f2& b) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(p));
+  asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"(sa));
+}
+__device__ __forceinline__ float lo32(f2 v) { return __uint_as_float(unsigned(v)); }
+__device__ __forceinline__ float hi32(f2 v) { return __uint_as_float(unsigned(v >> 32)); }
+__device__ __forceinline__ f2 dup2(float x) {
+  const unsigned long long u = __float_as_uint(x);
+  return u | (u << 32);
+}
+
+// order-preserving key of a float (larger value -> larger key; 0 = none)
+__device__ __forceinline__ unsigned fkey(float v) {
+  const unsigned u = __float_as_uint(v);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+template <int NM, bool COLLECT>
+__global__ void __launch_bounds__(kXW * 32, 1) xmix_kernel(
+    const float* __restrict__ b, const float* __restrict__ U, long long n, int K, int nm, int m0,
+    const float* __restrict__ W, const float* __restrict__ w0, const int* __restrict__ cid,
+    const float* __restrict__ xtaps, const int4* __restrict__ xmeta, int xtaps_total,
+    int stage_rows, int nx, int ny, int nz, int4 wlo, int4 whi, double lam,
+    float* __restrict__ fields, Best* __restrict__ partial, Collect col) {
+  constexpr int J = kXJ, S = kXJ + kXP, TI = kXTI, NT = kXW * 32;
+  static_assert(S % 4 == 0 && S <= 8, "window steps come in 4-tap groups");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // ring slot: [stage_rows][TI] term rows, then [kXTo][TI] rows of b (filled
+  // with the tile's first term)
+  const int slot_f = (stage_rows + kXTo) * TI;
+  float* stage = reinterpret_cast<float*>(smem_raw);     // kXNS slots
+  f2* sW = reinterpret_cast<f2*>(stage + kXNS * slot_f); // [K][NM] (w, w)
+  f2* sw0 = sW + K * NM;                                 // [NM]
+  f2* st = sw0 + NM;                                     // taps (t, t), xtaps_total + 8
+  int4* smeta = reinterpret_cast<int4*>(st + xtaps_total + 8);  // [K]
+  __shared__ float red_v[NM][kXW];
+  __shared__ long long red_i[NM][kXW];
+
+  const int stride = ny * nz;  // n < 2^31 (host check)
+  const int ntx = (nx + kXTo - 1) / kXTo;
+  const int ntiles = ntx * (stride / TI);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int my_tiles;
+  if constexpr (COLLECT) {
+    // one tile per CTA, revisited only when one of its maxima qualifies
+    const int q = threadIdx.x < nm &&
+                  col.part[(long long)(m0 + threadIdx.x) * col.parents + blockIdx.x].v >=
+                      col.thr[m0 + threadIdx.x];
+    if (!__syncthreads_or(q)) return;
+    my_tiles = 1;
+  } else {
+    my_tiles = (ntiles - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x);
+  }
+  for (int e = threadIdx.x; e < K * NM; e += NT) {
+    const int k = e / NM, m = e % NM;
+    sW[e] = dup2(m < nm ? W[size_t(m0 + m) * K + k] : 0.f);
+  }
+  for (int e = threadIdx.x; e < NM; e += NT) sw0[e] = dup2(e < nm ? w0[m0 + e] : 0.f);
+  for (int e = threadIdx.x; e < xtaps_total + 8; e += NT) st[e] = dup2(e < xtaps_total ? xtaps[e] : 0.f);
+  for (int e = threadIdx.x; e < K; e += NT) smeta[e] = xmeta[e];
+  __syncthreads();
+
+  // producer cursor: sequence entry (tile pi, term pk) -> ring slot pg
+  auto tile_geo = [&](int i, int& a0, int& inner0) {
+    const int tile = COLLECT ? int(blockIdx.x) : int(blockIdx.x) + i * int(gridDim.x);
+    const int ti = tile / ntx;
+    a0 = (tile - ti * ntx) * kXTo;
+    inner0 = ti * TI;
+  };
+  int pk = 0, pi = 0, pg = 0, pa0, pinner0;
+  tile_geo(0, pa0, pinner0);
+  constexpr int kV = TI / 4, dr = NT / kV;  // 16-byte chunks per row, rows per step
+  const int c = (threadIdx.x % kV) * 4, r0 = threadIdx.x / kV;
+  auto stage_next = [&]() {
+    float* slot = stage + (pg % kXNS) * slot_f + c;
+    const int4 mt = smeta[pk];
+    const int rows = kXTo + mt.z - 1;
+    const float* src = U + (long long)pk * n + pinner0 + c;
+    int x = (pa0 + mt.y + r0) % nx;
+    if (x < 0) x += nx;
+    for (int r = r0; r < rows; r += dr) {
+      cp_async16(slot + r * TI, src + x * stride);
+      x += dr;
+      while (x >= nx) x -= nx;
+    }
+    if (pk == 0) {  // the tile's b rows a0 .. a0 + kXTo - 1 (wrapped)
+      const float* bs = b + pinner0 + c;
+      for (int rb = r0; rb < kXTo; rb += dr) {
+        int xb = pa0 + rb;
+        while (xb >= nx) xb -= nx;
+        cp_async16(slot + (stage_rows + rb) * TI, bs + xb * stride);
+      }
+    }
+    ++pg;
+    if (++pk == K) {
+      pk = 0;
+      ++pi;
+      tile_geo(pi, pa0, pinner0);
+    }
+  };
+
+  const int G = my_tiles * K;
+#pragma unroll
+  for (int g = 0; g < kXNS - 1; ++g) {
+    if (g < G) stage_next();
+    cp_async_commit();
+  }
+  f2 acc[NM][J];
+  for (int i = 0; i < my_tiles; ++i) {
+    int a0, inner0;
+    tile_geo(i, a0, inner0);
+    const int tile = COLLECT ? int(blockIdx.x) : int(blockIdx.x) + i * int(gridDim.x);
+    for (int k = 0; k < K; ++k) {
+      const int g = i * K + k;
+      cp_async_wait_group<kXNS - 2>();  // this thread's copies of entry g landed
+      __syncthreads();                   // everyone's; everyone is done with g - 1
+      if (g + kXNS - 1 < G) stage_next();
+      cp_async_commit();
+      const float* cur = stage + (g % kXNS) * slot_f;
+      if (k == 0) {  // acc[m][j] = w0_m b(x_j)
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const f2 bv = lds2v(cur + (stage_rows + warp * J + j) * TI + 2 * lane);
+#pragma unroll
+          for (int m = 0; m < NM; ++m) {
+            acc[m][j] = 0ull;
+            ffma2(acc[m][j], sw0[m], bv);
+          }
+        }
+      }
+      const int4 mt = smeta[k];
+      const f2* tp = st + mt.x;
+      const int nt4 = mt.z;
+      const float* src = cur + (warp * J) * TI + 2 * lane;
+      f2 win[S], o[J];
+#pragma unroll
+      for (int s2 = 0; s2 < S; ++s2) win[s2] = lds2v(src + s2 * TI);
+#pragma unroll
+      for (int j = 0; j < J; ++j) o[j] = 0ull;
+      // volatile shared loads stay in program order: each tap group is read
+      // one group ahead, each window row kXP steps ahead of its first use
+      f2 tn[4];
+      lds22v(tp, tn[0], tn[1]);
+      lds22v(tp + 2, tn[2], tn[3]);
+      int q0 = 0;
+      for (; q0 + S <= nt4; q0 += S) {
+#pragma unroll
+        for (int r = 0; r < S; r += 4) {
+          const f2 tv[4] = {tn[0], tn[1], tn[2], tn[3]};
+          lds22v(tp + q0 + r + 4, tn[0], tn[1]);
+          lds22v(tp + q0 + r + 6, tn[2], tn[3]);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+#pragma unroll
+            for (int j = 0; j < J; ++j) ffma2(o[j], tv[kk], win[(r + kk + j) % S]);
+            win[r + kk] = lds2v(src + (q0 + r + kk + S) * TI);
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < S; r += 4) {
+        if (q0 + r >= nt4) break;
+        const f2 tv[4] = {tn[0], tn[1], tn[2], tn[3]};
+        lds22v(tp + q0 + r + 4, tn[0], tn[1]);
+        lds22v(tp + q0 + r + 6, tn[2], tn[3]);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+#pragma unroll
+          for (int j = 0; j < J; ++j) ffma2(o[j], tv[kk], win[(r + kk + j) % S]);
+          win[r + kk] = lds2v(src + (q0 + r + kk + S) * TI);
+        }
+      }
+      // fold T_k into every member (k ascending: the mix kernel's FMA order)
+#pragma unroll
+      for (int m2 = 0; m2 < NM; m2 += 2) {
+        f2 wa, wb;
+        lds22v(sW + k * NM + m2, wa, wb);
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          ffma2(acc[m2][j], wa, o[j]);
+          ffma2(acc[m2 + 1][j], wb, o[j]);
+        }
+      }
+    }
+
+    // ---- tile epilogue: window test, fields / collect / argmax. Value
+    // (j, h) of this thread is voxel x = a0 + warp J + j, inner = inner0 +
+    // 2 lane + h; C-order index x * stride + inner.
+    const int xw = a0 + warp * J;
+    unsigned vmask = 0;  // bit 2 j + h: in the window
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int inner = inner0 + 2 * lane + h;
+      const int y = inner / nz, z = inner - y * nz;
+      if (y < wlo.y || y > whi.y || z < wlo.z || z > whi.z) continue;
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const int x = xw + j;
+        if (x < nx && x >= wlo.x && x <= whi.x) vmask |= 1u << (2 * j + h);
+      }
+    }
+    if constexpr (COLLECT) {
+#pragma unroll
+      for (int m = 0; m < NM; ++m) {
+        if (m >= nm) break;
+#pragma unroll
+        for (int q = 0; q < 2 * J; ++q) {
+          const float v = (q & 1) ? hi32(acc[m][q >> 1]) : lo32(acc[m][q >> 1]);
+          if (((vmask >> q) & 1u) && double(v) / lam >= col.thr[m0 + m]) {
+            atomicAdd(col.count + 1 + m0 + m, 1);
+            const int slot = atomicAdd(col.count, 1);
+            if (slot < col.cap) {
+              col.cand[slot] = cid[m0 + m];
+              col.idx[slot] = (long long)(xw + (q >> 1)) * stride + inner0 + 2 * lane + (q & 1);
+            }
+          }
+        }
+      }
+      continue;
+    }
+#pragma unroll
+    for (int m = 0; m < NM; ++m) {
+      if (m >= nm) break;
+      if (fields) {
+        float* f = fields + (long long)cid[m0 + m] * n + inner0 + 2 * lane;
+#pragma unroll
+        for (int j = 0; j < J; ++j)
+          if (xw + j < nx)
+            __stcs(reinterpret_cast<float2*>(f + (long long)(xw + j) * stride),
+                   make_float2(float(double(lo32(acc[m][j])) / lam),
+                               float(double(hi32(acc[m][j])) / lam)));
+      }
+      // first maximum of the thread (x, then inner ascending); the warp's:
+      // largest key, ties to the smallest x offset, then the lowest lane
+      unsigned key = 0;
+      int bq = 2 * J;
+#pragma unroll
+      for (int q = 0; q < 2 * J; ++q) {
+        const float v = (q & 1) ? hi32(acc[m][q >> 1]) : lo32(acc[m][q >> 1]);
+        const unsigned kq = ((vmask >> q) & 1u) ? fkey(v) : 0u;
+        if (kq > key) {
+          key = kq;
+          bq = q;
+        }
+      }
+      const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
+      unsigned tied = __ballot_sync(0xffffffffu, key == kmax);
+      if (__popc(tied) > 1) {
+        const unsigned jmin = __reduce_min_sync(0xffffffffu, key == kmax ? unsigned(bq >> 1) : 0xffu);
+        tied = __ballot_sync(0xffffffffu, key == kmax && unsigned(bq >> 1) == jmin);
+      }
+      const int src_lane = __ffs(tied) - 1;
+      const int wq = __shfl_sync(0xffffffffu, bq, src_lane);
+      if (lane == 0) {
+        const unsigned u = (kmax & 0x80000000u) ? (kmax & 0x7fffffffu) : ~kmax;
+        red_v[m][warp] = kmax == 0 ? -INFINITY : __uint_as_float(u);
+        red_i[m][warp] = kmax == 0 ? 0x7fffffffffffffffLL
+                                   : (long long)(xw + (wq >> 1)) * stride + inner0 + 2 * src_lane + (wq & 1);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < nm) {
+      const int m = threadIdx.x;
+      float bv = red_v[m][0];
+      long long bi = red_i[m][0];
+      for (int w = 1; w < kXW; ++w)
+        if (red_v[m][w] > bv || (red_v[m][w] == bv && red_i[m][w] < bi)) {
+          bv = red_v[m][w];
+          bi = red_i[m][w];
+        }
+      partial[(long long)(m0 + m) * ntiles + tile] =
+          Best{bi == 0x7fffffffffffffffLL ? -INFINITY : double(bv) / lam, bi};
+    }
+  }
+}
+
 __global__ void member_reduce_kernel(const Best* __restrict__ partial, int nblocks,
                                      const int* __restrict__ cid, Best* __restrict__ best_dev) {
   __shared__ Best sb[32];
@@ -1045,11 +1380,41 @@ __global__ void member_reduce_kernel(const Best* __restrict__ partial, int nbloc
 
 }  // namespace
 
-size_t basis_set_scratch(const BasisSet* s, long long n, int dtype) {
+static size_t xmix_smem(const BasisSet* s);
+// The fused x pass + mix (opt-in: SFW3D_XMIX=1) applies to fp32 tables whose
+// inner (y, z) plane is a multiple of the 64-wide tile and whose weights and
+// taps fit in shared memory. Measured on config 4 (16 members, 26 terms): the
+// 16 x J accumulators hold the kernel at 8 warps per SM and it issues at
+// ~45-55% — 17-21 ms against 14.3 ms for the separate x pass (26 launches,
+// J = 32 register windows) + HBM-bound mix, so the separate kernels stay the
+// default (profiles/round1/xmix_notes.md).
+static bool xmix_ok(const BasisSet* s, int dtype, const int dims[3]) {
+  const char* e = getenv("SFW3D_XMIX");
+  if (!(e && atoi(e) == 1) || dtype != SFW3D_F32 || !s->xtaps_dev) return false;
+  if ((long long)dims[1] * dims[2] % kXTI != 0) return false;
+  return xmix_smem(s) <= 200 * 1024;
+}
+static int xmix_stage_rows(const BasisSet* s) { return kXTo + s->max_nt4x + kXJ + kXP + 4; }
+static size_t xmix_smem(const BasisSet* s) {
+  const int K = int(s->betas.size());
+  return sizeof(float) * size_t(kXNS) * (xmix_stage_rows(s) + kXTo) * kXTI +
+         sizeof(f2) * (size_t(K) * 16 + 16 + s->xtaps_total + 8) + sizeof(int4) * K;
+}
+static long long xmix_tiles(const int dims[3]) {
+  return (long long)((dims[0] + kXTo - 1) / kXTo) * ((long long)dims[1] * dims[2] / kXTI);
+}
+// per-member partial maxima: one per evaluation CTA
+static long long eval_blocks(const BasisSet* s, int dtype, const int dims[3], int num_sms) {
+  if (xmix_ok(s, dtype, dims)) return xmix_tiles(dims);
+  return std::min<long long>(4096, (long long)num_sms * 8);
+}
+
+size_t basis_set_scratch(const BasisSet* s, long long n, int dtype, const int dims[3]) {
   if (!s || s->members.empty()) return 0;
   const size_t es = dtype == SFW3D_F64 ? 8 : 4;
+  const long long nb = std::max<long long>(4096, eval_blocks(s, dtype, dims, 4096));
   return Carver::need({size_t(n) * es, size_t(n) * es, size_t(n) * es * s->betas.size(),
-                       s->members.size() * 4096 * sizeof(Best)});
+                       s->members.size() * size_t(nb) * sizeof(Best)});
 }
 
 template <typename T, int NM, int V>
@@ -1097,6 +1462,37 @@ static int launch_mix(sfw3d_ctx* ctx, int nblocks, const void* b, const void* te
 #undef SFW3D_MIX
 }
 
+template <int NM, bool COLLECT>
+static int launch_xmix_nm(sfw3d_ctx* ctx, const BasisSet* s, const int dims[3], const float* b,
+                          const float* U, int K, int nm, int m0, int4 wlo, int4 whi, double lam,
+                          float* fields, Best* partial, const Collect* col) {
+  const size_t smem = xmix_smem(s);
+  SFW3D_CUDA_TRY(cudaFuncSetAttribute(xmix_kernel<NM, COLLECT>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  // persistent CTAs (one per SM) for the evaluation; one tile per CTA for
+  // the collect pass (most tiles exit at once)
+  const long long tiles = xmix_tiles(dims);
+  const unsigned grid = COLLECT ? unsigned(tiles) : unsigned(std::min<long long>(tiles, ctx->num_sms));
+  xmix_kernel<NM, COLLECT><<<grid, kXW * 32, smem, ctx->stream>>>(
+      b, U, vol_count(dims), K, nm, m0, static_cast<const float*>(s->W_dev),
+      static_cast<const float*>(s->w0_dev), s->cid_dev, s->xtaps_dev, s->xmeta_dev, s->xtaps_total,
+      xmix_stage_rows(s), dims[0], dims[1], dims[2], wlo, whi, lam, fields, partial,
+      col ? *col : Collect{});
+  SFW3D_LAUNCH_CHECK(ctx);
+  return SFW3D_OK;
+}
+
+static int launch_xmix(sfw3d_ctx* ctx, const BasisSet* s, const int dims[3], const float* b,
+                       const float* U, int K, int nm, int m0, int4 wlo, int4 whi, double lam,
+                       float* fields, Best* partial, const Collect* col) {
+  if (col) {
+    if (nm <= 8) return launch_xmix_nm<8, true>(ctx, s, dims, b, U, K, nm, m0, wlo, whi, lam, fields, partial, col);
+    return launch_xmix_nm<16, true>(ctx, s, dims, b, U, K, nm, m0, wlo, whi, lam, fields, partial, col);
+  }
+  if (nm <= 8) return launch_xmix_nm<8, false>(ctx, s, dims, b, U, K, nm, m0, wlo, whi, lam, fields, partial, col);
+  return launch_xmix_nm<16, false>(ctx, s, dims, b, U, K, nm, m0, wlo, whi, lam, fields, partial, col);
+}
+
 int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[3], const void* b,
                    double lam, const int32_t win[6], void* fields, Best* best_dev, void* scratch) {
   const int nm = fields ? s->n_nnls : int(s->members.size()), nt = int(s->betas.size());
@@ -1111,8 +1507,26 @@ int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[
   char* t1 = cv.take<char>(size_t(n) * es);
   char* t2 = cv.take<char>(size_t(n) * es);
   char* terms = cv.take<char>(size_t(n) * es * nt);
-  const int nblocks = std::min<long long>(4096, (long long)ctx->num_sms * 8);
+  const int nblocks = int(eval_blocks(s, dtype, dims, ctx->num_sms));
   Best* partial = cv.take<Best>(size_t(nm) * nblocks);
+  const int4 wlo = make_int4(win[0], win[2], win[4], 0), whi = make_int4(win[1], win[3], win[5], 0);
+  if (xmix_ok(s, dtype, dims)) {
+    // U_k = f_k^(y) f_k^(z) * b per term, then the fused x pass + mix
+    for (int t = 0; t < nt; ++t) {
+      const char* tp = static_cast<const char*>(s->taps[t]);
+      const int l0 = s->tlen[0][t], l1 = s->tlen[1][t], l2 = s->tlen[2][t];
+      SFW3D_TRY(corr_pass_impl(ctx, dtype, b, t1, dims, 2, tp + es * (l0 + l1), s->tlo[2][t], l2,
+                               nullptr, 0.0, 1.0, "eta_basis"));
+      SFW3D_TRY(corr_pass_impl(ctx, dtype, t1, terms + size_t(t) * n * es, dims, 1, tp + es * l0,
+                               s->tlo[1][t], l1, nullptr, 0.0, 1.0, "eta_basis"));
+    }
+    for (int m0 = 0; m0 < nm; m0 += 16) {
+      SFW3D_PROF(ctx, "eta_mix");
+      SFW3D_TRY(launch_xmix(ctx, s, dims, static_cast<const float*>(b),
+                            reinterpret_cast<const float*>(terms), nt, std::min(16, nm - m0), m0,
+                            wlo, whi, lam, static_cast<float*>(fields), partial, nullptr));
+    }
+  } else {
   // T_k = (f_k x f_k x f_k) * b for every shared term
   for (int t = 0; t < nt; ++t) {
     const char* tp = static_cast<const char*>(s->taps[t]);
@@ -1124,7 +1538,6 @@ int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[
     SFW3D_TRY(corr_pass_impl(ctx, dtype, t2, terms + size_t(t) * n * es, dims, 0, tp, s->tlo[0][t],
                              l0, nullptr, 0.0, 1.0, "eta_basis"));
   }
-  const int4 wlo = make_int4(win[0], win[2], win[4], 0), whi = make_int4(win[1], win[3], win[5], 0);
   for (int m0 = 0; m0 < nm; m0 += kMixMax) {
     const int nmm = std::min(kMixMax, nm - m0);
     SFW3D_PROF(ctx, "eta_mix");
@@ -1135,6 +1548,7 @@ int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[
       SFW3D_TRY(launch_mix<float>(ctx, nblocks, b, terms, n, nt, nmm, m0, s, dims, wlo, whi, lam,
                                   fields, partial, nullptr));
     SFW3D_LAUNCH_CHECK(ctx);
+  }
   }
   {
     SFW3D_PROF(ctx, "argmax");
@@ -1156,10 +1570,21 @@ int basis_set_collect(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int di
   cv.take<char>(size_t(n) * es);
   cv.take<char>(size_t(n) * es);
   const char* terms = cv.take<char>(size_t(n) * es * nt);  // left by basis_set_eval
-  const int nblocks = std::min<long long>(4096, (long long)ctx->num_sms * 8);
+  const int nblocks = int(eval_blocks(s, dtype, dims, ctx->num_sms));
   const Best* partial = cv.take<Best>(size_t(nm) * nblocks);  // left by basis_set_eval
   const int4 wlo = make_int4(win[0], win[2], win[4], 0), whi = make_int4(win[1], win[3], win[5], 0);
   SFW3D_CUDA_TRY(cudaMemsetAsync(count_dev, 0, sizeof(int) * (1 + nm), ctx->stream));
+  if (xmix_ok(s, dtype, dims)) {
+    // re-run the fused kernel on the tiles whose evaluation maxima qualify
+    const Collect col{thr_dev, cand_dev, idx_dev, count_dev, cap, partial, nblocks, 1};
+    for (int m0 = 0; m0 < nm; m0 += 16) {
+      SFW3D_PROF(ctx, "eta_refine");
+      SFW3D_TRY(launch_xmix(ctx, s, dims, static_cast<const float*>(b),
+                            reinterpret_cast<const float*>(terms), nt, std::min(16, nm - m0), m0,
+                            wlo, whi, lam, nullptr, nullptr, &col));
+    }
+    return SFW3D_OK;
+  }
   constexpr int kSplit = 32;
   const Collect col{thr_dev, cand_dev, idx_dev, count_dev, cap, partial, nblocks, kSplit};
   if (getenv("SFW3D_DEBUG_COLLECT")) {

@@ -65,7 +65,7 @@ double basis_set_flops(const BasisSet* s);          // executed flops per voxel 
 double basis_set_member_flops(const BasisSet* s);   // mix flops per voxel per member
 
 // Scratch (bytes) basis_set_eval needs for a volume of n elements.
-size_t basis_set_scratch(const BasisSet* s, long long n, int dtype);
+size_t basis_set_scratch(const BasisSet* s, long long n, int dtype, const int dims[3]);
 // eta for all members: best_dev[cand] receives each member's windowed
 // argmax; fields (n_cand volumes, candidate-major) are written when non-NULL
 // (then the signed members are skipped: their values are not certified).

@@ -924,7 +924,7 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   std::vector<char> direct(nc, 0);
   for (int ci = 0; ci < nc; ++ci) direct[ci] = !use_basis(t, ci, dtype, fl);
   const BasisSet* bset = t->set(dtype);
-  const size_t sb = any_basis ? basis_set_scratch(bset, n, dtype) : 0;
+  const size_t sb = any_basis ? basis_set_scratch(bset, n, dtype, dims) : 0;
   // the padded copy of b feeds the direct kernels only (refinement may fall
   // back to them: the copy is then made on demand)
   const size_t pbytes = size_t(t->pdims[0]) * t->pdims[1] * t->pdims[2] * sizeof(T);

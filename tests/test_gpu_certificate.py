@@ -199,3 +199,32 @@ def test_signed_members_refined_maxima(P, prec, tol, cap, monkeypatch):
         assert abs(rec.value - v) <= tol * abs(val), (c, rec.value, v)
         assert abs(rec.value - drec.value) <= tol * abs(val), (c, rec.value, drec.value)
         assert tuple(rec.pos) == tuple(pos), (c, tuple(rec.pos), pos)
+
+
+@pytest.mark.parametrize("dims", [(70, 24, 40), (33, 20, 16), (64, 30, 30)])
+def test_eta_f32_fused_xmix_matches_separate_passes(P, dims, monkeypatch):
+    """The fused x pass + member mix (xmix_kernel, fp32, inner plane a multiple
+    of 32) and the separate x pass + mix kernel run the same FMA chains: the
+    fields agree to fp32 rounding of the final division and the per-candidate
+    maxima are identical; (64, 30, 30) takes the unfused path in both runs."""
+    import torch
+    rng = np.random.default_rng(21)
+    r = rng.standard_normal(dims)
+    kernel = O.box_gaussian_psf(dims, (1.5, 1.5, 1.5), (4, 4, 4))
+    psf = P.Psf(P.Volume(kernel), normalize=False)
+    sg, dg = np.array([1.0, 1.8, 2.6]), np.array([1.5, 2.0, 2.5])
+    win = ((2, dims[0] - 3), (1, dims[1] - 2), (0, dims[2] - 1))
+    out = {}
+    with P.precision("f32"):
+        table = P.build_template_table(psf, sg, dg, tap_tol=1e-12)
+        rd = torch.tensor(r, device="cuda", dtype=torch.float32)
+        for flag in ("1", "0"):  # fused (opt-in) vs separate
+            monkeypatch.setenv("SFW3D_XMIX", flag)
+            best, recs, _ = P.certificate.eta_argmax_dev(rd, 0.7, table, win)
+            f = P.eta_field(P.Volume(r), 0.7, table, keep_fields=True)
+            out[flag] = (best, recs, np.stack([v.data for v in f.fields]))
+    (b1, r1, f1), (b0, r0, f0) = out["1"], out["0"]
+    assert np.max(np.abs(f1 - f0)) <= 1e-6 * np.max(np.abs(f0))
+    assert b1.value == b0.value and tuple(b1.pos) == tuple(b0.pos)
+    for a, c in zip(r1, r0):
+        assert abs(a.value - c.value) <= 1e-6 * abs(b0.value) and tuple(a.pos) == tuple(c.pos)
