@@ -1352,6 +1352,173 @@ __global__ void __launch_bounds__(kXW * 32, 1) xmix_kernel(
   }
 }
 
+// Evaluation-pass mix with a per-thread cp.async ring (same CTA chunking,
+// FMA order and per-CTA maxima as mix_argmax_kernel, so its COLLECT pass
+// revisits these chunks). Each thread streams its own 16-byte vector of b and
+// of every T_k through kMixNS shared-memory slots (no barriers: a thread only
+// reads what it copied), keeping kMixNS - 1 loads in flight across term and
+// vector boundaries — the flattened (vector, term) sequence never drains.
+constexpr int kMixNS = 8;
+
+template <typename T, int NM>
+__global__ void __launch_bounds__(kMixThreads, sizeof(T) == 4 ? 2 : 1) mix_ring_kernel(
+    const T* __restrict__ b, const T* __restrict__ terms, long long n, int K, int nm, int m0,
+    const T* __restrict__ W, const T* __restrict__ w0, const int* __restrict__ cid, int nx, int ny,
+    int nz, int4 wlo, int4 whi, double lam, T* __restrict__ fields, Best* __restrict__ partial) {
+  constexpr int V = 16 / sizeof(T);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* ring = reinterpret_cast<T*>(smem_raw);            // [kMixNS][kMixThreads][V]
+  T* sW = ring + kMixNS * kMixThreads * V;             // [K][NM]
+  T* sw0 = sW + K * NM;
+  __shared__ Best red[NM][kMixThreads / 32];
+  for (int e = threadIdx.x; e < K * NM; e += kMixThreads) {
+    const int k = e / NM, m = e % NM;
+    sW[e] = m < nm ? W[size_t(m0 + m) * K + k] : T(0);
+  }
+  for (int e = threadIdx.x; e < NM; e += kMixThreads) sw0[e] = e < nm ? w0[m0 + e] : T(0);
+  __syncthreads();
+  const long long nv = n / V;
+  const long long chunk =
+      ((nv + gridDim.x - 1) / gridDim.x + kMixThreads - 1) / kMixThreads * kMixThreads;
+  const long long qbeg = blockIdx.x * chunk + threadIdx.x, qend = min(nv, (blockIdx.x + 1) * chunk);
+  const int iters = qbeg < qend ? int((qend - qbeg + kMixThreads - 1) / kMixThreads) : 0;
+  const int E = K + 1;  // sequence entries per vector: b, then T_0 .. T_{K-1}
+  const int G = iters * E;
+  T* myslot = ring + threadIdx.x * V;
+  constexpr int kSlot = kMixThreads * V;  // elements between consecutive slots
+  // producer: entry pointer (b, then T_0 .. T_{K-1} of the same vector, then
+  // the next vector's b), ring slot pg & (kMixNS - 1). Byte steps between
+  // consecutive entries: b -> T_0, T_k -> T_{k+1}, T_{K-1} -> next b.
+  const char* pptr = reinterpret_cast<const char*>(b + qbeg * V);
+  const long long d_b = reinterpret_cast<const char*>(terms) - reinterpret_cast<const char*>(b);
+  const long long d_t = (long long)n * sizeof(T);
+  const long long d_w = -d_b - (long long)(K - 1) * d_t + (long long)kMixThreads * V * sizeof(T);
+  const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(myslot));
+  int pe = 0;
+  unsigned pg = 0;
+  auto issue = [&]() {
+    const unsigned sa = sbase + (pg & (kMixNS - 1)) * (kSlot * sizeof(T));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(pptr));
+    ++pg;
+    pptr += pe == 0 ? d_b : (pe == K ? d_w : d_t);
+    pe = pe == K ? 0 : pe + 1;
+  };
+  static_assert((kMixNS & (kMixNS - 1)) == 0, "ring depth is a power of two");
+#pragma unroll
+  for (int g = 0; g < kMixNS - 1; ++g) {
+    if (g < G) issue();
+    cp_async_commit();
+  }
+  // running per-thread maxima live in shared memory (read once per vector,
+  // written only on improvement): keeps the accumulators and the producer
+  // state in registers at 2 CTAs per SM
+  T* sbv = sw0 + NM;                                        // [NM][kMixThreads]
+  int* sbi = reinterpret_cast<int*>(sbv + NM * kMixThreads);  // [NM][kMixThreads]
+#pragma unroll
+  for (int m = 0; m < NM; ++m) {
+    sbv[m * kMixThreads + threadIdx.x] = T(-INFINITY);
+    sbi[m * kMixThreads + threadIdx.x] = 0x7fffffff;
+  }
+  unsigned g = 0;
+  auto take = [&](T (&v)[V]) {
+    cp_async_wait_group<kMixNS - 2>();
+    const T* sl = myslot + (g & (kMixNS - 1)) * kSlot;
+    if constexpr (sizeof(T) == 4) {
+      const float4 q = *reinterpret_cast<const float4*>(sl);
+      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
+      const double2 q = *reinterpret_cast<const double2*>(sl);
+      v[0] = q.x; v[1] = q.y;
+    }
+    if (g + kMixNS - 1 < G) issue();
+    cp_async_commit();
+    ++g;
+  };
+  for (int it = 0; it < iters; ++it) {
+    const long long i0 = (qbeg + (long long)it * kMixThreads) * V;
+    T acc[NM][V];
+    {
+      T v[V];
+      take(v);
+#pragma unroll
+      for (int m = 0; m < NM; ++m)
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[m][j] = sw0[m] * v[j];
+    }
+    for (int k = 0; k < K; ++k) {
+      T v[V];
+      take(v);
+      const T* wk = sW + k * NM;
+#pragma unroll
+      for (int m = 0; m < NM; ++m) {
+        const T w = wk[m];
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[m][j] = fma(w, v[j], acc[m][j]);
+      }
+    }
+    // the V voxels share one (x, y) row (nz % V == 0)
+    const int z0 = int(i0 % nz);
+    const long long row = i0 / nz;
+    const int y = int(row % ny), x = int(row / ny);
+    const bool row_win = x >= wlo.x && x <= whi.x && y >= wlo.y && y <= whi.y;
+#pragma unroll
+    for (int m = 0; m < NM; ++m) {
+      if (m >= nm) break;
+      if (fields) {
+        T f[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) f[j] = T(double(acc[m][j]) / lam);
+        T* dst = fields + (long long)cid[m0 + m] * n + i0;
+        if constexpr (sizeof(T) == 4)
+          __stcs(reinterpret_cast<float4*>(dst), make_float4(f[0], f[1], f[2], f[3]));
+        else
+          __stcs(reinterpret_cast<double2*>(dst), make_double2(f[0], f[1]));
+      }
+      if (row_win) {
+        const T cur = sbv[m * kMixThreads + threadIdx.x];
+        T bv = cur;
+        int bj = -1;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          const int z = z0 + j;
+          // ascending i within the thread: strict '>' keeps the first maximum
+          if (z >= wlo.z && z <= whi.z && acc[m][j] > bv) {
+            bv = acc[m][j];
+            bj = j;
+          }
+        }
+        if (bj >= 0) {
+          sbv[m * kMixThreads + threadIdx.x] = bv;
+          sbi[m * kMixThreads + threadIdx.x] = int(i0 + bj);
+        }
+      }
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int m = 0; m < NM; ++m) {
+    if (m >= nm) break;
+    const int bi = sbi[m * kMixThreads + threadIdx.x];
+    Best bm = {bi == 0x7fffffff ? -INFINITY : double(sbv[m * kMixThreads + threadIdx.x]) / lam,
+               bi == 0x7fffffff ? 0x7fffffffffffffffLL : (long long)bi};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bm.v, o);
+      const long long oi = __shfl_xor_sync(0xffffffffu, bm.idx, o);
+      if (better(ov, oi, bm.v, bm.idx)) bm = {ov, oi};
+    }
+    if (lane == 0) red[m][warp] = bm;
+  }
+  __syncthreads();
+  if (threadIdx.x < nm) {
+    Best bm = red[threadIdx.x][0];
+    for (int w = 1; w < kMixThreads / 32; ++w)
+      if (better(red[threadIdx.x][w].v, red[threadIdx.x][w].idx, bm.v, bm.idx))
+        bm = red[threadIdx.x][w];
+    partial[(long long)(m0 + threadIdx.x) * gridDim.x + blockIdx.x] = bm;
+  }
+}
+
 __global__ void member_reduce_kernel(const Best* __restrict__ partial, int nblocks,
                                      const int* __restrict__ cid, Best* __restrict__ best_dev) {
   __shared__ Best sb[32];
@@ -1451,6 +1618,18 @@ static int launch_mix(sfw3d_ctx* ctx, int nblocks, const void* b, const void* te
                       int4 whi, double lam, void* fields, Best* partial, const Collect* col) {
   constexpr int V4 = 16 / sizeof(T);  // 4 floats / 2 doubles
   const int nz = dims[2];
+  if (!col && nz % V4 == 0 && nmm <= 16 && !getenv("SFW3D_MIX_V1")) {
+    const size_t smem = (size_t(kMixNS) * kMixThreads * V4 + size_t(nt) * 16 + 16 + 16 * kMixThreads) * sizeof(T) +
+                        16 * kMixThreads * sizeof(int);
+    if (smem > 48 * 1024)
+      SFW3D_CUDA_TRY(cudaFuncSetAttribute(mix_ring_kernel<T, 16>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    mix_ring_kernel<T, 16><<<nblocks, kMixThreads, smem, ctx->stream>>>(
+        static_cast<const T*>(b), static_cast<const T*>(terms), n, nt, nmm, m0,
+        static_cast<const T*>(s->W_dev), static_cast<const T*>(s->w0_dev), s->cid_dev, dims[0],
+        dims[1], dims[2], wlo, whi, lam, static_cast<T*>(fields), partial);
+    return SFW3D_OK;
+  }
 #define SFW3D_MIX(NM, V)                                                                        \
   return launch_mix_nm<T, NM, V>(ctx, nblocks, b, terms, n, nt, nmm, m0, s, dims, wlo, whi, lam, \
                                  fields, partial, col)
