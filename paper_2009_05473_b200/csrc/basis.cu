@@ -1618,7 +1618,13 @@ static int launch_mix(sfw3d_ctx* ctx, int nblocks, const void* b, const void* te
                       int4 whi, double lam, void* fields, Best* partial, const Collect* col) {
   constexpr int V4 = 16 / sizeof(T);  // 4 floats / 2 doubles
   const int nz = dims[2];
-  if (!col && nz % V4 == 0 && nmm <= 16 && !getenv("SFW3D_MIX_V1")) {
+  const bool ring = nz % V4 == 0 && nmm <= 16 && !getenv("SFW3D_MIX_V1");
+  // the collect pass must chunk the volume exactly as the evaluation pass did
+  // (it revisits evaluation CTAs by their maxima): same V as the ring kernel
+  if (col && ring)
+    return launch_mix_nm<T, 16, V4>(ctx, nblocks, b, terms, n, nt, nmm, m0, s, dims, wlo, whi,
+                                    lam, fields, partial, col);
+  if (!col && ring) {
     const size_t smem = (size_t(kMixNS) * kMixThreads * V4 + size_t(nt) * 16 + 16 + 16 * kMixThreads) * sizeof(T) +
                         16 * kMixThreads * sizeof(int);
     if (smem > 48 * 1024)

@@ -72,7 +72,10 @@ class Volume:
         key = (str(device), dtype)
         t = self._dev.get(key)
         if t is None:
-            host = torch.from_numpy(self._data)
+            import warnings
+            with warnings.catch_warnings():  # read-only source: only read (pinned copy below)
+                warnings.simplefilter("ignore", UserWarning)
+                host = torch.from_numpy(self._data)
             if dtype != torch.float64:
                 host = host.to(dtype)
             t = host.pin_memory().to(device, non_blocking=True)
