@@ -143,7 +143,15 @@ __global__ void __launch_bounds__(NT) pass_tiled_kernel(
     const int a1 = a0 + ag * J;
     const long long o0 = base0 + (long long)a1 * stride + il;
     T* po = out + o0;
-    if (addend) {
+    if (!addend && a1 + J <= n_axis) {  // full group: unguarded stores
+      if (w == T(1)) {
+#pragma unroll
+        for (int j = 0; j < J; ++j, po += stride) *po = acc[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < J; ++j, po += stride) *po = T(w * acc[j]);
+      }
+    } else if (addend) {
       const T* pa = addend + o0;
 #pragma unroll
       for (int j = 0; j < J; ++j, po += stride, pa += stride)
@@ -261,7 +269,12 @@ __global__ void __launch_bounds__(NT, MINB) pass_tile2_kernel(
     if (a < 0) a += n_axis;
     const T* src = in + base0 + c;
     T* dst = tile + r * TI + c;
-    if (n_axis >= dr) {  // at most one wrap per step
+    if (a0 + lo >= 0 && a0 + lo + rows <= n_axis) {
+      // no wrap anywhere in the tile (interior CTAs): one pointer bump per row
+      const long long step = (long long)dr * stride;
+      const T* p = src + (long long)a * stride;
+      for (; r < rows; r += dr, dst += dr * TI, p += step) cp_async16(dst, p);
+    } else if (n_axis >= dr) {  // at most one wrap per step
       for (; r < rows; r += dr, dst += dr * TI) {
         cp_async16(dst, src + (long long)a * stride);
         a += dr;
@@ -315,7 +328,15 @@ __global__ void __launch_bounds__(NT, MINB) pass_tile2_kernel(
     const int a1 = a0 + ag * J;
     const long long o0 = base0 + (long long)a1 * stride + il;
     T* po = out + o0;
-    if (addend) {
+    if (!addend && a1 + J <= n_axis) {  // full group: unguarded stores
+      if (w == T(1)) {
+#pragma unroll
+        for (int j = 0; j < J; ++j, po += stride) *po = acc[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < J; ++j, po += stride) *po = T(w * acc[j]);
+      }
+    } else if (addend) {
       const T* pa = addend + o0;
 #pragma unroll
       for (int j = 0; j < J; ++j, po += stride, pa += stride)
@@ -357,6 +378,18 @@ __global__ void __launch_bounds__(128, MINB) pass_z2_kernel(
     if (zs < 0) zs += nz;
     // lanes over 16-byte vectors of a row (wrapped column per lane is fixed
     // across rows), warps over rows
+    if (row0 + 32 <= nrows) {
+      // full row group: one wrap test per vector, one pointer bump per row
+      const long long step = 4LL * nz;
+      for (int v = lane; v < nv; v += 32) {
+        int z = zs + v * kVec;
+        if (z >= nz) z = z < 2 * nz ? z - nz : z % nz;
+        const T* p = in + (row0 + warp) * nz + z;
+        T* d = tile + warp * pitch + v * kVec;
+#pragma unroll
+        for (int i = 0; i < 8; ++i, p += step, d += 4 * pitch) cp_async16(d, p);
+      }
+    } else
     for (int v = lane; v < nv; v += 32) {
       int z = (zs + v * kVec) % nz;
       for (int r = warp; r < 32; r += 4) {
@@ -386,6 +419,19 @@ __global__ void __launch_bounds__(128, MINB) pass_z2_kernel(
     // same thread's consecutive stores)
     if (row < nrows) {
       T* po = out + row * nz + zc;
+#pragma unroll
+      if (w == T(1) && zc + J <= nz) {
+#pragma unroll
+        for (int j = 0; j < J; j += 4) {
+          if constexpr (sizeof(T) == 4) {
+            __stcs(reinterpret_cast<float4*>(po + j), make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]));
+          } else {
+            __stcs(reinterpret_cast<double2*>(po + j), make_double2(acc[j], acc[j + 1]));
+            __stcs(reinterpret_cast<double2*>(po + j + 2), make_double2(acc[j + 2], acc[j + 3]));
+          }
+        }
+        return;
+      }
 #pragma unroll
       for (int j = 0; j < J; j += 4) {
         if (zc + j >= nz) break;
