@@ -34,7 +34,11 @@ struct BasisSet;
 // on_device = false fits on the host only (no device buffers; eval unusable);
 // prune = greedily drop shared terms while every member stays within tol.
 int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands, int dtype,
-                    double tol, BasisSet** out, bool on_device = true, bool prune = false);
+                    double tol, BasisSet** out, bool on_device = true, bool prune = false,
+                    double loose = 0.0);
+// storage-dependent looser selection tolerance for the shared terms (fp32:
+// SFW3D_BASIS_LOOSE, default below; fp64: none)
+double basis_loose_tol(int dtype);
 // host copy of the fit: betas[n_terms], weights[n_cand][max_terms] (member rows,
 // zero elsewhere), w0[n_cand], fit_err[n_cand], member[n_cand]; NULLs skipped
 void basis_set_export(const BasisSet* s, int max_terms, int* n_terms, double* betas,

@@ -464,21 +464,27 @@ __global__ void abs_sum_kernel(const T* __restrict__ b, long long n, double* __r
   }
 }
 
-// one CTA per item: eta = sum_v G_c(v) b(m + v) / lam over the candidate's
-// box (periodic indexing), warps over template rows, lanes over taps
+// gridDim.y CTAs per item (blockIdx.y = contiguous share of the template
+// rows): partial sums of eta * lam = sum_v G_c(v) b(m + v) over the
+// candidate's box (periodic indexing), warps over template rows, lanes over
+// taps; refine_combine_kernel adds the shares in order (deterministic). The
+// split keeps the latency-bound row walk short for the wide boxes (up to
+// 171^2 rows).
 template <typename T>
 __global__ void __launch_bounds__(256) refine_kernel(const T* __restrict__ b, int nx, int ny,
                                                      int nz, const RefCand* __restrict__ rc,
                                                      const int* __restrict__ item_cand,
                                                      const long long* __restrict__ item_idx,
-                                                     double lam, double* __restrict__ out) {
+                                                     double* __restrict__ part) {
   __shared__ double red[8];
   const RefCand c = rc[item_cand[blockIdx.x]];
   const long long lin = item_idx[blockIdx.x];
   const int z = int(lin % nz), y = int((lin / nz) % ny), x = int(lin / ((long long)ny * nz));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nrows = c.la * c.lb, S = int(gridDim.y);
+  const int r0 = int((long long)nrows * blockIdx.y / S), r1 = int((long long)nrows * (blockIdx.y + 1) / S);
   double acc = 0.0;
-  for (int r = warp; r < c.la * c.lb; r += 8) {
+  for (int r = r0 + warp; r < r1; r += 8) {
     const int2 rr = c.rows[r];
     if (rr.y <= 0) continue;
     const int ai = r / c.lb, bi = r - ai * c.lb;
@@ -501,8 +507,17 @@ __global__ void __launch_bounds__(256) refine_kernel(const T* __restrict__ b, in
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int w = 0; w < 8; ++w) t += red[w];
-    out[blockIdx.x] = t / lam;
+    part[(long long)blockIdx.x * S + blockIdx.y] = t;
   }
+}
+
+__global__ void refine_combine_kernel(const double* __restrict__ part, int S, int count,
+                                      double lam, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  double t = 0.0;
+  for (int s = 0; s < S; ++s) t += part[(long long)i * S + s];
+  out[i] = t / lam;
 }
 
 int round_up(int v, int m) { return (v + m - 1) / m * m; }
@@ -621,7 +636,7 @@ static int ensure_basis(const sfw3d_table* t, int dtype) {
   SFW3D_CUDA_TRY(cudaSetDevice(t->device));
   BasisSet* built = nullptr;
   const int st = basis_set_build(t->dims, t->bcands, dtype, tol, &built, true,
-                                 basis_prune_rule(t->dims));
+                                 basis_prune_rule(t->dims), basis_loose_tol(dtype));
   cudaSetDevice(dev);
   if (st != SFW3D_OK) {
     basis_set_destroy(built);
@@ -759,7 +774,8 @@ extern "C" int sfw3d_basis_set_fit(const int32_t dims[3], int n_sigma, const dou
       bc.push_back(c);
     }
   BasisSet* s = nullptr;
-  const int st = basis_set_build(dm, bc, dtype, tol, &s, /*on_device=*/false, basis_prune_rule(dm));
+  const int st = basis_set_build(dm, bc, dtype, tol, &s, /*on_device=*/false, basis_prune_rule(dm),
+                                 basis_loose_tol(dtype));
   if (st == SFW3D_OK)
     basis_set_export(s, max_terms, n_terms, betas, weights, w0, fit_err, member);
   basis_set_destroy(s);
@@ -947,7 +963,10 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   const int nxp = ow[1] - ow[0] + 1;
   const long long nblocks_direct = (long long)nty * ntz * nxp;
   const long long nblocks = nblocks_direct;
-  const size_t rb = any_refine ? size_t(kRefCap) * (4 + 8 + 8) + size_t(nc) * 12 + 352 : 0;
+  const int kRefPart = std::max(kRefCap, 4096);  // per-share partial sums
+  const size_t rb = any_refine ? size_t(kRefCap) * (4 + 8 + 8) + size_t(kRefPart) * 8 +
+                                     size_t(nc) * 12 + 352
+                               : 0;
   // folded kernel slice sums in global memory (tuning variant)
   size_t ab = 0;
   if (fold_accd_global(sizeof(T))) {
@@ -969,6 +988,7 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   int* ref_cand = any_refine ? cv.take<int>(kRefCap) : nullptr;
   long long* ref_idx = any_refine ? cv.take<long long>(kRefCap) : nullptr;
   double* ref_val = any_refine ? cv.take<double>(kRefCap) : nullptr;
+  double* ref_part = any_refine ? cv.take<double>(kRefPart) : nullptr;
   double* ref_thr = any_refine ? cv.take<double>(nc) : nullptr;
   double* ref_l1 = any_refine ? cv.take<double>(2) : nullptr;  // [sum |b|, max |b| bits]
   int* ref_count = any_refine ? cv.take<int>(1 + nc) : nullptr;  // [total, per member]
@@ -1071,9 +1091,14 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
       count = 0;
     } else if (count > 0) {
       SFW3D_PROF(ctx, "eta_refine");
-      refine_kernel<T><<<count, 256, 0, ctx->stream>>>(
+      // shares per item: ~4096 CTAs in all, at most 64 per item
+      const int S = std::max(1, std::min(64, kRefPart / count));
+      refine_kernel<T><<<dim3(unsigned(count), unsigned(S)), 256, 0, ctx->stream>>>(
           b, dims[0], dims[1], dims[2], static_cast<const RefCand*>(t->refcand_dev), ref_cand,
-          ref_idx, lam, ref_val);
+          ref_idx, ref_part);
+      SFW3D_LAUNCH_CHECK(ctx);
+      refine_combine_kernel<<<(count + 255) / 256, 256, 0, ctx->stream>>>(ref_part, S, count, lam,
+                                                                          ref_val);
       SFW3D_LAUNCH_CHECK(ctx);
       std::vector<int> hc(count);
       std::vector<long long> hi(count);
