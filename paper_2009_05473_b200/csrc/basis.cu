@@ -271,7 +271,14 @@ struct BasisSet {
   int dtype;
   int lo[3], hi[3];                 // common offset box
   std::vector<double> betas;        // shared terms
-  std::vector<int> tlo[3], tlen[3];  // per term, per axis tap range
+  std::vector<int> tlo[3], tlen[3];  // per term, per axis tap range (of the passes)
+  // chained terms (fp32): T_t = (g_t x g_t x g_t) * T_parent[t] instead of
+  // f_t^3 * b, with g_t the Gaussian whose convolution with the parent's
+  // factor is f_t (variances add); parent -1 = from b. The effective factor
+  // (parent's effective factor convolved with g_t, as the passes compute it)
+  // on [elo, elo + elen) per axis is what the signed bounds use.
+  std::vector<int> parent;
+  std::vector<int> elo[3], elen[3];
   std::vector<void*> taps;          // per term: 3 axes contiguous, storage dtype
   std::vector<int> members;         // candidate ids on the basis path
   std::vector<double> W, w0;        // [member][term], [member]
@@ -327,30 +334,39 @@ double env_double(const char* name, double def) {
 
 void fit_signed_members(BasisSet* s, const std::vector<BasisCandidate>& cands, int dtype,
                         const std::vector<double>& Sfit,
-                        const std::vector<std::vector<double>>& hstore) {
+                        const std::vector<std::vector<double>>& hstore,
+                        const std::vector<double>& pass_taps) {
   if (env_double("SFW3D_SIGNED", 1.0) == 0.0) return;
   const int nc = int(cands.size()), nt = int(s->betas.size());
   const double u = dtype == SFW3D_F64 ? 0x1p-53 : 0x1p-24;
   const double accept = env_double("SFW3D_SIGNED_ACCEPT", 0.01);
   const bool debug = env_double("SFW3D_SIGNED_DEBUG", 0.0) != 0.0;
-  // per term: factor mass over C and the three passes' rounding factor
-  std::vector<double> Sk(nt), rho(nt);
+  // per term: (effective) factor mass, its part outside the common box C
+  // (chained factors may reach past C, where every template is 0), and the
+  // passes' rounding factor (a chained term adds its own passes' rounding
+  // to its parent's, relative to the same mass)
+  std::vector<double> Sk(nt), rho(nt), ext(nt);
   std::vector<size_t> aoff[3];
   for (int a = 0; a < 3; ++a) aoff[a].resize(nt);
-  for (int t = 0; t < nt; ++t) {
-    double prod = 1.0;
-    int L = 0;
+  for (int t = nt - 1; t >= 0; --t) {  // parents (narrower) have larger indices
+    double prod = 1.0, pin = 1.0;
     size_t off = 0;
     for (int a = 0; a < 3; ++a) {
       aoff[a][t] = off;
-      double sa = 0.0;
-      for (int q = 0; q < s->tlen[a][t]; ++q) sa += std::fabs(hstore[t][off + q]);
-      off += s->tlen[a][t];
+      double sa = 0.0, si = 0.0;
+      for (int q = 0; q < s->elen[a][t]; ++q) {
+        const double v = std::fabs(hstore[t][off + q]);
+        sa += v;
+        const int o = s->elo[a][t] + q;
+        if (o >= s->lo[a] && o <= s->hi[a]) si += v;
+      }
+      off += s->elen[a][t];
       prod *= sa;
-      L += s->tlen[a][t];
+      pin *= si;
     }
     Sk[t] = prod;
-    rho[t] = 1.01 * u * L;
+    ext[t] = std::max(0.0, prod - pin);
+    rho[t] = 1.01 * u * pass_taps[t] + (s->parent[t] >= 0 ? rho[s->parent[t]] * (1.0 + 1.01 * u * pass_taps[t]) : 0.0);
   }
   const double gmix = 1.01 * u * (nt + 2);
   // axis representatives: offsets +t and -t share one (multiplicity 2) when
@@ -363,7 +379,7 @@ void fit_signed_members(BasisSet* s, const std::vector<BasisCandidate>& cands, i
   std::vector<std::vector<double>> fval[3];  // [a][rep][term]
   for (int a = 0; a < 3; ++a) {
     const int lo = s->lo[a], hi = s->hi[a];
-    auto in_term = [&](int t, int k) { return t >= s->tlo[a][k] && t < s->tlo[a][k] + s->tlen[a][k]; };
+    auto in_term = [&](int t, int k) { return t >= s->elo[a][k] && t < s->elo[a][k] + s->elen[a][k]; };
     for (int t = 0; t <= std::max(-lo, hi); ++t) {
       const bool pos = t >= lo && t <= hi, neg = t > 0 && -t >= lo && -t <= hi;
       bool same = pos && neg;
@@ -378,7 +394,7 @@ void fit_signed_members(BasisSet* s, const std::vector<BasisCandidate>& cands, i
     for (const Rep& r : reps[a]) {
       std::vector<double> f(nt, 0.0);
       for (int k = 0; k < nt; ++k)
-        if (in_term(r.t, k)) f[k] = hstore[k][aoff[a][k] + (r.t - s->tlo[a][k])];
+        if (in_term(r.t, k)) f[k] = hstore[k][aoff[a][k] + (r.t - s->elo[a][k])];
       fval[a].push_back(std::move(f));
     }
   }
@@ -404,7 +420,7 @@ void fit_signed_members(BasisSet* s, const std::vector<BasisCandidate>& cands, i
       A[size_t(nt) * Mt + i] = Sfit[i] == 0.0 ? 1.0L : 0.0L;
     }
     std::vector<double> pen(ncol);
-    for (int k = 0; k < nt; ++k) pen[k] = Sk[k] * (rho[k] + gmix * (1.0 + rho[k]));
+    for (int k = 0; k < nt; ++k) pen[k] = Sk[k] * (rho[k] + gmix * (1.0 + rho[k])) + ext[k];
     pen[nt] = gmix;
     std::vector<int> cols(ncol);
     for (int k = 0; k < ncol; ++k) cols[k] = k;
@@ -728,24 +744,97 @@ int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands,
   for (int a = 0; a < 3; ++a) {
     s->tlo[a].resize(nt);
     s->tlen[a].resize(nt);
+    s->elo[a].resize(nt);
+    s->elen[a].resize(nt);
+  }
+  s->parent.assign(nt, -1);
+  for (int t = 0; t < nt; ++t) s->betas.push_back(dict[kmap[t]]);
+  const double lneps = std::log(1.0 / eps);
+  auto radius = [&](double beta) { return int(std::ceil(std::sqrt(lneps / beta))); };
+  // Chains (fp32 storage, not with the fused x pass): a term whose factor is
+  // not clipped by C takes the narrower term p that minimises the taps of
+  // g = exp(-beta_g q^2) with 1/beta = 1/beta_p + 1/beta_g, when that saves
+  // passes taps and the lattice convolution of the two sampled Gaussians is a
+  // sampled Gaussian to ~1e-9 (Poisson ripple exp(-pi^2 / (beta_p + beta_g))).
+  // The bounds below use the effective factors, so the choice never costs
+  // certification, only fit quality at the ripple level.
+  const bool chains = dtype == SFW3D_F32 && env_double("SFW3D_CHAIN", 1.0) != 0.0 &&
+                      !(getenv("SFW3D_XMIX") && atoi(getenv("SFW3D_XMIX")) == 1);
+  std::vector<double> gbeta(nt, 0.0);
+  if (chains) {
+    int rbox = 1 << 30;
+    for (int a = 0; a < 3; ++a) rbox = std::min({rbox, -s->lo[a], s->hi[a]});
+    const double kRipple = 0.45;  // beta_p + beta_g: exp(-pi^2 / 0.45) = 3e-10
+    for (int t = 0; t < nt; ++t) {
+      const double bt = s->betas[t];
+      const int rt = radius(bt);
+      if (rt > rbox) continue;
+      int best = -1, rb_best = rt - 3;  // worth a chain: >= 6 fewer taps per axis
+      double gb_best = 0.0;
+      for (int p = t + 1; p < nt; ++p) {
+        const double bp = s->betas[p];
+        if (!(bp > bt * (1.0 + 1e-9))) continue;
+        const double bg = bp * bt / (bp - bt);
+        if (bp + bg > kRipple) continue;
+        const int rg = radius(bg);
+        if (rg < rb_best) {
+          rb_best = rg;
+          best = p;
+          gb_best = bg;
+        }
+      }
+      if (best >= 0) {
+        s->parent[t] = best;
+        gbeta[t] = gb_best;
+      }
+    }
   }
   // stored factor values (rounded to the storage precision) per term, axes
-  // 0, 1, 2 contiguous: what the passes multiply by
-  std::vector<std::vector<double>> hstore(nt);
-  for (int t = 0; t < nt; ++t) {
-    const double beta = dict[kmap[t]];
-    s->betas.push_back(beta);
-    const int r = int(std::ceil(std::sqrt(std::log(1.0 / eps) / beta)));
+  // 0, 1, 2 contiguous: what the passes multiply by; heff: effective factors
+  std::vector<std::vector<double>> hstore(nt), heff(nt);
+  std::vector<double> pass_taps(nt, 0.0);
+  for (int t = nt - 1; t >= 0; --t) {  // parents first (larger beta, larger index)
+    const double beta = s->betas[t];
     std::vector<double>& h = hstore[t];
+    const int p = s->parent[t];
     for (int a = 0; a < 3; ++a) {
-      s->tlo[a][t] = std::max(s->lo[a], -r);
-      s->tlen[a][t] = std::min(s->hi[a], r) - s->tlo[a][t] + 1;
-      for (int q = s->tlo[a][t]; q < s->tlo[a][t] + s->tlen[a][t]; ++q) {
-        const double v = std::exp(-beta * double(q) * q);
-        h.push_back(dtype == SFW3D_F64 ? v : double(float(v)));
+      if (p < 0) {
+        const int r = radius(beta);
+        s->tlo[a][t] = std::max(s->lo[a], -r);
+        s->tlen[a][t] = std::min(s->hi[a], r) - s->tlo[a][t] + 1;
+        for (int q = s->tlo[a][t]; q < s->tlo[a][t] + s->tlen[a][t]; ++q) {
+          const double v = std::exp(-beta * double(q) * q);
+          h.push_back(dtype == SFW3D_F64 ? v : double(float(v)));
+        }
+        s->elo[a][t] = s->tlo[a][t];
+        s->elen[a][t] = s->tlen[a][t];
+        heff[t].insert(heff[t].end(), h.end() - s->tlen[a][t], h.end());
+      } else {
+        const double bg = gbeta[t], bp = s->betas[p];
+        const int r = radius(bg);
+        const double scale = std::sqrt((bp + bg) / M_PI);
+        s->tlo[a][t] = -r;
+        s->tlen[a][t] = 2 * r + 1;
+        std::vector<double> g;
+        for (int q = -r; q <= r; ++q) g.push_back(double(float(scale * std::exp(-bg * double(q) * q))));
+        h.insert(h.end(), g.begin(), g.end());
+        // effective factor: parent's effective factor (this axis) * g, exactly
+        size_t poff = 0;
+        for (int b2 = 0; b2 < a; ++b2) poff += s->elen[b2][p];
+        const int plo = s->elo[a][p], plen = s->elen[a][p];
+        s->elo[a][t] = plo - r;
+        s->elen[a][t] = plen + 2 * r;
+        std::vector<long double> e(size_t(s->elen[a][t]), 0.0L);
+        for (int i = 0; i < plen; ++i)
+          for (int j = 0; j <= 2 * r; ++j) e[size_t(i + j)] += (long double)heff[p][poff + i] * g[j];
+        for (long double v : e) heff[t].push_back(double(v));
       }
       s->taps_per_voxel += s->tlen[a][t];
+      pass_taps[t] += s->tlen[a][t];
     }
+  }
+  for (int t = 0; t < nt; ++t) {
+    const std::vector<double>& h = hstore[t];
     if (!on_device) continue;
     void* dev = nullptr;
     int st;
@@ -767,7 +856,7 @@ int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands,
   }
   s->n_nnls = nm;
   s->ebound.assign(nc, 0.0);
-  if (nt > 0) fit_signed_members(s, cands, dtype, Sfit, hstore);
+  if (nt > 0) fit_signed_members(s, cands, dtype, Sfit, heff, pass_taps);
   const int nmt = int(s->members.size());
   if (nmt && on_device) {
     if (dtype == SFW3D_F64) {
@@ -1734,11 +1823,13 @@ int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[
                             wlo, whi, lam, static_cast<float*>(fields), partial, nullptr));
     }
   } else {
-  // T_k = (f_k x f_k x f_k) * b for every shared term
-  for (int t = 0; t < nt; ++t) {
+  // T_k = (f_k x f_k x f_k) * b for every shared term; chained terms
+  // T_k = (g_k x g_k x g_k) * T_parent (parents: narrower, larger index)
+  for (int t = nt - 1; t >= 0; --t) {
     const char* tp = static_cast<const char*>(s->taps[t]);
     const int l0 = s->tlen[0][t], l1 = s->tlen[1][t], l2 = s->tlen[2][t];
-    SFW3D_TRY(corr_pass_impl(ctx, dtype, b, t1, dims, 2, tp + es * (l0 + l1), s->tlo[2][t], l2,
+    const void* src = s->parent[t] < 0 ? b : terms + size_t(s->parent[t]) * n * es;
+    SFW3D_TRY(corr_pass_impl(ctx, dtype, src, t1, dims, 2, tp + es * (l0 + l1), s->tlo[2][t], l2,
                              nullptr, 0.0, 1.0, "eta_basis"));
     SFW3D_TRY(corr_pass_impl(ctx, dtype, t1, t2, dims, 1, tp + es * l0, s->tlo[1][t], l1, nullptr,
                              0.0, 1.0, "eta_basis"));

@@ -562,10 +562,10 @@ int launch_z(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* ta
   return SFW3D_OK;
 }
 
-template <typename T, int J, int MINB = 1>
+template <typename T, int J, int MINB = 1, int NT = 256>
 int launch_tile2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis, const T* taps,
                  int lo, int ntaps, const T* addend, double aw, double w) {
-  constexpr int TI = 64, NT = 256, To = J * (NT / TI);
+  constexpr int TI = 64, To = J * (NT / TI);
   long long stride = 1;
   for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
   long long outer = 1;
@@ -663,6 +663,12 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
   long long stride = 1;
   for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
   if (v2 == 0 && stride % 64 == 0 && ntaps <= 512) {
+    static const int nt128 = [] {
+      const char* e = getenv("SFW3D_TILE2_NT");
+      return e ? atoi(e) == 128 : 0;
+    }();
+    if (nt128 && dims[axis] >= 128 && ntaps > narrow_taps())
+      return launch_tile2<T, 32, 5, 128>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
     if (dims[axis] >= 128 && ntaps > narrow_taps())
       return pass_occ(0) == 3
                  ? launch_tile2<T, 32, 3>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w)
