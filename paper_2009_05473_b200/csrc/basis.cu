@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstring>
 #include <thread>
+#include <type_traits>
 
 #include "basis.cuh"
 #include "window.cuh"
@@ -297,6 +298,14 @@ struct BasisSet {
   int max_nt4x = 0, xtaps_total = 0;
   long long taps_per_voxel = 0;
   int device = 0;
+  // mix_ring2_kernel: dense members (W rows [nmd][K], w0) and copy members
+  // (one weight-1 term, w0 = 0) with cterm[k] = copy slot of term k or -1
+  int nmd = 0, nmc = 0;
+  void* Wd_dev = nullptr;
+  void* w0d_dev = nullptr;
+  int* dmem_dev = nullptr;
+  int* cmem_dev = nullptr;
+  int* cterm_dev = nullptr;
 };
 
 // coarse dictionary size (the fine one has 2 * kDictCoarse - 1 points)
@@ -872,6 +881,45 @@ int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands,
     }
     SFW3D_TRY(upload(reinterpret_cast<void**>(&s->cid_dev), s->members.data(),
                      s->members.size() * sizeof(int)));
+    {
+      // dense / copy member split for mix_ring2_kernel
+      std::vector<int> dmem, cmem, cterm(nt, -1);
+      std::vector<double> Wd, w0d;
+      for (int m = 0; m < nmt; ++m) {
+        int nz = 0, k1 = -1;
+        for (int t = 0; t < nt; ++t)
+          if (s->W[size_t(m) * nt + t] != 0.0) {
+            ++nz;
+            k1 = t;
+          }
+        if (nz == 1 && s->W[size_t(m) * nt + k1] == 1.0 && s->w0[m] == 0.0 && cterm[k1] < 0 &&
+            int(cmem.size()) < 8) {
+          cterm[k1] = int(cmem.size());
+          cmem.push_back(m);
+        } else {
+          dmem.push_back(m);
+          Wd.insert(Wd.end(), s->W.begin() + size_t(m) * nt, s->W.begin() + size_t(m + 1) * nt);
+          w0d.push_back(s->w0[m]);
+        }
+      }
+      s->nmd = int(dmem.size());
+      s->nmc = int(cmem.size());
+      Wd.push_back(0.0);
+      w0d.push_back(0.0);
+      dmem.push_back(0);
+      cmem.push_back(0);
+      if (dtype == SFW3D_F64) {
+        SFW3D_TRY(upload(&s->Wd_dev, Wd.data(), Wd.size() * sizeof(double)));
+        SFW3D_TRY(upload(&s->w0d_dev, w0d.data(), w0d.size() * sizeof(double)));
+      } else {
+        std::vector<float> Wf(Wd.begin(), Wd.end()), w0f(w0d.begin(), w0d.end());
+        SFW3D_TRY(upload(&s->Wd_dev, Wf.data(), Wf.size() * sizeof(float)));
+        SFW3D_TRY(upload(&s->w0d_dev, w0f.data(), w0f.size() * sizeof(float)));
+      }
+      SFW3D_TRY(upload(reinterpret_cast<void**>(&s->dmem_dev), dmem.data(), dmem.size() * sizeof(int)));
+      SFW3D_TRY(upload(reinterpret_cast<void**>(&s->cmem_dev), cmem.data(), cmem.size() * sizeof(int)));
+      SFW3D_TRY(upload(reinterpret_cast<void**>(&s->cterm_dev), cterm.data(), cterm.size() * sizeof(int)));
+    }
     if (dtype == SFW3D_F32) {
       std::vector<float> xt;
       std::vector<int4> meta;
@@ -898,6 +946,9 @@ void basis_set_destroy(BasisSet* s) {
   if (s->cid_dev) cudaFree(s->cid_dev);
   if (s->xtaps_dev) cudaFree(s->xtaps_dev);
   if (s->xmeta_dev) cudaFree(s->xmeta_dev);
+  for (void* p : {s->Wd_dev, s->w0d_dev, static_cast<void*>(s->dmem_dev),
+                  static_cast<void*>(s->cmem_dev), static_cast<void*>(s->cterm_dev)})
+    if (p) cudaFree(p);
   delete s;
 }
 
@@ -1630,6 +1681,221 @@ __global__ void __launch_bounds__(kMixThreads, sizeof(T) == 4 ? 2 : 1) mix_ring_
   }
 }
 
+// Evaluation-pass mix, v2 of mix_ring_kernel (same CTA chunking, so the
+// collect pass revisits the same chunks): members split into DENSE members
+// (NMD accumulators per voxel, W from shared memory) and COPY members (the
+// exact d == 2 members: eta = T_k / lam for one term k, w0 = 0), which cost
+// no FMA — their running maxima are updated when their term streams by. The
+// producer walks the flattened (vector, entry) sequence through a table of
+// byte offsets; the running maxima take the max of the 4 voxels first and
+// do index work only on improvement (interior z).
+template <typename T, int NMD, int NS>
+__global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
+    const T* __restrict__ b, const T* __restrict__ terms, long long n, int K,
+    const T* __restrict__ Wd, const T* __restrict__ w0d, const int* __restrict__ dmem, int nmd,
+    const int* __restrict__ cterm, int nmc, const int* __restrict__ cmem,
+    const int* __restrict__ cid, int nx, int ny, int nz, int4 wlo, int4 whi, double lam,
+    T* __restrict__ fields, Best* __restrict__ partial) {
+  constexpr int V = 16 / sizeof(T);
+  constexpr int NMC = 8;  // copy members (at most)
+  static_assert((NS & (NS - 1)) == 0, "ring depth is a power of two");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* ring = reinterpret_cast<T*>(smem_raw);                       // [NS][threads][V]
+  T* sW = ring + NS * kMixThreads * V;                            // [K][NMD], 16-byte rows
+  T* sw0 = sW + K * NMD;                                          // [NMD]
+  T* sbv = sw0 + NMD;                                             // [NMD + NMC][threads]
+  int* sbi = reinterpret_cast<int*>(sbv + (NMD + NMC) * kMixThreads);
+  int* sCt = sbi + (NMD + NMC) * kMixThreads;                     // [K]: copy slot or -1
+  __shared__ Best red[NMD + NMC][kMixThreads / 32];
+  for (int e = threadIdx.x; e < K * NMD; e += kMixThreads) {
+    const int k = e / NMD, m = e % NMD;
+    sW[e] = m < nmd ? Wd[size_t(m) * K + k] : T(0);
+  }
+  for (int e = threadIdx.x; e < NMD; e += kMixThreads) sw0[e] = e < nmd ? w0d[e] : T(0);
+  for (int e = threadIdx.x; e < K; e += kMixThreads) sCt[e] = cterm[e];
+#pragma unroll
+  for (int m = 0; m < NMD + NMC; ++m) {
+    sbv[m * kMixThreads + threadIdx.x] = T(-INFINITY);
+    sbi[m * kMixThreads + threadIdx.x] = 0x7fffffff;
+  }
+  __syncthreads();
+  const long long nv = n / V;
+  const long long chunk =
+      ((nv + gridDim.x - 1) / gridDim.x + kMixThreads - 1) / kMixThreads * kMixThreads;
+  const long long qbeg = blockIdx.x * chunk + threadIdx.x, qend = min(nv, (blockIdx.x + 1) * chunk);
+  const int iters = qbeg < qend ? int((qend - qbeg + kMixThreads - 1) / kMixThreads) : 0;
+  const int E = K + 1;
+  const int G = iters * E;
+  T* myslot = ring + threadIdx.x * V;
+  constexpr int kSlot = kMixThreads * V;
+  // producer: entry pe of the vector stream (0 = b, 1 + k = T_k), running
+  // pointers into b and the terms, running ring-slot byte offsets
+  const char* bq = reinterpret_cast<const char*>(b + qbeg * V);
+  const char* tq = reinterpret_cast<const char*>(terms + qbeg * V);
+  const long long vstep = (long long)kMixThreads * V * sizeof(T);
+  const long long nstride = n * (long long)sizeof(T);
+  const long long twrap = vstep - (long long)K * nstride;
+  const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(myslot));
+  constexpr unsigned kSlotB = kSlot * sizeof(T), kRingB = NS * kSlotB;
+  int pe = 0, pleft = G;
+  unsigned poff = 0, coff = 0;
+  auto issue = [&]() {
+    const char* a = pe == 0 ? bq : tq;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + poff), "l"(a));
+    poff = poff + kSlotB == kRingB ? 0u : poff + kSlotB;
+    --pleft;
+    if (pe != 0) tq += nstride;
+    if (++pe == E) {
+      pe = 0;
+      bq += vstep;
+      tq += twrap;
+    }
+  };
+#pragma unroll
+  for (int g = 0; g < NS - 1; ++g) {
+    if (pleft > 0) issue();
+    cp_async_commit();
+  }
+  auto take = [&](T (&v)[V]) {
+    cp_async_wait_group<NS - 2>();
+    const T* sl = reinterpret_cast<const T*>(reinterpret_cast<const char*>(myslot) + coff);
+    if constexpr (sizeof(T) == 4) {
+      const float4 q = *reinterpret_cast<const float4*>(sl);
+      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
+      const double2 q = *reinterpret_cast<const double2*>(sl);
+      v[0] = q.x; v[1] = q.y;
+    }
+    coff = coff + kSlotB == kRingB ? 0u : coff + kSlotB;
+    if (pleft > 0) issue();
+    cp_async_commit();
+  };
+  // running maximum of member slot m over this vector's V voxels
+  auto track = [&](int m, const T (&a)[V], long long i0, bool zfull, int z0) {
+    T* pv = sbv + m * kMixThreads + threadIdx.x;
+    if (zfull) {
+      T mx = a[0];
+#pragma unroll
+      for (int j = 1; j < V; ++j) mx = max(mx, a[j]);
+      if (mx > *pv) {
+        int bj = V - 1;
+#pragma unroll
+        for (int j = V - 2; j >= 0; --j)
+          if (a[j] == mx) bj = j;
+        *pv = mx;
+        sbi[m * kMixThreads + threadIdx.x] = int(i0 + bj);
+      }
+    } else {
+      T bv = *pv;
+      int bj = -1;
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const int z = z0 + j;
+        if (z >= wlo.z && z <= whi.z && a[j] > bv) {
+          bv = a[j];
+          bj = j;
+        }
+      }
+      if (bj >= 0) {
+        *pv = bv;
+        sbi[m * kMixThreads + threadIdx.x] = int(i0 + bj);
+      }
+    }
+  };
+  for (int it = 0; it < iters; ++it) {
+    const long long i0 = (qbeg + (long long)it * kMixThreads) * V;
+    const int z0 = int(i0 % nz);
+    const long long row = i0 / nz;
+    const int y = int(row % ny), x = int(row / ny);
+    const bool row_win = x >= wlo.x && x <= whi.x && y >= wlo.y && y <= whi.y;
+    const bool zfull = z0 >= wlo.z && z0 + V - 1 <= whi.z;
+    T acc[NMD][V];
+    {
+      T v[V];
+      take(v);
+#pragma unroll
+      for (int m = 0; m < NMD; ++m)
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[m][j] = sw0[m] * v[j];
+    }
+    for (int k = 0; k < K; ++k) {
+      T v[V];
+      take(v);
+      const T* wk = sW + k * NMD;
+      T wv[NMD];
+#pragma unroll
+      for (int m = 0; m < NMD; m += 16 / sizeof(T)) {
+        if constexpr (sizeof(T) == 4) {
+          const float4 q = *reinterpret_cast<const float4*>(wk + m);
+          wv[m] = q.x; wv[m + 1] = q.y; wv[m + 2] = q.z; wv[m + 3] = q.w;
+        } else {
+          const double2 q = *reinterpret_cast<const double2*>(wk + m);
+          wv[m] = q.x; wv[m + 1] = q.y;
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < NMD; ++m)
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[m][j] = fma(wv[m], v[j], acc[m][j]);
+      const int c = sCt[k];
+      if (c >= 0) {  // a copy member's eta * lam is T_k itself
+        if (fields) {
+          T f[V];
+#pragma unroll
+          for (int j = 0; j < V; ++j) f[j] = T(double(v[j]) / lam);
+          T* dst = fields + (long long)cid[cmem[c]] * n + i0;
+          if constexpr (sizeof(T) == 4)
+            __stcs(reinterpret_cast<float4*>(dst), make_float4(f[0], f[1], f[2], f[3]));
+          else
+            __stcs(reinterpret_cast<double2*>(dst), make_double2(f[0], f[1]));
+        }
+        if (row_win) track(NMD + c, v, i0, zfull, z0);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < NMD; ++m) {
+      if (m >= nmd) break;
+      if (fields) {
+        T f[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) f[j] = T(double(acc[m][j]) / lam);
+        T* dst = fields + (long long)cid[dmem[m]] * n + i0;
+        if constexpr (sizeof(T) == 4)
+          __stcs(reinterpret_cast<float4*>(dst), make_float4(f[0], f[1], f[2], f[3]));
+        else
+          __stcs(reinterpret_cast<double2*>(dst), make_double2(f[0], f[1]));
+      }
+      if (row_win) track(m, acc[m], i0, zfull, z0);
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int m = 0; m < NMD + NMC; ++m) {
+    if (m < NMD ? m >= nmd : m - NMD >= nmc) continue;
+    const int bi = sbi[m * kMixThreads + threadIdx.x];
+    Best bm = {bi == 0x7fffffff ? -INFINITY : double(sbv[m * kMixThreads + threadIdx.x]) / lam,
+               bi == 0x7fffffff ? 0x7fffffffffffffffLL : (long long)bi};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bm.v, o);
+      const long long oi = __shfl_xor_sync(0xffffffffu, bm.idx, o);
+      if (better(ov, oi, bm.v, bm.idx)) bm = {ov, oi};
+    }
+    if (lane == 0) red[m][warp] = bm;
+  }
+  __syncthreads();
+  if (threadIdx.x < NMD + NMC) {
+    const int m = threadIdx.x;
+    if (m < NMD ? m < nmd : m - NMD < nmc) {
+      Best bm = red[m][0];
+      for (int w = 1; w < kMixThreads / 32; ++w)
+        if (better(red[m][w].v, red[m][w].idx, bm.v, bm.idx)) bm = red[m][w];
+      const int mem = m < NMD ? dmem[m] : cmem[m - NMD];  // member index
+      partial[(long long)mem * gridDim.x + blockIdx.x] = bm;
+    }
+  }
+}
+
 __global__ void member_reduce_kernel(const Best* __restrict__ partial, int nblocks,
                                      const int* __restrict__ cid, Best* __restrict__ best_dev) {
   __shared__ Best sb[32];
@@ -1721,6 +1987,25 @@ static int launch_mix_nm(sfw3d_ctx* ctx, int nblocks, const void* b, const void*
   return SFW3D_OK;
 }
 
+template <typename T, int NMD, int NS>
+static int launch_ring2(sfw3d_ctx* ctx, int nblocks, const void* b, const void* terms, long long n,
+                        int nt, const BasisSet* s, const int dims[3], int4 wlo, int4 whi,
+                        double lam, Best* partial) {
+  constexpr int V4 = 16 / sizeof(T);
+  const size_t smem = size_t(NS) * kMixThreads * V4 * sizeof(T) + size_t(nt + 1) * 8 +
+                      (size_t(nt) * NMD + NMD + size_t(NMD + 8) * kMixThreads) * sizeof(T) +
+                      size_t(NMD + 8) * kMixThreads * sizeof(int) + size_t(nt) * sizeof(int) + 16;
+  if (smem > 48 * 1024)
+    SFW3D_CUDA_TRY(cudaFuncSetAttribute(mix_ring2_kernel<T, NMD, NS>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  mix_ring2_kernel<T, NMD, NS><<<nblocks, kMixThreads, smem, ctx->stream>>>(
+      static_cast<const T*>(b), static_cast<const T*>(terms), n, nt,
+      static_cast<const T*>(s->Wd_dev), static_cast<const T*>(s->w0d_dev), s->dmem_dev, s->nmd,
+      s->cterm_dev, s->nmc, s->cmem_dev, s->cid_dev, dims[0], dims[1], dims[2], wlo, whi, lam,
+      nullptr, partial);
+  return SFW3D_OK;
+}
+
 // member-count buckets keep the accumulators in registers: V voxels per
 // thread x NM members <= 32 accumulators (16-byte loads where z allows)
 template <typename T>
@@ -1730,6 +2015,25 @@ static int launch_mix(sfw3d_ctx* ctx, int nblocks, const void* b, const void* te
   constexpr int V4 = 16 / sizeof(T);  // 4 floats / 2 doubles
   const int nz = dims[2];
   const bool ring = nz % V4 == 0 && nmm <= 16 && !getenv("SFW3D_MIX_V1");
+  // v2 ring: all members in one launch, argmax only (fields keep the v1 path)
+  if (!col && !fields && ring && m0 == 0 && nmm == int(s->members.size()) && s->nmd <= 16 &&
+      s->nmc <= 8 && s->Wd_dev && !getenv("SFW3D_MIX_RING1")) {
+    // ring depth (SFW3D_MIX_NS: 8 or 16 slots of 16 bytes per thread)
+    static const int ns = [] {
+      const char* e = getenv("SFW3D_MIX_NS");
+      return e ? atoi(e) : 16;
+    }();
+#define SFW3D_RING2(NMD)                                                                        \
+  return ns == 8 ? launch_ring2<T, NMD, 8>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, \
+                                           partial)                                             \
+                 : launch_ring2<T, NMD, 16>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, \
+                                            partial)
+    if (s->nmd <= 4) SFW3D_RING2(4);
+    if (s->nmd <= 8) SFW3D_RING2(8);
+    if (s->nmd <= 12) SFW3D_RING2(12);
+    SFW3D_RING2(16);
+#undef SFW3D_RING2
+  }
   // the collect pass must chunk the volume exactly as the evaluation pass did
   // (it revisits evaluation CTAs by their maxima): same V as the ring kernel
   if (col && ring)
