@@ -2133,10 +2133,15 @@ int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[
     const char* tp = static_cast<const char*>(s->taps[t]);
     const int l0 = s->tlen[0][t], l1 = s->tlen[1][t], l2 = s->tlen[2][t];
     const void* src = s->parent[t] < 0 ? b : terms + size_t(s->parent[t]) * n * es;
-    SFW3D_TRY(corr_pass_impl(ctx, dtype, src, t1, dims, 2, tp + es * (l0 + l1), s->tlo[2][t], l2,
-                             nullptr, 0.0, 1.0, "eta_basis"));
-    SFW3D_TRY(corr_pass_impl(ctx, dtype, t1, t2, dims, 1, tp + es * l0, s->tlo[1][t], l1, nullptr,
-                             0.0, 1.0, "eta_basis"));
+    if (zy_ok(dims, l1, l2)) {
+      SFW3D_TRY(corr_pass_zy(ctx, dtype, src, t2, dims, tp + es * (l0 + l1), s->tlo[2][t], l2,
+                             tp + es * l0, s->tlo[1][t], l1, "eta_basis"));
+    } else {
+      SFW3D_TRY(corr_pass_impl(ctx, dtype, src, t1, dims, 2, tp + es * (l0 + l1), s->tlo[2][t], l2,
+                               nullptr, 0.0, 1.0, "eta_basis"));
+      SFW3D_TRY(corr_pass_impl(ctx, dtype, t1, t2, dims, 1, tp + es * l0, s->tlo[1][t], l1,
+                               nullptr, 0.0, 1.0, "eta_basis"));
+    }
     SFW3D_TRY(corr_pass_impl(ctx, dtype, t2, terms + size_t(t) * n * es, dims, 0, tp, s->tlo[0][t],
                              l0, nullptr, 0.0, 1.0, "eta_basis"));
   }

@@ -2,7 +2,8 @@
 the persistent bulk-copy pipelines (v3: partial row / column tiles, periodic
 wrap inside a staged row, axes shorter than a tile, wide and narrow filters,
 odd offsets) and the v2 fallbacks (short axes, rows wider than the axis),
-checked against the oracle's FFT circular convolution / correlation.
+and the fused in-plane z+y pass (narrow factors), checked against the
+oracle's FFT circular convolution / correlation.
 
 Bars: fp64 1e-12 of max|ref|; fp32 storage 2e-6 of max|ref| (fp32 FMA
 chains of <= 89 taps)."""
@@ -30,6 +31,8 @@ GEOMS = [
     ((96, 192, 256), (9.0, 9.0, 9.0), (30, 44, 44)),    # 61- and 89-tap filters
     ((130, 64, 132), (0.5, 2.0, 0.7), (1, 9, 2)),       # z row wider than the axis: v2
     ((48, 40, 36), (1.5, 1.5, 2.0), (3, 3, 4)),         # short axes: v2 everywhere
+    ((40, 40, 64), (1.0, 4.0, 5.0), (3, 15, 17)),       # fused z+y: z taps wrap the axis
+    ((24, 72, 200), (1.0, 3.0, 2.0), (2, 17, 6)),       # fused z+y: partial y and z tiles
 ]
 
 
