@@ -358,7 +358,8 @@ __global__ void __launch_bounds__(NT, MINB) pass_tile2_kernel(
 template <typename T, int J, int MINB = 1>
 __global__ void __launch_bounds__(128, MINB) pass_z2_kernel(
     const T* __restrict__ in, T* __restrict__ out, int nz, long long nrows,
-    const T* __restrict__ taps_g, int lo, int ntaps, int pitch, const T* addend, T aw, T w) {
+    const T* __restrict__ taps_g, int lo, int ntaps, int pitch, const T* addend, T aw, T w,
+    int zt) {
   constexpr int kVec = 16 / sizeof(T);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int sh = ((lo % 4) + 4) % 4;
@@ -413,6 +414,34 @@ __global__ void __launch_bounds__(128, MINB) pass_z2_kernel(
   }
   const long long row = row0 + lane;
   const int zc = z0 + warp * J;
+  if (!addend && J == 16 && zt && row0 + 32 <= nrows && z0 + 4 * J <= nz) {
+    // narrow filters: transpose through shared memory so every warp store
+    // instruction writes whole rows (2 x 256 contiguous bytes)
+    __syncthreads();  // every thread is done reading the staged input
+    T* res = tile + lane * pitch + warp * J;
+#pragma unroll
+    for (int j = 0; j < J; j += 4) {
+      if constexpr (sizeof(T) == 4) {
+        *reinterpret_cast<float4*>(res + j) = make_float4(w * acc[j], w * acc[j + 1], w * acc[j + 2], w * acc[j + 3]);
+      } else {
+        *reinterpret_cast<double2*>(res + j) = make_double2(w * acc[j], w * acc[j + 1]);
+        *reinterpret_cast<double2*>(res + j + 2) = make_double2(w * acc[j + 2], w * acc[j + 3]);
+      }
+    }
+    __syncthreads();
+    constexpr int vpr = 4 * J / kVec;  // 16-byte vectors per row
+#pragma unroll
+    for (int e = threadIdx.x; e < 32 * vpr; e += 128) {
+      const int r = e / vpr, v = e - r * vpr;
+      const T* sv = tile + r * pitch + v * kVec;
+      T* dv = out + (row0 + r) * nz + z0 + v * kVec;
+      if constexpr (sizeof(T) == 4)
+        __stcs(reinterpret_cast<float4*>(dv), *reinterpret_cast<const float4*>(sv));
+      else
+        __stcs(reinterpret_cast<double2*>(dv), *reinterpret_cast<const double2*>(sv));
+    }
+    return;
+  }
   if (!addend) {
     // straight from registers: J consecutive outputs per thread as 16-byte
     // vector stores (the two halves of each 32-byte sector come from the
@@ -750,8 +779,10 @@ int launch_z2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* t
     SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_z2_kernel<T, J, MINB>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   dim3 grid(unsigned((dims[2] + 4 * J - 1) / (4 * J)), unsigned((nrows + 31) / 32));
+  const char* e = getenv("SFW3D_Z2T");
+  const int zt = e ? atoi(e) : 1;
   pass_z2_kernel<T, J, MINB><<<grid, 128, smem, ctx->stream>>>(in, out, dims[2], nrows, taps, lo, ntaps,
-                                                         pitch, addend, T(aw), T(w));
+                                                         pitch, addend, T(aw), T(w), zt);
   SFW3D_LAUNCH_CHECK(ctx);
   return SFW3D_OK;
 }
@@ -870,10 +901,8 @@ int corr_pass_impl(sfw3d_ctx* ctx, int dtype, const void* in, void* out, const i
 // 512^3 with 15 taps it is instruction-bound (0.54 ms vs 0.52 ms for the two
 // separate passes), see DESIGN.md.
 bool zy_ok(const int dims[3], int ly, int lz) {
-  static const int on = [] {
-    const char* e = getenv("SFW3D_ZY");
-    return e ? atoi(e) : 0;
-  }();
+  const char* e = getenv("SFW3D_ZY");  // (read per call: tests toggle it)
+  const int on = e ? atoi(e) : 0;
   return on && dims[2] % 4 == 0 && dims[2] >= 64 && dims[1] >= 16 && ly <= 36 && lz <= 36;
 }
 

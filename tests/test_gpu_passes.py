@@ -38,7 +38,9 @@ GEOMS = [
 
 @pytest.mark.parametrize("dims,sig,half", GEOMS)
 @pytest.mark.parametrize("prec", ["f32", "f64"])
-def test_psf_passes_vs_fft(P, dims, sig, half, prec):
+@pytest.mark.parametrize("zy", ["0", "1"])
+def test_psf_passes_vs_fft(P, dims, sig, half, prec, zy, monkeypatch):
+    monkeypatch.setenv("SFW3D_ZY", zy)  # fused z+y pass off / on where eligible
     rng = np.random.default_rng(sum(dims))
     kernel = O.box_gaussian_psf(dims, sig, half)
     x = rng.standard_normal(dims)
