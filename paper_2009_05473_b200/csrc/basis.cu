@@ -348,7 +348,11 @@ void fit_signed_members(BasisSet* s, const std::vector<BasisCandidate>& cands, i
   if (env_double("SFW3D_SIGNED", 1.0) == 0.0) return;
   const int nc = int(cands.size()), nt = int(s->betas.size());
   const double u = dtype == SFW3D_F64 ? 0x1p-53 : 0x1p-24;
-  const double accept = env_double("SFW3D_SIGNED_ACCEPT", 0.01);
+  // acceptance of a signed member: bound E <= accept x template mass. A
+  // member's maxima are refined exactly whatever E is; E only sizes the
+  // refinement set. fp32: 0.1 (with the 1e-5 loose term selection, config 4
+  // keeps all 16 members on 12 shared terms, ~360 refined voxels); fp64: 0.01
+  const double accept = env_double("SFW3D_SIGNED_ACCEPT", dtype == SFW3D_F32 ? 0.1 : 0.01);
   const bool debug = env_double("SFW3D_SIGNED_DEBUG", 0.0) != 0.0;
   // per term: (effective) factor mass, its part outside the common box C
   // (chained factors may reach past C, where every template is 0), and the
@@ -529,9 +533,10 @@ void fit_signed_members(BasisSet* s, const std::vector<BasisCandidate>& cands, i
 
 }  // namespace
 
-// fp32 default: config 4 measured 26 -> 17 shared terms, 31.3 -> 22.4 ms
-// per certificate, ~40 refined voxels (SFW3D_BASIS_LOOSE=0 disables)
-constexpr double kLooseF32 = 1.5e-6;
+// fp32 default: config 4 measured 26 -> 12 shared terms (with the fp32
+// signed acceptance 0.1), 31.3 -> 13.5 ms per certificate, ~360 refined
+// voxels (SFW3D_BASIS_LOOSE=0 disables)
+constexpr double kLooseF32 = 1e-5;
 double basis_loose_tol(int dtype) {
   if (dtype != SFW3D_F32) return 0.0;
   const char* e = getenv("SFW3D_BASIS_LOOSE");
