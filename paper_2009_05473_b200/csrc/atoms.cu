@@ -28,7 +28,19 @@ namespace {
 constexpr int kChunk = 4096;               // atom-sum chunk (voxels)
 constexpr int kSumThreads = 256;
 constexpr int kMaxAxis = 1024;             // tabulated axis length in atom sums
-constexpr int kMaxRows = 512;              // rows per chunk
+constexpr int kMaxRows = 512;              // rows per chunk (fp64)
+// fp32: 4x larger chunks (amortise the row table and the fp64 block
+// reduction over 64 voxels per thread), SFW3D_CHUNK32 overrides
+constexpr int kChunk32 = 16384, kMaxRows32 = 2048;
+template <typename T>
+constexpr int max_rows() { return sizeof(T) == 8 ? kMaxRows : kMaxRows32; }
+static int chunk32() {
+  static const int v = [] {
+    const char* e = getenv("SFW3D_CHUNK32");
+    return e ? std::max(256, atoi(e)) : kChunk32;
+  }();
+  return v;
+}
 
 // a mod n in [0, n) without a division on the common path (|a| < 2n)
 __device__ __forceinline__ int pmod(int a, int n) {
@@ -293,7 +305,7 @@ template <typename T>
 __global__ void __launch_bounds__(kSumThreads) atom_sums_kernel(
     const AtomGeo* __restrict__ atoms, const Chunk* __restrict__ chunks, int nx, int ny, int nz,
     const T* __restrict__ field, double* __restrict__ partials) {
-  __shared__ RowRec<T> rows[kMaxRows];
+  __shared__ RowRec<T> rows[max_rows<T>()];
   __shared__ T tzo[kMaxAxis];   // z offsets (full z axes only)
   const Chunk ch = chunks[blockIdx.x];
   const AtomGeo& a = atoms[ch.atom];
@@ -517,14 +529,14 @@ int render_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const AtomGeo* ato
 // Row chunks (~kChunk voxels of whole z-rows) per atom, in atom order; the
 // atom's chunks are contiguous and first[i]..first[i+1] delimits them.
 static void chunk_plan(const std::vector<AtomGeo>& atoms, std::vector<Chunk>& chunks,
-                       std::vector<int>& first) {
+                       std::vector<int>& first, int chunk = kChunk, int max_rows = kMaxRows) {
   chunks.clear();
   first.assign(atoms.size() + 1, 0);
   for (size_t i = 0; i < atoms.size(); ++i) {
     first[i] = int(chunks.size());
     const AtomGeo& a = atoms[i];
     const int rows = a.len[0] * a.len[1];
-    const int per = std::min(kMaxRows, std::max(1, kChunk / std::max(1, a.len[2])));
+    const int per = std::min(max_rows, std::max(1, chunk / std::max(1, a.len[2])));
     for (int r = 0; r < rows; r += per) chunks.push_back({int(i), r, std::min(per, rows - r)});
   }
   first[atoms.size()] = int(chunks.size());
@@ -552,7 +564,11 @@ int atom_sums_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const void* fie
   if (k == 0) return SFW3D_OK;
   std::vector<Chunk> chunks;
   std::vector<int> first;
-  chunk_plan(atoms, chunks, first);
+  // (atom_sums_scratch sizes for the fp64 plan: never fewer chunks)
+  if (dtype == SFW3D_F64 || !small_boxes(atoms, dims))
+    chunk_plan(atoms, chunks, first);
+  else
+    chunk_plan(atoms, chunks, first, std::max(kChunk, chunk32()), kMaxRows32);
   Carver cv(scratch);
   Chunk* ch_dev = cv.take<Chunk>(chunks.size());
   int* first_dev = cv.take<int>(first.size());
