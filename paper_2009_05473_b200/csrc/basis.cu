@@ -861,6 +861,10 @@ int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands,
     if (st != SFW3D_OK) return st;
     s->taps.push_back(dev);
   }
+  if (env_double("SFW3D_BASIS_DEBUG", 0.0) != 0.0)
+    for (int t = 0; t < nt; ++t)
+      fprintf(stderr, "[basis] term %d beta %.5g parent %d pass taps %d %d %d\n", t, s->betas[t],
+              s->parent[t], s->tlen[0][t], s->tlen[1][t], s->tlen[2][t]);
   s->W.assign(size_t(nm) * nt, 0.0);
   s->w0.assign(nm, 0.0);
   for (int m = 0; m < nm; ++m) {
