@@ -9,9 +9,12 @@ N=1000 atoms, random std-0.1 perturbations).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-Multi-GPU (torchrun, one rank per GPU): x-slabs of the output grid per rank
-on the replicated residual; the only collective is the all-gather of the
-16-byte argmax records (and the max-over-ranks timing). scaling = strong.
+Multi-GPU (torchrun, one rank per GPU): each rank holds its x-slab of the
+residual plus halo planes (PSF x-extent + largest candidate radius) and runs
+the single-GPU certificate on that sub-volume with the window restricted to
+its slab (distributed.SlabCertificate); the only collective is the all-gather
+of the 24-byte argmax records (and the max-over-ranks timing). scaling =
+strong (the halo planes are the redundant work).
 `--impl reference` times the reference algorithm (the CPU oracle port of
 sfw3d's FFT eta_field, threads over candidates as the reference's
 map_ordered does) on rank 0 only.
@@ -47,6 +50,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--cg-steps", type=int, default=20)
+    ap.add_argument("--one-rank", default=None, metavar="R/W",
+                    help="testing aid: run only rank R of a W-rank layout on this GPU, "
+                         "no process group (per-rank timing; records not combined)")
     return ap.parse_args()
 
 
@@ -101,9 +107,18 @@ class Clocks:
 
 
 # ------------------------------------------------------------ distributed
+ONE_RANK = None  # (rank, world) of --one-rank: layout of W ranks, no collectives
+
+
 def dist_env():
+    if ONE_RANK:
+        return ONE_RANK[0], ONE_RANK[1], 0
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def collective(world):
+    return world > 1 and not ONE_RANK
 
 
 def peaks():
@@ -209,17 +224,32 @@ def cert_workload(args, rank, world, dev):
     residual = torch.randn(dims, generator=g, device=dev, dtype=torch.float32)
     residual += psf_apply_dev(psf, render_dev(inst.truth, dims, N.F32), False)
     n = dims[0]
-    x0, x1 = rank * n // world, (rank + 1) * n // world - 1
-    window = ((x0, x1), (0, dims[1] - 1), (0, dims[2] - 1))
     ctx = N.context(dev)
     stream = torch.cuda.current_stream(dev)
+    if world > 1:
+        # x-slab per rank on its own sub-volume (slab + halo planes): no
+        # collective inside the step, one 24-byte record all-gather after it
+        from paper_2009_05473_b200 import distributed as D
+        x0, x1 = D.slab_bounds(n, world, rank)
+        slab = D.SlabCertificate(psf, inst.sigma_grid, inst.shape_grid, dims, x0, x1,
+                                 tap_tol=args.tap_tol, mode=args.mode)
+        table, info = slab.table, slab.table.info()
+        work = slab.subvolume(residual)
+        del residual
+        wdims = slab.local_dims
+        off = x0 - slab.halo
+        window = ((slab.halo, slab.halo + x1 - x0), (0, dims[1] - 1), (0, dims[2] - 1))
+    else:
+        work, wdims, off = residual, dims, 0
+        window = ((0, n - 1), (0, dims[1] - 1), (0, dims[2] - 1))
+    x0, x1 = window[0][0], window[0][1]
 
     def step():
-        return eta_argmax_dev(residual, 1.0, table, window)[0]
+        return eta_argmax_dev(work, 1.0, table, window)[0]
 
     for _ in range(args.warmup):
         step()
-    if world > 1:
+    if collective(world):
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
     clocks = Clocks(dev)
@@ -235,10 +265,11 @@ def cert_workload(args, rank, world, dev):
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     # global argmax over ranks: all-gather (value, cand, linear index)
+    gx = (best.pos[0] + off) % n  # global x of the rank's winner
     rec = torch.tensor([best.value, float(best.cand),
-                        float((best.pos[0] * dims[1] + best.pos[1]) * dims[2] + best.pos[2])],
+                        float((gx * dims[1] + best.pos[1]) * dims[2] + best.pos[2])],
                        dtype=torch.float64, device=dev)
-    if world > 1:
+    if collective(world):
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
@@ -264,7 +295,7 @@ def cert_workload(args, rank, world, dev):
     fp32_peak = ctx.probe_fp32()
     hbm_peak = peaks()["hbm_gbs"]
     win_vox = (x1 - x0 + 1) * dims[1] * dims[2]
-    nvox = int(np.prod(dims))
+    nvox = int(np.prod(wdims))  # the volume this rank's kernels sweep
     rooflines = {}
     if fam["eta_direct"][1]:
         flops = info["direct_flops_per_voxel"] * win_vox  # executed FP32 ops (FMA = 2)
@@ -330,8 +361,8 @@ def cert_workload(args, rank, world, dev):
     # residual from pinned host memory (double-buffered: step i+1's H2D runs
     # on a copy stream while step i's certificate computes) and reads the
     # argmax records back (the call returns after their D2H)
-    host = residual.to("cpu").pin_memory()
-    bufs = [torch.empty_like(residual) for _ in range(2)]
+    host = work.to("cpu").pin_memory()
+    bufs = [torch.empty_like(work) for _ in range(2)]
     copy_stream = torch.cuda.Stream(dev)
     copied = [torch.cuda.Event() for _ in range(2)]
     done = [torch.cuda.Event() for _ in range(2)]
@@ -359,7 +390,7 @@ def cert_workload(args, rank, world, dev):
     run_e2e(args.steps)
     torch.cuda.synchronize(dev)
     e2e_s = (time.perf_counter() - t0) / args.steps
-    if world > 1:
+    if collective(world):
         t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
@@ -373,6 +404,7 @@ def cert_workload(args, rank, world, dev):
         "value": value, "ms_per_step": ms_step, "launches": launches, "clocks": clk,
         "roofline": roof, "e2e": e2e, "kernel_ms": {k: v[0] for k, v in fam.items() if v[1]},
         "table": info, "best": {"eta": gbest[0], "cand": int(gbest[1]), "lin": int(gbest[2])},
+        "halo": slab.halo if world > 1 else 0,
         "refined_voxels": refine_count,
         "inst": inst, "dims": dims,
     }
@@ -456,7 +488,11 @@ def solve_workload(dev):
 
 
 def main():
+    global ONE_RANK
     args = parse()
+    if args.one_rank:
+        r, w = (int(v) for v in args.one_rank.split("/"))
+        ONE_RANK = (r, w)
     if args.impl == "reference":
         reference_arm(args)
         return
@@ -464,7 +500,7 @@ def main():
     rank, world, local = dist_env()
     dev = local
     torch.cuda.set_device(dev)
-    if world > 1:
+    if collective(world):
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", dev))
     res = cert_workload(args, rank, world, dev)
     secondary = []
@@ -480,7 +516,7 @@ def main():
         cpu = {"value": vc / times[0], "unit": "voxel-candidates/s", "cores": 1, "kind": "port",
                "sample": f"1 candidate (sigma=3, d=1.5) x {args.n}^3: rfftn + irfftn + argmax, "
                          "scipy.fft single thread (the reference never threads its FFTs)"}
-    if rank == 0:
+    if rank == 0 or ONE_RANK:
         line = {
             "metric": "certificate voxel-candidates/s", "value": res["value"],
             "unit": "voxel-candidates/s", "n_gpus": world, "steps": args.steps,
@@ -491,15 +527,19 @@ def main():
                                    "PSF sigma_h=3 31^3, eta at every voxel + global argmax",
                        "grid": args.n, "candidates": res["table"]["n_cand"],
                        "tap_tol": args.tap_tol, "mode": args.mode,
-                       "parallelism": f"x-slabs x{world} (replicated residual)",
+                       "parallelism": (f"x-slabs x{world}: each rank's slab + {res['halo']} halo "
+                                       "planes resident, argmax records all-gathered")
+                       if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (512 MiB residual, 0.9 GiB padded copy)"},
             "gpu_launches": res["launches"], "clocks": res["clocks"], "roofline": res["roofline"],
             "cpu_baseline": cpu, "e2e": res["e2e"], "kernel_ms_per_step": res["kernel_ms"],
             "table": res["table"], "argmax": res["best"], "refined_voxels": res["refined_voxels"],
             "secondary": secondary,
         }
+        if ONE_RANK:
+            line["one_rank"] = f"{ONE_RANK[0]}/{ONE_RANK[1]}"  # testing aid: this rank's time only
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if collective(world):
         torch.distributed.destroy_process_group()
 
 

@@ -190,3 +190,90 @@ def cost_grad_sharded(psf, y, rows, lam, group=None):
         return out
 
     return c, sharded_rows(compute_rows, rows.shape[0], group, y.device)
+
+
+# ------------------------------------------- slab-local certificate (GPU)
+def slab_halo(psf, sigma_grid, shape_grid) -> int:
+    """x-planes of halo an x-slab sub-volume needs so that eta on the slab is
+    the global eta: the PSF's x-extent (b = H^T r) plus the largest candidate
+    support radius (forward.py:97-99). The chained basis factors reach a few
+    planes further with values below the 1e-12 truncation; the signed members'
+    bounds cover those taps whatever data they meet (basis.cu)."""
+    from .forward import support_radius
+    k = psf.kernel.data
+    c = k.shape[0] // 2
+    nzx = np.flatnonzero(np.abs(k).sum(axis=(1, 2)))
+    hx = int(max(c - nzx.min(), nzx.max() - c))
+    r = max(support_radius(s, d) for s in sigma_grid for d in shape_grid)
+    return hx + r
+
+
+def local_psf_kernel(kernel: np.ndarray, local_dims) -> np.ndarray:
+    """The kernel's non-zero box re-centred (origin n//2 per axis) in a volume
+    of `local_dims`."""
+    out = np.zeros(tuple(local_dims))
+    src, dst = [], []
+    for a in range(3):
+        other = tuple(b for b in range(3) if b != a)
+        ix = np.flatnonzero(np.abs(kernel).sum(axis=other))
+        n, ln = kernel.shape[a], local_dims[a]
+        lo, hi = ix.min() - n // 2, ix.max() - n // 2
+        if ln // 2 + lo < 0 or ln // 2 + hi >= ln:
+            raise ValueError("PSF support wider than the local sub-volume")
+        src.append(slice(ix.min(), ix.max() + 1))
+        dst.append(slice(ln // 2 + lo, ln // 2 + hi + 1))
+    out[tuple(dst)] = kernel[tuple(src)]
+    return out
+
+
+class SlabCertificate:
+    """Certificate of one rank's x-slab [x0, x1] computed on its own
+    sub-volume: planes x0 - halo .. x1 + halo of the (periodic) residual.
+
+    Every eta value on the slab equals the global one (the sub-volume holds
+    all the residual the slab's b = H^T r and templates touch), so each rank
+    runs the single-GPU certificate on (x1 - x0 + 1 + 2 halo) planes with the
+    window restricted to its slab, and the only collective is the all-gather
+    of 24-byte argmax records (combine_best: the reference's order). The
+    redundant work is the 2 halo planes per slab plane count. The basis is
+    pruned by the GLOBAL volume's rule (SFW3D_BASIS_PRUNE is set for the
+    process) so every rank fits the same shared terms as one GPU would."""
+
+    def __init__(self, psf, sigma_grid, shape_grid, dims, x0: int, x1: int, halo: int | None = None,
+                 **table_kw):
+        import os
+        import torch
+        from .certificate import build_template_table
+        from .forward import Psf, support_radius
+        from .volumes import Volume
+        self.dims = tuple(int(v) for v in dims)
+        self.x0, self.x1 = int(x0), int(x1)
+        self.halo = int(slab_halo(psf, sigma_grid, shape_grid) if halo is None else halo)
+        n = self.dims[0]
+        rmax = max(support_radius(s, d) for s in sigma_grid for d in shape_grid)
+        self.local_dims = (self.x1 - self.x0 + 1 + 2 * self.halo, self.dims[1], self.dims[2])
+        if 2 * rmax + 1 >= n or 2 * rmax + 1 >= self.local_dims[0]:
+            raise ValueError("candidate boxes span the x axis: slabs cannot shard this table")
+        os.environ["SFW3D_BASIS_PRUNE"] = "1" if int(np.prod(self.dims)) >= (1 << 26) else "0"
+        self.psf = Psf(Volume(local_psf_kernel(psf.kernel.data, self.local_dims)), normalize=False)
+        self.table = build_template_table(self.psf, sigma_grid, shape_grid, **table_kw)
+        self.index = torch.arange(self.x0 - self.halo, self.x1 + self.halo + 1) % n
+
+    def subvolume(self, residual):
+        """This rank's sub-volume of a global residual (device or host tensor)."""
+        return residual.index_select(0, self.index.to(residual.device)).contiguous()
+
+    def argmax(self, sub, lam: float, window=None):
+        """(eta, cand, global C-order index) of the slab's part of `window`
+        (global coordinates; None = every voxel), or (-inf, big, big)."""
+        from .certificate import eta_argmax_dev
+        (wx0, wx1), wy, wz = window or ((0, self.dims[0] - 1), (0, self.dims[1] - 1),
+                                        (0, self.dims[2] - 1))
+        lo, hi = max(self.x0, wx0), min(self.x1, wx1)
+        if lo > hi:
+            return (float("-inf"), 2 ** 31, 2 ** 62)
+        off = self.x0 - self.halo
+        best, _, _ = eta_argmax_dev(sub, lam, self.table, ((lo - off, hi - off), wy, wz))
+        x = (best.pos[0] + off) % self.dims[0]
+        lin = (x * self.dims[1] + best.pos[1]) * self.dims[2] + best.pos[2]
+        return (float(best.value), int(best.cand), int(lin))

@@ -228,3 +228,43 @@ def test_eta_f32_fused_xmix_matches_separate_passes(P, dims, monkeypatch):
     assert b1.value == b0.value and tuple(b1.pos) == tuple(b0.pos)
     for a, c in zip(r1, r0):
         assert abs(a.value - c.value) <= 1e-6 * abs(b0.value) and tuple(a.pos) == tuple(c.pos)
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_slab_certificate_matches_global(P, nranks, prec, monkeypatch):
+    """Multi-GPU certificate layout (distributed.SlabCertificate), ranks run
+    one after another on this GPU: each rank evaluates its x-slab on its own
+    sub-volume (slab + halo planes of the periodic residual) and the records
+    combine (eta desc, candidate asc, C-order index asc) to EXACTLY the
+    single-volume certificate's winner (same kernels, same per-voxel
+    arithmetic), and the winner matches the FFT oracle."""
+    import torch
+    from paper_2009_05473_b200 import distributed as D
+    monkeypatch.setenv("SFW3D_BASIS_PRUNE", "0")  # (restored after the test)
+    dims = (96, 48, 64)
+    rng = np.random.default_rng(5)
+    kernel = O.box_gaussian_psf(dims, (1.5, 1.5, 1.5), (3, 3, 3))
+    rows = np.column_stack([rng.uniform(5, 10, 6), rng.uniform(0, 48, (6, 3)),
+                            rng.uniform(1, 2, 6), rng.uniform(1.8, 2.5, 6)])
+    r = rng.standard_normal(dims) + O.conv(O.render(rows, dims), O.psf_hat(kernel))
+    r = r.astype(np.float32).astype(np.float64)
+    sg, dg = np.array([1.0, 1.5, 2.0]), np.array([1.8, 2.0, 2.5])
+    psf = P.Psf(P.Volume(kernel), normalize=False)
+    with P.precision(prec):
+        table = P.build_template_table(psf, sg, dg)
+        rd = torch.tensor(r, device="cuda", dtype=torch.float32 if prec == "f32" else torch.float64)
+        full = ((0, dims[0] - 1), (0, dims[1] - 1), (0, dims[2] - 1))
+        best, _, _ = P.certificate.eta_argmax_dev(rd, 0.7, table, full)
+        glin = (best.pos[0] * dims[1] + best.pos[1]) * dims[2] + best.pos[2]
+        recs = []
+        for rank in range(nranks):
+            x0, x1 = D.slab_bounds(dims[0], nranks, rank)
+            slab = D.SlabCertificate(psf, sg, dg, dims, x0, x1)
+            recs.append(slab.argmax(slab.subvolume(rd), 0.7))
+    v, c, lin = D.combine_best(recs)
+    assert (v, c, lin) == (float(best.value), int(best.cand), int(glin))
+    hats = O.template_hats(O.psf_hat(kernel), dims, sg, dg)
+    pos, _, val, _, _ = O.eta_field(r, 0.7, hats, len(dg))
+    assert tuple(best.pos) == tuple(pos)
+    assert abs(v - val) <= (1e-5 if prec == "f32" else 1e-10) * abs(val)
