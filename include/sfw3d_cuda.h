@@ -217,6 +217,19 @@ int sfw3d_nnlasso_cd(sfw3d_ctx* ctx, int k, const double* gram_host, const doubl
                      double lam, double tol, int max_iter, double* w_host,
                      int32_t* info_host, double* kkt_host);
 
+/* K9' — the same non-negative LASSO solved by an active-set (Lawson-Hanson)
+ * iteration on the device: Cholesky of the free set's Gram block in shared
+ * memory, exact optimum of the QP min 1/2 w'Gw - (b - lam)'w, w >= 0, stopped
+ * by the reference's KKT residual <= tol (solvers.py:161-169). Same arguments
+ * as sfw3d_nnlasso_cd; info_host[0] = outer iterations, info_host[1] = 0 kkt /
+ * 2 cap / 3 not applicable (k > 150 or a near-singular free block: w_host is
+ * then unspecified and the caller uses sfw3d_nnlasso_cd). Used for fp32-
+ * storage solves (kernel-level parity); fp64 solves keep the reference's CD
+ * trajectory. */
+int sfw3d_nnlasso_qp(sfw3d_ctx* ctx, int k, const double* gram_host, const double* b_host,
+                     double lam, double tol, int max_iter, double* w_host,
+                     int32_t* info_host, double* kkt_host);
+
 /* K5 — out = y - sum_i w_i phi_i in list order (_residual, solvers.py:253-257);
  * out_dev may be NULL; sumsq_host (may be NULL) receives ||out||^2 in fp64. */
 int sfw3d_residual(sfw3d_ctx* ctx, int dtype, int64_t n, const void* y_dev,

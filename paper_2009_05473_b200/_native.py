@@ -29,7 +29,7 @@ EXPORTS = (
     "sfw3d_ctx_sync", "sfw3d_ctx_launches", "sfw3d_atom_geometry", "sfw3d_psf_create",
     "sfw3d_psf_info", "sfw3d_psf_destroy", "sfw3d_psf_apply", "sfw3d_render",
     "sfw3d_atom_sums", "sfw3d_cost_grad", "sfw3d_table_create", "sfw3d_table_info",
-    "sfw3d_table_destroy", "sfw3d_eta_argmax", "sfw3d_dots", "sfw3d_nnlasso_cd",
+    "sfw3d_table_destroy", "sfw3d_eta_argmax", "sfw3d_dots", "sfw3d_nnlasso_cd", "sfw3d_nnlasso_qp",
     "sfw3d_residual", "sfw3d_ctx_profile", "sfw3d_ctx_profile_read", "sfw3d_probe_fp32",
     "sfw3d_table_candidate", "sfw3d_basis_fit", "sfw3d_basis_set_fit",
     "sfw3d_last_refine_count",
@@ -72,6 +72,8 @@ _SIGNATURES = {
                                    C.POINTER(Argmax), _vp]),
     "sfw3d_dots": (C.c_int, [_vp, C.c_int, C.c_int64, C.POINTER(_vp), C.c_int, _vp, _dp]),
     "sfw3d_nnlasso_cd": (C.c_int, [_vp, C.c_int, _dp, _dp, C.c_double, C.c_double, C.c_int, _dp,
+                                   _i32p, _dp]),
+    "sfw3d_nnlasso_qp": (C.c_int, [_vp, C.c_int, _dp, _dp, C.c_double, C.c_double, C.c_int, _dp,
                                    _i32p, _dp]),
     "sfw3d_residual": (C.c_int, [_vp, C.c_int, C.c_int64, _vp, C.POINTER(_vp), _dp, C.c_int, _vp,
                                  _dp]),

@@ -44,13 +44,13 @@ double basis_loose_tol(int dtype);
 void basis_set_export(const BasisSet* s, int max_terms, int* n_terms, double* betas,
                       double* weights, double* w0, double* fit_err, int32_t* member);
 void basis_set_destroy(BasisSet* s);
-// tables prune their shared terms for volumes of >= 2^26 voxels (~406^3):
-// there a term's three full-volume passes per certificate outweigh the
-// seconds of host NNLS refits the pruning costs once per table
-// (SFW3D_BASIS_PRUNE=0/1 overrides, for measurements)
-inline bool basis_prune_rule(const int dims[3]) {
+// tables prune their shared terms for volumes of >= 2^26 voxels (~406^3;
+// fp32 storage: >= 2^24, 256^3): there a term's three full-volume passes per
+// certificate outweigh the seconds of host NNLS refits the pruning costs
+// once per table (config 3: 48 -> 18 terms). SFW3D_BASIS_PRUNE=0/1 overrides.
+inline bool basis_prune_rule(const int dims[3], int dtype) {
   if (const char* e = getenv("SFW3D_BASIS_PRUNE")) return atoi(e) != 0;
-  return (long long)dims[0] * dims[1] * dims[2] >= (1LL << 26);
+  return (long long)dims[0] * dims[1] * dims[2] >= (dtype == SFW3D_F32 ? (1LL << 24) : (1LL << 26));
 }
 // candidate -> (is member, fit error of its shared-dictionary fit)
 bool basis_set_member(const BasisSet* s, int cand, double* fit_err);

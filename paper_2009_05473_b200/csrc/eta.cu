@@ -636,7 +636,7 @@ static int ensure_basis(const sfw3d_table* t, int dtype) {
   SFW3D_CUDA_TRY(cudaSetDevice(t->device));
   BasisSet* built = nullptr;
   const int st = basis_set_build(t->dims, t->bcands, dtype, tol, &built, true,
-                                 basis_prune_rule(t->dims), basis_loose_tol(dtype));
+                                 basis_prune_rule(t->dims, dtype), basis_loose_tol(dtype));
   cudaSetDevice(dev);
   if (st != SFW3D_OK) {
     basis_set_destroy(built);
@@ -774,7 +774,7 @@ extern "C" int sfw3d_basis_set_fit(const int32_t dims[3], int n_sigma, const dou
       bc.push_back(c);
     }
   BasisSet* s = nullptr;
-  const int st = basis_set_build(dm, bc, dtype, tol, &s, /*on_device=*/false, basis_prune_rule(dm),
+  const int st = basis_set_build(dm, bc, dtype, tol, &s, /*on_device=*/false, basis_prune_rule(dm, dtype),
                                  basis_loose_tol(dtype));
   if (st == SFW3D_OK)
     basis_set_export(s, max_terms, n_terms, betas, weights, w0, fit_err, member);

@@ -91,14 +91,28 @@ __global__ void sum_partials_kernel(const double* __restrict__ p, int n, double*
 
 // One warp; solvers.py:149-180 step for step. Gram rows are read for the
 // column update: the host assembles the Gram matrix exactly symmetric.
-__global__ void __launch_bounds__(32) cd_kernel(int k, const double* __restrict__ gram,
-                                                const double* __restrict__ b, double lam,
+// GRAM_SMEM: the Gram matrix and b are staged in shared memory first (k <=
+// kCdSmemK): the sweep's per-coordinate reads then cost shared-memory
+// latency instead of L2 round trips; the arithmetic is unchanged.
+template <bool GRAM_SMEM>
+__global__ void __launch_bounds__(32) cd_kernel(int k, const double* __restrict__ gram_g,
+                                                const double* __restrict__ b_g, double lam,
                                                 double tol, int max_iter, double* __restrict__ w_io,
                                                 int* __restrict__ info, double* __restrict__ kkt_out) {
   extern __shared__ double sm[];
   double* w = sm;
   double* gw = sm + k;
   const int lane = threadIdx.x;
+  const double* gram = gram_g;
+  const double* b = b_g;
+  if constexpr (GRAM_SMEM) {
+    double* sg = sm + 2 * k;
+    double* sb = sg + (size_t)k * k;
+    for (long long e = lane; e < (long long)k * k; e += 32) sg[e] = gram_g[e];
+    for (int i = lane; i < k; i += 32) sb[i] = b_g[i];
+    gram = sg;
+    b = sb;
+  }
   for (int i = lane; i < k; i += 32) w[i] = w_io[i];
   __syncwarp();
   // gw = gram @ w (row order)
@@ -178,6 +192,189 @@ __global__ void __launch_bounds__(32) cd_kernel(int k, const double* __restrict_
   }
 }
 
+// Active-set solve of the same non-negative LASSO (fp32-storage solves):
+// min 1/2 w'Gw - (b - lam)'w subject to w >= 0 is a strictly convex QP
+// (Gram of distinct blurred atoms); Lawson-Hanson's active-set iteration
+// reaches its exact optimum in a few dense solves instead of hundreds of CD
+// sweeps. One CTA: the free set's Gram block is gathered into shared memory
+// and Cholesky-factored in place (column-parallel), two triangular solves,
+// the step / set update, and the reference's KKT residual as the stop test.
+// info[1]: 0 KKT <= tol, 2 iteration cap, 3 factorisation failed (near-
+// singular free block: the caller falls back to cd_kernel).
+constexpr int kQpThreads = 256;
+constexpr int kQpMaxFree = 150;  // free-set block <= 150^2 doubles in shared memory
+
+__device__ double qp_block_max(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double r = red[0];
+  for (int w = 1; w < kQpThreads / 32; ++w) r = fmax(r, red[w]);
+  return r;
+}
+
+__global__ void __launch_bounds__(kQpThreads) nnqp_kernel(int k, const double* __restrict__ G,
+                                                         const double* __restrict__ b, double lam,
+                                                         double tol, int max_iter,
+                                                         double* __restrict__ w_io,
+                                                         int* __restrict__ info,
+                                                         double* __restrict__ kkt_out) {
+  extern __shared__ double sm[];
+  double* A = sm;                                   // [kQpMaxFree * kQpMaxFree]
+  double* w = A + kQpMaxFree * kQpMaxFree;          // [k]
+  double* z = w + k;                                // [k] (free-set solution, slot order)
+  double* g = z + k;                                // [k] b - lam - G w
+  int* fidx = reinterpret_cast<int*>(g + k);        // [k] free indices
+  __shared__ double red[kQpThreads / 32];
+  __shared__ int s_nf, s_flag, s_arg;
+  __shared__ double s_alpha;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < k; i += kQpThreads) w[i] = w_io[i];
+  double dmax = 0.0;
+  for (int i = tid; i < k; i += kQpThreads) dmax = fmax(dmax, G[(long long)i * k + i]);
+  dmax = qp_block_max(dmax, red);
+  int reason = 2, it = 0;
+  double kkt = INFINITY;
+  bool solved = false;  // w is the exact solve on its current free set
+  for (it = 1; it <= max_iter; ++it) {
+    // gradient residual g = (b - lam) - G w and the reference KKT measure
+    for (int i = tid; i < k; i += kQpThreads) {
+      double x = 0.0;
+      const double* row = G + (long long)i * k;
+      for (int j = 0; j < k; ++j) x += row[j] * w[j];
+      g[i] = (b[i] - lam) - x;
+    }
+    __syncthreads();
+    double ka = 0.0, best = -INFINITY;
+    int arg = -1;
+    for (int i = tid; i < k; i += kQpThreads) {
+      if (w[i] > 0.0) {
+        ka = fmax(ka, fabs(g[i]));
+      } else {
+        ka = fmax(ka, fmax(0.0, g[i]));
+        if (g[i] > best) { best = g[i]; arg = i; }
+      }
+    }
+    kkt = qp_block_max(ka, red);
+    if (kkt <= tol) { reason = 0; break; }
+    // entering index: the inactive coordinate with the largest g (ties: lowest)
+    {
+      double v = best;
+      int a = arg;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int oa = __shfl_xor_sync(0xffffffffu, a, o);
+        if (ov > v || (ov == v && oa >= 0 && (a < 0 || oa < a))) { v = ov; a = oa; }
+      }
+      __shared__ double rv[kQpThreads / 32];
+      __shared__ int ra[kQpThreads / 32];
+      if ((tid & 31) == 0) { rv[tid >> 5] = v; ra[tid >> 5] = a; }
+      __syncthreads();
+      if (tid == 0) {
+        double bv = rv[0];
+        int ba = ra[0];
+        for (int q = 1; q < kQpThreads / 32; ++q)
+          if (rv[q] > bv || (rv[q] == bv && ra[q] >= 0 && (ba < 0 || ra[q] < ba))) { bv = rv[q]; ba = ra[q]; }
+        s_arg = bv > tol ? ba : -1;
+      }
+      __syncthreads();
+    }
+    const int enter = s_arg;
+    if (enter < 0 && solved) {  // KKT limited by rounding on the solved free set
+      reason = 0;
+      break;
+    }
+    // inner loop: solve on the free set, step back while the solution leaves w >= 0
+    bool entered = false;
+    solved = false;
+    for (int inner = 0; inner < 4 * k + 4; ++inner) {
+      if (tid == 0) {
+        int nf = 0;
+        for (int i = 0; i < k; ++i)
+          if (w[i] > 0.0 || (!entered && i == enter)) fidx[nf++] = i;
+        s_nf = nf;
+      }
+      __syncthreads();
+      entered = true;
+      const int nf = s_nf;
+      if (nf > kQpMaxFree) { reason = 3; break; }
+      if (nf == 0) break;
+      for (int e = tid; e < nf * nf; e += kQpThreads) {
+        const int r = e / nf, c = e - r * nf;
+        A[e] = G[(long long)fidx[r] * k + fidx[c]];
+      }
+      for (int r = tid; r < nf; r += kQpThreads) z[r] = b[fidx[r]] - lam;
+      if (tid == 0) s_flag = 0;
+      __syncthreads();
+      // Cholesky A = L L^T (lower, in place), right-looking
+      for (int j = 0; j < nf; ++j) {
+        if (tid == 0) {
+          const double d = A[j * nf + j];
+          if (!(d > 1e-13 * dmax)) s_flag = 1;
+          A[j * nf + j] = sqrt(fmax(d, 1e-300));
+        }
+        __syncthreads();
+        if (s_flag) break;
+        const double ljj = A[j * nf + j];
+        for (int r = j + 1 + tid; r < nf; r += kQpThreads) A[r * nf + j] /= ljj;
+        __syncthreads();
+        const int m = nf - j - 1;
+        for (int e = tid; e < m * m; e += kQpThreads) {
+          const int r = j + 1 + e / m, c = j + 1 + e % m;
+          if (c <= r) A[r * nf + c] -= A[r * nf + j] * A[c * nf + j];
+        }
+        __syncthreads();
+      }
+      if (s_flag) { reason = 3; break; }
+      // L y = rhs, L^T z = y (one thread per step: nf <= 150)
+      if (tid == 0) {
+        for (int r = 0; r < nf; ++r) {
+          double x = z[r];
+          for (int c = 0; c < r; ++c) x -= A[r * nf + c] * z[c];
+          z[r] = x / A[r * nf + r];
+        }
+        for (int r = nf - 1; r >= 0; --r) {
+          double x = z[r];
+          for (int c = r + 1; c < nf; ++c) x -= A[c * nf + r] * z[c];
+          z[r] = x / A[r * nf + r];
+        }
+        // feasible: accept; else step from w toward z until a free weight hits 0
+        double alpha = 1.0;
+        for (int r = 0; r < nf; ++r)
+          if (z[r] <= 0.0) {
+            const double wi = w[fidx[r]];
+            const double a = wi / (wi - z[r]);
+            alpha = fmin(alpha, a);
+          }
+        s_alpha = alpha;
+        for (int r = 0; r < nf; ++r) {
+          const int i = fidx[r];
+          double nw = alpha >= 1.0 ? z[r] : w[i] + alpha * (z[r] - w[i]);
+          if (alpha < 1.0 && (z[r] <= 0.0 && w[i] / (w[i] - z[r]) <= alpha)) nw = 0.0;
+          w[i] = nw > 0.0 ? nw : 0.0;
+        }
+      }
+      __syncthreads();
+      if (s_alpha >= 1.0) {
+        solved = true;
+        break;
+      }
+    }
+    if (reason == 3) break;
+  }
+  __syncthreads();
+  for (int i = tid; i < k; i += kQpThreads) w_io[i] = w[i];
+  if (tid == 0) {
+    info[0] = it;
+    info[1] = reason;
+    *kkt_out = kkt;
+  }
+}
+
 }  // namespace
 }  // namespace sfw3d
 
@@ -251,9 +448,27 @@ extern "C" int sfw3d_residual(sfw3d_ctx* ctx, int dtype, int64_t n, const void* 
   return SFW3D_OK;
 }
 
+static int nnlasso_run(sfw3d_ctx* ctx, int k, const double* gram_host, const double* b_host,
+                       double lam, double tol, int max_iter, double* w_host, int32_t* info_host,
+                       double* kkt_host, bool qp);
+
+extern "C" int sfw3d_nnlasso_qp(sfw3d_ctx* ctx, int k, const double* gram_host, const double* b_host,
+                                double lam, double tol, int max_iter, double* w_host,
+                                int32_t* info_host, double* kkt_host) {
+  return nnlasso_run(ctx, k, gram_host, b_host, lam, tol, max_iter, w_host, info_host, kkt_host,
+                     true);
+}
+
 extern "C" int sfw3d_nnlasso_cd(sfw3d_ctx* ctx, int k, const double* gram_host, const double* b_host,
                                 double lam, double tol, int max_iter, double* w_host,
                                 int32_t* info_host, double* kkt_host) {
+  return nnlasso_run(ctx, k, gram_host, b_host, lam, tol, max_iter, w_host, info_host, kkt_host,
+                     false);
+}
+
+static int nnlasso_run(sfw3d_ctx* ctx, int k, const double* gram_host, const double* b_host,
+                       double lam, double tol, int max_iter, double* w_host, int32_t* info_host,
+                       double* kkt_host, bool qp) {
   SFW3D_CHECK_ARG(ctx && w_host, "NULL argument");
   SFW3D_CHECK_ARG(k >= 0 && (k == 0 || (gram_host && b_host)), "sizes");
   SFW3D_CHECK_ARG(lam > 0.0, "lam must be > 0");
@@ -280,13 +495,34 @@ extern "C" int sfw3d_nnlasso_cd(sfw3d_ctx* ctx, int k, const double* gram_host, 
   SFW3D_TRY(stage_upload(ctx, g, gram_host, kk * sizeof(double)));
   SFW3D_TRY(stage_upload(ctx, bd, b_host, size_t(k) * sizeof(double)));
   SFW3D_TRY(stage_upload(ctx, wd, w_host, size_t(k) * sizeof(double)));
-  const size_t smem = 2 * size_t(k) * sizeof(double);
-  if (smem > 48 * 1024)
-    SFW3D_CUDA_TRY(cudaFuncSetAttribute(cd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  if (qp) {
+    if (k > kQpMaxFree) {
+      if (info_host) info_host[0] = 0, info_host[1] = 3;  // too large: caller falls back
+      return SFW3D_OK;
+    }
+    const size_t smem = (size_t(kQpMaxFree) * kQpMaxFree + 3 * size_t(k)) * sizeof(double) +
+                        size_t(k) * sizeof(int);
+    SFW3D_CUDA_TRY(cudaFuncSetAttribute(nnqp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(smem)));
+    SFW3D_PROF(ctx, "cd");
+    nnqp_kernel<<<1, kQpThreads, smem, ctx->stream>>>(k, g, bd, lam, tol, max_iter, wd, info, kkt);
+    SFW3D_LAUNCH_CHECK(ctx);
+  } else {
+  const bool gs = (kk + 3 * size_t(k)) * sizeof(double) <= 200 * 1024;  // k <= ~158
+  const size_t smem = (gs ? kk + 3 * size_t(k) : 2 * size_t(k)) * sizeof(double);
   {
     SFW3D_PROF(ctx, "cd");
-    cd_kernel<<<1, 32, smem, ctx->stream>>>(k, g, bd, lam, tol, max_iter, wd, info, kkt);
+    if (gs) {
+      if (smem > 48 * 1024)
+        SFW3D_CUDA_TRY(cudaFuncSetAttribute(cd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      cd_kernel<true><<<1, 32, smem, ctx->stream>>>(k, g, bd, lam, tol, max_iter, wd, info, kkt);
+    } else {
+      if (smem > 48 * 1024)
+        SFW3D_CUDA_TRY(cudaFuncSetAttribute(cd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      cd_kernel<false><<<1, 32, smem, ctx->stream>>>(k, g, bd, lam, tol, max_iter, wd, info, kkt);
+    }
     SFW3D_LAUNCH_CHECK(ctx);
+  }
   }
   // results: w, info, kkt in one pinned download each
   SFW3D_TRY(download_sync(ctx, w_host, wd, size_t(k) * sizeof(double)));

@@ -254,7 +254,9 @@ class SlabCertificate:
         self.local_dims = (self.x1 - self.x0 + 1 + 2 * self.halo, self.dims[1], self.dims[2])
         if 2 * rmax + 1 >= n or 2 * rmax + 1 >= self.local_dims[0]:
             raise ValueError("candidate boxes span the x axis: slabs cannot shard this table")
-        os.environ["SFW3D_BASIS_PRUNE"] = "1" if int(np.prod(self.dims)) >= (1 << 26) else "0"
+        from . import _native as N
+        big = (1 << 24) if N.dtype_code() == N.F32 else (1 << 26)  # basis_prune_rule (basis.cuh)
+        os.environ["SFW3D_BASIS_PRUNE"] = "1" if int(np.prod(self.dims)) >= big else "0"
         self.psf = Psf(Volume(local_psf_kernel(psf.kernel.data, self.local_dims)), normalize=False)
         self.table = build_template_table(self.psf, sigma_grid, shape_grid, **table_kw)
         self.index = torch.arange(self.x0 - self.halo, self.x1 + self.halo + 1) % n

@@ -309,3 +309,27 @@ def test_solve_golden(P, golden, algo):
     assert np.max(np.abs(rows[:, 1:4] - ref_rows[:, 1:4])) < 1e-3
     np.testing.assert_allclose(rows[:, 0], ref_rows[:, 0], rtol=1e-4, atol=1e-8)
     assert P.audit_criterion_path(res.trace).ok
+
+
+def test_qp_lasso_matches_converged_cd(P):
+    """K9' (fp32-storage solves): the active-set QP reaches the LASSO optimum
+    the reference's CD converges to — cold and warm starts, a sparse optimum
+    (large lam), KKT residual within tol — and reports 'not applicable' for a
+    near-singular free block (the caller then runs the CD)."""
+    from paper_2009_05473_b200.solvers import cd_dev
+    rng = np.random.default_rng(7)
+    A = rng.standard_normal((60, 500))
+    gram = A @ A.T
+    gram = 0.5 * (gram + gram.T)
+    b = A @ rng.standard_normal(500)
+    for lam, w_init in ((0.5, np.zeros(60)), (0.5, np.abs(rng.standard_normal(60))),
+                        (40.0, np.zeros(60))):
+        w_ref, _, why = O.cd_solve(gram, b, lam, w_init.copy(), 1e-11, 200000)
+        w, it, reason, kkt = cd_dev(gram, b, lam, w_init, 1e-9, 500, method="qp")
+        assert reason == "kkt" and kkt <= 1e-9, (lam, reason, kkt)
+        np.testing.assert_allclose(w, w_ref, rtol=1e-7, atol=1e-9)
+        assert (w >= 0).all() and ((w > 0) == (w_ref > 0)).all()
+    A[5] = A[4]  # exactly duplicated atom: singular free block -> not applicable
+    gram = A @ A.T
+    b = A @ rng.standard_normal(500)
+    assert cd_dev(gram, b, 0.5, np.ones(60), 1e-9, 500, method="qp") is None
