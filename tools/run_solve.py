@@ -19,44 +19,53 @@ from paper_2009_05473_b200 import _native as N, configs, solvers  # noqa: E402
 from paper_2009_05473_b200.certificate import eta_field_dev  # noqa: E402
 from paper_2009_05473_b200.forward import psf_apply_dev, render_dev  # noqa: E402
 
-ap = argparse.ArgumentParser()
-ap.add_argument("--config", type=int, default=2)
-ap.add_argument("--algo", default="bsfw")
-ap.add_argument("--max-outer", type=int, default=None)
-ap.add_argument("--seed", type=int, default=0)
-a = ap.parse_args()
-inst = {1: configs.config1, 2: configs.config2, 3: configs.config3}[a.config](a.seed)
-P.set_precision(inst.precision)
-psf = P.Psf(P.Volume(inst.kernel), normalize=False)
-t0 = time.perf_counter()
-clean = psf_apply_dev(psf, render_dev(inst.truth, inst.dims, N.dtype_code()), False)
-noise = float(torch.sqrt(torch.mean(clean.double() ** 2) / 10 ** (inst.snr_db / 10)))
-g = torch.Generator(device="cuda")
-g.manual_seed(1000 + a.seed)
-y_dev = clean + noise * torch.randn(inst.dims, generator=g, device="cuda", dtype=clean.dtype)
-y = P.Volume(y_dev.double().cpu().numpy())
-table = P.build_template_table(psf, inst.sigma_grid, inst.shape_grid, bounds=inst.bounds)
-lam = inst.lam_factor * eta_field_dev(y.device_tensor(y_dev.dtype, y_dev.device), 1.0, table,
-                                     inst.bounds).eta_max
-orig = solvers.make_parameter_grids
-solvers.make_parameter_grids = lambda b, ns, nd: (inst.sigma_grid, inst.shape_grid)
-opts = P.SolverOptions(lam=lam, max_outer_iterations=a.max_outer or 3 * len(inst.truth))
-t1 = time.perf_counter()
-res = getattr(P, a.algo)(y, psf, opts, inst.bounds)
-t2 = time.perf_counter()
-solvers.make_parameter_grids = orig
-rows = res.measure.to_rows()
-truth = inst.truth
-d = np.linalg.norm(rows[:, None, 1:4] - truth[None, :, 1:4], axis=2) if len(rows) else np.zeros((0, len(truth)))
-matched = int(np.sum(d.min(axis=0) < 2.0)) if len(rows) else 0
-print(json.dumps({
-    "config": a.config, "algo": a.algo, "precision": inst.precision, "dims": inst.dims,
-    "lam": lam, "noise_sigma": noise, "solve_s": t2 - t1, "setup_s": t1 - t0,
-    "outer_iterations": len(res.trace.records), "atoms": len(res.measure),
-    "termination": res.termination, "criterion": res.criterion,
-    "truth_atoms": len(truth), "truth_matched_within_2vox": matched,
-    "split_s": {"certificate": res.trace.step_time("certificate"),
-                "lasso": res.trace.step_time("lasso"), "descent": res.trace.step_time("descent"),
-                "table": res.trace.t_table},
-    "eta_trace": [round(r.eta_max, 4) for r in res.trace.records][:80],
-}))
+def run(config=2, algo="bsfw", max_outer=None, seed=0) -> dict:
+    """One full solve on a config recipe; returns the summary dict."""
+    inst = {1: configs.config1, 2: configs.config2, 3: configs.config3}[config](seed)
+    P.set_precision(inst.precision)
+    psf = P.Psf(P.Volume(inst.kernel), normalize=False)
+    t0 = time.perf_counter()
+    clean = psf_apply_dev(psf, render_dev(inst.truth, inst.dims, N.dtype_code()), False)
+    noise = float(torch.sqrt(torch.mean(clean.double() ** 2) / 10 ** (inst.snr_db / 10)))
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1000 + seed)
+    y_dev = clean + noise * torch.randn(inst.dims, generator=g, device="cuda", dtype=clean.dtype)
+    y = P.Volume(y_dev.double().cpu().numpy())
+    table = P.build_template_table(psf, inst.sigma_grid, inst.shape_grid, bounds=inst.bounds)
+    lam = inst.lam_factor * eta_field_dev(y.device_tensor(y_dev.dtype, y_dev.device), 1.0, table,
+                                         inst.bounds).eta_max
+    orig = solvers.make_parameter_grids
+    solvers.make_parameter_grids = lambda b, ns, nd: (inst.sigma_grid, inst.shape_grid)
+    try:
+        opts = P.SolverOptions(lam=lam, max_outer_iterations=max_outer or 3 * len(inst.truth))
+        t1 = time.perf_counter()
+        res = getattr(P, algo)(y, psf, opts, inst.bounds)
+        t2 = time.perf_counter()
+    finally:
+        solvers.make_parameter_grids = orig
+    rows = res.measure.to_rows()
+    truth = inst.truth
+    d = (np.linalg.norm(rows[:, None, 1:4] - truth[None, :, 1:4], axis=2) if len(rows)
+         else np.zeros((0, len(truth))))
+    matched = int(np.sum(d.min(axis=0) < 2.0)) if len(rows) else 0
+    return {
+        "config": config, "algo": algo, "precision": inst.precision, "dims": inst.dims,
+        "lam": lam, "noise_sigma": noise, "solve_s": t2 - t1, "setup_s": t1 - t0,
+        "outer_iterations": len(res.trace.records), "atoms": len(res.measure),
+        "termination": res.termination, "criterion": res.criterion,
+        "truth_atoms": len(truth), "truth_matched_within_2vox": matched,
+        "split_s": {"certificate": res.trace.step_time("certificate"),
+                    "lasso": res.trace.step_time("lasso"), "descent": res.trace.step_time("descent"),
+                    "table": res.trace.t_table},
+        "eta_trace": [round(r.eta_max, 4) for r in res.trace.records][:80],
+    }
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--algo", default="bsfw")
+    ap.add_argument("--max-outer", type=int, default=None)
+    ap.add_argument("--seed", type=int, default=0)
+    a = ap.parse_args()
+    print(json.dumps(run(a.config, a.algo, a.max_outer, a.seed)))

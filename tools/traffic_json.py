@@ -9,7 +9,7 @@ import json
 import re
 import sys
 
-FAMILIES = (("eta_basis", r"pass_(tile|z|tiled)"), ("eta_mix", r"mix_argmax_kernel<[^>]*, 0>"),
+FAMILIES = (("eta_basis", r"pass_(tile|z|tiled|zy)"), ("eta_mix", r"mix_argmax_kernel<[^>]*, 0>|mix_ring2?_kernel"),
             ("eta_direct", r"eta_(fold|direct|sym)_kernel"), ("eta_refine", r"refine_kernel"))
 
 
