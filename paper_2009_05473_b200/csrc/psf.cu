@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(128, MINB) pass_z2_kernel(
   }
   const long long row = row0 + lane;
   const int zc = z0 + warp * J;
-  if (!addend && J == 16 && zt && row0 + 32 <= nrows && z0 + 4 * J <= nz) {
+  if (!addend && (J == 16 ? (zt & 1) : (zt & 2)) && row0 + 32 <= nrows && z0 + 4 * J <= nz) {
     // narrow filters: transpose through shared memory so every warp store
     // instruction writes whole rows (2 x 256 contiguous bytes)
     __syncthreads();  // every thread is done reading the staged input
@@ -779,8 +779,8 @@ int launch_z2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* t
     SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_z2_kernel<T, J, MINB>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   dim3 grid(unsigned((dims[2] + 4 * J - 1) / (4 * J)), unsigned((nrows + 31) / 32));
-  const char* e = getenv("SFW3D_Z2T");
-  const int zt = e ? atoi(e) : 1;
+  const char* e = getenv("SFW3D_Z2T");  // bit 0: J = 16, bit 1: J = 32 (measured both faster)
+  const int zt = e ? atoi(e) : 3;
   pass_z2_kernel<T, J, MINB><<<grid, 128, smem, ctx->stream>>>(in, out, dims[2], nrows, taps, lo, ntaps,
                                                          pitch, addend, T(aw), T(w), zt);
   SFW3D_LAUNCH_CHECK(ctx);
