@@ -509,13 +509,17 @@ __global__ void __launch_bounds__(128, MINB) pass_z2_kernel(
 //   3. y pass: lane = z, 16 consecutive y outputs per thread from a register
 //      window over the intermediate rows (as pass_tile2_kernel) -> coalesced
 //      stores along z.
-constexpr int kZyTY = 32, kZyTZ = 128, kZyThreads = 256;
+constexpr int kZyThreads = 256;
 
-template <typename T>
+// TY x TZ outputs per CTA; z pass: lane = staged row (rounds of 32 rows),
+// warp = JZ-column group (TZ = 8 JZ); y pass: thread = (z column, group of JY
+// rows), 256 / TZ groups (TY = JY * 256 / TZ).
+template <typename T, int TY, int TZ, int JZ, int JY>
 __global__ void __launch_bounds__(kZyThreads) pass_zy_kernel(
     const T* __restrict__ in, T* __restrict__ out, int ny, int nz, const T* __restrict__ tz_g,
     int loz, int lz, const T* __restrict__ ty_g, int loy, int ly, int pitch, int ipitch, int rin) {
-  constexpr int kVec = 16 / sizeof(T), J = 16;
+  static_assert(TZ == 8 * JZ && TY == JY * (kZyThreads / TZ), "tile geometry");
+  constexpr int kVec = 16 / sizeof(T);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int sh = ((loz % 4) + 4) % 4;
   const int nt4 = (lz + sh + 3) & ~3;        // z taps incl. sh leading zeros
@@ -525,12 +529,12 @@ __global__ void __launch_bounds__(kZyThreads) pass_zy_kernel(
   T* tile = tys + ny4 + 4;                   // [rin][pitch]
   T* inter = tile + size_t(rin) * pitch;     // [rin][ipitch]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int x = blockIdx.z, y0 = blockIdx.y * kZyTY, z0 = blockIdx.x * kZyTZ;
+  const int x = blockIdx.z, y0 = blockIdx.y * TY, z0 = blockIdx.x * TZ;
   for (int q = threadIdx.x; q < nt4 + 8; q += kZyThreads)
     tzs[q] = (q >= sh && q - sh < lz) ? tz_g[q - sh] : T(0);
   for (int q = threadIdx.x; q < ny4 + 4; q += kZyThreads) tys[q] = q < ly ? ty_g[q] : T(0);
   // 1. stage rows y0 + loy + r (wrapped), columns [zs, zs + width)
-  const int width = kZyTZ + nt4 + 4;
+  const int width = TZ + nt4 + 4;
   const int nv = width / kVec;
   {
     int zs = (z0 + loz - sh) % nz;
@@ -556,14 +560,14 @@ __global__ void __launch_bounds__(kZyThreads) pass_zy_kernel(
   for (int r0 = 0; r0 < rin; r0 += 32) {
     const int r = r0 + lane;
     if (r < rin) {
-      T acc[J];
+      T acc[JZ];
 #pragma unroll
-      for (int j = 0; j < J; ++j) acc[j] = T(0);
-      const T* const q[1] = {tile + r * pitch + warp * J};
-      Fold<T, J, 1>::row(acc, tzs, q, nt4 / 4);
-      T* dst = inter + r * ipitch + warp * J;
+      for (int j = 0; j < JZ; ++j) acc[j] = T(0);
+      const T* const q[1] = {tile + r * pitch + warp * JZ};
+      Fold<T, JZ, 1>::row(acc, tzs, q, nt4 / 4);
+      T* dst = inter + r * ipitch + warp * JZ;
 #pragma unroll
-      for (int j = 0; j < J; j += 4) {
+      for (int j = 0; j < JZ; j += 4) {
         if constexpr (sizeof(T) == 4) {
           *reinterpret_cast<float4*>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
         } else {
@@ -574,77 +578,95 @@ __global__ void __launch_bounds__(kZyThreads) pass_zy_kernel(
     }
   }
   __syncthreads();
-  // 3. y pass: thread = (z column, group of J consecutive y outputs)
-  const int zc = threadIdx.x % kZyTZ, g = threadIdx.x / kZyTZ;  // 2 groups of 16 rows
-  const T* src = inter + (g * J) * ipitch + zc;
-  T W[J], acc[J];
+  // 3. y pass: thread = (z column, group of JY consecutive y outputs)
+  const int zc = threadIdx.x % TZ, g = threadIdx.x / TZ;
+  const T* src = inter + (g * JY) * ipitch + zc;
+  T W[JY], acc[JY];
 #pragma unroll
-  for (int j = 0; j < J; ++j) {
+  for (int j = 0; j < JY; ++j) {
     W[j] = src[j * ipitch];
     acc[j] = T(0);
   }
   int q0 = 0;
-  for (; q0 + J <= ny4; q0 += J) {
+  for (; q0 + JY <= ny4; q0 += JY) {
 #pragma unroll
-    for (int r = 0; r < J; r += 4) {
+    for (int r = 0; r < JY; r += 4) {
       T t4[4];
       ld4(tys + q0 + r, t4[0], t4[1], t4[2], t4[3]);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
 #pragma unroll
-        for (int j = 0; j < J; ++j) acc[j] = fma(t4[k], W[(r + k + j) % J], acc[j]);
-        W[r + k] = src[(q0 + r + k + J) * ipitch];
+        for (int j = 0; j < JY; ++j) acc[j] = fma(t4[k], W[(r + k + j) % JY], acc[j]);
+        W[r + k] = src[(q0 + r + k + JY) * ipitch];
       }
     }
   }
 #pragma unroll
-  for (int r = 0; r < J; r += 4) {
+  for (int r = 0; r < JY; r += 4) {
     if (q0 + r >= ny4) break;
     T t4[4];
     ld4(tys + q0 + r, t4[0], t4[1], t4[2], t4[3]);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
 #pragma unroll
-      for (int j = 0; j < J; ++j) acc[j] = fma(t4[k], W[(r + k + j) % J], acc[j]);
-      W[r + k] = src[(q0 + r + k + J) * ipitch];
+      for (int j = 0; j < JY; ++j) acc[j] = fma(t4[k], W[(r + k + j) % JY], acc[j]);
+      W[r + k] = src[(q0 + r + k + JY) * ipitch];
     }
   }
   const int z = z0 + zc;
   if (z < nz) {
-    T* po = out + ((long long)x * ny + y0 + g * J) * nz + z;
+    T* po = out + ((long long)x * ny + y0 + g * JY) * nz + z;
+    if (y0 + TY <= ny) {
 #pragma unroll
-    for (int j = 0; j < J; ++j, po += nz)
-      if (y0 + g * J + j < ny) *po = acc[j];
+      for (int j = 0; j < JY; ++j, po += nz) *po = acc[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < JY; ++j, po += nz)
+        if (y0 + g * JY + j < ny) *po = acc[j];
+    }
   }
 }
 
-template <typename T>
-int launch_zy(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* tz, int loz, int lz,
-              const T* ty, int loy, int ly) {
+template <typename T, int TY, int TZ, int JZ, int JY>
+int launch_zy_t(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* tz, int loz,
+                int lz, const T* ty, int loy, int ly) {
   const int sh = ((loz % 4) + 4) % 4;
   const int nt4 = (lz + sh + 3) & ~3, ny4 = (ly + 3) & ~3;
-  const int width = kZyTZ + nt4 + 4;
+  const int width = TZ + nt4 + 4;
   // staged rows: outputs + padded taps (the y window's last read-ahead row,
-  // zero-weighted, is row kZyTY + ny4 - 1)
-  const int rin = kZyTY + ny4;
+  // zero-weighted, is row TY + ny4 - 1)
+  const int rin = TY + ny4;
   int pitch = (width + 3) & ~3;
-  int ipitch = kZyTZ + 4;
+  int ipitch = TZ + 4;
   if (sizeof(T) == 4) {
     if (pitch % 8 != 4) pitch += 4;
   } else {
     if (pitch % 4 != 2) pitch += 2;
-    ipitch = kZyTZ + 2;
+    ipitch = TZ + 2;
   }
   const size_t smem = (size_t(nt4) + 8 + ny4 + 4 + size_t(rin) * pitch + size_t(rin) * ipitch) * sizeof(T);
   if (smem > 48 * 1024)
-    SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_zy_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        int(smem)));
-  dim3 grid(unsigned((dims[2] + kZyTZ - 1) / kZyTZ), unsigned((dims[1] + kZyTY - 1) / kZyTY),
-            unsigned(dims[0]));
-  pass_zy_kernel<T><<<grid, kZyThreads, smem, ctx->stream>>>(in, out, dims[1], dims[2], tz, loz, lz, ty,
-                                                             loy, ly, pitch, ipitch, rin);
+    SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_zy_kernel<T, TY, TZ, JZ, JY>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  dim3 grid(unsigned((dims[2] + TZ - 1) / TZ), unsigned((dims[1] + TY - 1) / TY), unsigned(dims[0]));
+  pass_zy_kernel<T, TY, TZ, JZ, JY><<<grid, kZyThreads, smem, ctx->stream>>>(
+      in, out, dims[1], dims[2], tz, loz, lz, ty, loy, ly, pitch, ipitch, rin);
   SFW3D_LAUNCH_CHECK(ctx);
   return SFW3D_OK;
+}
+
+// tile variant (SFW3D_ZY_TILE): 0 = 32 x 128 (16, 16), 1 = 64 x 64 (8, 16),
+// 2 = 64 x 128 (16, 32), 3 = 32 x 64 (8, 8)
+template <typename T>
+int launch_zy(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* tz, int loz, int lz,
+              const T* ty, int loy, int ly) {
+  const char* e = getenv("SFW3D_ZY_TILE");
+  switch (e ? atoi(e) : 1) {
+    case 0: return launch_zy_t<T, 32, 128, 16, 16>(ctx, in, out, dims, tz, loz, lz, ty, loy, ly);
+    case 2: return launch_zy_t<T, 64, 128, 16, 32>(ctx, in, out, dims, tz, loz, lz, ty, loy, ly);
+    case 3: return launch_zy_t<T, 32, 64, 8, 8>(ctx, in, out, dims, tz, loz, lz, ty, loy, ly);
+    default: return launch_zy_t<T, 64, 64, 8, 16>(ctx, in, out, dims, tz, loz, lz, ty, loy, ly);
+  }
 }
 
 // General (non-separable) kernel: out[x] = sum_o K(o) in[x + sgn*o] over the
