@@ -301,6 +301,12 @@ struct BasisSet {
   // mix_ring2_kernel: dense members (W rows [nmd][K], w0) and copy members
   // (one weight-1 term, w0 = 0) with cterm[k] = copy slot of term k or -1
   int nmd = 0, nmc = 0;
+  // mix_mma_kernel (fp32, K + 1 <= 16 entries, <= 16 columns): B[entry][column]
+  // (columns: dense members then copies), column -> member index
+  bool mma_mix = false;
+  int ncol = 0;
+  float* Bmat_dev = nullptr;
+  int* colmem_dev = nullptr;
   void* Wd_dev = nullptr;
   void* w0d_dev = nullptr;
   int* dmem_dev = nullptr;
@@ -381,7 +387,11 @@ void fit_signed_members(BasisSet* s, const std::vector<BasisCandidate>& cands, i
     ext[t] = std::max(0.0, prod - pin);
     rho[t] = 1.01 * u * pass_taps[t] + (s->parent[t] >= 0 ? rho[s->parent[t]] * (1.0 + 1.01 * u * pass_taps[t]) : 0.0);
   }
-  const double gmix = 1.01 * u * (nt + 2);
+  // the mix's rounding: fp32 FFMA chains (u), or the tensor-core 3xTF32 mix
+  // (mix_mma_kernel: <= 3 x 2^-22 per product + truncating fp32 accumulation;
+  // 2^-19 is used)
+  const double umix = s->mma_mix ? 0x1p-19 : u;
+  const double gmix = 1.01 * umix * (nt + 2);
   // axis representatives: offsets +t and -t share one (multiplicity 2) when
   // both lie in C and every factor is defined at both
   struct Rep {
@@ -874,6 +884,9 @@ int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands,
   }
   s->n_nnls = nm;
   s->ebound.assign(nc, 0.0);
+  // opt-in (SFW3D_MIX_MMA=1): measured slower than mix_ring2_kernel on config
+  // 4 (2.98 vs 2.28 ms; legacy mma.sync issue, per-group latency chains)
+  s->mma_mix = dtype == SFW3D_F32 && nt + 1 <= 16 && env_double("SFW3D_MIX_MMA", 0.0) != 0.0;
   if (nt > 0) fit_signed_members(s, cands, dtype, Sfit, heff, pass_taps);
   const int nmt = int(s->members.size());
   if (nmt && on_device) {
@@ -913,6 +926,27 @@ int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands,
       }
       s->nmd = int(dmem.size());
       s->nmc = int(cmem.size());
+      if (s->mma_mix && s->nmd + s->nmc <= 16) {
+        std::vector<float> B(16 * 16, 0.f);
+        std::vector<int> colmem(16, 0);
+        int col = 0;
+        for (int q = 0; q < s->nmd; ++q, ++col) {
+          const int m = dmem[q];
+          colmem[col] = m;
+          B[0 * 16 + col] = float(s->w0[m]);
+          for (int t = 0; t < nt; ++t) B[(1 + t) * 16 + col] = float(s->W[size_t(m) * nt + t]);
+        }
+        for (int q = 0; q < s->nmc; ++q, ++col) {
+          const int m = cmem[q];
+          colmem[col] = m;
+          for (int t = 0; t < nt; ++t) B[(1 + t) * 16 + col] = float(s->W[size_t(m) * nt + t]);
+        }
+        s->ncol = col;
+        SFW3D_TRY(upload(reinterpret_cast<void**>(&s->Bmat_dev), B.data(), B.size() * sizeof(float)));
+        SFW3D_TRY(upload(reinterpret_cast<void**>(&s->colmem_dev), colmem.data(), colmem.size() * sizeof(int)));
+      } else {
+        s->mma_mix = false;
+      }
       Wd.push_back(0.0);
       w0d.push_back(0.0);
       dmem.push_back(0);
@@ -955,7 +989,7 @@ void basis_set_destroy(BasisSet* s) {
   if (s->cid_dev) cudaFree(s->cid_dev);
   if (s->xtaps_dev) cudaFree(s->xtaps_dev);
   if (s->xmeta_dev) cudaFree(s->xmeta_dev);
-  for (void* p : {s->Wd_dev, s->w0d_dev, static_cast<void*>(s->dmem_dev),
+  for (void* p : {static_cast<void*>(s->Bmat_dev), static_cast<void*>(s->colmem_dev), s->Wd_dev, s->w0d_dev, static_cast<void*>(s->dmem_dev),
                   static_cast<void*>(s->cmem_dev), static_cast<void*>(s->cterm_dev)})
     if (p) cudaFree(p);
   delete s;
@@ -1905,6 +1939,172 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
   }
 }
 
+// Evaluation-pass mix on the tensor cores (fp32 storage): for every voxel
+// the member values are a 16-entry dot product (b, T_0 .. T_{K-1}, zero pad)
+// with a 16-column weight matrix (dense members, then the exact d = 2 copies
+// with weight 1, zero pad) — a (voxels x 16) x (16 x 16) GEMM. Each warp streams
+// 16-voxel groups through its own cp.async ring ([entry][24] floats per
+// stage: conflict-free A-fragment loads) and issues mma.sync m16n8k8 TF32 in
+// the 3xTF32 split (a_hi b_hi + a_hi b_lo + a_lo b_hi, fp32 accumulate: ~2^-20
+// relative per product, which the signed members' bounds use). Same CTA
+// chunking as mix_ring2_kernel, so the collect pass revisits the same chunks.
+constexpr int kMmaNS = 8;       // ring stages per warp
+constexpr int kMmaPitch = 24;   // floats per entry row of a stage (16 used)
+
+__device__ __forceinline__ unsigned to_tf32(float x) {
+  unsigned r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const unsigned (&a)[4], unsigned b0,
+                                         unsigned b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__global__ void __launch_bounds__(kMixThreads, 2) mix_mma_kernel(
+    const float* __restrict__ b, const float* __restrict__ terms, long long n, int K,
+    const float* __restrict__ Bmat, const int* __restrict__ colmem, int ncol,
+    int nx, int ny, int nz, int4 wlo, int4 whi, double lam, Best* __restrict__ partial) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int kStage = 16 * kMmaPitch;  // floats
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  float* ring = reinterpret_cast<float*>(smem_raw) + warp * (kMmaNS * kStage);
+  __shared__ Best red[16][kMixThreads / 32];
+  // zero every stage once (entries >= K + 1 are never copied)
+  for (int e = lane; e < kMmaNS * kStage; e += 32) ring[e] = 0.f;
+  __syncwarp();
+  // B fragments (k-step s, n-tile q): b0 = B[8s + t][8q + g], b1 = B[8s + t + 4][8q + g]
+  unsigned bh[2][2][2], bl[2][2][2];
+#pragma unroll
+  for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float w = Bmat[(8 * s2 + t + 4 * h) * 16 + 8 * q + g];
+        bh[s2][q][h] = to_tf32(w);
+        bl[s2][q][h] = to_tf32(w - __uint_as_float(bh[s2][q][h]));
+      }
+  // this CTA's voxel range (mix_ring2_kernel's chunking, in 4-voxel vectors)
+  const long long nv = n / 4;
+  const long long chunk =
+      ((nv + gridDim.x - 1) / gridDim.x + kMixThreads - 1) / kMixThreads * kMixThreads;
+  const long long vbeg = blockIdx.x * chunk * 4, vend = min(n, (blockIdx.x + 1) * chunk * 4);
+  const int ngroups = vbeg < vend ? int((vend - vbeg) / 16) : 0;
+  const int E = K + 1;
+  const int pieces = 4 * E;  // 16-byte pieces per group (E entries x 16 voxels)
+  // my groups: warp, warp + 8, ...
+  const int mine = ngroups > warp ? (ngroups - warp + 7) / 8 : 0;
+  const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(ring));
+  auto issue = [&](int j) {  // group j of mine into stage j % NS
+    const long long v0 = vbeg + 16LL * (warp + 8LL * j);
+    const unsigned st = sbase + unsigned((j % kMmaNS) * kStage * 4);
+    for (int p = lane; p < pieces; p += 32) {
+      const int e = p >> 2, v4 = p & 3;
+      const float* src = (e == 0 ? b : terms + (long long)(e - 1) * n) + v0 + 4 * v4;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(st + unsigned((e * kMmaPitch + 4 * v4) * 4)),
+                   "l"(src));
+    }
+  };
+#pragma unroll 1
+  for (int j = 0; j < kMmaNS - 1; ++j) {
+    if (j < mine) issue(j);
+    cp_async_commit();
+  }
+  float bv[2][2];
+  int bi[2][2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      bv[q][h] = -INFINITY;
+      bi[q][h] = 0x7fffffff;
+    }
+  for (int j = 0; j < mine; ++j) {
+    cp_async_wait_group<kMmaNS - 2>();
+    __syncwarp();
+    const float* st = ring + (j % kMmaNS) * kStage;
+    float c[2][4];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) c[q][r] = 0.f;
+#pragma unroll
+    for (int s2 = 0; s2 < 2; ++s2) {
+      const float av[4] = {st[(8 * s2 + t) * kMmaPitch + g], st[(8 * s2 + t) * kMmaPitch + g + 8],
+                           st[(8 * s2 + t + 4) * kMmaPitch + g],
+                           st[(8 * s2 + t + 4) * kMmaPitch + g + 8]};
+      unsigned ah[4], al[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        ah[r] = to_tf32(av[r]);
+        al[r] = to_tf32(av[r] - __uint_as_float(ah[r]));
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        mma_tf32(c[q], al, bh[s2][q][0], bh[s2][q][1]);
+        mma_tf32(c[q], ah, bl[s2][q][0], bl[s2][q][1]);
+        mma_tf32(c[q], ah, bh[s2][q][0], bh[s2][q][1]);
+      }
+    }
+    __syncwarp();  // every lane is done with this stage before it is refilled
+    if (j + kMmaNS - 1 < mine) issue(j + kMmaNS - 1);
+    cp_async_commit();
+    // running maxima: columns 8q + 2t + h, voxels v0 + g (rows r = 0, 1) and v0 + g + 8
+    const long long v0 = vbeg + 16LL * (warp + 8LL * j);
+    const int z0 = int(v0 % nz);
+    const long long row = v0 / nz;
+    const int y = int(row % ny), x = int(row / ny);
+    if (x >= wlo.x && x <= whi.x && y >= wlo.y && y <= whi.y) {
+      const bool in0 = z0 + g >= wlo.z && z0 + g <= whi.z;
+      const bool in1 = z0 + g + 8 >= wlo.z && z0 + g + 8 <= whi.z;
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (in0 && c[q][h] > bv[q][h]) {
+            bv[q][h] = c[q][h];
+            bi[q][h] = int(v0 + g);
+          }
+          if (in1 && c[q][2 + h] > bv[q][h]) {
+            bv[q][h] = c[q][2 + h];
+            bi[q][h] = int(v0 + g + 8);
+          }
+        }
+    }
+  }
+  cp_async_wait_group<0>();
+  // reduce each column over the 8 lanes that share t (lane bits 2..4), then warps
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      Best bm = {bi[q][h] == 0x7fffffff ? -INFINITY : double(bv[q][h]) / lam,
+                 bi[q][h] == 0x7fffffff ? 0x7fffffffffffffffLL : (long long)bi[q][h]};
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bm.v, o);
+        const long long oi = __shfl_xor_sync(0xffffffffu, bm.idx, o);
+        if (better(ov, oi, bm.v, bm.idx)) bm = {ov, oi};
+      }
+      if (g == 0) red[8 * q + 2 * t + h][warp] = bm;
+    }
+  __syncthreads();
+  if (threadIdx.x < ncol) {
+    const int col = threadIdx.x;
+    Best bm = red[col][0];
+    for (int w = 1; w < kMixThreads / 32; ++w)
+      if (better(red[col][w].v, red[col][w].idx, bm.v, bm.idx)) bm = red[col][w];
+    partial[(long long)colmem[col] * gridDim.x + blockIdx.x] = bm;
+  }
+}
+
 __global__ void member_reduce_kernel(const Best* __restrict__ partial, int nblocks,
                                      const int* __restrict__ cid, Best* __restrict__ best_dev) {
   __shared__ Best sb[32];
@@ -2024,6 +2224,19 @@ static int launch_mix(sfw3d_ctx* ctx, int nblocks, const void* b, const void* te
   constexpr int V4 = 16 / sizeof(T);  // 4 floats / 2 doubles
   const int nz = dims[2];
   const bool ring = nz % V4 == 0 && nmm <= 16 && !getenv("SFW3D_MIX_V1");
+  // tensor-core mix (fp32): all members in one launch, argmax only
+  if constexpr (sizeof(T) == 4) {
+    if (!col && !fields && s->mma_mix && s->Bmat_dev && m0 == 0 && nmm == int(s->members.size()) &&
+        s->ncol == nmm && n % 16 == 0 && nz % 16 == 0) {
+      const size_t smem = size_t(kMixThreads / 32) * kMmaNS * 16 * kMmaPitch * sizeof(float);
+      SFW3D_CUDA_TRY(cudaFuncSetAttribute(mix_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(smem)));
+      mix_mma_kernel<<<nblocks, kMixThreads, smem, ctx->stream>>>(
+          static_cast<const float*>(b), static_cast<const float*>(terms), n, nt, s->Bmat_dev,
+          s->colmem_dev, s->ncol, dims[0], dims[1], dims[2], wlo, whi, lam, partial);
+      return SFW3D_OK;
+    }
+  }
   // v2 ring: all members in one launch, argmax only (fields keep the v1 path)
   if (!col && !fields && ring && m0 == 0 && nmm == int(s->members.size()) && s->nmd <= 16 &&
       s->nmc <= 8 && s->Wd_dev && !getenv("SFW3D_MIX_RING1")) {
