@@ -2199,7 +2199,8 @@ static int launch_mix_nm(sfw3d_ctx* ctx, int nblocks, const void* b, const void*
 template <typename T, int NMD, int NS>
 static int launch_ring2(sfw3d_ctx* ctx, int nblocks, const void* b, const void* terms, long long n,
                         int nt, const BasisSet* s, const int dims[3], int4 wlo, int4 whi,
-                        double lam, Best* partial) {
+                        double lam, Best* partial, int d0 = 0, int dn = -1, bool copies = true) {
+  if (dn < 0) dn = s->nmd;
   constexpr int V4 = 16 / sizeof(T);
   const size_t smem = size_t(NS) * kMixThreads * V4 * sizeof(T) + size_t(nt + 1) * 8 +
                       (size_t(nt) * NMD + NMD + size_t(NMD + 8) * kMixThreads) * sizeof(T) +
@@ -2209,9 +2210,39 @@ static int launch_ring2(sfw3d_ctx* ctx, int nblocks, const void* b, const void* 
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   mix_ring2_kernel<T, NMD, NS><<<nblocks, kMixThreads, smem, ctx->stream>>>(
       static_cast<const T*>(b), static_cast<const T*>(terms), n, nt,
-      static_cast<const T*>(s->Wd_dev), static_cast<const T*>(s->w0d_dev), s->dmem_dev, s->nmd,
-      s->cterm_dev, s->nmc, s->cmem_dev, s->cid_dev, dims[0], dims[1], dims[2], wlo, whi, lam,
-      nullptr, partial);
+      static_cast<const T*>(s->Wd_dev) + size_t(d0) * nt, static_cast<const T*>(s->w0d_dev) + d0,
+      s->dmem_dev + d0, dn, s->cterm_dev, copies ? s->nmc : 0, s->cmem_dev, s->cid_dev, dims[0],
+      dims[1], dims[2], wlo, whi, lam, nullptr, partial);
+  return SFW3D_OK;
+}
+
+// every member through mix_ring2_kernel (dense members 16 per launch, the
+// copies with the first): argmax-only evaluations whose z extent takes
+// 16-byte vectors. The collect pass then chunks with the same V = 16 / es.
+static bool ring2_all_ok(const BasisSet* s, int dtype, const int dims[3]) {
+  const int V4 = dtype == SFW3D_F64 ? 2 : 4;
+  return s->Wd_dev && !s->mma_mix && s->nmc <= 8 && dims[2] % V4 == 0 &&
+         !getenv("SFW3D_MIX_V1") && !getenv("SFW3D_MIX_RING1");
+}
+
+template <typename T>
+static int launch_ring2_all(sfw3d_ctx* ctx, int nblocks, const void* b, const void* terms,
+                            long long n, int nt, const BasisSet* s, const int dims[3], int4 wlo,
+                            int4 whi, double lam, Best* partial) {
+  for (int d0 = 0; d0 < std::max(s->nmd, 1); d0 += 16) {
+    const int dn = std::max(0, std::min(16, s->nmd - d0));
+    const bool cp = d0 == 0;
+    SFW3D_PROF(ctx, "eta_mix");
+    if (dn <= 4)
+      SFW3D_TRY((launch_ring2<T, 4, 16>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp)));
+    else if (dn <= 8)
+      SFW3D_TRY((launch_ring2<T, 8, 16>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp)));
+    else if (dn <= 12)
+      SFW3D_TRY((launch_ring2<T, 12, 16>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp)));
+    else
+      SFW3D_TRY((launch_ring2<T, 16, 16>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp)));
+    SFW3D_LAUNCH_CHECK(ctx);
+  }
   return SFW3D_OK;
 }
 
@@ -2258,9 +2289,13 @@ static int launch_mix(sfw3d_ctx* ctx, int nblocks, const void* b, const void* te
   }
   // the collect pass must chunk the volume exactly as the evaluation pass did
   // (it revisits evaluation CTAs by their maxima): same V as the ring kernel
-  if (col && ring)
-    return launch_mix_nm<T, 16, V4>(ctx, nblocks, b, terms, n, nt, nmm, m0, s, dims, wlo, whi,
-                                    lam, fields, partial, col);
+  if (col && (ring || (!fields && ring2_all_ok(s, sizeof(T) == 8 ? SFW3D_F64 : SFW3D_F32, dims)))) {
+    if (nmm <= 16)
+      return launch_mix_nm<T, 16, V4>(ctx, nblocks, b, terms, n, nt, nmm, m0, s, dims, wlo, whi,
+                                      lam, fields, partial, col);
+    return launch_mix_nm<T, kMixMax, V4>(ctx, nblocks, b, terms, n, nt, nmm, m0, s, dims, wlo,
+                                         whi, lam, fields, partial, col);
+  }
   if (!col && ring) {
     const size_t smem = (size_t(kMixNS) * kMixThreads * V4 + size_t(nt) * 16 + 16 + 16 * kMixThreads) * sizeof(T) +
                         16 * kMixThreads * sizeof(int);
@@ -2367,6 +2402,12 @@ int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[
     SFW3D_TRY(corr_pass_impl(ctx, dtype, t2, terms + size_t(t) * n * es, dims, 0, tp, s->tlo[0][t],
                              l0, nullptr, 0.0, 1.0, "eta_basis"));
   }
+  if (!fields && ring2_all_ok(s, dtype, dims)) {
+    if (dtype == SFW3D_F64)
+      SFW3D_TRY(launch_ring2_all<double>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial));
+    else
+      SFW3D_TRY(launch_ring2_all<float>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial));
+  } else
   for (int m0 = 0; m0 < nm; m0 += kMixMax) {
     const int nmm = std::min(kMixMax, nm - m0);
     SFW3D_PROF(ctx, "eta_mix");
@@ -2438,8 +2479,11 @@ int basis_set_collect(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int di
     }
     fprintf(stderr, "[collect] %d of %d CTAs qualify\n", any, nblocks);
   }
-  for (int m0 = 0; m0 < nm; m0 += kMixMax) {
-    const int nmm = std::min(kMixMax, nm - m0);
+  // (16-member slices when the evaluation ran through mix_ring2_kernel: the
+  // V = 4 collect kernel keeps 16 x 4 accumulators in registers)
+  const int step = (!fields && ring2_all_ok(s, dtype, dims)) ? 16 : kMixMax;
+  for (int m0 = 0; m0 < nm; m0 += step) {
+    const int nmm = std::min(step, nm - m0);
     SFW3D_PROF(ctx, "eta_refine");
     if (dtype == SFW3D_F64)
       SFW3D_TRY(launch_mix<double>(ctx, nblocks * kSplit, b, terms, n, nt, nmm, m0, s, dims, wlo,
