@@ -548,9 +548,9 @@ void fit_signed_members(BasisSet* s, const std::vector<BasisCandidate>& cands, i
 // voxels (SFW3D_BASIS_LOOSE=0 disables)
 constexpr double kLooseF32 = 1e-5;
 double basis_loose_tol(int dtype) {
-  if (dtype != SFW3D_F32) return 0.0;
-  const char* e = getenv("SFW3D_BASIS_LOOSE");
-  return e ? atof(e) : kLooseF32;
+  const char* e = getenv(dtype == SFW3D_F32 ? "SFW3D_BASIS_LOOSE" : "SFW3D_BASIS_LOOSE64");
+  if (e) return atof(e);
+  return dtype == SFW3D_F32 ? kLooseF32 : 0.0;
 }
 
 int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands, int dtype,
@@ -1780,23 +1780,27 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
   const long long twrap = vstep - (long long)K * nstride;
   const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(myslot));
   constexpr unsigned kSlotB = kSlot * sizeof(T), kRingB = NS * kSlotB;
+  static_assert((kRingB & (kRingB - 1)) == 0, "ring bytes are a power of two");
   int pe = 0, pleft = G;
   unsigned poff = 0, coff = 0;
+  // branch-free: past the end of the stream the copy has src-size 0 (no
+  // global read, the slot is zero-filled and never consumed)
   auto issue = [&]() {
     const char* a = pe == 0 ? bq : tq;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + poff), "l"(a));
-    poff = poff + kSlotB == kRingB ? 0u : poff + kSlotB;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sbase + poff), "l"(a),
+                 "r"(pleft > 0 ? 16 : 0));
+    poff = (poff + kSlotB) & (kRingB - 1);
     --pleft;
-    if (pe != 0) tq += nstride;
-    if (++pe == E) {
-      pe = 0;
-      bq += vstep;
-      tq += twrap;
-    }
+    tq += pe != 0 ? nstride : 0LL;
+    ++pe;
+    const bool wrap = pe == E;
+    pe = wrap ? 0 : pe;
+    bq += wrap ? vstep : 0LL;
+    tq += wrap ? twrap : 0LL;
   };
 #pragma unroll
   for (int g = 0; g < NS - 1; ++g) {
-    if (pleft > 0) issue();
+    issue();
     cp_async_commit();
   }
   auto take = [&](T (&v)[V]) {
@@ -1809,8 +1813,8 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
       const double2 q = *reinterpret_cast<const double2*>(sl);
       v[0] = q.x; v[1] = q.y;
     }
-    coff = coff + kSlotB == kRingB ? 0u : coff + kSlotB;
-    if (pleft > 0) issue();
+    coff = (coff + kSlotB) & (kRingB - 1);
+    issue();
     cp_async_commit();
   };
   // running maximum of member slot m over this vector's V voxels
@@ -1845,11 +1849,32 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
       }
     }
   };
-  for (int it = 0; it < iters; ++it) {
-    const long long i0 = (qbeg + (long long)it * kMixThreads) * V;
-    const int z0 = int(i0 % nz);
+  // voxel position of this thread's vector, advanced incrementally (one
+  // kMixThreads * V step per iteration) instead of divided out per vector
+  const int step = kMixThreads * V;
+  const int dzs = step % nz, dys = step / nz;
+  int z0 = 0, y = 0, x = 0;
+  if (iters > 0) {
+    const long long i0 = qbeg * V;
+    z0 = int(i0 % nz);
     const long long row = i0 / nz;
-    const int y = int(row % ny), x = int(row / ny);
+    y = int(row % ny);
+    x = int(row / ny);
+  }
+  for (int it = 0; it < iters; ++it) {
+    if (it > 0) {
+      z0 += dzs;
+      y += dys;
+      if (z0 >= nz) {
+        z0 -= nz;
+        ++y;
+      }
+      while (y >= ny) {
+        y -= ny;
+        ++x;
+      }
+    }
+    const long long i0 = (qbeg + (long long)it * kMixThreads) * V;
     const bool row_win = x >= wlo.x && x <= whi.x && y >= wlo.y && y <= whi.y;
     const bool zfull = z0 >= wlo.z && z0 + V - 1 <= whi.z;
     T acc[NMD][V];
@@ -1881,34 +1906,15 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
 #pragma unroll
         for (int j = 0; j < V; ++j) acc[m][j] = fma(wv[m], v[j], acc[m][j]);
       const int c = sCt[k];
-      if (c >= 0) {  // a copy member's eta * lam is T_k itself
-        if (fields) {
-          T f[V];
-#pragma unroll
-          for (int j = 0; j < V; ++j) f[j] = T(double(v[j]) / lam);
-          T* dst = fields + (long long)cid[cmem[c]] * n + i0;
-          if constexpr (sizeof(T) == 4)
-            __stcs(reinterpret_cast<float4*>(dst), make_float4(f[0], f[1], f[2], f[3]));
-          else
-            __stcs(reinterpret_cast<double2*>(dst), make_double2(f[0], f[1]));
-        }
-        if (row_win) track(NMD + c, v, i0, zfull, z0);
-      }
+      if (c >= 0 && row_win) track(NMD + c, v, i0, zfull, z0);  // a copy's eta * lam is T_k
     }
 #pragma unroll
-    for (int m = 0; m < NMD; ++m) {
-      if (m >= nmd) break;
-      if (fields) {
-        T f[V];
+    if (row_win) {
 #pragma unroll
-        for (int j = 0; j < V; ++j) f[j] = T(double(acc[m][j]) / lam);
-        T* dst = fields + (long long)cid[dmem[m]] * n + i0;
-        if constexpr (sizeof(T) == 4)
-          __stcs(reinterpret_cast<float4*>(dst), make_float4(f[0], f[1], f[2], f[3]));
-        else
-          __stcs(reinterpret_cast<double2*>(dst), make_double2(f[0], f[1]));
+      for (int m = 0; m < NMD; ++m) {
+        if (m >= nmd) break;
+        track(m, acc[m], i0, zfull, z0);
       }
-      if (row_win) track(m, acc[m], i0, zfull, z0);
     }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -2229,18 +2235,20 @@ template <typename T>
 static int launch_ring2_all(sfw3d_ctx* ctx, int nblocks, const void* b, const void* terms,
                             long long n, int nt, const BasisSet* s, const int dims[3], int4 wlo,
                             int4 whi, double lam, Best* partial) {
+  // ring depth: 16 slots (fp32); 8 for fp64 (keeps 2 CTAs per SM)
+  constexpr int NS = sizeof(T) == 8 ? 8 : 16;
   for (int d0 = 0; d0 < std::max(s->nmd, 1); d0 += 16) {
     const int dn = std::max(0, std::min(16, s->nmd - d0));
     const bool cp = d0 == 0;
     SFW3D_PROF(ctx, "eta_mix");
     if (dn <= 4)
-      SFW3D_TRY((launch_ring2<T, 4, 16>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp)));
+      SFW3D_TRY((launch_ring2<T, 4, NS>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp)));
     else if (dn <= 8)
-      SFW3D_TRY((launch_ring2<T, 8, 16>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp)));
+      SFW3D_TRY((launch_ring2<T, 8, NS>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp)));
     else if (dn <= 12)
-      SFW3D_TRY((launch_ring2<T, 12, 16>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp)));
+      SFW3D_TRY((launch_ring2<T, 12, NS>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp)));
     else
-      SFW3D_TRY((launch_ring2<T, 16, 16>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp)));
+      SFW3D_TRY((launch_ring2<T, 16, NS>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp)));
     SFW3D_LAUNCH_CHECK(ctx);
   }
   return SFW3D_OK;

@@ -1,5 +1,5 @@
-"""Per-family device time of one config-3 certificate (256^3 fp32, 8 x 6
-candidates) on a synthetic residual."""
+"""Per-family device time of one config-2 (128^3 f64) or config-3 (256^3
+fp32) certificate on a synthetic residual: python tools/cert_cfg3.py [2|3]"""
 import sys
 from pathlib import Path
 
@@ -12,10 +12,13 @@ from paper_2009_05473_b200 import _native as N, configs  # noqa: E402
 from paper_2009_05473_b200.certificate import eta_argmax_dev  # noqa: E402
 from paper_2009_05473_b200.forward import psf_apply_dev, render_dev  # noqa: E402
 
-inst = configs.config3(0)
-P.set_precision("f32")
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+inst = {2: configs.config2, 3: configs.config3}[cfg](0)
+P.set_precision(inst.precision)
 psf = P.Psf(P.Volume(inst.kernel), normalize=False)
-r = 0.01 * torch.randn(inst.dims, device="cuda") + psf_apply_dev(psf, render_dev(inst.truth, inst.dims, N.F32), False)
+code = N.dtype_code()
+clean = psf_apply_dev(psf, render_dev(inst.truth, inst.dims, code), False)
+r = 0.01 * torch.randn(inst.dims, device="cuda", dtype=clean.dtype) + clean
 table = P.build_template_table(psf, inst.sigma_grid, inst.shape_grid, bounds=inst.bounds)
 win = ((0, inst.dims[0] - 1), (0, inst.dims[1] - 1), (0, inst.dims[2] - 1))
 for _ in range(3):
