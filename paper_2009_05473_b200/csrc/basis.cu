@@ -1738,10 +1738,12 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
     const T* __restrict__ Wd, const T* __restrict__ w0d, const int* __restrict__ dmem, int nmd,
     const int* __restrict__ cterm, int nmc, const int* __restrict__ cmem,
     const int* __restrict__ cid, int nx, int ny, int nz, int4 wlo, int4 whi, double lam,
-    T* __restrict__ fields, Best* __restrict__ partial) {
+    double* __restrict__ absparts, Best* __restrict__ partial) {
   constexpr int V = 16 / sizeof(T);
   constexpr int NMC = 8;  // copy members (at most)
   static_assert((NS & (NS - 1)) == 0, "ring depth is a power of two");
+  double abs_s = 0.0;  // sum |b| (fp64) and max |b| of the vectors read (absparts)
+  T abs_m = T(0);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* ring = reinterpret_cast<T*>(smem_raw);                       // [NS][threads][V]
   T* sW = ring + NS * kMixThreads * V;                            // [K][NMD], 16-byte rows
@@ -1885,6 +1887,13 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
       for (int m = 0; m < NMD; ++m)
 #pragma unroll
         for (int j = 0; j < V; ++j) acc[m][j] = sw0[m] * v[j];
+      if (absparts) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          abs_s += double(fabs(v[j]));
+          abs_m = fmax(abs_m, fabs(v[j]));
+        }
+      }
     }
     for (int k = 0; k < K; ++k) {
       T v[V];
@@ -1941,6 +1950,29 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
         if (better(red[m][w].v, red[m][w].idx, bm.v, bm.idx)) bm = red[m][w];
       const int mem = m < NMD ? dmem[m] : cmem[m - NMD];  // member index
       partial[(long long)mem * gridDim.x + blockIdx.x] = bm;
+    }
+  }
+  if (absparts) {  // per-CTA |b| statistics (fixed-order reduce: abs_reduce_kernel)
+    double ds = abs_s, dm = double(abs_m);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ds += __shfl_xor_sync(0xffffffffu, ds, o);
+      dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+    }
+    __shared__ double sa[kMixThreads / 32][2];
+    if (lane == 0) {
+      sa[warp][0] = ds;
+      sa[warp][1] = dm;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0, mm = 0.0;
+      for (int w = 0; w < kMixThreads / 32; ++w) {
+        t += sa[w][0];
+        mm = fmax(mm, sa[w][1]);
+      }
+      absparts[2 * blockIdx.x] = t;
+      absparts[2 * blockIdx.x + 1] = mm;
     }
   }
 }
@@ -2111,6 +2143,19 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_mma_kernel(
   }
 }
 
+// [sum |b|, max |b|] from the mix's per-CTA statistics, fixed order
+__global__ void abs_reduce_kernel(const double* __restrict__ parts, int nblocks,
+                                  double* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  double t = 0.0, m = 0.0;
+  for (int b = 0; b < nblocks; ++b) {
+    t += parts[2 * b];
+    m = fmax(m, parts[2 * b + 1]);
+  }
+  out[0] = t;
+  out[1] = m;
+}
+
 __global__ void member_reduce_kernel(const Best* __restrict__ partial, int nblocks,
                                      const int* __restrict__ cid, Best* __restrict__ best_dev) {
   __shared__ Best sb[32];
@@ -2173,7 +2218,7 @@ size_t basis_set_scratch(const BasisSet* s, long long n, int dtype, const int di
   const size_t es = dtype == SFW3D_F64 ? 8 : 4;
   const long long nb = std::max<long long>(4096, eval_blocks(s, dtype, dims, 4096));
   return Carver::need({size_t(n) * es, size_t(n) * es, size_t(n) * es * s->betas.size(),
-                       s->members.size() * size_t(nb) * sizeof(Best)});
+                       s->members.size() * size_t(nb) * sizeof(Best), 2 * size_t(nb) * sizeof(double)});
 }
 
 template <typename T, int NM, int V>
@@ -2205,7 +2250,8 @@ static int launch_mix_nm(sfw3d_ctx* ctx, int nblocks, const void* b, const void*
 template <typename T, int NMD, int NS>
 static int launch_ring2(sfw3d_ctx* ctx, int nblocks, const void* b, const void* terms, long long n,
                         int nt, const BasisSet* s, const int dims[3], int4 wlo, int4 whi,
-                        double lam, Best* partial, int d0 = 0, int dn = -1, bool copies = true) {
+                        double lam, Best* partial, int d0 = 0, int dn = -1, bool copies = true,
+                        double* absparts = nullptr) {
   if (dn < 0) dn = s->nmd;
   constexpr int V4 = 16 / sizeof(T);
   const size_t smem = size_t(NS) * kMixThreads * V4 * sizeof(T) + size_t(nt + 1) * 8 +
@@ -2218,7 +2264,7 @@ static int launch_ring2(sfw3d_ctx* ctx, int nblocks, const void* b, const void* 
       static_cast<const T*>(b), static_cast<const T*>(terms), n, nt,
       static_cast<const T*>(s->Wd_dev) + size_t(d0) * nt, static_cast<const T*>(s->w0d_dev) + d0,
       s->dmem_dev + d0, dn, s->cterm_dev, copies ? s->nmc : 0, s->cmem_dev, s->cid_dev, dims[0],
-      dims[1], dims[2], wlo, whi, lam, nullptr, partial);
+      dims[1], dims[2], wlo, whi, lam, absparts, partial);
   return SFW3D_OK;
 }
 
@@ -2234,7 +2280,7 @@ static bool ring2_all_ok(const BasisSet* s, int dtype, const int dims[3]) {
 template <typename T>
 static int launch_ring2_all(sfw3d_ctx* ctx, int nblocks, const void* b, const void* terms,
                             long long n, int nt, const BasisSet* s, const int dims[3], int4 wlo,
-                            int4 whi, double lam, Best* partial) {
+                            int4 whi, double lam, Best* partial, double* absparts = nullptr) {
   // ring depth: 16 slots (fp32); 8 for fp64 (keeps 2 CTAs per SM)
   constexpr int NS = sizeof(T) == 8 ? 8 : 16;
   for (int d0 = 0; d0 < std::max(s->nmd, 1); d0 += 16) {
@@ -2242,13 +2288,13 @@ static int launch_ring2_all(sfw3d_ctx* ctx, int nblocks, const void* b, const vo
     const bool cp = d0 == 0;
     SFW3D_PROF(ctx, "eta_mix");
     if (dn <= 4)
-      SFW3D_TRY((launch_ring2<T, 4, NS>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp)));
+      SFW3D_TRY((launch_ring2<T, 4, NS>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp, cp ? absparts : nullptr)));
     else if (dn <= 8)
-      SFW3D_TRY((launch_ring2<T, 8, NS>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp)));
+      SFW3D_TRY((launch_ring2<T, 8, NS>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp, cp ? absparts : nullptr)));
     else if (dn <= 12)
-      SFW3D_TRY((launch_ring2<T, 12, NS>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp)));
+      SFW3D_TRY((launch_ring2<T, 12, NS>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp, cp ? absparts : nullptr)));
     else
-      SFW3D_TRY((launch_ring2<T, 16, NS>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp)));
+      SFW3D_TRY((launch_ring2<T, 16, NS>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp, cp ? absparts : nullptr)));
     SFW3D_LAUNCH_CHECK(ctx);
   }
   return SFW3D_OK;
@@ -2359,7 +2405,9 @@ static int launch_xmix(sfw3d_ctx* ctx, const BasisSet* s, const int dims[3], con
 }
 
 int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[3], const void* b,
-                   double lam, const int32_t win[6], void* fields, Best* best_dev, void* scratch) {
+                   double lam, const int32_t win[6], void* fields, Best* best_dev, void* scratch,
+                   double* abs_dev, bool* abs_done) {
+  if (abs_done) *abs_done = false;
   const int nm = fields ? s->n_nnls : int(s->members.size()), nt = int(s->betas.size());
   if (nm == 0) return SFW3D_OK;
   const long long n = vol_count(dims);
@@ -2374,6 +2422,7 @@ int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[
   char* terms = cv.take<char>(size_t(n) * es * nt);
   const int nblocks = int(eval_blocks(s, dtype, dims, ctx->num_sms));
   Best* partial = cv.take<Best>(size_t(nm) * nblocks);
+  double* absparts = cv.take<double>(2 * size_t(nblocks));
   const int4 wlo = make_int4(win[0], win[2], win[4], 0), whi = make_int4(win[1], win[3], win[5], 0);
   if (xmix_ok(s, dtype, dims)) {
     // U_k = f_k^(y) f_k^(z) * b per term, then the fused x pass + mix
@@ -2411,10 +2460,16 @@ int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[
                              l0, nullptr, 0.0, 1.0, "eta_basis"));
   }
   if (!fields && ring2_all_ok(s, dtype, dims)) {
+    double* ap = abs_dev ? absparts : nullptr;  // |b| statistics ride along with the mix
     if (dtype == SFW3D_F64)
-      SFW3D_TRY(launch_ring2_all<double>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial));
+      SFW3D_TRY(launch_ring2_all<double>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, ap));
     else
-      SFW3D_TRY(launch_ring2_all<float>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial));
+      SFW3D_TRY(launch_ring2_all<float>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, ap));
+    if (ap) {
+      abs_reduce_kernel<<<1, 32, 0, ctx->stream>>>(ap, nblocks, abs_dev);
+      SFW3D_LAUNCH_CHECK(ctx);
+      if (abs_done) *abs_done = true;
+    }
   } else
   for (int m0 = 0; m0 < nm; m0 += kMixMax) {
     const int nmm = std::min(kMixMax, nm - m0);

@@ -73,8 +73,11 @@ size_t basis_set_scratch(const BasisSet* s, long long n, int dtype, const int di
 // eta for all members: best_dev[cand] receives each member's windowed
 // argmax; fields (n_cand volumes, candidate-major) are written when non-NULL
 // (then the signed members are skipped: their values are not certified).
+// abs_dev (optional, device [2]): receives [sum |b|, max |b|] when the mix
+// computed them on the way (*abs_done = true), saving a separate pass over b.
 int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[3], const void* b,
-                   double lam, const int32_t win[6], void* fields, Best* best_dev, void* scratch);
+                   double lam, const int32_t win[6], void* fields, Best* best_dev, void* scratch,
+                   double* abs_dev = nullptr, bool* abs_done = nullptr);
 
 // Refinement support (inexact / signed members): re-runs the fused mix over
 // the terms basis_set_eval left in `scratch` (same `fields` flag; only the

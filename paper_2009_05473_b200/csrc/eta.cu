@@ -1026,18 +1026,22 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   const int budget = std::min(smem_max - 2048, 110 * 1024);
   // every basis member at once: shared separable terms + fused mix/argmax,
   // writing cbest[cand] (and the member fields) directly
+  bool abs_done = false;
   if (any_basis)
-    SFW3D_TRY(basis_set_eval(ctx, bset, dtype, dims, b, lam, win, fields, cbest, bscratch));
+    SFW3D_TRY(basis_set_eval(ctx, bset, dtype, dims, b, lam, win, fields, cbest, bscratch,
+                             any_refine ? ref_l1 : nullptr, &abs_done));
   if (any_refine) {
     // Every refined member's approximate eta~ is within E_c of its direct
     // value at every voxel: signed members E_c = ebound_c ||b||_inf / lam
     // (basis.cu), fp64 non-negative members E_c = (e_c + 2e-12) ||b||_1 / lam.
     // The true maximum lies among the voxels with eta~ >= max eta~ - 2 E_c.
     SFW3D_PROF(ctx, "eta_refine");
-    SFW3D_CUDA_TRY(cudaMemsetAsync(ref_l1, 0, 2 * sizeof(double), ctx->stream));
-    abs_sum_kernel<T><<<4 * ctx->num_sms, 256, 0, ctx->stream>>>(
-        b, n, ref_l1, reinterpret_cast<unsigned long long*>(ref_l1 + 1));
-    SFW3D_LAUNCH_CHECK(ctx);
+    if (!abs_done) {  // (the mix computes them when it streams b: mix_ring2_kernel)
+      SFW3D_CUDA_TRY(cudaMemsetAsync(ref_l1, 0, 2 * sizeof(double), ctx->stream));
+      abs_sum_kernel<T><<<4 * ctx->num_sms, 256, 0, ctx->stream>>>(
+          b, n, ref_l1, reinterpret_cast<unsigned long long*>(ref_l1 + 1));
+      SFW3D_LAUNCH_CHECK(ctx);
+    }
     std::vector<Best> hb0(nc);
     double l1[2] = {0.0, 0.0};
     SFW3D_TRY(download_sync(ctx, hb0.data(), cbest, size_t(nc) * sizeof(Best)));
