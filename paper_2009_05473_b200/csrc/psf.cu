@@ -349,6 +349,117 @@ __global__ void __launch_bounds__(NT, MINB) pass_tile2_kernel(
   }
 }
 
+// Persistent, double-buffered variant of pass_tile2_kernel (no addend,
+// w = 1): each CTA walks tiles t = blockIdx.x, + gridDim.x, ... (axis-major
+// order, so consecutive tiles of a CTA share nothing but neighbours in the
+// grid share halos through L2) and stages tile t + 1 with cp.async while it
+// computes tile t, so the staging latency overlaps the FFMA work instead of
+// relying on other resident CTAs.
+template <typename T, int J, int TI, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) pass_tile2p_kernel(
+    const T* __restrict__ in, T* __restrict__ out, int n_axis, long long stride,
+    const T* __restrict__ taps_g, int lo, int ntaps, int tiles_x, int tiles_y, long long ntiles) {
+  constexpr int G = NT / TI, To = J * G;
+  constexpr int kVec = 16 / sizeof(T), kRowVecs = TI / kVec;
+  static_assert(NT % kRowVecs == 0, "row vectors");
+  constexpr int dr = NT / kRowVecs;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int nt4 = (ntaps + 3) & ~3;
+  const int rows = To + nt4;
+  T* taps = reinterpret_cast<T*>(smem_raw);
+  T* const stage0 = taps + nt4;
+  const int stage_elems = rows * TI;
+  for (int q = threadIdx.x; q < nt4; q += NT) taps[q] = q < ntaps ? taps_g[q] : T(0);
+  const int c = (threadIdx.x % kRowVecs) * kVec;
+  auto tile_of = [&](long long t, int& a0, long long& base0) {
+    const int bx = int(t % tiles_x);
+    const long long rest = t / tiles_x;
+    const int by = int(rest % tiles_y);
+    const long long bz = rest / tiles_y;
+    a0 = bx * To;
+    base0 = bz * n_axis * stride + (long long)by * TI;
+  };
+  auto load = [&](long long t, T* tile) {
+    int a0;
+    long long base0;
+    tile_of(t, a0, base0);
+    int r = threadIdx.x / kRowVecs;
+    int a = (a0 + lo + r) % n_axis;
+    if (a < 0) a += n_axis;
+    const T* src = in + base0 + c;
+    T* dst = tile + r * TI + c;
+    if (a0 + lo >= 0 && a0 + lo + rows <= n_axis) {
+      const long long step = (long long)dr * stride;
+      const T* p = src + (long long)a * stride;
+      for (; r < rows; r += dr, dst += dr * TI, p += step) cp_async16(dst, p);
+    } else {
+      for (; r < rows; r += dr, dst += dr * TI) {
+        cp_async16(dst, src + (long long)a * stride);
+        a = (a + dr) % n_axis;
+      }
+    }
+  };
+  const int il = threadIdx.x % TI, ag = threadIdx.x / TI;
+  long long t = blockIdx.x;
+  if (t < ntiles) load(t, stage0);
+  cp_async_commit();
+  for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
+    const long long tn = t + gridDim.x;
+    if (tn < ntiles) load(tn, stage0 + ((i + 1) & 1) * stage_elems);
+    cp_async_commit();
+    cp_async_wait_group<1>();
+    __syncthreads();
+    const T* src = stage0 + (i & 1) * stage_elems + (ag * J) * TI + il;
+    T W[J], acc[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      W[j] = src[j * TI];
+      acc[j] = T(0);
+    }
+    int q0 = 0;
+    for (; q0 + J <= nt4; q0 += J) {
+#pragma unroll
+      for (int r = 0; r < J; r += 4) {
+        T t4[4];
+        ld4(taps + q0 + r, t4[0], t4[1], t4[2], t4[3]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+#pragma unroll
+          for (int j = 0; j < J; ++j) acc[j] = fma(t4[k], W[(r + k + j) % J], acc[j]);
+          W[r + k] = src[(q0 + r + k + J) * TI];
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < J; r += 4) {
+      if (q0 + r >= nt4) break;
+      T t4[4];
+      ld4(taps + q0 + r, t4[0], t4[1], t4[2], t4[3]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+#pragma unroll
+        for (int j = 0; j < J; ++j) acc[j] = fma(t4[k], W[(r + k + j) % J], acc[j]);
+        W[r + k] = src[(q0 + r + k + J) * TI];
+      }
+    }
+    int a0;
+    long long base0;
+    tile_of(t, a0, base0);
+    const int a1 = a0 + ag * J;
+    T* po = out + base0 + (long long)a1 * stride + il;
+    if (a1 + J <= n_axis) {
+#pragma unroll
+      for (int j = 0; j < J; ++j, po += stride) *po = acc[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < J; ++j, po += stride)
+        if (a1 + j < n_axis) *po = acc[j];
+    }
+    __syncthreads();  // the stage is refilled two iterations on
+  }
+  cp_async_wait_group<0>();
+}
+
 // Contiguous axis (2), nz % 4 == 0: a CTA owns 32 rows (lane = row) x 4 J
 // outputs (warp = J-column group). The staged row span starts at the aligned
 // column floor4(z0 + lo); the misalignment sh = lo mod 4 is absorbed by sh
@@ -782,6 +893,31 @@ int launch_tile2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axi
   return SFW3D_OK;
 }
 
+template <typename T, int J, int MINB>
+int launch_tile2p(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis, const T* taps,
+                  int lo, int ntaps) {
+  constexpr int TI = 64, NT = 256, To = J * (NT / TI);
+  long long stride = 1;
+  for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
+  long long outer = 1;
+  for (int a = 0; a < axis; ++a) outer *= dims[a];
+  const int n = dims[axis];
+  const int nt4 = (ntaps + 3) & ~3;
+  const size_t smem = (size_t(nt4) + 2 * size_t(To + nt4) * TI) * sizeof(T);
+  SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_tile2p_kernel<T, J, TI, NT, MINB>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  int per_sm = 0;
+  SFW3D_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, pass_tile2p_kernel<T, J, TI, NT, MINB>, NT, smem));
+  const int tiles_x = (n + To - 1) / To, tiles_y = int(stride / TI);
+  const long long ntiles = (long long)tiles_x * tiles_y * outer;
+  const long long grid = std::min<long long>(ntiles, (long long)std::max(per_sm, 1) * ctx->num_sms);
+  pass_tile2p_kernel<T, J, TI, NT, MINB><<<unsigned(grid), NT, smem, ctx->stream>>>(
+      in, out, n, stride, taps, lo, ntaps, tiles_x, tiles_y, ntiles);
+  SFW3D_LAUNCH_CHECK(ctx);
+  return SFW3D_OK;
+}
+
 template <typename T, int J, int MINB = 1>
 int launch_z2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* taps, int lo,
               int ntaps, const T* addend, double aw, double w) {
@@ -863,6 +999,18 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
   }
   long long stride = 1;
   for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
+  {
+    const char* e = getenv("SFW3D_TILE2P");  // persistent double-buffered strided passes
+    const int tp = e ? atoi(e) : 0;           // bit 0: narrow (J = 16), bit 1: wide (J = 32)
+    if (tp && sizeof(T) == 4 && v2 == 0 && stride % 64 == 0 && ntaps <= 512 && !addend && aw == 0.0 && w == 1.0 &&
+        dims[axis] >= 128) {
+      if (ntaps > narrow_taps()) {
+        if (tp & 2) return launch_tile2p<T, 32, 2>(ctx, in, out, dims, axis, taps, lo, ntaps);
+      } else if (tp & 1) {
+        return launch_tile2p<T, 16, 3>(ctx, in, out, dims, axis, taps, lo, ntaps);
+      }
+    }
+  }
   if (v2 == 0 && stride % 64 == 0 && ntaps <= 512) {
     static const int nt128 = [] {
       const char* e = getenv("SFW3D_TILE2_NT");
