@@ -268,3 +268,33 @@ def test_slab_certificate_matches_global(P, nranks, prec, monkeypatch):
     pos, _, val, _, _ = O.eta_field(r, 0.7, hats, len(dg))
     assert tuple(best.pos) == tuple(pos)
     assert abs(v - val) <= (1e-5 if prec == "f32" else 1e-10) * abs(val)
+
+
+def test_many_members_ring_slices_vs_oracle(P):
+    """48 candidates (config 3's 8 sigma x 6 d grid) in fp32: the dense members
+    go through mix_ring2_kernel in 16-member slices (copies with the first),
+    the refinement's collect pass in matching 16-member V = 4 slices; every
+    candidate's windowed maximum and position equal the FFT oracle's."""
+    import torch
+    rng = np.random.default_rng(12)
+    dims = (48, 40, 64)
+    kernel = O.box_gaussian_psf(dims, (1.5, 1.5, 1.5), (4, 4, 4))
+    rows = np.column_stack([rng.uniform(3, 6, 5), rng.uniform(8, 36, (5, 3)),
+                            rng.uniform(1, 3, 5), rng.uniform(1.5, 2.5, 5)])
+    r = rng.standard_normal(dims) + O.conv(O.render(rows, dims), O.psf_hat(kernel))
+    r = r.astype(np.float32).astype(np.float64)
+    sg, dg = np.geomspace(1, 3, 8), np.linspace(1.5, 2.5, 6)
+    win = ((2, 45), (0, 39), (3, 60))
+    hats = O.template_hats(O.psf_hat(kernel), dims, sg, dg)
+    _, _, val, per, _ = O.eta_field(r, 0.8, hats, len(dg), win)
+    psf = P.Psf(P.Volume(kernel), normalize=False)
+    with P.precision("f32"):
+        table = P.build_template_table(psf, sg, dg)
+        assert table.info()["n_basis"] > 16
+        rd = torch.tensor(r, device="cuda", dtype=torch.float32)
+        best, recs, _ = P.certificate.eta_argmax_dev(rd, 0.8, table, win)
+    assert abs(best.value - val) <= 1e-5 * abs(val)
+    for c, rec in enumerate(recs):
+        pos, v = per[c]
+        assert abs(rec.value - v) <= 1e-5 * abs(val), (c, rec.value, v)
+        assert tuple(rec.pos) == tuple(pos), (c, tuple(rec.pos), pos)
