@@ -57,13 +57,65 @@ __global__ void __launch_bounds__(256) residual_kernel(const T* __restrict__ y,
                                                        long long n, T* __restrict__ out,
                                                        double* __restrict__ partials) {
   double s = 0.0;
-  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+  // V consecutive voxels per thread (16-byte loads) and 4 atoms' loads issued
+  // before their (in-order) updates: the k streams are read with enough
+  // loads in flight; the per-voxel update order is the reference's
+  constexpr int V = 16 / sizeof(T);
+  const long long nv = n / V;
+  for (long long q = blockIdx.x * 256LL + threadIdx.x; q < nv; q += (long long)gridDim.x * 256) {
+    const long long i = q * V;
+    T r[V];
+#pragma unroll
+    for (int u = 0; u < V; ++u) r[u] = y[i + u];
+    int j = 0;
+    for (; j + 4 <= k; j += 4) {
+      T ph[4][V];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        if constexpr (sizeof(T) == 8) {
+          const double2 v = __ldg(reinterpret_cast<const double2*>(phis[j + a] + i));
+          ph[a][0] = v.x; ph[a][1] = v.y;
+        } else {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(phis[j + a] + i));
+          ph[a][0] = v.x; ph[a][1] = v.y; ph[a][2] = v.z; ph[a][3] = v.w;
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const double wj = w[j + a];
+#pragma unroll
+        for (int u = 0; u < V; ++u) {
+          if constexpr (sizeof(T) == 8)
+            r[u] = __dsub_rn(r[u], __dmul_rn(wj, ph[a][u]));  // data -= w * phi
+          else
+            r[u] = T(double(r[u]) - wj * double(ph[a][u]));
+        }
+      }
+    }
+    for (; j < k; ++j) {
+      const double wj = w[j];
+#pragma unroll
+      for (int u = 0; u < V; ++u) {
+        if constexpr (sizeof(T) == 8)
+          r[u] = __dsub_rn(r[u], __dmul_rn(wj, phis[j][i + u]));
+        else
+          r[u] = T(double(r[u]) - wj * double(phis[j][i + u]));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      if (out) out[i + u] = r[u];
+      s += double(r[u]) * double(r[u]);
+    }
+  }
+  // (tail voxels when n is not a multiple of V)
+  for (long long i = nv * V + blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
     T r = y[i];
-    for (int j = 0; j < k; ++j) {
+    for (int j2 = 0; j2 < k; ++j2) {
       if constexpr (sizeof(T) == 8)
-        r = __dsub_rn(r, __dmul_rn(w[j], phis[j][i]));  // data -= w * phi
+        r = __dsub_rn(r, __dmul_rn(w[j2], phis[j2][i]));
       else
-        r = T(double(r) - w[j] * double(phis[j][i]));
+        r = T(double(r) - w[j2] * double(phis[j2][i]));
     }
     if (out) out[i] = r;
     s += double(r) * double(r);
