@@ -25,7 +25,26 @@ __global__ void __launch_bounds__(kDotThreads) dots_kernel(const T* const* __res
                                                            double* __restrict__ partials) {
   const T* a = vecs[blockIdx.y];
   double s = 0.0;
-  for (long long i = blockIdx.x * (long long)kDotThreads + threadIdx.x; i < n;
+  // 16-byte loads (fixed partition: the sum order depends only on n)
+  constexpr int V = 16 / sizeof(T);
+  const long long nv = n / V;
+  for (long long q = blockIdx.x * (long long)kDotThreads + threadIdx.x; q < nv;
+       q += (long long)kDotBlocks * kDotThreads) {
+    if constexpr (sizeof(T) == 8) {
+      const double2 x = __ldg(reinterpret_cast<const double2*>(a) + q);
+      const double2 z = __ldg(reinterpret_cast<const double2*>(v) + q);
+      s += x.x * z.x;
+      s += x.y * z.y;
+    } else {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(a) + q);
+      const float4 z = __ldg(reinterpret_cast<const float4*>(v) + q);
+      s += double(x.x) * double(z.x);
+      s += double(x.y) * double(z.y);
+      s += double(x.z) * double(z.z);
+      s += double(x.w) * double(z.w);
+    }
+  }
+  for (long long i = nv * V + blockIdx.x * (long long)kDotThreads + threadIdx.x; i < n;
        i += (long long)kDotBlocks * kDotThreads)
     s += double(a[i]) * double(v[i]);
   __shared__ double red[kDotThreads / 32];

@@ -771,8 +771,11 @@ int launch_zy_t(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T*
 template <typename T>
 int launch_zy(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* tz, int loz, int lz,
               const T* ty, int loy, int ly) {
-  const char* e = getenv("SFW3D_ZY_TILE");
-  switch (e ? atoi(e) : 1) {
+  static const int tile = [] {
+    const char* e = getenv("SFW3D_ZY_TILE");
+    return e ? atoi(e) : 1;
+  }();
+  switch (tile) {
     case 0: return launch_zy_t<T, 32, 128, 16, 16>(ctx, in, out, dims, tz, loz, lz, ty, loy, ly);
     case 2: return launch_zy_t<T, 64, 128, 16, 32>(ctx, in, out, dims, tz, loz, lz, ty, loy, ly);
     case 3: return launch_zy_t<T, 32, 64, 8, 8>(ctx, in, out, dims, tz, loz, lz, ty, loy, ly);
@@ -937,8 +940,10 @@ int launch_z2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* t
     SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_z2_kernel<T, J, MINB>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   dim3 grid(unsigned((dims[2] + 4 * J - 1) / (4 * J)), unsigned((nrows + 31) / 32));
-  const char* e = getenv("SFW3D_Z2T");  // bit 0: J = 16, bit 1: J = 32 (measured both faster)
-  const int zt = e ? atoi(e) : 3;
+  static const int zt = [] {  // bit 0: J = 16, bit 1: J = 32 (measured both faster)
+    const char* e = getenv("SFW3D_Z2T");
+    return e ? atoi(e) : 3;
+  }();
   pass_z2_kernel<T, J, MINB><<<grid, 128, smem, ctx->stream>>>(in, out, dims[2], nrows, taps, lo, ntaps,
                                                          pitch, addend, T(aw), T(w), zt);
   SFW3D_LAUNCH_CHECK(ctx);
@@ -1000,8 +1005,10 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
   long long stride = 1;
   for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
   {
-    const char* e = getenv("SFW3D_TILE2P");  // persistent double-buffered strided passes
-    const int tp = e ? atoi(e) : 0;           // bit 0: narrow (J = 16), bit 1: wide (J = 32)
+    static const int tp = [] {  // persistent double-buffered strided passes (opt-in):
+      const char* e = getenv("SFW3D_TILE2P");  // bit 0: narrow (J = 16), bit 1: wide (J = 32)
+      return e ? atoi(e) : 0;
+    }();
     if (tp && sizeof(T) == 4 && v2 == 0 && stride % 64 == 0 && ntaps <= 512 && !addend && aw == 0.0 && w == 1.0 &&
         dims[axis] >= 128) {
       if (ntaps > narrow_taps()) {
