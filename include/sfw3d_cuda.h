@@ -131,6 +131,19 @@ int sfw3d_cost_grad(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void*
                     const double* params_host, int k, double lam, double* cost_host,
                     double* grad_host, void* back_dev);
 
+/* K3-K6 on one rank's x-slab (multi-GPU criterion_and_gradient, SURVEY
+ * §8(e); forward.py:232-257 split over z/x-slabs). `psf` is created on the
+ * window dims (x1 - x0 + 1 + 2 halo, ny, nz), y_dev holds y on the window
+ * planes x0 - halo .. x1 + halo of the periodic (gnx, ny, nz) volume, halo >=
+ * the PSF's x half-extent. Atom x-spans are clipped to the window; the
+ * residual is taken on the slab planes only. Outputs this rank's partials:
+ * half_sumsq = 1/2 sum_slab (model - y)^2 and raw sums_host[6i + c] =
+ * <P_c(atom i), H^T (r 1_slab)> (0 for atoms missing the window). Summed over
+ * ranks: C = half_sumsq + lam sum w, row i = [s0 + lam, w s1..w s5]. */
+int sfw3d_cost_grad_slab(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* y_dev,
+                         const double* params_host, int k, int gnx, int x0, int x1, int halo,
+                         double* half_sumsq_host, double* sums_host);
+
 /* ---- certificate (certificate.py:37-236) ------------------------------ */
 /* K2 — candidate table for the (sigma, d) grid, sigma-major (sorted
  * ascending, as build_template_table sorts them, certificate.py:72-73).

@@ -28,7 +28,7 @@ EXPORTS = (
     "sfw3d_abi_version", "sfw3d_last_error", "sfw3d_ctx_create", "sfw3d_ctx_destroy",
     "sfw3d_ctx_sync", "sfw3d_ctx_launches", "sfw3d_atom_geometry", "sfw3d_psf_create",
     "sfw3d_psf_info", "sfw3d_psf_destroy", "sfw3d_psf_apply", "sfw3d_render",
-    "sfw3d_atom_sums", "sfw3d_cost_grad", "sfw3d_table_create", "sfw3d_table_info",
+    "sfw3d_atom_sums", "sfw3d_cost_grad", "sfw3d_cost_grad_slab", "sfw3d_table_create", "sfw3d_table_info",
     "sfw3d_table_destroy", "sfw3d_eta_argmax", "sfw3d_dots", "sfw3d_nnlasso_cd", "sfw3d_nnlasso_qp",
     "sfw3d_residual", "sfw3d_ctx_profile", "sfw3d_ctx_profile_read", "sfw3d_probe_fp32",
     "sfw3d_table_candidate", "sfw3d_basis_fit", "sfw3d_basis_set_fit",
@@ -61,6 +61,8 @@ _SIGNATURES = {
     "sfw3d_render": (C.c_int, [_vp, C.c_int, _ip, _dp, C.c_int, _vp]),
     "sfw3d_atom_sums": (C.c_int, [_vp, C.c_int, _ip, _vp, _dp, C.c_int, _dp]),
     "sfw3d_cost_grad": (C.c_int, [_vp, _vp, C.c_int, _vp, _dp, C.c_int, C.c_double, _dp, _dp, _vp]),
+    "sfw3d_cost_grad_slab": (C.c_int, [_vp, _vp, C.c_int, _vp, _dp, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.c_int, _dp, _dp]),
     "sfw3d_table_create": (C.c_int, [_vp, _vp, C.c_int, _dp, C.c_int, _dp, C.c_double, C.c_int,
                                      C.c_double, C.POINTER(_vp)]),
     "sfw3d_table_info": (C.c_int, [_vp, C.c_int, _ip, _ip, _ip, C.POINTER(C.c_int64),

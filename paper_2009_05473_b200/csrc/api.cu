@@ -1,5 +1,6 @@
 // C-ABI entry points, context / workspace management, atom geometry and the
 // PSF object. See include/sfw3d_cuda.h for the contract of every function.
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 
@@ -467,3 +468,91 @@ extern "C" int sfw3d_cost_grad(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, 
   return SFW3D_OK;
 }
 
+
+// ------------------------------------------------ slab-local cost + gradient
+// One rank's share of criterion_and_gradient (forward.py:232-257) on its
+// x-slab [x0, x1] of a periodic (gnx, ny, nz) volume. The rank holds the
+// window of planes x0 - halo .. x1 + halo (halo >= the PSF's x half-extent),
+// `psf` is created on those window dims, y_dev is y on the window. Each atom's
+// x-span is clipped to the window (one piece per periodic image that meets
+// it; the unwrapped offsets p - m are kept), so render and the atom sums run
+// on the window only. The residual is formed on the slab planes and zeroed
+// elsewhere, so back = H^T (r 1_slab): summed over ranks, the raw sums and
+// 1/2 ||r||^2 are exactly the single-volume ones (up to summation order).
+extern "C" int sfw3d_cost_grad_slab(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* y_dev,
+                                    const double* params_host, int k, int gnx, int x0, int x1,
+                                    int halo, double* half_sumsq_host, double* sums_host) {
+  SFW3D_CHECK_ARG(ctx && psf && y_dev && half_sumsq_host && sums_host, "NULL argument");
+  SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
+  SFW3D_CHECK_ARG(k >= 0 && (k == 0 || params_host), "params");
+  const int* dims = psf->dims;
+  const int nxl = x1 - x0 + 1 + 2 * halo;
+  SFW3D_CHECK_ARG(gnx > 0 && x0 >= 0 && x1 >= x0 && x1 < gnx && halo >= 0, "slab bounds");
+  SFW3D_CHECK_ARG(dims[0] == nxl && nxl <= gnx, "psf dims[0] must be x1 - x0 + 1 + 2 halo <= gnx");
+  SFW3D_TRY(begin_call(ctx));
+  const int gdims[3] = {gnx, dims[1], dims[2]};
+  std::vector<AtomGeo> atoms;
+  SFW3D_TRY(build_atoms(gdims, params_host, k, atoms));
+  // clip every atom's x-span to the window [gx0, gx0 + nxl) (unwrapped)
+  const int gx0 = x0 - halo;
+  std::vector<AtomGeo> pieces;
+  std::vector<int> owner;
+  for (int i = 0; i < k; ++i) {
+    const AtomGeo& a = atoms[i];
+    if (a.full[0]) {
+      set_error("invalid argument: an atom box spans the x axis; slabs cannot shard it");
+      return SFW3D_EINVAL;
+    }
+    for (int j = -1; j <= 1; ++j) {
+      const int s = a.start[0] + j * gnx;
+      const int lo = std::max(s, gx0), hi = std::min(s + a.len[0], gx0 + nxl);
+      if (lo >= hi) continue;
+      AtomGeo p = a;
+      p.m[0] = a.m[0] + double(j * gnx - gx0);
+      p.start[0] = lo - gx0;
+      p.len[0] = hi - lo;
+      p.nvox = (long long)p.len[0] * p.len[1] * p.len[2];
+      pieces.push_back(p);
+      owner.push_back(i);
+    }
+  }
+  const int kp = int(pieces.size());
+  const int64_t n = vol_count(dims);
+  const size_t es = dtype_size(dtype), vb = size_t(n) * es;
+  SFW3D_TRY(ensure_device(ctx, ctx->ws, Carver::need({vb, vb})));
+  Carver cw(ctx->ws.ptr);
+  char* A = cw.take<char>(vb);
+  char* B = cw.take<char>(vb);
+  const size_t scratch = atom_sums_scratch(pieces);
+  const int nred = 4 * ctx->num_sms;
+  SFW3D_TRY(ensure_device(ctx, ctx->ws_small,
+                          Carver::need({(size_t(kp) + 1) * sizeof(AtomGeo), (size_t(kp) * 6 + 1) * sizeof(double),
+                                        size_t(nred) * sizeof(double), scratch})));
+  Carver cs(ctx->ws_small.ptr);
+  AtomGeo* ad = cs.take<AtomGeo>(kp + 1);
+  double* res = cs.take<double>(size_t(kp) * 6 + 1);
+  double* partials = cs.take<double>(nred);
+  void* scr = cs.take<char>(scratch);
+  SFW3D_TRY(upload_atoms(ctx, pieces, ad));
+  SFW3D_TRY(render_impl(ctx, dtype, dims, ad, kp, A));
+  SFW3D_TRY(psf_apply_impl(ctx, psf, dtype, A, B, 0, A));
+  // r = model - y on the slab planes only, 0 on the halo planes
+  const size_t plane = size_t(dims[1]) * dims[2];
+  const size_t off = size_t(halo) * plane * es;
+  SFW3D_CUDA_TRY(cudaMemsetAsync(A, 0, vb, ctx->stream));
+  SFW3D_TRY(sumsq_diff_impl(ctx, dtype, int64_t(x1 - x0 + 1) * int64_t(plane), B + off,
+                            static_cast<const char*>(y_dev) + off, A + off, partials, res));
+  SFW3D_TRY(psf_apply_impl(ctx, psf, dtype, A, B, 1, A));
+  SFW3D_TRY(atom_sums_impl(ctx, dtype, dims, B, pieces, ad, res + 1, scr, scratch));
+  std::vector<double> host(size_t(kp) * 6 + 1);
+  SFW3D_TRY(download_sync(ctx, host.data(), res, host.size() * sizeof(double)));
+  *half_sumsq_host = 0.5 * host[0];
+  std::fill(sums_host, sums_host + size_t(k) * 6, 0.0);
+  for (int q = 0; q < kp; ++q)
+    for (int c = 0; c < 6; ++c) sums_host[6 * owner[q] + c] += host[1 + 6 * q + c];
+  if (!finite_all(sums_host, size_t(k) * 6)) {
+    set_error("non-finite criterion gradient; atom parameters left the smooth regime");
+    return SFW3D_ENONFINITE;
+  }
+  return SFW3D_OK;
+}

@@ -192,6 +192,82 @@ def cost_grad_sharded(psf, y, rows, lam, group=None):
     return c, sharded_rows(compute_rows, rows.shape[0], group, y.device)
 
 
+# ------------------------------------- slab-local cost + gradient (GPU)
+def psf_x_halo(kernel: np.ndarray) -> int:
+    """x half-extent of the PSF's non-zero box (planes a slab needs each side)."""
+    c = kernel.shape[0] // 2
+    nzx = np.flatnonzero(np.abs(kernel).sum(axis=(1, 2)))
+    return int(max(c - nzx.min(), nzx.max() - c))
+
+
+def finish_cost_grad(half_sumsq: float, sums: np.ndarray, rows: np.ndarray, lam: float):
+    """Rank-summed partials -> (C, (k, 6) gradient rows), forward.py:218-220
+    and the criterion's lam * total mass (forward.py:182-190)."""
+    mass = 0.0
+    for w in rows[:, 0]:
+        mass += float(w)  # total_mass: sum in row order
+    g = np.empty_like(sums)
+    g[:, 0] = sums[:, 0] + lam
+    g[:, 1:] = rows[:, :1] * sums[:, 1:]
+    return half_sumsq + lam * mass, g
+
+
+class SlabCostGrad:
+    """criterion_and_gradient (forward.py:232-257) sharded as x-slabs
+    (SURVEY §8(e)): rank r owns planes [x0, x1] of the periodic (n, ny, nz)
+    volume and keeps y on the window x0 - halo .. x1 + halo (halo = the PSF's
+    x half-extent). Each rank renders only the clipped x-spans of the atoms
+    meeting its window, convolves on the window, forms the residual on its own
+    planes, back-projects it and takes the per-atom raw sums
+    (sfw3d_cost_grad_slab). The one collective is the all-reduce of the
+    6k + 1 fp64 partials (48 KB at k = 1000); the sum over ranks equals the
+    single-volume C and gradient up to summation order."""
+
+    def __init__(self, psf, dims, x0: int, x1: int):
+        from .forward import Psf
+        from .volumes import Volume
+        self.dims = tuple(int(v) for v in dims)
+        self.x0, self.x1 = int(x0), int(x1)
+        self.halo = psf_x_halo(psf.kernel.data)
+        n = self.dims[0]
+        self.local_dims = (self.x1 - self.x0 + 1 + 2 * self.halo, self.dims[1], self.dims[2])
+        if self.local_dims[0] > n:
+            raise ValueError("slab + 2 halo planes exceed the volume: use the single-volume path")
+        self.psf = Psf(Volume(local_psf_kernel(psf.kernel.data, self.local_dims)), normalize=False)
+        import torch
+        self.index = torch.arange(self.x0 - self.halo, self.x1 + self.halo + 1) % n
+
+    def window(self, y):
+        """This rank's window of a global observation (device or host tensor)."""
+        return y.index_select(0, self.index.to(y.device)).contiguous()
+
+    def partials(self, y_win, rows: np.ndarray):
+        """(1/2 sum_slab r^2, (k, 6) raw sums) of this rank."""
+        import ctypes as C
+        from . import _native as N
+        from .forward import code_of
+        rows = np.ascontiguousarray(rows, dtype=np.float64).reshape(-1, 6)
+        k = rows.shape[0]
+        dev = y_win.device.index
+        ctx = N.context(dev)
+        half = C.c_double()
+        sums = np.zeros((k, 6))
+        N.check(N.lib().sfw3d_cost_grad_slab(
+            ctx.handle, self.psf.native(dev), code_of(y_win), N.ptr(y_win), N.f64_ptr(rows), k,
+            self.dims[0], self.x0, self.x1, self.halo, C.byref(half), N.f64_ptr(sums)))
+        return half.value, sums
+
+    def cost_grad(self, y_win, rows: np.ndarray, lam: float, group=None):
+        """(C, (k, 6) rows) of the whole volume: partials all-reduced over the
+        process group (this rank alone when no group is initialised)."""
+        rows = np.ascontiguousarray(rows, dtype=np.float64).reshape(-1, 6)
+        half, sums = self.partials(y_win, rows)
+        if world()[1] > 1:
+            flat = allreduce_f64(np.concatenate([[half], sums.ravel()]), group, y_win.device)
+            half, sums = float(flat[0]), flat[1:].reshape(-1, 6)
+        return finish_cost_grad(half, sums, rows, lam)
+
+
 # ------------------------------------------- slab-local certificate (GPU)
 def slab_halo(psf, sigma_grid, shape_grid) -> int:
     """x-planes of halo an x-slab sub-volume needs so that eta on the slab is

@@ -298,3 +298,40 @@ def test_many_members_ring_slices_vs_oracle(P):
         pos, v = per[c]
         assert abs(rec.value - v) <= 1e-5 * abs(val), (c, rec.value, v)
         assert tuple(rec.pos) == tuple(pos), (c, tuple(rec.pos), pos)
+
+
+@pytest.mark.parametrize("nranks,prec,tc,tg", [(2, "f64", 1e-12, 1e-11), (3, "f64", 1e-12, 1e-11),
+                                               (4, "f32", 1e-5, 1e-4)])
+def test_slab_cost_grad_matches_global(P, nranks, prec, tc, tg):
+    """Multi-GPU cost + gradient (distributed.SlabCostGrad through
+    sfw3d_cost_grad_slab): the ranks run one after another on this GPU on
+    their own windows; their partials summed equal the oracle's C and
+    gradient. Atoms straddle the periodic x seam and (nranks = 2) meet a
+    window through two periodic images."""
+    import torch
+    from paper_2009_05473_b200 import distributed as D
+    rng = np.random.default_rng(31 + nranks)
+    dims = (48, 20, 24)
+    kernel = O.box_gaussian_psf(dims, (1.5, 1.2, 2.0), (4, 3, 5))
+    k = 40
+    rows = np.column_stack([rng.uniform(0.5, 2, k), rng.uniform(0, 48, k), rng.uniform(0, 20, k),
+                            rng.uniform(0, 24, k), rng.uniform(0.8, 1.5, k), rng.uniform(2.0, 2.8, k)])
+    rows[:4, 1] = [0.2, 47.7, 23.9, 24.1]   # seam and slab-boundary centres
+    y = rng.standard_normal(dims)
+    c0, g0, _ = O.criterion_and_gradient(y, rows, O.psf_hat(kernel), 0.15)
+    with P.precision(prec):
+        psf = P.Psf(P.Volume(kernel), normalize=False)
+        from paper_2009_05473_b200.forward import to_dev
+        yd = to_dev(y)
+        half, sums = 0.0, np.zeros((k, 6))
+        for r in range(nranks):
+            x0, x1 = D.slab_bounds(dims[0], nranks, r)
+            sl = D.SlabCostGrad(psf, dims, x0, x1)
+            h, s = sl.partials(sl.window(yd), rows)
+            half += h
+            sums += s
+        torch.cuda.synchronize()
+    c, g = D.finish_cost_grad(half, sums, rows, 0.15)
+    assert abs(c - c0) <= tc * abs(c0)
+    scale = np.maximum(np.max(np.abs(g0), axis=0), 1e-300)
+    assert float(np.max(np.max(np.abs(g - g0), axis=0) / scale)) < tg
