@@ -447,6 +447,42 @@ def costgrad_workload(args, dev):
             "timing": "wall clock per synchronous C-ABI call (host params in, C + gradient out)"}
 
 
+def slab_costgrad_workload(args, dev, rank, world):
+    """Config 5 cost + gradient sharded as x-slabs over the N ranks
+    (distributed.SlabCostGrad): each rank renders / convolves / back-projects
+    its window only; the 6k+1 fp64 partials are all-reduced over NCCL every
+    evaluation. Time = max over ranks of the synchronous per-eval time."""
+    import torch
+    import paper_2009_05473_b200 as P
+    from paper_2009_05473_b200 import _native as N, configs, distributed as D
+    from paper_2009_05473_b200.forward import psf_apply_dev, render_dev
+
+    P.set_precision("f32")
+    inst = configs.config5()
+    psf = P.Psf(P.Volume(inst.kernel), normalize=False)
+    y = psf_apply_dev(psf, render_dev(inst.truth, inst.dims, N.F32), False)
+    x0, x1 = D.slab_bounds(inst.dims[0], world, rank)
+    sl = D.SlabCostGrad(psf, inst.dims, x0, x1)
+    yw = sl.window(y)
+    del y
+    perts = configs.perturbations(inst.truth, 100)
+    for i in range(3):
+        sl.cost_grad(yw, perts[i], 0.1)
+    torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for i in range(args.cg_steps):
+        sl.cost_grad(yw, perts[i % 100], 0.1)
+    torch.cuda.synchronize(dev)
+    t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=f"cuda:{dev}")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    s = float(t.item()) / args.cg_steps
+    return {"metric": f"cost+grad evals/s (cfg5, x-slab sharded over {world} ranks)",
+            "value": 1.0 / s, "unit": "evals/s", "ms_per_eval": 1e3 * s, "halo": sl.halo,
+            "timing": "max over ranks of wall clock per synchronous eval (C-ABI call + "
+                      "48 KB fp64 all-reduce)"}
+
+
 def solve_workload(dev):
     """Config 1 BSFW end to end (64^3 f64) on the reference-generated
     observation in tests/golden/config1.npz (the GPU parity test compares the
@@ -518,6 +554,10 @@ def main():
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", dev))
     res = cert_workload(args, rank, world, dev)
     secondary = []
+    if collective(world) and not args.no_secondary:
+        cg = slab_costgrad_workload(args, dev, rank, world)  # every rank (all-reduce)
+        if rank == 0:
+            secondary.append(cg)
     if rank == 0 and not args.no_secondary:
         secondary.append(costgrad_workload(args, dev))
         secondary.append(solve_workload(dev))

@@ -203,9 +203,8 @@ def psf_x_halo(kernel: np.ndarray) -> int:
 def finish_cost_grad(half_sumsq: float, sums: np.ndarray, rows: np.ndarray, lam: float):
     """Rank-summed partials -> (C, (k, 6) gradient rows), forward.py:218-220
     and the criterion's lam * total mass (forward.py:182-190)."""
-    mass = 0.0
-    for w in rows[:, 0]:
-        mass += float(w)  # total_mass: sum in row order
+    # total_mass: sequential sum in row order (cumsum adds left to right)
+    mass = float(np.cumsum(rows[:, 0])[-1]) if rows.shape[0] else 0.0
     g = np.empty_like(sums)
     g[:, 0] = sums[:, 0] + lam
     g[:, 1:] = rows[:, :1] * sums[:, 1:]
