@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define SFW3D_ABI_VERSION 1
+#define SFW3D_ABI_VERSION 2
 
 typedef enum {
   SFW3D_OK = 0,
@@ -179,11 +179,13 @@ int sfw3d_basis_fit(const int32_t lo[3], const int32_t hi[3], double sigma, doub
  * Writes the shared term count, up to max_terms betas, the member rows of
  * weights (zero rows elsewhere), w0, fit_err (max abs error on the common
  * box's lattice incl. the 1e-12 factor truncation; +inf for d > 2) and
- * member (1 = certificate takes the basis path) per candidate. */
+ * member (1 = certificate takes the basis path) per candidate. prune and
+ * loose_tol as the table options below (-1 / negative = the defaults). */
 int sfw3d_basis_set_fit(const int32_t dims[3], int n_sigma, const double* sigma_host,
                         int n_shape, const double* shape_host, int dtype, double tol,
-                        int max_terms, int* n_terms, double* betas, double* weights, double* w0,
-                        double* fit_err, int32_t* member);
+                        int prune, double loose_tol, int max_terms, int* n_terms,
+                        double* betas, double* weights, double* w0, double* fit_err,
+                        int32_t* member);
 /* One candidate (flat sigma-major index): evaluator used for `dtype` by an
  * argmax-only evaluation (uses_basis: 0 direct, 1 shared separable basis,
  * 2 basis with exact refinement of its maxima — fp64 non-negative members
@@ -198,6 +200,19 @@ int sfw3d_basis_set_fit(const int32_t dims[3], int n_sigma, const double* sigma_
 int sfw3d_table_candidate(const sfw3d_table* t, int dtype, int cand, int* uses_basis,
                           int* n_terms, double* fit_err, int64_t* direct_taps,
                           int64_t* basis_taps, double* flops);
+/* Table options (no reference counterpart: tuning of the B200 evaluator,
+ * never of the result beyond the certified bounds). Set before the first
+ * evaluation; "prune" and "loose_tol" refit the shared bases on next use.
+ *   "prune"      -1 (default: prune the shared terms for >= 2^24-voxel fp32 /
+ *                2^26-voxel fp64 volumes), 0 never, 1 always.
+ *   "global_voxels" > 0: the voxel count the default pruning rule uses
+ *                (a sharded certificate passes the GLOBAL volume's, so every
+ *                rank fits the same shared terms as one GPU would).
+ *   "loose_tol"  fp32 shared-term selection tolerance (< 0: default 1e-5;
+ *                0: select at basis_tol itself).
+ *   "refine_cap" exactly re-evaluated voxels per call before members fall
+ *                back to the direct kernel (default 65536). */
+int sfw3d_table_set_option(sfw3d_table* t, const char* name, double value);
 int sfw3d_table_destroy(sfw3d_table* t);
 /* Diagnostics: voxels the calling thread's last sfw3d_eta_argmax re-evaluated
  * exactly (refined basis members; > 65536 means it fell back to direct). */

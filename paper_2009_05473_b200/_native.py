@@ -12,7 +12,6 @@ from __future__ import annotations
 
 import contextlib
 import ctypes as C
-import os
 import threading
 from pathlib import Path
 
@@ -32,7 +31,7 @@ EXPORTS = (
     "sfw3d_table_destroy", "sfw3d_eta_argmax", "sfw3d_dots", "sfw3d_nnlasso_cd", "sfw3d_nnlasso_qp",
     "sfw3d_residual", "sfw3d_ctx_profile", "sfw3d_ctx_profile_read", "sfw3d_probe_fp32",
     "sfw3d_table_candidate", "sfw3d_basis_fit", "sfw3d_basis_set_fit",
-    "sfw3d_last_refine_count",
+    "sfw3d_last_refine_count", "sfw3d_table_set_option",
 )
 
 
@@ -70,6 +69,7 @@ _SIGNATURES = {
     "sfw3d_table_candidate": (C.c_int, [_vp, C.c_int, C.c_int, _ip, _ip, _dp, C.POINTER(C.c_int64),
                                         C.POINTER(C.c_int64), _dp]),
     "sfw3d_table_destroy": (C.c_int, [_vp]),
+    "sfw3d_table_set_option": (C.c_int, [_vp, C.c_char_p, C.c_double]),
     "sfw3d_eta_argmax": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_double, _i32p, C.POINTER(Argmax),
                                    C.POINTER(Argmax), _vp]),
     "sfw3d_dots": (C.c_int, [_vp, C.c_int, C.c_int64, C.POINTER(_vp), C.c_int, _vp, _dp]),
@@ -82,7 +82,8 @@ _SIGNATURES = {
     "sfw3d_basis_fit": (C.c_int, [_i32p, _i32p, C.c_double, C.c_double, C.c_int, _dp, _dp, _dp,
                                   _ip, _dp]),
     "sfw3d_basis_set_fit": (C.c_int, [_ip, C.c_int, _dp, C.c_int, _dp, C.c_int, C.c_double,
-                                      C.c_int, _ip, _dp, _dp, _dp, _dp, _i32p]),
+                                      C.c_int, C.c_double, C.c_int, _ip, _dp, _dp, _dp, _dp,
+                                      _i32p]),
     "sfw3d_ctx_profile": (C.c_int, [_vp, C.c_int]),
     "sfw3d_ctx_profile_read": (C.c_int, [_vp, C.c_char_p, _dp, C.POINTER(C.c_int64)]),
     "sfw3d_probe_fp32": (C.c_int, [_vp, _dp]),
@@ -168,10 +169,11 @@ def basis_fit(lo, hi, sigma: float, d: float):
     return betas[:k], weights[:k], w0.value, err.value
 
 
-def basis_set_fit(dims, sigmas, shapes, dtype: int, tol: float, max_terms: int = 256):
+def basis_set_fit(dims, sigmas, shapes, dtype: int, tol: float, max_terms: int = 256,
+                  prune: int = -1, loose_tol: float = -1.0):
     """Host-only: the shared separable basis a table fits for the candidate
     grid (sigma-major): dict(betas [T], weights [C, T], w0 [C], fit_err [C],
-    member [C] bool)."""
+    member [C] bool). prune / loose_tol as sfw3d_table_set_option (-1 = default)."""
     sg = np.ascontiguousarray(sigmas, dtype=np.float64)
     sh = np.ascontiguousarray(shapes, dtype=np.float64)
     nc = sg.size * sh.size
@@ -181,7 +183,8 @@ def basis_set_fit(dims, sigmas, shapes, dtype: int, tol: float, max_terms: int =
     member = np.zeros(nc, np.int32)
     nt = C.c_int()
     check(lib().sfw3d_basis_set_fit(dims_arg(dims), sg.size, f64_ptr(sg), sh.size, f64_ptr(sh),
-                                    int(dtype), float(tol), max_terms, C.byref(nt),
+                                    int(dtype), float(tol), int(prune), float(loose_tol),
+                                    max_terms, C.byref(nt),
                                     f64_ptr(betas), f64_ptr(weights), f64_ptr(w0), f64_ptr(err),
                                     i32_ptr(member)))
     if nt.value > max_terms:
@@ -317,6 +320,3 @@ def torch_dtype(code: int):
 def ptr(t) -> _vp:
     return _vp(t.data_ptr())
 
-
-def env_flag(name: str, default: str = "") -> str:
-    return os.environ.get(name, default)

@@ -55,7 +55,7 @@ class AtomTemplateTable:
     """
 
     def __init__(self, sigma_grid, shape_grid, dims, psf: Psf, tap_tol: float, mode: str,
-                 basis_tol: float):
+                 basis_tol: float, options: dict | None = None):
         self.sigma_grid = sigma_grid
         self.shape_grid = shape_grid
         self.dims = tuple(dims)
@@ -63,6 +63,8 @@ class AtomTemplateTable:
         self.tap_tol = float(tap_tol)
         self.mode = mode
         self.basis_tol = float(basis_tol)
+        # evaluator options (sfw3d_table_set_option): prune, loose_tol, refine_cap
+        self.options = {k: float(v) for k, v in (options or {}).items() if v is not None}
         self._native = {}
         self._hats = None
 
@@ -78,6 +80,8 @@ class AtomTemplateTable:
                                                self.tap_tol, MODES[self.mode], self.basis_tol,
                                                C.byref(hp)))
             h = _TableHandle(hp)
+            for key, val in self.options.items():
+                N.check(N.lib().sfw3d_table_set_option(hp, key.encode(), val))
             self._native[device] = h
         return h.handle
 
@@ -129,13 +133,18 @@ class AtomTemplateTable:
 
 def build_template_table(psf: Psf, sigma_grid, shape_grid, bounds: DomainBounds | None = None,
                          workers: int | None = None, *, tap_tol: float = 0.0,
-                         mode: str = "auto", basis_tol: float = 1e-9) -> AtomTemplateTable:
+                         mode: str = "auto", basis_tol: float = 1e-9, prune: bool | None = None,
+                         global_voxels: int | None = None, loose_tol: float | None = None,
+                         refine_cap: int | None = None) -> AtomTemplateTable:
     """Candidate table for the (sigma, d) grid (certificate.py:65-97).
 
     Keyword-only extras: ``tap_tol`` skips template taps below it (0 keeps
     the reference's full 1e-12 support box); ``mode`` "auto" lets the
     library pick the fastest exact-to-``basis_tol`` evaluation per
-    candidate, "direct" forces direct correlation.
+    candidate, "direct" forces direct correlation. ``prune`` / ``global_voxels``
+    (the voxel count of the default pruning rule) / ``loose_tol`` / ``refine_cap`` tune the shared separable basis (sfw3d_table_set_option;
+    None keeps the library default: pruning by volume size, fp32 term
+    selection at 1e-5, 65536 exactly re-evaluated voxels per call).
     """
     sigma_grid = np.sort(np.asarray(sigma_grid, dtype=float))
     shape_grid = np.sort(np.asarray(shape_grid, dtype=float))
@@ -150,7 +159,11 @@ def build_template_table(psf: Psf, sigma_grid, shape_grid, bounds: DomainBounds 
         raise ValueError("template table requires a centro-symmetric kernel")
     if mode not in MODES:
         raise ValueError(f"mode must be one of {sorted(MODES)}")
-    table = AtomTemplateTable(sigma_grid, shape_grid, psf.dims, psf, tap_tol, mode, basis_tol)
+    opts = {"prune": None if prune is None else int(bool(prune)),
+            "global_voxels": global_voxels, "loose_tol": loose_tol,
+            "refine_cap": refine_cap}
+    table = AtomTemplateTable(sigma_grid, shape_grid, psf.dims, psf, tap_tol, mode, basis_tol,
+                              opts)
     table.native(N.device_index(None))
     return table
 

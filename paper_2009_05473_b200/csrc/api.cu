@@ -489,6 +489,8 @@ extern "C" int sfw3d_cost_grad_slab(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dt
   const int nxl = x1 - x0 + 1 + 2 * halo;
   SFW3D_CHECK_ARG(gnx > 0 && x0 >= 0 && x1 >= x0 && x1 < gnx && halo >= 0, "slab bounds");
   SFW3D_CHECK_ARG(dims[0] == nxl && nxl <= gnx, "psf dims[0] must be x1 - x0 + 1 + 2 halo <= gnx");
+  SFW3D_CHECK_ARG(-psf->lo[0] <= halo && psf->hi[0] <= halo,
+                  "halo must cover the PSF's x half-extent (else the window convolution wraps)");
   SFW3D_TRY(begin_call(ctx));
   const int gdims[3] = {gnx, dims[1], dims[2]};
   std::vector<AtomGeo> atoms;

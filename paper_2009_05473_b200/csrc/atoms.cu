@@ -30,17 +30,11 @@ constexpr int kSumThreads = 256;
 constexpr int kMaxAxis = 1024;             // tabulated axis length in atom sums
 constexpr int kMaxRows = 512;              // rows per chunk (fp64)
 // fp32: 4x larger chunks (amortise the row table and the fp64 block
-// reduction over 64 voxels per thread), SFW3D_CHUNK32 overrides
+// reduction over 64 voxels per thread)
 constexpr int kChunk32 = 16384, kMaxRows32 = 2048;
 template <typename T>
 constexpr int max_rows() { return sizeof(T) == 8 ? kMaxRows : kMaxRows32; }
-static int chunk32() {
-  static const int v = [] {
-    const char* e = getenv("SFW3D_CHUNK32");
-    return e ? std::max(256, atoi(e)) : kChunk32;
-  }();
-  return v;
-}
+static int chunk32() { return kChunk32; }
 
 // a mod n in [0, n) without a division on the common path (|a| < 2n)
 __device__ __forceinline__ int pmod(int a, int n) {

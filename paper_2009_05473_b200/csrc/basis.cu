@@ -290,23 +290,11 @@ struct BasisSet {
   void* W_dev = nullptr;            // storage dtype, [member][term]
   void* w0_dev = nullptr;
   int* cid_dev = nullptr;           // member -> candidate id
-  // fp32 fused x pass + mix (xmix_kernel): every term's axis-0 taps, each
-  // padded with zeros to a multiple of 4, concatenated; per term {offset, lo,
-  // padded length, 0}
-  float* xtaps_dev = nullptr;
-  int4* xmeta_dev = nullptr;
-  int max_nt4x = 0, xtaps_total = 0;
   long long taps_per_voxel = 0;
   int device = 0;
   // mix_ring2_kernel: dense members (W rows [nmd][K], w0) and copy members
   // (one weight-1 term, w0 = 0) with cterm[k] = copy slot of term k or -1
   int nmd = 0, nmc = 0;
-  // mix_mma_kernel (fp32, K + 1 <= 16 entries, <= 16 columns): B[entry][column]
-  // (columns: dense members then copies), column -> member index
-  bool mma_mix = false;
-  int ncol = 0;
-  float* Bmat_dev = nullptr;
-  int* colmem_dev = nullptr;
   void* Wd_dev = nullptr;
   void* w0d_dev = nullptr;
   int* dmem_dev = nullptr;
@@ -342,24 +330,17 @@ namespace {
 
 constexpr int kRidgeMin = -34, kRidgeMax = -6;  // ridge weights 10^e (and 0)
 
-double env_double(const char* name, double def) {
-  const char* e = getenv(name);
-  return e ? atof(e) : def;
-}
-
 void fit_signed_members(BasisSet* s, const std::vector<BasisCandidate>& cands, int dtype,
                         const std::vector<double>& Sfit,
                         const std::vector<std::vector<double>>& hstore,
                         const std::vector<double>& pass_taps) {
-  if (env_double("SFW3D_SIGNED", 1.0) == 0.0) return;
   const int nc = int(cands.size()), nt = int(s->betas.size());
   const double u = dtype == SFW3D_F64 ? 0x1p-53 : 0x1p-24;
   // acceptance of a signed member: bound E <= accept x template mass. A
   // member's maxima are refined exactly whatever E is; E only sizes the
   // refinement set. fp32: 0.1 (with the 1e-5 loose term selection, config 4
   // keeps all 16 members on 12 shared terms, ~360 refined voxels); fp64: 0.01
-  const double accept = env_double("SFW3D_SIGNED_ACCEPT", dtype == SFW3D_F32 ? 0.1 : 0.01);
-  const bool debug = env_double("SFW3D_SIGNED_DEBUG", 0.0) != 0.0;
+  const double accept = dtype == SFW3D_F32 ? 0.1 : 0.01;
   // per term: (effective) factor mass, its part outside the common box C
   // (chained factors may reach past C, where every template is 0), and the
   // passes' rounding factor (a chained term adds its own passes' rounding
@@ -387,11 +368,8 @@ void fit_signed_members(BasisSet* s, const std::vector<BasisCandidate>& cands, i
     ext[t] = std::max(0.0, prod - pin);
     rho[t] = 1.01 * u * pass_taps[t] + (s->parent[t] >= 0 ? rho[s->parent[t]] * (1.0 + 1.01 * u * pass_taps[t]) : 0.0);
   }
-  // the mix's rounding: fp32 FFMA chains (u), or the tensor-core 3xTF32 mix
-  // (mix_mma_kernel: <= 3 x 2^-22 per product + truncating fp32 accumulation;
-  // 2^-19 is used)
-  const double umix = s->mma_mix ? 0x1p-19 : u;
-  const double gmix = 1.01 * umix * (nt + 2);
+  // the mix's rounding: (K + 1)-term FFMA chains in the storage precision
+  const double gmix = 1.01 * u * (nt + 2);
   // axis representatives: offsets +t and -t share one (multiplicity 2) when
   // both lie in C and every factor is defined at both
   struct Rep {
@@ -527,10 +505,6 @@ void fit_signed_members(BasisSet* s, const std::vector<BasisCandidate>& cands, i
   }
   for (int c : todo) {
     const bool ok = std::isfinite(esig[c]) && esig[c] <= accept * mass[c];
-    if (debug)
-      fprintf(stderr, "[signed] cand %d sigma %.3f d %.3f: D1 %.3e R %.3e E/mass %.3e -> %s\n", c,
-              cands[c].sigma, cands[c].d, dsig[c], esig[c] - dsig[c], esig[c] / mass[c],
-              ok ? "member" : "direct");
     if (!ok) continue;
     s->is_member[c] = 2;
     s->ebound[c] = esig[c];
@@ -545,13 +519,9 @@ void fit_signed_members(BasisSet* s, const std::vector<BasisCandidate>& cands, i
 
 // fp32 default: config 4 measured 26 -> 12 shared terms (with the fp32
 // signed acceptance 0.1), 31.3 -> 13.5 ms per certificate, ~360 refined
-// voxels (SFW3D_BASIS_LOOSE=0 disables)
+// voxels (the table option "loose_tol" overrides; 0 disables)
 constexpr double kLooseF32 = 1e-5;
-double basis_loose_tol(int dtype) {
-  const char* e = getenv(dtype == SFW3D_F32 ? "SFW3D_BASIS_LOOSE" : "SFW3D_BASIS_LOOSE64");
-  if (e) return atof(e);
-  return dtype == SFW3D_F32 ? kLooseF32 : 0.0;
-}
+double basis_loose_tol(int dtype) { return dtype == SFW3D_F32 ? kLooseF32 : 0.0; }
 
 int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands, int dtype,
                     double tol, BasisSet** out, bool on_device, bool prune, double loose) {
@@ -782,8 +752,7 @@ int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands,
   // sampled Gaussian to ~1e-9 (Poisson ripple exp(-pi^2 / (beta_p + beta_g))).
   // The bounds below use the effective factors, so the choice never costs
   // certification, only fit quality at the ripple level.
-  const bool chains = dtype == SFW3D_F32 && env_double("SFW3D_CHAIN", 1.0) != 0.0 &&
-                      !(getenv("SFW3D_XMIX") && atoi(getenv("SFW3D_XMIX")) == 1);
+  const bool chains = dtype == SFW3D_F32;
   std::vector<double> gbeta(nt, 0.0);
   if (chains) {
     int rbox = 1 << 30;
@@ -871,10 +840,6 @@ int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands,
     if (st != SFW3D_OK) return st;
     s->taps.push_back(dev);
   }
-  if (env_double("SFW3D_BASIS_DEBUG", 0.0) != 0.0)
-    for (int t = 0; t < nt; ++t)
-      fprintf(stderr, "[basis] term %d beta %.5g parent %d pass taps %d %d %d\n", t, s->betas[t],
-              s->parent[t], s->tlen[0][t], s->tlen[1][t], s->tlen[2][t]);
   s->W.assign(size_t(nm) * nt, 0.0);
   s->w0.assign(nm, 0.0);
   for (int m = 0; m < nm; ++m) {
@@ -884,9 +849,6 @@ int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands,
   }
   s->n_nnls = nm;
   s->ebound.assign(nc, 0.0);
-  // opt-in (SFW3D_MIX_MMA=1): measured slower than mix_ring2_kernel on config
-  // 4 (2.98 vs 2.28 ms; legacy mma.sync issue, per-group latency chains)
-  s->mma_mix = dtype == SFW3D_F32 && nt + 1 <= 16 && env_double("SFW3D_MIX_MMA", 0.0) != 0.0;
   if (nt > 0) fit_signed_members(s, cands, dtype, Sfit, heff, pass_taps);
   const int nmt = int(s->members.size());
   if (nmt && on_device) {
@@ -926,27 +888,6 @@ int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands,
       }
       s->nmd = int(dmem.size());
       s->nmc = int(cmem.size());
-      if (s->mma_mix && s->nmd + s->nmc <= 16) {
-        std::vector<float> B(16 * 16, 0.f);
-        std::vector<int> colmem(16, 0);
-        int col = 0;
-        for (int q = 0; q < s->nmd; ++q, ++col) {
-          const int m = dmem[q];
-          colmem[col] = m;
-          B[0 * 16 + col] = float(s->w0[m]);
-          for (int t = 0; t < nt; ++t) B[(1 + t) * 16 + col] = float(s->W[size_t(m) * nt + t]);
-        }
-        for (int q = 0; q < s->nmc; ++q, ++col) {
-          const int m = cmem[q];
-          colmem[col] = m;
-          for (int t = 0; t < nt; ++t) B[(1 + t) * 16 + col] = float(s->W[size_t(m) * nt + t]);
-        }
-        s->ncol = col;
-        SFW3D_TRY(upload(reinterpret_cast<void**>(&s->Bmat_dev), B.data(), B.size() * sizeof(float)));
-        SFW3D_TRY(upload(reinterpret_cast<void**>(&s->colmem_dev), colmem.data(), colmem.size() * sizeof(int)));
-      } else {
-        s->mma_mix = false;
-      }
       Wd.push_back(0.0);
       w0d.push_back(0.0);
       dmem.push_back(0);
@@ -963,19 +904,6 @@ int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands,
       SFW3D_TRY(upload(reinterpret_cast<void**>(&s->cmem_dev), cmem.data(), cmem.size() * sizeof(int)));
       SFW3D_TRY(upload(reinterpret_cast<void**>(&s->cterm_dev), cterm.data(), cterm.size() * sizeof(int)));
     }
-    if (dtype == SFW3D_F32) {
-      std::vector<float> xt;
-      std::vector<int4> meta;
-      for (int t = 0; t < nt; ++t) {
-        const int len = s->tlen[0][t], nt4 = (len + 3) & ~3;
-        meta.push_back(make_int4(int(xt.size()), s->tlo[0][t], nt4, 0));
-        for (int q = 0; q < nt4; ++q) xt.push_back(q < len ? float(hstore[t][q]) : 0.f);
-        s->max_nt4x = std::max(s->max_nt4x, nt4);
-      }
-      s->xtaps_total = int(xt.size());
-      SFW3D_TRY(upload(reinterpret_cast<void**>(&s->xtaps_dev), xt.data(), xt.size() * sizeof(float)));
-      SFW3D_TRY(upload(reinterpret_cast<void**>(&s->xmeta_dev), meta.data(), meta.size() * sizeof(int4)));
-    }
   }
   return SFW3D_OK;
 }
@@ -987,9 +915,7 @@ void basis_set_destroy(BasisSet* s) {
   if (s->W_dev) cudaFree(s->W_dev);
   if (s->w0_dev) cudaFree(s->w0_dev);
   if (s->cid_dev) cudaFree(s->cid_dev);
-  if (s->xtaps_dev) cudaFree(s->xtaps_dev);
-  if (s->xmeta_dev) cudaFree(s->xmeta_dev);
-  for (void* p : {static_cast<void*>(s->Bmat_dev), static_cast<void*>(s->colmem_dev), s->Wd_dev, s->w0d_dev, static_cast<void*>(s->dmem_dev),
+  for (void* p : {s->Wd_dev, s->w0d_dev, static_cast<void*>(s->dmem_dev),
                   static_cast<void*>(s->cmem_dev), static_cast<void*>(s->cterm_dev)})
     if (p) cudaFree(p);
   delete s;
@@ -1241,319 +1167,6 @@ __global__ void __launch_bounds__(kMixThreads) mix_argmax_kernel(
       if (better(red[threadIdx.x][w].v, red[threadIdx.x][w].idx, bm.v, bm.idx))
         bm = red[threadIdx.x][w];
     partial[(long long)(m0 + threadIdx.x) * gridDim.x + blockIdx.x] = bm;
-  }
-}
-
-// ------------------------------------------------ fused x pass + member mix
-// fp32 storage. `U` holds, per shared term k, U_k = f_k^(y) f_k^(z) * b (the
-// two in-plane passes). This kernel forms T_k = f_k^(x) * U_k for a tile of
-// kXTo x-outputs x kXTI consecutive inner (y, z) indices in registers and
-// folds it straight into every member's accumulator,
-//     acc_m = w0_m b + sum_k W[m][k] T_k      (k ascending, one FMA each),
-// so T_k never goes to HBM and the (K + 1)-volume mix read disappears. The
-// arithmetic is the same FMA chains as pass + mix_argmax_kernel (same
-// rounding bound, basis.cu signed members).
-//   Packed fp32x2 (FFMA2): lane l owns the inner pair (2l, 2l + 1), so a
-//   staged row gives the pair with one 8-byte LDS, and every FMA of the pass
-//   and of the mix is one FFMA2 on (inner 2l, inner 2l + 1) — half the
-//   issue slots of scalar FFMA at the same FP32 pipe rate, which leaves room
-//   for the loads at 8 warps per SM (the 16 x J accumulator pairs take 128
-//   registers). Taps and weights are stored as duplicated pairs (t, t).
-//   CTA = kXW persistent warps; warp w owns x-outputs a0 + w J .. + J - 1.
-//   The (tile, term) sequence streams rows a0 + lo_k .. a0 + kXTo + nt4_k - 2
-//   (wrapped) of the 64-wide inner column through a kXNS-deep cp.async ring
-//   (one commit group per entry, one barrier per entry).
-constexpr int kXJ = 4;                 // x-outputs per thread
-constexpr int kXP = 4;                 // window prefetch (steps)
-constexpr int kXW = 8;                 // warps per CTA
-constexpr int kXTo = kXJ * kXW;        // x-outputs per tile
-constexpr int kXTI = 64;               // inner indices per tile (2 per lane)
-constexpr int kXNS = 4;                // ring depth
-
-typedef unsigned long long f2;  // packed fp32 pair (low = first)
-
-__device__ __forceinline__ void ffma2(f2& c, f2 a, f2 b) {
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c) : "l"(a), "l"(b));
-}
-__device__ __forceinline__ f2 lds2v(const float* p) {
-  f2 v;
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(p));
-  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(sa));
-  return v;
-}
-__device__ __forceinline__ void lds22v(const f2* p, f2& a, f2& b) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(p));
-  asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"(sa));
-}
-__device__ __forceinline__ float lo32(f2 v) { return __uint_as_float(unsigned(v)); }
-__device__ __forceinline__ float hi32(f2 v) { return __uint_as_float(unsigned(v >> 32)); }
-__device__ __forceinline__ f2 dup2(float x) {
-  const unsigned long long u = __float_as_uint(x);
-  return u | (u << 32);
-}
-
-// order-preserving key of a float (larger value -> larger key; 0 = none)
-__device__ __forceinline__ unsigned fkey(float v) {
-  const unsigned u = __float_as_uint(v);
-  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-
-template <int NM, bool COLLECT>
-__global__ void __launch_bounds__(kXW * 32, 1) xmix_kernel(
-    const float* __restrict__ b, const float* __restrict__ U, long long n, int K, int nm, int m0,
-    const float* __restrict__ W, const float* __restrict__ w0, const int* __restrict__ cid,
-    const float* __restrict__ xtaps, const int4* __restrict__ xmeta, int xtaps_total,
-    int stage_rows, int nx, int ny, int nz, int4 wlo, int4 whi, double lam,
-    float* __restrict__ fields, Best* __restrict__ partial, Collect col) {
-  constexpr int J = kXJ, S = kXJ + kXP, TI = kXTI, NT = kXW * 32;
-  static_assert(S % 4 == 0 && S <= 8, "window steps come in 4-tap groups");
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  // ring slot: [stage_rows][TI] term rows, then [kXTo][TI] rows of b (filled
-  // with the tile's first term)
-  const int slot_f = (stage_rows + kXTo) * TI;
-  float* stage = reinterpret_cast<float*>(smem_raw);     // kXNS slots
-  f2* sW = reinterpret_cast<f2*>(stage + kXNS * slot_f); // [K][NM] (w, w)
-  f2* sw0 = sW + K * NM;                                 // [NM]
-  f2* st = sw0 + NM;                                     // taps (t, t), xtaps_total + 8
-  int4* smeta = reinterpret_cast<int4*>(st + xtaps_total + 8);  // [K]
-  __shared__ float red_v[NM][kXW];
-  __shared__ long long red_i[NM][kXW];
-
-  const int stride = ny * nz;  // n < 2^31 (host check)
-  const int ntx = (nx + kXTo - 1) / kXTo;
-  const int ntiles = ntx * (stride / TI);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int my_tiles;
-  if constexpr (COLLECT) {
-    // one tile per CTA, revisited only when one of its maxima qualifies
-    const int q = threadIdx.x < nm &&
-                  col.part[(long long)(m0 + threadIdx.x) * col.parents + blockIdx.x].v >=
-                      col.thr[m0 + threadIdx.x];
-    if (!__syncthreads_or(q)) return;
-    my_tiles = 1;
-  } else {
-    my_tiles = (ntiles - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x);
-  }
-  for (int e = threadIdx.x; e < K * NM; e += NT) {
-    const int k = e / NM, m = e % NM;
-    sW[e] = dup2(m < nm ? W[size_t(m0 + m) * K + k] : 0.f);
-  }
-  for (int e = threadIdx.x; e < NM; e += NT) sw0[e] = dup2(e < nm ? w0[m0 + e] : 0.f);
-  for (int e = threadIdx.x; e < xtaps_total + 8; e += NT) st[e] = dup2(e < xtaps_total ? xtaps[e] : 0.f);
-  for (int e = threadIdx.x; e < K; e += NT) smeta[e] = xmeta[e];
-  __syncthreads();
-
-  // producer cursor: sequence entry (tile pi, term pk) -> ring slot pg
-  auto tile_geo = [&](int i, int& a0, int& inner0) {
-    const int tile = COLLECT ? int(blockIdx.x) : int(blockIdx.x) + i * int(gridDim.x);
-    const int ti = tile / ntx;
-    a0 = (tile - ti * ntx) * kXTo;
-    inner0 = ti * TI;
-  };
-  int pk = 0, pi = 0, pg = 0, pa0, pinner0;
-  tile_geo(0, pa0, pinner0);
-  constexpr int kV = TI / 4, dr = NT / kV;  // 16-byte chunks per row, rows per step
-  const int c = (threadIdx.x % kV) * 4, r0 = threadIdx.x / kV;
-  auto stage_next = [&]() {
-    float* slot = stage + (pg % kXNS) * slot_f + c;
-    const int4 mt = smeta[pk];
-    const int rows = kXTo + mt.z - 1;
-    const float* src = U + (long long)pk * n + pinner0 + c;
-    int x = (pa0 + mt.y + r0) % nx;
-    if (x < 0) x += nx;
-    for (int r = r0; r < rows; r += dr) {
-      cp_async16(slot + r * TI, src + x * stride);
-      x += dr;
-      while (x >= nx) x -= nx;
-    }
-    if (pk == 0) {  // the tile's b rows a0 .. a0 + kXTo - 1 (wrapped)
-      const float* bs = b + pinner0 + c;
-      for (int rb = r0; rb < kXTo; rb += dr) {
-        int xb = pa0 + rb;
-        while (xb >= nx) xb -= nx;
-        cp_async16(slot + (stage_rows + rb) * TI, bs + xb * stride);
-      }
-    }
-    ++pg;
-    if (++pk == K) {
-      pk = 0;
-      ++pi;
-      tile_geo(pi, pa0, pinner0);
-    }
-  };
-
-  const int G = my_tiles * K;
-#pragma unroll
-  for (int g = 0; g < kXNS - 1; ++g) {
-    if (g < G) stage_next();
-    cp_async_commit();
-  }
-  f2 acc[NM][J];
-  for (int i = 0; i < my_tiles; ++i) {
-    int a0, inner0;
-    tile_geo(i, a0, inner0);
-    const int tile = COLLECT ? int(blockIdx.x) : int(blockIdx.x) + i * int(gridDim.x);
-    for (int k = 0; k < K; ++k) {
-      const int g = i * K + k;
-      cp_async_wait_group<kXNS - 2>();  // this thread's copies of entry g landed
-      __syncthreads();                   // everyone's; everyone is done with g - 1
-      if (g + kXNS - 1 < G) stage_next();
-      cp_async_commit();
-      const float* cur = stage + (g % kXNS) * slot_f;
-      if (k == 0) {  // acc[m][j] = w0_m b(x_j)
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-          const f2 bv = lds2v(cur + (stage_rows + warp * J + j) * TI + 2 * lane);
-#pragma unroll
-          for (int m = 0; m < NM; ++m) {
-            acc[m][j] = 0ull;
-            ffma2(acc[m][j], sw0[m], bv);
-          }
-        }
-      }
-      const int4 mt = smeta[k];
-      const f2* tp = st + mt.x;
-      const int nt4 = mt.z;
-      const float* src = cur + (warp * J) * TI + 2 * lane;
-      f2 win[S], o[J];
-#pragma unroll
-      for (int s2 = 0; s2 < S; ++s2) win[s2] = lds2v(src + s2 * TI);
-#pragma unroll
-      for (int j = 0; j < J; ++j) o[j] = 0ull;
-      // volatile shared loads stay in program order: each tap group is read
-      // one group ahead, each window row kXP steps ahead of its first use
-      f2 tn[4];
-      lds22v(tp, tn[0], tn[1]);
-      lds22v(tp + 2, tn[2], tn[3]);
-      int q0 = 0;
-      for (; q0 + S <= nt4; q0 += S) {
-#pragma unroll
-        for (int r = 0; r < S; r += 4) {
-          const f2 tv[4] = {tn[0], tn[1], tn[2], tn[3]};
-          lds22v(tp + q0 + r + 4, tn[0], tn[1]);
-          lds22v(tp + q0 + r + 6, tn[2], tn[3]);
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-#pragma unroll
-            for (int j = 0; j < J; ++j) ffma2(o[j], tv[kk], win[(r + kk + j) % S]);
-            win[r + kk] = lds2v(src + (q0 + r + kk + S) * TI);
-          }
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < S; r += 4) {
-        if (q0 + r >= nt4) break;
-        const f2 tv[4] = {tn[0], tn[1], tn[2], tn[3]};
-        lds22v(tp + q0 + r + 4, tn[0], tn[1]);
-        lds22v(tp + q0 + r + 6, tn[2], tn[3]);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-#pragma unroll
-          for (int j = 0; j < J; ++j) ffma2(o[j], tv[kk], win[(r + kk + j) % S]);
-          win[r + kk] = lds2v(src + (q0 + r + kk + S) * TI);
-        }
-      }
-      // fold T_k into every member (k ascending: the mix kernel's FMA order)
-#pragma unroll
-      for (int m2 = 0; m2 < NM; m2 += 2) {
-        f2 wa, wb;
-        lds22v(sW + k * NM + m2, wa, wb);
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-          ffma2(acc[m2][j], wa, o[j]);
-          ffma2(acc[m2 + 1][j], wb, o[j]);
-        }
-      }
-    }
-
-    // ---- tile epilogue: window test, fields / collect / argmax. Value
-    // (j, h) of this thread is voxel x = a0 + warp J + j, inner = inner0 +
-    // 2 lane + h; C-order index x * stride + inner.
-    const int xw = a0 + warp * J;
-    unsigned vmask = 0;  // bit 2 j + h: in the window
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int inner = inner0 + 2 * lane + h;
-      const int y = inner / nz, z = inner - y * nz;
-      if (y < wlo.y || y > whi.y || z < wlo.z || z > whi.z) continue;
-#pragma unroll
-      for (int j = 0; j < J; ++j) {
-        const int x = xw + j;
-        if (x < nx && x >= wlo.x && x <= whi.x) vmask |= 1u << (2 * j + h);
-      }
-    }
-    if constexpr (COLLECT) {
-#pragma unroll
-      for (int m = 0; m < NM; ++m) {
-        if (m >= nm) break;
-#pragma unroll
-        for (int q = 0; q < 2 * J; ++q) {
-          const float v = (q & 1) ? hi32(acc[m][q >> 1]) : lo32(acc[m][q >> 1]);
-          if (((vmask >> q) & 1u) && double(v) / lam >= col.thr[m0 + m]) {
-            atomicAdd(col.count + 1 + m0 + m, 1);
-            const int slot = atomicAdd(col.count, 1);
-            if (slot < col.cap) {
-              col.cand[slot] = cid[m0 + m];
-              col.idx[slot] = (long long)(xw + (q >> 1)) * stride + inner0 + 2 * lane + (q & 1);
-            }
-          }
-        }
-      }
-      continue;
-    }
-#pragma unroll
-    for (int m = 0; m < NM; ++m) {
-      if (m >= nm) break;
-      if (fields) {
-        float* f = fields + (long long)cid[m0 + m] * n + inner0 + 2 * lane;
-#pragma unroll
-        for (int j = 0; j < J; ++j)
-          if (xw + j < nx)
-            __stcs(reinterpret_cast<float2*>(f + (long long)(xw + j) * stride),
-                   make_float2(float(double(lo32(acc[m][j])) / lam),
-                               float(double(hi32(acc[m][j])) / lam)));
-      }
-      // first maximum of the thread (x, then inner ascending); the warp's:
-      // largest key, ties to the smallest x offset, then the lowest lane
-      unsigned key = 0;
-      int bq = 2 * J;
-#pragma unroll
-      for (int q = 0; q < 2 * J; ++q) {
-        const float v = (q & 1) ? hi32(acc[m][q >> 1]) : lo32(acc[m][q >> 1]);
-        const unsigned kq = ((vmask >> q) & 1u) ? fkey(v) : 0u;
-        if (kq > key) {
-          key = kq;
-          bq = q;
-        }
-      }
-      const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
-      unsigned tied = __ballot_sync(0xffffffffu, key == kmax);
-      if (__popc(tied) > 1) {
-        const unsigned jmin = __reduce_min_sync(0xffffffffu, key == kmax ? unsigned(bq >> 1) : 0xffu);
-        tied = __ballot_sync(0xffffffffu, key == kmax && unsigned(bq >> 1) == jmin);
-      }
-      const int src_lane = __ffs(tied) - 1;
-      const int wq = __shfl_sync(0xffffffffu, bq, src_lane);
-      if (lane == 0) {
-        const unsigned u = (kmax & 0x80000000u) ? (kmax & 0x7fffffffu) : ~kmax;
-        red_v[m][warp] = kmax == 0 ? -INFINITY : __uint_as_float(u);
-        red_i[m][warp] = kmax == 0 ? 0x7fffffffffffffffLL
-                                   : (long long)(xw + (wq >> 1)) * stride + inner0 + 2 * src_lane + (wq & 1);
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x < nm) {
-      const int m = threadIdx.x;
-      float bv = red_v[m][0];
-      long long bi = red_i[m][0];
-      for (int w = 1; w < kXW; ++w)
-        if (red_v[m][w] > bv || (red_v[m][w] == bv && red_i[m][w] < bi)) {
-          bv = red_v[m][w];
-          bi = red_i[m][w];
-        }
-      partial[(long long)(m0 + m) * ntiles + tile] =
-          Best{bi == 0x7fffffffffffffffLL ? -INFINITY : double(bv) / lam, bi};
-    }
   }
 }
 
@@ -1977,172 +1590,6 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
   }
 }
 
-// Evaluation-pass mix on the tensor cores (fp32 storage): for every voxel
-// the member values are a 16-entry dot product (b, T_0 .. T_{K-1}, zero pad)
-// with a 16-column weight matrix (dense members, then the exact d = 2 copies
-// with weight 1, zero pad) — a (voxels x 16) x (16 x 16) GEMM. Each warp streams
-// 16-voxel groups through its own cp.async ring ([entry][24] floats per
-// stage: conflict-free A-fragment loads) and issues mma.sync m16n8k8 TF32 in
-// the 3xTF32 split (a_hi b_hi + a_hi b_lo + a_lo b_hi, fp32 accumulate: ~2^-20
-// relative per product, which the signed members' bounds use). Same CTA
-// chunking as mix_ring2_kernel, so the collect pass revisits the same chunks.
-constexpr int kMmaNS = 8;       // ring stages per warp
-constexpr int kMmaPitch = 24;   // floats per entry row of a stage (16 used)
-
-__device__ __forceinline__ unsigned to_tf32(float x) {
-  unsigned r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
-}
-
-__device__ __forceinline__ void mma_tf32(float (&c)[4], const unsigned (&a)[4], unsigned b0,
-                                         unsigned b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};\n"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-__global__ void __launch_bounds__(kMixThreads, 2) mix_mma_kernel(
-    const float* __restrict__ b, const float* __restrict__ terms, long long n, int K,
-    const float* __restrict__ Bmat, const int* __restrict__ colmem, int ncol,
-    int nx, int ny, int nz, int4 wlo, int4 whi, double lam, Best* __restrict__ partial) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int kStage = 16 * kMmaPitch;  // floats
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  float* ring = reinterpret_cast<float*>(smem_raw) + warp * (kMmaNS * kStage);
-  __shared__ Best red[16][kMixThreads / 32];
-  // zero every stage once (entries >= K + 1 are never copied)
-  for (int e = lane; e < kMmaNS * kStage; e += 32) ring[e] = 0.f;
-  __syncwarp();
-  // B fragments (k-step s, n-tile q): b0 = B[8s + t][8q + g], b1 = B[8s + t + 4][8q + g]
-  unsigned bh[2][2][2], bl[2][2][2];
-#pragma unroll
-  for (int s2 = 0; s2 < 2; ++s2)
-#pragma unroll
-    for (int q = 0; q < 2; ++q)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const float w = Bmat[(8 * s2 + t + 4 * h) * 16 + 8 * q + g];
-        bh[s2][q][h] = to_tf32(w);
-        bl[s2][q][h] = to_tf32(w - __uint_as_float(bh[s2][q][h]));
-      }
-  // this CTA's voxel range (mix_ring2_kernel's chunking, in 4-voxel vectors)
-  const long long nv = n / 4;
-  const long long chunk =
-      ((nv + gridDim.x - 1) / gridDim.x + kMixThreads - 1) / kMixThreads * kMixThreads;
-  const long long vbeg = blockIdx.x * chunk * 4, vend = min(n, (blockIdx.x + 1) * chunk * 4);
-  const int ngroups = vbeg < vend ? int((vend - vbeg) / 16) : 0;
-  const int E = K + 1;
-  const int pieces = 4 * E;  // 16-byte pieces per group (E entries x 16 voxels)
-  // my groups: warp, warp + 8, ...
-  const int mine = ngroups > warp ? (ngroups - warp + 7) / 8 : 0;
-  const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(ring));
-  auto issue = [&](int j) {  // group j of mine into stage j % NS
-    const long long v0 = vbeg + 16LL * (warp + 8LL * j);
-    const unsigned st = sbase + unsigned((j % kMmaNS) * kStage * 4);
-    for (int p = lane; p < pieces; p += 32) {
-      const int e = p >> 2, v4 = p & 3;
-      const float* src = (e == 0 ? b : terms + (long long)(e - 1) * n) + v0 + 4 * v4;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(st + unsigned((e * kMmaPitch + 4 * v4) * 4)),
-                   "l"(src));
-    }
-  };
-#pragma unroll 1
-  for (int j = 0; j < kMmaNS - 1; ++j) {
-    if (j < mine) issue(j);
-    cp_async_commit();
-  }
-  float bv[2][2];
-  int bi[2][2];
-#pragma unroll
-  for (int q = 0; q < 2; ++q)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      bv[q][h] = -INFINITY;
-      bi[q][h] = 0x7fffffff;
-    }
-  for (int j = 0; j < mine; ++j) {
-    cp_async_wait_group<kMmaNS - 2>();
-    __syncwarp();
-    const float* st = ring + (j % kMmaNS) * kStage;
-    float c[2][4];
-#pragma unroll
-    for (int q = 0; q < 2; ++q)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) c[q][r] = 0.f;
-#pragma unroll
-    for (int s2 = 0; s2 < 2; ++s2) {
-      const float av[4] = {st[(8 * s2 + t) * kMmaPitch + g], st[(8 * s2 + t) * kMmaPitch + g + 8],
-                           st[(8 * s2 + t + 4) * kMmaPitch + g],
-                           st[(8 * s2 + t + 4) * kMmaPitch + g + 8]};
-      unsigned ah[4], al[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        ah[r] = to_tf32(av[r]);
-        al[r] = to_tf32(av[r] - __uint_as_float(ah[r]));
-      }
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        mma_tf32(c[q], al, bh[s2][q][0], bh[s2][q][1]);
-        mma_tf32(c[q], ah, bl[s2][q][0], bl[s2][q][1]);
-        mma_tf32(c[q], ah, bh[s2][q][0], bh[s2][q][1]);
-      }
-    }
-    __syncwarp();  // every lane is done with this stage before it is refilled
-    if (j + kMmaNS - 1 < mine) issue(j + kMmaNS - 1);
-    cp_async_commit();
-    // running maxima: columns 8q + 2t + h, voxels v0 + g (rows r = 0, 1) and v0 + g + 8
-    const long long v0 = vbeg + 16LL * (warp + 8LL * j);
-    const int z0 = int(v0 % nz);
-    const long long row = v0 / nz;
-    const int y = int(row % ny), x = int(row / ny);
-    if (x >= wlo.x && x <= whi.x && y >= wlo.y && y <= whi.y) {
-      const bool in0 = z0 + g >= wlo.z && z0 + g <= whi.z;
-      const bool in1 = z0 + g + 8 >= wlo.z && z0 + g + 8 <= whi.z;
-#pragma unroll
-      for (int q = 0; q < 2; ++q)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (in0 && c[q][h] > bv[q][h]) {
-            bv[q][h] = c[q][h];
-            bi[q][h] = int(v0 + g);
-          }
-          if (in1 && c[q][2 + h] > bv[q][h]) {
-            bv[q][h] = c[q][2 + h];
-            bi[q][h] = int(v0 + g + 8);
-          }
-        }
-    }
-  }
-  cp_async_wait_group<0>();
-  // reduce each column over the 8 lanes that share t (lane bits 2..4), then warps
-#pragma unroll
-  for (int q = 0; q < 2; ++q)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      Best bm = {bi[q][h] == 0x7fffffff ? -INFINITY : double(bv[q][h]) / lam,
-                 bi[q][h] == 0x7fffffff ? 0x7fffffffffffffffLL : (long long)bi[q][h]};
-#pragma unroll
-      for (int o = 4; o < 32; o <<= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bm.v, o);
-        const long long oi = __shfl_xor_sync(0xffffffffu, bm.idx, o);
-        if (better(ov, oi, bm.v, bm.idx)) bm = {ov, oi};
-      }
-      if (g == 0) red[8 * q + 2 * t + h][warp] = bm;
-    }
-  __syncthreads();
-  if (threadIdx.x < ncol) {
-    const int col = threadIdx.x;
-    Best bm = red[col][0];
-    for (int w = 1; w < kMixThreads / 32; ++w)
-      if (better(red[col][w].v, red[col][w].idx, bm.v, bm.idx)) bm = red[col][w];
-    partial[(long long)colmem[col] * gridDim.x + blockIdx.x] = bm;
-  }
-}
-
 // [sum |b|, max |b|] from the mix's per-CTA statistics, fixed order
 __global__ void abs_reduce_kernel(const double* __restrict__ parts, int nblocks,
                                   double* __restrict__ out) {
@@ -2184,32 +1631,9 @@ __global__ void member_reduce_kernel(const Best* __restrict__ partial, int nbloc
 
 }  // namespace
 
-static size_t xmix_smem(const BasisSet* s);
-// The fused x pass + mix (opt-in: SFW3D_XMIX=1) applies to fp32 tables whose
-// inner (y, z) plane is a multiple of the 64-wide tile and whose weights and
-// taps fit in shared memory. Measured on config 4 (16 members, 26 terms): the
-// 16 x J accumulators hold the kernel at 8 warps per SM and it issues at
-// ~45-55% — 17-21 ms against 14.3 ms for the separate x pass (26 launches,
-// J = 32 register windows) + HBM-bound mix, so the separate kernels stay the
-// default (profiles/round1/xmix_notes.md).
-static bool xmix_ok(const BasisSet* s, int dtype, const int dims[3]) {
-  const char* e = getenv("SFW3D_XMIX");
-  if (!(e && atoi(e) == 1) || dtype != SFW3D_F32 || !s->xtaps_dev) return false;
-  if ((long long)dims[1] * dims[2] % kXTI != 0) return false;
-  return xmix_smem(s) <= 200 * 1024;
-}
-static int xmix_stage_rows(const BasisSet* s) { return kXTo + s->max_nt4x + kXJ + kXP + 4; }
-static size_t xmix_smem(const BasisSet* s) {
-  const int K = int(s->betas.size());
-  return sizeof(float) * size_t(kXNS) * (xmix_stage_rows(s) + kXTo) * kXTI +
-         sizeof(f2) * (size_t(K) * 16 + 16 + s->xtaps_total + 8) + sizeof(int4) * K;
-}
-static long long xmix_tiles(const int dims[3]) {
-  return (long long)((dims[0] + kXTo - 1) / kXTo) * ((long long)dims[1] * dims[2] / kXTI);
-}
 // per-member partial maxima: one per evaluation CTA
 static long long eval_blocks(const BasisSet* s, int dtype, const int dims[3], int num_sms) {
-  if (xmix_ok(s, dtype, dims)) return xmix_tiles(dims);
+  (void)s; (void)dtype; (void)dims;
   return std::min<long long>(4096, (long long)num_sms * 8);
 }
 
@@ -2273,8 +1697,7 @@ static int launch_ring2(sfw3d_ctx* ctx, int nblocks, const void* b, const void* 
 // 16-byte vectors. The collect pass then chunks with the same V = 16 / es.
 static bool ring2_all_ok(const BasisSet* s, int dtype, const int dims[3]) {
   const int V4 = dtype == SFW3D_F64 ? 2 : 4;
-  return s->Wd_dev && !s->mma_mix && s->nmc <= 8 && dims[2] % V4 == 0 &&
-         !getenv("SFW3D_MIX_V1") && !getenv("SFW3D_MIX_RING1");
+  return s->Wd_dev && s->nmc <= 8 && dims[2] % V4 == 0;
 }
 
 template <typename T>
@@ -2308,33 +1731,13 @@ static int launch_mix(sfw3d_ctx* ctx, int nblocks, const void* b, const void* te
                       int4 whi, double lam, void* fields, Best* partial, const Collect* col) {
   constexpr int V4 = 16 / sizeof(T);  // 4 floats / 2 doubles
   const int nz = dims[2];
-  const bool ring = nz % V4 == 0 && nmm <= 16 && !getenv("SFW3D_MIX_V1");
-  // tensor-core mix (fp32): all members in one launch, argmax only
-  if constexpr (sizeof(T) == 4) {
-    if (!col && !fields && s->mma_mix && s->Bmat_dev && m0 == 0 && nmm == int(s->members.size()) &&
-        s->ncol == nmm && n % 16 == 0 && nz % 16 == 0) {
-      const size_t smem = size_t(kMixThreads / 32) * kMmaNS * 16 * kMmaPitch * sizeof(float);
-      SFW3D_CUDA_TRY(cudaFuncSetAttribute(mix_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          int(smem)));
-      mix_mma_kernel<<<nblocks, kMixThreads, smem, ctx->stream>>>(
-          static_cast<const float*>(b), static_cast<const float*>(terms), n, nt, s->Bmat_dev,
-          s->colmem_dev, s->ncol, dims[0], dims[1], dims[2], wlo, whi, lam, partial);
-      return SFW3D_OK;
-    }
-  }
+  const bool ring = nz % V4 == 0 && nmm <= 16;
   // v2 ring: all members in one launch, argmax only (fields keep the v1 path)
   if (!col && !fields && ring && m0 == 0 && nmm == int(s->members.size()) && s->nmd <= 16 &&
-      s->nmc <= 8 && s->Wd_dev && !getenv("SFW3D_MIX_RING1")) {
-    // ring depth (SFW3D_MIX_NS: 8 or 16 slots of 16 bytes per thread)
-    static const int ns = [] {
-      const char* e = getenv("SFW3D_MIX_NS");
-      return e ? atoi(e) : 16;
-    }();
-#define SFW3D_RING2(NMD)                                                                        \
-  return ns == 8 ? launch_ring2<T, NMD, 8>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, \
-                                           partial)                                             \
-                 : launch_ring2<T, NMD, 16>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, \
-                                            partial)
+      s->nmc <= 8 && s->Wd_dev) {
+    // (16 ring slots of 16 bytes per thread)
+#define SFW3D_RING2(NMD) \
+  return launch_ring2<T, NMD, 16>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial)
     if (s->nmd <= 4) SFW3D_RING2(4);
     if (s->nmd <= 8) SFW3D_RING2(8);
     if (s->nmd <= 12) SFW3D_RING2(12);
@@ -2373,37 +1776,6 @@ static int launch_mix(sfw3d_ctx* ctx, int nblocks, const void* b, const void* te
 #undef SFW3D_MIX
 }
 
-template <int NM, bool COLLECT>
-static int launch_xmix_nm(sfw3d_ctx* ctx, const BasisSet* s, const int dims[3], const float* b,
-                          const float* U, int K, int nm, int m0, int4 wlo, int4 whi, double lam,
-                          float* fields, Best* partial, const Collect* col) {
-  const size_t smem = xmix_smem(s);
-  SFW3D_CUDA_TRY(cudaFuncSetAttribute(xmix_kernel<NM, COLLECT>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  // persistent CTAs (one per SM) for the evaluation; one tile per CTA for
-  // the collect pass (most tiles exit at once)
-  const long long tiles = xmix_tiles(dims);
-  const unsigned grid = COLLECT ? unsigned(tiles) : unsigned(std::min<long long>(tiles, ctx->num_sms));
-  xmix_kernel<NM, COLLECT><<<grid, kXW * 32, smem, ctx->stream>>>(
-      b, U, vol_count(dims), K, nm, m0, static_cast<const float*>(s->W_dev),
-      static_cast<const float*>(s->w0_dev), s->cid_dev, s->xtaps_dev, s->xmeta_dev, s->xtaps_total,
-      xmix_stage_rows(s), dims[0], dims[1], dims[2], wlo, whi, lam, fields, partial,
-      col ? *col : Collect{});
-  SFW3D_LAUNCH_CHECK(ctx);
-  return SFW3D_OK;
-}
-
-static int launch_xmix(sfw3d_ctx* ctx, const BasisSet* s, const int dims[3], const float* b,
-                       const float* U, int K, int nm, int m0, int4 wlo, int4 whi, double lam,
-                       float* fields, Best* partial, const Collect* col) {
-  if (col) {
-    if (nm <= 8) return launch_xmix_nm<8, true>(ctx, s, dims, b, U, K, nm, m0, wlo, whi, lam, fields, partial, col);
-    return launch_xmix_nm<16, true>(ctx, s, dims, b, U, K, nm, m0, wlo, whi, lam, fields, partial, col);
-  }
-  if (nm <= 8) return launch_xmix_nm<8, false>(ctx, s, dims, b, U, K, nm, m0, wlo, whi, lam, fields, partial, col);
-  return launch_xmix_nm<16, false>(ctx, s, dims, b, U, K, nm, m0, wlo, whi, lam, fields, partial, col);
-}
-
 int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[3], const void* b,
                    double lam, const int32_t win[6], void* fields, Best* best_dev, void* scratch,
                    double* abs_dev, bool* abs_done) {
@@ -2424,38 +1796,17 @@ int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[
   Best* partial = cv.take<Best>(size_t(nm) * nblocks);
   double* absparts = cv.take<double>(2 * size_t(nblocks));
   const int4 wlo = make_int4(win[0], win[2], win[4], 0), whi = make_int4(win[1], win[3], win[5], 0);
-  if (xmix_ok(s, dtype, dims)) {
-    // U_k = f_k^(y) f_k^(z) * b per term, then the fused x pass + mix
-    for (int t = 0; t < nt; ++t) {
-      const char* tp = static_cast<const char*>(s->taps[t]);
-      const int l0 = s->tlen[0][t], l1 = s->tlen[1][t], l2 = s->tlen[2][t];
-      SFW3D_TRY(corr_pass_impl(ctx, dtype, b, t1, dims, 2, tp + es * (l0 + l1), s->tlo[2][t], l2,
-                               nullptr, 0.0, 1.0, "eta_basis"));
-      SFW3D_TRY(corr_pass_impl(ctx, dtype, t1, terms + size_t(t) * n * es, dims, 1, tp + es * l0,
-                               s->tlo[1][t], l1, nullptr, 0.0, 1.0, "eta_basis"));
-    }
-    for (int m0 = 0; m0 < nm; m0 += 16) {
-      SFW3D_PROF(ctx, "eta_mix");
-      SFW3D_TRY(launch_xmix(ctx, s, dims, static_cast<const float*>(b),
-                            reinterpret_cast<const float*>(terms), nt, std::min(16, nm - m0), m0,
-                            wlo, whi, lam, static_cast<float*>(fields), partial, nullptr));
-    }
-  } else {
+  {
   // T_k = (f_k x f_k x f_k) * b for every shared term; chained terms
   // T_k = (g_k x g_k x g_k) * T_parent (parents: narrower, larger index)
   for (int t = nt - 1; t >= 0; --t) {
     const char* tp = static_cast<const char*>(s->taps[t]);
     const int l0 = s->tlen[0][t], l1 = s->tlen[1][t], l2 = s->tlen[2][t];
     const void* src = s->parent[t] < 0 ? b : terms + size_t(s->parent[t]) * n * es;
-    if (zy_ok(dims, l1, l2)) {
-      SFW3D_TRY(corr_pass_zy(ctx, dtype, src, t2, dims, tp + es * (l0 + l1), s->tlo[2][t], l2,
-                             tp + es * l0, s->tlo[1][t], l1, "eta_basis"));
-    } else {
-      SFW3D_TRY(corr_pass_impl(ctx, dtype, src, t1, dims, 2, tp + es * (l0 + l1), s->tlo[2][t], l2,
-                               nullptr, 0.0, 1.0, "eta_basis"));
-      SFW3D_TRY(corr_pass_impl(ctx, dtype, t1, t2, dims, 1, tp + es * l0, s->tlo[1][t], l1,
-                               nullptr, 0.0, 1.0, "eta_basis"));
-    }
+    SFW3D_TRY(corr_pass_impl(ctx, dtype, src, t1, dims, 2, tp + es * (l0 + l1), s->tlo[2][t], l2,
+                             nullptr, 0.0, 1.0, "eta_basis"));
+    SFW3D_TRY(corr_pass_impl(ctx, dtype, t1, t2, dims, 1, tp + es * l0, s->tlo[1][t], l1,
+                             nullptr, 0.0, 1.0, "eta_basis"));
     SFW3D_TRY(corr_pass_impl(ctx, dtype, t2, terms + size_t(t) * n * es, dims, 0, tp, s->tlo[0][t],
                              l0, nullptr, 0.0, 1.0, "eta_basis"));
   }
@@ -2507,41 +1858,8 @@ int basis_set_collect(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int di
   const Best* partial = cv.take<Best>(size_t(nm) * nblocks);  // left by basis_set_eval
   const int4 wlo = make_int4(win[0], win[2], win[4], 0), whi = make_int4(win[1], win[3], win[5], 0);
   SFW3D_CUDA_TRY(cudaMemsetAsync(count_dev, 0, sizeof(int) * (1 + nm), ctx->stream));
-  if (xmix_ok(s, dtype, dims)) {
-    // re-run the fused kernel on the tiles whose evaluation maxima qualify
-    const Collect col{thr_dev, cand_dev, idx_dev, count_dev, cap, partial, nblocks, 1};
-    for (int m0 = 0; m0 < nm; m0 += 16) {
-      SFW3D_PROF(ctx, "eta_refine");
-      SFW3D_TRY(launch_xmix(ctx, s, dims, static_cast<const float*>(b),
-                            reinterpret_cast<const float*>(terms), nt, std::min(16, nm - m0), m0,
-                            wlo, whi, lam, nullptr, nullptr, &col));
-    }
-    return SFW3D_OK;
-  }
   constexpr int kSplit = 32;
   const Collect col{thr_dev, cand_dev, idx_dev, count_dev, cap, partial, nblocks, kSplit};
-  if (getenv("SFW3D_DEBUG_COLLECT")) {
-    std::vector<Best> hp(size_t(nm) * nblocks);
-    std::vector<double> ht(nm);
-    SFW3D_TRY(download_sync(ctx, hp.data(), partial, hp.size() * sizeof(Best)));
-    SFW3D_TRY(download_sync(ctx, ht.data(), thr_dev, ht.size() * sizeof(double)));
-    int any = 0;
-    for (int b = 0; b < nblocks; ++b) {
-      int a = 0;
-      for (int m = 0; m < nm; ++m) a |= hp[size_t(m) * nblocks + b].v >= ht[m];
-      any += a;
-    }
-    for (int m = 0; m < nm; ++m) {
-      double mx = -INFINITY;
-      int q = 0;
-      for (int b = 0; b < nblocks; ++b) {
-        mx = std::max(mx, hp[size_t(m) * nblocks + b].v);
-        q += hp[size_t(m) * nblocks + b].v >= ht[m];
-      }
-      fprintf(stderr, "[collect] member %d thr %.9g max %.9g ctas %d\n", m, ht[m], mx, q);
-    }
-    fprintf(stderr, "[collect] %d of %d CTAs qualify\n", any, nblocks);
-  }
   // (16-member slices when the evaluation ran through mix_ring2_kernel: the
   // V = 4 collect kernel keeps 16 x 4 accumulators in registers)
   const int step = (!fields && ring2_all_ok(s, dtype, dims)) ? 16 : kMixMax;

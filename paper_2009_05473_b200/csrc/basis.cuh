@@ -37,7 +37,7 @@ int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands,
                     double tol, BasisSet** out, bool on_device = true, bool prune = false,
                     double loose = 0.0);
 // storage-dependent looser selection tolerance for the shared terms (fp32:
-// SFW3D_BASIS_LOOSE, default below; fp64: none)
+// 1e-5; fp64: none)
 double basis_loose_tol(int dtype);
 // host copy of the fit: betas[n_terms], weights[n_cand][max_terms] (member rows,
 // zero elsewhere), w0[n_cand], fit_err[n_cand], member[n_cand]; NULLs skipped
@@ -47,10 +47,13 @@ void basis_set_destroy(BasisSet* s);
 // tables prune their shared terms for volumes of >= 2^26 voxels (~406^3;
 // fp32 storage: >= 2^24, 256^3): there a term's three full-volume passes per
 // certificate outweigh the seconds of host NNLS refits the pruning costs
-// once per table (config 3: 48 -> 18 terms). SFW3D_BASIS_PRUNE=0/1 overrides.
+// once per table (config 3: 48 -> 18 terms). The table option "prune"
+// overrides (sfw3d_table_set_option); sharded tables pass the GLOBAL dims.
+inline bool basis_prune_voxels(long long voxels, int dtype) {
+  return voxels >= (dtype == SFW3D_F32 ? (1LL << 24) : (1LL << 26));
+}
 inline bool basis_prune_rule(const int dims[3], int dtype) {
-  if (const char* e = getenv("SFW3D_BASIS_PRUNE")) return atoi(e) != 0;
-  return (long long)dims[0] * dims[1] * dims[2] >= (dtype == SFW3D_F32 ? (1LL << 24) : (1LL << 26));
+  return basis_prune_voxels((long long)dims[0] * dims[1] * dims[2], dtype);
 }
 // candidate -> (is member, fit error of its shared-dictionary fit)
 bool basis_set_member(const BasisSet* s, int cand, double* fit_err);

@@ -24,9 +24,11 @@
 //   voxels within 2 E_c of the member's approximate maximum are re-evaluated
 //   with the direct taps, so maxima / argmaxima are the direct ones.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
+#include <string>
 #include <utility>
 
 #include "basis.cuh"
@@ -60,6 +62,12 @@ struct sfw3d_table {
   int device;
   int mode;      // 0 auto, 1 direct only
   double basis_tol;
+  // sfw3d_table_set_option: basis term pruning (-1 = by volume size), fp32
+  // shared-term selection tolerance (< 0 = default), refinement item cap
+  int prune = -1;
+  long long global_voxels = 0;  // > 0: the pruning rule's voxel count (sharded tables)
+  double loose_tol = -1.0;
+  int refine_cap = 1 << 16;
   int smem_max;  // opt-in shared memory per block of the device
   // shared separable bases (basis.cu), one per storage precision, fitted on
   // first use of that precision (a solve only ever touches one)
@@ -635,8 +643,12 @@ static int ensure_basis(const sfw3d_table* t, int dtype) {
   SFW3D_CUDA_TRY(cudaGetDevice(&dev));
   SFW3D_CUDA_TRY(cudaSetDevice(t->device));
   BasisSet* built = nullptr;
-  const int st = basis_set_build(t->dims, t->bcands, dtype, tol, &built, true,
-                                 basis_prune_rule(t->dims, dtype), basis_loose_tol(dtype));
+  bool prune = t->prune != 0;
+  if (t->prune < 0)
+    prune = t->global_voxels > 0 ? basis_prune_voxels(t->global_voxels, dtype)
+                                 : basis_prune_rule(t->dims, dtype);
+  const double loose = t->loose_tol < 0.0 ? basis_loose_tol(dtype) : t->loose_tol;
+  const int st = basis_set_build(t->dims, t->bcands, dtype, tol, &built, true, prune, loose);
   cudaSetDevice(dev);
   if (st != SFW3D_OK) {
     basis_set_destroy(built);
@@ -663,30 +675,15 @@ static bool use_refine(const sfw3d_table* t, int ci, int dtype, bool fields = fa
   return dtype == SFW3D_F64 && basis_set_member(s, ci, &fe) && fe > 0.0;
 }
 
-// folded kernel tile: outputs per thread along z (fp32 32, fp64 16) and
-// y rows (32 x NWY, fp32 NWY = 2); SFW3D_FOLD_KJ / SFW3D_FOLD_NWY override
-// the fp32 choice for tuning. z extent, smem row pitch, dynamic smem bytes.
-static int env_int(const char* name, int def) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : def;
-}
-static int fold_kj_rt(int esize) {
-  static const int kj32 = env_int("SFW3D_FOLD_KJ", 32) == 16 ? 16 : 32;
-  return esize == 8 ? 16 : kj32;
-}
-static int fold_nwy_rt(int esize) {
-  static const int nwy32 = env_int("SFW3D_FOLD_NWY", 1) == 2 ? 2 : 1;
-  return esize == 8 ? 1 : nwy32;
-}
+// folded kernel tile: outputs per thread along z (fp32 32, fp64 16), one
+// 32-row y group per CTA. z extent, smem row pitch, dynamic smem bytes.
+static int fold_kj_rt(int esize) { return esize == 8 ? 16 : 32; }
+static int fold_nwy_rt(int) { return 1; }
 static int fold_tz(int esize) { return fold_kj_rt(esize) * kWarps; }
 // fp32 KJ = 32 tiles keep the per-slice sums in a global scratch slab per
 // CTA (L2-resident traffic of 2 x 16 KB per slice): the freed 16 KB of shared
 // memory and a 128-register budget give 4 resident CTAs instead of 3
-// (SFW3D_FOLD_ACCD_GLOBAL=0: shared-memory sums, for comparison)
-static bool fold_accd_global(int esize) {
-  static const int ag = env_int("SFW3D_FOLD_ACCD_GLOBAL", 1);
-  return esize == 4 && ag != 0 && fold_kj_rt(esize) == 32 && fold_nwy_rt(esize) == 1;
-}
+static bool fold_accd_global(int esize) { return esize == 4; }
 static int fold_smem(const CandHost& c, int esize) {
   const int kj = fold_kj_rt(esize), nwy = fold_nwy_rt(esize);
   if (fold_accd_global(esize)) {
@@ -755,8 +752,9 @@ extern "C" int sfw3d_basis_fit(const int32_t lo[3], const int32_t hi[3], double 
 
 extern "C" int sfw3d_basis_set_fit(const int32_t dims[3], int n_sigma, const double* sigmas,
                                    int n_shape, const double* shapes, int dtype, double tol,
-                                   int max_terms, int* n_terms, double* betas, double* weights,
-                                   double* w0, double* fit_err, int32_t* member) {
+                                   int prune, double loose_tol, int max_terms, int* n_terms,
+                                   double* betas, double* weights, double* w0, double* fit_err,
+                                   int32_t* member) {
   SFW3D_CHECK_ARG(dims && sigmas && shapes && n_terms, "NULL argument");
   SFW3D_CHECK_ARG(n_sigma > 0 && n_shape > 0, "empty candidate grid");
   SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
@@ -774,12 +772,41 @@ extern "C" int sfw3d_basis_set_fit(const int32_t dims[3], int n_sigma, const dou
       bc.push_back(c);
     }
   BasisSet* s = nullptr;
-  const int st = basis_set_build(dm, bc, dtype, tol, &s, /*on_device=*/false, basis_prune_rule(dm, dtype),
-                                 basis_loose_tol(dtype));
+  const bool pr = prune < 0 ? basis_prune_rule(dm, dtype) : prune != 0;
+  const double lo = loose_tol < 0.0 ? basis_loose_tol(dtype) : loose_tol;
+  const int st = basis_set_build(dm, bc, dtype, tol, &s, /*on_device=*/false, pr, lo);
   if (st == SFW3D_OK)
     basis_set_export(s, max_terms, n_terms, betas, weights, w0, fit_err, member);
   basis_set_destroy(s);
   return st;
+}
+
+extern "C" int sfw3d_table_set_option(sfw3d_table* t, const char* name, double value) {
+  SFW3D_CHECK_ARG(t && name, "NULL argument");
+  const std::string key(name);
+  if (key == "prune") {
+    SFW3D_CHECK_ARG(value == -1.0 || value == 0.0 || value == 1.0, "prune must be -1, 0 or 1");
+    t->prune = int(value);
+  } else if (key == "global_voxels") {
+    SFW3D_CHECK_ARG(value >= 0.0 && value < 0x1p62, "global_voxels out of range");
+    t->global_voxels = (long long)value;
+  } else if (key == "loose_tol") {
+    SFW3D_CHECK_ARG(std::isfinite(value), "loose_tol must be finite");
+    t->loose_tol = value;
+  } else if (key == "refine_cap") {
+    SFW3D_CHECK_ARG(value >= 1.0 && value <= double(1 << 24), "refine_cap out of range");
+    t->refine_cap = int(value);
+    return SFW3D_OK;  // (no basis rebuild)
+  } else {
+    set_error("unknown table option (prune, global_voxels, loose_tol, refine_cap)");
+    return SFW3D_EINVAL;
+  }
+  // the shared bases depend on prune / loose_tol: refit on next use
+  cudaSetDevice(t->device);
+  basis_set_destroy(t->set32);
+  basis_set_destroy(t->set64);
+  t->set32 = t->set64 = nullptr;
+  return SFW3D_OK;
 }
 
 extern "C" int sfw3d_table_destroy(sfw3d_table* t) {
@@ -945,11 +972,8 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   // back to them: the copy is then made on demand)
   const size_t pbytes = size_t(t->pdims[0]) * t->pdims[1] * t->pdims[2] * sizeof(T);
   const size_t pb = (any_direct || any_refine) ? pbytes : 0;
-  // refinement items per call (SFW3D_REFINE_CAP overrides, for tests)
-  const int kRefCap = [] {
-    const char* e = getenv("SFW3D_REFINE_CAP");
-    return e ? std::max(1, atoi(e)) : (1 << 16);
-  }();
+  // refinement items per call (a table option: tests shrink it)
+  const int kRefCap = t->refine_cap;
   // direct output tiles: the window, or the whole grid when fields are requested
   int ow[6];
   if (fields) {
@@ -1149,16 +1173,7 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
         SFW3D_PROF(ctx, "eta_direct");
         dim3 grid(unsigned(gc.nty * gc.ntz), unsigned(nxp));
         if constexpr (sizeof(T) == 4) {
-          if (kj == 32 && nwy == 1 && fold_accd_global(4))
-            SFW3D_TRY((launch_fold<T, 32, 1, true>(ctx, grid, smem, bpad, gc, cd, fld, partial)));
-          else if (kj == 32 && nwy == 2)
-            SFW3D_TRY((launch_fold<T, 32, 2>(ctx, grid, smem, bpad, gc, cd, fld, partial)));
-          else if (kj == 32)
-            SFW3D_TRY((launch_fold<T, 32, 1>(ctx, grid, smem, bpad, gc, cd, fld, partial)));
-          else if (nwy == 2)
-            SFW3D_TRY((launch_fold<T, 16, 2>(ctx, grid, smem, bpad, gc, cd, fld, partial)));
-          else
-            SFW3D_TRY((launch_fold<T, 16, 1>(ctx, grid, smem, bpad, gc, cd, fld, partial)));
+          SFW3D_TRY((launch_fold<T, 32, 1, true>(ctx, grid, smem, bpad, gc, cd, fld, partial)));
         } else {
           SFW3D_TRY((launch_fold<T, 16, 1>(ctx, grid, smem, bpad, gc, cd, fld, partial)));
         }

@@ -175,11 +175,6 @@ int psf_apply_impl(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* 
 int corr_pass_impl(sfw3d_ctx* ctx, int dtype, const void* in, void* out, const int dims[3], int axis,
                    const void* taps, int lo, int ntaps, const void* addend, double addend_w,
                    double w, const char* family);
-// fused z + y passes (psf.cu pass_zy_kernel): out = f_y * (f_z * in)
-bool zy_ok(const int dims[3], int ly, int lz);
-int corr_pass_zy(sfw3d_ctx* ctx, int dtype, const void* in, void* out, const int dims[3],
-                 const void* tz, int loz, int lz, const void* ty, int loy, int ly,
-                 const char* family);
 
 // Launch helpers implemented in the .cu files.
 int render_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const AtomGeo* atoms_dev,

@@ -92,77 +92,6 @@ __global__ void __launch_bounds__(256) pass_strided_kernel(
   }
 }
 
-// Strided axes, shared-memory tiled: a CTA owns 64 consecutive inner
-// (contiguous) indices x 4J outputs along the axis; the (4J + taps) input
-// rows are staged once with coalesced 256-byte row loads, so each input is
-// read ~ (4J + taps) / 4J times instead of (J + taps) / J. Lanes run over the
-// inner index: conflict-free smem, coalesced stores.
-
-template <typename T, int J, int kTInner, int NT>
-__global__ void __launch_bounds__(NT) pass_tiled_kernel(
-    const T* __restrict__ in, T* out, int n_axis, long long stride, const T* __restrict__ taps_g,
-    int lo, int ntaps, const T* addend, T aw, T w) {
-  constexpr int kTGroups = NT / kTInner;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int npad = (ntaps + J - 1) / J * J;
-  T* taps = reinterpret_cast<T*>(smem_raw);
-  T* tile = taps + npad;
-  constexpr int To = J * kTGroups;
-  const int a0 = blockIdx.x * To;
-  const long long inner0 = (long long)blockIdx.y * kTInner;
-  const long long base0 = (long long)blockIdx.z * n_axis * stride + inner0;
-  const int rows = To + npad;
-  load_taps_padded<T, J>(taps, taps_g, ntaps, npad);
-  constexpr int kVec = 16 / sizeof(T);  // elements per 16-byte async copy
-  constexpr int kRowVecs = kTInner / kVec;
-  for (int e = threadIdx.x; e < rows * kRowVecs; e += blockDim.x) {
-    const int r = e / kRowVecs, c = (e % kRowVecs) * kVec;
-    const int a = pmod_i(a0 + lo + r, n_axis);
-    cp_async16(tile + r * kTInner + c, in + base0 + (long long)a * stride + c);
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  const int il = threadIdx.x % kTInner, ag = threadIdx.x / kTInner;
-  const T* src = tile + (ag * J) * kTInner + il;
-  T W[J], acc[J];
-#pragma unroll
-  for (int j = 0; j < J; ++j) {
-    W[j] = src[j * kTInner];
-    acc[j] = T(0);
-  }
-  for (int q0 = 0; q0 < npad; q0 += J) {
-#pragma unroll
-    for (int r = 0; r < J; ++r) {
-      const T t = taps[q0 + r];
-#pragma unroll
-      for (int j = 0; j < J; ++j) acc[j] = fma(t, W[(r + j) % J], acc[j]);
-      W[r] = src[(q0 + r + J) * kTInner];
-    }
-  }
-  {
-    const int a1 = a0 + ag * J;
-    const long long o0 = base0 + (long long)a1 * stride + il;
-    T* po = out + o0;
-    if (!addend && a1 + J <= n_axis) {  // full group: unguarded stores
-      if (w == T(1)) {
-#pragma unroll
-        for (int j = 0; j < J; ++j, po += stride) *po = acc[j];
-      } else {
-#pragma unroll
-        for (int j = 0; j < J; ++j, po += stride) *po = T(w * acc[j]);
-      }
-    } else if (addend) {
-      const T* pa = addend + o0;
-#pragma unroll
-      for (int j = 0; j < J; ++j, po += stride, pa += stride)
-        if (a1 + j < n_axis) *po = T(aw * *pa + w * acc[j]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < J; ++j, po += stride)
-        if (a1 + j < n_axis) *po = T(w * acc[j]);
-    }
-  }
-}
 
 constexpr int kZRows = 32;   // rows per CTA (one per lane)
 constexpr int kZWarps = 4;   // z-groups per CTA
@@ -349,116 +278,6 @@ __global__ void __launch_bounds__(NT, MINB) pass_tile2_kernel(
   }
 }
 
-// Persistent, double-buffered variant of pass_tile2_kernel (no addend,
-// w = 1): each CTA walks tiles t = blockIdx.x, + gridDim.x, ... (axis-major
-// order, so consecutive tiles of a CTA share nothing but neighbours in the
-// grid share halos through L2) and stages tile t + 1 with cp.async while it
-// computes tile t, so the staging latency overlaps the FFMA work instead of
-// relying on other resident CTAs.
-template <typename T, int J, int TI, int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) pass_tile2p_kernel(
-    const T* __restrict__ in, T* __restrict__ out, int n_axis, long long stride,
-    const T* __restrict__ taps_g, int lo, int ntaps, int tiles_x, int tiles_y, long long ntiles) {
-  constexpr int G = NT / TI, To = J * G;
-  constexpr int kVec = 16 / sizeof(T), kRowVecs = TI / kVec;
-  static_assert(NT % kRowVecs == 0, "row vectors");
-  constexpr int dr = NT / kRowVecs;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int nt4 = (ntaps + 3) & ~3;
-  const int rows = To + nt4;
-  T* taps = reinterpret_cast<T*>(smem_raw);
-  T* const stage0 = taps + nt4;
-  const int stage_elems = rows * TI;
-  for (int q = threadIdx.x; q < nt4; q += NT) taps[q] = q < ntaps ? taps_g[q] : T(0);
-  const int c = (threadIdx.x % kRowVecs) * kVec;
-  auto tile_of = [&](long long t, int& a0, long long& base0) {
-    const int bx = int(t % tiles_x);
-    const long long rest = t / tiles_x;
-    const int by = int(rest % tiles_y);
-    const long long bz = rest / tiles_y;
-    a0 = bx * To;
-    base0 = bz * n_axis * stride + (long long)by * TI;
-  };
-  auto load = [&](long long t, T* tile) {
-    int a0;
-    long long base0;
-    tile_of(t, a0, base0);
-    int r = threadIdx.x / kRowVecs;
-    int a = (a0 + lo + r) % n_axis;
-    if (a < 0) a += n_axis;
-    const T* src = in + base0 + c;
-    T* dst = tile + r * TI + c;
-    if (a0 + lo >= 0 && a0 + lo + rows <= n_axis) {
-      const long long step = (long long)dr * stride;
-      const T* p = src + (long long)a * stride;
-      for (; r < rows; r += dr, dst += dr * TI, p += step) cp_async16(dst, p);
-    } else {
-      for (; r < rows; r += dr, dst += dr * TI) {
-        cp_async16(dst, src + (long long)a * stride);
-        a = (a + dr) % n_axis;
-      }
-    }
-  };
-  const int il = threadIdx.x % TI, ag = threadIdx.x / TI;
-  long long t = blockIdx.x;
-  if (t < ntiles) load(t, stage0);
-  cp_async_commit();
-  for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
-    const long long tn = t + gridDim.x;
-    if (tn < ntiles) load(tn, stage0 + ((i + 1) & 1) * stage_elems);
-    cp_async_commit();
-    cp_async_wait_group<1>();
-    __syncthreads();
-    const T* src = stage0 + (i & 1) * stage_elems + (ag * J) * TI + il;
-    T W[J], acc[J];
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      W[j] = src[j * TI];
-      acc[j] = T(0);
-    }
-    int q0 = 0;
-    for (; q0 + J <= nt4; q0 += J) {
-#pragma unroll
-      for (int r = 0; r < J; r += 4) {
-        T t4[4];
-        ld4(taps + q0 + r, t4[0], t4[1], t4[2], t4[3]);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-#pragma unroll
-          for (int j = 0; j < J; ++j) acc[j] = fma(t4[k], W[(r + k + j) % J], acc[j]);
-          W[r + k] = src[(q0 + r + k + J) * TI];
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < J; r += 4) {
-      if (q0 + r >= nt4) break;
-      T t4[4];
-      ld4(taps + q0 + r, t4[0], t4[1], t4[2], t4[3]);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-#pragma unroll
-        for (int j = 0; j < J; ++j) acc[j] = fma(t4[k], W[(r + k + j) % J], acc[j]);
-        W[r + k] = src[(q0 + r + k + J) * TI];
-      }
-    }
-    int a0;
-    long long base0;
-    tile_of(t, a0, base0);
-    const int a1 = a0 + ag * J;
-    T* po = out + base0 + (long long)a1 * stride + il;
-    if (a1 + J <= n_axis) {
-#pragma unroll
-      for (int j = 0; j < J; ++j, po += stride) *po = acc[j];
-    } else {
-#pragma unroll
-      for (int j = 0; j < J; ++j, po += stride)
-        if (a1 + j < n_axis) *po = acc[j];
-    }
-    __syncthreads();  // the stage is refilled two iterations on
-  }
-  cp_async_wait_group<0>();
-}
 
 // Contiguous axis (2), nz % 4 == 0: a CTA owns 32 rows (lane = row) x 4 J
 // outputs (warp = J-column group). The staged row span starts at the aligned
@@ -469,8 +288,7 @@ __global__ void __launch_bounds__(NT, MINB) pass_tile2p_kernel(
 template <typename T, int J, int MINB = 1>
 __global__ void __launch_bounds__(128, MINB) pass_z2_kernel(
     const T* __restrict__ in, T* __restrict__ out, int nz, long long nrows,
-    const T* __restrict__ taps_g, int lo, int ntaps, int pitch, const T* addend, T aw, T w,
-    int zt) {
+    const T* __restrict__ taps_g, int lo, int ntaps, int pitch, const T* addend, T aw, T w) {
   constexpr int kVec = 16 / sizeof(T);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int sh = ((lo % 4) + 4) % 4;
@@ -525,7 +343,7 @@ __global__ void __launch_bounds__(128, MINB) pass_z2_kernel(
   }
   const long long row = row0 + lane;
   const int zc = z0 + warp * J;
-  if (!addend && (J == 16 ? (zt & 1) : (zt & 2)) && row0 + 32 <= nrows && z0 + 4 * J <= nz) {
+  if (!addend && row0 + 32 <= nrows && z0 + 4 * J <= nz) {
     // narrow filters: transpose through shared memory so every warp store
     // instruction writes whole rows (2 x 256 contiguous bytes)
     __syncthreads();  // every thread is done reading the staged input
@@ -610,178 +428,6 @@ __global__ void __launch_bounds__(128, MINB) pass_z2_kernel(
   }
 }
 
-// Fused in-plane pass (z then y) for narrow factors: out = f_y * (f_z * in)
-// per x-plane, without the intermediate volume's HBM round trip. A CTA owns
-// kZyTY (y) x kZyTZ (z) outputs of one x-plane:
-//   1. stages the wrapped input rows [y0 + lo_y, y0 + kZyTY + hi_y] x the
-//      aligned column span (16-byte cp.async; pitch = 4 mod 8 words),
-//   2. z pass: lane = staged row, warp = 16-column group, the Fold register
-//      window (as pass_z2_kernel) -> intermediate rows in shared memory,
-//   3. y pass: lane = z, 16 consecutive y outputs per thread from a register
-//      window over the intermediate rows (as pass_tile2_kernel) -> coalesced
-//      stores along z.
-constexpr int kZyThreads = 256;
-
-// TY x TZ outputs per CTA; z pass: lane = staged row (rounds of 32 rows),
-// warp = JZ-column group (TZ = 8 JZ); y pass: thread = (z column, group of JY
-// rows), 256 / TZ groups (TY = JY * 256 / TZ).
-template <typename T, int TY, int TZ, int JZ, int JY>
-__global__ void __launch_bounds__(kZyThreads) pass_zy_kernel(
-    const T* __restrict__ in, T* __restrict__ out, int ny, int nz, const T* __restrict__ tz_g,
-    int loz, int lz, const T* __restrict__ ty_g, int loy, int ly, int pitch, int ipitch, int rin) {
-  static_assert(TZ == 8 * JZ && TY == JY * (kZyThreads / TZ), "tile geometry");
-  constexpr int kVec = 16 / sizeof(T);
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int sh = ((loz % 4) + 4) % 4;
-  const int nt4 = (lz + sh + 3) & ~3;        // z taps incl. sh leading zeros
-  const int ny4 = (ly + 3) & ~3;
-  T* tzs = reinterpret_cast<T*>(smem_raw);   // [nt4 + 8]
-  T* tys = tzs + nt4 + 8;                    // [ny4 + 4]
-  T* tile = tys + ny4 + 4;                   // [rin][pitch]
-  T* inter = tile + size_t(rin) * pitch;     // [rin][ipitch]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int x = blockIdx.z, y0 = blockIdx.y * TY, z0 = blockIdx.x * TZ;
-  for (int q = threadIdx.x; q < nt4 + 8; q += kZyThreads)
-    tzs[q] = (q >= sh && q - sh < lz) ? tz_g[q - sh] : T(0);
-  for (int q = threadIdx.x; q < ny4 + 4; q += kZyThreads) tys[q] = q < ly ? ty_g[q] : T(0);
-  // 1. stage rows y0 + loy + r (wrapped), columns [zs, zs + width)
-  const int width = TZ + nt4 + 4;
-  const int nv = width / kVec;
-  {
-    int zs = (z0 + loz - sh) % nz;
-    if (zs < 0) zs += nz;
-    const T* plane = in + (long long)x * ny * nz;
-    int y = (y0 + loy + warp) % ny;
-    if (y < 0) y += ny;
-    for (int r = warp; r < rin; r += kZyThreads / 32) {  // warp = row, lanes over 16-byte vectors
-      const T* prow = plane + (long long)y * nz;
-      T* drow = tile + r * pitch;
-      for (int v = lane; v < nv; v += 32) {
-        int z = zs + v * kVec;
-        while (z >= nz) z -= nz;
-        cp_async16(drow + v * kVec, prow + z);
-      }
-      y += kZyThreads / 32;
-      while (y >= ny) y -= ny;
-    }
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  // 2. z pass over every staged row: lane = row, warp = column group
-  for (int r0 = 0; r0 < rin; r0 += 32) {
-    const int r = r0 + lane;
-    if (r < rin) {
-      T acc[JZ];
-#pragma unroll
-      for (int j = 0; j < JZ; ++j) acc[j] = T(0);
-      const T* const q[1] = {tile + r * pitch + warp * JZ};
-      Fold<T, JZ, 1>::row(acc, tzs, q, nt4 / 4);
-      T* dst = inter + r * ipitch + warp * JZ;
-#pragma unroll
-      for (int j = 0; j < JZ; j += 4) {
-        if constexpr (sizeof(T) == 4) {
-          *reinterpret_cast<float4*>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-        } else {
-          *reinterpret_cast<double2*>(dst + j) = make_double2(acc[j], acc[j + 1]);
-          *reinterpret_cast<double2*>(dst + j + 2) = make_double2(acc[j + 2], acc[j + 3]);
-        }
-      }
-    }
-  }
-  __syncthreads();
-  // 3. y pass: thread = (z column, group of JY consecutive y outputs)
-  const int zc = threadIdx.x % TZ, g = threadIdx.x / TZ;
-  const T* src = inter + (g * JY) * ipitch + zc;
-  T W[JY], acc[JY];
-#pragma unroll
-  for (int j = 0; j < JY; ++j) {
-    W[j] = src[j * ipitch];
-    acc[j] = T(0);
-  }
-  int q0 = 0;
-  for (; q0 + JY <= ny4; q0 += JY) {
-#pragma unroll
-    for (int r = 0; r < JY; r += 4) {
-      T t4[4];
-      ld4(tys + q0 + r, t4[0], t4[1], t4[2], t4[3]);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-#pragma unroll
-        for (int j = 0; j < JY; ++j) acc[j] = fma(t4[k], W[(r + k + j) % JY], acc[j]);
-        W[r + k] = src[(q0 + r + k + JY) * ipitch];
-      }
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < JY; r += 4) {
-    if (q0 + r >= ny4) break;
-    T t4[4];
-    ld4(tys + q0 + r, t4[0], t4[1], t4[2], t4[3]);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-#pragma unroll
-      for (int j = 0; j < JY; ++j) acc[j] = fma(t4[k], W[(r + k + j) % JY], acc[j]);
-      W[r + k] = src[(q0 + r + k + JY) * ipitch];
-    }
-  }
-  const int z = z0 + zc;
-  if (z < nz) {
-    T* po = out + ((long long)x * ny + y0 + g * JY) * nz + z;
-    if (y0 + TY <= ny) {
-#pragma unroll
-      for (int j = 0; j < JY; ++j, po += nz) *po = acc[j];
-    } else {
-#pragma unroll
-      for (int j = 0; j < JY; ++j, po += nz)
-        if (y0 + g * JY + j < ny) *po = acc[j];
-    }
-  }
-}
-
-template <typename T, int TY, int TZ, int JZ, int JY>
-int launch_zy_t(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* tz, int loz,
-                int lz, const T* ty, int loy, int ly) {
-  const int sh = ((loz % 4) + 4) % 4;
-  const int nt4 = (lz + sh + 3) & ~3, ny4 = (ly + 3) & ~3;
-  const int width = TZ + nt4 + 4;
-  // staged rows: outputs + padded taps (the y window's last read-ahead row,
-  // zero-weighted, is row TY + ny4 - 1)
-  const int rin = TY + ny4;
-  int pitch = (width + 3) & ~3;
-  int ipitch = TZ + 4;
-  if (sizeof(T) == 4) {
-    if (pitch % 8 != 4) pitch += 4;
-  } else {
-    if (pitch % 4 != 2) pitch += 2;
-    ipitch = TZ + 2;
-  }
-  const size_t smem = (size_t(nt4) + 8 + ny4 + 4 + size_t(rin) * pitch + size_t(rin) * ipitch) * sizeof(T);
-  if (smem > 48 * 1024)
-    SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_zy_kernel<T, TY, TZ, JZ, JY>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  dim3 grid(unsigned((dims[2] + TZ - 1) / TZ), unsigned((dims[1] + TY - 1) / TY), unsigned(dims[0]));
-  pass_zy_kernel<T, TY, TZ, JZ, JY><<<grid, kZyThreads, smem, ctx->stream>>>(
-      in, out, dims[1], dims[2], tz, loz, lz, ty, loy, ly, pitch, ipitch, rin);
-  SFW3D_LAUNCH_CHECK(ctx);
-  return SFW3D_OK;
-}
-
-// tile variant (SFW3D_ZY_TILE): 0 = 32 x 128 (16, 16), 1 = 64 x 64 (8, 16),
-// 2 = 64 x 128 (16, 32), 3 = 32 x 64 (8, 8)
-template <typename T>
-int launch_zy(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* tz, int loz, int lz,
-              const T* ty, int loy, int ly) {
-  static const int tile = [] {
-    const char* e = getenv("SFW3D_ZY_TILE");
-    return e ? atoi(e) : 1;
-  }();
-  switch (tile) {
-    case 0: return launch_zy_t<T, 32, 128, 16, 16>(ctx, in, out, dims, tz, loz, lz, ty, loy, ly);
-    case 2: return launch_zy_t<T, 64, 128, 16, 32>(ctx, in, out, dims, tz, loz, lz, ty, loy, ly);
-    case 3: return launch_zy_t<T, 32, 64, 8, 8>(ctx, in, out, dims, tz, loz, lz, ty, loy, ly);
-    default: return launch_zy_t<T, 64, 64, 8, 16>(ctx, in, out, dims, tz, loz, lz, ty, loy, ly);
-  }
-}
 
 // General (non-separable) kernel: out[x] = sum_o K(o) in[x + sgn*o] over the
 // non-zero offset box [lo, hi]^3; sgn = -1 convolution, +1 correlation.
@@ -834,27 +480,6 @@ int launch_strided(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int a
   return SFW3D_OK;
 }
 
-template <typename T, int J, int kTInner, int NT>
-int launch_tiled(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis, const T* taps,
-                 int lo, int ntaps, const T* addend, double aw, double w) {
-  constexpr int kTGroups = NT / kTInner;
-  long long stride = 1;
-  for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
-  long long outer = 1;
-  for (int a = 0; a < axis; ++a) outer *= dims[a];
-  const int n = dims[axis];
-  constexpr int To = J * kTGroups;
-  const int npad = (ntaps + J - 1) / J * J;
-  const size_t smem = (size_t(npad) + size_t(To + npad) * kTInner) * sizeof(T);
-  if (smem > 48 * 1024)
-    SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_tiled_kernel<T, J, kTInner, NT>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  dim3 grid(unsigned((n + To - 1) / To), unsigned(stride / kTInner), unsigned(outer));
-  pass_tiled_kernel<T, J, kTInner, NT><<<grid, NT, smem, ctx->stream>>>(
-      in, out, n, stride, taps, lo, ntaps, addend, T(aw), T(w));
-  SFW3D_LAUNCH_CHECK(ctx);
-  return SFW3D_OK;
-}
 
 template <typename T, int J>
 int launch_z(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* taps, int lo,
@@ -896,30 +521,6 @@ int launch_tile2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axi
   return SFW3D_OK;
 }
 
-template <typename T, int J, int MINB>
-int launch_tile2p(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis, const T* taps,
-                  int lo, int ntaps) {
-  constexpr int TI = 64, NT = 256, To = J * (NT / TI);
-  long long stride = 1;
-  for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
-  long long outer = 1;
-  for (int a = 0; a < axis; ++a) outer *= dims[a];
-  const int n = dims[axis];
-  const int nt4 = (ntaps + 3) & ~3;
-  const size_t smem = (size_t(nt4) + 2 * size_t(To + nt4) * TI) * sizeof(T);
-  SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_tile2p_kernel<T, J, TI, NT, MINB>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  int per_sm = 0;
-  SFW3D_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &per_sm, pass_tile2p_kernel<T, J, TI, NT, MINB>, NT, smem));
-  const int tiles_x = (n + To - 1) / To, tiles_y = int(stride / TI);
-  const long long ntiles = (long long)tiles_x * tiles_y * outer;
-  const long long grid = std::min<long long>(ntiles, (long long)std::max(per_sm, 1) * ctx->num_sms);
-  pass_tile2p_kernel<T, J, TI, NT, MINB><<<unsigned(grid), NT, smem, ctx->stream>>>(
-      in, out, n, stride, taps, lo, ntaps, tiles_x, tiles_y, ntiles);
-  SFW3D_LAUNCH_CHECK(ctx);
-  return SFW3D_OK;
-}
 
 template <typename T, int J, int MINB = 1>
 int launch_z2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* taps, int lo,
@@ -940,41 +541,19 @@ int launch_z2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* t
     SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_z2_kernel<T, J, MINB>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   dim3 grid(unsigned((dims[2] + 4 * J - 1) / (4 * J)), unsigned((nrows + 31) / 32));
-  static const int zt = [] {  // bit 0: J = 16, bit 1: J = 32 (measured both faster)
-    const char* e = getenv("SFW3D_Z2T");
-    return e ? atoi(e) : 3;
-  }();
   pass_z2_kernel<T, J, MINB><<<grid, 128, smem, ctx->stream>>>(in, out, dims[2], nrows, taps, lo, ntaps,
-                                                         pitch, addend, T(aw), T(w), zt);
+                                                         pitch, addend, T(aw), T(w));
   SFW3D_LAUNCH_CHECK(ctx);
   return SFW3D_OK;
 }
 
-// resident-CTA targets of the J = 32 v2 tiles: 3 strided (80 registers),
-// 5 contiguous (96 registers) — measured 29.1 -> 27.7 ms over the config-4
-// basis passes; SFW3D_PASS_OCC="1,1" restores the unconstrained allocation.
-// (A persistent NS-stage cp.async ring and a warp-specialised bulk-copy
-// producer were both measured slower than these one-shot tiles here.)
-static int pass_occ(int which) {
-  static const int v[2] = {[] {
-    const char* e = getenv("SFW3D_PASS_OCC");
-    return e ? atoi(e) : 3;
-  }(), [] {
-    const char* e = getenv("SFW3D_PASS_OCC");
-    const char* c = e ? strchr(e, ',') : nullptr;
-    return c ? atoi(c + 1) : 5;
-  }()};
-  return v[which];
-}
-
-// taps at or below which a pass takes the J = 16 tile (SFW3D_NARROW_TAPS)
-static int narrow_taps() {
-  static const int v = [] {
-    const char* e = getenv("SFW3D_NARROW_TAPS");
-    return e ? atoi(e) : 24;
-  }();
-  return v;
-}
+// Tile choice. Wide filters (> kNarrowTaps taps) take J = 32 outputs per
+// thread; fp32 wide tiles are register-capped for 3 (strided) / 5
+// (contiguous) resident CTAs per SM (measured 29.1 -> 27.7 ms over the
+// config-4 basis passes). fp64 keeps the unconstrained allocation: with
+// twice the registers per value the capped tiles spill (round-1 ptxas log).
+// Narrow filters are HBM-bound: the J = 16 tile keeps more CTAs resident.
+constexpr int kNarrowTaps = 24;
 
 template <typename T>
 int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis, const T* taps,
@@ -983,20 +562,14 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
     set_error("1-D pass with more than 4096 taps");
     return SFW3D_EINVAL;
   }
-  const bool wide = ntaps > 24;
-  // kernel generation (SFW3D_PASS_VARIANT, for tuning; default 0 = v2)
-  static const int variant = [] {
-    const char* e = getenv("SFW3D_PASS_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
-  const int v2 = variant;
+  constexpr bool f32 = sizeof(T) == 4;
+  const bool wide = ntaps > kNarrowTaps;
   if (axis == 2) {
-    if (v2 == 0 && dims[2] % 4 == 0 && ntaps <= 1024) {
-      // narrow filters are HBM-bound: the smaller tile keeps more CTAs resident
-      if (dims[2] >= 128 && ntaps > narrow_taps())
-        return pass_occ(1) == 5
-                   ? launch_z2<T, 32, 5>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w)
-                   : launch_z2<T, 32>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
+    if (dims[2] % 4 == 0 && ntaps <= 1024) {
+      if (dims[2] >= 128 && wide) {
+        if constexpr (f32) return launch_z2<T, 32, 5>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
+        else return launch_z2<T, 32, 1>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
+      }
       return launch_z2<T, 16>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
     }
     return wide ? launch_z<T, 32>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w)
@@ -1004,55 +577,12 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
   }
   long long stride = 1;
   for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
-  {
-    static const int tp = [] {  // persistent double-buffered strided passes (opt-in):
-      const char* e = getenv("SFW3D_TILE2P");  // bit 0: narrow (J = 16), bit 1: wide (J = 32)
-      return e ? atoi(e) : 0;
-    }();
-    if (tp && sizeof(T) == 4 && v2 == 0 && stride % 64 == 0 && ntaps <= 512 && !addend && aw == 0.0 && w == 1.0 &&
-        dims[axis] >= 128) {
-      if (ntaps > narrow_taps()) {
-        if (tp & 2) return launch_tile2p<T, 32, 2>(ctx, in, out, dims, axis, taps, lo, ntaps);
-      } else if (tp & 1) {
-        return launch_tile2p<T, 16, 3>(ctx, in, out, dims, axis, taps, lo, ntaps);
-      }
+  if (stride % 64 == 0 && ntaps <= 512) {
+    if (dims[axis] >= 128 && wide) {
+      if constexpr (f32) return launch_tile2<T, 32, 3>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
+      else return launch_tile2<T, 32, 1>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
     }
-  }
-  if (v2 == 0 && stride % 64 == 0 && ntaps <= 512) {
-    static const int nt128 = [] {
-      const char* e = getenv("SFW3D_TILE2_NT");
-      return e ? atoi(e) == 128 : 0;
-    }();
-    if (nt128 && dims[axis] >= 128 && ntaps > narrow_taps())
-      return launch_tile2<T, 32, 5, 128>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
-    if (dims[axis] >= 128 && ntaps > narrow_taps())
-      return pass_occ(0) == 3
-                 ? launch_tile2<T, 32, 3>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w)
-                 : launch_tile2<T, 32>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
     return launch_tile2<T, 16>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
-  }
-  if (ntaps <= 512) {
-    switch (v2) {
-      case 1:
-        if (stride % 128 == 0)
-          return launch_tiled<T, 16, 128, 512>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
-        break;
-      case 2:
-        if (stride % 256 == 0)
-          return launch_tiled<T, 16, 256, 256>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
-        break;
-      case 3:
-        if (stride % 64 == 0)
-          return launch_tiled<T, 32, 64, 256>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
-        break;
-      case 4:
-        if (stride % 128 == 0)
-          return launch_tiled<T, 32, 128, 256>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
-        break;
-      default:  // (variant 5: v1 default)
-        if (stride % 64 == 0)
-          return launch_tiled<T, 16, 64, 256>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
-    }
   }
   return wide ? launch_strided<T, 32>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w)
               : launch_strided<T, 8>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
@@ -1073,28 +603,6 @@ int corr_pass_impl(sfw3d_ctx* ctx, int dtype, const void* in, void* out, const i
                            static_cast<const float*>(addend), addend_w, w);
 }
 
-// fused z + y passes (pass_zy_kernel) where the factors are narrow enough:
-// taps <= 36 on both axes, nz % 4 == 0. Opt-in (SFW3D_ZY=1): measured at
-// 512^3 with 15 taps it is instruction-bound (0.54 ms vs 0.52 ms for the two
-// separate passes), see DESIGN.md.
-bool zy_ok(const int dims[3], int ly, int lz) {
-  const char* e = getenv("SFW3D_ZY");  // (read per call: tests toggle it)
-  const int on = e ? atoi(e) : 0;
-  return on && dims[2] % 4 == 0 && dims[2] >= 64 && dims[1] >= 16 && ly <= 36 && lz <= 36;
-}
-
-int corr_pass_zy(sfw3d_ctx* ctx, int dtype, const void* in, void* out, const int dims[3],
-                 const void* tz, int loz, int lz, const void* ty, int loy, int ly,
-                 const char* family) {
-  SFW3D_PROF(ctx, family);
-  if (dtype == SFW3D_F64)
-    return launch_zy<double>(ctx, static_cast<const double*>(in), static_cast<double*>(out), dims,
-                             static_cast<const double*>(tz), loz, lz,
-                             static_cast<const double*>(ty), loy, ly);
-  return launch_zy<float>(ctx, static_cast<const float*>(in), static_cast<float*>(out), dims,
-                          static_cast<const float*>(tz), loz, lz, static_cast<const float*>(ty),
-                          loy, ly);
-}
 
 int psf_apply_impl(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* in, void* out,
                    int adjoint, void* tmp) {
@@ -1113,15 +621,10 @@ int psf_apply_impl(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* 
       else
         tp[a] = adjoint ? psf->taps32[a] : psf->taps32[a] + nt[a];
     }
-    if (zy_ok(dims, nt[1], nt[2]) && in != tmp) {
-      SFW3D_TRY(corr_pass_zy(ctx, dtype, in, tmp, dims, tp[2], lo[2], nt[2], tp[1], lo[1], nt[1],
-                             "psf_pass"));
-    } else {
-      SFW3D_TRY(corr_pass_impl(ctx, dtype, in, out, dims, 2, tp[2], lo[2], nt[2], nullptr, 0.0,
-                               1.0, "psf_pass"));
-      SFW3D_TRY(corr_pass_impl(ctx, dtype, out, tmp, dims, 1, tp[1], lo[1], nt[1], nullptr, 0.0,
-                               1.0, "psf_pass"));
-    }
+    SFW3D_TRY(corr_pass_impl(ctx, dtype, in, out, dims, 2, tp[2], lo[2], nt[2], nullptr, 0.0,
+                             1.0, "psf_pass"));
+    SFW3D_TRY(corr_pass_impl(ctx, dtype, out, tmp, dims, 1, tp[1], lo[1], nt[1], nullptr, 0.0,
+                             1.0, "psf_pass"));
     SFW3D_TRY(corr_pass_impl(ctx, dtype, tmp, out, dims, 0, tp[0], lo[0], nt[0], nullptr, 0.0, 1.0,
                              "psf_pass"));
     return SFW3D_OK;

@@ -245,6 +245,8 @@ class SlabCostGrad:
         import ctypes as C
         from . import _native as N
         from .forward import code_of
+        if tuple(y_win.shape) != tuple(self.local_dims):
+            raise ValueError(f"y window shape {tuple(y_win.shape)} != {tuple(self.local_dims)}")
         rows = np.ascontiguousarray(rows, dtype=np.float64).reshape(-1, 6)
         k = rows.shape[0]
         dev = y_win.device.index
@@ -311,12 +313,11 @@ class SlabCertificate:
     window restricted to its slab, and the only collective is the all-gather
     of 24-byte argmax records (combine_best: the reference's order). The
     redundant work is the 2 halo planes per slab plane count. The basis is
-    pruned by the GLOBAL volume's rule (SFW3D_BASIS_PRUNE is set for the
-    process) so every rank fits the same shared terms as one GPU would."""
+    pruned by the GLOBAL volume's rule (table option global_voxels) so every
+    rank fits the same shared terms as one GPU would."""
 
     def __init__(self, psf, sigma_grid, shape_grid, dims, x0: int, x1: int, halo: int | None = None,
                  **table_kw):
-        import os
         import torch
         from .certificate import build_template_table
         from .forward import Psf, support_radius
@@ -329,9 +330,7 @@ class SlabCertificate:
         self.local_dims = (self.x1 - self.x0 + 1 + 2 * self.halo, self.dims[1], self.dims[2])
         if 2 * rmax + 1 >= n or 2 * rmax + 1 >= self.local_dims[0]:
             raise ValueError("candidate boxes span the x axis: slabs cannot shard this table")
-        from . import _native as N
-        big = (1 << 24) if N.dtype_code() == N.F32 else (1 << 26)  # basis_prune_rule (basis.cuh)
-        os.environ["SFW3D_BASIS_PRUNE"] = "1" if int(np.prod(self.dims)) >= big else "0"
+        table_kw.setdefault("global_voxels", int(np.prod(self.dims)))
         self.psf = Psf(Volume(local_psf_kernel(psf.kernel.data, self.local_dims)), normalize=False)
         self.table = build_template_table(self.psf, sigma_grid, shape_grid, **table_kw)
         self.index = torch.arange(self.x0 - self.halo, self.x1 + self.halo + 1) % n

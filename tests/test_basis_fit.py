@@ -74,7 +74,7 @@ def common_box(dims, sigmas, shapes):
     ("cfg2", (128,) * 3, list(np.geomspace(1, 3, 6)), list(np.linspace(1.2, 2.8, 5))),
     ("cfg3", (256,) * 3, list(np.geomspace(1, 3, 8)), list(np.linspace(1.5, 2.5, 6))),
 ])
-def test_shared_basis_set(name, dims, sigmas, shapes, monkeypatch):
+def test_shared_basis_set(name, dims, sigmas, shapes):
     """The table's shared dictionary fit (f32 storage, basis_tol 1e-9): every
     member's mixture reproduces its profile on the COMMON box lattice within
     the reported error (which includes the 1e-12 factor truncation), members
@@ -82,8 +82,7 @@ def test_shared_basis_set(name, dims, sigmas, shapes, monkeypatch):
     exact term of weight 1 and d > 2 candidates are never non-negative
     members (they join as signed members, test_signed_members)."""
     tol = 1e-9
-    monkeypatch.setenv("SFW3D_BASIS_LOOSE", "0")  # terms selected at tol itself
-    r = N.basis_set_fit(dims, sigmas, shapes, 0, tol)
+    r = N.basis_set_fit(dims, sigmas, shapes, 0, tol, loose_tol=0.0)  # terms selected at tol
     lo, hi = common_box(dims, sigmas, shapes)
     s = lattice(lo, hi).astype(float)
     E = np.exp(-np.outer(s, r["betas"]))
@@ -117,15 +116,13 @@ def test_shared_basis_set(name, dims, sigmas, shapes, monkeypatch):
     ("cfg1", (64,) * 3, [1.5, 2.0, 2.5, 3.0], [1.5, 2.0, 2.5]),
     ("cfg4", (512,) * 3, [1.0, 1.5, 2.0, 3.0], [1.5, 2.0, 2.5, 3.0]),
 ])
-def test_loose_basis_demotes_to_signed(name, dims, sigmas, shapes, monkeypatch):
-    """fp32 tables select their shared terms at the looser SFW3D_BASIS_LOOSE
-    (default 1.5e-6): no more terms than the tight selection, every d == 2
+def test_loose_basis_demotes_to_signed(name, dims, sigmas, shapes):
+    """fp32 tables select their shared terms at the looser loose_tol
+    (default 1e-5): no more terms than the tight selection, every d == 2
     candidate stays an exact single-term member, and every other candidate
     that was a tight non-negative member is now a SIGNED member (certified
     bound, exact refinement of its maxima) rather than dropped."""
-    monkeypatch.setenv("SFW3D_BASIS_LOOSE", "0")
-    tight = N.basis_set_fit(dims, sigmas, shapes, 0, 1e-9)
-    monkeypatch.delenv("SFW3D_BASIS_LOOSE")
+    tight = N.basis_set_fit(dims, sigmas, shapes, 0, 1e-9, loose_tol=0.0)
     loose = N.basis_set_fit(dims, sigmas, shapes, 0, 1e-9)
     assert len(loose["betas"]) <= len(tight["betas"])
     for c, (sg, d) in enumerate([(a, b) for a in sigmas for b in shapes]):

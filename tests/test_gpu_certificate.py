@@ -164,7 +164,7 @@ def test_eta_f64_refined_maxima(P):
 
 @pytest.mark.parametrize("prec,tol,cap", [("f32", 1e-5, None), ("f64", 1e-10, None),
                                           ("f32", 1e-5, "6")])
-def test_signed_members_refined_maxima(P, prec, tol, cap, monkeypatch):
+def test_signed_members_refined_maxima(P, prec, tol, cap):
     """d > 2 candidates on the shared basis with signed weights: an argmax-only
     evaluation refines every voxel within 2 E_c of each member's approximate
     maximum exactly, so each candidate's maximum and position equal the FFT
@@ -173,8 +173,6 @@ def test_signed_members_refined_maxima(P, prec, tol, cap, monkeypatch):
     members with the most near-maximal voxels fall back to the direct
     kernels and the rest are still refined."""
     import torch
-    if cap:
-        monkeypatch.setenv("SFW3D_REFINE_CAP", cap)
     from paper_2009_05473_b200 import _native as N
     dims, kernel, r = cfg4_like(72, seed=11)
     sg, dg = np.array([1.0, 1.5, 2.0, 3.0]), np.array([1.5, 2.0, 2.5, 3.0])
@@ -183,7 +181,8 @@ def test_signed_members_refined_maxima(P, prec, tol, cap, monkeypatch):
     _, _, val, per, _ = O.eta_field(r, 0.9, hats, len(dg), win)
     psf = P.Psf(P.Volume(kernel), normalize=False)
     with P.precision(prec):
-        table = P.build_template_table(psf, sg, dg, tap_tol=1e-12)
+        table = P.build_template_table(psf, sg, dg, tap_tol=1e-12,
+                                       refine_cap=int(cap) if cap else None)
         paths = [c["path"] for c in table.info()["candidates"]]
         assert all(p == "basis+refine" for p, (s, d) in zip(paths, [(a, b) for a in sg for b in dg])
                    if d > 2.0)
@@ -201,38 +200,9 @@ def test_signed_members_refined_maxima(P, prec, tol, cap, monkeypatch):
         assert tuple(rec.pos) == tuple(pos), (c, tuple(rec.pos), pos)
 
 
-@pytest.mark.parametrize("dims", [(70, 24, 40), (33, 20, 16), (64, 30, 30)])
-def test_eta_f32_fused_xmix_matches_separate_passes(P, dims, monkeypatch):
-    """The fused x pass + member mix (xmix_kernel, fp32, inner plane a multiple
-    of 32) and the separate x pass + mix kernel run the same FMA chains: the
-    fields agree to fp32 rounding of the final division and the per-candidate
-    maxima are identical; (64, 30, 30) takes the unfused path in both runs."""
-    import torch
-    rng = np.random.default_rng(21)
-    r = rng.standard_normal(dims)
-    kernel = O.box_gaussian_psf(dims, (1.5, 1.5, 1.5), (4, 4, 4))
-    psf = P.Psf(P.Volume(kernel), normalize=False)
-    sg, dg = np.array([1.0, 1.8, 2.6]), np.array([1.5, 2.0, 2.5])
-    win = ((2, dims[0] - 3), (1, dims[1] - 2), (0, dims[2] - 1))
-    out = {}
-    with P.precision("f32"):
-        table = P.build_template_table(psf, sg, dg, tap_tol=1e-12)
-        rd = torch.tensor(r, device="cuda", dtype=torch.float32)
-        for flag in ("1", "0"):  # fused (opt-in) vs separate
-            monkeypatch.setenv("SFW3D_XMIX", flag)
-            best, recs, _ = P.certificate.eta_argmax_dev(rd, 0.7, table, win)
-            f = P.eta_field(P.Volume(r), 0.7, table, keep_fields=True)
-            out[flag] = (best, recs, np.stack([v.data for v in f.fields]))
-    (b1, r1, f1), (b0, r0, f0) = out["1"], out["0"]
-    assert np.max(np.abs(f1 - f0)) <= 1e-6 * np.max(np.abs(f0))
-    assert b1.value == b0.value and tuple(b1.pos) == tuple(b0.pos)
-    for a, c in zip(r1, r0):
-        assert abs(a.value - c.value) <= 1e-6 * abs(b0.value) and tuple(a.pos) == tuple(c.pos)
-
-
 @pytest.mark.parametrize("nranks", [2, 3])
 @pytest.mark.parametrize("prec", ["f32", "f64"])
-def test_slab_certificate_matches_global(P, nranks, prec, monkeypatch):
+def test_slab_certificate_matches_global(P, nranks, prec):
     """Multi-GPU certificate layout (distributed.SlabCertificate), ranks run
     one after another on this GPU: each rank evaluates its x-slab on its own
     sub-volume (slab + halo planes of the periodic residual) and the records
@@ -241,7 +211,6 @@ def test_slab_certificate_matches_global(P, nranks, prec, monkeypatch):
     arithmetic), and the winner matches the FFT oracle."""
     import torch
     from paper_2009_05473_b200 import distributed as D
-    monkeypatch.setenv("SFW3D_BASIS_PRUNE", "0")  # (restored after the test)
     dims = (96, 48, 64)
     rng = np.random.default_rng(5)
     kernel = O.box_gaussian_psf(dims, (1.5, 1.5, 1.5), (3, 3, 3))

@@ -1,9 +1,9 @@
 """GPU tests of the separable 1-D pass kernels (K4) across tile geometries:
-the persistent bulk-copy pipelines (v3: partial row / column tiles, periodic
-wrap inside a staged row, axes shorter than a tile, wide and narrow filters,
-odd offsets) and the v2 fallbacks (short axes, rows wider than the axis),
-and the fused in-plane z+y pass (narrow factors), checked against the
-oracle's FFT circular convolution / correlation.
+the staged register-window tiles (pass_z2 contiguous, pass_tile2 strided:
+partial row / column tiles, periodic wrap inside a staged row, wide and
+narrow filters, odd offsets) and the fallbacks (short axes, rows wider than
+the axis, z extents not a multiple of 4), checked against the oracle's FFT
+circular convolution / correlation.
 
 Bars: fp64 1e-12 of max|ref|; fp32 storage 2e-6 of max|ref| (fp32 FMA
 chains of <= 89 taps)."""
@@ -26,21 +26,21 @@ def P():
 
 
 GEOMS = [
-    ((128, 128, 128), (2.0, 2.0, 2.0), (7, 7, 7)),      # v3 everywhere, full tiles
+    ((128, 128, 128), (2.0, 2.0, 2.0), (7, 7, 7)),      # staged tiles everywhere, full tiles
     ((97, 65, 192), (3.0, 1.0, 4.0), (15, 3, 15)),      # partial row / column tiles, To > n
     ((96, 192, 256), (9.0, 9.0, 9.0), (30, 44, 44)),    # 61- and 89-tap filters
-    ((130, 64, 132), (0.5, 2.0, 0.7), (1, 9, 2)),       # z row wider than the axis: v2
-    ((48, 40, 36), (1.5, 1.5, 2.0), (3, 3, 4)),         # short axes: v2 everywhere
-    ((40, 40, 64), (1.0, 4.0, 5.0), (3, 15, 17)),       # fused z+y: z taps wrap the axis
-    ((24, 72, 200), (1.0, 3.0, 2.0), (2, 17, 6)),       # fused z+y: partial y and z tiles
+    ((130, 64, 132), (0.5, 2.0, 0.7), (1, 9, 2)),       # z row wider than the axis
+    ((48, 40, 36), (1.5, 1.5, 2.0), (3, 3, 4)),         # short axes
+    ((40, 40, 64), (1.0, 4.0, 5.0), (3, 15, 17)),       # z taps wrap the axis
+    ((24, 72, 200), (1.0, 3.0, 2.0), (2, 17, 6)),       # partial y and z tiles
+    ((20, 18, 30), (1.0, 1.0, 1.0), (3, 3, 3)),         # nz % 4 != 0, stride % 64 != 0
+    ((256, 16, 64), (6.0, 1.0, 1.0), (25, 3, 3)),       # wide fp32/fp64 strided tiles
 ]
 
 
 @pytest.mark.parametrize("dims,sig,half", GEOMS)
 @pytest.mark.parametrize("prec", ["f32", "f64"])
-@pytest.mark.parametrize("zy", ["0", "1"])
-def test_psf_passes_vs_fft(P, dims, sig, half, prec, zy, monkeypatch):
-    monkeypatch.setenv("SFW3D_ZY", zy)  # fused z+y pass off / on where eligible
+def test_psf_passes_vs_fft(P, dims, sig, half, prec):
     rng = np.random.default_rng(sum(dims))
     kernel = O.box_gaussian_psf(dims, sig, half)
     x = rng.standard_normal(dims)
