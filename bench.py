@@ -129,77 +129,88 @@ def peaks():
 
 
 # ------------------------------------------------------ CPU oracle timing
-def oracle_cert_sample(residual: np.ndarray, kernel: np.ndarray, cands, threads: int, reps: int,
-                       warm: int):
+def oracle_threads(dims, n_cand: int) -> int:
+    """Host threads for the FFT oracle: every core, bounded by memory (per
+    worker: the product spectrum + one field; plus all template spectra)."""
+    import psutil
+    nproc = os.cpu_count() or 1
+    vol = 8 * int(np.prod(dims))
+    avail = psutil.virtual_memory().available - (n_cand + 4) * vol
+    return max(1, min(nproc, n_cand, int(avail // (2.5 * vol))))
+
+
+def oracle_cert(residual: np.ndarray, kernel: np.ndarray, sigma_grid, shape_grid, threads: int,
+                reps: int, warm: int):
     """The reference's FFT eta_field (certificate.py:156-172) restated by the
-    oracle, over `len(cands)` candidates mapped on `threads` host threads.
-    Returns (seconds per step list, voxel-candidates per step)."""
+    oracle: template spectra built once (untimed, as build_template_table),
+    then per step rfftn(r) + one irfftn + argmax per candidate, candidates
+    mapped on `threads` host threads (the reference's map_ordered). Returns
+    (seconds per step, per-candidate [(position, eta)] in sigma-major order,
+    voxel-candidates per step)."""
     from concurrent.futures import ThreadPoolExecutor
     import scipy.fft as sfft
     sys.path.insert(0, str(ROOT / "oracle"))
     import sfw3d_oracle as O
     dims = residual.shape
+    r64 = np.asarray(residual, dtype=np.float64)
     khat = O.psf_hat(kernel)
-    hats = [O.template_hats(khat, dims, [s], [d])[0] for s, d in cands]
-
-    def one(h, rhat):
-        vals = sfft.irfftn(rhat * np.conj(h), s=dims)
-        i = int(np.argmax(vals))
-        return float(vals.flat[i]), i
-
-    times = []
+    cands = [(s, d) for s in np.sort(sigma_grid) for d in np.sort(shape_grid)]
     with ThreadPoolExecutor(max_workers=threads) as pool:
+        hats = list(pool.map(lambda c: O.template_hats(khat, dims, [c[0]], [c[1]])[0], cands))
+
+        def one(h, rhat):
+            vals = sfft.irfftn(rhat * np.conj(h), s=dims)
+            i = int(np.argmax(vals))  # first C-order maximum (certificate.py:161-163)
+            return tuple(int(q) for q in np.unravel_index(i, dims)), float(vals.flat[i])
+
+        times, per = [], None
         for it in range(warm + reps):
             t0 = time.perf_counter()
-            rhat = sfft.rfftn(residual)
-            res = list(pool.map(lambda h: one(h, rhat), hats))
-            _ = max(res)
+            rhat = sfft.rfftn(r64)
+            per = list(pool.map(lambda h: one(h, rhat), hats))
             if it >= warm:
                 times.append(time.perf_counter() - t0)
-    return times, int(np.prod(dims)) * len(cands)
+    return times, per, int(np.prod(dims)) * len(cands)
 
 
-def host_residual_cfg4(inst):
-    """Host (numpy) copy of the cfg-4 residual for the CPU arms."""
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import sfw3d_oracle as O
-    rng = np.random.default_rng(4)
-    r = rng.standard_normal(inst.dims)
-    r += O.conv(O.render(inst.truth, inst.dims), O.psf_hat(inst.kernel))
-    return r.astype(np.float32).astype(np.float64)
+def oracle_winner(per):
+    """Global best by strict '>' over sigma-major candidates (certificate.py:168-172)."""
+    best = 0
+    for c, (_, v) in enumerate(per):
+        if v > per[best][1]:
+            best = c
+    return best, per[best][0], per[best][1]
 
 
 def reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    import psutil
     from paper_2009_05473_b200 import configs
     inst = configs.config4(n=args.n)
-    residual = host_residual_cfg4(inst)
-    cands = [(s, d) for s in inst.sigma_grid for d in inst.shape_grid]
-    nproc = os.cpu_count() or 1
-    per_thread = 4.5 * residual.nbytes  # hat + product + field + slack
-    avail = psutil.virtual_memory().available - 3 * residual.nbytes
-    threads = max(1, min(nproc, len(cands), int(avail // per_thread)))
-    sample = cands[-threads:]
-    times, vc = oracle_cert_sample(residual, inst.kernel, sample, threads, args.steps,
-                                   max(0, min(args.warmup, 1)))
+    residual = configs.cfg4_residual_host(inst)
+    n_cand = len(inst.sigma_grid) * len(inst.shape_grid)
+    threads = oracle_threads(inst.dims, n_cand)
+    times, per, vc = oracle_cert(residual, inst.kernel, inst.sigma_grid, inst.shape_grid, threads,
+                                 args.steps, max(0, min(args.warmup, 1)))
     t = statistics.median(times)
     value = vc / t
+    c, pos, v = oracle_winner(per)
     line = {
         "impl": "reference", "metric": "certificate voxel-candidates/s", "value": value,
         "unit": "voxel-candidates/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"cfg4 certificate {args.n}^3 x {len(sample)} of 16 candidates "
-                               "(FFT eta_field, oracle port of sfw3d certificate.py:140-184)"},
+        "config": {"workload": f"cfg4 certificate {args.n}^3 x {n_cand} candidates (FFT "
+                               "eta_field, oracle port of sfw3d certificate.py:140-184) on the "
+                               "host residual configs.cfg4_residual_host (same array as the GPU arm)"},
         "cpu_baseline": {"value": value, "unit": "voxel-candidates/s", "cores": threads,
                          "kind": "port",
-                         "sample": f"{len(sample)} candidates x {args.n}^3 per step "
-                                   f"(threads over candidates, median of {len(times)})"},
+                         "sample": f"all {n_cand} candidates x {args.n}^3 per step (threads over "
+                                   f"candidates, median of {len(times)}; template spectra untimed)"},
         "e2e": {"value": value, "unit": "voxel-candidates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "argmax": {"eta": v, "cand": c, "pos": list(pos)},
     }
     print(json.dumps(line), flush=True)
 
@@ -219,10 +230,8 @@ def cert_workload(args, rank, world, dev):
     table = P.build_template_table(psf, inst.sigma_grid, inst.shape_grid, tap_tol=args.tap_tol,
                                    mode=args.mode)
     info = table.info()
-    g = torch.Generator(device=dev)
-    g.manual_seed(4)
-    residual = torch.randn(dims, generator=g, device=dev, dtype=torch.float32)
-    residual += psf_apply_dev(psf, render_dev(inst.truth, dims, N.F32), False)
+    host_residual = configs.cfg4_residual_host(inst)  # the array the CPU arms also use
+    residual = torch.from_numpy(host_residual).to(dev)
     n = dims[0]
     ctx = N.context(dev)
     stream = torch.cuda.current_stream(dev)
@@ -249,6 +258,7 @@ def cert_workload(args, rank, world, dev):
 
     for _ in range(args.warmup):
         step()
+    _, per_cand, _ = eta_argmax_dev(work, 1.0, table, window)
     if collective(world):
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
@@ -403,8 +413,11 @@ def cert_workload(args, rank, world, dev):
     out = {
         "value": value, "ms_per_step": ms_step, "launches": launches, "clocks": clk,
         "roofline": roof, "e2e": e2e, "kernel_ms": {k: v[0] for k, v in fam.items() if v[1]},
-        "table": info, "best": {"eta": gbest[0], "cand": int(gbest[1]), "lin": int(gbest[2])},
-        "halo": slab.halo if world > 1 else 0,
+        "table": info, "best": {"eta": gbest[0], "cand": int(gbest[1]), "lin": int(gbest[2]),
+                                "pos": [int(q) for q in np.unravel_index(int(gbest[2]), dims)]},
+        "halo": slab.halo if world > 1 else 0, "host_residual": host_residual,
+        "per_cand": [(tuple(int(q) for q in r.pos), float(r.value)) for r in per_cand]
+        if world == 1 else None,
         "refined_voxels": refine_count,
         "inst": inst, "dims": dims,
     }
@@ -562,15 +575,32 @@ def main():
         secondary.append(costgrad_workload(args, dev))
         secondary.append(solve_workload(dev))
         secondary.append(solve_cfg3_workload())
-    cpu = None
+    cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # the reference algorithm (oracle FFT eta_field) on the SAME host
+        # residual, every candidate: the CPU baseline and the parity check of
+        # the headline step
         inst = res["inst"]
-        residual = host_residual_cfg4(inst)
-        cands = [(inst.sigma_grid[-1], inst.shape_grid[0])]
-        times, vc = oracle_cert_sample(residual, inst.kernel, cands, 1, 1, 0)
-        cpu = {"value": vc / times[0], "unit": "voxel-candidates/s", "cores": 1, "kind": "port",
-               "sample": f"1 candidate (sigma=3, d=1.5) x {args.n}^3: rfftn + irfftn + argmax, "
-                         "scipy.fft single thread (the reference never threads its FFTs)"}
+        n_cand = res["table"]["n_cand"]
+        threads = oracle_threads(inst.dims, n_cand)
+        times, per, vc = oracle_cert(res["host_residual"], inst.kernel, inst.sigma_grid,
+                                     inst.shape_grid, threads, 1, 0)
+        cpu = {"value": vc / times[0], "unit": "voxel-candidates/s", "cores": threads,
+               "kind": "port",
+               "sample": f"one full step: all {n_cand} candidates x {args.n}^3 (rfftn + "
+                         f"{n_cand} irfftn + argmax, candidates on {threads} threads; template "
+                         "spectra untimed) on the same host residual"}
+        c, pos, v = oracle_winner(per)
+        got = res["per_cand"]
+        errs = [abs(g[1] - o[1]) for g, o in zip(got, per)]
+        parity = {
+            "oracle": "FFT eta_field port (certificate.py:140-184), f64 on the fp32 residual",
+            "argmax_equal": bool(tuple(res["best"]["pos"]) == tuple(pos)
+                                 and res["best"]["cand"] == c),
+            "oracle_argmax": {"eta": v, "cand": c, "pos": list(pos)},
+            "max_rel_eta_err": max(errs) / abs(v),
+            "per_candidate_positions_equal": sum(int(g[0] == o[0]) for g, o in zip(got, per)),
+            "candidates": len(per), "bar": "1e-5 of eta_max (north_star)"}
     if rank == 0 or ONE_RANK:
         line = {
             "metric": "certificate voxel-candidates/s", "value": res["value"],
@@ -588,7 +618,8 @@ def main():
                        "l2": "inputs larger than L2 (512 MiB residual, 0.9 GiB padded copy)"},
             "gpu_launches": res["launches"], "clocks": res["clocks"], "roofline": res["roofline"],
             "cpu_baseline": cpu, "e2e": res["e2e"], "kernel_ms_per_step": res["kernel_ms"],
-            "table": res["table"], "argmax": res["best"], "refined_voxels": res["refined_voxels"],
+            "table": res["table"], "argmax": res["best"], "parity": parity,
+            "refined_voxels": res["refined_voxels"],
             "secondary": secondary,
         }
         if ONE_RANK:

@@ -241,6 +241,32 @@ def eta_field(residual, lam, hats, n_shape, window=None, keep_fields=False):
     return best[0], best[1], best[2], per, fields
 
 
+def eta_maxima(residual, lam, kernel_hat, sigma_grid, shape_grid, window=None, threads=1):
+    """certificate.py:140-172 per candidate, memory-bounded for large grids:
+    each worker builds one template spectrum (certificate.py:86-92), takes
+    irfftn(r_hat conj(T_hat)) / lam and its first C-order maximum in the
+    window. Returns [(position, eta)] in sigma-major order."""
+    from concurrent.futures import ThreadPoolExecutor
+    dims = residual.shape
+    if window is None:
+        window = position_window(dims)
+    reg = tuple(slice(a, b + 1) for a, b in window)
+    rhat = sfft.rfftn(np.asarray(residual, dtype=float))
+    cands = [(s, d) for s in np.sort(np.asarray(sigma_grid, dtype=float))
+             for d in np.sort(np.asarray(shape_grid, dtype=float))]
+
+    def one(c):
+        h = template_hats(kernel_hat, dims, [c[0]], [c[1]])[0]
+        vals = sfft.irfftn(rhat * np.conj(h), s=dims) / lam
+        loc = vals[reg]
+        p = np.unravel_index(int(np.argmax(loc)), loc.shape)
+        p = tuple(int(q + a) for q, (a, _) in zip(p, window))
+        return p, float(vals[p])
+
+    with ThreadPoolExecutor(max_workers=max(1, int(threads))) as pool:
+        return list(pool.map(one, cands))
+
+
 def eta_value_grad(back: np.ndarray, theta, lam: float):
     """certificate.py:201-209 (neg_eta, sign flipped): eta(theta) and its 5-gradient."""
     idx, val, grads = atom_profile(theta, back.shape, True)
@@ -248,6 +274,69 @@ def eta_value_grad(back: np.ndarray, theta, lam: float):
     v = float(np.vdot(val, sub).real) / lam
     g = np.array([float(np.vdot(q, sub).real) for q in grads]) / lam
     return v, g
+
+
+def clamp_theta(theta, box5):
+    """measures.py:160-168: project (m_x, m_y, m_z, sigma, d) onto the box."""
+    return np.array([min(max(float(x), lo), hi) for x, (lo, hi) in zip(theta, box5)])
+
+
+def refine_eta_max(back, lam, start, box5, max_iter=200, gtol=1e-8):
+    """certificate.py:187-224: L-BFGS-B ascent of eta from the grid seed with
+    the analytic 5-gradient; keeps the start if not improved. `back` =
+    H^T r; box5 = [(lo, hi)] for (m_x, m_y, m_z, sigma, d). Returns (theta, eta)."""
+    from scipy.optimize import minimize
+    start = clamp_theta(start, box5)
+
+    def neg_eta(vec):
+        v, g = eta_value_grad(back, vec, lam)
+        if not (np.isfinite(v) and np.isfinite(g).all()):
+            raise FloatingPointError("non-finite certificate value")
+        return -v, -g
+
+    start_val = -neg_eta(start)[0]
+    res = minimize(neg_eta, start, jac=True, method="L-BFGS-B", bounds=list(box5),
+                   options={"maxiter": max_iter, "gtol": gtol})
+    if not np.isfinite(res.fun):
+        raise FloatingPointError("certificate ascent diverged to a non-finite value")
+    if -res.fun < start_val:
+        return start, start_val
+    return clamp_theta(res.x, box5), float(-res.fun)
+
+
+def local_descent(y, rows, khat, lam, box5, gtol=1e-6, ftol=1e-10, max_iter=400):
+    """solvers.py:197-240: joint L-BFGS-B slide of all (w, m, sigma, d) rows
+    with w >= 0 (_unpack takes max(0, w)); keeps the start if not improved.
+    Returns ((k, 6) rows, criterion)."""
+    from scipy.optimize import minimize
+    p = np.asarray(rows, dtype=float).reshape(-1, 6).copy()
+    k = p.shape[0]
+    for i in range(k):
+        p[i, 1:] = clamp_theta(p[i, 1:], box5)
+
+    def unpack(x):
+        r = np.array(x, dtype=float).reshape(k, 6)
+        r[:, 0] = np.maximum(r[:, 0], 0.0)
+        return r
+
+    def fun(x):
+        value, g, _ = criterion_and_gradient(y, unpack(x), khat, lam)
+        return value, g.ravel()
+
+    box = []
+    for _ in range(k):
+        box.append((0.0, None))
+        box.extend(box5)
+    x0 = p.ravel()
+    f0 = fun(x0)[0]
+    res = minimize(fun, x0, jac=True, method="L-BFGS-B", bounds=box,
+                   options={"maxiter": max_iter, "gtol": gtol, "ftol": ftol})
+    if not np.isfinite(res.fun) or res.fun > f0:
+        return p, float(f0)
+    out = unpack(res.x)
+    for i in range(k):
+        out[i, 1:] = clamp_theta(out[i, 1:], box5)
+    return out, float(res.fun)
 
 
 # --------------------------------------------------------------------------

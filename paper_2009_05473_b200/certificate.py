@@ -292,6 +292,12 @@ def certificate_max(residual: Volume, lam: float, table: AtomTemplateTable, psf:
     return certificate_max_dev(to_dev(residual), lam, table, psf, bounds)
 
 
-def certificate_max_dev(residual, lam, table, psf, bounds):
+def certificate_max_dev(residual, lam, table, psf, bounds, info: dict | None = None):
+    """Grid argmax then refinement on a device residual; `info` (optional)
+    receives the grid seed ("start", "eta_grid") for step-level replays."""
     field = eta_field_dev(residual, lam, table, bounds, keep_fields=False)
+    if info is not None:
+        info["start"] = field.argmax_params
+        info["eta_grid"] = field.eta_max
+        info["cand"] = (field.argmax_sigma_index, field.argmax_shape_index)
     return refine_eta_max_dev(residual, lam, psf, field.argmax_params, bounds)

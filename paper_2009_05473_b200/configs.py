@@ -1,9 +1,10 @@
 """Seeded synthetic instances of the BASELINE.json configs.
 
 No public dataset is involved: every config is a recipe (atoms drawn from a
-seeded numpy Generator in the order positions, sigma, d, w; noise from a
-seeded torch generator on the device) rendered with this package's own
-forward operator. Shapes, sizes and value distributions follow
+seeded numpy Generator in the order positions, sigma, d, w) rendered with
+this package's own forward operator, except the config-4 residual, which is
+generated on the host (``cfg4_residual_host``) so that the GPU arm and the
+CPU reference arm of ``bench.py`` consume the identical array. Shapes, sizes and value distributions follow
 BASELINE.json `configs`; unspecified items use the SURVEY Appendix A
 choices, restated in each docstring.
 """
@@ -126,3 +127,37 @@ def perturbations(truth: np.ndarray, count: int, std: float = 0.1, seed: int = 1
         p[:, 5] = np.maximum(p[:, 5], 1.05)
         out.append(p)
     return out
+
+
+def _render_host(rows: np.ndarray, dims) -> np.ndarray:
+    """Host rendering of generalized Gaussians for synthetic DATA generation
+    (not a compute path): w exp(-|s - m|^d / (2 sigma^d)) on the periodic
+    box round(m) +- ceil(sigma (2 ln 1e12)^(1/d)) per axis (boxes < n)."""
+    out = np.zeros(tuple(dims))
+    for w, mx, my, mz, sg, d in np.asarray(rows, dtype=float).reshape(-1, 6):
+        r = int(np.ceil(sg * (2.0 * np.log(1e12)) ** (1.0 / d)))
+        idx, off = [], []
+        for m, n in zip((mx, my, mz), dims):
+            span = np.arange(int(np.round(m)) - r, int(np.round(m)) + r + 1)
+            idx.append(np.remainder(span, n))
+            off.append(span - m)
+        u2 = off[0][:, None, None] ** 2 + off[1][None, :, None] ** 2 + off[2][None, None, :] ** 2
+        out[np.ix_(*idx)] += w * np.exp(-0.5 * u2 ** (0.5 * d) / sg ** d)
+    return out
+
+
+def cfg4_residual_host(inst: Instance, seed: int = 4) -> np.ndarray:
+    """Config-4 residual as a host float32 array: N(0,1) i.i.d. noise (numpy
+    Generator(seed)) + the 200 generalized Gaussians blurred by the PSF
+    (circular, through scipy.fft). Both bench arms use this exact array."""
+    import os
+    import scipy.fft as sfft
+    dims = inst.dims
+    workers = os.cpu_count() or 1
+    atoms = _render_host(inst.truth, dims)
+    khat = sfft.rfftn(sfft.ifftshift(inst.kernel), workers=workers)
+    blurred = sfft.irfftn(sfft.rfftn(atoms, workers=workers) * khat, s=dims, workers=workers)
+    del atoms, khat
+    r = np.random.default_rng(seed).standard_normal(dims, dtype=np.float32)
+    r += blurred.astype(np.float32)
+    return r

@@ -438,11 +438,10 @@ struct RefCand {
   int lo_a, lo_b, cl, la, lb, lc4;
 };
 
-// sum |b| (fp64, one atomicAdd per block) and max |b| (bit pattern of a
-// non-negative double: integer order = value order) over the volume
+// sum |b| and max |b| over the volume: per-block partials (fp64), then
+// abs_parts_reduce_kernel adds them in block order (run-to-run identical)
 template <typename T>
-__global__ void abs_sum_kernel(const T* __restrict__ b, long long n, double* __restrict__ out,
-                               unsigned long long* __restrict__ amax) {
+__global__ void abs_sum_kernel(const T* __restrict__ b, long long n, double* __restrict__ parts) {
   __shared__ double red[8];
   __shared__ double redm[8];
   double sacc = 0.0, m = 0.0;
@@ -467,9 +466,21 @@ __global__ void abs_sum_kernel(const T* __restrict__ b, long long n, double* __r
       t += red[w];
       mm = fmax(mm, redm[w]);
     }
-    atomicAdd(out, t);
-    atomicMax(amax, static_cast<unsigned long long>(__double_as_longlong(mm)));
+    parts[2 * blockIdx.x] = t;
+    parts[2 * blockIdx.x + 1] = mm;
   }
+}
+
+__global__ void abs_parts_reduce_kernel(const double* __restrict__ parts, int nblocks,
+                                        double* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  double t = 0.0, m = 0.0;
+  for (int i = 0; i < nblocks; ++i) {
+    t += parts[2 * i];
+    m = fmax(m, parts[2 * i + 1]);
+  }
+  out[0] = t;
+  out[1] = m;
 }
 
 // gridDim.y CTAs per item (blockIdx.y = contiguous share of the template
@@ -1014,7 +1025,7 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   double* ref_val = any_refine ? cv.take<double>(kRefCap) : nullptr;
   double* ref_part = any_refine ? cv.take<double>(kRefPart) : nullptr;
   double* ref_thr = any_refine ? cv.take<double>(nc) : nullptr;
-  double* ref_l1 = any_refine ? cv.take<double>(2) : nullptr;  // [sum |b|, max |b| bits]
+  double* ref_l1 = any_refine ? cv.take<double>(2) : nullptr;  // [sum |b|, max |b|]
   int* ref_count = any_refine ? cv.take<int>(1 + nc) : nullptr;  // [total, per member]
   std::vector<Best> refined(nc, Best{NAN, -1});  // exact maxima of refined members
   void* accd_g = ab ? cv.take<char>(ab) : nullptr;
@@ -1061,9 +1072,10 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
     // The true maximum lies among the voxels with eta~ >= max eta~ - 2 E_c.
     SFW3D_PROF(ctx, "eta_refine");
     if (!abs_done) {  // (the mix computes them when it streams b: mix_ring2_kernel)
-      SFW3D_CUDA_TRY(cudaMemsetAsync(ref_l1, 0, 2 * sizeof(double), ctx->stream));
-      abs_sum_kernel<T><<<4 * ctx->num_sms, 256, 0, ctx->stream>>>(
-          b, n, ref_l1, reinterpret_cast<unsigned long long*>(ref_l1 + 1));
+      const int nab = std::min(4 * ctx->num_sms, kRefPart / 2);  // partials in ref_part
+      abs_sum_kernel<T><<<nab, 256, 0, ctx->stream>>>(b, n, ref_part);
+      SFW3D_LAUNCH_CHECK(ctx);
+      abs_parts_reduce_kernel<<<1, 32, 0, ctx->stream>>>(ref_part, nab, ref_l1);
       SFW3D_LAUNCH_CHECK(ctx);
     }
     std::vector<Best> hb0(nc);
