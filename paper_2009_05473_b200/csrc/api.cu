@@ -178,6 +178,8 @@ extern "C" int sfw3d_ctx_destroy(sfw3d_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   if (ctx->ws.ptr) cudaFree(ctx->ws.ptr);
   if (ctx->ws_small.ptr) cudaFree(ctx->ws_small.ptr);
+  if (ctx->ws_aux.ptr) cudaFree(ctx->ws_aux.ptr);
+  if (ctx->ws_plan.ptr) cudaFree(ctx->ws_plan.ptr);
   if (ctx->pinned.ptr) cudaFreeHost(ctx->pinned.ptr);
   if (ctx->pinned_out.ptr) cudaFreeHost(ctx->pinned_out.ptr);
   delete ctx;
@@ -374,7 +376,7 @@ extern "C" int sfw3d_render(sfw3d_ctx* ctx, int dtype, const int dims[3], const 
   SFW3D_TRY(ensure_device(ctx, ctx->ws_small, (size_t(k) + 1) * sizeof(AtomGeo) + 4096));
   AtomGeo* ad = static_cast<AtomGeo*>(ctx->ws_small.ptr);
   SFW3D_TRY(upload_atoms(ctx, atoms, ad));
-  return render_impl(ctx, dtype, dims, ad, k, out_dev);
+  return render_impl(ctx, dtype, dims, atoms, ad, k, out_dev);
 }
 
 static int finite_all(const double* x, size_t n) {
@@ -393,15 +395,13 @@ extern "C" int sfw3d_atom_sums(sfw3d_ctx* ctx, int dtype, const int dims[3], con
   if (k == 0) return SFW3D_OK;
   std::vector<AtomGeo> atoms;
   SFW3D_TRY(build_atoms(dims, params_host, k, atoms));
-  const size_t scratch = atom_sums_scratch(atoms);
-  const size_t need = Carver::need({size_t(k) * sizeof(AtomGeo), size_t(k) * 6 * sizeof(double), scratch});
+  const size_t need = Carver::need({size_t(k) * sizeof(AtomGeo), size_t(k) * 6 * sizeof(double)});
   SFW3D_TRY(ensure_device(ctx, ctx->ws_small, need));
   Carver cv(ctx->ws_small.ptr);
   AtomGeo* ad = cv.take<AtomGeo>(k);
   double* sums = cv.take<double>(size_t(k) * 6);
-  void* scr = cv.take<char>(scratch);
   SFW3D_TRY(upload_atoms(ctx, atoms, ad));
-  SFW3D_TRY(atom_sums_impl(ctx, dtype, dims, field_dev, atoms, ad, sums, scr, scratch));
+  SFW3D_TRY(atom_sums_impl(ctx, dtype, dims, field_dev, atoms, ad, sums));
   SFW3D_TRY(download_sync(ctx, sums_host, sums, size_t(k) * 6 * sizeof(double)));
   if (!finite_all(sums_host, size_t(k) * 6)) {
     set_error("non-finite atom inner product; atom parameters left the smooth regime");
@@ -427,26 +427,24 @@ extern "C" int sfw3d_cost_grad(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, 
   Carver cw(ctx->ws.ptr);
   void* A = cw.take<char>(vb);
   void* B = cw.take<char>(vb);
-  const size_t scratch = atom_sums_scratch(atoms);
   const int nred = 4 * ctx->num_sms;
   SFW3D_TRY(ensure_device(ctx, ctx->ws_small,
                           Carver::need({(size_t(k) + 1) * sizeof(AtomGeo), (size_t(k) * 6 + 1) * sizeof(double),
-                                        size_t(nred) * sizeof(double), scratch})));
+                                        size_t(nred) * sizeof(double)})));
   Carver cs(ctx->ws_small.ptr);
   AtomGeo* ad = cs.take<AtomGeo>(k + 1);
   double* res = cs.take<double>(size_t(k) * 6 + 1);  // [sumsq, sums...]
   double* partials = cs.take<double>(nred);
-  void* scr = cs.take<char>(scratch);
   SFW3D_TRY(upload_atoms(ctx, atoms, ad));
   // model = H * sum w G  (A -> B, A used as pass scratch)
-  SFW3D_TRY(render_impl(ctx, dtype, dims, ad, k, A));
+  SFW3D_TRY(render_impl(ctx, dtype, dims, atoms, ad, k, A));
   SFW3D_TRY(psf_apply_impl(ctx, psf, dtype, A, B, 0, A));
   // resid = model - y -> A ; ||resid||^2
   SFW3D_TRY(sumsq_diff_impl(ctx, dtype, n, B, y_dev, A, partials, res));
   if (grad_host || back_dev) {
     void* back = back_dev ? back_dev : B;
     SFW3D_TRY(psf_apply_impl(ctx, psf, dtype, A, back, 1, back == B ? A : B));
-    if (grad_host) SFW3D_TRY(atom_sums_impl(ctx, dtype, dims, back, atoms, ad, res + 1, scr, scratch));
+    if (grad_host) SFW3D_TRY(atom_sums_impl(ctx, dtype, dims, back, atoms, ad, res + 1));
   }
   std::vector<double> host(size_t(k) * 6 + 1);
   SFW3D_TRY(download_sync(ctx, host.data(), res, (grad_host ? host.size() : 1) * sizeof(double)));
@@ -525,18 +523,16 @@ extern "C" int sfw3d_cost_grad_slab(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dt
   Carver cw(ctx->ws.ptr);
   char* A = cw.take<char>(vb);
   char* B = cw.take<char>(vb);
-  const size_t scratch = atom_sums_scratch(pieces);
   const int nred = 4 * ctx->num_sms;
   SFW3D_TRY(ensure_device(ctx, ctx->ws_small,
                           Carver::need({(size_t(kp) + 1) * sizeof(AtomGeo), (size_t(kp) * 6 + 1) * sizeof(double),
-                                        size_t(nred) * sizeof(double), scratch})));
+                                        size_t(nred) * sizeof(double)})));
   Carver cs(ctx->ws_small.ptr);
   AtomGeo* ad = cs.take<AtomGeo>(kp + 1);
   double* res = cs.take<double>(size_t(kp) * 6 + 1);
   double* partials = cs.take<double>(nred);
-  void* scr = cs.take<char>(scratch);
   SFW3D_TRY(upload_atoms(ctx, pieces, ad));
-  SFW3D_TRY(render_impl(ctx, dtype, dims, ad, kp, A));
+  SFW3D_TRY(render_impl(ctx, dtype, dims, pieces, ad, kp, A));
   SFW3D_TRY(psf_apply_impl(ctx, psf, dtype, A, B, 0, A));
   // r = model - y on the slab planes only, 0 on the halo planes
   const size_t plane = size_t(dims[1]) * dims[2];
@@ -545,7 +541,7 @@ extern "C" int sfw3d_cost_grad_slab(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dt
   SFW3D_TRY(sumsq_diff_impl(ctx, dtype, int64_t(x1 - x0 + 1) * int64_t(plane), B + off,
                             static_cast<const char*>(y_dev) + off, A + off, partials, res));
   SFW3D_TRY(psf_apply_impl(ctx, psf, dtype, A, B, 1, A));
-  SFW3D_TRY(atom_sums_impl(ctx, dtype, dims, B, pieces, ad, res + 1, scr, scratch));
+  SFW3D_TRY(atom_sums_impl(ctx, dtype, dims, B, pieces, ad, res + 1));
   std::vector<double> host(size_t(kp) * 6 + 1);
   SFW3D_TRY(download_sync(ctx, host.data(), res, host.size() * sizeof(double)));
   *half_sumsq_host = 0.5 * host[0];

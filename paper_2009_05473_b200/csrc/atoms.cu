@@ -97,6 +97,11 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float lg2_approx(float x) {
   float y;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -451,6 +456,261 @@ __global__ void __launch_bounds__(kSumThreads) atom_sums_big_kernel(
   }
 }
 
+// ------------------------------------------------ render, fp32 interval path
+// fp32 storage when every atom box is a product of three unwrapped intervals
+// that meet a brick in ONE run per axis (no full axis, len <= n - brick):
+// then box ∩ brick is an interval per axis and every offset is linear,
+// o(i) = o0 + i. A CTA owns a 16 x 16 x 32 brick with its accumulator in
+// shared memory (row pitch 33), compacts the atoms meeting it in row order
+// (256 per pass) and prepares each listed atom's intersection record in
+// parallel (one thread per atom). Warp w owns x-planes 2w, 2w + 1 and walks
+// the list on its own: the voxels of (its planes ∩ atom) are spread over the
+// lanes (4 x-y rows at one z per lane: lanes along z), then __syncwarp — so
+// every voxel still sums its atoms in the reference's row order, with no
+// CTA-wide barrier per atom.
+constexpr int kFX = 16, kFY = 16, kFZ = 32, kFP = kFZ + 1, kFT = 256, kFW = kFX / (kFT / 32);
+
+struct FAtom {
+  float o0x, o0y, o0z;
+  int lo, cnt;       // brick-local start / count per axis: byte a = axis
+  float w, hd, inv2sd;  // inv2sd: -log2(e) / (2 sigma^d)
+  int d2;
+  float inv_ngz;  // 1 / ceil(cz / 4)
+};
+
+// run of the unwrapped box [s, s + l) meeting brick coords [b0, b0 + B)
+// (l <= n - B: one run); returns the count (0 = none)
+__device__ __forceinline__ int brick_run(int s, int l, double m, int b0, int B, int n, int& lo,
+                                         float& o0) {
+  const int d = pmod(b0 - s, n);
+  if (d < l) {  // brick start inside the box
+    lo = 0;
+    o0 = float(double(s + d) - m);
+    return min(l - d, B);
+  }
+  const int e = pmod(s - b0, n);  // box start inside the brick?
+  if (e < B) {
+    lo = e;
+    o0 = float(double(s) - m);
+    return min(l, B - e);
+  }
+  lo = 0;
+  o0 = 0.f;
+  return 0;
+}
+
+// exact small-integer division a / b (a < 2^21) through a float reciprocal
+__device__ __forceinline__ int fdiv_small(int a, int, float inv_b) {
+  return __float2int_rz((float(a) + 0.5f) * inv_b);
+}
+
+__global__ void __launch_bounds__(kFT) render_f32_kernel(const AtomGeo* __restrict__ atoms,
+                                                         const int4* __restrict__ boxes, int k,
+                                                         int nx, int ny, int nz,
+                                                         float* __restrict__ out) {
+  __shared__ float acc[kFX * kFY * kFP];
+  __shared__ FAtom fa[kFT];
+  __shared__ int warp_cnt[kFT / 32];
+  __shared__ int list_n;
+  const int nbz = (nz + kFZ - 1) / kFZ, nby = (ny + kFY - 1) / kFY;
+  const int bz = blockIdx.x % nbz, by = (blockIdx.x / nbz) % nby, bx = blockIdx.x / (nbz * nby);
+  const int x0 = bx * kFX, y0 = by * kFY, z0 = bz * kFZ;
+  const int BX = min(kFX, nx - x0), BY = min(kFY, ny - y0), BZ = min(kFZ, nz - z0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < kFX * kFY * kFP; e += kFT) acc[e] = 0.f;
+  const int wx0 = warp * kFW;  // this warp's first x-plane
+  for (int base = 0; base < k; base += kFT) {
+    const int ai = base + tid;
+    FAtom f;
+    bool hit = false;
+    if (ai < k) {
+      const int4 bx4 = boxes[ai];  // start x, y, z; lengths (10 bits each)
+      const int l[3] = {bx4.w & 1023, (bx4.w >> 10) & 1023, bx4.w >> 20};
+      const int st[3] = {bx4.x, bx4.y, bx4.z};
+      const int b0[3] = {x0, y0, z0}, B[3] = {BX, BY, BZ}, n[3] = {nx, ny, nz};
+      int lo[3], c[3];
+      float o0[3];
+      hit = true;
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        // (offsets need the centre: read only for atoms that meet the brick)
+        c[ax] = brick_run(st[ax], l[ax], 0.0, b0[ax], B[ax], n[ax], lo[ax], o0[ax]);
+        hit &= c[ax] > 0;
+      }
+      if (hit) {
+        const AtomGeo& a = atoms[ai];
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax)
+          brick_run(st[ax], l[ax], a.m[ax], b0[ax], B[ax], n[ax], lo[ax], o0[ax]);
+        f.o0x = o0[0];
+        f.o0y = o0[1];
+        f.o0z = o0[2];
+        f.lo = lo[0] | (lo[1] << 8) | (lo[2] << 16);
+        f.cnt = c[0] | (c[1] << 8) | (c[2] << 16);
+        f.w = float(a.w);
+        f.hd = float(a.half_d);
+        f.inv2sd = float(-1.4426950408889634 * a.inv2sd);  // (-log2 e) / (2 sigma^d)
+        f.d2 = a.d2;
+        f.inv_ngz = rcp_approx(float((c[2] + 3) >> 2));
+      }
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) warp_cnt[warp] = __popc(mask);
+    __syncthreads();  // (also: the previous pass's warps are done with fa)
+    if (tid == 0) {
+      int sacc = 0;
+      for (int w = 0; w < kFT / 32; ++w) {
+        const int c = warp_cnt[w];
+        warp_cnt[w] = sacc;
+        sacc += c;
+      }
+      list_n = sacc;
+    }
+    __syncthreads();
+    if (hit) fa[warp_cnt[warp] + __popc(mask & ((1u << lane) - 1u))] = f;
+    __syncthreads();
+    const int cnt = list_n;
+    for (int q = 0; q < cnt; ++q) {
+      const FAtom g = fa[q];
+      const int lo0 = g.lo & 255, lo1 = (g.lo >> 8) & 255, lo2 = g.lo >> 16;
+      const int cx = g.cnt & 255, cy = (g.cnt >> 8) & 255, cz = g.cnt >> 16;
+      const int px0 = max(wx0, lo0), px1 = min(wx0 + kFW, lo0 + cx);
+      const int rows = (px1 - px0) * cy;
+      if (rows <= 0) continue;
+      const int ngz = (cz + 3) >> 2;
+      const int units = rows * ngz;
+      const float ox0 = g.o0x + float(px0 - lo0);
+      const bool d2 = g.d2 != 0;
+      // unit = one x-y row x 4 consecutive z (lanes along z groups)
+      for (int u = lane; u < units; u += 32) {
+        const int row = fdiv_small(u, ngz, g.inv_ngz);
+        const int gz = u - row * ngz;
+        const int ix = row >= cy ? 1 : 0;  // (kFW = 2 planes per warp)
+        const int iy = row - ix * cy;
+        const float ox = ox0 + float(ix), oy = g.o0y + float(iy);
+        const float oxy2 = fmaf(ox, ox, oy * oy);
+        float oz = g.o0z + float(4 * gz);
+        float* pa = acc + ((px0 + ix) * kFY + lo1 + iy) * kFP + lo2 + 4 * gz;
+        const int nz4 = cz - 4 * gz;  // valid voxels of this group (>= 1)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float u2 = fmaf(oz, oz, oxy2);
+          const float p = d2 ? u2 : ex2_approx(g.hd * lg2_approx(u2));
+          const float v = ex2_approx(g.inv2sd * p);  // exp(-u2^(d/2) / (2 sigma^d))
+          if (j < nz4) pa[j] = fmaf(g.w, v, pa[j]);
+          oz += 1.f;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < kFX * kFY * kFZ; e += kFT) {
+    const int z = e & (kFZ - 1), y = (e >> 5) & (kFY - 1), x = e >> 9;
+    if (x < BX && y < BY && z < BZ)
+      out[((long long)(x0 + x) * ny + y0 + y) * nz + z0 + z] = acc[(x * kFY + y) * kFP + z];
+  }
+}
+
+// ------------------------------------------- atom sums, fp32 interval path
+// Same chunks as atom_sums_kernel (runs of whole rows of one box). A thread
+// unit is 4 consecutive rows at one z (lanes along z: coalesced field loads);
+// offsets are linear in the box indices, so per voxel the work is the profile
+// (lg2, ex2, ex2 on the MUFU), one reciprocal and the accumulations:
+//   s0 += v b, s4 += v t b (x d/sigma at the end), s5 += v t b log2(u2)
+//   (-> -(ln2/2 s5 - ln sigma s4)), and with ab = d v t b / u2:
+//   s1 += ab ox, s2 += ab oy, s3 += oz sum_rows ab.
+struct RowF {
+  float ox, oy, oxy2;
+  int lin;  // volume offset of the row's z = 0
+};
+
+__global__ void __launch_bounds__(kSumThreads) atom_sums_f32_kernel(
+    const AtomGeo* __restrict__ atoms, const Chunk* __restrict__ chunks, int nx, int ny, int nz,
+    const float* __restrict__ field, double* __restrict__ partials) {
+  __shared__ RowF rows[kMaxRows32 + 4];
+  const Chunk ch = chunks[blockIdx.x];
+  const AtomGeo& a = atoms[ch.atom];
+  const int l1 = a.len[1], l2 = a.len[2];
+  const float inv2sd = float(a.inv2sd), hd = float(a.half_d);
+  const bool d2 = a.d2 != 0;
+  const float o0z = float(double(a.start[2]) - a.m[2]);
+  const int zs = pmod(a.start[2], nz);
+  // per-row record: offsets and the wrapped row base (padding rows: b = 0)
+  for (int q = threadIdx.x; q < ch.nrows; q += kSumThreads) {
+    RowF rr;
+    {
+      const int r = ch.row0 + q;
+      const int ix = r / l1, iy = r - ix * l1;
+      const int px = a.start[0] + ix, py = a.start[1] + iy;
+      rr.ox = float(double(px) - a.m[0]);
+      rr.oy = float(double(py) - a.m[1]);
+      rr.oxy2 = fmaf(rr.ox, rr.ox, rr.oy * rr.oy);
+      rr.lin = (pmod(px, nx) * ny + pmod(py, ny)) * nz;
+    }
+    rows[q] = rr;
+  }
+  __syncthreads();
+  const int ngz = (l2 + 3) >> 2;
+  const float inv_ngz = rcp_approx(float(ngz));
+  const int units = ch.nrows * ngz;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f, s5 = 0.f;
+  // unit = one x-y row x 4 consecutive z (lanes along z groups: the four
+  // field loads of a warp share their 32-byte sectors)
+  for (int u = threadIdx.x; u < units; u += kSumThreads) {
+    const int q = fdiv_small(u, ngz, inv_ngz);
+    const int g4 = 4 * (u - q * ngz);
+    const RowF rr = rows[q];
+    const int nz4 = l2 - g4;
+    int gz = zs + g4;
+    gz = gz >= nz ? gz - nz : gz;
+    float b[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      b[j] = j < nz4 ? __ldg(field + rr.lin + gz) : 0.f;
+      gz = gz + 1 == nz ? 0 : gz + 1;
+    }
+    float oz = o0z + float(g4);
+    float sab = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float u2 = fmaf(oz, oz, rr.oxy2);
+      float t, lg;
+      const float v = profile32(inv2sd, hd, d2, u2, t, lg);
+      const float vb = v * b[j];
+      const float vtb = vb * t;
+      s0 += vb;
+      s4 += vtb;
+      s5 = fmaf(vtb, fmaxf(lg, -126.f), s5);  // (u2 = 0: vtb = 0, lg = -inf)
+      const float ab = vtb * rcp_approx(fmaxf(u2, 1e-30f));
+      sab += ab;
+      s3 = fmaf(ab, oz, s3);
+      oz += 1.f;
+    }
+    s1 = fmaf(sab, rr.ox, s1);
+    s2 = fmaf(sab, rr.oy, s2);
+  }
+  const float dd = float(a.d);
+  double s[6] = {double(s0), double(dd * s1), double(dd * s2), double(dd * s3),
+                 double(s4) * a.d_over_sigma,
+                 -(0.34657359027997264 * double(s5) - a.log_sigma * double(s4))};
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ double red[6][kSumThreads / 32];
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    double x = s[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (lane == 0) red[c][warp] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    double x = 0.0;
+    for (int w = 0; w < kSumThreads / 32; ++w) x += red[threadIdx.x][w];
+    partials[(long long)blockIdx.x * 6 + threadIdx.x] = x;
+  }
+}
+
 __global__ void chunk_combine_kernel(const int* __restrict__ first_chunk, int k,
                                      const double* __restrict__ partials, double* __restrict__ sums) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -508,11 +768,38 @@ __global__ void final_sum_kernel(const double* __restrict__ partials, int n, dou
 
 }  // namespace
 
-int render_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const AtomGeo* atoms_dev, int k,
-                void* out) {
+// every box a product of unwrapped intervals meeting any brick of size B in
+// one run per axis (the fp32 interval kernels' precondition)
+static bool interval_boxes(const std::vector<AtomGeo>& atoms, const int dims[3], const int B[3]) {
+  if ((long long)dims[0] * dims[1] * dims[2] >= (1LL << 31)) return false;
+  for (const auto& a : atoms)
+    for (int ax = 0; ax < 3; ++ax)
+      if (a.full[ax] || a.len[ax] > dims[ax] - B[ax] || a.len[ax] >= 1024) return false;
+  return true;
+}
+
+int render_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const std::vector<AtomGeo>& atoms,
+                const AtomGeo* atoms_dev, int k, void* out) {
+  SFW3D_PROF(ctx, "render");
+  static const int kFB[3] = {kFX, kFY, kFZ};
+  if (dtype == SFW3D_F32 && interval_boxes(atoms, dims, kFB)) {
+    const int nbf = ((dims[0] + kFX - 1) / kFX) * ((dims[1] + kFY - 1) / kFY) *
+                    ((dims[2] + kFZ - 1) / kFZ);
+    // compact boxes for the per-brick culling: start x, y, z; lengths
+    std::vector<int4> bx(std::max(k, 1));
+    for (int i = 0; i < k; ++i)
+      bx[i] = make_int4(atoms[i].start[0], atoms[i].start[1], atoms[i].start[2],
+                        atoms[i].len[0] | (atoms[i].len[1] << 10) | (atoms[i].len[2] << 20));
+    SFW3D_TRY(ensure_device(ctx, ctx->ws_aux, bx.size() * sizeof(int4)));
+    int4* bx_dev = static_cast<int4*>(ctx->ws_aux.ptr);
+    SFW3D_TRY(stage_upload(ctx, bx_dev, bx.data(), bx.size() * sizeof(int4)));
+    render_f32_kernel<<<nbf, kFT, 0, ctx->stream>>>(atoms_dev, bx_dev, k, dims[0], dims[1],
+                                                    dims[2], static_cast<float*>(out));
+    SFW3D_LAUNCH_CHECK(ctx);
+    return SFW3D_OK;
+  }
   const int nb = ((dims[0] + kSX - 1) / kSX) * ((dims[1] + kSY - 1) / kSY) *
                  ((dims[2] + kSZ - 1) / kSZ);
-  SFW3D_PROF(ctx, "render");
   if (dtype == SFW3D_F64)
     render_kernel<double><<<nb, 512, 0, ctx->stream>>>(atoms_dev, k, dims[0], dims[1], dims[2],
                                                         static_cast<double*>(out));
@@ -546,34 +833,26 @@ static bool small_boxes(const std::vector<AtomGeo>& atoms, const int dims[3]) {
   return true;
 }
 
-size_t atom_sums_scratch(const std::vector<AtomGeo>& atoms) {
-  std::vector<Chunk> chunks;
-  std::vector<int> first;
-  chunk_plan(atoms, chunks, first);
-  const size_t nch = chunks.size();
-  return Carver::need({nch * sizeof(Chunk), (atoms.size() + 1) * sizeof(int), nch * 6 * sizeof(double)});
-}
-
+// The chunk plan is made here, on the host, typically while the device is
+// still rendering / convolving (the callers enqueue those first); its device
+// copy and the chunk partials live in the context's own ws_plan arena.
 int atom_sums_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const void* field,
-                   const std::vector<AtomGeo>& atoms, const AtomGeo* atoms_dev, double* sums_dev,
-                   void* scratch, size_t scratch_bytes) {
+                   const std::vector<AtomGeo>& atoms, const AtomGeo* atoms_dev, double* sums_dev) {
   const int k = int(atoms.size());
   if (k == 0) return SFW3D_OK;
   std::vector<Chunk> chunks;
   std::vector<int> first;
-  // (atom_sums_scratch sizes for the fp64 plan: never fewer chunks)
   if (dtype == SFW3D_F64 || !small_boxes(atoms, dims))
     chunk_plan(atoms, chunks, first);
   else
     chunk_plan(atoms, chunks, first, std::max(kChunk, chunk32()), kMaxRows32);
-  Carver cv(scratch);
+  SFW3D_TRY(ensure_device(ctx, ctx->ws_plan,
+                          Carver::need({chunks.size() * sizeof(Chunk), first.size() * sizeof(int),
+                                        chunks.size() * 6 * sizeof(double)})));
+  Carver cv(ctx->ws_plan.ptr);
   Chunk* ch_dev = cv.take<Chunk>(chunks.size());
   int* first_dev = cv.take<int>(first.size());
   double* part = cv.take<double>(chunks.size() * 6);
-  if (cv.off > scratch_bytes) {
-    set_error("atom_sums scratch too small");
-    return SFW3D_ECUDA;
-  }
   SFW3D_TRY(stage_upload(ctx, ch_dev, chunks.data(), chunks.size() * sizeof(Chunk)));
   SFW3D_TRY(stage_upload(ctx, first_dev, first.data(), first.size() * sizeof(int)));
   const unsigned nch = unsigned(chunks.size());
@@ -587,7 +866,11 @@ int atom_sums_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const void* fie
       atom_sums_big_kernel<double><<<nch, kSumThreads, 0, ctx->stream>>>(
           atoms_dev, ch_dev, dims[0], dims[1], dims[2], static_cast<const double*>(field), part);
   } else {
-    if (small)
+    static const int kOne[3] = {1, 1, 1};
+    if (interval_boxes(atoms, dims, kOne))
+      atom_sums_f32_kernel<<<nch, kSumThreads, 0, ctx->stream>>>(
+          atoms_dev, ch_dev, dims[0], dims[1], dims[2], static_cast<const float*>(field), part);
+    else if (small)
       atom_sums_kernel<float><<<nch, kSumThreads, 0, ctx->stream>>>(
           atoms_dev, ch_dev, dims[0], dims[1], dims[2], static_cast<const float*>(field), part);
     else

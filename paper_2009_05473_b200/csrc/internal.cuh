@@ -71,6 +71,8 @@ struct sfw3d_ctx {
   size_t pin_off = 0;      // bytes of `pinned` referenced by in-flight copies
   sfw3d::Arena pinned_out; // pinned host buffer for small downloads
   sfw3d::Arena ws_small;   // small device scratch (params, partials)
+  sfw3d::Arena ws_aux;     // auxiliary small device scratch (render culling boxes)
+  sfw3d::Arena ws_plan;    // atom-sum chunk plan + chunk partials
   // kernel-family timing (sfw3d_ctx_profile)
   int profile = 0;
   struct Mark {
@@ -177,12 +179,12 @@ int corr_pass_impl(sfw3d_ctx* ctx, int dtype, const void* in, void* out, const i
                    double w, const char* family);
 
 // Launch helpers implemented in the .cu files.
-int render_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const AtomGeo* atoms_dev,
+int render_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const std::vector<AtomGeo>& atoms,
+                const AtomGeo* atoms_dev,
                 int k, void* out);
 int atom_sums_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const void* field,
                    const std::vector<AtomGeo>& atoms, const AtomGeo* atoms_dev,
-                   double* sums_dev, void* scratch, size_t scratch_bytes);
-size_t atom_sums_scratch(const std::vector<AtomGeo>& atoms);
+                   double* sums_dev);
 
 // fp64 block reductions
 int sumsq_diff_impl(sfw3d_ctx* ctx, int dtype, int64_t n, const void* a, const void* b,

@@ -172,6 +172,37 @@ def test_cost_grad_f32(P):
     assert colwise(g.per_atom, r0) < 1e-4     # measured 1.5e-6 on B200
 
 
+@pytest.mark.parametrize("dims", [(96, 80, 128), (48, 64, 96), (40, 40, 64)])
+def test_cost_grad_f32_interval_kernels(P, dims):
+    """The fp32 interval render / atom-sum kernels (boxes meeting every brick
+    in one run per axis): atoms on the periodic seams, integer centres (u2 = 0
+    voxels), d == 2 exactly, partial bricks; plus the forward render alone."""
+    rng = np.random.default_rng(sum(dims))
+    kernel = O.box_gaussian_psf(dims, (1.5, 1.5, 2.0), (4, 4, 6))
+    psf = P.Psf(P.Volume(kernel), normalize=False)
+    k = 60
+    m = rng.uniform(0, 1, (k, 3)) * np.array(dims)
+    m[:6] = [[0.2, 0.1, 0.3], [dims[0] - 0.4, 3.0, dims[2] - 0.2], [5.0, 7.0, 9.0],
+             [dims[0] - 1.0, dims[1] - 1.0, 0.0], [12.5, 0.5, 31.5], [1.0, dims[1] / 2, 2.0]]
+    rows = np.column_stack([rng.uniform(0.5, 2, k), m, rng.uniform(1, 2.2, k),
+                            rng.uniform(1.9, 2.6, k)])
+    rows[::7, 5] = 2.0
+    y = (O.conv(O.render(rows, dims), O.psf_hat(kernel))
+         + 0.01 * rng.standard_normal(dims)).astype(np.float32).astype(np.float64)
+    pert = rows.copy()
+    pert[6:, 1:4] += 0.1 * rng.standard_normal((k - 6, 3))  # rows 0-5 keep their centres
+    pert[:, 1:4] %= np.array(dims)
+    pert[2, 1:4] = [5.0, 7.0, 9.0]  # integer centre: a u2 = 0 voxel
+    c0, r0, _ = O.criterion_and_gradient(y, pert, O.psf_hat(kernel), 0.1)
+    with P.precision("f32"):
+        c, g = P.criterion_and_gradient(P.Volume(y), measure(P, pert), psf, 0.1)
+        fwd = P.forward(measure(P, pert), psf).data
+    assert abs(c - c0) <= 1e-5 * abs(c0)
+    assert colwise(g.per_atom, r0) < 1e-4
+    ref = O.conv(O.render(pert, dims), O.psf_hat(kernel))
+    assert np.max(np.abs(fwd - ref)) <= 2e-6 * np.max(np.abs(ref))
+
+
 # ---------------------------------------------------------------- K1 / K7
 def test_certificate_golden(P, golden):
     g = golden("certificate")

@@ -65,17 +65,29 @@ def test_cfg2_solve_shape(cfg2_solve):
     assert 15 <= len(res.measure) <= 40
 
 
-@pytest.mark.parametrize("which", [0, 1, 2, -1])
-def test_cfg2_certificate_step_replay(cfg2_solve, which):
+def _cert_steps(c):
+    return [r for r in c["record"] if r["step"] == "certificate"]
+
+
+def _lasso_steps(c):
+    return [r for r in c["record"] if r["step"] == "lasso"]
+
+
+@pytest.mark.parametrize("part", range(4))
+def test_cfg2_certificate_step_replay(cfg2_solve, part):
+    """Every certificate step of the solve (split over 4 test items)."""
     c = cfg2_solve
-    steps = [r for r in c["record"] if r["step"] == "certificate"]
-    st = steps[which]
+    for st in _cert_steps(c)[part::4]:
+        _replay_certificate(c, st)
+
+
+def _replay_certificate(c, st):
     r = _residual(c["y"], c["khat"], st["thetas"], st["weights"])
     per = O.eta_maxima(r, c["lam"], c["khat"], c["sg"], c["dg"], c["win"], threads=8)
     flat = max(range(len(per)), key=lambda i: (per[i][1], -i))
     pos, val = per[flat]
     i, j = divmod(flat, len(c["dg"]))
-    assert st["cand"] == (i, j) and tuple(st["start"].m) == tuple(float(p) for p in pos)
+    assert st["cand"] == (i, j) and tuple(st["start"].m) == tuple(float(p) for p in pos), st["k"]
     assert abs(st["eta_grid"] - val) <= 1e-9 * abs(val)
     back = O.corr(r, c["khat"])
     start = np.array([*pos, c["sg"][i], c["dg"][j]], dtype=float)
@@ -84,11 +96,14 @@ def test_cfg2_certificate_step_replay(cfg2_solve, which):
     np.testing.assert_allclose(st["theta"].to_array(), theta, atol=1e-6, rtol=0)
 
 
-@pytest.mark.parametrize("which", [0, 1, 2, -1])
-def test_cfg2_lasso_step_replay(cfg2_solve, which):
+def test_cfg2_lasso_step_replay(cfg2_solve):
+    """Every weight step of the solve."""
     c = cfg2_solve
-    steps = [r for r in c["record"] if r["step"] == "lasso"]
-    st = steps[which]
+    for st in _lasso_steps(c):
+        _replay_lasso(c, st)
+
+
+def _replay_lasso(c, st):
     phis = np.stack([O.phi(t.to_array(), c["khat"], c["y"].shape) for t in st["thetas"]])
     gram, b = O.gram_system(phis, c["y"])
     w, _, _ = O.cd_solve(gram, b, c["lam"], st["w_init"], tol=1e-6, max_iter=2000)
