@@ -18,7 +18,7 @@ import numpy as np
 from scipy.optimize import minimize
 
 from . import _native as N
-from .forward import Psf, atom_sums_dev, psf_apply_dev, to_dev
+from .forward import Psf, as_psf, atom_sums_dev, psf_apply_dev, to_dev
 from .measures import AtomParams, DomainBounds, bounds_box, clamp_to_domain
 from .volumes import Volume
 
@@ -117,6 +117,8 @@ class AtomTemplateTable:
         """Reference representation (n_sigma, n_shape, rfft dims), computed lazily."""
         if self._hats is None:
             import scipy.fft as sfft
+            from .forward import _warn_host_fft
+            _warn_host_fft("AtomTemplateTable.template_hats", self.dims)
             from .forward import render_dev  # device render, then host FFT (compatibility only)
             out = []
             for s in self.sigma_grid:
@@ -146,6 +148,7 @@ def build_template_table(psf: Psf, sigma_grid, shape_grid, bounds: DomainBounds 
     None keeps the library default: pruning by volume size, fp32 term
     selection at 1e-5, 65536 exactly re-evaluated voxels per call).
     """
+    psf = as_psf(psf)
     sigma_grid = np.sort(np.asarray(sigma_grid, dtype=float))
     shape_grid = np.sort(np.asarray(shape_grid, dtype=float))
     if sigma_grid.size == 0 or shape_grid.size == 0:

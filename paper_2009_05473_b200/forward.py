@@ -58,8 +58,10 @@ class Psf:
 
     @property
     def kernel_hat(self) -> np.ndarray:
+        """Reference compatibility only: a HOST FFT (the B200 path never uses it)."""
         if self._hat is None:
             import scipy.fft as sfft
+            _warn_host_fft("Psf.kernel_hat", self.dims)
             self._hat = sfft.rfftn(sfft.ifftshift(self.kernel.data))
         return self._hat
 
@@ -93,6 +95,39 @@ class Psf:
         sep = C.c_int()
         N.check(N.lib().sfw3d_psf_info(self.native(N.device_index(device)), C.byref(sep), None, None))
         return bool(sep.value)
+
+
+def _warn_host_fft(what: str, dims) -> None:
+    if int(np.prod(dims)) >= (1 << 21):
+        import warnings
+        warnings.warn(f"{what}: computing a host FFT of a {dims} volume for reference "
+                      "compatibility (the B200 path does not use it)", RuntimeWarning,
+                      stacklevel=3)
+
+
+_FOREIGN_PSF = None
+
+
+def as_psf(psf) -> Psf:
+    """This package's Psf for `psf`: itself, or (cached per object) a wrapper
+    of a reference ``sfw3d.forward.Psf`` / any object with ``.kernel.data``
+    (already normalised: the reference normalises in its constructor)."""
+    global _FOREIGN_PSF
+    if isinstance(psf, Psf):
+        return psf
+    if not hasattr(psf, "kernel") or not hasattr(psf.kernel, "data"):
+        raise TypeError(f"expected a Psf, got {type(psf).__name__}")
+    if _FOREIGN_PSF is None:
+        import weakref
+        _FOREIGN_PSF = weakref.WeakKeyDictionary()
+    try:
+        got = _FOREIGN_PSF.get(psf)
+    except TypeError:  # (not weak-referenceable: wrap every time)
+        return Psf(Volume(np.asarray(psf.kernel.data, dtype=np.float64)), normalize=False)
+    if got is None:
+        got = Psf(Volume(np.asarray(psf.kernel.data, dtype=np.float64)), normalize=False)
+        _FOREIGN_PSF[psf] = got
+    return got
 
 
 class _PsfHandle:
@@ -144,7 +179,7 @@ def psf_apply_dev(psf: Psf, x, adjoint: bool, out=None):
     dev = x.device.index
     ctx = N.context(dev)
     out = torch.empty_like(x) if out is None else out
-    N.check(N.lib().sfw3d_psf_apply(ctx.handle, psf.native(dev), code_of(x), N.ptr(x), N.ptr(out),
+    N.check(N.lib().sfw3d_psf_apply(ctx.handle, as_psf(psf).native(dev), code_of(x), N.ptr(x), N.ptr(out),
                                     1 if adjoint else 0))
     return out
 
@@ -185,7 +220,7 @@ def cost_grad_dev(psf: Psf, y, rows: np.ndarray, lam: float, want_grad: bool = T
     cost = C.c_double()
     grad = np.zeros((k, 6)) if want_grad else None
     N.check(N.lib().sfw3d_cost_grad(
-        ctx.handle, psf.native(dev), code_of(y), N.ptr(y), N.f64_ptr(rows), k, float(lam),
+        ctx.handle, as_psf(psf).native(dev), code_of(y), N.ptr(y), N.f64_ptr(rows), k, float(lam),
         C.byref(cost), N.f64_ptr(grad) if want_grad else None,
         N.ptr(back) if back is not None else None))
     return cost.value, grad

@@ -75,3 +75,34 @@ def test_device_calls_fail_loudly_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError):
         N.context()
+
+
+REFERENCE_SRC = Path("/root/reference/pkg/src")
+
+
+@pytest.mark.skipif(not (REFERENCE_SRC / "sfw3d").exists(), reason="reference not present")
+def test_integration_snippet_rebinds_real_reference():
+    """INTEGRATION.md's binding, executed verbatim against the real sfw3d
+    0.1.0 (build container only; no compute): every name the reference's
+    modules bind by import is replaced in every namespace, incl. the CLI's
+    solvers and the Psf class the CLI constructs (cli.py:20-23, 85-86)."""
+    import subprocess
+    import sys
+    code = f"""
+import sys
+sys.path[:0] = [{str(REFERENCE_SRC)!r}, {str(ROOT)!r}, {str(ROOT / 'tests')!r}]
+import sfw3d, sfw3d.cli, sfw3d.experiment
+from integration_snippet import load_snippet
+done = load_snippet()["enable"]("f64")
+import paper_2009_05473_b200 as gpu
+want = [("sfw3d.cli", "bsfw"), ("sfw3d.cli", "sfw"), ("sfw3d.forward", "Psf"),
+        ("sfw3d.solvers", "certificate_max"), ("sfw3d.solvers", "local_descent"),
+        ("sfw3d.certificate", "eta_field"), ("sfw3d.experiment", "forward"), ("sfw3d", "bsfw")]
+for m, n in want:
+    assert (m, n) in done, (m, n)
+    assert getattr(sys.modules[m], n) is getattr(gpu, n), (m, n)
+print("rebound", len(done))
+"""
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "rebound" in out.stdout
