@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--cg-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-sfw", action="store_true",
+                    help="skip the CPU oracle's config-1 SFW solve (~20 s)")
     ap.add_argument("--one-rank", default=None, metavar="R/W",
                     help="testing aid: run only rank R of a W-rank layout on this GPU, "
                          "no process group (per-rank timing; records not combined)")
@@ -496,54 +498,74 @@ def slab_costgrad_workload(args, dev, rank, world):
                       "48 KB fp64 all-reduce)"}
 
 
-def solve_workload(dev):
-    """Config 1 BSFW end to end (64^3 f64) on the reference-generated
+def solve_workload(dev, algo: str = "bsfw", cpu: bool = True):
+    """Config 1 SFW / BSFW end to end (64^3 f64) on the reference-generated
     observation in tests/golden/config1.npz (the GPU parity test compares the
-    result with the reference's own solve of it)."""
+    BSFW result with the reference's own solve of it). cpu_baseline: the
+    oracle's restatement of the reference solver (oracle.solve, pinned to the
+    reference's cfg1 BSFW result by tests/test_oracle.py) timed on this box's
+    host on the same observation."""
     import paper_2009_05473_b200 as P
     from paper_2009_05473_b200 import solvers
     g = np.load(ROOT / "tests" / "golden" / "config1.npz")
     P.set_precision("f64")
     from paper_2009_05473_b200.configs import box_psf_kernel
     dims = (64, 64, 64)
-    psf = P.Psf(P.Volume(box_psf_kernel(dims, (2, 2, 2), (7, 7, 7))), normalize=False)
+    kernel = box_psf_kernel(dims, (2, 2, 2), (7, 7, 7))
+    psf = P.Psf(P.Volume(kernel), normalize=False)
     bounds = P.DomainBounds((8.0,) * 3, (56.0,) * 3, 1.5, 3.0, 1.5, 2.5)
     sg, dg = np.array([1.5, 2.0, 2.5, 3.0]), np.array([1.5, 2.0, 2.5])
     orig = solvers.make_parameter_grids
     solvers.make_parameter_grids = lambda b, ns, nd: (sg, dg)
+    run = getattr(P, algo)
     try:
         y = P.Volume(g["y"])
         opts = P.SolverOptions(lam=float(g["lam"]), max_outer_iterations=20)
-        P.bsfw(y, psf, opts, bounds)  # warm-up (as experiment.py:487-492 does)
+        run(y, psf, opts, bounds)  # warm-up (as experiment.py:487-492 does)
         t0 = time.perf_counter()
-        res = P.bsfw(P.Volume(g["y"]), psf, opts, bounds)
+        res = run(P.Volume(g["y"]), psf, opts, bounds)
         t = time.perf_counter() - t0
     finally:
         solvers.make_parameter_grids = orig
-    rows = res.measure.to_rows()
-    ref = g["rows"]
-    return {"metric": "BSFW solve time, config 1 (64^3 f64, N=5, 12 candidates)",
-            "value": t, "unit": "s", "higher_is_better": False,
-            "outer_iterations": len(res.trace.records), "atoms": len(res.measure),
-            "criterion": res.criterion, "reference_atoms": int(ref.shape[0]),
-            "reference_criterion": float(g["C"]),
-            "reference_cpu_s": float(g["t_total"]),
-            "reference_cpu_note": "sfw3d 0.1.0 bsfw on the same observation, timed in the build "
-                                  "container (8-core VM) when the golden was generated",
-            "split_s": {"certificate": res.trace.step_time("certificate"),
-                        "lasso": res.trace.step_time("lasso"),
-                        "descent": res.trace.step_time("descent"),
-                        "table": res.trace.t_table}}
+    out = {"metric": f"{algo.upper()} solve time, config 1 (64^3 f64, N=5, 12 candidates)",
+           "value": t, "unit": "s", "higher_is_better": False,
+           "outer_iterations": len(res.trace.records), "atoms": len(res.measure),
+           "criterion": res.criterion, "termination": res.termination,
+           "split_s": {"certificate": res.trace.step_time("certificate"),
+                       "lasso": res.trace.step_time("lasso"),
+                       "descent": res.trace.step_time("descent"),
+                       "table": res.trace.t_table}}
+    if algo == "bsfw":
+        out.update({"reference_atoms": int(g["rows"].shape[0]), "reference_criterion": float(g["C"]),
+                    "reference_cpu_s_build_container": float(g["t_total"])})
+    if cpu:
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import sfw3d_oracle as O
+        box5 = [(8.0, 56.0)] * 3 + [(1.5, 3.0), (1.5, 2.5)]
+        t0 = time.perf_counter()
+        o = O.solve(g["y"], O.psf_hat(kernel), float(g["lam"]), sg, dg, box5, algo,
+                    max_outer_iterations=20)
+        tc = time.perf_counter() - t0
+        out["cpu_baseline"] = {
+            "value": tc, "unit": "s", "cores": 1, "kind": "port",
+            "sample": f"the whole config-1 {algo.upper()} solve on the same observation "
+                      "(oracle.solve: the reference solver restated in numpy/scipy, single "
+                      "thread FFTs as in the reference)",
+            "atoms": int(o["rows"].shape[0]), "criterion": o["criterion"],
+            "termination": o["termination"]}
+        out["speedup_vs_cpu"] = tc / t
+    return out
 
 
-def solve_cfg3_workload():
-    """Config 3 BSFW end to end (256^3 fp32 storage, N=100 atoms, 8 x 6
-    candidates) on the frozen synthetic recipe (tools/run_solve.py); the
-    reference does not finish this config on CPU."""
+def solve_recipe_workload(config: int, algo: str):
+    """BASELINE config 2 / 3 SFW or BSFW end to end on the frozen synthetic
+    recipe (tools/run_solve.py); the reference does not finish these on CPU
+    (SURVEY §6), so there is no CPU arm."""
     sys.path.insert(0, str(ROOT / "tools"))
     import run_solve
-    r = run_solve.run(3)
-    return {"metric": "BSFW solve time, config 3 (256^3 fp32, N=100, 48 candidates)",
+    r = run_solve.run(config, algo)
+    desc = {2: "128^3 f64, N=20, 30 candidates", 3: "256^3 fp32, N=100, 48 candidates"}[config]
+    return {"metric": f"{algo.upper()} solve time, config {config} ({desc})",
             "value": r["solve_s"], "unit": "s", "higher_is_better": False,
             **{k: r[k] for k in ("outer_iterations", "atoms", "termination", "criterion",
                                  "truth_atoms", "truth_matched_within_2vox", "split_s",
@@ -573,8 +595,16 @@ def main():
             secondary.append(cg)
     if rank == 0 and not args.no_secondary:
         secondary.append(costgrad_workload(args, dev))
-        secondary.append(solve_workload(dev))
-        secondary.append(solve_cfg3_workload())
+        cpu_solve = not args.no_cpu_baseline
+        s1b = solve_workload(dev, "bsfw", cpu_solve)
+        s1s = solve_workload(dev, "sfw", cpu_solve and not args.no_cpu_sfw)
+        s1b["bsfw_over_sfw_time"] = s1b["value"] / s1s["value"]
+        if "cpu_baseline" in s1s:
+            s1b["cpu_bsfw_over_sfw_time"] = s1b["cpu_baseline"]["value"] / s1s["cpu_baseline"]["value"]
+        secondary += [s1b, s1s]
+        s2b, s2s = solve_recipe_workload(2, "bsfw"), solve_recipe_workload(2, "sfw")
+        s2b["bsfw_over_sfw_time"] = s2b["value"] / s2s["value"]
+        secondary += [s2b, s2s, solve_recipe_workload(3, "bsfw")]
     cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # the reference algorithm (oracle FFT eta_field) on the SAME host

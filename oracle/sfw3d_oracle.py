@@ -398,6 +398,95 @@ def residual(y, weights, phis) -> np.ndarray:
 
 
 # --------------------------------------------------------------------------
+# outer loop: SFW / boosted SFW                     (solvers.py:286-405)
+# --------------------------------------------------------------------------
+
+def solve(y, kernel_hat, lam, sigma_grid, shape_grid, box5, algorithm="bsfw",
+          max_outer_iterations=50, eta_threshold=1.0, eta_slack=5e-3, lasso_tol=1e-6,
+          lasso_max_iter=2000, descent_gtol=1e-6, descent_ftol=1e-10, descent_max_iter=400,
+          prune_rel_tol=1e-10, duplicate_tol=1e-6):
+    """solvers.py:286-395 restated on the oracle's numpy kernels: per outer
+    iteration the certificate (FFT eta over the template spectra in the
+    position window + L-BFGS-B refine), the duplicate guard, the weight step
+    (Gram + cyclic CD with the warm start), the SFW descent after every atom
+    or the BSFW final slide with its re-check, the relative prune and the
+    stall rule. box5 = [(lo, hi)] for (m_x, m_y, m_z, sigma, d). Returns
+    dict(rows (k, 6), criterion, termination, eta (per iteration), atoms
+    (per iteration))."""
+    dims = y.shape
+    hats = template_hats(kernel_hat, dims, sigma_grid, shape_grid)
+    sg, dg = np.sort(np.asarray(sigma_grid, float)), np.sort(np.asarray(shape_grid, float))
+    window = position_window(dims, [b[0] for b in box5[:3]], [b[1] for b in box5[:3]])
+    stop_at = eta_threshold + eta_slack
+    thetas, weights, phis = [], np.zeros(0), []
+    crit = 0.5 * float(np.vdot(y, y).real)
+    term, dup_streak = "iteration_cap", 0
+    etas, counts = [], []
+
+    def cert(thetas_, weights_, phis_):
+        r = residual(y, weights_, phis_)
+        pos, flat, _, _, _ = eta_field(r, lam, hats, len(dg), window)
+        i, j = divmod(flat, len(dg))
+        return refine_eta_max(corr(r, kernel_hat), lam, np.array([*pos, sg[i], dg[j]], float), box5)
+
+    def lasso_crit(weights_, phis_):
+        r = residual(y, weights_, phis_)
+        return 0.5 * float(np.vdot(r, r).real) + lam * float(np.sum(weights_))
+
+    def prune(thetas_, weights_, phis_):
+        tol = prune_rel_tol * float(np.max(weights_)) if len(weights_) else 0.0
+        keep = [i for i, w in enumerate(weights_) if w > tol]
+        return [thetas_[i] for i in keep], weights_[keep], [phis_[i] for i in keep]
+
+    for k in range(1, max_outer_iterations + 1):
+        c_before = crit
+        theta, eta = cert(thetas, weights, phis)
+        etas.append(eta)
+        if eta <= stop_at:
+            term = "certificate"
+            if algorithm == "bsfw" and thetas:
+                rows0 = np.column_stack([weights, np.array(thetas)])
+                slid, c_desc = local_descent(y, rows0, kernel_hat, lam, box5, descent_gtol,
+                                             descent_ftol, descent_max_iter)
+                st = [list(r[1:]) for r in slid]
+                sp = [phi(t, kernel_hat, dims) for t in st]
+                st, sw, sp = prune(st, slid[:, 0].copy(), sp)
+                _, eta_slid = cert(st, sw, sp)
+                if c_desc <= crit and eta_slid <= stop_at:
+                    thetas, weights, phis, crit = st, sw, sp, c_desc
+            counts.append(len(thetas))
+            break
+        duplicate = any(np.max(np.abs(np.asarray(theta) - np.asarray(t))) <= duplicate_tol
+                        for t in thetas)
+        thetas.append(list(theta))
+        phis.append(phi(theta, kernel_hat, dims))
+        w_init = np.append(weights, 0.0)
+        gram, b = gram_system(np.stack(phis), y)
+        weights, _, _ = cd_solve(gram, b, lam, w_init, lasso_tol, lasso_max_iter)
+        crit = lasso_crit(weights, phis)
+        if algorithm == "sfw":
+            rows0 = np.column_stack([weights, np.array(thetas)])
+            slid, crit = local_descent(y, rows0, kernel_hat, lam, box5, descent_gtol,
+                                       descent_ftol, descent_max_iter)
+            thetas = [list(r[1:]) for r in slid]
+            weights = slid[:, 0].copy()
+            phis = [phi(t, kernel_hat, dims) for t in thetas]
+        thetas, weights, phis = prune(thetas, weights, phis)
+        counts.append(len(thetas))
+        if duplicate and crit >= c_before * (1.0 - 1e-12):
+            dup_streak += 1
+            if dup_streak >= 2:
+                term = "stalled_duplicate_atom"
+                break
+        else:
+            dup_streak = 0
+    rows = np.column_stack([weights, np.array(thetas).reshape(-1, 5)]) if thetas else np.zeros((0, 6))
+    tol = prune_rel_tol * float(np.max(weights)) if len(weights) else 0.0
+    rows = rows[rows[:, 0] > tol]
+    return {"rows": rows, "criterion": crit, "termination": term, "eta": etas, "atoms": counts}
+
+
+# --------------------------------------------------------------------------
 # synthetic configs (SURVEY Appendix A; BASELINE.json configs)
 # --------------------------------------------------------------------------
 

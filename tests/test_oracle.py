@@ -100,3 +100,24 @@ def test_support_and_axis_box():
     idx, off = O.axis_box(8, 0.25, 10)
     assert list(idx) == list(range(8))
     assert off.min() >= -4.0 and off.max() < 4.0
+
+
+def test_oracle_bsfw_matches_reference_config1(golden):
+    """The oracle's outer loop (solve, solvers.py:286-405) reproduces the
+    reference's own config-1 BSFW solve (tests/golden/config1.npz): same
+    termination, atom count and criterion; atoms within 1e-6 voxel and 1e-6
+    relative (measured ~1e-9)."""
+    g = golden("config1")
+    dims = (64, 64, 64)
+    k = O.box_gaussian_psf(dims, (2, 2, 2), (7, 7, 7))
+    box5 = [(8.0, 56.0)] * 3 + [(1.5, 3.0), (1.5, 2.5)]
+    r = O.solve(g["y"], O.psf_hat(k), float(g["lam"]), [1.5, 2, 2.5, 3], [1.5, 2, 2.5], box5,
+                "bsfw", max_outer_iterations=20)
+    ref = g["rows"]
+    assert r["termination"] == str(g["term"]) and r["rows"].shape == ref.shape
+    assert abs(r["criterion"] - float(g["C"])) <= 1e-9 * abs(float(g["C"]))
+    np.testing.assert_allclose(r["eta"], g["eta"], rtol=1e-6)
+    for q in ref:
+        j = int(np.argmin(np.linalg.norm(r["rows"][:, 1:4] - q[1:4], axis=1)))
+        assert np.linalg.norm(r["rows"][j, 1:4] - q[1:4]) < 1e-6
+        np.testing.assert_allclose(r["rows"][j, [0, 4, 5]], q[[0, 4, 5]], rtol=1e-6)
