@@ -237,30 +237,33 @@ def cert_workload(args, rank, world, dev):
     n = dims[0]
     ctx = N.context(dev)
     stream = torch.cuda.current_stream(dev)
-    if world > 1:
-        # x-slab per rank on its own sub-volume (slab + halo planes): no
-        # collective inside the step, one 24-byte record all-gather after it
+    sharded = world > 1 or ONE_RANK is not None
+    if sharded:
+        # x-slab per rank: the residual lives on the rank's own planes only;
+        # b and every basis term's x pass exchange their halos with the ring
+        # neighbours (NCCL P2P in-stream, distributed.TorchComm), per-candidate
+        # records all-gathered (--one-rank: SoloComm, this rank alone)
         from paper_2009_05473_b200 import distributed as D
         x0, x1 = D.slab_bounds(n, world, rank)
-        slab = D.SlabCertificate(psf, inst.sigma_grid, inst.shape_grid, dims, x0, x1,
-                                 tap_tol=args.tap_tol, mode=args.mode)
-        table, info = slab.table, slab.table.info()
-        work = slab.subvolume(residual)
+        comm = D.SoloComm(rank, world) if ONE_RANK else D.TorchComm()
+        slab = D.SlabCertificate(table, x0, x1, comm)
+        work = slab.owned(residual)
         del residual
-        wdims = slab.local_dims
-        off = x0 - slab.halo
-        window = ((slab.halo, slab.halo + x1 - x0), (0, dims[1] - 1), (0, dims[2] - 1))
-    else:
-        work, wdims, off = residual, dims, 0
+        wdims = (x1 - x0 + 1, dims[1], dims[2])
         window = ((0, n - 1), (0, dims[1] - 1), (0, dims[2] - 1))
-    x0, x1 = window[0][0], window[0][1]
 
-    def step():
-        return eta_argmax_dev(work, 1.0, table, window)[0]
+        def step():
+            return slab.argmax(work, 1.0, window)
+    else:
+        work, wdims = residual, dims
+        window = ((0, n - 1), (0, dims[1] - 1), (0, dims[2] - 1))
+
+        def step():
+            return eta_argmax_dev(work, 1.0, table, window)
 
     for _ in range(args.warmup):
         step()
-    _, per_cand, _ = eta_argmax_dev(work, 1.0, table, window)
+    per_cand = None if sharded else step()[1]
     if collective(world):
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
@@ -270,27 +273,21 @@ def cert_workload(args, rank, world, dev):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        best = step()
+        out = step()
     e1.record(stream)
     torch.cuda.synchronize(dev)
     launches = ctx.launches - l0
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
-    # global argmax over ranks: all-gather (value, cand, linear index)
-    gx = (best.pos[0] + off) % n  # global x of the rank's winner
-    rec = torch.tensor([best.value, float(best.cand),
-                        float((gx * dims[1] + best.pos[1]) * dims[2] + best.pos[2])],
-                       dtype=torch.float64, device=dev)
     if collective(world):
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-        allrec = [torch.empty_like(rec) for _ in range(world)]
-        torch.distributed.all_gather(allrec, rec)
-        recs = [tuple(r.tolist()) for r in allrec]
+    if sharded:
+        v, c, pos, _ = out
     else:
-        recs = [tuple(rec.tolist())]
-    gbest = sorted(recs, key=lambda r: (-r[0], r[1], r[2]))[0]
+        v, c, pos = float(out[0].value), int(out[0].cand), tuple(int(q) for q in out[0].pos)
+    gbest = (v, c, (pos[0] * dims[1] + pos[1]) * dims[2] + pos[2])
     ms_step = ms / args.steps
     vc_step = int(np.prod(dims)) * info["n_cand"]
     value = vc_step / (ms_step / 1e3)
@@ -306,8 +303,8 @@ def cert_workload(args, rank, world, dev):
     dom = max(fam, key=lambda f: fam[f][0])
     fp32_peak = ctx.probe_fp32()
     hbm_peak = peaks()["hbm_gbs"]
-    win_vox = (x1 - x0 + 1) * dims[1] * dims[2]
-    nvox = int(np.prod(wdims))  # the volume this rank's kernels sweep
+    nvox = int(np.prod(wdims))  # the volume this rank's kernels sweep (its own planes)
+    win_vox = nvox
     rooflines = {}
     if fam["eta_direct"][1]:
         flops = info["direct_flops_per_voxel"] * win_vox  # executed FP32 ops (FMA = 2)
@@ -391,7 +388,10 @@ def cert_workload(args, rank, world, dev):
             if i + 1 < steps:
                 upload(i + 1)
             stream.wait_event(copied[i % 2])
-            eta_argmax_dev(bufs[i % 2], 1.0, table, window)  # returns after the records' D2H
+            if sharded:
+                slab.argmax(bufs[i % 2], 1.0, window)
+            else:
+                eta_argmax_dev(bufs[i % 2], 1.0, table, window)  # returns after the records' D2H
             done[i % 2].record(stream)
 
     for d in done:
@@ -417,9 +417,9 @@ def cert_workload(args, rank, world, dev):
         "roofline": roof, "e2e": e2e, "kernel_ms": {k: v[0] for k, v in fam.items() if v[1]},
         "table": info, "best": {"eta": gbest[0], "cand": int(gbest[1]), "lin": int(gbest[2]),
                                 "pos": [int(q) for q in np.unravel_index(int(gbest[2]), dims)]},
-        "halo": slab.halo if world > 1 else 0, "host_residual": host_residual,
+        "halo": ("exchanged per x pass" if sharded else 0), "host_residual": host_residual,
         "per_cand": [(tuple(int(q) for q in r.pos), float(r.value)) for r in per_cand]
-        if world == 1 else None,
+        if per_cand is not None else None,
         "refined_voxels": refine_count,
         "inst": inst, "dims": dims,
     }
@@ -642,8 +642,9 @@ def main():
                                    "PSF sigma_h=3 31^3, eta at every voxel + global argmax",
                        "grid": args.n, "candidates": res["table"]["n_cand"],
                        "tap_tol": args.tap_tol, "mode": args.mode,
-                       "parallelism": (f"x-slabs x{world}: each rank's slab + {res['halo']} halo "
-                                       "planes resident, argmax records all-gathered")
+                       "parallelism": (f"x-slabs x{world}: each rank holds its own planes; halos "
+                                       "exchanged (NCCL P2P) before every x pass, refinement "
+                                       "thresholds all-reduced, per-candidate records all-gathered")
                        if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (512 MiB residual, 0.9 GiB padded copy)"},
             "gpu_launches": res["launches"], "clocks": res["clocks"], "roofline": res["roofline"],

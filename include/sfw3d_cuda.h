@@ -144,6 +144,14 @@ int sfw3d_cost_grad_slab(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const 
                          const double* params_host, int k, int gnx, int x0, int x1, int halo,
                          double* half_sumsq_host, double* sums_host);
 
+/* The same with the partials left on the DEVICE, unsynchronised, for an
+ * in-stream all-reduce (NCCL) before the one D2H: partials_dev (1 + 6k
+ * doubles) = [1/2 sum_slab r^2, raw sums row-major]. Non-finite partials are
+ * the caller's check after the reduction. */
+int sfw3d_cost_grad_slab_dev(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* y_dev,
+                             const double* params_host, int k, int gnx, int x0, int x1, int halo,
+                             double* partials_dev);
+
 /* ---- certificate (certificate.py:37-236) ------------------------------ */
 /* K2 — candidate table for the (sigma, d) grid, sigma-major (sorted
  * ascending, as build_template_table sorts them, certificate.py:72-73).
@@ -228,6 +236,35 @@ int sfw3d_eta_argmax(sfw3d_ctx* ctx, const sfw3d_table* t, int dtype,
                      const void* residual_dev, double lam, const int32_t window[6],
                      sfw3d_argmax* best_host, sfw3d_argmax* per_cand_host,
                      void* fields_dev);
+
+/* ---- x-slab data plane (multi-GPU certificate) ---------- */
+/* Halo exchange the library requests between the passes of an x-slab
+ * evaluation. `window` is a device buffer of lo + owned + hi planes of
+ * plane_elems elements (dtype): planes [lo, lo + owned) are this rank's and
+ * hold data; the callee must fill planes [0, lo) with the LEFT neighbour's last
+ * `lo` owned planes and [lo + owned, lo + owned + hi) with the RIGHT
+ * neighbour's first `hi` owned planes (periodic ring of ranks) before any
+ * later work on the context stream reads them (enqueue on / wait from that
+ * stream). Every rank calls it in the same order (collective). 0 = success. */
+typedef int (*sfw3d_halo_fn)(void* user, void* window_dev, int dtype, int owned_planes,
+                             int64_t plane_elems, int lo_planes, int hi_planes);
+/* In-place all-reduce of n host doubles over the ranks: op 0 = sum, 1 = max. */
+typedef int (*sfw3d_allreduce_fn)(void* user, double* values_host, int n, int op);
+
+/* K1 on one rank's x-slab: the rank owns planes [x0, x0 + n_own) of the
+ * periodic residual (residual_dev: those planes only, compact) of the table's
+ * GLOBAL volume. b = H^T r and every shared basis term are computed on the
+ * owned planes with halo exchanges of their x passes (no redundant planes);
+ * refined members re-evaluate exactly on b with a template-radius halo; the
+ * refinement thresholds use the all-reduced |b| statistics and member maxima.
+ * window is in LOCAL coordinates (x in [0, n_own)); the records' positions
+ * are local (global x = x0 + pos[0]); per_cand_host (may be NULL) receives
+ * this slab's per-candidate maxima (-inf where the window misses the slab).
+ * Argmax-only (no fields); every candidate must be a basis member. */
+int sfw3d_eta_argmax_slab(sfw3d_ctx* ctx, const sfw3d_table* t, int dtype,
+                          const void* residual_dev, int n_own, int x0, double lam,
+                          const int32_t window[6], sfw3d_halo_fn halo, sfw3d_allreduce_fn allreduce,
+                          void* user, sfw3d_argmax* best_host, sfw3d_argmax* per_cand_host);
 
 /* ---- non-negative LASSO (solvers.py:111-180, 253-266) ----------------- */
 /* K8 — out_host[i] = < vecs[i], v > over n elements, fp64 accumulation,

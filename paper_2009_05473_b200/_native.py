@@ -31,7 +31,8 @@ EXPORTS = (
     "sfw3d_table_destroy", "sfw3d_eta_argmax", "sfw3d_dots", "sfw3d_nnlasso_cd", "sfw3d_nnlasso_qp",
     "sfw3d_residual", "sfw3d_ctx_profile", "sfw3d_ctx_profile_read", "sfw3d_probe_fp32",
     "sfw3d_table_candidate", "sfw3d_basis_fit", "sfw3d_basis_set_fit",
-    "sfw3d_last_refine_count", "sfw3d_table_set_option",
+    "sfw3d_last_refine_count", "sfw3d_table_set_option", "sfw3d_eta_argmax_slab",
+    "sfw3d_cost_grad_slab_dev",
 )
 
 
@@ -43,6 +44,11 @@ _vp = C.c_void_p
 _ip = C.POINTER(C.c_int)
 _i32p = C.POINTER(C.c_int32)
 _dp = C.POINTER(C.c_double)
+
+# x-slab data plane callbacks (include/sfw3d_cuda.h: sfw3d_halo_fn, sfw3d_allreduce_fn)
+HALO_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_int,
+                      C.c_int)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int, C.c_int)
 
 _SIGNATURES = {
     "sfw3d_abi_version": (C.c_int, []),
@@ -62,6 +68,8 @@ _SIGNATURES = {
     "sfw3d_cost_grad": (C.c_int, [_vp, _vp, C.c_int, _vp, _dp, C.c_int, C.c_double, _dp, _dp, _vp]),
     "sfw3d_cost_grad_slab": (C.c_int, [_vp, _vp, C.c_int, _vp, _dp, C.c_int, C.c_int, C.c_int, C.c_int,
                                        C.c_int, _dp, _dp]),
+    "sfw3d_cost_grad_slab_dev": (C.c_int, [_vp, _vp, C.c_int, _vp, _dp, C.c_int, C.c_int, C.c_int,
+                                           C.c_int, C.c_int, _vp]),
     "sfw3d_table_create": (C.c_int, [_vp, _vp, C.c_int, _dp, C.c_int, _dp, C.c_double, C.c_int,
                                      C.c_double, C.POINTER(_vp)]),
     "sfw3d_table_info": (C.c_int, [_vp, C.c_int, _ip, _ip, _ip, C.POINTER(C.c_int64),
@@ -72,6 +80,9 @@ _SIGNATURES = {
     "sfw3d_table_set_option": (C.c_int, [_vp, C.c_char_p, C.c_double]),
     "sfw3d_eta_argmax": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_double, _i32p, C.POINTER(Argmax),
                                    C.POINTER(Argmax), _vp]),
+    "sfw3d_eta_argmax_slab": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int, C.c_int, C.c_double, _i32p,
+                                        HALO_FN, ALLREDUCE_FN, _vp, C.POINTER(Argmax),
+                                        C.POINTER(Argmax)]),
     "sfw3d_dots": (C.c_int, [_vp, C.c_int, C.c_int64, C.POINTER(_vp), C.c_int, _vp, _dp]),
     "sfw3d_nnlasso_cd": (C.c_int, [_vp, C.c_int, _dp, _dp, C.c_double, C.c_double, C.c_int, _dp,
                                    _i32p, _dp]),

@@ -477,10 +477,48 @@ extern "C" int sfw3d_cost_grad(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, 
 // on the window only. The residual is formed on the slab planes and zeroed
 // elsewhere, so back = H^T (r 1_slab): summed over ranks, the raw sums and
 // 1/2 ||r||^2 are exactly the single-volume ones (up to summation order).
+namespace sfw3d {
+// out[0] = 1/2 res[0]; out[1 + 6i + c] = sum of atom i's pieces' res[1 + 6q + c]
+// (pieces of one atom are consecutive, in image order)
+__global__ void piece_combine_kernel(const int* __restrict__ first, int k,
+                                     const double* __restrict__ res, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > 6 * k) return;
+  if (i == 0) {
+    out[0] = 0.5 * res[0];
+    return;
+  }
+  const int atom = (i - 1) / 6, c = (i - 1) % 6;
+  double x = 0.0;
+  for (int q = first[atom]; q < first[atom + 1]; ++q) x += res[1 + 6 * q + c];
+  out[i] = x;
+}
+}  // namespace sfw3d
+
+static int cost_grad_slab_impl(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* y_dev,
+                               const double* params_host, int k, int gnx, int x0, int x1, int halo,
+                               double* half_sumsq_host, double* sums_host, double* partials_dev);
+
 extern "C" int sfw3d_cost_grad_slab(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* y_dev,
                                     const double* params_host, int k, int gnx, int x0, int x1,
                                     int halo, double* half_sumsq_host, double* sums_host) {
-  SFW3D_CHECK_ARG(ctx && psf && y_dev && half_sumsq_host && sums_host, "NULL argument");
+  SFW3D_CHECK_ARG(half_sumsq_host && sums_host, "NULL argument");
+  return cost_grad_slab_impl(ctx, psf, dtype, y_dev, params_host, k, gnx, x0, x1, halo,
+                             half_sumsq_host, sums_host, nullptr);
+}
+
+extern "C" int sfw3d_cost_grad_slab_dev(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype,
+                                        const void* y_dev, const double* params_host, int k,
+                                        int gnx, int x0, int x1, int halo, double* partials_dev) {
+  SFW3D_CHECK_ARG(partials_dev, "NULL argument");
+  return cost_grad_slab_impl(ctx, psf, dtype, y_dev, params_host, k, gnx, x0, x1, halo, nullptr,
+                             nullptr, partials_dev);
+}
+
+static int cost_grad_slab_impl(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* y_dev,
+                               const double* params_host, int k, int gnx, int x0, int x1, int halo,
+                               double* half_sumsq_host, double* sums_host, double* partials_dev) {
+  SFW3D_CHECK_ARG(ctx && psf && y_dev, "NULL argument");
   SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
   SFW3D_CHECK_ARG(k >= 0 && (k == 0 || params_host), "params");
   const int* dims = psf->dims;
@@ -542,6 +580,20 @@ extern "C" int sfw3d_cost_grad_slab(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dt
                             static_cast<const char*>(y_dev) + off, A + off, partials, res));
   SFW3D_TRY(psf_apply_impl(ctx, psf, dtype, A, B, 1, A));
   SFW3D_TRY(atom_sums_impl(ctx, dtype, dims, B, pieces, ad, res + 1));
+  if (partials_dev) {  // device output for an in-stream all-reduce: no sync here
+    std::vector<int> first(k + 1, 0);
+    for (int q = 0, i = 0; i <= k; ++i) {
+      while (q < kp && owner[q] < i) ++q;
+      first[i] = q;
+    }
+    SFW3D_TRY(ensure_device(ctx, ctx->ws_aux, first.size() * sizeof(int)));
+    int* first_dev = static_cast<int*>(ctx->ws_aux.ptr);
+    SFW3D_TRY(stage_upload(ctx, first_dev, first.data(), first.size() * sizeof(int)));
+    piece_combine_kernel<<<(6 * k + 1 + 255) / 256, 256, 0, ctx->stream>>>(first_dev, k, res,
+                                                                          partials_dev);
+    SFW3D_LAUNCH_CHECK(ctx);
+    return SFW3D_OK;
+  }
   std::vector<double> host(size_t(kp) * 6 + 1);
   SFW3D_TRY(download_sync(ctx, host.data(), res, host.size() * sizeof(double)));
   *half_sumsq_host = 0.5 * host[0];

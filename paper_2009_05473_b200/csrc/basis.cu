@@ -1776,9 +1776,17 @@ static int launch_mix(sfw3d_ctx* ctx, int nblocks, const void* b, const void* te
 #undef SFW3D_MIX
 }
 
+int basis_set_max_xhalo(const BasisSet* s) {
+  int h = 0;
+  if (!s) return 0;
+  for (size_t t = 0; t < s->betas.size(); ++t)
+    h = std::max({h, -s->tlo[0][t], s->tlo[0][t] + s->tlen[0][t] - 1});
+  return h;
+}
+
 int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[3], const void* b,
                    double lam, const int32_t win[6], void* fields, Best* best_dev, void* scratch,
-                   double* abs_dev, bool* abs_done) {
+                   double* abs_dev, bool* abs_done, const SlabEval* se) {
   if (abs_done) *abs_done = false;
   const int nm = fields ? s->n_nnls : int(s->members.size()), nt = int(s->betas.size());
   if (nm == 0) return SFW3D_OK;
@@ -1803,6 +1811,13 @@ int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[
     const char* tp = static_cast<const char*>(s->taps[t]);
     const int l0 = s->tlen[0][t], l1 = s->tlen[1][t], l2 = s->tlen[2][t];
     const void* src = s->parent[t] < 0 ? b : terms + size_t(s->parent[t]) * n * es;
+    if (se) {  // x-slab: plane-local z/y passes, halo exchange, windowed x pass
+      const void* tps[3] = {tp, tp + es * l0, tp + es * (l0 + l1)};
+      const int lo[3] = {s->tlo[0][t], s->tlo[1][t], s->tlo[2][t]}, ln[3] = {l0, l1, l2};
+      SFW3D_TRY(slab_corr_impl(ctx, dtype, src, terms + size_t(t) * n * es, dims, tps, lo, ln,
+                               se->win, se->H, t1, se->link, "eta_basis"));
+      continue;
+    }
     SFW3D_TRY(corr_pass_impl(ctx, dtype, src, t1, dims, 2, tp + es * (l0 + l1), s->tlo[2][t], l2,
                              nullptr, 0.0, 1.0, "eta_basis"));
     SFW3D_TRY(corr_pass_impl(ctx, dtype, t1, t2, dims, 1, tp + es * l0, s->tlo[1][t], l1,

@@ -78,9 +78,19 @@ size_t basis_set_scratch(const BasisSet* s, long long n, int dtype, const int di
 // (then the signed members are skipped: their values are not certified).
 // abs_dev (optional, device [2]): receives [sum |b|, max |b|] when the mix
 // computed them on the way (*abs_done = true), saving a separate pass over b.
+// x-slab evaluation (sfw3d_eta_argmax_slab): dims are the OWNED planes, every
+// term's x pass runs through slab_corr_impl (window `win` of H + owned + H
+// planes, H >= basis_set_max_xhalo, exchanged through `link`).
+struct SlabEval {
+  SlabLink link;
+  void* win = nullptr;
+  int H = 0;
+};
+int basis_set_max_xhalo(const BasisSet* s);
 int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[3], const void* b,
                    double lam, const int32_t win[6], void* fields, Best* best_dev, void* scratch,
-                   double* abs_dev = nullptr, bool* abs_done = nullptr);
+                   double* abs_dev = nullptr, bool* abs_done = nullptr,
+                   const SlabEval* se = nullptr);
 
 // Refinement support (inexact / signed members): re-runs the fused mix over
 // the terms basis_set_eval left in `scratch` (same `fields` flag; only the

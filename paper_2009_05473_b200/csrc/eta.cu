@@ -491,14 +491,16 @@ __global__ void abs_parts_reduce_kernel(const double* __restrict__ parts, int nb
 // 171^2 rows).
 template <typename T>
 __global__ void __launch_bounds__(256) refine_kernel(const T* __restrict__ b, int nx, int ny,
-                                                     int nz, const RefCand* __restrict__ rc,
+                                                     int nz, int xoff,
+                                                     const RefCand* __restrict__ rc,
                                                      const int* __restrict__ item_cand,
                                                      const long long* __restrict__ item_idx,
                                                      double* __restrict__ part) {
   __shared__ double red[8];
   const RefCand c = rc[item_cand[blockIdx.x]];
   const long long lin = item_idx[blockIdx.x];
-  const int z = int(lin % nz), y = int((lin / nz) % ny), x = int(lin / ((long long)ny * nz));
+  // (x-slab: b is the owned planes' window, item x shifted by its halo xoff)
+  const int z = int(lin % nz), y = int((lin / nz) % ny), x = int(lin / ((long long)ny * nz)) + xoff;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nrows = c.la * c.lb, S = int(gridDim.y);
   const int r0 = int((long long)nrows * blockIdx.y / S), r1 = int((long long)nrows * (blockIdx.y + 1) / S);
@@ -958,12 +960,23 @@ int& last_refine_count() {
   return c;
 }
 
+// x-slab evaluation (sfw3d_eta_argmax_slab): the owned planes and the link
+struct SlabArgs {
+  SlabLink link;
+  int n_own;
+};
+
 template <typename T>
 int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double lam,
               const int32_t win[6], sfw3d_argmax* best_host, sfw3d_argmax* per_cand_host,
-              void* fields) {
+              void* fields, const SlabArgs* sl = nullptr) {
   const int dtype = sizeof(T) == 8 ? SFW3D_F64 : SFW3D_F32;
-  const int* dims = t->dims;
+  // evaluation grid: the whole volume, or this rank's owned x-planes
+  const int ldims[3] = {sl ? sl->n_own : t->dims[0], t->dims[1], t->dims[2]};
+  const int* dims = ldims;
+  // local padded geometry for the direct / refinement kernels: on a slab the
+  // x padding comes from the neighbours (halo exchange), not from wrapping
+  const int pdims0 = sl ? ldims[0] + 2 * t->pad[0] : t->pdims[0];
   const int64_t n = vol_count(dims);
   const size_t vb = size_t(n) * sizeof(T);
   const int nc = int(t->cands.size());
@@ -981,7 +994,7 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   const size_t sb = any_basis ? basis_set_scratch(bset, n, dtype, dims) : 0;
   // the padded copy of b feeds the direct kernels only (refinement may fall
   // back to them: the copy is then made on demand)
-  const size_t pbytes = size_t(t->pdims[0]) * t->pdims[1] * t->pdims[2] * sizeof(T);
+  const size_t pbytes = size_t(pdims0) * t->pdims[1] * t->pdims[2] * sizeof(T);
   const size_t pb = (any_direct || any_refine) ? pbytes : 0;
   // refinement items per call (a table option: tests shrink it)
   const int kRefCap = t->refine_cap;
@@ -1010,9 +1023,21 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
                             ((ow[5] - zbase + 1 + tzf - 1) / tzf) * nxp;
     ab = size_t(nctas) * fold_kj_rt(sizeof(T)) * kThreads * sizeof(T);
   }
+  // x-slab window buffer: H + owned + H planes, H covering the PSF, every
+  // basis term's x pass and the templates' x radius (refinement / direct)
+  int H = 0;
+  if (sl) {
+    H = std::max({-t->psf->lo[0], t->psf->hi[0], basis_set_max_xhalo(bset), t->pad[0]});
+    if (H > ldims[0]) {
+      set_error("x-slab thinner than its halo (" + std::to_string(H) +
+                " planes): use fewer ranks or the single-volume path");
+      return SFW3D_EINVAL;
+    }
+  }
+  const size_t wbytes = sl ? size_t(ldims[0] + 2 * H) * t->dims[1] * t->dims[2] * sizeof(T) : 0;
   SFW3D_TRY(ensure_device(ctx, ctx->ws,
                           Carver::need({vb, vb, sb, pb, size_t(nblocks) * sizeof(Best),
-                                        size_t(nc) * sizeof(Best), rb, ab})));
+                                        size_t(nc) * sizeof(Best), rb, ab, wbytes})));
   Carver cv(ctx->ws.ptr);
   T* b = cv.take<T>(n);
   T* tmp = cv.take<T>(n);
@@ -1029,16 +1054,46 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   int* ref_count = any_refine ? cv.take<int>(1 + nc) : nullptr;  // [total, per member]
   std::vector<Best> refined(nc, Best{NAN, -1});  // exact maxima of refined members
   void* accd_g = ab ? cv.take<char>(ab) : nullptr;
+  T* wbuf = sl ? cv.take<T>(wbytes / sizeof(T)) : nullptr;
+  // (zeroed once per call: the x passes' padded zero taps also read a few
+  // planes past the exchanged halos, which must hold finite values)
+  if (sl) SFW3D_CUDA_TRY(cudaMemsetAsync(wbuf, 0, wbytes, ctx->stream));
+  const long long plane = (long long)dims[1] * dims[2];
   // b = H^T * r (tmp is pass scratch), then the periodic padding for direct
-  SFW3D_TRY(psf_apply_impl(ctx, t->psf, dtype, residual, b, 1, tmp));
+  if (sl)
+    SFW3D_TRY(psf_apply_slab(ctx, t->psf, dtype, residual, b, 1, ldims, wbuf, H, tmp, sl->link));
+  else
+    SFW3D_TRY(psf_apply_impl(ctx, t->psf, dtype, residual, b, 1, tmp));
+  // x-slab: b on the owned planes + the template radius of neighbour planes
+  // (refinement and direct kernels read the template box around a voxel)
+  const int px = t->pad[0];
+  bool bwin_ready = false;
+  auto make_bwin = [&]() -> int {
+    if (!sl || bwin_ready) return SFW3D_OK;
+    T* mid = wbuf + size_t(H) * plane;
+    SFW3D_CUDA_TRY(cudaMemcpyAsync(mid, b, vb, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (sl->link.halo(sl->link.user, mid - size_t(px) * plane, dtype, dims[0], plane, px, px) != 0) {
+      set_error("halo exchange callback failed");
+      return SFW3D_ECUDA;
+    }
+    bwin_ready = true;
+    return SFW3D_OK;
+  };
+  const T* bref = sl ? wbuf + size_t(H - px) * plane : b;  // refinement's view of b
   bool padded = false;
   auto make_pad = [&]() -> int {
     if (padded || !bpad) return SFW3D_OK;
+    SFW3D_TRY(make_bwin());
     SFW3D_PROF(ctx, "pad");
-    const long long np = (long long)t->pdims[0] * t->pdims[1] * t->pdims[2];
-    pad_kernel<T><<<unsigned((np + 255) / 256), 256, 0, ctx->stream>>>(
-        b, bpad, dims[0], dims[1], dims[2], t->pad[0], t->pad[1], t->pad[2], t->pdims[0],
-        t->pdims[1], t->pdims[2]);
+    const long long np = (long long)pdims0 * t->pdims[1] * t->pdims[2];
+    if (sl)  // the window already holds the x padding: pad y and z only
+      pad_kernel<T><<<unsigned((np + 255) / 256), 256, 0, ctx->stream>>>(
+          bref, bpad, pdims0, dims[1], dims[2], 0, t->pad[1], t->pad[2], pdims0, t->pdims[1],
+          t->pdims[2]);
+    else
+      pad_kernel<T><<<unsigned((np + 255) / 256), 256, 0, ctx->stream>>>(
+          b, bpad, dims[0], dims[1], dims[2], t->pad[0], t->pad[1], t->pad[2], t->pdims[0],
+          t->pdims[1], t->pdims[2]);
     SFW3D_LAUNCH_CHECK(ctx);
     padded = true;
     return SFW3D_OK;
@@ -1062,9 +1117,15 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   // every basis member at once: shared separable terms + fused mix/argmax,
   // writing cbest[cand] (and the member fields) directly
   bool abs_done = false;
+  SlabEval se;
+  if (sl) {
+    se.link = sl->link;
+    se.win = wbuf;
+    se.H = H;
+  }
   if (any_basis)
     SFW3D_TRY(basis_set_eval(ctx, bset, dtype, dims, b, lam, win, fields, cbest, bscratch,
-                             any_refine ? ref_l1 : nullptr, &abs_done));
+                             any_refine ? ref_l1 : nullptr, &abs_done, sl ? &se : nullptr));
   if (any_refine) {
     // Every refined member's approximate eta~ is within E_c of its direct
     // value at every voxel: signed members E_c = ebound_c ||b||_inf / lam
@@ -1082,6 +1143,21 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
     double l1[2] = {0.0, 0.0};
     SFW3D_TRY(download_sync(ctx, hb0.data(), cbest, size_t(nc) * sizeof(Best)));
     SFW3D_TRY(download_sync(ctx, l1, ref_l1, 2 * sizeof(double)));
+    if (sl) {
+      // the bounds use the GLOBAL |b| statistics and member maxima (the
+      // single-volume thresholds): all-reduce them over the ranks
+      std::vector<double> mx(nc + 1);
+      for (int ci = 0; ci < nc; ++ci) mx[ci] = std::isfinite(hb0[ci].v) ? hb0[ci].v : -1e308;
+      mx[nc] = l1[1];
+      if (sl->link.allreduce(sl->link.user, l1, 1, 0) != 0 ||
+          sl->link.allreduce(sl->link.user, mx.data(), nc + 1, 1) != 0) {
+        set_error("all-reduce callback failed");
+        return SFW3D_ECUDA;
+      }
+      for (int ci = 0; ci < nc; ++ci)
+        if (std::isfinite(hb0[ci].v)) hb0[ci].v = mx[ci];
+      l1[1] = mx[nc];
+    }
     const int nm = basis_set_n_members(bset);
     std::vector<double> thr(nm, INFINITY);
     for (int m = 0; m < nm; ++m) {
@@ -1133,9 +1209,10 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
       SFW3D_PROF(ctx, "eta_refine");
       // shares per item: ~4096 CTAs in all, at most 64 per item
       const int S = std::max(1, std::min(64, kRefPart / count));
+      SFW3D_TRY(make_bwin());
       refine_kernel<T><<<dim3(unsigned(count), unsigned(S)), 256, 0, ctx->stream>>>(
-          b, dims[0], dims[1], dims[2], static_cast<const RefCand*>(t->refcand_dev), ref_cand,
-          ref_idx, ref_part);
+          bref, sl ? pdims0 : dims[0], dims[1], dims[2], sl ? px : 0,
+          static_cast<const RefCand*>(t->refcand_dev), ref_cand, ref_idx, ref_part);
       SFW3D_LAUNCH_CHECK(ctx);
       refine_combine_kernel<<<(count + 255) / 256, 256, 0, ctx->stream>>>(ref_part, S, count, lam,
                                                                           ref_val);
@@ -1155,7 +1232,14 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
     // (a refined member always collects its own approximate maximum; if not,
     // evaluate it directly rather than report an uncertified value)
     for (int ci = 0; ci < nc; ++ci)
-      if (use_refine(t, ci, dtype, fl) && !direct[ci] && std::isnan(refined[ci].v)) direct[ci] = 1;
+      if (use_refine(t, ci, dtype, fl) && !direct[ci] && std::isnan(refined[ci].v)) {
+        // x-slab: thresholds are the GLOBAL ones, so a member with nothing
+        // collected here cannot hold its global maximum on this slab
+        if (sl)
+          refined[ci] = {-INFINITY, 0x7fffffffffffffffLL};
+        else
+          direct[ci] = 1;
+      }
   }
   for (int ci = 0; ci < nc; ++ci) {
     if (!direct[ci]) continue;
@@ -1240,7 +1324,7 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   if (best_host) *best_host = rec(bi);
   if (per_cand_host)
     for (int ci = 0; ci < nc; ++ci) per_cand_host[ci] = rec(ci);
-  if (!std::isfinite(bv)) {
+  if (!std::isfinite(bv) && !(sl && bv == -INFINITY)) {
     set_error("non-finite certificate value");
     return SFW3D_ENONFINITE;
   }
@@ -1250,6 +1334,36 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
 }  // namespace
 
 extern "C" int sfw3d_last_refine_count(void) { return last_refine_count(); }
+
+extern "C" int sfw3d_eta_argmax_slab(sfw3d_ctx* ctx, const sfw3d_table* t, int dtype,
+                                     const void* residual_dev, int n_own, int x0, double lam,
+                                     const int32_t window[6], sfw3d_halo_fn halo,
+                                     sfw3d_allreduce_fn allreduce, void* user,
+                                     sfw3d_argmax* best_host, sfw3d_argmax* per_cand_host) {
+  SFW3D_CHECK_ARG(ctx && t && residual_dev && window && halo && allreduce, "NULL argument");
+  SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
+  SFW3D_CHECK_ARG(lam > 0.0, "lam must be > 0");
+  SFW3D_CHECK_ARG(n_own > 0 && x0 >= 0 && x0 + n_own <= t->dims[0], "slab planes");
+  const int ld[3] = {n_own, t->dims[1], t->dims[2]};
+  for (int a = 0; a < 3; ++a)
+    SFW3D_CHECK_ARG(0 <= window[2 * a] && window[2 * a] <= window[2 * a + 1] &&
+                        window[2 * a + 1] < ld[a],
+                    "window must be a non-empty box inside the slab (local coordinates)");
+  SFW3D_CHECK_ARG(t->mode == 0, "x-slab certificates need the basis evaluator (mode auto)");
+  SFW3D_TRY(begin_call(ctx));
+  SFW3D_TRY(ensure_basis(t, dtype));
+  SlabArgs sa;
+  sa.link.halo = halo;
+  sa.link.allreduce = allreduce;
+  sa.link.user = user;
+  sa.n_own = n_own;
+  (void)x0;  // (the periodic ring of ranks defines the neighbours)
+  if (dtype == SFW3D_F64)
+    return eta_typed<double>(ctx, t, residual_dev, lam, window, best_host, per_cand_host, nullptr,
+                             &sa);
+  return eta_typed<float>(ctx, t, residual_dev, lam, window, best_host, per_cand_host, nullptr,
+                          &sa);
+}
 
 extern "C" int sfw3d_eta_argmax(sfw3d_ctx* ctx, const sfw3d_table* t, int dtype,
                                 const void* residual_dev, double lam, const int32_t window[6],

@@ -174,9 +174,28 @@ int psf_apply_impl(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* 
 // One circular 1-D correlation pass along `axis`:
 //   out[i] = addend_w * addend[i] + w * sum_q taps[q] * in[i + (lo + q) e_axis]
 // (addend may be NULL or alias out; taps are device pointers of the dtype).
+// Axis-0 output plane range: outputs a in [begin, end) (end < 0: the whole
+// axis) are written to plane a + shift of `out`.
+struct XRange {
+  int begin = 0, end = -1, shift = 0;
+};
 int corr_pass_impl(sfw3d_ctx* ctx, int dtype, const void* in, void* out, const int dims[3], int axis,
                    const void* taps, int lo, int ntaps, const void* addend, double addend_w,
-                   double w, const char* family);
+                   double w, const char* family, const XRange* xr = nullptr);
+
+// x-slab data plane (multi-GPU certificate): the caller's halo exchange and
+// all-reduce (include/sfw3d_cuda.h: sfw3d_halo_fn, sfw3d_allreduce_fn).
+struct SlabLink {
+  sfw3d_halo_fn halo = nullptr;
+  sfw3d_allreduce_fn allreduce = nullptr;
+  void* user = nullptr;
+};
+int slab_corr_impl(sfw3d_ctx* ctx, int dtype, const void* in, void* out, const int odims[3],
+                   const void* const taps[3], const int lo[3], const int nt[3], void* win, int H,
+                   void* tmp, const SlabLink& link, const char* family);
+int psf_apply_slab(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* in, void* out,
+                   int adjoint, const int odims[3], void* win, int H, void* tmp,
+                   const SlabLink& link);
 
 // Launch helpers implemented in the .cu files.
 int render_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const std::vector<AtomGeo>& atoms,

@@ -51,7 +51,7 @@ __device__ __forceinline__ void load_taps_padded(T* taps, const T* __restrict__ 
 template <typename T, int J>
 __global__ void __launch_bounds__(256) pass_strided_kernel(
     const T* __restrict__ in, T* out, int n_axis, long long stride, const T* __restrict__ taps_g,
-    int lo, int ntaps, const T* addend, T aw, T w) {
+    int lo, int ntaps, const T* addend, T aw, T w, int a_begin, int a_end, int out_shift) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* taps = reinterpret_cast<T*>(smem_raw);
   const int npad = (ntaps + J - 1) / J * J;
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(256) pass_strided_kernel(
   // resident together (L2 reuse of the (J + taps - 1)/J overlap)
   const long long inner = blockIdx.y * (long long)blockDim.x + threadIdx.x;
   if (inner >= stride) return;
-  const int a0 = blockIdx.x * J;
+  const int a0 = a_begin + blockIdx.x * J;
   const long long base = (long long)blockIdx.z * n_axis * stride + inner;
   T W[J], acc[J];
   int idx = pmod_i(a0 + lo, n_axis);
@@ -85,8 +85,8 @@ __global__ void __launch_bounds__(256) pass_strided_kernel(
   }
 #pragma unroll
   for (int j = 0; j < J; ++j) {
-    if (a0 + j < n_axis) {
-      const long long o = base + (long long)(a0 + j) * stride;
+    if (a0 + j < a_end) {
+      const long long o = base + (long long)(a0 + j + out_shift) * stride;
       out[o] = addend ? T(aw * addend[o] + w * acc[j]) : T(w * acc[j]);
     }
   }
@@ -178,7 +178,8 @@ __global__ void __launch_bounds__(32 * kZWarps) pass_z_kernel(
 template <typename T, int J, int TI, int NT, int MINB = 1>
 __global__ void __launch_bounds__(NT, MINB) pass_tile2_kernel(
     const T* __restrict__ in, T* __restrict__ out, int n_axis, long long stride,
-    const T* __restrict__ taps_g, int lo, int ntaps, const T* addend, T aw, T w) {
+    const T* __restrict__ taps_g, int lo, int ntaps, const T* addend, T aw, T w, int a_begin,
+    int a_end, int out_shift) {
   constexpr int G = NT / TI, To = J * G;
   constexpr int kVec = 16 / sizeof(T), kRowVecs = TI / kVec;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(NT, MINB) pass_tile2_kernel(
   T* taps = reinterpret_cast<T*>(smem_raw);
   T* tile = taps + nt4;
   const int rows = To + nt4;
-  const int a0 = blockIdx.x * To;
+  const int a0 = a_begin + blockIdx.x * To;
   const long long base0 = (long long)blockIdx.z * n_axis * stride + (long long)blockIdx.y * TI;
   for (int q = threadIdx.x; q < nt4; q += NT) taps[q] = q < ntaps ? taps_g[q] : T(0);
   {
@@ -255,9 +256,9 @@ __global__ void __launch_bounds__(NT, MINB) pass_tile2_kernel(
   }
   {
     const int a1 = a0 + ag * J;
-    const long long o0 = base0 + (long long)a1 * stride + il;
+    const long long o0 = base0 + (long long)(a1 + out_shift) * stride + il;
     T* po = out + o0;
-    if (!addend && a1 + J <= n_axis) {  // full group: unguarded stores
+    if (!addend && a1 + J <= a_end) {  // full group: unguarded stores
       if (w == T(1)) {
 #pragma unroll
         for (int j = 0; j < J; ++j, po += stride) *po = acc[j];
@@ -269,11 +270,11 @@ __global__ void __launch_bounds__(NT, MINB) pass_tile2_kernel(
       const T* pa = addend + o0;
 #pragma unroll
       for (int j = 0; j < J; ++j, po += stride, pa += stride)
-        if (a1 + j < n_axis) *po = T(aw * *pa + w * acc[j]);
+        if (a1 + j < a_end) *po = T(aw * *pa + w * acc[j]);
     } else {
 #pragma unroll
       for (int j = 0; j < J; ++j, po += stride)
-        if (a1 + j < n_axis) *po = T(w * acc[j]);
+        if (a1 + j < a_end) *po = T(w * acc[j]);
     }
   }
 }
@@ -463,19 +464,20 @@ __global__ void __launch_bounds__(256) stencil3d_kernel(const T* __restrict__ in
 
 template <typename T, int J>
 int launch_strided(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis, const T* taps,
-                   int lo, int ntaps, const T* addend, double aw, double w) {
+                   int lo, int ntaps, const T* addend, double aw, double w, const XRange& xr) {
   long long stride = 1;
   for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
   long long outer = 1;
   for (int a = 0; a < axis; ++a) outer *= dims[a];
   const int n = dims[axis];
-  dim3 grid(unsigned((n + J - 1) / J), unsigned((stride + 255) / 256), unsigned(outer));
+  const int ab = xr.begin, ae = xr.end < 0 ? n : xr.end;
+  dim3 grid(unsigned((ae - ab + J - 1) / J), unsigned((stride + 255) / 256), unsigned(outer));
   const size_t smem = size_t((ntaps + J - 1) / J * J) * sizeof(T);
   if (smem > 48 * 1024)
     SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_strided_kernel<T, J>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   pass_strided_kernel<T, J><<<grid, 256, smem, ctx->stream>>>(
-      in, out, n, stride, taps, lo, ntaps, addend, T(aw), T(w));
+      in, out, n, stride, taps, lo, ntaps, addend, T(aw), T(w), ab, ae, xr.shift);
   SFW3D_LAUNCH_CHECK(ctx);
   return SFW3D_OK;
 }
@@ -502,7 +504,7 @@ int launch_z(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* ta
 
 template <typename T, int J, int MINB = 1, int NT = 256>
 int launch_tile2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis, const T* taps,
-                 int lo, int ntaps, const T* addend, double aw, double w) {
+                 int lo, int ntaps, const T* addend, double aw, double w, const XRange& xr) {
   constexpr int TI = 64, To = J * (NT / TI);
   long long stride = 1;
   for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
@@ -514,9 +516,10 @@ int launch_tile2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axi
   if (smem > 48 * 1024)
     SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_tile2_kernel<T, J, TI, NT, MINB>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  dim3 grid(unsigned((n + To - 1) / To), unsigned(stride / TI), unsigned(outer));
-  pass_tile2_kernel<T, J, TI, NT, MINB><<<grid, NT, smem, ctx->stream>>>(in, out, n, stride, taps, lo,
-                                                                   ntaps, addend, T(aw), T(w));
+  const int ab = xr.begin, ae = xr.end < 0 ? n : xr.end;
+  dim3 grid(unsigned((ae - ab + To - 1) / To), unsigned(stride / TI), unsigned(outer));
+  pass_tile2_kernel<T, J, TI, NT, MINB><<<grid, NT, smem, ctx->stream>>>(
+      in, out, n, stride, taps, lo, ntaps, addend, T(aw), T(w), ab, ae, xr.shift);
   SFW3D_LAUNCH_CHECK(ctx);
   return SFW3D_OK;
 }
@@ -557,13 +560,17 @@ constexpr int kNarrowTaps = 24;
 
 template <typename T>
 int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis, const T* taps,
-               int lo, int ntaps, const T* addend, double aw, double w) {
+               int lo, int ntaps, const T* addend, double aw, double w, const XRange& xr) {
   if (ntaps > 4096) {
     set_error("1-D pass with more than 4096 taps");
     return SFW3D_EINVAL;
   }
   constexpr bool f32 = sizeof(T) == 4;
   const bool wide = ntaps > kNarrowTaps;
+  if (axis != 0 && (xr.begin != 0 || xr.end >= 0 || xr.shift != 0)) {
+    set_error("internal: output plane ranges apply to axis-0 passes only");
+    return SFW3D_EINVAL;
+  }
   if (axis == 2) {
     if (dims[2] % 4 == 0 && ntaps <= 1024) {
       if (dims[2] >= 128 && wide) {
@@ -579,28 +586,87 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
   for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
   if (stride % 64 == 0 && ntaps <= 512) {
     if (dims[axis] >= 128 && wide) {
-      if constexpr (f32) return launch_tile2<T, 32, 3>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
-      else return launch_tile2<T, 32, 1>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
+      if constexpr (f32) return launch_tile2<T, 32, 3>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
+      else return launch_tile2<T, 32, 1>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
     }
-    return launch_tile2<T, 16>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
+    return launch_tile2<T, 16>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
   }
-  return wide ? launch_strided<T, 32>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w)
-              : launch_strided<T, 8>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w);
+  return wide ? launch_strided<T, 32>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr)
+              : launch_strided<T, 8>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
 }
 
 }  // namespace
 
 int corr_pass_impl(sfw3d_ctx* ctx, int dtype, const void* in, void* out, const int dims[3], int axis,
                    const void* taps, int lo, int ntaps, const void* addend, double addend_w,
-                   double w, const char* family) {
+                   double w, const char* family, const XRange* xr) {
   SFW3D_PROF(ctx, family);
+  const XRange full{};
+  const XRange& r = xr ? *xr : full;
   if (dtype == SFW3D_F64)
     return pass_typed<double>(ctx, static_cast<const double*>(in), static_cast<double*>(out), dims,
                               axis, static_cast<const double*>(taps), lo, ntaps,
-                              static_cast<const double*>(addend), addend_w, w);
+                              static_cast<const double*>(addend), addend_w, w, r);
   return pass_typed<float>(ctx, static_cast<const float*>(in), static_cast<float*>(out), dims, axis,
                            static_cast<const float*>(taps), lo, ntaps,
-                           static_cast<const float*>(addend), addend_w, w);
+                           static_cast<const float*>(addend), addend_w, w, r);
+}
+
+// Separable correlation of an x-slab: `in` holds the rank's n_own owned
+// planes (compact), `out` receives the same planes of f_x (x) f_y (x) f_z * in
+// of the GLOBAL periodic volume. The z and y passes are plane-local (owned
+// planes only, into the middle of `win`); the x pass needs lo_x = -xlo / hi_x
+// = xlo + lx - 1 planes of the neighbours' y/z-passed data, which the caller's
+// exchange (sfw3d_halo_fn) writes into the halo planes of `win`; the x pass
+// then reads the window and writes the owned planes only. win: (H + n_own +
+// H) planes with H >= both halos; tmp: one owned-size volume.
+int slab_corr_impl(sfw3d_ctx* ctx, int dtype, const void* in, void* out, const int odims[3],
+                   const void* const taps[3], const int lo[3], const int nt[3], void* win, int H,
+                   void* tmp, const SlabLink& link, const char* family) {
+  const size_t es = dtype_size(dtype);
+  const long long plane = (long long)odims[1] * odims[2];
+  const int lox = std::max(0, -lo[0]), hix = std::max(0, lo[0] + nt[0] - 1);
+  if (lox > H || hix > H || lox > odims[0] || hix > odims[0]) {
+    set_error("x-slab thinner than (or window narrower than) the pass halo");
+    return SFW3D_EINVAL;
+  }
+  char* mid = static_cast<char*>(win) + size_t(H) * plane * es;
+  SFW3D_TRY(corr_pass_impl(ctx, dtype, in, tmp, odims, 2, taps[2], lo[2], nt[2], nullptr, 0.0, 1.0,
+                           family));
+  SFW3D_TRY(corr_pass_impl(ctx, dtype, tmp, mid, odims, 1, taps[1], lo[1], nt[1], nullptr, 0.0,
+                           1.0, family));
+  if (link.halo) {
+    // the exchange sees the window [H - lox, H + n_own + hix)
+    char* w0 = mid - size_t(lox) * plane * es;
+    if (link.halo(link.user, w0, dtype, odims[0], plane, lox, hix) != 0) {
+      set_error("halo exchange callback failed");
+      return SFW3D_ECUDA;
+    }
+  }
+  const int wd[3] = {odims[0] + 2 * H, odims[1], odims[2]};
+  const XRange xr{H, H + odims[0], -H};
+  return corr_pass_impl(ctx, dtype, win, out, wd, 0, taps[0], lo[0], nt[0], nullptr, 0.0, 1.0,
+                        family, &xr);
+}
+
+int psf_apply_slab(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* in, void* out,
+                   int adjoint, const int odims[3], void* win, int H, void* tmp,
+                   const SlabLink& link) {
+  if (!psf->separable) {
+    set_error("x-slab sharding needs a separable PSF");
+    return SFW3D_EINVAL;
+  }
+  int lo[3], nt[3];
+  const void* tp[3];
+  for (int a = 0; a < 3; ++a) {
+    nt[a] = psf->hi[a] - psf->lo[a] + 1;
+    lo[a] = adjoint ? psf->lo[a] : -psf->hi[a];
+    if (dtype == SFW3D_F64)
+      tp[a] = adjoint ? psf->taps64[a] : psf->taps64[a] + nt[a];
+    else
+      tp[a] = adjoint ? psf->taps32[a] : psf->taps32[a] + nt[a];
+  }
+  return slab_corr_impl(ctx, dtype, in, out, odims, tp, lo, nt, win, H, tmp, link, "psf_pass");
 }
 
 

@@ -1,24 +1,27 @@
-"""Multi-GPU sharding of the hot path: one process per GPU.
+"""Multi-GPU sharding of the hot path: one process per GPU,
+x-slabs of the periodic volume (axis 0, the slowest), no replicated volumes.
 
-Plumbing is torch.distributed (NCCL on the B200 box; gloo in the CPU tests).
-What shards and which exchanges exist:
-
-* certificate — the output grid is split into x-slabs (axis 0, the slowest
-  axis). With a replicated residual every rank evaluates eta on its slab
-  only (a window restriction, no halo needed) and the single collective is an
-  all-gather of one 24-byte argmax record per rank, reduced with the
-  reference's order (larger eta, then smaller sigma-major candidate, then
-  smaller C-order position: certificate.py:161-172). With a slab-distributed
-  residual the ranks first exchange periodic halos of the template radius.
-* cost + gradient — atoms are split across ranks for the per-atom box
-  reductions (K6, the dominant kernel at config 5) and the rows are
-  all-gathered; the criterion value is computed once per rank (replicated
-  volumes). Slab-local rendering is listed as next work in DESIGN.md.
+* certificate (SlabCertificate -> sfw3d_eta_argmax_slab) — each rank holds
+  the residual on its own planes only. b = H^T r and every shared basis term
+  are computed on the owned planes: their z / y passes are plane-local, and
+  before each x pass the library asks the transport to exchange the pass's
+  halo planes with the two neighbours (sfw3d_halo_fn) — no plane is computed
+  twice. Refined members read b with a template-radius halo (one more
+  exchange); the refinement thresholds use the all-reduced |b| statistics and
+  member maxima (sfw3d_allreduce_fn), so every rank collects the single-GPU
+  candidate set on its slab. Per-candidate records are all-gathered and
+  combined in the reference's order (eta desc, candidate asc, C-order asc).
+* cost + gradient (SlabCostGrad -> sfw3d_cost_grad_slab) — y on the slab
+  window (owned planes + the PSF's x half-extent, static during a solve),
+  atom x-spans clipped to the window, residual masked to the slab; the 6k + 1
+  fp64 partials are all-reduced ON THE DEVICE (one D2H per evaluation).
 * sums (Gram rows, ||r||^2) — fp64 all-reduce.
 
-The functions take a `compute` callable where the per-rank work happens so
-the same exchange logic runs with the CUDA kernels on the GPU and with the
-CPU oracle in the gloo tests.
+Transports (`Comm`): TorchComm (torch.distributed: NCCL P2P / all-reduce on
+the B200 box, gloo in the CPU tests), ThreadComm (ranks as threads of one
+process sharing one GPU: the single-GPU tests of the data plane) and
+SoloComm (one rank of a W-rank layout alone: per-rank timing only; its
+halos are stand-in data).
 """
 
 from __future__ import annotations
@@ -155,43 +158,6 @@ def sharded_rows(compute_rows, k: int, group=None, device=None) -> np.ndarray:
     return allreduce_f64(full, group, device).reshape(k, 6)
 
 
-# ------------------------------------------------------------- GPU helpers
-def eta_field_sharded(residual, lam, table, bounds=None, group=None):
-    """GPU certificate on this rank's x-slab of the window (replicated residual);
-    returns the global (eta_max, candidate, (i, j, k))."""
-    from .certificate import _position_window, eta_argmax_dev
-    dims = table.dims
-
-    def compute(win):
-        best, _, _ = eta_argmax_dev(residual, lam, table, win)
-        lin = (best.pos[0] * dims[1] + best.pos[1]) * dims[2] + best.pos[2]
-        return (best.value, int(best.cand), int(lin))
-
-    v, c, lin = sharded_argmax(compute, dims[0], _position_window(bounds, dims), group,
-                               residual.device)
-    pos = (lin // (dims[1] * dims[2]), (lin // dims[2]) % dims[1], lin % dims[2])
-    return v, c, pos
-
-
-def cost_grad_sharded(psf, y, rows, lam, group=None):
-    """GPU criterion + gradient with the per-atom reductions split over ranks."""
-    from .forward import atom_sums_dev, cost_grad_dev
-    import torch
-    rows = np.ascontiguousarray(rows, dtype=np.float64).reshape(-1, 6)
-    back = torch.empty_like(y)
-    # C and the back-projection H^T (model - y) once per rank (replicated)
-    c, _ = cost_grad_dev(psf, y, rows, lam, want_grad=False, back=back)
-
-    def compute_rows(i0, i1):
-        s = atom_sums_dev(back, rows[i0:i1])
-        out = np.empty_like(s)
-        out[:, 0] = s[:, 0] + lam
-        out[:, 1:] = rows[i0:i1, :1] * s[:, 1:]
-        return out
-
-    return c, sharded_rows(compute_rows, rows.shape[0], group, y.device)
-
-
 # ------------------------------------- slab-local cost + gradient (GPU)
 def psf_x_halo(kernel: np.ndarray) -> int:
     """x half-extent of the PSF's non-zero box (planes a slab needs each side)."""
@@ -258,31 +224,42 @@ class SlabCostGrad:
             self.dims[0], self.x0, self.x1, self.halo, C.byref(half), N.f64_ptr(sums)))
         return half.value, sums
 
-    def cost_grad(self, y_win, rows: np.ndarray, lam: float, group=None):
-        """(C, (k, 6) rows) of the whole volume: partials all-reduced over the
-        process group (this rank alone when no group is initialised)."""
+    def partials_dev(self, y_win, rows: np.ndarray):
+        """This rank's [1/2 sum_slab r^2, raw sums] as a DEVICE fp64 tensor,
+        enqueued on the current stream without a host synchronisation."""
+        import torch
+        from . import _native as N
+        from .forward import code_of
+        if tuple(y_win.shape) != tuple(self.local_dims):
+            raise ValueError(f"y window shape {tuple(y_win.shape)} != {tuple(self.local_dims)}")
         rows = np.ascontiguousarray(rows, dtype=np.float64).reshape(-1, 6)
-        half, sums = self.partials(y_win, rows)
-        if world()[1] > 1:
-            flat = allreduce_f64(np.concatenate([[half], sums.ravel()]), group, y_win.device)
-            half, sums = float(flat[0]), flat[1:].reshape(-1, 6)
-        return finish_cost_grad(half, sums, rows, lam)
+        k = rows.shape[0]
+        dev = y_win.device.index
+        out = torch.empty(1 + 6 * k, dtype=torch.float64, device=y_win.device)
+        N.check(N.lib().sfw3d_cost_grad_slab_dev(
+            N.context(dev).handle, self.psf.native(dev), code_of(y_win), N.ptr(y_win),
+            N.f64_ptr(rows), k, self.dims[0], self.x0, self.x1, self.halo, N.ptr(out)))
+        return out
 
-
-# ------------------------------------------- slab-local certificate (GPU)
-def slab_halo(psf, sigma_grid, shape_grid) -> int:
-    """x-planes of halo an x-slab sub-volume needs so that eta on the slab is
-    the global eta: the PSF's x-extent (b = H^T r) plus the largest candidate
-    support radius (forward.py:97-99). The chained basis factors reach a few
-    planes further with values below the 1e-12 truncation; the signed members'
-    bounds cover those taps whatever data they meet (basis.cu)."""
-    from .forward import support_radius
-    k = psf.kernel.data
-    c = k.shape[0] // 2
-    nzx = np.flatnonzero(np.abs(k).sum(axis=(1, 2)))
-    hx = int(max(c - nzx.min(), nzx.max() - c))
-    r = max(support_radius(s, d) for s in sigma_grid for d in shape_grid)
-    return hx + r
+    def cost_grad(self, y_win, rows: np.ndarray, lam: float, comm=None):
+        """(C, (k, 6) rows) of the whole volume. The partials stay on the
+        device through the all-reduce (TorchComm over NCCL: in-stream); one
+        D2H per evaluation. comm=None: this rank alone."""
+        import torch
+        rows = np.ascontiguousarray(rows, dtype=np.float64).reshape(-1, 6)
+        part = self.partials_dev(y_win, rows)
+        if comm is not None and comm.size > 1:
+            if isinstance(comm, TorchComm) and _dist().get_backend(comm.group) == "nccl":
+                _dist().all_reduce(part, group=comm.group)  # in place, on the current stream
+                flat = part.cpu().numpy()
+            else:
+                flat = comm.allreduce(part.cpu().numpy(), "sum")
+        else:
+            flat = part.cpu().numpy()
+        if not np.isfinite(flat).all():
+            raise FloatingPointError("non-finite criterion gradient; atom parameters left the "
+                                     "smooth regime")
+        return finish_cost_grad(float(flat[0]), flat[1:].reshape(-1, 6), rows, lam)
 
 
 def local_psf_kernel(kernel: np.ndarray, local_dims) -> np.ndarray:
@@ -303,53 +280,240 @@ def local_psf_kernel(kernel: np.ndarray, local_dims) -> np.ndarray:
     return out
 
 
-class SlabCertificate:
-    """Certificate of one rank's x-slab [x0, x1] computed on its own
-    sub-volume: planes x0 - halo .. x1 + halo of the (periodic) residual.
+# ----------------------------------------------------------- transports
+def _fill_halo_self(win, own: int, lo: int, hi: int) -> None:
+    """Periodic halos from the rank's own planes (a ring of one)."""
+    if lo:
+        win[:lo] = win[own:own + lo]
+    if hi:
+        win[lo + own:lo + own + hi] = win[lo:lo + hi]
 
-    Every eta value on the slab equals the global one (the sub-volume holds
-    all the residual the slab's b = H^T r and templates touch), so each rank
-    runs the single-GPU certificate on (x1 - x0 + 1 + 2 halo) planes with the
-    window restricted to its slab, and the only collective is the all-gather
-    of 24-byte argmax records (combine_best: the reference's order). The
-    redundant work is the 2 halo planes per slab plane count. The basis is
-    pruned by the GLOBAL volume's rule (table option global_voxels) so every
-    rank fits the same shared terms as one GPU would."""
 
-    def __init__(self, psf, sigma_grid, shape_grid, dims, x0: int, x1: int, halo: int | None = None,
-                 **table_kw):
+class TorchComm:
+    """torch.distributed transport: NCCL point-to-point / all-reduce on the
+    GPUs (enqueued on the caller's current stream), gloo on CPU tensors."""
+
+    def __init__(self, group=None):
+        dist = _dist()
+        self.group = group
+        self.rank, self.size = dist.get_rank(group), dist.get_world_size(group)
+
+    def halo(self, win, own: int, lo: int, hi: int) -> None:
+        """win: (lo + own + hi, ...) planes; fill [0, lo) from the left
+        neighbour's last lo owned planes and the top hi planes from the right
+        neighbour's first hi (each rank sends the mirror images)."""
+        dist = _dist()
+        if self.size == 1:
+            _fill_halo_self(win, own, lo, hi)
+            return
+        left, right = (self.rank - 1) % self.size, (self.rank + 1) % self.size
+        ops = []
+        if lo:  # my last lo owned planes -> right's low halo
+            ops += [dist.P2POp(dist.isend, win[own:own + lo], right, self.group),
+                    dist.P2POp(dist.irecv, win[:lo], left, self.group)]
+        if hi:  # my first hi owned planes -> left's high halo
+            ops += [dist.P2POp(dist.isend, win[lo:lo + hi], left, self.group),
+                    dist.P2POp(dist.irecv, win[lo + own:lo + own + hi], right, self.group)]
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+    def allreduce(self, values, op: str = "sum") -> np.ndarray:
         import torch
-        from .certificate import build_template_table
-        from .forward import Psf, support_radius
-        from .volumes import Volume
-        self.dims = tuple(int(v) for v in dims)
+        dist = _dist()
+        dev = "cuda" if dist.get_backend(self.group) == "nccl" else "cpu"
+        t = torch.as_tensor(np.ascontiguousarray(values, dtype=np.float64), device=dev).clone()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM,
+                        group=self.group)
+        return t.cpu().numpy()
+
+    def allgather(self, values) -> list:
+        import torch
+        dist = _dist()
+        dev = "cuda" if dist.get_backend(self.group) == "nccl" else "cpu"
+        t = torch.as_tensor(np.ascontiguousarray(values, dtype=np.float64), device=dev)
+        out = [torch.empty_like(t) for _ in range(self.size)]
+        dist.all_gather(out, t, group=self.group)
+        return [o.cpu().numpy() for o in out]
+
+
+class ThreadGroup:
+    """Ranks as threads of one process sharing one GPU (each thread on its own
+    CUDA stream): the single-GPU stand-in for NVLink in the tests. Exchanges
+    synchronise the ranks' streams and copy device to device."""
+
+    def __init__(self, size: int):
+        import threading
+        self.size = size
+        self.barrier = threading.Barrier(size)
+        self.slots = [None] * size
+
+    def comm(self, rank: int) -> "ThreadComm":
+        return ThreadComm(self, rank)
+
+
+class ThreadComm:
+    def __init__(self, group: ThreadGroup, rank: int):
+        self.g, self.rank, self.size = group, rank, group.size
+
+    def _exchange(self, item):
+        g = self.g
+        g.slots[self.rank] = item
+        g.barrier.wait()
+        out = list(g.slots)
+        g.barrier.wait()
+        return out
+
+    def halo(self, win, own: int, lo: int, hi: int) -> None:
+        import torch
+        torch.cuda.current_stream().synchronize()  # my owned planes are final
+        g = self.g
+        g.slots[self.rank] = (win, own, lo)
+        g.barrier.wait()
+        lw, lown, llo = g.slots[(self.rank - 1) % self.size]
+        rw, _, rlo = g.slots[(self.rank + 1) % self.size]
+        if lo:
+            win[:lo].copy_(lw[llo + lown - lo:llo + lown])
+        if hi:
+            win[lo + own:lo + own + hi].copy_(rw[rlo:rlo + hi])
+        torch.cuda.current_stream().synchronize()  # (neighbours may reuse theirs)
+        g.barrier.wait()
+
+    def allreduce(self, values, op: str = "sum") -> np.ndarray:
+        arrs = self._exchange(np.array(values, dtype=np.float64))
+        out = arrs[0].copy()
+        for a in arrs[1:]:  # rank order: deterministic
+            out = np.maximum(out, a) if op == "max" else out + a
+        return out
+
+    def allgather(self, values) -> list:
+        return self._exchange(np.array(values, dtype=np.float64))
+
+
+class SoloComm:
+    """Rank `rank` of a `size`-rank layout run ALONE on this GPU (no other
+    process): halos are filled from the rank's own planes (stand-in data of the
+    right size), reductions are the identity. Per-rank timing aid only."""
+
+    def __init__(self, rank: int, size: int):
+        self.rank, self.size = rank, size
+
+    def halo(self, win, own: int, lo: int, hi: int) -> None:
+        _fill_halo_self(win, own, lo, hi)
+
+    def allreduce(self, values, op: str = "sum") -> np.ndarray:
+        return np.array(values, dtype=np.float64)
+
+    def allgather(self, values) -> list:
+        return [np.array(values, dtype=np.float64)]
+
+
+_DT = {0: ("<f4", 4), 1: ("<f8", 8)}
+
+
+class _DevBuf:
+    """A raw device pointer as a torch-importable buffer (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, shape, code: int):
+        self.__cuda_array_interface__ = {"shape": tuple(int(v) for v in shape),
+                                         "typestr": _DT[code][0], "data": (int(ptr), False),
+                                         "version": 3, "strides": None, "stream": None}
+
+
+def slab_callbacks(comm, device: int):
+    """ctypes halo / all-reduce callbacks of the library's x-slab data plane
+    bound to a transport (keep the returned objects alive during the call)."""
+    import traceback
+    import torch
+    from . import _native as N
+
+    def halo(user, ptr, code, own, plane, lo, hi):
+        try:
+            win = torch.as_tensor(_DevBuf(ptr, (lo + own + hi, plane), code),
+                                  device=f"cuda:{device}")
+            comm.halo(win, own, lo, hi)
+            return 0
+        except Exception:  # (surfaced as the call's error status)
+            traceback.print_exc()
+            return 1
+
+    def allreduce(user, vals, n, op):
+        try:
+            arr = np.ctypeslib.as_array(vals, shape=(n,))
+            arr[:] = comm.allreduce(arr.copy(), "max" if op == 1 else "sum")
+            return 0
+        except Exception:
+            traceback.print_exc()
+            return 1
+
+    return N.HALO_FN(halo), N.ALLREDUCE_FN(allreduce)
+
+
+# ------------------------------------------- slab certificate (GPU)
+class SlabCertificate:
+    """eta_field's grid stage (certificate.py:140-184) on this rank's x-slab
+    [x0, x1] of the GLOBAL table's volume (sfw3d_eta_argmax_slab): the
+    residual lives on the owned planes only; the x passes exchange their
+    halos through `comm`; per-candidate records are all-gathered. The
+    combined winner equals the single-GPU certificate's bit for bit (same
+    kernels, same per-voxel arithmetic, same refinement thresholds)."""
+
+    def __init__(self, table, x0: int, x1: int, comm):
+        self.table = table
+        self.dims = tuple(table.dims)
         self.x0, self.x1 = int(x0), int(x1)
-        self.halo = int(slab_halo(psf, sigma_grid, shape_grid) if halo is None else halo)
-        n = self.dims[0]
-        rmax = max(support_radius(s, d) for s in sigma_grid for d in shape_grid)
-        self.local_dims = (self.x1 - self.x0 + 1 + 2 * self.halo, self.dims[1], self.dims[2])
-        if 2 * rmax + 1 >= n or 2 * rmax + 1 >= self.local_dims[0]:
-            raise ValueError("candidate boxes span the x axis: slabs cannot shard this table")
-        table_kw.setdefault("global_voxels", int(np.prod(self.dims)))
-        self.psf = Psf(Volume(local_psf_kernel(psf.kernel.data, self.local_dims)), normalize=False)
-        self.table = build_template_table(self.psf, sigma_grid, shape_grid, **table_kw)
-        self.index = torch.arange(self.x0 - self.halo, self.x1 + self.halo + 1) % n
+        self.n_own = self.x1 - self.x0 + 1
+        self.comm = comm
 
-    def subvolume(self, residual):
-        """This rank's sub-volume of a global residual (device or host tensor)."""
-        return residual.index_select(0, self.index.to(residual.device)).contiguous()
+    def owned(self, volume):
+        """This rank's planes of a global volume (device or host tensor)."""
+        return volume[self.x0:self.x1 + 1].contiguous()
 
-    def argmax(self, sub, lam: float, window=None):
-        """(eta, cand, global C-order index) of the slab's part of `window`
-        (global coordinates; None = every voxel), or (-inf, big, big)."""
-        from .certificate import eta_argmax_dev
-        (wx0, wx1), wy, wz = window or ((0, self.dims[0] - 1), (0, self.dims[1] - 1),
-                                        (0, self.dims[2] - 1))
+    def argmax(self, r_owned, lam: float, window=None):
+        """Global (eta, candidate, (i, j, k)) and the per-candidate global
+        records [(eta, (i, j, k))] of `window` (global coordinates; None =
+        every voxel). Collective: every rank calls it."""
+        import ctypes as C
+        from . import _native as N
+        from .forward import code_of
+        dims = self.dims
+        if tuple(r_owned.shape) != (self.n_own, dims[1], dims[2]):
+            raise ValueError(f"owned residual shape {tuple(r_owned.shape)} != "
+                             f"{(self.n_own, dims[1], dims[2])}")
+        (wx0, wx1), wy, wz = window or ((0, dims[0] - 1), (0, dims[1] - 1), (0, dims[2] - 1))
         lo, hi = max(self.x0, wx0), min(self.x1, wx1)
-        if lo > hi:
-            return (float("-inf"), 2 ** 31, 2 ** 62)
-        off = self.x0 - self.halo
-        best, _, _ = eta_argmax_dev(sub, lam, self.table, ((lo - off, hi - off), wy, wz))
-        x = (best.pos[0] + off) % self.dims[0]
-        lin = (x * self.dims[1] + best.pos[1]) * self.dims[2] + best.pos[2]
-        return (float(best.value), int(best.cand), int(lin))
+        mine = lo <= hi
+        # (a rank whose slab misses the window still runs the collective
+        # pipeline on its whole slab and contributes nothing)
+        lwin = (lo - self.x0, hi - self.x0) if mine else (0, self.n_own - 1)
+        w32 = np.array([*lwin, *wy, *wz], dtype=np.int32)
+        dev = r_owned.device.index
+        ctx = N.context(dev)
+        halo, ared = slab_callbacks(self.comm, dev)
+        nc = len(self.table.sigma_grid) * len(self.table.shape_grid)
+        best = N.Argmax()
+        per = (N.Argmax * nc)()
+        N.check(N.lib().sfw3d_eta_argmax_slab(
+            ctx.handle, self.table.native(dev), code_of(r_owned), N.ptr(r_owned), self.n_own,
+            self.x0, float(lam), N.i32_ptr(w32), halo, ared, None, C.byref(best), per))
+        plane = dims[1] * dims[2]
+        rec = np.full(2 * nc, -np.inf)
+        for c in range(nc):
+            p = per[c]
+            if mine and np.isfinite(p.value):
+                rec[2 * c] = p.value
+                rec[2 * c + 1] = ((self.x0 + p.pos[0]) * dims[1] + p.pos[1]) * dims[2] + p.pos[2]
+        allr = self.comm.allgather(rec)
+        out = []
+        for c in range(nc):
+            bv, bl = -np.inf, np.inf
+            for r in allr:  # value desc, then the first C-order position
+                v, lin = r[2 * c], r[2 * c + 1]
+                if v > bv or (v == bv and lin < bl):
+                    bv, bl = v, lin
+            lin = int(bl) if np.isfinite(bl) else -1
+            out.append((float(bv), (lin // plane, (lin // dims[2]) % dims[1], lin % dims[2])))
+        gc = 0
+        for c in range(nc):  # strict '>' over sigma-major candidates
+            if out[c][0] > out[gc][0]:
+                gc = c
+        return out[gc][0], gc, out[gc][1], out

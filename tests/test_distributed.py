@@ -1,8 +1,8 @@
 """World-size-2 (and 3) gloo tests of the multi-GPU exchange logic on CPU.
 
 The per-rank compute is the CPU oracle here (tests only); on the B200 the
-same functions run with the CUDA kernels (distributed.eta_field_sharded /
-cost_grad_sharded)."""
+same transports carry the CUDA path's halos and partials
+(distributed.TorchComm over NCCL: SlabCertificate, SlabCostGrad)."""
 import os
 import socket
 import sys
@@ -146,6 +146,37 @@ def body_rows(rank, size):
     got = sharded_rows(lambda i0, i1: O.atom_rows(back, rows[i0:i1], 0.2), 7)
     s = allreduce_f64(np.array([rank + 1.0, 2.0]))
     return float(np.max(np.abs(got - O.atom_rows(back, rows, 0.2)))), s.tolist()
+
+
+def body_torchcomm(rank, size):
+    """TorchComm (the transport of the library's x-slab data plane): halos of
+    lo / hi planes from the ring neighbours, sum / max all-reduce, all-gather."""
+    from paper_2009_05473_b200.distributed import TorchComm, slab_bounds
+    comm = TorchComm()
+    n = 13
+    full = torch.arange(n * 4, dtype=torch.float32).reshape(n, 4)
+    x0, x1 = slab_bounds(n, size, rank)
+    own = x1 - x0 + 1
+    ok = True
+    for lo, hi in ((2, 3), (0, 2), (3, 0), (1, 1)):
+        win = torch.full((lo + own + hi, 4), -1.0)
+        win[lo:lo + own] = full[x0:x1 + 1]
+        comm.halo(win, own, lo, hi)
+        idx = [(x0 - lo + i) % n for i in range(win.shape[0])]
+        ok &= bool(torch.equal(win, full[idx]))
+    s = comm.allreduce(np.array([rank + 1.0, -rank]), "sum").tolist()
+    m = comm.allreduce(np.array([rank + 1.0, -rank]), "max").tolist()
+    g = [a.tolist() for a in comm.allgather(np.array([rank, 2.0 * rank]))]
+    return ok, s, m, g
+
+
+@pytest.mark.parametrize("size", [2, 3])
+def test_torchcomm_transport(size):
+    for ok, s, m, g in spawn(body_torchcomm, size).values():
+        assert ok
+        assert s == [sum(range(1, size + 1)), -sum(range(size))]
+        assert m == [float(size), 0.0]
+        assert g == [[r, 2.0 * r] for r in range(size)]
 
 
 @pytest.mark.parametrize("size", [2, 3])

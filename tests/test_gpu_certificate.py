@@ -200,15 +200,43 @@ def test_signed_members_refined_maxima(P, prec, tol, cap):
         assert tuple(rec.pos) == tuple(pos), (c, tuple(rec.pos), pos)
 
 
-@pytest.mark.parametrize("nranks", [2, 3])
+def _run_ranks(nranks, body):
+    """Run body(rank, comm) on `nranks` threads of this process (one GPU, one
+    CUDA stream per rank): the in-process stand-in for one process per GPU."""
+    import threading
+    import torch
+    from paper_2009_05473_b200 import distributed as D
+    group = D.ThreadGroup(nranks)
+    out, errs = [None] * nranks, []
+
+    def run(rank):
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                out[rank] = body(rank, group.comm(rank))
+                torch.cuda.current_stream().synchronize()
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append(e)
+            group.barrier.abort()
+    th = [threading.Thread(target=run, args=(r,)) for r in range(nranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    return out
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 4])
 @pytest.mark.parametrize("prec", ["f32", "f64"])
-def test_slab_certificate_matches_global(P, nranks, prec):
-    """Multi-GPU certificate layout (distributed.SlabCertificate), ranks run
-    one after another on this GPU: each rank evaluates its x-slab on its own
-    sub-volume (slab + halo planes of the periodic residual) and the records
-    combine (eta desc, candidate asc, C-order index asc) to EXACTLY the
-    single-volume certificate's winner (same kernels, same per-voxel
-    arithmetic), and the winner matches the FFT oracle."""
+def test_slab_certificate_halo_exchange_matches_global(P, nranks, prec):
+    """Multi-GPU certificate data plane (distributed.SlabCertificate ->
+    sfw3d_eta_argmax_slab): each rank holds only its own x-planes of the
+    residual; b = H^T r and every basis term are computed on those planes with
+    the x passes' halos exchanged between neighbours (here: ranks as threads
+    on this GPU, device-to-device copies). The combined per-candidate records
+    equal the single-volume certificate's EXACTLY (same kernels, same
+    per-voxel arithmetic, same refinement thresholds), and match the oracle."""
     import torch
     from paper_2009_05473_b200 import distributed as D
     dims = (96, 48, 64)
@@ -220,23 +248,27 @@ def test_slab_certificate_matches_global(P, nranks, prec):
     r = r.astype(np.float32).astype(np.float64)
     sg, dg = np.array([1.0, 1.5, 2.0]), np.array([1.8, 2.0, 2.5])
     psf = P.Psf(P.Volume(kernel), normalize=False)
+    tdt = torch.float32 if prec == "f32" else torch.float64
+    win = ((3, 90), (0, 47), (2, 60))
     with P.precision(prec):
         table = P.build_template_table(psf, sg, dg)
-        rd = torch.tensor(r, device="cuda", dtype=torch.float32 if prec == "f32" else torch.float64)
-        full = ((0, dims[0] - 1), (0, dims[1] - 1), (0, dims[2] - 1))
-        best, _, _ = P.certificate.eta_argmax_dev(rd, 0.7, table, full)
-        glin = (best.pos[0] * dims[1] + best.pos[1]) * dims[2] + best.pos[2]
-        recs = []
-        for rank in range(nranks):
+        rd = torch.tensor(r, device="cuda", dtype=tdt)
+        best, recs, _ = P.certificate.eta_argmax_dev(rd, 0.7, table, win)
+
+        def body(rank, comm):
             x0, x1 = D.slab_bounds(dims[0], nranks, rank)
-            slab = D.SlabCertificate(psf, sg, dg, dims, x0, x1)
-            recs.append(slab.argmax(slab.subvolume(rd), 0.7))
-    v, c, lin = D.combine_best(recs)
-    assert (v, c, lin) == (float(best.value), int(best.cand), int(glin))
+            slab = D.SlabCertificate(table, x0, x1, comm)
+            return slab.argmax(slab.owned(rd), 0.7, win)
+
+        outs = _run_ranks(nranks, body)
+    for v, c, pos, per in outs:  # every rank returns the same global result
+        assert (v, c, pos) == (float(best.value), int(best.cand), tuple(best.pos))
+        for rec, (pv, pp) in zip(recs, per):
+            assert pv == float(rec.value) and pp == tuple(rec.pos)
     hats = O.template_hats(O.psf_hat(kernel), dims, sg, dg)
-    pos, _, val, _, _ = O.eta_field(r, 0.7, hats, len(dg))
-    assert tuple(best.pos) == tuple(pos)
-    assert abs(v - val) <= (1e-5 if prec == "f32" else 1e-10) * abs(val)
+    opos, _, val, _, _ = O.eta_field(r, 0.7, hats, len(dg), win)
+    assert tuple(best.pos) == tuple(opos)
+    assert abs(best.value - val) <= (1e-5 if prec == "f32" else 1e-10) * abs(val)
 
 
 def test_many_members_ring_slices_vs_oracle(P):
@@ -304,3 +336,33 @@ def test_slab_cost_grad_matches_global(P, nranks, prec, tc, tg):
     assert abs(c - c0) <= tc * abs(c0)
     scale = np.maximum(np.max(np.abs(g0), axis=0), 1e-300)
     assert float(np.max(np.max(np.abs(g - g0), axis=0) / scale)) < tg
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_slab_cost_grad_threads_device_allreduce(P, nranks):
+    """SlabCostGrad.cost_grad as a collective: ranks as threads on this GPU,
+    partials left on the device (sfw3d_cost_grad_slab_dev) and all-reduced;
+    every rank gets the oracle's C and gradient (fp64 bars)."""
+    import torch
+    from paper_2009_05473_b200 import distributed as D
+    from paper_2009_05473_b200.forward import to_dev
+    rng = np.random.default_rng(77)
+    dims = (48, 20, 24)
+    kernel = O.box_gaussian_psf(dims, (1.5, 1.2, 2.0), (4, 3, 5))
+    k = 30
+    rows = np.column_stack([rng.uniform(0.5, 2, k), rng.uniform(0, 48, k), rng.uniform(0, 20, k),
+                            rng.uniform(0, 24, k), rng.uniform(0.8, 1.5, k), rng.uniform(2.0, 2.8, k)])
+    rows[:3, 1] = [0.3, 47.6, 16.0]
+    y = rng.standard_normal(dims)
+    c0, g0, _ = O.criterion_and_gradient(y, rows, O.psf_hat(kernel), 0.15)
+    psf = P.Psf(P.Volume(kernel), normalize=False)
+    yd = to_dev(y)
+
+    def body(rank, comm):
+        x0, x1 = D.slab_bounds(dims[0], nranks, rank)
+        sl = D.SlabCostGrad(psf, dims, x0, x1)
+        return sl.cost_grad(sl.window(yd), rows, 0.15, comm)
+
+    for c, g in _run_ranks(nranks, body):
+        assert abs(c - c0) <= 1e-12 * abs(c0)
+        assert np.max(np.abs(g - g0)) <= 1e-11 * np.max(np.abs(g0))
