@@ -3,18 +3,25 @@
 
 Headline (`metric`): certificate voxel-candidates/s on BASELINE config 4 —
 eta over every voxel of a 512^3 fp32 residual x 16 (sigma, d) candidates
-with the global argmax — one "step" = one full certificate evaluation.
+with the global argmax — one "step" = one full certificate evaluation. The
+residual is one host array (configs.cfg4_residual_host) that the CPU arms
+also use; the line's `parity` block compares every candidate's maximum and
+position with the oracle's FFT eta_field on it (the cpu_baseline leg).
 Secondary (`secondary`): cost+gradient evaluations/s on config 5 (256^3,
-N=1000 atoms, random std-0.1 perturbations).
+N=1000 atoms, random std-0.1 perturbations); BSFW and SFW solve times on
+configs 1 (with the CPU oracle solve on the same observation), 2 and 3.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-Multi-GPU (torchrun, one rank per GPU): each rank holds its x-slab of the
-residual plus halo planes (PSF x-extent + largest candidate radius) and runs
-the single-GPU certificate on that sub-volume with the window restricted to
-its slab (distributed.SlabCertificate); the only collective is the all-gather
-of the 24-byte argmax records (and the max-over-ranks timing). scaling =
-strong (the halo planes are the redundant work).
+Multi-GPU (torchrun, one rank per GPU): x-slabs. Each rank holds its own
+planes of the residual; b = H^T r and every basis term's x pass exchange
+their halo planes with the ring neighbours (NCCL P2P, distributed.TorchComm)
+— no plane is computed twice — the refinement thresholds are all-reduced and
+the per-candidate records all-gathered (distributed.SlabCertificate ->
+sfw3d_eta_argmax_slab). Secondaries under torchrun: x-slab cost + gradient
+(device partials all-reduced) and the config-3 BSFW solve sharded as x-slabs
+(sharded.sharded_solve). scaling = strong. --one-rank R/W runs one rank of a
+W-rank layout alone (SoloComm: per-rank compute time).
 `--impl reference` times the reference algorithm (the CPU oracle port of
 sfw3d's FFT eta_field, threads over candidates as the reference's
 map_ordered does) on rank 0 only.
@@ -462,6 +469,51 @@ def costgrad_workload(args, dev):
             "timing": "wall clock per synchronous C-ABI call (host params in, C + gradient out)"}
 
 
+def sharded_solve_workload(dev, rank, world, config: int = 3, algo: str = "bsfw"):
+    """BASELINE config 3 BSFW solve sharded as x-slabs over the ranks
+    (sharded.sharded_solve over distributed.TorchComm: NCCL halo exchanges
+    and all-reduces). Time = max over ranks of the wall time of the solve."""
+    import torch
+    import paper_2009_05473_b200 as P
+    from paper_2009_05473_b200 import configs, distributed as D, solvers
+    from paper_2009_05473_b200.sharded import sharded_solve
+    inst = {2: configs.config2, 3: configs.config3}[config]()
+    P.set_precision(inst.precision)
+    y = configs.observation_host(inst, seed=1000)
+    psf = P.Psf(P.Volume(inst.kernel), normalize=False)
+    comm = D.TorchComm()
+    x0, x1 = D.slab_bounds(inst.dims[0], world, rank)
+    table = P.build_template_table(psf, inst.sigma_grid, inst.shape_grid, bounds=inst.bounds)
+    cert = D.SlabCertificate(table, x0, x1, comm)
+    win = P.certificate._position_window(inst.bounds, inst.dims)
+    y_own = torch.from_numpy(np.ascontiguousarray(y[x0:x1 + 1])).to(
+        f"cuda:{dev}", torch.float32 if inst.precision == "f32" else torch.float64)
+    lam = inst.lam_factor * cert.argmax(y_own, 1.0, win)[0]
+    orig = solvers.make_parameter_grids
+    solvers.make_parameter_grids = lambda b, ns, nd: (inst.sigma_grid, inst.shape_grid)
+    import paper_2009_05473_b200.sharded as SH
+    SH.make_parameter_grids = solvers.make_parameter_grids
+    try:
+        opts = P.SolverOptions(lam=lam, max_outer_iterations=3 * len(inst.truth))
+        torch.distributed.barrier()
+        t0 = time.perf_counter()
+        res = sharded_solve(P.Volume(y), psf, opts, inst.bounds, algo, comm)
+        torch.cuda.synchronize(dev)
+        t = time.perf_counter() - t0
+    finally:
+        solvers.make_parameter_grids = orig
+        SH.make_parameter_grids = orig
+    tt = torch.tensor([t], dtype=torch.float64, device=f"cuda:{dev}")
+    torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+    return {"metric": f"{algo.upper()} solve time, config {config} sharded as x-slabs over "
+                      f"{world} ranks", "value": float(tt.item()), "unit": "s",
+            "higher_is_better": False, "outer_iterations": len(res.trace.records),
+            "atoms": len(res.measure), "termination": res.termination,
+            "criterion": res.criterion,
+            "timing": "max over ranks of the wall time of sharded.sharded_solve (NCCL halo "
+                      "exchanges + all-reduces; y, phis and the residual on each rank's planes)"}
+
+
 def slab_costgrad_workload(args, dev, rank, world):
     """Config 5 cost + gradient sharded as x-slabs over the N ranks
     (distributed.SlabCostGrad): each rank renders / convolves / back-projects
@@ -478,16 +530,17 @@ def slab_costgrad_workload(args, dev, rank, world):
     y = psf_apply_dev(psf, render_dev(inst.truth, inst.dims, N.F32), False)
     x0, x1 = D.slab_bounds(inst.dims[0], world, rank)
     sl = D.SlabCostGrad(psf, inst.dims, x0, x1)
+    comm = D.TorchComm()
     yw = sl.window(y)
     del y
     perts = configs.perturbations(inst.truth, 100)
     for i in range(3):
-        sl.cost_grad(yw, perts[i], 0.1)
+        sl.cost_grad(yw, perts[i], 0.1, comm)
     torch.distributed.barrier()
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     for i in range(args.cg_steps):
-        sl.cost_grad(yw, perts[i % 100], 0.1)
+        sl.cost_grad(yw, perts[i % 100], 0.1, comm)
     torch.cuda.synchronize(dev)
     t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=f"cuda:{dev}")
     torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -495,7 +548,7 @@ def slab_costgrad_workload(args, dev, rank, world):
     return {"metric": f"cost+grad evals/s (cfg5, x-slab sharded over {world} ranks)",
             "value": 1.0 / s, "unit": "evals/s", "ms_per_eval": 1e3 * s, "halo": sl.halo,
             "timing": "max over ranks of wall clock per synchronous eval (C-ABI call + "
-                      "48 KB fp64 all-reduce)"}
+                      "48 KB fp64 all-reduce of the device partials, one D2H)"}
 
 
 def solve_workload(dev, algo: str = "bsfw", cpu: bool = True):
@@ -591,8 +644,9 @@ def main():
     secondary = []
     if collective(world) and not args.no_secondary:
         cg = slab_costgrad_workload(args, dev, rank, world)  # every rank (all-reduce)
+        sv = sharded_solve_workload(dev, rank, world)         # every rank (collective)
         if rank == 0:
-            secondary.append(cg)
+            secondary += [cg, sv]
     if rank == 0 and not args.no_secondary:
         secondary.append(costgrad_workload(args, dev))
         cpu_solve = not args.no_cpu_baseline

@@ -152,6 +152,19 @@ int sfw3d_cost_grad_slab_dev(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, co
                              const double* params_host, int k, int gnx, int x0, int x1, int halo,
                              double* partials_dev);
 
+/* x-slab render (the sharded solver's blurred atoms phi_i, solvers.py:260-261):
+ * the atoms of the periodic (gdims) volume clipped to the window planes
+ * x0 - halo .. x1 + halo, rendered on that window (out_dev: window dims). */
+int sfw3d_render_slab(sfw3d_ctx* ctx, int dtype, const int gdims[3], const double* params_host,
+                      int k, int x0, int x1, int halo, void* out_dev);
+/* x-slab K7 (neg_eta of the sharded refine, certificate.py:201-209): raw
+ * per-atom sums over the OWNED planes [x0, x1] only; field_dev is a window of
+ * x1 - x0 + 1 + 2 halo planes (plane 0 = global x0 - halo). Summed over the
+ * ranks: the single-volume sfw3d_atom_sums. */
+int sfw3d_atom_sums_slab(sfw3d_ctx* ctx, int dtype, const int gdims[3], const void* field_dev,
+                         const double* params_host, int k, int x0, int x1, int halo,
+                         double* sums_host);
+
 /* ---- certificate (certificate.py:37-236) ------------------------------ */
 /* K2 — candidate table for the (sigma, d) grid, sigma-major (sorted
  * ascending, as build_template_table sorts them, certificate.py:72-73).
@@ -241,9 +254,10 @@ int sfw3d_eta_argmax(sfw3d_ctx* ctx, const sfw3d_table* t, int dtype,
 /* Halo exchange the library requests between the passes of an x-slab
  * evaluation. `window` is a device buffer of lo + owned + hi planes of
  * plane_elems elements (dtype): planes [lo, lo + owned) are this rank's and
- * hold data; the callee must fill planes [0, lo) with the LEFT neighbour's last
- * `lo` owned planes and [lo + owned, lo + owned + hi) with the RIGHT
- * neighbour's first `hi` owned planes (periodic ring of ranks) before any
+ * hold data; the callee must fill planes [0, lo) with the lo global planes just
+ * below this rank's first plane and [lo + owned, lo + owned + hi) with the hi
+ * planes just above its last (periodic; a halo wider than a neighbour's slab
+ * takes planes from further ranks) before any
  * later work on the context stream reads them (enqueue on / wait from that
  * stream). Every rank calls it in the same order (collective). 0 = success. */
 typedef int (*sfw3d_halo_fn)(void* user, void* window_dev, int dtype, int owned_planes,

@@ -161,3 +161,21 @@ def cfg4_residual_host(inst: Instance, seed: int = 4) -> np.ndarray:
     r = np.random.default_rng(seed).standard_normal(dims, dtype=np.float32)
     r += blurred.astype(np.float32)
     return r
+
+
+def observation_host(inst: Instance, seed: int = 0) -> np.ndarray:
+    """y = H * truth + white noise at the config's power SNR, as a host float64
+    array (numpy Generator(seed) noise, circular blur through scipy.fft):
+    identical on every rank of a sharded run (which builds it independently)."""
+    import os
+    import scipy.fft as sfft
+    dims = inst.dims
+    workers = os.cpu_count() or 1
+    khat = sfft.rfftn(sfft.ifftshift(inst.kernel), workers=workers)
+    clean = sfft.irfftn(sfft.rfftn(_render_host(inst.truth, dims), workers=workers) * khat, s=dims,
+                        workers=workers)
+    sigma = float(np.sqrt(np.mean(clean ** 2) / 10 ** (inst.snr_db / 10)))
+    y = clean + sigma * np.random.default_rng(seed).standard_normal(dims)
+    if inst.precision == "f32":
+        y = y.astype(np.float32).astype(np.float64)
+    return y

@@ -478,6 +478,36 @@ extern "C" int sfw3d_cost_grad(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, 
 // elsewhere, so back = H^T (r 1_slab): summed over ranks, the raw sums and
 // 1/2 ||r||^2 are exactly the single-volume ones (up to summation order).
 namespace sfw3d {
+// x-slabs: every atom's unwrapped x-span clipped to the global planes
+// [clip0, clip0 + clip_len), one piece per periodic image that meets them,
+// in coordinates whose plane 0 is global plane `origin` (start and centre
+// shifted by the same integer: the offsets p - m are unchanged)
+int clip_atoms_x(const std::vector<AtomGeo>& atoms, int gnx, int clip0, int clip_len, int origin,
+                 std::vector<AtomGeo>& pieces, std::vector<int>& owner) {
+  pieces.clear();
+  owner.clear();
+  for (int i = 0; i < int(atoms.size()); ++i) {
+    const AtomGeo& a = atoms[i];
+    if (a.full[0]) {
+      set_error("invalid argument: an atom box spans the x axis; slabs cannot shard it");
+      return SFW3D_EINVAL;
+    }
+    for (int j = -1; j <= 1; ++j) {
+      const int s = a.start[0] + j * gnx;
+      const int lo = std::max(s, clip0), hi = std::min(s + a.len[0], clip0 + clip_len);
+      if (lo >= hi) continue;
+      AtomGeo p = a;
+      p.m[0] = a.m[0] + double(j * gnx - origin);
+      p.start[0] = lo - origin;
+      p.len[0] = hi - lo;
+      p.nvox = (long long)p.len[0] * p.len[1] * p.len[2];
+      pieces.push_back(p);
+      owner.push_back(i);
+    }
+  }
+  return SFW3D_OK;
+}
+
 // out[0] = 1/2 res[0]; out[1 + 6i + c] = sum of atom i's pieces' res[1 + 6q + c]
 // (pieces of one atom are consecutive, in image order)
 __global__ void piece_combine_kernel(const int* __restrict__ first, int k,
@@ -535,25 +565,7 @@ static int cost_grad_slab_impl(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, 
   const int gx0 = x0 - halo;
   std::vector<AtomGeo> pieces;
   std::vector<int> owner;
-  for (int i = 0; i < k; ++i) {
-    const AtomGeo& a = atoms[i];
-    if (a.full[0]) {
-      set_error("invalid argument: an atom box spans the x axis; slabs cannot shard it");
-      return SFW3D_EINVAL;
-    }
-    for (int j = -1; j <= 1; ++j) {
-      const int s = a.start[0] + j * gnx;
-      const int lo = std::max(s, gx0), hi = std::min(s + a.len[0], gx0 + nxl);
-      if (lo >= hi) continue;
-      AtomGeo p = a;
-      p.m[0] = a.m[0] + double(j * gnx - gx0);
-      p.start[0] = lo - gx0;
-      p.len[0] = hi - lo;
-      p.nvox = (long long)p.len[0] * p.len[1] * p.len[2];
-      pieces.push_back(p);
-      owner.push_back(i);
-    }
-  }
+  SFW3D_TRY(clip_atoms_x(atoms, gnx, gx0, nxl, gx0, pieces, owner));
   const int kp = int(pieces.size());
   const int64_t n = vol_count(dims);
   const size_t es = dtype_size(dtype), vb = size_t(n) * es;
@@ -604,5 +616,62 @@ static int cost_grad_slab_impl(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, 
     set_error("non-finite criterion gradient; atom parameters left the smooth regime");
     return SFW3D_ENONFINITE;
   }
+  return SFW3D_OK;
+}
+
+// ------------------------------------------------ x-slab render / atom sums
+extern "C" int sfw3d_render_slab(sfw3d_ctx* ctx, int dtype, const int gdims[3],
+                                 const double* params_host, int k, int x0, int x1, int halo,
+                                 void* out_dev) {
+  SFW3D_CHECK_ARG(ctx && out_dev && gdims, "NULL argument");
+  SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
+  SFW3D_CHECK_ARG(k >= 0 && (k == 0 || params_host), "params");
+  SFW3D_CHECK_ARG(gdims[0] > 0 && x0 >= 0 && x1 >= x0 && x1 < gdims[0] && halo >= 0,
+                  "slab bounds");
+  SFW3D_TRY(begin_call(ctx));
+  std::vector<AtomGeo> atoms, pieces;
+  std::vector<int> owner;
+  SFW3D_TRY(build_atoms(gdims, params_host, k, atoms));
+  const int nxl = x1 - x0 + 1 + 2 * halo;
+  SFW3D_TRY(clip_atoms_x(atoms, gdims[0], x0 - halo, nxl, x0 - halo, pieces, owner));
+  const int kp = int(pieces.size());
+  const int wd[3] = {nxl, gdims[1], gdims[2]};
+  SFW3D_TRY(ensure_device(ctx, ctx->ws_small, (size_t(kp) + 1) * sizeof(AtomGeo) + 4096));
+  AtomGeo* ad = static_cast<AtomGeo*>(ctx->ws_small.ptr);
+  SFW3D_TRY(upload_atoms(ctx, pieces, ad));
+  return render_impl(ctx, dtype, wd, pieces, ad, kp, out_dev);
+}
+
+extern "C" int sfw3d_atom_sums_slab(sfw3d_ctx* ctx, int dtype, const int gdims[3],
+                                    const void* field_dev, const double* params_host, int k,
+                                    int x0, int x1, int halo, double* sums_host) {
+  SFW3D_CHECK_ARG(ctx && field_dev && sums_host && gdims, "NULL argument");
+  SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
+  SFW3D_CHECK_ARG(k >= 0 && (k == 0 || params_host), "params");
+  SFW3D_CHECK_ARG(gdims[0] > 0 && x0 >= 0 && x1 >= x0 && x1 < gdims[0] && halo >= 0,
+                  "slab bounds");
+  SFW3D_TRY(begin_call(ctx));
+  std::fill(sums_host, sums_host + size_t(k) * 6, 0.0);
+  if (k == 0) return SFW3D_OK;
+  std::vector<AtomGeo> atoms, pieces;
+  std::vector<int> owner;
+  SFW3D_TRY(build_atoms(gdims, params_host, k, atoms));
+  // the sums run over the OWNED planes [x0, x1]; the field is the window
+  // whose plane 0 is global plane x0 - halo
+  SFW3D_TRY(clip_atoms_x(atoms, gdims[0], x0, x1 - x0 + 1, x0 - halo, pieces, owner));
+  const int kp = int(pieces.size());
+  if (kp == 0) return SFW3D_OK;
+  const int wd[3] = {x1 - x0 + 1 + 2 * halo, gdims[1], gdims[2]};
+  SFW3D_TRY(ensure_device(ctx, ctx->ws_small,
+                          Carver::need({size_t(kp) * sizeof(AtomGeo), size_t(kp) * 6 * sizeof(double)})));
+  Carver cv(ctx->ws_small.ptr);
+  AtomGeo* ad = cv.take<AtomGeo>(kp);
+  double* sums = cv.take<double>(size_t(kp) * 6);
+  SFW3D_TRY(upload_atoms(ctx, pieces, ad));
+  SFW3D_TRY(atom_sums_impl(ctx, dtype, wd, field_dev, pieces, ad, sums));
+  std::vector<double> host(size_t(kp) * 6);
+  SFW3D_TRY(download_sync(ctx, host.data(), sums, host.size() * sizeof(double)));
+  for (int q = 0; q < kp; ++q)
+    for (int c = 0; c < 6; ++c) sums_host[6 * owner[q] + c] += host[6 * q + c];
   return SFW3D_OK;
 }

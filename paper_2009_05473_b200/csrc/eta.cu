@@ -1027,12 +1027,8 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   // basis term's x pass and the templates' x radius (refinement / direct)
   int H = 0;
   if (sl) {
+    // (halos wider than a slab come from several ranks: the transport's job)
     H = std::max({-t->psf->lo[0], t->psf->hi[0], basis_set_max_xhalo(bset), t->pad[0]});
-    if (H > ldims[0]) {
-      set_error("x-slab thinner than its halo (" + std::to_string(H) +
-                " planes): use fewer ranks or the single-volume path");
-      return SFW3D_EINVAL;
-    }
   }
   const size_t wbytes = sl ? size_t(ldims[0] + 2 * H) * t->dims[1] * t->dims[2] * sizeof(T) : 0;
   SFW3D_TRY(ensure_device(ctx, ctx->ws,
@@ -1126,6 +1122,9 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
   if (any_basis)
     SFW3D_TRY(basis_set_eval(ctx, bset, dtype, dims, b, lam, win, fields, cbest, bscratch,
                              any_refine ? ref_l1 : nullptr, &abs_done, sl ? &se : nullptr));
+  // x-slab: the b window exchange is a collective, so every rank makes it at
+  // this fixed point (whatever its own refinement / direct work turns out to be)
+  if (sl && (any_refine || any_direct)) SFW3D_TRY(make_bwin());
   if (any_refine) {
     // Every refined member's approximate eta~ is within E_c of its direct
     // value at every voxel: signed members E_c = ebound_c ||b||_inf / lam

@@ -281,15 +281,57 @@ def local_psf_kernel(kernel: np.ndarray, local_dims) -> np.ndarray:
 
 
 # ----------------------------------------------------------- transports
+def _runs(planes):
+    """Consecutive runs of a list of ints: [(first, count)]."""
+    out = []
+    for p in planes:
+        if out and p == out[-1][0] + out[-1][1]:
+            out[-1] = (out[-1][0], out[-1][1] + 1)
+        else:
+            out.append((p, 1))
+    return out
+
+
+def halo_plan(bounds, n: int, rank: int, lo: int, hi: int):
+    """Where rank's window halos come from: [(owner, window_row, owner_row, count)]
+    for the lo planes below its slab and the hi planes above it (periodic),
+    as contiguous runs per owner; owner_row is local to the owner's slab.
+    Every rank computes every plan (the send lists are the peers' plans)."""
+    x0, x1 = bounds[rank]
+    own = x1 - x0 + 1
+    rows = [(i, (x0 - lo + i) % n) for i in range(lo)]
+    rows += [(lo + own + i, (x1 + 1 + i) % n) for i in range(hi)]
+    starts = [b[0] for b in bounds]
+    plan = []
+    for row, g in rows:
+        q = max(i for i, st in enumerate(starts) if st <= g)  # slab_bounds is ordered
+        orow = g - bounds[q][0]
+        if plan and plan[-1][0] == q and plan[-1][1] + plan[-1][3] == row \
+                and plan[-1][2] + plan[-1][3] == orow:
+            plan[-1] = (q, plan[-1][1], plan[-1][2], plan[-1][3] + 1)
+        else:
+            plan.append((q, row, orow, 1))
+    return plan
+
+
+class _Layout:
+    """The x-slab layout every transport needs for multi-hop halos."""
+
+    def layout(self, n: int):
+        self.n = int(n)
+        self.bounds = [slab_bounds(self.n, self.size, r) for r in range(self.size)]
+        return self
+
+
 def _fill_halo_self(win, own: int, lo: int, hi: int) -> None:
     """Periodic halos from the rank's own planes (a ring of one)."""
-    if lo:
-        win[:lo] = win[own:own + lo]
-    if hi:
-        win[lo + own:lo + own + hi] = win[lo:lo + hi]
+    for i in range(lo):  # plane x0 - lo + i  ==  owned plane (own - lo + i) mod own
+        win[i] = win[lo + (own - lo + i) % own]
+    for i in range(hi):
+        win[lo + own + i] = win[lo + i % own]
 
 
-class TorchComm:
+class TorchComm(_Layout):
     """torch.distributed transport: NCCL point-to-point / all-reduce on the
     GPUs (enqueued on the caller's current stream), gloo on CPU tensors."""
 
@@ -297,25 +339,35 @@ class TorchComm:
         dist = _dist()
         self.group = group
         self.rank, self.size = dist.get_rank(group), dist.get_world_size(group)
+        self.n = None
 
     def halo(self, win, own: int, lo: int, hi: int) -> None:
-        """win: (lo + own + hi, ...) planes; fill [0, lo) from the left
-        neighbour's last lo owned planes and the top hi planes from the right
-        neighbour's first hi (each rank sends the mirror images)."""
+        """win: (lo + own + hi, ...) planes; fill [0, lo) with the lo global
+        planes below this rank's slab and the top hi with those above it
+        (each rank sends the peers' plans: single or multi-hop)."""
         dist = _dist()
         if self.size == 1:
             _fill_halo_self(win, own, lo, hi)
             return
-        left, right = (self.rank - 1) % self.size, (self.rank + 1) % self.size
-        ops = []
-        if lo:  # my last lo owned planes -> right's low halo
-            ops += [dist.P2POp(dist.isend, win[own:own + lo], right, self.group),
-                    dist.P2POp(dist.irecv, win[:lo], left, self.group)]
-        if hi:  # my first hi owned planes -> left's high halo
-            ops += [dist.P2POp(dist.isend, win[lo:lo + hi], left, self.group),
-                    dist.P2POp(dist.irecv, win[lo + own:lo + own + hi], right, self.group)]
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+        if self.n is None:
+            raise RuntimeError("TorchComm.layout(n) must be called before halo exchanges")
+        ops, local = [], []
+        for q in range(self.size):  # my sends, in each receiver's plan order
+            if q == self.rank:
+                continue
+            for owner, _, orow, cnt in halo_plan(self.bounds, self.n, q, lo, hi):
+                if owner == self.rank:
+                    ops.append(dist.P2POp(dist.isend, win[lo + orow:lo + orow + cnt], q, self.group))
+        for owner, row, orow, cnt in halo_plan(self.bounds, self.n, self.rank, lo, hi):
+            if owner == self.rank:
+                local.append((row, orow, cnt))
+            else:
+                ops.append(dist.P2POp(dist.irecv, win[row:row + cnt], owner, self.group))
+        for row, orow, cnt in local:
+            win[row:row + cnt] = win[lo + orow:lo + orow + cnt]
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
 
     def allreduce(self, values, op: str = "sum") -> np.ndarray:
         import torch
@@ -351,9 +403,10 @@ class ThreadGroup:
         return ThreadComm(self, rank)
 
 
-class ThreadComm:
+class ThreadComm(_Layout):
     def __init__(self, group: ThreadGroup, rank: int):
         self.g, self.rank, self.size = group, rank, group.size
+        self.n = None
 
     def _exchange(self, item):
         g = self.g
@@ -367,15 +420,20 @@ class ThreadComm:
         import torch
         torch.cuda.current_stream().synchronize()  # my owned planes are final
         g = self.g
-        g.slots[self.rank] = (win, own, lo)
+        g.slots[self.rank] = ("halo", win, lo)
         g.barrier.wait()
-        lw, lown, llo = g.slots[(self.rank - 1) % self.size]
-        rw, _, rlo = g.slots[(self.rank + 1) % self.size]
-        if lo:
-            win[:lo].copy_(lw[llo + lown - lo:llo + lown])
-        if hi:
-            win[lo + own:lo + own + hi].copy_(rw[rlo:rlo + hi])
-        torch.cuda.current_stream().synchronize()  # (neighbours may reuse theirs)
+        slots = list(g.slots)
+        if any(sl[0] != "halo" for sl in slots):
+            raise RuntimeError("ranks out of step: halo exchange met another collective")
+        if self.size == 1:
+            _fill_halo_self(win, own, lo, hi)
+        else:
+            if self.n is None:
+                raise RuntimeError("ThreadComm.layout(n) must be called before halo exchanges")
+            for owner, row, orow, cnt in halo_plan(self.bounds, self.n, self.rank, lo, hi):
+                _, ow, olo = slots[owner]
+                win[row:row + cnt].copy_(ow[olo + orow:olo + orow + cnt])
+        torch.cuda.current_stream().synchronize()  # (owners may reuse their windows)
         g.barrier.wait()
 
     def allreduce(self, values, op: str = "sum") -> np.ndarray:
@@ -389,13 +447,14 @@ class ThreadComm:
         return self._exchange(np.array(values, dtype=np.float64))
 
 
-class SoloComm:
+class SoloComm(_Layout):
     """Rank `rank` of a `size`-rank layout run ALONE on this GPU (no other
     process): halos are filled from the rank's own planes (stand-in data of the
     right size), reductions are the identity. Per-rank timing aid only."""
 
     def __init__(self, rank: int, size: int):
         self.rank, self.size = rank, size
+        self.n = None
 
     def halo(self, win, own: int, lo: int, hi: int) -> None:
         _fill_halo_self(win, own, lo, hi)
@@ -463,6 +522,7 @@ class SlabCertificate:
         self.x0, self.x1 = int(x0), int(x1)
         self.n_own = self.x1 - self.x0 + 1
         self.comm = comm
+        comm.layout(self.dims[0])
 
     def owned(self, volume):
         """This rank's planes of a global volume (device or host tensor)."""

@@ -150,15 +150,16 @@ def body_rows(rank, size):
 
 def body_torchcomm(rank, size):
     """TorchComm (the transport of the library's x-slab data plane): halos of
-    lo / hi planes from the ring neighbours, sum / max all-reduce, all-gather."""
+    lo / hi planes from the ring neighbours (wider than a slab: from several
+    ranks), sum / max all-reduce, all-gather."""
     from paper_2009_05473_b200.distributed import TorchComm, slab_bounds
-    comm = TorchComm()
     n = 13
+    comm = TorchComm().layout(n)
     full = torch.arange(n * 4, dtype=torch.float32).reshape(n, 4)
     x0, x1 = slab_bounds(n, size, rank)
     own = x1 - x0 + 1
     ok = True
-    for lo, hi in ((2, 3), (0, 2), (3, 0), (1, 1)):
+    for lo, hi in ((2, 3), (0, 2), (3, 0), (1, 1), (8, 6), (13, 1)):  # (multi-hop halos)
         win = torch.full((lo + own + hi, 4), -1.0)
         win[lo:lo + own] = full[x0:x1 + 1]
         comm.halo(win, own, lo, hi)

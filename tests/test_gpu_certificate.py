@@ -227,14 +227,16 @@ def _run_ranks(nranks, body):
     return out
 
 
-@pytest.mark.parametrize("nranks", [2, 3, 4])
+@pytest.mark.parametrize("nranks", [2, 3, 4, 8])
 @pytest.mark.parametrize("prec", ["f32", "f64"])
 def test_slab_certificate_halo_exchange_matches_global(P, nranks, prec):
     """Multi-GPU certificate data plane (distributed.SlabCertificate ->
     sfw3d_eta_argmax_slab): each rank holds only its own x-planes of the
     residual; b = H^T r and every basis term are computed on those planes with
     the x passes' halos exchanged between neighbours (here: ranks as threads
-    on this GPU, device-to-device copies). The combined per-candidate records
+    on this GPU, device-to-device copies; at 8 ranks the 12-plane slabs are
+    thinner than the halos, which then come from two ranks away). The
+    combined per-candidate records
     equal the single-volume certificate's EXACTLY (same kernels, same
     per-voxel arithmetic, same refinement thresholds), and match the oracle."""
     import torch

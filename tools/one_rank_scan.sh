@@ -1,17 +1,13 @@
 #!/usr/bin/env bash
-# Per-rank certificate time of the x-slab layout for W = 2, 4, 8, one rank at a
-# time on this GPU (no process group): the max over ranks predicts the W-GPU
-# step (ranks exchange only the argmax records).
+# Per-rank certificate step of a W-rank x-slab layout, each rank run ALONE on
+# this GPU (bench.py --one-rank R/W: SoloComm, halos filled locally) — the
+# compute side of the multi-GPU projection; NVLink time is added separately.
 set -u
-OUT=gpurun_out/onerank; mkdir -p $OUT
-for W in ${WS:-2 4 8}; do
-  for R in $(seq 0 $((W - 1))); do
-    [ "$R" -gt 1 ] && [ "${ALL:-0}" = 0 ] && break   # slabs are equal-sized: ranks 0-1 suffice
-    timeout 600 python bench.py --one-rank $R/$W --no-secondary --no-cpu-baseline --steps 5 > $OUT/w${W}_r${R}.json 2> $OUT/w${W}_r${R}.err
-    python - $OUT/w${W}_r${R}.json <<'PY'
-import json, sys
-d = json.load(open(sys.argv[1]))
-print(d["one_rank"], "ms/step %.3f" % d["ms_per_step"], "halo", d["config"]["parallelism"][:60], "best", d["argmax"])
-PY
+OUT=gpurun_out/${1:-onerank}
+mkdir -p $OUT
+for W in 2 4 8; do
+  for R in 0 $((W-1)); do
+    timeout 300 python bench.py --one-rank $R/$W --steps 5 --warmup 3 --no-secondary --no-cpu-baseline > $OUT/r${R}_w${W}.json 2> $OUT/r${R}_w${W}.err
+    python -c "import json;d=json.load(open('$OUT/r${R}_w${W}.json'));print('W=$W R=$R ms', round(d['ms_per_step'],3), 'kernels', {k: round(v,3) for k,v in d['kernel_ms_per_step'].items()})"
   done
 done
