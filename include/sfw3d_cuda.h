@@ -250,6 +250,18 @@ int sfw3d_eta_argmax(sfw3d_ctx* ctx, const sfw3d_table* t, int dtype,
                      sfw3d_argmax* best_host, sfw3d_argmax* per_cand_host,
                      void* fields_dev);
 
+/* ---- .vol IO straight to HBM (volumes.py:96-113) ----------------------- */
+/* Host-only: the dims of a .vol file after validating its magic and size. */
+int sfw3d_volume_info(const char* path, int32_t dims[3]);
+/* Read the float64 payload into out_dev (dims from sfw3d_volume_info) in
+ * the storage dtype, streamed through pinned staging with the conversion and
+ * the finite check on the device. EINVAL for a malformed file (the
+ * reference's VolumeFormatError) or a non-finite payload. */
+int sfw3d_volume_read(sfw3d_ctx* ctx, const char* path, int dtype, void* out_dev);
+/* Write a device volume as a .vol file (float64 payload, bit-exact for fp64). */
+int sfw3d_volume_write(sfw3d_ctx* ctx, const char* path, int dtype, const int dims[3],
+                       const void* in_dev);
+
 /* ---- x-slab data plane (multi-GPU certificate) ---------- */
 /* Halo exchange the library requests between the passes of an x-slab
  * evaluation. `window` is a device buffer of lo + owned + hi planes of

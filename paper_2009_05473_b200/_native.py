@@ -33,6 +33,7 @@ EXPORTS = (
     "sfw3d_table_candidate", "sfw3d_basis_fit", "sfw3d_basis_set_fit",
     "sfw3d_last_refine_count", "sfw3d_table_set_option", "sfw3d_eta_argmax_slab",
     "sfw3d_cost_grad_slab_dev", "sfw3d_render_slab", "sfw3d_atom_sums_slab",
+    "sfw3d_volume_info", "sfw3d_volume_read", "sfw3d_volume_write",
 )
 
 
@@ -73,6 +74,9 @@ _SIGNATURES = {
     "sfw3d_render_slab": (C.c_int, [_vp, C.c_int, _ip, _dp, C.c_int, C.c_int, C.c_int, C.c_int, _vp]),
     "sfw3d_atom_sums_slab": (C.c_int, [_vp, C.c_int, _ip, _vp, _dp, C.c_int, C.c_int, C.c_int, C.c_int,
                                        _dp]),
+    "sfw3d_volume_info": (C.c_int, [C.c_char_p, _i32p]),
+    "sfw3d_volume_read": (C.c_int, [_vp, C.c_char_p, C.c_int, _vp]),
+    "sfw3d_volume_write": (C.c_int, [_vp, C.c_char_p, C.c_int, _ip, _vp]),
     "sfw3d_table_create": (C.c_int, [_vp, _vp, C.c_int, _dp, C.c_int, _dp, C.c_double, C.c_int,
                                      C.c_double, C.POINTER(_vp)]),
     "sfw3d_table_info": (C.c_int, [_vp, C.c_int, _ip, _ip, _ip, C.POINTER(C.c_int64),

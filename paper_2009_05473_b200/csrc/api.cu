@@ -47,6 +47,8 @@ static int ensure_pinned_arena(sfw3d_ctx* ctx, Arena& a, size_t bytes) {
   return SFW3D_OK;
 }
 
+int ensure_pinned_io(sfw3d_ctx* ctx, size_t bytes) { return ensure_pinned_arena(ctx, ctx->pinned_io, bytes); }
+
 int begin_call(sfw3d_ctx* ctx) {
   SFW3D_TRY(activate(ctx));
   if (ctx->pin_off) {
@@ -182,6 +184,7 @@ extern "C" int sfw3d_ctx_destroy(sfw3d_ctx* ctx) {
   if (ctx->ws_plan.ptr) cudaFree(ctx->ws_plan.ptr);
   if (ctx->pinned.ptr) cudaFreeHost(ctx->pinned.ptr);
   if (ctx->pinned_out.ptr) cudaFreeHost(ctx->pinned_out.ptr);
+  if (ctx->pinned_io.ptr) cudaFreeHost(ctx->pinned_io.ptr);
   delete ctx;
   return SFW3D_OK;
 }
@@ -674,4 +677,194 @@ extern "C" int sfw3d_atom_sums_slab(sfw3d_ctx* ctx, int dtype, const int gdims[3
   for (int q = 0; q < kp; ++q)
     for (int c = 0; c < 6; ++c) sums_host[6 * owner[q] + c] += host[6 * q + c];
   return SFW3D_OK;
+}
+
+// ------------------------------------------------ .vol IO straight to HBM
+// volumes.py:96-113 format: b"SFW3DV01", nx, ny, nz (little-endian uint32),
+// then nx*ny*nz little-endian float64 in C order. The payload streams through
+// two pinned staging buffers (the disk read of chunk i + 1 overlaps the H2D of
+// chunk i); fp32 storage converts on the device; a device pass counts
+// non-finite values (the reference's VolumeFormatError, here SFW3D_EINVAL).
+namespace sfw3d {
+namespace {
+constexpr size_t kVolChunk = size_t(32) << 20;  // bytes per staging buffer
+
+// dst == NULL: check only (fp64 storage reads straight into place)
+template <typename T>
+__global__ void vol_convert_kernel(const double* src, T* dst, long long n,
+                                   unsigned long long* __restrict__ bad) {
+  unsigned long long b = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double v = src[i];
+    b += !isfinite(v);
+    if (dst) dst[i] = T(v);
+  }
+  if (b) atomicAdd(bad, b);  // (an integer count: order-independent)
+}
+
+template <typename T>
+__global__ void vol_export_kernel(const T* __restrict__ src, double* __restrict__ dst, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = double(src[i]);
+}
+
+int vol_header(FILE* f, const char* path, int dims[3], long long* payload) {
+  unsigned char h[20];
+  if (fread(h, 1, 20, f) != 20) {
+    set_error(std::string(path) + ": truncated header");
+    return SFW3D_EINVAL;
+  }
+  if (memcmp(h, "SFW3DV01", 8) != 0) {
+    set_error(std::string(path) + ": bad magic");
+    return SFW3D_EINVAL;
+  }
+  long long n = 1;
+  for (int a = 0; a < 3; ++a) {
+    const uint32_t v = uint32_t(h[8 + 4 * a]) | (uint32_t(h[9 + 4 * a]) << 8) |
+                       (uint32_t(h[10 + 4 * a]) << 16) | (uint32_t(h[11 + 4 * a]) << 24);
+    if (v < 1 || v > (1u << 30)) {
+      set_error(std::string(path) + ": dims must be three positive integers");
+      return SFW3D_EINVAL;
+    }
+    dims[a] = int(v);
+    n *= v;
+  }
+  fseeko(f, 0, SEEK_END);
+  const long long size = ftello(f);
+  fseeko(f, 20, SEEK_SET);
+  if (size != 20 + 8 * n) {
+    set_error(std::string(path) + ": payload size mismatch (header says " +
+              std::to_string(20 + 8 * n) + " bytes, file has " + std::to_string(size) + ")");
+    return SFW3D_EINVAL;
+  }
+  *payload = n;
+  return SFW3D_OK;
+}
+}  // namespace
+}  // namespace sfw3d
+
+extern "C" int sfw3d_volume_info(const char* path, int32_t dims[3]) {
+  SFW3D_CHECK_ARG(path && dims, "NULL argument");
+  FILE* f = fopen(path, "rb");
+  if (!f) {
+    set_error(std::string(path) + ": cannot open");
+    return SFW3D_EINVAL;
+  }
+  int d[3];
+  long long n = 0;
+  const int st = vol_header(f, path, d, &n);
+  fclose(f);
+  if (st == SFW3D_OK)
+    for (int a = 0; a < 3; ++a) dims[a] = d[a];
+  return st;
+}
+
+extern "C" int sfw3d_volume_read(sfw3d_ctx* ctx, const char* path, int dtype, void* out_dev) {
+  SFW3D_CHECK_ARG(ctx && path && out_dev, "NULL argument");
+  SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
+  SFW3D_TRY(begin_call(ctx));
+  FILE* f = fopen(path, "rb");
+  if (!f) {
+    set_error(std::string(path) + ": cannot open");
+    return SFW3D_EINVAL;
+  }
+  int dims[3];
+  long long n = 0;
+  int st = vol_header(f, path, dims, &n);
+  if (st != SFW3D_OK) {
+    fclose(f);
+    return st;
+  }
+  // staging: 2 pinned host buffers + (fp32) one device f64 chunk + the counter
+  SFW3D_TRY(ensure_pinned_io(ctx, 2 * kVolChunk));
+  SFW3D_TRY(ensure_device(ctx, ctx->ws_aux, kVolChunk + 256));
+  double* dchunk = static_cast<double*>(ctx->ws_aux.ptr);
+  unsigned long long* bad = reinterpret_cast<unsigned long long*>(
+      static_cast<char*>(ctx->ws_aux.ptr) + kVolChunk);
+  SFW3D_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(*bad), ctx->stream));
+  cudaEvent_t ev[2];
+  SFW3D_CUDA_TRY(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  SFW3D_CUDA_TRY(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  const long long per = (long long)(kVolChunk / 8);
+  long long done = 0;
+  int i = 0;
+  for (; done < n && st == SFW3D_OK; ++i) {
+    const long long cnt = std::min(per, n - done);
+    char* host = static_cast<char*>(ctx->pinned_io.ptr) + (i & 1) * kVolChunk;
+    if (i >= 2) cudaEventSynchronize(ev[i & 1]);  // that buffer's copy has landed
+    if (fread(host, 8, size_t(cnt), f) != size_t(cnt)) {
+      set_error(std::string(path) + ": short read");
+      st = SFW3D_EINVAL;
+      break;
+    }
+    void* dst = dtype == SFW3D_F64 ? static_cast<void*>(static_cast<double*>(out_dev) + done)
+                                   : static_cast<void*>(dchunk);
+    cudaMemcpyAsync(dst, host, size_t(cnt) * 8, cudaMemcpyHostToDevice, ctx->stream);
+    const unsigned grid = unsigned(std::min<long long>(4LL * ctx->num_sms, (cnt + 255) / 256));
+    if (dtype == SFW3D_F64)
+      vol_convert_kernel<double><<<grid, 256, 0, ctx->stream>>>(
+          static_cast<double*>(dst), nullptr, cnt, bad);
+    else
+      vol_convert_kernel<float><<<grid, 256, 0, ctx->stream>>>(
+          dchunk, static_cast<float*>(out_dev) + done, cnt, bad);
+    SFW3D_LAUNCH_CHECK(ctx);
+    cudaEventRecord(ev[i & 1], ctx->stream);
+    done += cnt;
+  }
+  fclose(f);
+  unsigned long long hbad = 0;
+  if (st == SFW3D_OK) st = download_sync(ctx, &hbad, bad, sizeof(hbad));
+  else cudaStreamSynchronize(ctx->stream);
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  if (st == SFW3D_OK && hbad) {
+    set_error(std::string(path) + ": payload contains non-finite values");
+    return SFW3D_EINVAL;
+  }
+  return st;
+}
+
+extern "C" int sfw3d_volume_write(sfw3d_ctx* ctx, const char* path, int dtype, const int dims[3],
+                                  const void* in_dev) {
+  SFW3D_CHECK_ARG(ctx && path && in_dev && dims, "NULL argument");
+  SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
+  SFW3D_CHECK_ARG(dims[0] > 0 && dims[1] > 0 && dims[2] > 0, "dims must be positive");
+  SFW3D_TRY(begin_call(ctx));
+  FILE* f = fopen(path, "wb");
+  if (!f) {
+    set_error(std::string(path) + ": cannot open for writing");
+    return SFW3D_EINVAL;
+  }
+  unsigned char h[20];
+  memcpy(h, "SFW3DV01", 8);
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 4; ++b) h[8 + 4 * a + b] = (uint32_t(dims[a]) >> (8 * b)) & 255;
+  fwrite(h, 1, 20, f);
+  SFW3D_TRY(ensure_pinned_io(ctx, 2 * kVolChunk));
+  SFW3D_TRY(ensure_device(ctx, ctx->ws_aux, kVolChunk));
+  double* dchunk = static_cast<double*>(ctx->ws_aux.ptr);
+  const long long n = (long long)dims[0] * dims[1] * dims[2], per = (long long)(kVolChunk / 8);
+  int st = SFW3D_OK;
+  for (long long done = 0; done < n; done += per) {
+    const long long cnt = std::min(per, n - done);
+    const double* src = static_cast<const double*>(in_dev) + done;
+    if (dtype == SFW3D_F32) {
+      vol_export_kernel<float><<<unsigned(std::min<long long>(4LL * ctx->num_sms, (cnt + 255) / 256)),
+                                 256, 0, ctx->stream>>>(static_cast<const float*>(in_dev) + done,
+                                                        dchunk, cnt);
+      src = dchunk;
+    }
+    char* host = static_cast<char*>(ctx->pinned_io.ptr);
+    cudaMemcpyAsync(host, src, size_t(cnt) * 8, cudaMemcpyDeviceToHost, ctx->stream);
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess ||
+        fwrite(host, 8, size_t(cnt), f) != size_t(cnt)) {
+      set_error(std::string(path) + ": write failed");
+      st = SFW3D_ECUDA;
+      break;
+    }
+  }
+  fclose(f);
+  return st;
 }

@@ -73,6 +73,7 @@ struct sfw3d_ctx {
   sfw3d::Arena ws_small;   // small device scratch (params, partials)
   sfw3d::Arena ws_aux;     // auxiliary small device scratch (render culling boxes)
   sfw3d::Arena ws_plan;    // atom-sum chunk plan + chunk partials
+  sfw3d::Arena pinned_io;  // pinned staging of the .vol reader / writer
   // kernel-family timing (sfw3d_ctx_profile)
   int profile = 0;
   struct Mark {
@@ -86,6 +87,7 @@ struct sfw3d_ctx {
 namespace sfw3d {
 
 int ensure_device(sfw3d_ctx* ctx, Arena& a, size_t bytes);
+int ensure_pinned_io(sfw3d_ctx* ctx, size_t bytes);
 // Host->device upload through the pinned staging area (asynchronous on
 // ctx->stream). The staging area is recycled at the next begin_call or
 // after a synchronising download.

@@ -150,3 +150,36 @@ def read_volume(path) -> Volume:
     if not np.isfinite(data).all():
         raise VolumeFormatError(f"{path}: payload contains non-finite values")
     return Volume(data.astype(np.float64, copy=True))
+
+
+# -- .vol IO straight to HBM (B200 build: SURVEY §8(f)4) ----------------------
+def read_volume_device(path, device=None, precision: str | None = None):
+    """A ``.vol`` file as a device tensor in the storage precision, without a
+    host float64 Volume: the payload streams through pinned staging into HBM
+    (sfw3d_volume_read); the format checks are the reference's
+    (volumes.py:96-113) and raise VolumeFormatError."""
+    import torch
+    from . import _native as N
+    p = str(Path(path)).encode()
+    dims = np.zeros(3, np.int32)
+    code = N.dtype_code(precision)
+    try:
+        N.check(N.lib().sfw3d_volume_info(p, N.i32_ptr(dims)))
+        dev = N.device_index(device)
+        out = torch.empty(tuple(int(d) for d in dims), dtype=N.torch_dtype(code),
+                          device=f"cuda:{dev}")
+        N.check(N.lib().sfw3d_volume_read(N.context(dev).handle, p, code, N.ptr(out)))
+    except ValueError as e:
+        raise VolumeFormatError(str(e)) from None
+    return out
+
+
+def write_volume_device(tensor, path) -> None:
+    """Write a device volume (fp32 or fp64) as a ``.vol`` file (float64
+    payload; bit-exact round trip for fp64)."""
+    from . import _native as N
+    from .forward import code_of
+    t = tensor.contiguous()
+    dev = t.device.index
+    N.check(N.lib().sfw3d_volume_write(N.context(dev).handle, str(Path(path)).encode(), code_of(t),
+                                       N.dims_arg(t.shape), N.ptr(t)))
