@@ -18,7 +18,7 @@ $(OBJDIR)/%.o: paper_2009_05473_b200/csrc/%.cu $(HDR)
 
 $(LIB): $(OBJ)
 	@mkdir -p $(dir $@)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart -lpthread
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart -lcufft -lpthread
 	@cat $(OBJDIR)/*.ptxas.log > build_ptxas.log
 
 oracle:

@@ -347,6 +347,7 @@ extern "C" int sfw3d_psf_destroy(sfw3d_psf* psf) {
   }
   if (psf->box64) cudaFree(psf->box64);
   if (psf->box32) cudaFree(psf->box32);
+  psf_fft_destroy(psf);
   delete psf;
   return SFW3D_OK;
 }

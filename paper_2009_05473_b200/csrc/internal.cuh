@@ -153,6 +153,8 @@ int build_atoms(const int dims[3], const double* params, int k, std::vector<Atom
 // ---------------------------------------------------------------- PSF
 }  // namespace sfw3d
 
+namespace sfw3d { struct PsfFft; }
+
 struct sfw3d_psf {
   int dims[3];
   int separable;
@@ -164,6 +166,8 @@ struct sfw3d_psf {
   double* box64 = nullptr;
   float* box32 = nullptr;
   int device = 0;
+  // general kernels at size: cuFFT plans + kernel spectra (fft.cu), lazily
+  mutable sfw3d::PsfFft* fft = nullptr;
 };
 
 namespace sfw3d {
@@ -195,6 +199,10 @@ struct SlabLink {
 int slab_corr_impl(sfw3d_ctx* ctx, int dtype, const void* in, void* out, const int odims[3],
                    const void* const taps[3], const int lo[3], const int nt[3], void* win, int H,
                    void* tmp, const SlabLink& link, const char* family);
+bool psf_use_fft(const sfw3d_psf* psf);
+int psf_fft_apply(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* in, void* out,
+                  int adjoint);
+void psf_fft_destroy(sfw3d_psf* psf);
 int psf_apply_slab(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* in, void* out,
                    int adjoint, const int odims[3], void* win, int H, void* tmp,
                    const SlabLink& link);

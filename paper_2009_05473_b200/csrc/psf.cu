@@ -702,6 +702,7 @@ int psf_apply_impl(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* 
                              "psf_pass"));
     return SFW3D_OK;
   }
+  if (psf_use_fft(psf)) return psf_fft_apply(ctx, psf, dtype, in, out, adjoint);
   const long long n = vol_count(dims);
   const int l0 = psf->hi[0] - psf->lo[0] + 1, l1 = psf->hi[1] - psf->lo[1] + 1,
             l2 = psf->hi[2] - psf->lo[2] + 1;
