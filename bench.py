@@ -290,7 +290,11 @@ def cert_workload(args, rank, world, dev):
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
+    halo_mb = None
     if sharded:
+        hb0 = comm.halo_bytes
+        step()
+        halo_mb = (comm.halo_bytes - hb0) / 2 ** 20  # received per rank per step
         v, c, pos, _ = out
     else:
         v, c, pos = float(out[0].value), int(out[0].cand), tuple(int(q) for q in out[0].pos)
@@ -425,6 +429,7 @@ def cert_workload(args, rank, world, dev):
         "table": info, "best": {"eta": gbest[0], "cand": int(gbest[1]), "lin": int(gbest[2]),
                                 "pos": [int(q) for q in np.unravel_index(int(gbest[2]), dims)]},
         "halo": ("exchanged per x pass" if sharded else 0), "host_residual": host_residual,
+        "halo_mib_per_step": halo_mb,
         "per_cand": [(tuple(int(q) for q in r.pos), float(r.value)) for r in per_cand]
         if per_cand is not None else None,
         "refined_voxels": refine_count,
@@ -707,6 +712,8 @@ def main():
             "refined_voxels": res["refined_voxels"],
             "secondary": secondary,
         }
+        if res.get("halo_mib_per_step") is not None:
+            line["halo_mib_received_per_step"] = res["halo_mib_per_step"]
         if ONE_RANK:
             line["one_rank"] = f"{ONE_RANK[0]}/{ONE_RANK[1]}"  # testing aid: this rank's time only
         print(json.dumps(line), flush=True)

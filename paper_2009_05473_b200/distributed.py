@@ -315,7 +315,13 @@ def halo_plan(bounds, n: int, rank: int, lo: int, hi: int):
 
 
 class _Layout:
-    """The x-slab layout every transport needs for multi-hop halos."""
+    """The x-slab layout every transport needs for multi-hop halos, and the
+    halo bytes it has received (for the multi-GPU projections)."""
+
+    halo_bytes = 0
+
+    def _count(self, win, lo: int, hi: int) -> None:
+        self.halo_bytes += (lo + hi) * win[0].numel() * win.element_size()
 
     def layout(self, n: int):
         self.n = int(n)
@@ -346,6 +352,7 @@ class TorchComm(_Layout):
         planes below this rank's slab and the top hi with those above it
         (each rank sends the peers' plans: single or multi-hop)."""
         dist = _dist()
+        self._count(win, lo, hi)
         if self.size == 1:
             _fill_halo_self(win, own, lo, hi)
             return
@@ -418,6 +425,7 @@ class ThreadComm(_Layout):
 
     def halo(self, win, own: int, lo: int, hi: int) -> None:
         import torch
+        self._count(win, lo, hi)
         torch.cuda.current_stream().synchronize()  # my owned planes are final
         g = self.g
         g.slots[self.rank] = ("halo", win, lo)
@@ -457,6 +465,7 @@ class SoloComm(_Layout):
         self.n = None
 
     def halo(self, win, own: int, lo: int, hi: int) -> None:
+        self._count(win, lo, hi)
         _fill_halo_self(win, own, lo, hi)
 
     def allreduce(self, values, op: str = "sum") -> np.ndarray:
