@@ -3,7 +3,7 @@
 # code is needed: device helpers are header-inline, cross-file calls are host.
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v -diag-suppress 20208 --expt-relaxed-constexpr
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fopenmp -Xptxas -v -diag-suppress 20208 --expt-relaxed-constexpr
 SRC := $(wildcard paper_2009_05473_b200/csrc/*.cu)
 HDR := $(wildcard paper_2009_05473_b200/csrc/*.cuh) include/sfw3d_cuda.h
 OBJDIR := build/obj
@@ -18,7 +18,7 @@ $(OBJDIR)/%.o: paper_2009_05473_b200/csrc/%.cu $(HDR)
 
 $(LIB): $(OBJ)
 	@mkdir -p $(dir $@)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart -lcufft -lpthread
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart -lcufft -lgomp -lpthread
 	@cat $(OBJDIR)/*.ptxas.log > build_ptxas.log
 
 oracle:

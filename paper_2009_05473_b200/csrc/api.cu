@@ -100,44 +100,55 @@ static int axis_geometry(int n, double centre, int radius, int& start, int& len,
   return SFW3D_OK;
 }
 
+// One atom's geometry (forward.py:97-116, 130-137); returns a status and
+// sets the thread's error message on failure.
+static int build_one(const int dims[3], const double* r, int i, AtomGeo& a) {
+  for (int c = 0; c < 6; ++c)
+    if (!std::isfinite(r[c])) {
+      set_error("invalid argument: non-finite atom parameters (row " + std::to_string(i) + ")");
+      return SFW3D_EINVAL;
+    }
+  a.w = r[0];
+  a.m[0] = r[1];
+  a.m[1] = r[2];
+  a.m[2] = r[3];
+  a.sigma = r[4];
+  a.d = r[5];
+  if (!(a.sigma > 0.0 && a.d > 0.0)) {
+    set_error("invalid argument: sigma and d must be positive (row " + std::to_string(i) + ")");
+    return SFW3D_EINVAL;
+  }
+  // forward.py:97-99 support_radius
+  const double rr = std::ceil(a.sigma * std::pow(kTailExponent, 1.0 / a.d));
+  if (!(rr < 1e9)) {
+    set_error("invalid argument: support radius overflow");
+    return SFW3D_EINVAL;
+  }
+  a.radius = int(rr);
+  a.inv2sd = 0.5 / std::pow(a.sigma, a.d);
+  a.half_d = 0.5 * a.d;
+  a.log_sigma = std::log(a.sigma);
+  a.d_over_sigma = a.d / a.sigma;
+  a.d2 = (a.d == 2.0) ? 1 : 0;
+  a.nvox = 1;
+  for (int ax = 0; ax < 3; ++ax) {
+    axis_geometry(dims[ax], a.m[ax], a.radius, a.start[ax], a.len[ax], a.full[ax]);
+    a.nvox *= a.len[ax];
+  }
+  return SFW3D_OK;
+}
+
+// The host geometry of k atoms (libm pow / ceil / nearbyint exactly as the
+// reference). Large k is split over OpenMP threads (the per-atom work is
+// independent; a failure is re-run on the calling thread for its message).
 int build_atoms(const int dims[3], const double* params, int k, std::vector<AtomGeo>& out) {
   out.resize(k);
-  for (int i = 0; i < k; ++i) {
-    const double* r = params + 6 * i;
-    for (int c = 0; c < 6; ++c)
-      if (!std::isfinite(r[c])) {
-        set_error("invalid argument: non-finite atom parameters (row " + std::to_string(i) + ")");
-        return SFW3D_EINVAL;
-      }
-    AtomGeo& a = out[i];
-    a.w = r[0];
-    a.m[0] = r[1];
-    a.m[1] = r[2];
-    a.m[2] = r[3];
-    a.sigma = r[4];
-    a.d = r[5];
-    if (!(a.sigma > 0.0 && a.d > 0.0)) {
-      set_error("invalid argument: sigma and d must be positive (row " + std::to_string(i) + ")");
-      return SFW3D_EINVAL;
-    }
-    // forward.py:97-99 support_radius
-    const double rr = std::ceil(a.sigma * std::pow(kTailExponent, 1.0 / a.d));
-    if (!(rr < 1e9)) {
-      set_error("invalid argument: support radius overflow");
-      return SFW3D_EINVAL;
-    }
-    a.radius = int(rr);
-    a.inv2sd = 0.5 / std::pow(a.sigma, a.d);
-    a.half_d = 0.5 * a.d;
-    a.log_sigma = std::log(a.sigma);
-    a.d_over_sigma = a.d / a.sigma;
-    a.d2 = (a.d == 2.0) ? 1 : 0;
-    a.nvox = 1;
-    for (int ax = 0; ax < 3; ++ax) {
-      axis_geometry(dims[ax], a.m[ax], a.radius, a.start[ax], a.len[ax], a.full[ax]);
-      a.nvox *= a.len[ax];
-    }
-  }
+  int bad = k;
+  const int nth = k >= 512 ? std::min(8, k / 128) : 1;
+#pragma omp parallel for num_threads(nth) schedule(static) reduction(min : bad) if (nth > 1)
+  for (int i = 0; i < k; ++i)
+    if (build_one(dims, params + 6 * i, i, out[i]) != SFW3D_OK) bad = std::min(bad, i);
+  if (bad < k) return build_one(dims, params + 6 * bad, bad, out[bad]);
   return SFW3D_OK;
 }
 
@@ -431,7 +442,10 @@ extern "C" int sfw3d_cost_grad(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, 
   Carver cw(ctx->ws.ptr);
   void* A = cw.take<char>(vb);
   void* B = cw.take<char>(vb);
-  const int nred = 4 * ctx->num_sms;
+  // partials of ||r||^2: the grid-stride reduction, or one per CTA of the
+  // fused residual x pass (<= ceil(nx / 64) * ny nz / 64)
+  const int nred = int(std::max<long long>(4LL * ctx->num_sms,
+                                           (long long)((dims[0] + 63) / 64) * ((long long)dims[1] * dims[2] / 64)));
   SFW3D_TRY(ensure_device(ctx, ctx->ws_small,
                           Carver::need({(size_t(k) + 1) * sizeof(AtomGeo), (size_t(k) * 6 + 1) * sizeof(double),
                                         size_t(nred) * sizeof(double)})));
@@ -440,11 +454,18 @@ extern "C" int sfw3d_cost_grad(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, 
   double* res = cs.take<double>(size_t(k) * 6 + 1);  // [sumsq, sums...]
   double* partials = cs.take<double>(nred);
   SFW3D_TRY(upload_atoms(ctx, atoms, ad));
-  // model = H * sum w G  (A -> B, A used as pass scratch)
-  SFW3D_TRY(render_impl(ctx, dtype, dims, atoms, ad, k, A));
-  SFW3D_TRY(psf_apply_impl(ctx, psf, dtype, A, B, 0, A));
-  // resid = model - y -> A ; ||resid||^2
-  SFW3D_TRY(sumsq_diff_impl(ctx, dtype, n, B, y_dev, A, partials, res));
+  // model = H * sum w G, resid = model - y -> A with ||resid||^2 fused into
+  // the PSF's last pass (B scratch); else the separate residual pass
+  SFW3D_TRY(render_impl(ctx, dtype, dims, atoms, ad, k, B));
+  int nparts = 0;
+  SFW3D_TRY(psf_apply_resid(ctx, psf, dtype, B, A, B, y_dev, partials, nred, &nparts));
+  if (nparts > 0) {
+    SFW3D_TRY(sum_parts_impl(ctx, partials, nparts, res));
+  } else {
+    SFW3D_TRY(render_impl(ctx, dtype, dims, atoms, ad, k, A));
+    SFW3D_TRY(psf_apply_impl(ctx, psf, dtype, A, B, 0, A));
+    SFW3D_TRY(sumsq_diff_impl(ctx, dtype, n, B, y_dev, A, partials, res));
+  }
   if (grad_host || back_dev) {
     void* back = back_dev ? back_dev : B;
     SFW3D_TRY(psf_apply_impl(ctx, psf, dtype, A, back, 1, back == B ? A : B));

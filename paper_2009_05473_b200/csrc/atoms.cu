@@ -883,6 +883,12 @@ int atom_sums_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const void* fie
   return SFW3D_OK;
 }
 
+int sum_parts_impl(sfw3d_ctx* ctx, const double* parts, int n, double* out) {
+  final_sum_kernel<<<1, kRedThreads, 0, ctx->stream>>>(parts, n, out);
+  SFW3D_LAUNCH_CHECK(ctx);
+  return SFW3D_OK;
+}
+
 int sumsq_diff_impl(sfw3d_ctx* ctx, int dtype, int64_t n, const void* a, const void* b,
                     void* diff_out, double* partials, double* result_dev) {
   const int nblk = 4 * ctx->num_sms;

@@ -1590,17 +1590,35 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
   }
 }
 
-// [sum |b|, max |b|] from the mix's per-CTA statistics, fixed order
-__global__ void abs_reduce_kernel(const double* __restrict__ parts, int nblocks,
-                                  double* __restrict__ out) {
-  if (threadIdx.x != 0) return;
+// [sum |b|, max |b|] from the mix's per-CTA statistics: a fixed-order tree
+// (thread i sums blocks i, i + 256, ...; then a fixed shuffle / warp order)
+__global__ void __launch_bounds__(256) abs_reduce_kernel(const double* __restrict__ parts,
+                                                         int nblocks, double* __restrict__ out) {
+  __shared__ double st[8], sm[8];
   double t = 0.0, m = 0.0;
-  for (int b = 0; b < nblocks; ++b) {
+  for (int b = threadIdx.x; b < nblocks; b += 256) {
     t += parts[2 * b];
     m = fmax(m, parts[2 * b + 1]);
   }
-  out[0] = t;
-  out[1] = m;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    t += __shfl_down_sync(0xffffffffu, t, o);
+    m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    st[threadIdx.x >> 5] = t;
+    sm[threadIdx.x >> 5] = m;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tt = 0.0, mm = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      tt += st[w];
+      mm = fmax(mm, sm[w]);
+    }
+    out[0] = tt;
+    out[1] = mm;
+  }
 }
 
 __global__ void member_reduce_kernel(const Best* __restrict__ partial, int nblocks,
@@ -1832,7 +1850,7 @@ int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[
     else
       SFW3D_TRY(launch_ring2_all<float>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, ap));
     if (ap) {
-      abs_reduce_kernel<<<1, 32, 0, ctx->stream>>>(ap, nblocks, abs_dev);
+      abs_reduce_kernel<<<1, 256, 0, ctx->stream>>>(ap, nblocks, abs_dev);
       SFW3D_LAUNCH_CHECK(ctx);
       if (abs_done) *abs_done = true;
     }

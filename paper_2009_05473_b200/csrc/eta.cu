@@ -471,16 +471,33 @@ __global__ void abs_sum_kernel(const T* __restrict__ b, long long n, double* __r
   }
 }
 
-__global__ void abs_parts_reduce_kernel(const double* __restrict__ parts, int nblocks,
-                                        double* __restrict__ out) {
-  if (threadIdx.x != 0) return;
+__global__ void __launch_bounds__(256) abs_parts_reduce_kernel(const double* __restrict__ parts,
+                                                               int nblocks, double* __restrict__ out) {
+  __shared__ double st[8], sm[8];
   double t = 0.0, m = 0.0;
-  for (int i = 0; i < nblocks; ++i) {
+  for (int i = threadIdx.x; i < nblocks; i += 256) {  // fixed-order tree
     t += parts[2 * i];
     m = fmax(m, parts[2 * i + 1]);
   }
-  out[0] = t;
-  out[1] = m;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    t += __shfl_down_sync(0xffffffffu, t, o);
+    m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    st[threadIdx.x >> 5] = t;
+    sm[threadIdx.x >> 5] = m;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tt = 0.0, mm = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      tt += st[w];
+      mm = fmax(mm, sm[w]);
+    }
+    out[0] = tt;
+    out[1] = mm;
+  }
 }
 
 // gridDim.y CTAs per item (blockIdx.y = contiguous share of the template
@@ -1135,7 +1152,7 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
       const int nab = std::min(4 * ctx->num_sms, kRefPart / 2);  // partials in ref_part
       abs_sum_kernel<T><<<nab, 256, 0, ctx->stream>>>(b, n, ref_part);
       SFW3D_LAUNCH_CHECK(ctx);
-      abs_parts_reduce_kernel<<<1, 32, 0, ctx->stream>>>(ref_part, nab, ref_l1);
+      abs_parts_reduce_kernel<<<1, 256, 0, ctx->stream>>>(ref_part, nab, ref_l1);
       SFW3D_LAUNCH_CHECK(ctx);
     }
     std::vector<Best> hb0(nc);

@@ -184,6 +184,8 @@ int psf_apply_impl(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* 
 // axis) are written to plane a + shift of `out`.
 struct XRange {
   int begin = 0, end = -1, shift = 0;
+  double* sq = nullptr;     // (axis-0 tiled pass with an addend) per-CTA sum of squares
+  mutable int nsq = 0;      // number of partials written
 };
 int corr_pass_impl(sfw3d_ctx* ctx, int dtype, const void* in, void* out, const int dims[3], int axis,
                    const void* taps, int lo, int ntaps, const void* addend, double addend_w,
@@ -200,6 +202,10 @@ int slab_corr_impl(sfw3d_ctx* ctx, int dtype, const void* in, void* out, const i
                    const void* const taps[3], const int lo[3], const int nt[3], void* win, int H,
                    void* tmp, const SlabLink& link, const char* family);
 bool psf_use_fft(const sfw3d_psf* psf);
+int psf_apply_resid(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* in, void* out,
+                    void* tmp, const void* y, double* sq_parts, int max_parts, int* nparts);
+// fixed-order fp64 sum of n partials into *out (atoms.cu)
+int sum_parts_impl(sfw3d_ctx* ctx, const double* parts, int n, double* out);
 int psf_fft_apply(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* in, void* out,
                   int adjoint);
 void psf_fft_destroy(sfw3d_psf* psf);

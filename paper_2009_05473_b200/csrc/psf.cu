@@ -179,7 +179,7 @@ template <typename T, int J, int TI, int NT, int MINB = 1>
 __global__ void __launch_bounds__(NT, MINB) pass_tile2_kernel(
     const T* __restrict__ in, T* __restrict__ out, int n_axis, long long stride,
     const T* __restrict__ taps_g, int lo, int ntaps, const T* addend, T aw, T w, int a_begin,
-    int a_end, int out_shift) {
+    int a_end, int out_shift, double* __restrict__ sq_parts) {
   constexpr int G = NT / TI, To = J * G;
   constexpr int kVec = 16 / sizeof(T), kRowVecs = TI / kVec;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -268,9 +268,26 @@ __global__ void __launch_bounds__(NT, MINB) pass_tile2_kernel(
       }
     } else if (addend) {
       const T* pa = addend + o0;
+      double sq = 0.0;  // (fused residual: sum of squares of what is stored)
 #pragma unroll
       for (int j = 0; j < J; ++j, po += stride, pa += stride)
-        if (a1 + j < a_end) *po = T(aw * *pa + w * acc[j]);
+        if (a1 + j < a_end) {
+          const T v = T(aw * *pa + w * acc[j]);
+          *po = v;
+          sq += double(v) * double(v);
+        }
+      if (sq_parts) {  // per-CTA fp64 partial, fixed-order tree
+        __shared__ double red[NT / 32];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_down_sync(0xffffffffu, sq, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          double t = 0.0;
+          for (int q = 0; q < NT / 32; ++q) t += red[q];
+          sq_parts[blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z)] = t;
+        }
+      }
     } else {
 #pragma unroll
       for (int j = 0; j < J; ++j, po += stride)
@@ -519,7 +536,8 @@ int launch_tile2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axi
   const int ab = xr.begin, ae = xr.end < 0 ? n : xr.end;
   dim3 grid(unsigned((ae - ab + To - 1) / To), unsigned(stride / TI), unsigned(outer));
   pass_tile2_kernel<T, J, TI, NT, MINB><<<grid, NT, smem, ctx->stream>>>(
-      in, out, n, stride, taps, lo, ntaps, addend, T(aw), T(w), ab, ae, xr.shift);
+      in, out, n, stride, taps, lo, ntaps, addend, T(aw), T(w), ab, ae, xr.shift, xr.sq);
+  xr.nsq = int(grid.x * grid.y * grid.z);
   SFW3D_LAUNCH_CHECK(ctx);
   return SFW3D_OK;
 }
@@ -567,6 +585,10 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
   }
   constexpr bool f32 = sizeof(T) == 4;
   const bool wide = ntaps > kNarrowTaps;
+  if (xr.sq && !(axis == 0 && addend && (dims[1] * (long long)dims[2]) % 64 == 0 && ntaps <= 512)) {
+    set_error("internal: fused sum of squares needs an axis-0 tiled pass with an addend");
+    return SFW3D_EINVAL;
+  }
   if (axis != 0 && (xr.begin != 0 || xr.end >= 0 || xr.shift != 0)) {
     set_error("internal: output plane ranges apply to axis-0 passes only");
     return SFW3D_EINVAL;
@@ -654,6 +676,39 @@ int slab_corr_impl(sfw3d_ctx* ctx, int dtype, const void* in, void* out, const i
   const XRange xr{H, H + odims[0], -H};
   return corr_pass_impl(ctx, dtype, win, out, wd, 0, taps[0], lo[0], nt[0], nullptr, 0.0, 1.0,
                         family, &xr);
+}
+
+// out = H * in - y (the residual, forward.py:249-252) with the x pass's
+// epilogue subtracting y and adding up the fp64 squares per CTA into sq_parts
+// (returns their count in *nparts); 0 partials = not applicable (the caller
+// uses psf_apply_impl + sumsq_diff_impl).
+int psf_apply_resid(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* in, void* out,
+                    void* tmp, const void* y, double* sq_parts, int max_parts, int* nparts) {
+  *nparts = 0;
+  const int* dims = psf->dims;
+  const int nt0 = psf->hi[0] - psf->lo[0] + 1;
+  if (!psf->separable || (dims[1] * (long long)dims[2]) % 64 != 0 || nt0 > 512) return SFW3D_OK;
+  // (the x pass's grid: at most ceil(n / 64) x (ny nz / 64) CTAs)
+  const long long ctas = (long long)((dims[0] + 63) / 64) * (dims[1] * (long long)dims[2] / 64);
+  if (ctas > max_parts) return SFW3D_OK;
+  int lo[3], nt[3];
+  const void* tp[3];
+  for (int a = 0; a < 3; ++a) {
+    nt[a] = psf->hi[a] - psf->lo[a] + 1;
+    lo[a] = -psf->hi[a];
+    tp[a] = dtype == SFW3D_F64 ? static_cast<const void*>(psf->taps64[a] + nt[a])
+                               : static_cast<const void*>(psf->taps32[a] + nt[a]);
+  }
+  SFW3D_TRY(corr_pass_impl(ctx, dtype, in, out, dims, 2, tp[2], lo[2], nt[2], nullptr, 0.0, 1.0,
+                           "psf_pass"));
+  SFW3D_TRY(corr_pass_impl(ctx, dtype, out, tmp, dims, 1, tp[1], lo[1], nt[1], nullptr, 0.0, 1.0,
+                           "psf_pass"));
+  XRange xr;
+  xr.sq = sq_parts;
+  SFW3D_TRY(corr_pass_impl(ctx, dtype, tmp, out, dims, 0, tp[0], lo[0], nt[0], y, -1.0, 1.0,
+                           "psf_pass", &xr));
+  *nparts = xr.nsq;
+  return SFW3D_OK;
 }
 
 int psf_apply_slab(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* in, void* out,
