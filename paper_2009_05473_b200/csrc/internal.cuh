@@ -225,6 +225,25 @@ int atom_sums_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const void* fie
 int sumsq_diff_impl(sfw3d_ctx* ctx, int dtype, int64_t n, const void* a, const void* b,
                     void* diff_out, double* partials, double* result_dev);
 
+// Packed fp32 pairs (sm_100 FFMA2 / FMUL2: two independent RN operations per
+// instruction, bit-identical to the scalar ones). Low half = first element.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 pack2(float lo, float hi) {
+  return (f32x2)__float_as_uint(lo) | ((f32x2)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ float lo32(f32x2 v) { return __uint_as_float(unsigned(v)); }
+__device__ __forceinline__ float hi32(f32x2 v) { return __uint_as_float(unsigned(v >> 32)); }
+
 // Asynchronous global->shared copies (LDGSTS): staging loops issue all of
 // their copies without a register round trip, then wait once.
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {

@@ -599,7 +599,8 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
         if constexpr (f32) return launch_z2<T, 32, 5>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
         else return launch_z2<T, 32, 1>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
       }
-      return launch_z2<T, 16>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
+      if constexpr (f32) return launch_z2<T, 16, 8>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
+      else return launch_z2<T, 16>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
     }
     return wide ? launch_z<T, 32>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w)
                 : launch_z<T, 16>(ctx, in, out, dims, taps, lo, ntaps, addend, aw, w);
@@ -618,7 +619,8 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
       if constexpr (f32) return launch_tile2<T, 32, 3>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
       else return launch_tile2<T, 32, 1>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
     }
-    return launch_tile2<T, 16>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
+    if constexpr (f32) return launch_tile2<T, 16, 5>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
+    else return launch_tile2<T, 16>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
   }
   return wide ? launch_strided<T, 32>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr)
               : launch_strided<T, 8>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);

@@ -1,6 +1,5 @@
-"""Time the 1-D pass kernels at 512^3 fp32 for a narrow (15-tap) and a wide
-(89-tap) separable kernel: forward + adjoint PSF application, per-family
-device time. Run under different SFW3D_PASS_VARIANT values."""
+"""Time the 1-D pass kernels at 512^3 fp32 for narrow and wide separable
+kernels: adjoint PSF application (z, y, x passes), per-family device time."""
 import os
 import sys
 from pathlib import Path
@@ -18,7 +17,7 @@ n = int(os.environ.get("N", "512"))
 dims = (n, n, n)
 x = torch.randn(dims, device="cuda", dtype=torch.float32)
 ctx = N.context()
-for half in (7, 44):
+for half in (4, 7, 11, 15, 44):
     psf = P.Psf(P.Volume(box_psf_kernel(dims, (3.0,) * 3, (half,) * 3)), normalize=False)
     out = torch.empty_like(x)
     for _ in range(2):
@@ -31,5 +30,5 @@ for half in (7, 44):
     ctx.profile(False)
     per = ms / cnt
     gbs = 2 * x.numel() * 4 / (per / 1e3) / 1e9
-    print(f"variant={os.environ.get('SFW3D_PASS_VARIANT', '0')} taps={2 * half + 1}: "
+    print(f"taps={2 * half + 1}: "
           f"{per:.3f} ms/pass (avg of z,y,x) -> {gbs:.0f} GB/s (read+write)")
