@@ -80,18 +80,64 @@ void lsq_qr(const std::vector<ld>& A, int M, const std::vector<int>& cols, const
   for (int j = 0; j < p; ++j) z[j] *= scale[j];
 }
 
+// Householder compression of a tall least-squares problem: R (p x p upper,
+// column-major in a p x p block) and c = (Q^T g)[0:p] with A = Q R (thin).
+// min ||A z - g||^2 + |D z|^2 = min ||[R; D] z - [c; 0]||^2 + const, so a
+// ridge sweep solves (2p x p) systems instead of (M + p) x p ones.
+void qr_compress(const std::vector<ld>& A, int M, int p, const std::vector<ld>& g,
+                 std::vector<ld>& R, std::vector<ld>& c) {
+  std::vector<ld> B(A.begin(), A.begin() + size_t(M) * p), rhs(g.begin(), g.begin() + M), v(M);
+  for (int j = 0; j < p; ++j) {
+    ld* col = &B[size_t(j) * M];
+    ld nrm = 0.0L;
+    for (int i = j; i < M; ++i) nrm += col[i] * col[i];
+    nrm = std::sqrt(nrm);
+    if (nrm == 0.0L) continue;
+    const ld alpha = col[j] > 0 ? -nrm : nrm;
+    for (int i = j; i < M; ++i) v[i] = col[i];
+    v[j] -= alpha;
+    ld vn = 0.0L;
+    for (int i = j; i < M; ++i) vn += v[i] * v[i];
+    if (vn == 0.0L) continue;
+    auto apply = [&](ld* x) {
+      ld dot = 0.0L;
+      for (int i = j; i < M; ++i) dot += v[i] * x[i];
+      const ld f = 2.0L * dot / vn;
+      for (int i = j; i < M; ++i) x[i] -= f * v[i];
+    };
+    for (int k = j; k < p; ++k) apply(&B[size_t(k) * M]);
+    apply(rhs.data());
+  }
+  R.assign(size_t(p) * p, 0.0L);
+  for (int k = 0; k < p; ++k)
+    for (int i = 0; i <= k && i < M; ++i) R[size_t(k) * p + i] = B[size_t(k) * M + i];
+  c.assign(rhs.begin(), rhs.begin() + std::min(p, M));
+  c.resize(p, 0.0L);
+}
+
 void nnls(const std::vector<double>& Ad, int M, int N, const std::vector<double>& gd,
           std::vector<double>& xd) {
-  std::vector<ld> A(Ad.begin(), Ad.end()), g(gd.begin(), gd.end()), x(N, 0.0L), r(M), cn(N);
+  std::vector<ld> A(Ad.begin(), Ad.end()), g(gd.begin(), gd.end()), x(N, 0.0L), cn(N);
   std::vector<char> passive(N, 0), banned(N, 0);
+  ld gn = 0.0L;
+  for (ld v : g) gn += v * v;
+  const ld tol = 1e-17L * std::sqrt(gn);
+  if (M > N) {
+    // tall problem: compress to the N x N triangular form once (A = Q R,
+    // A^T (g - A x) = R^T (Q^T g - R x)): every residual, gradient and
+    // passive-set solve below then runs on N rows instead of M
+    std::vector<ld> R, c;
+    qr_compress(A, M, N, g, R, c);
+    A.swap(R);
+    g.swap(c);
+    M = N;
+  }
+  std::vector<ld> r(M);
   for (int j = 0; j < N; ++j) {
     ld s = 0.0L;
     for (int i = 0; i < M; ++i) s += A[size_t(j) * M + i] * A[size_t(j) * M + i];
     cn[j] = s > 0.0L ? std::sqrt(s) : 1.0L;
   }
-  ld gn = 0.0L;
-  for (ld v : g) gn += v * v;
-  const ld tol = 1e-17L * std::sqrt(gn);
   for (int outer = 0; outer < 8 * N; ++outer) {
     for (int i = 0; i < M; ++i) {
       ld s = g[i];
@@ -409,22 +455,46 @@ void fit_signed_members(BasisSet* s, const std::vector<BasisCandidate>& cands, i
     if (ok) todo.push_back(c);
   }
   if (todo.empty()) return;
-  const int M = int(Sfit.size()), ncol = nt + 1, Mt = M + ncol;
+  const int M = int(Sfit.size()), ncol = nt + 1, Mt = 2 * ncol;
   std::vector<std::vector<double>> wsig(nc);
   std::vector<double> w0sig(nc, 0.0), esig(nc, INFINITY), dsig(nc, INFINITY), mass(nc, 0.0);
   auto fit_one = [&](int c) {
     const BasisCandidate& bc = cands[c];
+    // the lattice fit, compressed once (qr_compress); each ridge weight then
+    // solves [R; sqrt(mu) diag(pen)] z = [Q^T g; 0]
     std::vector<ld> A(size_t(Mt) * ncol, 0.0L), g(Mt, 0.0L);
-    for (int i = 0; i < M; ++i) {
-      g[i] = profile(Sfit[i], bc.sigma, bc.d);
-      for (int k = 0; k < nt; ++k) A[size_t(k) * Mt + i] = std::exp(-(ld)s->betas[k] * Sfit[i]);
-      A[size_t(nt) * Mt + i] = Sfit[i] == 0.0 ? 1.0L : 0.0L;
+    {
+      std::vector<ld> Af(size_t(M) * ncol, 0.0L), gf(M, 0.0L), Rc, cc;
+      for (int i = 0; i < M; ++i) {
+        gf[i] = profile(Sfit[i], bc.sigma, bc.d);
+        for (int k = 0; k < nt; ++k) Af[size_t(k) * M + i] = std::exp(-(ld)s->betas[k] * Sfit[i]);
+        Af[size_t(nt) * M + i] = Sfit[i] == 0.0 ? 1.0L : 0.0L;
+      }
+      qr_compress(Af, M, ncol, gf, Rc, cc);
+      for (int k = 0; k < ncol; ++k)
+        for (int i = 0; i < ncol; ++i) A[size_t(k) * Mt + i] = Rc[size_t(k) * ncol + i];
+      for (int i = 0; i < ncol; ++i) g[i] = cc[i];
     }
     std::vector<double> pen(ncol);
     for (int k = 0; k < nt; ++k) pen[k] = Sk[k] * (rho[k] + gmix * (1.0 + rho[k])) + ext[k];
     pen[nt] = gmix;
     std::vector<int> cols(ncol);
     for (int k = 0; k < ncol; ++k) cols[k] = k;
+    // the direct template at every representative triple (independent of the
+    // ridge weight: tabulated once)
+    const size_t nrx = reps[0].size(), nry = reps[1].size(), nrz = reps[2].size();
+    std::vector<double> gdt(nrx * nry * nrz, 0.0);
+    for (size_t ix = 0; ix < nrx; ++ix)
+      for (size_t iy = 0; iy < nry; ++iy) {
+        const int tx = reps[0][ix].t, ty = reps[1][iy].t;
+        if (std::abs(tx) > bc.hi[0] || std::abs(ty) > bc.hi[1]) continue;
+        const double sxy = double(tx) * tx + double(ty) * ty;
+        for (size_t iz = 0; iz < nrz; ++iz) {
+          const int tz = reps[2][iz].t;
+          if (std::abs(tz) <= bc.hi[2])
+            gdt[(ix * nry + iy) * nrz + iz] = profile(sxy + double(tz) * tz, bc.sigma, bc.d);
+        }
+      }
     // the direct template on its box, per representative triple
     double m = 0.0;
     for (int x = bc.lo[0]; x <= bc.hi[0]; ++x)
@@ -439,7 +509,7 @@ void fit_signed_members(BasisSet* s, const std::vector<BasisCandidate>& cands, i
     // one ridge weight 10^e (e < kRidgeMin: none): solve, bound, keep the best
     auto try_ridge = [&](int e) {
       const ld mu = e < kRidgeMin ? 0.0L : std::pow(10.0L, (ld)e);
-      for (int k = 0; k < ncol; ++k) A[size_t(k) * Mt + M + k] = std::sqrt(mu) * (ld)pen[k];
+      for (int k = 0; k < ncol; ++k) A[size_t(k) * Mt + ncol + k] = std::sqrt(mu) * (ld)pen[k];
       std::vector<ld> z;
       lsq_qr(A, Mt, cols, g, z);
       std::vector<double> w(nt);
@@ -459,18 +529,14 @@ void fit_signed_members(BasisSet* s, const std::vector<BasisCandidate>& cands, i
         for (size_t iy = 0; iy < reps[1].size(); ++iy) {
           const Rep ry = reps[1][iy];
           for (int k = 0; k < nt; ++k) P[k] = w[k] * fval[0][ix][k] * fval[1][iy][k];
-          const bool in_xy = std::abs(rx.t) <= bc.hi[0] && std::abs(ry.t) <= bc.hi[1];
-          const double sxy = double(rx.t) * rx.t + double(ry.t) * ry.t;
+          const double* gdr = &gdt[(ix * nry + iy) * nrz];
           double acc = 0.0;
-          for (size_t iz = 0; iz < reps[2].size(); ++iz) {
+          for (size_t iz = 0; iz < nrz; ++iz) {
             const Rep rz = reps[2][iz];
             const std::vector<double>& fz = fval[2][iz];
             double gv = (rx.t == 0 && ry.t == 0 && rz.t == 0) ? w0 : 0.0;
             for (int k = 0; k < nt; ++k) gv += P[k] * fz[k];
-            const double gd = in_xy && std::abs(rz.t) <= bc.hi[2]
-                                  ? profile(sxy + double(rz.t) * rz.t, bc.sigma, bc.d)
-                                  : 0.0;
-            acc += rz.w * std::fabs(gv - gd);
+            acc += rz.w * std::fabs(gv - gdr[iz]);
           }
           D1 += rx.w * ry.w * acc;
         }
