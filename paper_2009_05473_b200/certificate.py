@@ -265,9 +265,21 @@ def refine_eta_max_dev(residual, lam: float, psf: Psf, start: AtomParams, bounds
     if back is None:
         back = psf_apply_dev(psf, residual, True)
 
+    # the L-BFGS-B callback calls sfw3d_atom_sums ~30 times per refine: its
+    # arguments are bound once (context, field pointer, dims, buffers)
+    from .forward import code_of
+    ctx = N.context(back.device.index)
+    fn, handle, code = N.lib().sfw3d_atom_sums, ctx.handle, code_of(back)
+    dims_a, bptr = N.dims_arg(back.shape), N.ptr(back)
+    row = np.empty((1, 6))
+    row[0, 0] = 1.0
+    out = np.empty((1, 6))
+    row_p, out_p = N.f64_ptr(row), N.f64_ptr(out)
+
     def neg_eta(vec):
-        row = np.array([[1.0, *np.asarray(vec, dtype=float)]])
-        s = atom_sums_dev(back, row)[0]
+        row[0, 1:] = vec
+        N.check(fn(handle, code, dims_a, bptr, row_p, 1, out_p))
+        s = out[0]
         val = float(s[0]) / lam
         grad = s[1:] / lam
         if not (np.isfinite(val) and np.isfinite(grad).all()):

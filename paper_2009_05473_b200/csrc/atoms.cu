@@ -842,10 +842,16 @@ int atom_sums_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const void* fie
   if (k == 0) return SFW3D_OK;
   std::vector<Chunk> chunks;
   std::vector<int> first;
+  // chunk size: the defaults amortise the per-chunk row table over many
+  // voxels, but a few atoms (the certificate refine's single atom) would then
+  // fill only a fraction of the SMs: aim at >= 4 chunks per SM
+  long long total = 0;
+  for (const auto& a : atoms) total += (long long)a.len[0] * a.len[1] * a.len[2];
+  const int fill = int(std::max<long long>(512, total / (4LL * ctx->num_sms)));
   if (dtype == SFW3D_F64 || !small_boxes(atoms, dims))
-    chunk_plan(atoms, chunks, first);
+    chunk_plan(atoms, chunks, first, std::min(kChunk, fill));
   else
-    chunk_plan(atoms, chunks, first, std::max(kChunk, chunk32()), kMaxRows32);
+    chunk_plan(atoms, chunks, first, std::min(std::max(kChunk, chunk32()), fill), kMaxRows32);
   SFW3D_TRY(ensure_device(ctx, ctx->ws_plan,
                           Carver::need({chunks.size() * sizeof(Chunk), first.size() * sizeof(int),
                                         chunks.size() * 6 * sizeof(double)})));
