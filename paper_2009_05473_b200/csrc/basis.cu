@@ -583,10 +583,12 @@ void fit_signed_members(BasisSet* s, const std::vector<BasisCandidate>& cands, i
 
 }  // namespace
 
-// fp32 default: config 4 measured 26 -> 12 shared terms (with the fp32
-// signed acceptance 0.1), 31.3 -> 13.5 ms per certificate, ~360 refined
-// voxels (the table option "loose_tol" overrides; 0 disables)
-constexpr double kLooseF32 = 1e-5;
+// fp32 default: config 4 measured 26 -> 12 shared terms at 1e-5 (with the
+// fp32 signed acceptance 0.1), 31.3 -> 12.5 ms per certificate; 5e-5 drops one
+// more wide term (11 terms, ~1240 refined voxels, 11.7 ms; tools/loose_scan.py:
+// 1e-4 and looser lose members to the direct kernels). The table option
+// "loose_tol" overrides; 0 disables.
+constexpr double kLooseF32 = 5e-5;
 double basis_loose_tol(int dtype) { return dtype == SFW3D_F32 ? kLooseF32 : 0.0; }
 
 int basis_set_build(const int dims[3], const std::vector<BasisCandidate>& cands, int dtype,
