@@ -297,6 +297,103 @@ __global__ void __launch_bounds__(NT, MINB) pass_tile2_kernel(
 }
 
 
+// Strided axes, fp32, WIDE filters: pass_tile2_kernel with packed FFMA2.
+// Lane l owns the inner pair (2l, 2l + 1) of a 64-wide column block (one
+// 8-byte LDS per staged row), so every tap is one FFMA2 per output pair: half
+// the FMA issue slots of the scalar tile at the same per-element arithmetic
+// (two independent RN FMAs, bit-identical results). 8 groups of J outputs
+// along the axis per CTA (To = 8 J); taps stored duplicated (t, t).
+template <int J, int MINB>
+__global__ void __launch_bounds__(256, MINB) pass_tile2x2_kernel(
+    const float* __restrict__ in, float* __restrict__ out, int n_axis, long long stride,
+    const float* __restrict__ taps_g, int lo, int ntaps, int a_begin, int a_end, int out_shift) {
+  constexpr int TI = 64, G = 8, To = J * G;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int nt4 = (ntaps + 3) & ~3;
+  f32x2* taps2 = reinterpret_cast<f32x2*>(smem_raw);        // [nt4] (t, t)
+  float* tile = reinterpret_cast<float*>(taps2 + nt4);      // [To + nt4][TI]
+  const int rows = To + nt4;
+  const int a0 = a_begin + blockIdx.x * To;
+  const long long base0 = (long long)blockIdx.z * n_axis * stride + (long long)blockIdx.y * TI;
+  for (int q = threadIdx.x; q < nt4; q += 256) {
+    const float t = q < ntaps ? taps_g[q] : 0.f;
+    taps2[q] = pack2(t, t);
+  }
+  {
+    constexpr int kRowVecs = TI / 4, dr = 256 / kRowVecs;
+    const int c = (threadIdx.x % kRowVecs) * 4;
+    int r = threadIdx.x / kRowVecs;
+    int a = (a0 + lo + r) % n_axis;
+    if (a < 0) a += n_axis;
+    const float* src = in + base0 + c;
+    float* dst = tile + r * TI + c;
+    if (a0 + lo >= 0 && a0 + lo + rows <= n_axis) {
+      const long long step = (long long)dr * stride;
+      const float* p = src + (long long)a * stride;
+      for (; r < rows; r += dr, dst += dr * TI, p += step) cp_async16(dst, p);
+    } else if (n_axis >= dr) {
+      for (; r < rows; r += dr, dst += dr * TI) {
+        cp_async16(dst, src + (long long)a * stride);
+        a += dr;
+        a = a >= n_axis ? a - n_axis : a;
+      }
+    } else {
+      for (; r < rows; r += dr, dst += dr * TI) {
+        cp_async16(dst, src + (long long)a * stride);
+        a = (a + dr) % n_axis;
+      }
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const int lane = threadIdx.x & 31, ag = threadIdx.x >> 5;
+  const f32x2* src = reinterpret_cast<const f32x2*>(tile + (ag * J) * TI) + lane;  // row pitch TI / 2 pairs
+  constexpr int P = TI / 2;
+  f32x2 W[J], acc[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    W[j] = src[j * P];
+    acc[j] = 0ull;
+  }
+  int q0 = 0;
+  for (; q0 + J <= nt4; q0 += J) {
+#pragma unroll
+    for (int r = 0; r < J; r += 2) {
+      const ulonglong2 t2 = *reinterpret_cast<const ulonglong2*>(taps2 + q0 + r);
+      const f32x2 tt[2] = {t2.x, t2.y};
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+#pragma unroll
+        for (int j = 0; j < J; ++j) acc[j] = fma2(tt[k], W[(r + k + j) % J], acc[j]);
+        W[r + k] = src[(q0 + r + k + J) * P];
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < J; r += 2) {  // remaining taps (< J, a multiple of 4)
+    if (q0 + r >= nt4) break;
+    const ulonglong2 t2 = *reinterpret_cast<const ulonglong2*>(taps2 + q0 + r);
+    const f32x2 tt[2] = {t2.x, t2.y};
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+#pragma unroll
+      for (int j = 0; j < J; ++j) acc[j] = fma2(tt[k], W[(r + k + j) % J], acc[j]);
+      W[r + k] = src[(q0 + r + k + J) * P];
+    }
+  }
+  const int a1 = a0 + ag * J;
+  f32x2* po = reinterpret_cast<f32x2*>(out + base0 + (long long)(a1 + out_shift) * stride) + lane;
+  const long long pstep = stride / 2;
+  if (a1 + J <= a_end) {
+#pragma unroll
+    for (int j = 0; j < J; ++j, po += pstep) *po = acc[j];
+  } else {
+#pragma unroll
+    for (int j = 0; j < J; ++j, po += pstep)
+      if (a1 + j < a_end) *po = acc[j];
+  }
+}
+
 // Contiguous axis (2), nz % 4 == 0: a CTA owns 32 rows (lane = row) x 4 J
 // outputs (warp = J-column group). The staged row span starts at the aligned
 // column floor4(z0 + lo); the misalignment sh = lo mod 4 is absorbed by sh
@@ -543,6 +640,28 @@ int launch_tile2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axi
 }
 
 
+template <int J, int MINB>
+int launch_tile2x2(sfw3d_ctx* ctx, const float* in, float* out, const int dims[3], int axis,
+                   const float* taps, int lo, int ntaps, const XRange& xr) {
+  constexpr int TI = 64, To = J * 8;
+  long long stride = 1;
+  for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
+  long long outer = 1;
+  for (int a = 0; a < axis; ++a) outer *= dims[a];
+  const int n = dims[axis];
+  const int nt4 = (ntaps + 3) & ~3;
+  const size_t smem = size_t(nt4) * 8 + size_t(To + nt4) * TI * sizeof(float);
+  if (smem > 48 * 1024)
+    SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_tile2x2_kernel<J, MINB>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const int ab = xr.begin, ae = xr.end < 0 ? n : xr.end;
+  dim3 grid(unsigned((ae - ab + To - 1) / To), unsigned(stride / TI), unsigned(outer));
+  pass_tile2x2_kernel<J, MINB><<<grid, 256, smem, ctx->stream>>>(in, out, n, stride, taps, lo,
+                                                                 ntaps, ab, ae, xr.shift);
+  SFW3D_LAUNCH_CHECK(ctx);
+  return SFW3D_OK;
+}
+
 template <typename T, int J, int MINB = 1>
 int launch_z2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* taps, int lo,
               int ntaps, const T* addend, double aw, double w) {
@@ -616,8 +735,13 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
       else return launch_tile2<T, 32, 1, 128>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
     }
     if (dims[axis] >= 128 && wide) {
-      if constexpr (f32) return launch_tile2<T, 32, 3>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
-      else return launch_tile2<T, 32, 1>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
+      if constexpr (f32) {
+        if (!addend && w == 1.0 && xr.sq == nullptr)  // packed FFMA2 tile
+          return launch_tile2x2<16, 3>(ctx, in, out, dims, axis, taps, lo, ntaps, xr);
+        return launch_tile2<T, 32, 3>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
+      } else {
+        return launch_tile2<T, 32, 1>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
+      }
     }
     if constexpr (f32) return launch_tile2<T, 16, 5>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
     else return launch_tile2<T, 16>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
