@@ -1739,8 +1739,7 @@ static int launch_mix_nm(sfw3d_ctx* ctx, int nblocks, const void* b, const void*
   const size_t smem = (size_t(nt) * NM + NM) * sizeof(T);
   if (col) {
     if (smem > 48 * 1024)
-      SFW3D_CUDA_TRY(cudaFuncSetAttribute(mix_argmax_kernel<T, NM, V, true>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      SFW3D_CUDA_TRY(allow_dynamic_smem(reinterpret_cast<const void*>(mix_argmax_kernel<T, NM, V, true>), size_t(int(smem))));
     mix_argmax_kernel<T, NM, V, true><<<nblocks, kMixThreads, smem, ctx->stream>>>(
         static_cast<const T*>(b), static_cast<const T*>(terms), n, nt, nmm, m0,
         static_cast<const T*>(s->W_dev), static_cast<const T*>(s->w0_dev), s->cid_dev, dims[0],
@@ -1748,8 +1747,7 @@ static int launch_mix_nm(sfw3d_ctx* ctx, int nblocks, const void* b, const void*
     return SFW3D_OK;
   }
   if (smem > 48 * 1024)
-    SFW3D_CUDA_TRY(cudaFuncSetAttribute(mix_argmax_kernel<T, NM, V>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    SFW3D_CUDA_TRY(allow_dynamic_smem(reinterpret_cast<const void*>(mix_argmax_kernel<T, NM, V>), size_t(int(smem))));
   mix_argmax_kernel<T, NM, V><<<nblocks, kMixThreads, smem, ctx->stream>>>(
       static_cast<const T*>(b), static_cast<const T*>(terms), n, nt, nmm, m0,
       static_cast<const T*>(s->W_dev), static_cast<const T*>(s->w0_dev), s->cid_dev, dims[0],
@@ -1768,8 +1766,7 @@ static int launch_ring2(sfw3d_ctx* ctx, int nblocks, const void* b, const void* 
                       (size_t(nt) * NMD + NMD + size_t(NMD + 8) * kMixThreads) * sizeof(T) +
                       size_t(NMD + 8) * kMixThreads * sizeof(int) + size_t(nt) * sizeof(int) + 16;
   if (smem > 48 * 1024)
-    SFW3D_CUDA_TRY(cudaFuncSetAttribute(mix_ring2_kernel<T, NMD, NS>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    SFW3D_CUDA_TRY(allow_dynamic_smem(reinterpret_cast<const void*>(mix_ring2_kernel<T, NMD, NS>), size_t(int(smem))));
   mix_ring2_kernel<T, NMD, NS><<<nblocks, kMixThreads, smem, ctx->stream>>>(
       static_cast<const T*>(b), static_cast<const T*>(terms), n, nt,
       static_cast<const T*>(s->Wd_dev) + size_t(d0) * nt, static_cast<const T*>(s->w0d_dev) + d0,
@@ -1843,8 +1840,7 @@ static int launch_mix(sfw3d_ctx* ctx, int nblocks, const void* b, const void* te
     const size_t smem = (size_t(kMixNS) * kMixThreads * V4 + size_t(nt) * 16 + 16 + 16 * kMixThreads) * sizeof(T) +
                         16 * kMixThreads * sizeof(int);
     if (smem > 48 * 1024)
-      SFW3D_CUDA_TRY(cudaFuncSetAttribute(mix_ring_kernel<T, 16>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      SFW3D_CUDA_TRY(allow_dynamic_smem(reinterpret_cast<const void*>(mix_ring_kernel<T, 16>), size_t(int(smem))));
     mix_ring_kernel<T, 16><<<nblocks, kMixThreads, smem, ctx->stream>>>(
         static_cast<const T*>(b), static_cast<const T*>(terms), n, nt, nmm, m0,
         static_cast<const T*>(s->W_dev), static_cast<const T*>(s->w0_dev), s->cid_dev, dims[0],

@@ -730,8 +730,7 @@ static int fold_smem(const CandHost& c, int esize) {
 template <typename T, int KJ, int NWY, bool AG = false>
 static int launch_fold(sfw3d_ctx* ctx, dim3 grid, int smem, const T* bpad, const Geo& g,
                        const CandDev& cd, T* fld, Best* partial) {
-  SFW3D_CUDA_TRY(cudaFuncSetAttribute(eta_fold_kernel<T, KJ, NWY, AG>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  SFW3D_CUDA_TRY(allow_dynamic_smem(reinterpret_cast<const void*>(eta_fold_kernel<T, KJ, NWY, AG>), size_t(smem)));
   eta_fold_kernel<T, KJ, NWY, AG><<<grid, kThreads * NWY, smem, ctx->stream>>>(bpad, g, cd, fld, partial);
   SFW3D_LAUNCH_CHECK(ctx);
   return SFW3D_OK;
@@ -1300,8 +1299,7 @@ int eta_typed(sfw3d_ctx* ctx, const sfw3d_table* t, const void* residual, double
         }
         gc.brows = std::min(brows, c.lb);
         const int smem = (kTY + gc.brows - 1) * row_bytes;
-        SFW3D_CUDA_TRY(cudaFuncSetAttribute(eta_direct_kernel<T>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        SFW3D_CUDA_TRY(allow_dynamic_smem(reinterpret_cast<const void*>(eta_direct_kernel<T>), size_t(smem)));
         SFW3D_PROF(ctx, "eta_direct");
         dim3 grid(unsigned(nty * ntz), unsigned(nxp));
         eta_direct_kernel<T><<<grid, kThreads, smem, ctx->stream>>>(bpad, gc, cd, fld, partial);

@@ -6,6 +6,8 @@
 
 #include <cmath>
 #include <string>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "../../include/sfw3d_cuda.h"
@@ -243,6 +245,24 @@ __device__ __forceinline__ f32x2 pack2(float lo, float hi) {
 }
 __device__ __forceinline__ float lo32(f32x2 v) { return __uint_as_float(unsigned(v)); }
 __device__ __forceinline__ float hi32(f32x2 v) { return __uint_as_float(unsigned(v >> 32)); }
+
+// Raise a kernel's dynamic shared-memory limit MONOTONICALLY (per device):
+// contexts on several host threads launch the same kernel with different
+// sizes, and a per-launch cudaFuncSetAttribute could lower the limit under a
+// concurrent launch ("invalid argument").
+inline cudaError_t allow_dynamic_smem(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> lim;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> guard(mu);
+  size_t& cur = lim[{dev, func}];
+  if (bytes <= cur) return cudaSuccess;
+  const cudaError_t e =
+      cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
 
 // Asynchronous global->shared copies (LDGSTS): staging loops issue all of
 // their copies without a register round trip, then wait once.

@@ -573,8 +573,7 @@ static int nnlasso_run(sfw3d_ctx* ctx, int k, const double* gram_host, const dou
     }
     const size_t smem = (size_t(kQpMaxFree) * kQpMaxFree + 3 * size_t(k)) * sizeof(double) +
                         size_t(k) * sizeof(int);
-    SFW3D_CUDA_TRY(cudaFuncSetAttribute(nnqp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        int(smem)));
+    SFW3D_CUDA_TRY(allow_dynamic_smem(reinterpret_cast<const void*>(nnqp_kernel), size_t(int(smem))));
     SFW3D_PROF(ctx, "cd");
     nnqp_kernel<<<1, kQpThreads, smem, ctx->stream>>>(k, g, bd, lam, tol, max_iter, wd, info, kkt);
     SFW3D_LAUNCH_CHECK(ctx);
@@ -585,11 +584,11 @@ static int nnlasso_run(sfw3d_ctx* ctx, int k, const double* gram_host, const dou
     SFW3D_PROF(ctx, "cd");
     if (gs) {
       if (smem > 48 * 1024)
-        SFW3D_CUDA_TRY(cudaFuncSetAttribute(cd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        SFW3D_CUDA_TRY(allow_dynamic_smem(reinterpret_cast<const void*>(cd_kernel<true>), size_t(int(smem))));
       cd_kernel<true><<<1, 32, smem, ctx->stream>>>(k, g, bd, lam, tol, max_iter, wd, info, kkt);
     } else {
       if (smem > 48 * 1024)
-        SFW3D_CUDA_TRY(cudaFuncSetAttribute(cd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        SFW3D_CUDA_TRY(allow_dynamic_smem(reinterpret_cast<const void*>(cd_kernel<false>), size_t(int(smem))));
       cd_kernel<false><<<1, 32, smem, ctx->stream>>>(k, g, bd, lam, tol, max_iter, wd, info, kkt);
     }
     SFW3D_LAUNCH_CHECK(ctx);

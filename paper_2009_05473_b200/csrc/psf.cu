@@ -588,8 +588,7 @@ int launch_strided(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int a
   dim3 grid(unsigned((ae - ab + J - 1) / J), unsigned((stride + 255) / 256), unsigned(outer));
   const size_t smem = size_t((ntaps + J - 1) / J * J) * sizeof(T);
   if (smem > 48 * 1024)
-    SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_strided_kernel<T, J>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    SFW3D_CUDA_TRY(allow_dynamic_smem(reinterpret_cast<const void*>(pass_strided_kernel<T, J>), size_t(int(smem))));
   pass_strided_kernel<T, J><<<grid, 256, smem, ctx->stream>>>(
       in, out, n, stride, taps, lo, ntaps, addend, T(aw), T(w), ab, ae, xr.shift);
   SFW3D_LAUNCH_CHECK(ctx);
@@ -606,8 +605,7 @@ int launch_z(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* ta
   const int pitch = width | 1;  // odd: 32 lanes on 32 rows hit 32 banks
   const size_t smem = (size_t(npad) + size_t(kZRows) * pitch) * sizeof(T);
   if (smem > 48 * 1024)
-    SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_z_kernel<T, J>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    SFW3D_CUDA_TRY(allow_dynamic_smem(reinterpret_cast<const void*>(pass_z_kernel<T, J>), size_t(int(smem))));
   dim3 grid(unsigned((dims[2] + J * kZWarps - 1) / (J * kZWarps)),
             unsigned((nrows + kZRows - 1) / kZRows));
   pass_z_kernel<T, J><<<grid, 32 * kZWarps, smem, ctx->stream>>>(in, out, dims[2], nrows, taps, lo,
@@ -628,8 +626,7 @@ int launch_tile2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axi
   const int nt4 = (ntaps + 3) & ~3;
   const size_t smem = (size_t(nt4) + size_t(To + nt4) * TI) * sizeof(T);
   if (smem > 48 * 1024)
-    SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_tile2_kernel<T, J, TI, NT, MINB>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    SFW3D_CUDA_TRY(allow_dynamic_smem(reinterpret_cast<const void*>(pass_tile2_kernel<T, J, TI, NT, MINB>), size_t(int(smem))));
   const int ab = xr.begin, ae = xr.end < 0 ? n : xr.end;
   dim3 grid(unsigned((ae - ab + To - 1) / To), unsigned(stride / TI), unsigned(outer));
   pass_tile2_kernel<T, J, TI, NT, MINB><<<grid, NT, smem, ctx->stream>>>(
@@ -652,8 +649,7 @@ int launch_tile2x2(sfw3d_ctx* ctx, const float* in, float* out, const int dims[3
   const int nt4 = (ntaps + 3) & ~3;
   const size_t smem = size_t(nt4) * 8 + size_t(To + nt4) * TI * sizeof(float);
   if (smem > 48 * 1024)
-    SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_tile2x2_kernel<J, MINB>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    SFW3D_CUDA_TRY(allow_dynamic_smem(reinterpret_cast<const void*>(pass_tile2x2_kernel<J, MINB>), size_t(int(smem))));
   const int ab = xr.begin, ae = xr.end < 0 ? n : xr.end;
   dim3 grid(unsigned((ae - ab + To - 1) / To), unsigned(stride / TI), unsigned(outer));
   pass_tile2x2_kernel<J, MINB><<<grid, 256, smem, ctx->stream>>>(in, out, n, stride, taps, lo,
@@ -678,8 +674,7 @@ int launch_z2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* t
   }
   const size_t smem = (size_t(nt4) + 8 + size_t(32) * pitch) * sizeof(T);
   if (smem > 48 * 1024)
-    SFW3D_CUDA_TRY(cudaFuncSetAttribute(pass_z2_kernel<T, J, MINB>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    SFW3D_CUDA_TRY(allow_dynamic_smem(reinterpret_cast<const void*>(pass_z2_kernel<T, J, MINB>), size_t(int(smem))));
   dim3 grid(unsigned((dims[2] + 4 * J - 1) / (4 * J)), unsigned((nrows + 31) / 32));
   pass_z2_kernel<T, J, MINB><<<grid, 128, smem, ctx->stream>>>(in, out, dims[2], nrows, taps, lo, ntaps,
                                                          pitch, addend, T(aw), T(w));
