@@ -458,20 +458,45 @@ def costgrad_workload(args, dev):
         cost_grad_dev(psf, y, perts[i % 100], 0.1)
     s = (time.perf_counter() - t0) / args.cg_steps
     ctx.profile(True)
-    cost_grad_dev(psf, y, perts[0], 0.1)
+    reps = 10
+    for i in range(reps):
+        cost_grad_dev(psf, y, perts[i], 0.1)
     fam = {f: ctx.profile_read(f) for f in ("render", "psf_pass", "sumsq", "atom_sums")}
     ctx.profile(False)
     hbm = peaks()["hbm_gbs"]
     nbytes = int(np.prod(inst.dims)) * 4
-    # render writes 1 volume; 6 psf passes read+write; sumsq reads 2 + writes 1
-    psf_bytes = 6 * 2 * nbytes
-    psf_ms = fam["psf_pass"][0]
+    # psf: 6 passes read + write one volume each, the forward's last pass also
+    # reads y (fused residual + sum of squares)
+    psf_bytes = (6 * 2 + 1) * nbytes
+    psf_ms = fam["psf_pass"][0] / reps
+    # per atom-voxel work of the fp32 interval kernels:
+    # render 3 MUFU (lg2, ex2, ex2), atom sums 4 MUFU (lg2, ex2, ex2, rcp);
+    # sum of the atoms' 1e-12 boxes over the evaluated perturbations
+    sbox = float(np.mean([np.prod(N.atom_geometry(inst.dims, perts[i])[2], axis=1).sum()
+                          for i in range(reps)]))
+    clk = 1e6 * (peaks().get("sm_max_mhz") or 1965.0)
+    mufu_peak = 16 * ctx_sms(dev) * clk  # MUFU ops/s: 16 per SM per clock
+    roof = {}
+    for fam_name, kern, mufu in (("render", "render_f32_kernel", 3), ("atom_sums", "atom_sums_f32_kernel", 4)):
+        t = fam[fam_name][0] / reps / 1e3
+        ach = mufu * sbox / t
+        roof[fam_name] = {"bound": "mufu", "kernel": kern, "achieved": ach / 1e12, "peak": mufu_peak / 1e12,
+                          "unit": "Tops/s (MUFU)", "frac": ach / mufu_peak, "traffic": None,
+                          "ops_per_atom_voxel": mufu, "atom_voxels": sbox, "avg_launch_ms": 1e3 * t,
+                          "peak_source": "16 MUFU ops / clock / SM at the max SM clock"}
+    roof["psf_pass"] = {"bound": "hbm", "achieved": psf_bytes / (psf_ms / 1e3) / 1e9, "peak": hbm,
+                        "unit": "GB/s", "frac": psf_bytes / (psf_ms / 1e3) / 1e9 / hbm,
+                        "bytes_per_eval": psf_bytes, "launches_per_eval": fam["psf_pass"][1] / reps}
     return {"metric": "cost+grad evals/s (cfg5: 256^3 fp32, N=1000, 6000-entry gradient)",
             "value": 1.0 / s, "unit": "evals/s", "ms_per_eval": 1e3 * s,
-            "kernel_ms": {k: v[0] for k, v in fam.items()},
-            "psf_pass_gbs": psf_bytes / (psf_ms / 1e3) / 1e9 if psf_ms else None,
-            "psf_pass_frac_hbm": (psf_bytes / (psf_ms / 1e3) / 1e9) / hbm if psf_ms else None,
+            "kernel_ms": {k: v[0] / reps for k, v in fam.items()},
+            "roofline": roof,
             "timing": "wall clock per synchronous C-ABI call (host params in, C + gradient out)"}
+
+
+def ctx_sms(dev) -> int:
+    import torch
+    return torch.cuda.get_device_properties(dev).multi_processor_count
 
 
 def sharded_solve_workload(dev, rank, world, config: int = 3, algo: str = "bsfw"):
