@@ -9,7 +9,8 @@ import json
 import re
 import sys
 
-FAMILIES = (("eta_basis", r"pass_(tile|z|tiled|zy)"), ("eta_mix", r"mix_argmax_kernel<[^>]*, 0>|mix_ring2?_kernel"),
+FAMILIES = (("eta_basis", r"pass_(tile|z|tiled|zy)"), ("render", r"render"),
+            ("atom_sums", r"atom_sums"), ("eta_mix", r"mix_argmax_kernel<[^>]*, 0>|mix_ring2?_kernel"),
             ("eta_direct", r"eta_(fold|direct|sym)_kernel"), ("eta_refine", r"refine_kernel"))
 
 
