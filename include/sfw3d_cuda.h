@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define SFW3D_ABI_VERSION 2
+#define SFW3D_ABI_VERSION 3
 
 typedef enum {
   SFW3D_OK = 0,
@@ -326,6 +326,45 @@ int sfw3d_nnlasso_qp(sfw3d_ctx* ctx, int k, const double* gram_host, const doubl
 int sfw3d_residual(sfw3d_ctx* ctx, int dtype, int64_t n, const void* y_dev,
                    const void* const* phis_host, const double* w_host, int k,
                    void* out_dev, double* sumsq_host);
+
+/* ---- in-library L-BFGS-B (the reference's scipy.optimize.minimize calls) -- */
+/* Objective callback: 0 = ok with *f and g[0..n) written; any other value
+ * aborts the minimisation (an sfw3d_status is passed through). */
+typedef int (*sfw3d_objective_fn)(void* user, const double* x, double* f, double* g);
+
+/* L-BFGS-B with scipy's driver conventions (method="L-BFGS-B": maxcor, ftol,
+ * gtol, maxiter, maxfun, maxls; nbd[i]: 0 free, 1 lower, 2 both, 3 upper).
+ * x is updated in place; info = {status, iterations, evaluations}, status:
+ * 0 projected gradient <= gtol, 1 relative reduction <= ftol, 2 maxiter,
+ * 3 maxfun, 4 abnormal line-search termination. Host only (no context): the
+ * optimiser behind sfw3d_refine_eta_max / sfw3d_local_descent, exported so
+ * that it can be checked against scipy on any objective. */
+int sfw3d_lbfgsb_minimize(int n, double* x, const double* lower, const double* upper,
+                          const int32_t* nbd, int maxcor, double ftol, double gtol,
+                          int maxiter, int maxfun, int maxls, sfw3d_objective_fn fn,
+                          void* user, double* f_out, int32_t info[3]);
+
+/* refine_eta_max (certificate.py:187-224): box-constrained L-BFGS-B ascent
+ * of eta(theta) = <G_theta, back>/lam over theta = (m_x, m_y, m_z, sigma, d)
+ * from `start` (projected into the box), with back = H^T r on the device
+ * (correlate_adjoint, :198). Every evaluation is one sfw3d_atom_sums launch;
+ * the quasi-Newton algebra runs on the calling thread (no Python callback).
+ * The seed is kept when the ascent does not improve it (:221-222).
+ * SFW3D_ENONFINITE as the reference's FloatingPointError (:207-208,219-220). */
+int sfw3d_refine_eta_max(sfw3d_ctx* ctx, int dtype, const int dims[3], const void* back_dev,
+                         double lam, const double start[5], const double lower[5],
+                         const double upper[5], int max_iter, double gtol,
+                         double theta_out[5], double* eta_out, int32_t info[3]);
+
+/* local_descent (solvers.py:197-240): joint L-BFGS-B slide of the k atom rows
+ * (w, m, sigma, d) in params_host (in: start, out: result), bounds w >= 0 and
+ * the (m, sigma, d) box per atom, objective sfw3d_cost_grad. The start is
+ * kept (info[0] gets bit 0x100) when the result is not finite or worse
+ * (:236-237). info = {status, iterations, evaluations} as above. */
+int sfw3d_local_descent(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const void* y_dev,
+                        double* params_host, int k, double lam, const double lower[5],
+                        const double upper[5], double gtol, double ftol, int max_iter,
+                        double* cost_out, int32_t info[3]);
 
 #ifdef __cplusplus
 }

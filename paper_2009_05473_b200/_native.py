@@ -34,6 +34,7 @@ EXPORTS = (
     "sfw3d_last_refine_count", "sfw3d_table_set_option", "sfw3d_eta_argmax_slab",
     "sfw3d_cost_grad_slab_dev", "sfw3d_render_slab", "sfw3d_atom_sums_slab",
     "sfw3d_volume_info", "sfw3d_volume_read", "sfw3d_volume_write",
+    "sfw3d_lbfgsb_minimize", "sfw3d_refine_eta_max", "sfw3d_local_descent",
 )
 
 
@@ -51,7 +52,18 @@ HALO_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int
                       C.c_int)
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int, C.c_int)
 
+# objective callback of the in-library L-BFGS-B (include/sfw3d_cuda.h: sfw3d_objective_fn)
+OBJECTIVE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                           C.POINTER(C.c_double))
+
 _SIGNATURES = {
+    "sfw3d_lbfgsb_minimize": (C.c_int, [C.c_int, _dp, _dp, _dp, _i32p, C.c_int, C.c_double,
+                                        C.c_double, C.c_int, C.c_int, C.c_int, OBJECTIVE_FN, _vp,
+                                        _dp, _i32p]),
+    "sfw3d_refine_eta_max": (C.c_int, [_vp, C.c_int, _ip, _vp, C.c_double, _dp, _dp, _dp, C.c_int,
+                                       C.c_double, _dp, _dp, _i32p]),
+    "sfw3d_local_descent": (C.c_int, [_vp, _vp, C.c_int, _vp, _dp, C.c_int, C.c_double, _dp, _dp,
+                                      C.c_double, C.c_double, C.c_int, _dp, _i32p]),
     "sfw3d_abi_version": (C.c_int, []),
     "sfw3d_last_error": (C.c_char_p, []),
     "sfw3d_last_refine_count": (C.c_int, []),
@@ -108,6 +120,11 @@ _SIGNATURES = {
 }
 
 _lib = None
+
+# "native": refine_eta_max / local_descent run the in-library L-BFGS-B (one C
+# call per optimisation); "scipy": the reference's scipy.optimize loop over the
+# same device evaluations (kept as the cross-check of the parity tests)
+OPTIMIZER = "native"
 _lib_lock = threading.Lock()
 
 

@@ -258,17 +258,40 @@ def refine_eta_max(residual: Volume, lam: float, psf: Psf, start: AtomParams,
 
 
 def refine_eta_max_dev(residual, lam: float, psf: Psf, start: AtomParams, bounds: DomainBounds,
-                       max_iter: int = 200, gtol: float = 1e-8, back=None):
+                       max_iter: int = 200, gtol: float = 1e-8, back=None, info: dict | None = None):
+    """The ascent as ONE C call (sfw3d_refine_eta_max): the in-library L-BFGS-B
+    (scipy's algorithm and driver conventions, csrc/lbfgsb.cuh) evaluates eta
+    and its 5-gradient with the device atom-sum kernel per step; no Python
+    callback. `N.OPTIMIZER = "scipy"` selects the reference's own scipy loop
+    over the same device evaluations (the cross-check of the tests)."""
     if lam <= 0.0:
         raise ValueError(f"lam must be > 0, got {lam}")
     start = clamp_to_domain(start, bounds)
     if back is None:
         back = psf_apply_dev(psf, residual, True)
-
-    # the L-BFGS-B callback calls sfw3d_atom_sums ~30 times per refine: its
-    # arguments are bound once (context, field pointer, dims, buffers)
     from .forward import code_of
     ctx = N.context(back.device.index)
+    if N.OPTIMIZER == "scipy":
+        return _refine_scipy(ctx, back, lam, start, bounds, max_iter, gtol)
+    box = np.array(bounds_box(bounds), dtype=np.float64)
+    lo, hi = np.ascontiguousarray(box[:, 0]), np.ascontiguousarray(box[:, 1])
+    x0 = np.ascontiguousarray(start.to_array(), dtype=np.float64)
+    theta = np.empty(5)
+    eta = C.c_double()
+    stat = (C.c_int32 * 3)()
+    N.check(N.lib().sfw3d_refine_eta_max(ctx.handle, code_of(back), N.dims_arg(back.shape),
+                                         N.ptr(back), float(lam), N.f64_ptr(x0), N.f64_ptr(lo),
+                                         N.f64_ptr(hi), int(max_iter), float(gtol),
+                                         N.f64_ptr(theta), C.byref(eta), stat))
+    if info is not None:
+        info["lbfgsb"] = {"status": int(stat[0]), "iterations": int(stat[1]),
+                          "evaluations": int(stat[2])}
+    return clamp_to_domain(AtomParams.from_array(theta), bounds), float(eta.value)
+
+
+def _refine_scipy(ctx, back, lam, start, bounds, max_iter, gtol):
+    """certificate.py:201-224 with scipy's L-BFGS-B driving the device evaluations."""
+    from .forward import code_of
     fn, handle, code = N.lib().sfw3d_atom_sums, ctx.handle, code_of(back)
     dims_a, bptr = N.dims_arg(back.shape), N.ptr(back)
     row = np.empty((1, 6))

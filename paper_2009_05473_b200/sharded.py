@@ -35,6 +35,7 @@ from . import _native as N
 from .certificate import _position_window, build_template_table, make_parameter_grids
 from .distributed import SlabCertificate, SlabCostGrad, slab_bounds
 from .forward import GRADIENT_COLUMNS, as_psf, code_of, psf_apply_dev
+from .optimize import minimize as native_minimize
 from .measures import (AtomParams, WeightedMeasure, bounds_box, clamp_to_domain,
                        default_prune_tol, measure_rows, prune_zero_weights)
 from .solvers import (BSFW, SFW, TERMINATED_CERTIFICATE, TERMINATED_ITERATION_CAP,
@@ -137,6 +138,15 @@ class _SlabGram:
         return self.G[np.ix_(idx, idx)], self.b[idx]
 
 
+def _minimize(fun, x0, box, max_iter, gtol, ftol=2.220446049250313e-09):
+    """The solver's optimiser (N.OPTIMIZER): the in-library L-BFGS-B through its
+    callback form, or scipy's; every rank runs it on identical reduced values."""
+    if N.OPTIMIZER == "scipy":
+        return minimize(fun, x0, jac=True, method="L-BFGS-B", bounds=box,
+                        options={"maxiter": max_iter, "gtol": gtol, "ftol": ftol})
+    return native_minimize(fun, x0, box, maxiter=max_iter, gtol=gtol, ftol=ftol)
+
+
 def _refine(slab: _Slab, r_own, lam, start: AtomParams, bounds, max_iter=200, gtol=1e-8):
     """refine_eta_max (certificate.py:187-224) on the slab: neg_eta from the
     all-reduced per-atom sums of the windowed b."""
@@ -151,8 +161,7 @@ def _refine(slab: _Slab, r_own, lam, start: AtomParams, bounds, max_iter=200, gt
         return -val, -grad
 
     start_val = -neg_eta(start.to_array())[0]
-    res = minimize(neg_eta, start.to_array(), jac=True, method="L-BFGS-B",
-                   bounds=bounds_box(bounds), options={"maxiter": max_iter, "gtol": gtol})
+    res = _minimize(neg_eta, start.to_array(), bounds_box(bounds), max_iter, gtol)
     if not np.isfinite(res.fun):
         raise FloatingPointError("certificate ascent diverged to a non-finite value")
     if -res.fun < start_val:
@@ -177,8 +186,7 @@ def _descent(slab: _Slab, measure, lam, bounds, gtol, ftol, max_iter):
         box.extend(bounds_box(bounds))
     x0 = measure_rows(start).ravel()
     f0 = fun(x0)[0]
-    res = minimize(fun, x0, jac=True, method="L-BFGS-B", bounds=box,
-                   options={"maxiter": max_iter, "gtol": gtol, "ftol": ftol})
+    res = _minimize(fun, x0, box, max_iter, gtol, ftol)
     warn = not res.success and "ABNORMAL" in str(res.message).upper()
     if not np.isfinite(res.fun) or res.fun > f0:
         return start, float(f0), warn

@@ -26,7 +26,7 @@ def test_library_exports_every_header_symbol():
     lib = N.lib()
     for name in header_symbols():
         assert hasattr(lib, name), name
-    assert lib.sfw3d_abi_version() == 2
+    assert lib.sfw3d_abi_version() == 3
 
 
 def test_library_is_sm100a():
