@@ -196,6 +196,8 @@ extern "C" int sfw3d_ctx_destroy(sfw3d_ctx* ctx) {
   if (ctx->pinned.ptr) cudaFreeHost(ctx->pinned.ptr);
   if (ctx->pinned_out.ptr) cudaFreeHost(ctx->pinned_out.ptr);
   if (ctx->pinned_io.ptr) cudaFreeHost(ctx->pinned_io.ptr);
+  if (ctx->ws_one.ptr) cudaFree(ctx->ws_one.ptr);
+  if (ctx->one_host) cudaFreeHost(ctx->one_host);
   delete ctx;
   return SFW3D_OK;
 }

@@ -18,6 +18,8 @@
 // does (no FMA contraction where the reference rounds twice); fp32 volumes
 // use fp32 math on the MUFU (ex2/lg2/rcp) with fp64 accumulation.
 #include <algorithm>
+#include <atomic>
+#include <cstring>
 #include <type_traits>
 
 #include "internal.cuh"
@@ -456,6 +458,85 @@ __global__ void __launch_bounds__(kSumThreads) atom_sums_big_kernel(
   }
 }
 
+// ---------------------------------------------- one atom, for the ascent
+// neg_eta of the certificate ascent (certificate.py:201-209): the six inner
+// products of ONE unit atom with the device field, once per L-BFGS-B
+// evaluation. Built for latency: the atom's geometry arrives as a kernel
+// parameter (no upload), the voxels of its box are spread flat over the grid
+// with the offsets computed on the fly, fp64 profile math for fp32 and fp64
+// storage alike (the ascent's gtol = 1e-8 needs a smooth objective), CTA
+// partials combined in CTA order by the last CTA to finish (fixed order:
+// bit-reproducible), which writes the result and a sequence flag straight
+// into mapped pinned host memory, where the calling thread is spinning.
+constexpr int kOneThreads = 256;
+
+template <typename T>
+__global__ void __launch_bounds__(kOneThreads) refine_sums_kernel(
+    const __grid_constant__ AtomGeo a, int nx, int ny, int nz, const T* __restrict__ field,
+    double* __restrict__ partials, unsigned* __restrict__ ticket,
+    volatile double* __restrict__ out_host, volatile unsigned long long* __restrict__ flag_host,
+    unsigned long long seq) {
+  const int l1 = a.len[1], l2 = a.len[2];
+  const long long nv = (long long)a.len[0] * l1 * l2;
+  double s[6] = {0, 0, 0, 0, 0, 0};
+  float sf[6];
+  const long long stride = (long long)gridDim.x * kOneThreads;
+  for (long long v = (long long)blockIdx.x * kOneThreads + threadIdx.x; v < nv; v += stride) {
+    const int q = int(v / l2), ic = int(v - (long long)q * l2);
+    const int il[3] = {q / l1, q - (q / l1) * l1, ic};
+    const int dims[3] = {nx, ny, nz};
+    int g[3];
+    double o[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      if (a.full[ax]) {
+        g[ax] = il[ax];
+        o[ax] = min_image(il[ax], a.m[ax], dims[ax]);
+      } else {
+        const int p = a.start[ax] + il[ax];
+        g[ax] = pmod(p, dims[ax]);
+        o[ax] = __dsub_rn(double(p), a.m[ax]);
+      }
+    }
+    const double b = double(field[((long long)g[0] * ny + g[1]) * nz + g[2]]);
+    atom_terms<double>(a, o[0], o[1], o[2], b, s, sf, 0.f, 0.f, 0.f, 0.f, 0.f);
+  }
+  __shared__ double red[6][kOneThreads / 32];
+  __shared__ int last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    double x = s[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (lane == 0) red[c][warp] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    double x = 0.0;
+    for (int w = 0; w < kOneThreads / 32; ++w) x += red[threadIdx.x][w];
+    partials[(long long)blockIdx.x * 6 + threadIdx.x] = x;
+    __threadfence();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < 6) {
+    double x = 0.0;
+    for (unsigned bI = 0; bI < gridDim.x; ++bI) x += __ldcg(partials + (long long)bI * 6 + threadIdx.x);
+    out_host[threadIdx.x] = x;
+    __threadfence_system();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *ticket = 0u;  // ready for the next evaluation (stream order)
+    *flag_host = seq;
+    __threadfence_system();
+  }
+}
+
 // ------------------------------------------------ render, fp32 interval path
 // fp32 storage when every atom box is a product of three unwrapped intervals
 // that meet a brick in ONE run per axis (no full axis, len <= n - brick):
@@ -886,6 +967,60 @@ int atom_sums_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const void* fie
   SFW3D_LAUNCH_CHECK(ctx);
   chunk_combine_kernel<<<(k * 6 + 255) / 256, 256, 0, ctx->stream>>>(first_dev, k, part, sums_dev);
   SFW3D_LAUNCH_CHECK(ctx);
+  return SFW3D_OK;
+}
+
+int refine_sums_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const void* field,
+                     const AtomGeo& atom, double out[6]) {
+  if (!ctx->one_host) {
+    SFW3D_CUDA_TRY(cudaHostAlloc(&ctx->one_host, 8 * sizeof(double), cudaHostAllocMapped));
+    std::memset(ctx->one_host, 0, 8 * sizeof(double));
+    SFW3D_CUDA_TRY(cudaHostGetDevicePointer(&ctx->one_host_dev, ctx->one_host, 0));
+  }
+  const long long nv = (long long)atom.len[0] * atom.len[1] * atom.len[2];
+  const int maxg = 4 * ctx->num_sms;
+  const int grid = int(std::min<long long>(maxg, std::max<long long>(1, (nv + 2 * kOneThreads - 1) / (2 * kOneThreads))));
+  const size_t need = size_t(maxg) * 6 * sizeof(double) + 256;
+  if (ctx->ws_one.bytes < need) {
+    SFW3D_TRY(ensure_device(ctx, ctx->ws_one, need));
+    SFW3D_CUDA_TRY(cudaMemsetAsync(ctx->ws_one.ptr, 0, need, ctx->stream));
+  }
+  unsigned* ticket = static_cast<unsigned*>(ctx->ws_one.ptr);
+  double* partials = reinterpret_cast<double*>(static_cast<char*>(ctx->ws_one.ptr) + 256);
+  volatile double* host = static_cast<volatile double*>(ctx->one_host);
+  volatile unsigned long long* flag = reinterpret_cast<volatile unsigned long long*>(host + 7);
+  volatile double* host_dev = static_cast<volatile double*>(ctx->one_host_dev);
+  const unsigned long long seq = ++ctx->one_seq;
+  {
+    SFW3D_PROF(ctx, "atom_sums");
+    if (dtype == SFW3D_F64)
+      refine_sums_kernel<double><<<grid, kOneThreads, 0, ctx->stream>>>(
+          atom, dims[0], dims[1], dims[2], static_cast<const double*>(field), partials, ticket, host_dev,
+          reinterpret_cast<volatile unsigned long long*>(host_dev + 7), seq);
+    else
+      refine_sums_kernel<float><<<grid, kOneThreads, 0, ctx->stream>>>(
+          atom, dims[0], dims[1], dims[2], static_cast<const float*>(field), partials, ticket, host_dev,
+          reinterpret_cast<volatile unsigned long long*>(host_dev + 7), seq);
+    SFW3D_LAUNCH_CHECK(ctx);
+  }
+  // spin on the mapped flag (a stream synchronise costs more than the kernel);
+  // the stream is polled now and then so that a failed launch cannot hang us
+  for (unsigned spins = 1; *flag != seq; ++spins) {
+    if ((spins & 0x3fff) == 0) {
+      const cudaError_t e = cudaStreamQuery(ctx->stream);
+      if (e == cudaSuccess) {
+        if (*flag == seq) break;
+        set_error("ascent kernel finished without publishing its result");
+        return SFW3D_ECUDA;
+      }
+      if (e != cudaErrorNotReady) SFW3D_CUDA_TRY(e);
+    }
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  for (int c = 0; c < 6; ++c) out[c] = host[c];
   return SFW3D_OK;
 }
 

@@ -68,6 +68,11 @@ struct sfw3d_ctx {
   cudaStream_t stream = nullptr;
   int num_sms = 148;
   int64_t launches = 0;
+  // L2 residency of the 1-D pass chains (psf.cu: pass_typed sets it per pass):
+  // 1 when a pass's input and output volumes fit the 126 MB L2 together well
+  // enough to ping-pong there (input lines evict-first once consumed, output
+  // lines kept for the next pass), 0 for streaming volumes
+  int l2mode = 0;
   sfw3d::Arena ws;         // device scratch (grown on demand, reused)
   sfw3d::Arena pinned;     // pinned host staging for uploads (bump-allocated)
   size_t pin_off = 0;      // bytes of `pinned` referenced by in-flight copies
@@ -76,6 +81,12 @@ struct sfw3d_ctx {
   sfw3d::Arena ws_aux;     // auxiliary small device scratch (render culling boxes)
   sfw3d::Arena ws_plan;    // atom-sum chunk plan + chunk partials
   sfw3d::Arena pinned_io;  // pinned staging of the .vol reader / writer
+  // single-atom ascent evaluations (atoms.cu: refine_sums_impl): ticket + CTA
+  // partials on the device, result + sequence flag in mapped pinned memory
+  sfw3d::Arena ws_one;
+  void* one_host = nullptr;
+  void* one_host_dev = nullptr;
+  unsigned long long one_seq = 0;
   // kernel-family timing (sfw3d_ctx_profile)
   int profile = 0;
   struct Mark {
@@ -151,6 +162,10 @@ struct AtomGeo {
 // Builds AtomGeo rows; returns SFW3D_EINVAL for sigma<=0, d<=0 or
 // non-finite parameters (forward.py:130-131, measures.py:80-82).
 int build_atoms(const int dims[3], const double* params, int k, std::vector<AtomGeo>& out);
+// the six unit-atom inner products of ONE atom against a device field, fp64
+// math, result returned on the host (the certificate ascent's evaluation)
+int refine_sums_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const void* field,
+                     const AtomGeo& atom, double out[6]);
 
 // ---------------------------------------------------------------- PSF
 }  // namespace sfw3d
@@ -269,6 +284,17 @@ inline cudaError_t allow_dynamic_smem(const void* func, size_t bytes) {
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+// L2 eviction policy of a pass's global accesses (first = 1: evict-first)
+__device__ __forceinline__ unsigned long long l2_policy(int first) {
+  unsigned long long p;
+  if (first) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void cp_async16h(void* smem, const void* gmem, unsigned long long pol) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "l"(pol));
 }
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));

@@ -41,6 +41,7 @@ struct RefineUser {
   double sums[6];
   bool first = true;
   double f_first = 0.0;
+  std::vector<AtomGeo> atom;
 };
 
 // neg_eta (certificate.py:201-209): -<G_theta, back>/lam and its 5-gradient
@@ -48,8 +49,15 @@ int refine_objective(void* user, const double* x, double* f, double* g) {
   RefineUser* u = static_cast<RefineUser*>(user);
   u->row[0] = 1.0;
   for (int i = 0; i < 5; ++i) u->row[1 + i] = x[i];
-  const int rc = sfw3d_atom_sums(u->ctx, u->dtype, u->dims, u->back, u->row, 1, u->sums);
+  int rc = build_atoms(u->dims, u->row, 1, u->atom);
   if (rc != SFW3D_OK) return rc;
+  rc = refine_sums_impl(u->ctx, u->dtype, u->dims, u->back, u->atom[0], u->sums);
+  if (rc != SFW3D_OK) return rc;
+  for (int c = 0; c < 6; ++c)
+    if (!std::isfinite(u->sums[c])) {
+      set_error("non-finite certificate value; atom parameters left the smooth regime");
+      return SFW3D_ENONFINITE;
+    }
   *f = -(u->sums[0] / u->lam);
   for (int i = 0; i < 5; ++i) g[i] = -(u->sums[1 + i] / u->lam);
   if (u->first) { u->first = false; u->f_first = *f; }
@@ -118,6 +126,9 @@ extern "C" int sfw3d_refine_eta_max(sfw3d_ctx* ctx, int dtype, const int dims[3]
                                     double theta_out[5], double* eta_out, int32_t info[3]) {
   SFW3D_CHECK_ARG(ctx && back_dev && start && lower && upper && theta_out && eta_out, "NULL argument");
   SFW3D_CHECK_ARG(lam > 0.0, "lam must be > 0");
+  SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
+  SFW3D_CHECK_ARG(dims[0] > 0 && dims[1] > 0 && dims[2] > 0, "dims must be positive");
+  SFW3D_TRY(begin_call(ctx));
   RefineUser u{ctx, dtype, dims, back_dev, lam};
   double x[5];
   int nb[5];

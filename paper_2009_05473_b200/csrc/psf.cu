@@ -165,6 +165,14 @@ __global__ void __launch_bounds__(32 * kZWarps) pass_z_kernel(
   }
 }
 
+// Output stores of the contiguous pass: streaming (evict-first) for volumes
+// that cannot stay in L2, normal (kept for the next pass) in L2 mode.
+template <typename V>
+__device__ __forceinline__ void st_out(int l2mode, V* p, V v) {
+  if (l2mode) *p = v;
+  else __stcs(p, v);
+}
+
 // ------------------------------------------------------------ v2 passes
 // Register-window passes with ~94% FFMA issue density: taps padded only to a
 // multiple of 4 (the window consumes 4 taps per step), the staged tile reused
@@ -179,8 +187,9 @@ template <typename T, int J, int TI, int NT, int MINB = 1>
 __global__ void __launch_bounds__(NT, MINB) pass_tile2_kernel(
     const T* __restrict__ in, T* __restrict__ out, int n_axis, long long stride,
     const T* __restrict__ taps_g, int lo, int ntaps, const T* addend, T aw, T w, int a_begin,
-    int a_end, int out_shift, double* __restrict__ sq_parts) {
+    int a_end, int out_shift, double* __restrict__ sq_parts, int l2mode) {
   constexpr int G = NT / TI, To = J * G;
+  const unsigned long long pol = l2_policy(l2mode);
   constexpr int kVec = 16 / sizeof(T), kRowVecs = TI / kVec;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nt4 = (ntaps + 3) & ~3;
@@ -203,16 +212,16 @@ __global__ void __launch_bounds__(NT, MINB) pass_tile2_kernel(
       // no wrap anywhere in the tile (interior CTAs): one pointer bump per row
       const long long step = (long long)dr * stride;
       const T* p = src + (long long)a * stride;
-      for (; r < rows; r += dr, dst += dr * TI, p += step) cp_async16(dst, p);
+      for (; r < rows; r += dr, dst += dr * TI, p += step) cp_async16h(dst, p, pol);
     } else if (n_axis >= dr) {  // at most one wrap per step
       for (; r < rows; r += dr, dst += dr * TI) {
-        cp_async16(dst, src + (long long)a * stride);
+        cp_async16h(dst, src + (long long)a * stride, pol);
         a += dr;
         a = a >= n_axis ? a - n_axis : a;
       }
     } else {
       for (; r < rows; r += dr, dst += dr * TI) {
-        cp_async16(dst, src + (long long)a * stride);
+        cp_async16h(dst, src + (long long)a * stride, pol);
         a = (a + dr) % n_axis;
       }
     }
@@ -306,8 +315,10 @@ __global__ void __launch_bounds__(NT, MINB) pass_tile2_kernel(
 template <int J, int MINB>
 __global__ void __launch_bounds__(256, MINB) pass_tile2x2_kernel(
     const float* __restrict__ in, float* __restrict__ out, int n_axis, long long stride,
-    const float* __restrict__ taps_g, int lo, int ntaps, int a_begin, int a_end, int out_shift) {
+    const float* __restrict__ taps_g, int lo, int ntaps, int a_begin, int a_end, int out_shift,
+    int l2mode) {
   constexpr int TI = 64, G = 8, To = J * G;
+  const unsigned long long pol = l2_policy(l2mode);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nt4 = (ntaps + 3) & ~3;
   f32x2* taps2 = reinterpret_cast<f32x2*>(smem_raw);        // [nt4] (t, t)
@@ -330,16 +341,16 @@ __global__ void __launch_bounds__(256, MINB) pass_tile2x2_kernel(
     if (a0 + lo >= 0 && a0 + lo + rows <= n_axis) {
       const long long step = (long long)dr * stride;
       const float* p = src + (long long)a * stride;
-      for (; r < rows; r += dr, dst += dr * TI, p += step) cp_async16(dst, p);
+      for (; r < rows; r += dr, dst += dr * TI, p += step) cp_async16h(dst, p, pol);
     } else if (n_axis >= dr) {
       for (; r < rows; r += dr, dst += dr * TI) {
-        cp_async16(dst, src + (long long)a * stride);
+        cp_async16h(dst, src + (long long)a * stride, pol);
         a += dr;
         a = a >= n_axis ? a - n_axis : a;
       }
     } else {
       for (; r < rows; r += dr, dst += dr * TI) {
-        cp_async16(dst, src + (long long)a * stride);
+        cp_async16h(dst, src + (long long)a * stride, pol);
         a = (a + dr) % n_axis;
       }
     }
@@ -403,8 +414,10 @@ __global__ void __launch_bounds__(256, MINB) pass_tile2x2_kernel(
 template <typename T, int J, int MINB = 1>
 __global__ void __launch_bounds__(128, MINB) pass_z2_kernel(
     const T* __restrict__ in, T* __restrict__ out, int nz, long long nrows,
-    const T* __restrict__ taps_g, int lo, int ntaps, int pitch, const T* addend, T aw, T w) {
+    const T* __restrict__ taps_g, int lo, int ntaps, int pitch, const T* addend, T aw, T w,
+    int l2mode) {
   constexpr int kVec = 16 / sizeof(T);
+  const unsigned long long pol = l2_policy(l2mode);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int sh = ((lo % 4) + 4) % 4;
   const int nt4 = (ntaps + sh + 3) & ~3;
@@ -432,7 +445,7 @@ __global__ void __launch_bounds__(128, MINB) pass_z2_kernel(
         const T* p = in + (row0 + warp) * nz + z;
         T* d = tile + warp * pitch + v * kVec;
 #pragma unroll
-        for (int i = 0; i < 8; ++i, p += step, d += 4 * pitch) cp_async16(d, p);
+        for (int i = 0; i < 8; ++i, p += step, d += 4 * pitch) cp_async16h(d, p, pol);
       }
     } else
     for (int v = lane; v < nv; v += 32) {
@@ -441,7 +454,7 @@ __global__ void __launch_bounds__(128, MINB) pass_z2_kernel(
         const long long row = row0 + r;
         T* d = tile + r * pitch + v * kVec;
         if (row < nrows)
-          cp_async16(d, in + row * nz + z);
+          cp_async16h(d, in + row * nz + z, pol);
         else
           for (int k = 0; k < kVec; ++k) d[k] = T(0);
       }
@@ -480,9 +493,9 @@ __global__ void __launch_bounds__(128, MINB) pass_z2_kernel(
       const T* sv = tile + r * pitch + v * kVec;
       T* dv = out + (row0 + r) * nz + z0 + v * kVec;
       if constexpr (sizeof(T) == 4)
-        __stcs(reinterpret_cast<float4*>(dv), *reinterpret_cast<const float4*>(sv));
+        st_out(l2mode, reinterpret_cast<float4*>(dv), *reinterpret_cast<const float4*>(sv));
       else
-        __stcs(reinterpret_cast<double2*>(dv), *reinterpret_cast<const double2*>(sv));
+        st_out(l2mode, reinterpret_cast<double2*>(dv), *reinterpret_cast<const double2*>(sv));
     }
     return;
   }
@@ -497,10 +510,10 @@ __global__ void __launch_bounds__(128, MINB) pass_z2_kernel(
 #pragma unroll
         for (int j = 0; j < J; j += 4) {
           if constexpr (sizeof(T) == 4) {
-            __stcs(reinterpret_cast<float4*>(po + j), make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]));
+            st_out(l2mode, reinterpret_cast<float4*>(po + j), make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]));
           } else {
-            __stcs(reinterpret_cast<double2*>(po + j), make_double2(acc[j], acc[j + 1]));
-            __stcs(reinterpret_cast<double2*>(po + j + 2), make_double2(acc[j + 2], acc[j + 3]));
+            st_out(l2mode, reinterpret_cast<double2*>(po + j), make_double2(acc[j], acc[j + 1]));
+            st_out(l2mode, reinterpret_cast<double2*>(po + j + 2), make_double2(acc[j + 2], acc[j + 3]));
           }
         }
         return;
@@ -509,11 +522,11 @@ __global__ void __launch_bounds__(128, MINB) pass_z2_kernel(
       for (int j = 0; j < J; j += 4) {
         if (zc + j >= nz) break;
         if constexpr (sizeof(T) == 4) {
-          __stcs(reinterpret_cast<float4*>(po + j),
+          st_out(l2mode, reinterpret_cast<float4*>(po + j),
                  make_float4(w * acc[j], w * acc[j + 1], w * acc[j + 2], w * acc[j + 3]));
         } else {
-          __stcs(reinterpret_cast<double2*>(po + j), make_double2(w * acc[j], w * acc[j + 1]));
-          __stcs(reinterpret_cast<double2*>(po + j + 2), make_double2(w * acc[j + 2], w * acc[j + 3]));
+          st_out(l2mode, reinterpret_cast<double2*>(po + j), make_double2(w * acc[j], w * acc[j + 1]));
+          st_out(l2mode, reinterpret_cast<double2*>(po + j + 2), make_double2(w * acc[j + 2], w * acc[j + 3]));
         }
       }
     }
@@ -630,7 +643,7 @@ int launch_tile2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axi
   const int ab = xr.begin, ae = xr.end < 0 ? n : xr.end;
   dim3 grid(unsigned((ae - ab + To - 1) / To), unsigned(stride / TI), unsigned(outer));
   pass_tile2_kernel<T, J, TI, NT, MINB><<<grid, NT, smem, ctx->stream>>>(
-      in, out, n, stride, taps, lo, ntaps, addend, T(aw), T(w), ab, ae, xr.shift, xr.sq);
+      in, out, n, stride, taps, lo, ntaps, addend, T(aw), T(w), ab, ae, xr.shift, xr.sq, ctx->l2mode);
   xr.nsq = int(grid.x * grid.y * grid.z);
   SFW3D_LAUNCH_CHECK(ctx);
   return SFW3D_OK;
@@ -653,7 +666,7 @@ int launch_tile2x2(sfw3d_ctx* ctx, const float* in, float* out, const int dims[3
   const int ab = xr.begin, ae = xr.end < 0 ? n : xr.end;
   dim3 grid(unsigned((ae - ab + To - 1) / To), unsigned(stride / TI), unsigned(outer));
   pass_tile2x2_kernel<J, MINB><<<grid, 256, smem, ctx->stream>>>(in, out, n, stride, taps, lo,
-                                                                 ntaps, ab, ae, xr.shift);
+                                                                 ntaps, ab, ae, xr.shift, ctx->l2mode);
   SFW3D_LAUNCH_CHECK(ctx);
   return SFW3D_OK;
 }
@@ -677,7 +690,7 @@ int launch_z2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* t
     SFW3D_CUDA_TRY(allow_dynamic_smem(reinterpret_cast<const void*>(pass_z2_kernel<T, J, MINB>), size_t(int(smem))));
   dim3 grid(unsigned((dims[2] + 4 * J - 1) / (4 * J)), unsigned((nrows + 31) / 32));
   pass_z2_kernel<T, J, MINB><<<grid, 128, smem, ctx->stream>>>(in, out, dims[2], nrows, taps, lo, ntaps,
-                                                         pitch, addend, T(aw), T(w));
+                                                         pitch, addend, T(aw), T(w), ctx->l2mode);
   SFW3D_LAUNCH_CHECK(ctx);
   return SFW3D_OK;
 }
@@ -690,6 +703,15 @@ int launch_z2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* t
 // Narrow filters are HBM-bound: the J = 16 tile keeps more CTAs resident.
 constexpr int kNarrowTaps = 24;
 
+// A pass chain ping-pongs between two volumes. Up to 72 MiB per volume
+// (256^3 fp32) the pair stays L2-resident on B200 when consumed input lines
+// are marked evict-first and output lines are stored normally: measured
+// 9.0 TB/s against 5.8 TB/s for a copy-shaped pass at 64 MiB
+// (tools/micro/l2_pingpong.cu); no gain from 96 MiB on.
+inline int l2_mode_for(size_t vol_bytes) {
+  return vol_bytes <= (size_t(72) << 20) ? 1 : 0;
+}
+
 template <typename T>
 int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis, const T* taps,
                int lo, int ntaps, const T* addend, double aw, double w, const XRange& xr) {
@@ -699,6 +721,7 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
   }
   constexpr bool f32 = sizeof(T) == 4;
   const bool wide = ntaps > kNarrowTaps;
+  ctx->l2mode = l2_mode_for(size_t(vol_count(dims)) * sizeof(T));
   if (xr.sq && !(axis == 0 && addend && (dims[1] * (long long)dims[2]) % 64 == 0 && ntaps <= 512)) {
     set_error("internal: fused sum of squares needs an axis-0 tiled pass with an addend");
     return SFW3D_EINVAL;
@@ -738,7 +761,13 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
         return launch_tile2<T, 32, 1>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
       }
     }
-    if constexpr (f32) return launch_tile2<T, 16, 5>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
+    if constexpr (f32) {
+      // (packed FFMA2 tile also for narrow filters: 512^3 15-tap y/x passes
+      // 0.218 -> 0.205 ms, bit-identical)
+      if (dims[axis] >= 128 && !addend && w == 1.0 && xr.sq == nullptr)
+        return launch_tile2x2<16, 3>(ctx, in, out, dims, axis, taps, lo, ntaps, xr);
+      return launch_tile2<T, 16, 5>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
+    }
     else return launch_tile2<T, 16>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
   }
   return wide ? launch_strided<T, 32>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr)
