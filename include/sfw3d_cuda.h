@@ -366,6 +366,47 @@ int sfw3d_local_descent(sfw3d_ctx* ctx, const sfw3d_psf* psf, int dtype, const v
                         const double upper[5], double gtol, double ftol, int max_iter,
                         double* cost_out, int32_t info[3]);
 
+/* ---- the solver's outer loop as one call (solvers.py:286-405) ----------- */
+typedef struct {
+  double lam;
+  int32_t max_outer_iterations;
+  int32_t boosted;             /* 0 = SFW (slide after every atom), 1 = BSFW */
+  double eta_threshold, eta_slack;
+  double lasso_tol;
+  int32_t lasso_max_iter;
+  int32_t descent_max_iter;
+  double descent_gtol, descent_ftol;
+  double prune_rel_tol, duplicate_tol;
+  double lower[5], upper[5];   /* box of (m_x, m_y, m_z, sigma, d)          */
+  int32_t window[6];           /* integer position window of the grid stage */
+  int32_t n_sigma, n_shape;
+  const double* sigma_grid;    /* host, n_sigma                             */
+  const double* shape_grid;    /* host, n_shape                             */
+} sfw3d_solve_options;
+
+/* One IterationRecord (solvers.py:77-88); absent criteria are NaN. */
+typedef struct {
+  int32_t index;
+  double eta_max, criterion_before, criterion_after_lasso, criterion_after_descent;
+  int32_t atom_count;
+  double t_certificate, t_lasso, t_descent;
+} sfw3d_solve_record;
+
+enum { SFW3D_TERM_CERTIFICATE = 0, SFW3D_TERM_ITERATION_CAP = 1, SFW3D_TERM_STALLED = 2 };
+
+/* _solve (solvers.py:286-395): the whole SFW / boosted-SFW loop on a device
+ * observation y — certificate (grid argmax + L-BFGS-B ascent), phi of the
+ * new atom, Gram rows (cached), non-negative LASSO, residual + criterion,
+ * prune, duplicate guard, slide(s), final re-check — driven by a C++
+ * controller on the calling thread. arena_dev: caller-owned device memory of
+ * arena_volumes >= max_outer_iterations + 3 volumes of `dtype` (residual,
+ * scratch, one phi per atom). rows_out: max_outer_iterations x 6 doubles
+ * (w, m, sigma, d); records: max_outer_iterations entries. */
+int sfw3d_solve(sfw3d_ctx* ctx, const sfw3d_psf* psf, const sfw3d_table* table, int dtype,
+                const void* y_dev, const sfw3d_solve_options* opts, void* arena_dev,
+                int arena_volumes, double* rows_out, int* n_atoms, double* criterion_out,
+                int* termination, sfw3d_solve_record* records, int* n_records);
+
 #ifdef __cplusplus
 }
 #endif

@@ -34,7 +34,7 @@ EXPORTS = (
     "sfw3d_last_refine_count", "sfw3d_table_set_option", "sfw3d_eta_argmax_slab",
     "sfw3d_cost_grad_slab_dev", "sfw3d_render_slab", "sfw3d_atom_sums_slab",
     "sfw3d_volume_info", "sfw3d_volume_read", "sfw3d_volume_write",
-    "sfw3d_lbfgsb_minimize", "sfw3d_refine_eta_max", "sfw3d_local_descent",
+    "sfw3d_lbfgsb_minimize", "sfw3d_refine_eta_max", "sfw3d_local_descent", "sfw3d_solve",
 )
 
 
@@ -52,11 +52,33 @@ HALO_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int
                       C.c_int)
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int, C.c_int)
 
+class SolveOptions(C.Structure):
+    """sfw3d_solve_options (include/sfw3d_cuda.h)."""
+    _fields_ = [("lam", C.c_double), ("max_outer_iterations", C.c_int32), ("boosted", C.c_int32),
+                ("eta_threshold", C.c_double), ("eta_slack", C.c_double), ("lasso_tol", C.c_double),
+                ("lasso_max_iter", C.c_int32), ("descent_max_iter", C.c_int32),
+                ("descent_gtol", C.c_double), ("descent_ftol", C.c_double),
+                ("prune_rel_tol", C.c_double), ("duplicate_tol", C.c_double),
+                ("lower", C.c_double * 5), ("upper", C.c_double * 5), ("window", C.c_int32 * 6),
+                ("n_sigma", C.c_int32), ("n_shape", C.c_int32),
+                ("sigma_grid", C.POINTER(C.c_double)), ("shape_grid", C.POINTER(C.c_double))]
+
+
+class SolveRecord(C.Structure):
+    """sfw3d_solve_record (include/sfw3d_cuda.h)."""
+    _fields_ = [("index", C.c_int32), ("eta_max", C.c_double), ("criterion_before", C.c_double),
+                ("criterion_after_lasso", C.c_double), ("criterion_after_descent", C.c_double),
+                ("atom_count", C.c_int32), ("t_certificate", C.c_double), ("t_lasso", C.c_double),
+                ("t_descent", C.c_double)]
+
+
 # objective callback of the in-library L-BFGS-B (include/sfw3d_cuda.h: sfw3d_objective_fn)
 OBJECTIVE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
                            C.POINTER(C.c_double))
 
 _SIGNATURES = {
+    "sfw3d_solve": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp, C.POINTER(SolveOptions), _vp, C.c_int, _dp,
+                              _ip, _dp, _ip, C.POINTER(SolveRecord), _ip]),
     "sfw3d_lbfgsb_minimize": (C.c_int, [C.c_int, _dp, _dp, _dp, _i32p, C.c_int, C.c_double,
                                         C.c_double, C.c_int, C.c_int, C.c_int, OBJECTIVE_FN, _vp,
                                         _dp, _i32p]),
@@ -125,6 +147,11 @@ _lib = None
 # call per optimisation); "scipy": the reference's scipy.optimize loop over the
 # same device evaluations (kept as the cross-check of the parity tests)
 OPTIMIZER = "native"
+
+# "native": sfw / bsfw run the whole outer loop inside the library (sfw3d_solve);
+# "python": the host loop of solvers._solve over the same device calls (also
+# taken when a step record is requested or OPTIMIZER is "scipy")
+SOLVER = "native"
 _lib_lock = threading.Lock()
 
 

@@ -110,3 +110,35 @@ def test_bsfw_native_equals_scipy(P, case):
     np.testing.assert_allclose(a[:, [0, 4, 5]], b[:, [0, 4, 5]], rtol=1e-5)
     assert abs(rn.criterion - rs.criterion) <= 1e-9 * abs(rs.criterion)
     print(f"bsfw cfg1: native {rn.trace.t_total:.3f} s, scipy loop {rs.trace.t_total:.3f} s")
+
+
+@pytest.mark.parametrize("algorithm", ["bsfw", "sfw"])
+def test_native_loop_equals_python_loop(P, case, algorithm):
+    """sfw3d_solve (the outer loop inside the library) against
+    the host loop of solvers._solve over the same device calls."""
+    from paper_2009_05473_b200 import _native as N, solvers
+    orig = solvers.make_parameter_grids
+    solvers.make_parameter_grids = lambda b, ns, nd: case["grids"]
+    try:
+        def run(mode):
+            old, N.SOLVER = N.SOLVER, mode
+            try:
+                return getattr(P, algorithm)(
+                    P.Volume(case["y"]), case["psf"],
+                    P.SolverOptions(lam=case["lam"], max_outer_iterations=20), case["bounds"])
+            finally:
+                N.SOLVER = old
+        rn, rp = run("native"), run("python")
+    finally:
+        solvers.make_parameter_grids = orig
+    assert rn.termination == rp.termination
+    assert len(rn.trace.records) == len(rp.trace.records)
+    for a, b in zip(rn.trace.records, rp.trace.records):
+        assert a.index == b.index and a.atom_count == b.atom_count
+        assert (a.criterion_after_lasso is None) == (b.criterion_after_lasso is None)
+        assert (a.criterion_after_descent is None) == (b.criterion_after_descent is None)
+        np.testing.assert_allclose(a.eta_max, b.eta_max, rtol=1e-12)
+        np.testing.assert_allclose(a.criterion_before, b.criterion_before, rtol=1e-12)
+    np.testing.assert_allclose(rn.measure.to_rows(), rp.measure.to_rows(), rtol=1e-10, atol=1e-10)
+    assert abs(rn.criterion - rp.criterion) <= 1e-12 * abs(rp.criterion)
+    print(f"{algorithm} cfg1: library loop {rn.trace.t_total:.3f} s, host loop {rp.trace.t_total:.3f} s")
