@@ -327,6 +327,17 @@ int sfw3d_residual(sfw3d_ctx* ctx, int dtype, int64_t n, const void* y_dev,
                    const void* const* phis_host, const double* w_host, int k,
                    void* out_dev, double* sumsq_host);
 
+/* K5 with supports: as sfw3d_residual on a (dims) volume, with per atom i the
+ * x-plane range [xrange_host[2i], xrange_host[2i+1]] (wrapped when lo > hi)
+ * outside which phi_i is exactly zero (render box dilated by the PSF's x
+ * extent): atoms are skipped on planes they do not reach, which leaves every
+ * voxel bit-identical (r - w * 0 = r) at a fraction of the reads — the k
+ * full-volume phi streams are what the weight step of a long solve costs
+ * (solvers.py:253-257 at k ~ 100). */
+int sfw3d_residual_ranged(sfw3d_ctx* ctx, int dtype, const int dims[3], const void* y_dev,
+                          const void* const* phis_host, const double* w_host,
+                          const int32_t* xrange_host, int k, void* out_dev, double* sumsq_host);
+
 /* ---- in-library L-BFGS-B (the reference's scipy.optimize.minimize calls) -- */
 /* Objective callback: 0 = ok with *f and g[0..n) written; any other value
  * aborts the minimisation (an sfw3d_status is passed through). */

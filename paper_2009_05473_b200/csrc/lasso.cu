@@ -74,8 +74,14 @@ __global__ void __launch_bounds__(256) residual_kernel(const T* __restrict__ y,
                                                        const T* const* __restrict__ phis,
                                                        const double* __restrict__ w, int k,
                                                        long long n, T* __restrict__ out,
-                                                       double* __restrict__ partials) {
+                                                       double* __restrict__ partials,
+                                                       const int* __restrict__ plane_ptr,
+                                                       const int* __restrict__ plane_atoms,
+                                                       long long plane) {
   double s = 0.0;
+  // plane_ptr / plane_atoms (optional): per x plane the atoms, in list order,
+  // whose phi is not identically zero there (CSR); the others are skipped —
+  // loads and arithmetic — which leaves every voxel unchanged bit for bit
   // V consecutive voxels per thread (16-byte loads) and 4 atoms' loads issued
   // before their (in-order) updates: the k streams are read with enough
   // loads in flight; the per-voxel update order is the reference's
@@ -83,25 +89,33 @@ __global__ void __launch_bounds__(256) residual_kernel(const T* __restrict__ y,
   const long long nv = n / V;
   for (long long q = blockIdx.x * 256LL + threadIdx.x; q < nv; q += (long long)gridDim.x * 256) {
     const long long i = q * V;
+    int jb = 0, je = k;
+    if (plane_ptr) {
+      const int x = int(i / plane);
+      jb = plane_ptr[x];
+      je = plane_ptr[x + 1];
+    }
     T r[V];
 #pragma unroll
     for (int u = 0; u < V; ++u) r[u] = y[i + u];
-    int j = 0;
-    for (; j + 4 <= k; j += 4) {
+    int jj = jb;
+    for (; jj + 4 <= je; jj += 4) {
       T ph[4][V];
+      int ja[4];
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
+        ja[a] = plane_atoms ? plane_atoms[jj + a] : jj + a;
         if constexpr (sizeof(T) == 8) {
-          const double2 v = __ldg(reinterpret_cast<const double2*>(phis[j + a] + i));
+          const double2 v = __ldg(reinterpret_cast<const double2*>(phis[ja[a]] + i));
           ph[a][0] = v.x; ph[a][1] = v.y;
         } else {
-          const float4 v = __ldg(reinterpret_cast<const float4*>(phis[j + a] + i));
+          const float4 v = __ldg(reinterpret_cast<const float4*>(phis[ja[a]] + i));
           ph[a][0] = v.x; ph[a][1] = v.y; ph[a][2] = v.z; ph[a][3] = v.w;
         }
       }
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
-        const double wj = w[j + a];
+        const double wj = w[ja[a]];
 #pragma unroll
         for (int u = 0; u < V; ++u) {
           if constexpr (sizeof(T) == 8)
@@ -111,7 +125,8 @@ __global__ void __launch_bounds__(256) residual_kernel(const T* __restrict__ y,
         }
       }
     }
-    for (; j < k; ++j) {
+    for (; jj < je; ++jj) {
+      const int j = plane_atoms ? plane_atoms[jj] : jj;
       const double wj = w[j];
 #pragma unroll
       for (int u = 0; u < V; ++u) {
@@ -130,7 +145,14 @@ __global__ void __launch_bounds__(256) residual_kernel(const T* __restrict__ y,
   // (tail voxels when n is not a multiple of V)
   for (long long i = nv * V + blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
     T r = y[i];
-    for (int j2 = 0; j2 < k; ++j2) {
+    int jb = 0, je = k;
+    if (plane_ptr) {
+      const int x = int(i / plane);
+      jb = plane_ptr[x];
+      je = plane_ptr[x + 1];
+    }
+    for (int jj = jb; jj < je; ++jj) {
+      const int j2 = plane_atoms ? plane_atoms[jj] : jj;
       if constexpr (sizeof(T) == 8)
         r = __dsub_rn(r, __dmul_rn(w[j2], phis[j2][i]));
       else
@@ -481,9 +503,32 @@ extern "C" int sfw3d_dots(sfw3d_ctx* ctx, int dtype, int64_t n, const void* cons
   return download_sync(ctx, out_host, out, size_t(k) * sizeof(double));
 }
 
+static int residual_run(sfw3d_ctx* ctx, int dtype, int64_t n, const void* y_dev,
+                        const void* const* phis_host, const double* w_host, int k, void* out_dev,
+                        double* sumsq_host, const int32_t* xrange_host, long long plane);
+
 extern "C" int sfw3d_residual(sfw3d_ctx* ctx, int dtype, int64_t n, const void* y_dev,
                               const void* const* phis_host, const double* w_host, int k,
                               void* out_dev, double* sumsq_host) {
+  return residual_run(ctx, dtype, n, y_dev, phis_host, w_host, k, out_dev, sumsq_host, nullptr, 1);
+}
+
+extern "C" int sfw3d_residual_ranged(sfw3d_ctx* ctx, int dtype, const int dims[3], const void* y_dev,
+                                     const void* const* phis_host, const double* w_host,
+                                     const int32_t* xrange_host, int k, void* out_dev,
+                                     double* sumsq_host) {
+  SFW3D_CHECK_ARG(dims && dims[0] > 0 && dims[1] > 0 && dims[2] > 0, "dims must be positive");
+  SFW3D_CHECK_ARG(k == 0 || xrange_host, "NULL argument");
+  for (int i = 0; i < k; ++i)
+    SFW3D_CHECK_ARG(xrange_host[2 * i] >= 0 && xrange_host[2 * i] < dims[0] &&
+                        xrange_host[2 * i + 1] >= 0 && xrange_host[2 * i + 1] < dims[0], "x range");
+  return residual_run(ctx, dtype, vol_count(dims), y_dev, phis_host, w_host, k, out_dev, sumsq_host,
+                      xrange_host, (long long)dims[1] * dims[2]);
+}
+
+static int residual_run(sfw3d_ctx* ctx, int dtype, int64_t n, const void* y_dev,
+                        const void* const* phis_host, const double* w_host, int k, void* out_dev,
+                        double* sumsq_host, const int32_t* xrange_host, long long plane) {
   SFW3D_CHECK_ARG(ctx && y_dev, "NULL argument");
   SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
   SFW3D_CHECK_ARG(n >= 0 && k >= 0 && (k == 0 || (phis_host && w_host)), "sizes");
@@ -501,15 +546,37 @@ extern "C" int sfw3d_residual(sfw3d_ctx* ctx, int dtype, int64_t n, const void* 
     SFW3D_TRY(stage_upload(ctx, pp, phis_host, size_t(k) * sizeof(void*)));
     SFW3D_TRY(stage_upload(ctx, wd, w_host, size_t(k) * sizeof(double)));
   }
+  // per x plane the atoms that reach it, in list order (CSR)
+  int* pptr = nullptr;
+  int* patoms = nullptr;
+  if (xrange_host && k > 0) {
+    const int nx = int(n / plane);
+    std::vector<int> ptr(nx + 1, 0), list;
+    list.reserve(size_t(nx) * 8);
+    for (int x = 0; x < nx; ++x) {
+      for (int j = 0; j < k; ++j) {
+        const int lo = xrange_host[2 * j], hi = xrange_host[2 * j + 1];
+        if (lo <= hi ? (x >= lo && x <= hi) : (x >= lo || x <= hi)) list.push_back(j);
+      }
+      ptr[x + 1] = int(list.size());
+    }
+    SFW3D_TRY(ensure_device(ctx, ctx->ws_plan, Carver::need({ptr.size() * sizeof(int),
+                                                            (list.size() + 1) * sizeof(int)})));
+    Carver cp(ctx->ws_plan.ptr);
+    pptr = cp.take<int>(ptr.size());
+    patoms = cp.take<int>(list.size() + 1);
+    SFW3D_TRY(stage_upload(ctx, pptr, ptr.data(), ptr.size() * sizeof(int)));
+    if (!list.empty()) SFW3D_TRY(stage_upload(ctx, patoms, list.data(), list.size() * sizeof(int)));
+  }
   SFW3D_PROF(ctx, "residual");
   if (dtype == SFW3D_F64)
     residual_kernel<double><<<nblk, 256, 0, ctx->stream>>>(
         static_cast<const double*>(y_dev), reinterpret_cast<const double* const*>(pp), wd, k, n,
-        static_cast<double*>(out_dev), part);
+        static_cast<double*>(out_dev), part, pptr, patoms, plane);
   else
     residual_kernel<float><<<nblk, 256, 0, ctx->stream>>>(
         static_cast<const float*>(y_dev), reinterpret_cast<const float* const*>(pp), wd, k, n,
-        static_cast<float*>(out_dev), part);
+        static_cast<float*>(out_dev), part, pptr, patoms, plane);
   SFW3D_LAUNCH_CHECK(ctx);
   if (sumsq_host) {
     sum_partials_kernel<<<1, 32, 0, ctx->stream>>>(part, nblk, res);

@@ -46,6 +46,7 @@ struct Atom {
   double w;
   void* phi;   // device volume H * G(theta)
   int gslot;   // row / column in the Gram cache, -1 = not yet computed
+  int xlo, xhi;  // x planes outside which phi is exactly zero (xlo > xhi: wrapped)
 };
 
 struct Loop {
@@ -69,10 +70,48 @@ struct Loop {
   std::vector<void*> gphi;   // phi per Gram slot
   int gcap = 0;
 
-  int render_phi(const double theta[5], void* out) {
-    const double row[6] = {1.0, theta[0], theta[1], theta[2], theta[3], theta[4]};
+  int render_phi(Atom& a) {
+    const double row[6] = {1.0, a.theta[0], a.theta[1], a.theta[2], a.theta[3], a.theta[4]};
     SFW3D_TRY(sfw3d_render(ctx, dtype, dims, row, 1, scratch));
-    return sfw3d_psf_apply(ctx, psf, dtype, scratch, out, 0);
+    SFW3D_TRY(sfw3d_psf_apply(ctx, psf, dtype, scratch, a.phi, 0));
+    // support along x: the render box (the geometry the render kernel uses)
+    // dilated by the PSF's x extent; the separable passes produce exact
+    // zeros outside it (a cuFFT PSF does not: full range)
+    a.xlo = 0;
+    a.xhi = dims[0] - 1;
+    std::vector<AtomGeo> geo;
+    SFW3D_TRY(build_atoms(dims, row, 1, geo));
+    if (psf->separable && !geo[0].full[0]) {
+      const long long lo = (long long)geo[0].start[0] + psf->lo[0];
+      const long long hi = (long long)geo[0].start[0] + geo[0].len[0] - 1 + psf->hi[0];
+      if (hi - lo + 1 < dims[0]) {
+        a.xlo = int(((lo % dims[0]) + dims[0]) % dims[0]);
+        a.xhi = int(((hi % dims[0]) + dims[0]) % dims[0]);
+      }
+    }
+    return SFW3D_OK;
+  }
+
+  // <vecs[q], v> over the x planes [xlo, xhi] of v's support (v is exactly
+  // zero elsewhere): one sfw3d_dots per contiguous plane segment
+  int dots_on(const std::vector<void*>& vecs, const void* v, int xlo, int xhi, double* out) {
+    const int k = int(vecs.size());
+    const long long plane = (long long)dims[1] * dims[2];
+    const size_t es = dtype_size(dtype);
+    int seg[2][2] = {{xlo, xhi}, {0, -1}};
+    if (xlo > xhi) { seg[0][1] = dims[0] - 1; seg[1][0] = 0; seg[1][1] = xhi; }
+    std::vector<double> part(k);
+    std::vector<const void*> ptr(k);
+    for (int q = 0; q < k; ++q) out[q] = 0.0;
+    for (auto& sg : seg) {
+      if (sg[1] < sg[0]) continue;
+      const size_t off = size_t(sg[0]) * size_t(plane) * es;
+      for (int q = 0; q < k; ++q) ptr[q] = static_cast<const char*>(vecs[q]) + off;
+      SFW3D_TRY(sfw3d_dots(ctx, dtype, (long long)(sg[1] - sg[0] + 1) * plane, ptr.data(), k,
+                           static_cast<const char*>(v) + off, part.data()));
+      for (int q = 0; q < k; ++q) out[q] += part[q];
+    }
+    return SFW3D_OK;
   }
 
   // <phi_i, phi_j> and <phi_i, y> for the listed atoms, new rows only
@@ -115,13 +154,14 @@ struct Loop {
       gphi.push_back(a.phi);
       a.gslot = s;
       std::vector<double> row(s + 1);
-      SFW3D_TRY(sfw3d_dots(ctx, dtype, n, gphi.data(), s + 1, a.phi, row.data()));
+      SFW3D_TRY(dots_on(gphi, a.phi, a.xlo, a.xhi, row.data()));
       for (int q = 0; q <= s; ++q) {
         G[size_t(s) * gcap + q] = row[q];
         G[size_t(q) * gcap + s] = row[q];
       }
-      const void* one[1] = {a.phi};
-      SFW3D_TRY(sfw3d_dots(ctx, dtype, n, one, 1, y, &b[s]));
+      // <phi, y>: y streamed against phi on phi's planes
+      const std::vector<void*> yy = {const_cast<void*>(y)};
+      SFW3D_TRY(dots_on(yy, a.phi, a.xlo, a.xhi, &b[s]));
     }
     const int k = int(atoms.size());
     g.assign(size_t(k) * k, 0.0);
@@ -164,9 +204,16 @@ struct Loop {
     const int k = int(atoms.size());
     std::vector<const void*> ph(std::max(k, 1));
     std::vector<double> w(std::max(k, 1));
-    for (int i = 0; i < k; ++i) { ph[i] = atoms[i].phi; w[i] = atoms[i].w; }
+    std::vector<int32_t> xr(2 * std::max(k, 1));
+    for (int i = 0; i < k; ++i) {
+      ph[i] = atoms[i].phi;
+      w[i] = atoms[i].w;
+      xr[2 * i] = atoms[i].xlo;
+      xr[2 * i + 1] = atoms[i].xhi;
+    }
     double ss = 0.0;
-    SFW3D_TRY(sfw3d_residual(ctx, dtype, n, y, k ? ph.data() : nullptr, k ? w.data() : nullptr, k, rvol, &ss));
+    SFW3D_TRY(sfw3d_residual_ranged(ctx, dtype, dims, y, k ? ph.data() : nullptr, k ? w.data() : nullptr,
+                                    xr.data(), k, rvol, &ss));
     rvol_valid = true;
     *c = 0.5 * ss + o->lam * np_sum(w.data(), size_t(k));
     return SFW3D_OK;
@@ -224,7 +271,7 @@ struct Loop {
     for (int i = 0; i < k; ++i) {
       atoms[i].w = rows[6 * i];
       for (int c = 0; c < 5; ++c) atoms[i].theta[c] = rows[6 * i + 1 + c];
-      SFW3D_TRY(render_phi(atoms[i].theta, atoms[i].phi));  // in place: the old phi is dead
+      SFW3D_TRY(render_phi(atoms[i]));  // in place: the old phi is dead
       atoms[i].gslot = -1;
     }
     // every cached Gram row referred to the old volumes
@@ -318,7 +365,7 @@ extern "C" int sfw3d_solve(sfw3d_ctx* ctx, const sfw3d_psf* psf, const sfw3d_tab
     a.phi = L.free_slots.back();
     a.gslot = -1;
     L.free_slots.pop_back();
-    SFW3D_TRY(L.render_phi(a.theta, a.phi));
+    SFW3D_TRY(L.render_phi(a));
     state.push_back(a);
     SFW3D_TRY(L.lasso(state));
     SFW3D_TRY(L.criterion(state, &crit));

@@ -137,8 +137,55 @@ def test_native_loop_equals_python_loop(P, case, algorithm):
         assert a.index == b.index and a.atom_count == b.atom_count
         assert (a.criterion_after_lasso is None) == (b.criterion_after_lasso is None)
         assert (a.criterion_after_descent is None) == (b.criterion_after_descent is None)
-        np.testing.assert_allclose(a.eta_max, b.eta_max, rtol=1e-12)
-        np.testing.assert_allclose(a.criterion_before, b.criterion_before, rtol=1e-12)
-    np.testing.assert_allclose(rn.measure.to_rows(), rp.measure.to_rows(), rtol=1e-10, atol=1e-10)
-    assert abs(rn.criterion - rp.criterion) <= 1e-12 * abs(rp.criterion)
+        # (the library loop sums the Gram rows over each phi's x support only:
+        # same inner products, another rounding order, amplified by the slides)
+        np.testing.assert_allclose(a.eta_max, b.eta_max, rtol=1e-8)
+        np.testing.assert_allclose(a.criterion_before, b.criterion_before, rtol=1e-10)
+    np.testing.assert_allclose(rn.measure.to_rows(), rp.measure.to_rows(), rtol=1e-6, atol=1e-6)
+    assert abs(rn.criterion - rp.criterion) <= 1e-10 * abs(rp.criterion)
     print(f"{algorithm} cfg1: library loop {rn.trace.t_total:.3f} s, host loop {rp.trace.t_total:.3f} s")
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_residual_with_supports_is_bit_identical(P, case, prec):
+    """sfw3d_residual_ranged skips atoms on x planes where their phi is exactly
+    zero: same volume and sum of squares as sfw3d_residual, bit for bit."""
+    import ctypes as C
+    import torch
+    from paper_2009_05473_b200 import _native as N, solvers
+    from paper_2009_05473_b200.forward import code_of, to_dev
+    P.set_precision(prec)
+    try:
+        code = N.dtype_code()
+        y = to_dev(P.Volume(case["y"]), code)
+        thetas = [P.AtomParams(m=(30.2, 20.1, 40.7), sigma=2.0, d=2.0),
+                  P.AtomParams(m=(8.0, 50.0, 12.0), sigma=3.0, d=1.5),     # wraps through x = 0
+                  P.AtomParams(m=(55.5, 33.0, 30.0), sigma=2.5, d=2.5),    # wraps through x = n - 1
+                  P.AtomParams(m=(40.0, 40.0, 40.0), sigma=1.5, d=1.8)]
+        phis = [solvers.phi_dev(t, case["psf"], code) for t in thetas]
+        w = np.array([1.3, 0.7, 2.1, 0.4])
+        nx = y.shape[0]
+        xr = np.zeros((len(phis), 2), dtype=np.int32)
+        for i, p in enumerate(phis):
+            on = torch.any(p.reshape(nx, -1) != 0, dim=1).cpu().numpy()
+            idx = np.flatnonzero(on)
+            if on.all():
+                xr[i] = (0, nx - 1)
+            elif on[0] and on[-1]:  # wrapped support: the gap is in the middle
+                gap = np.flatnonzero(~on)
+                xr[i] = (gap[-1] + 1, gap[0] - 1)
+            else:
+                xr[i] = (idx[0], idx[-1])
+        assert (xr[:, 0] > xr[:, 1]).any() and (xr[:, 0] <= xr[:, 1]).any()
+        ref, ss_ref = solvers.residual_dev(y, w, phis)
+        out = torch.empty_like(y)
+        ss = C.c_double()
+        arr = (C.c_void_p * len(phis))(*[t.data_ptr() for t in phis])
+        N.check(N.lib().sfw3d_residual_ranged(N.context(0).handle, code_of(y), N.dims_arg(y.shape),
+                                              N.ptr(y), arr, N.f64_ptr(w),
+                                              xr.ctypes.data_as(C.POINTER(C.c_int32)), len(phis),
+                                              N.ptr(out), C.byref(ss)))
+        assert torch.equal(out, ref)
+        assert ss.value == ss_ref
+    finally:
+        P.set_precision("f64")
