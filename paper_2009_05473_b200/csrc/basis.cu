@@ -1560,6 +1560,69 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
     const long long i0 = (qbeg + (long long)it * kMixThreads) * V;
     const bool row_win = x >= wlo.x && x <= whi.x && y >= wlo.y && y <= whi.y;
     const bool zfull = z0 >= wlo.z && z0 + V - 1 <= whi.z;
+    if constexpr (sizeof(T) == 4 && NMD >= 16) {
+      // fp32, full 16-member slices (measured: config-3 mix 1.88 -> 1.52 ms;
+      // the 12-member config-4 slice is closer to its HBM bound and was 8%
+      // slower packed, so it keeps the scalar form): members in pairs
+      // (m, m + 1) on the packed FFMA2 pipe — the
+      // weight pairs come straight out of the 16-byte shared-memory loads,
+      // a voxel is broadcast to both halves; each half is the same RN FMA
+      // as the scalar form (bit-identical), at half the FMA issue slots
+      static_assert(NMD % 4 == 0, "member pairs from 16-byte rows");
+      f32x2 acc2[NMD / 2][V];
+      {
+        T v[V];
+        take(v);
+        f32x2 vv[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) vv[j] = pack2(v[j], v[j]);
+#pragma unroll
+        for (int p2 = 0; p2 < NMD / 2; p2 += 2) {
+          const ulonglong2 q = *reinterpret_cast<const ulonglong2*>(sw0 + 2 * p2);
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            acc2[p2][j] = mul2(q.x, vv[j]);
+            acc2[p2 + 1][j] = mul2(q.y, vv[j]);
+          }
+        }
+        if (absparts) {
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            abs_s += double(fabs(v[j]));
+            abs_m = fmax(abs_m, fabs(v[j]));
+          }
+        }
+      }
+      for (int k = 0; k < K; ++k) {
+        T v[V];
+        take(v);
+        f32x2 vv[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) vv[j] = pack2(v[j], v[j]);
+        const T* wk = sW + k * NMD;
+#pragma unroll
+        for (int p2 = 0; p2 < NMD / 2; p2 += 2) {
+          const ulonglong2 q = *reinterpret_cast<const ulonglong2*>(wk + 2 * p2);
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            acc2[p2][j] = fma2(q.x, vv[j], acc2[p2][j]);
+            acc2[p2 + 1][j] = fma2(q.y, vv[j], acc2[p2 + 1][j]);
+          }
+        }
+        const int c = sCt[k];
+        if (c >= 0 && row_win) track(NMD + c, v, i0, zfull, z0);  // a copy's eta * lam is T_k
+      }
+      if (row_win) {
+#pragma unroll
+        for (int m = 0; m < NMD; ++m) {
+          if (m >= nmd) break;
+          T a[V];
+#pragma unroll
+          for (int j = 0; j < V; ++j) a[j] = (m & 1) ? hi32(acc2[m / 2][j]) : lo32(acc2[m / 2][j]);
+          track(m, a, i0, zfull, z0);
+        }
+      }
+    } else {
     T acc[NMD][V];
     {
       T v[V];
@@ -1598,13 +1661,13 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
       const int c = sCt[k];
       if (c >= 0 && row_win) track(NMD + c, v, i0, zfull, z0);  // a copy's eta * lam is T_k
     }
-#pragma unroll
     if (row_win) {
 #pragma unroll
       for (int m = 0; m < NMD; ++m) {
         if (m >= nmd) break;
         track(m, acc[m], i0, zfull, z0);
       }
+    }
     }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
