@@ -353,8 +353,8 @@ def cert_workload(args, rank, world, dev):
     # roofline of the dominant kernel: one profiled step
     ctx.profile(True)
     step()
-    fam = {f: ctx.profile_read(f) for f in ("eta_direct", "eta_basis", "eta_mix", "eta_refine",
-                                           "psf_pass", "pad", "argmax")}
+    fam = {f: ctx.profile_read(f) for f in ("eta_direct", "eta_basis", "eta_basis_wide", "eta_mix",
+                                           "eta_refine", "psf_pass", "pad", "argmax")}
     ctx.profile(False)
     refine_count = N.last_refine_count()
     step_ms = sum(v[0] for v in fam.values())
@@ -376,28 +376,52 @@ def cert_workload(args, rank, world, dev):
             "launches": fam["eta_direct"][1],
             "avg_launch_ms": fam["eta_direct"][0] / fam["eta_direct"][1],
             "share_of_step": fam["eta_direct"][0] / step_ms if step_ms else None}
-    if fam["eta_basis"][1]:
-        n_pass = fam["eta_basis"][1]
-        n_terms = n_pass // 3
-        # per pass: read in + write out (fp32), one z/y/x triple per shared term
-        nbytes = 4.0 * nvox * 2 * n_pass
-        flops = 2.0 * info["basis_taps_per_voxel"] * nvox
-        t = fam["eta_basis"][0] / 1e3
+    # basis passes, each class against its own bound: filters of <= 24 taps run
+    # the narrow tiles (HBM-bound: 2 volumes moved per pass), longer ones the
+    # wide tiles (FP32-bound: 2 * taps FLOP per voxel); per-pass tap counts
+    # from the table (sfw3d_table_basis_passes), times from the library's events
+    ptaps = info.get("basis_pass_taps", [])
+    n_terms_basis = len(ptaps) // 3
+
+    def pass_roofline(ms, n_pass, taps_sum, kern, extra=None):
+        nbytes = 4.0 * nvox * 2 * n_pass          # per pass: read in + write out (fp32)
+        flops = 2.0 * taps_sum * nvox
+        t = ms / 1e3
         gbs, tfl = nbytes / t / 1e9, flops / t / 1e12
         hbm = gbs / hbm_peak > tfl / fp32_peak
-        rooflines["eta_basis"] = {
-            "bound": "hbm" if hbm else "fp32",
-            "kernel": "pass_tile2_kernel / pass_z2_kernel (shared separable basis terms)",
-            "achieved": gbs if hbm else tfl, "peak": hbm_peak if hbm else fp32_peak,
-            "unit": "GB/s" if hbm else "TFLOP/s",
-            "frac": max(gbs / hbm_peak, tfl / fp32_peak), "traffic": None,
-            "achieved_gbs": gbs, "achieved_tflops": tfl, "hbm_peak_gbs": hbm_peak,
-            "fp32_peak_tflops": fp32_peak, "bytes_per_step": nbytes, "flops_per_step": flops,
-            "shared_terms": n_terms, "launches": n_pass,
-            "avg_launch_ms": fam["eta_basis"][0] / n_pass,
-            "share_of_step": fam["eta_basis"][0] / step_ms if step_ms else None}
+        out = {"bound": "hbm" if hbm else "fp32", "kernel": kern,
+               "achieved": gbs if hbm else tfl, "peak": hbm_peak if hbm else fp32_peak,
+               "unit": "GB/s" if hbm else "TFLOP/s",
+               "frac": max(gbs / hbm_peak, tfl / fp32_peak), "traffic": None,
+               "achieved_gbs": gbs, "achieved_tflops": tfl, "hbm_peak_gbs": hbm_peak,
+               "fp32_peak_tflops": fp32_peak, "bytes_per_step": nbytes, "flops_per_step": flops,
+               "launches": n_pass, "avg_launch_ms": ms / n_pass,
+               "share_of_step": ms / step_ms if step_ms else None}
+        out.update(extra or {})
+        return out
+
+    nb_n, nb_w = fam["eta_basis"][1], fam["eta_basis_wide"][1]
+    if nb_n + nb_w:
+        # the family of the 1-D basis passes (z, y, x per shared term) ...
+        rooflines["eta_basis"] = pass_roofline(
+            fam["eta_basis"][0] + fam["eta_basis_wide"][0], nb_n + nb_w, info["basis_taps_per_voxel"],
+            "pass_tile2x2_kernel / pass_z2_kernel (shared separable basis terms)",
+            {"shared_terms": n_terms_basis or (nb_n + nb_w) // 3})
+        # ... and its two classes against their own bounds: filters of <= 24
+        # taps (narrow tiles), longer ones (wide tiles); tap counts from the
+        # table (sfw3d_table_basis_passes), times from the library's events
+        narrow, wide_t = [t for t in ptaps if t <= 24], [t for t in ptaps if t > 24]
+        if not sharded and len(narrow) == nb_n and len(wide_t) == nb_w:
+            classes = {}
+            if nb_n:
+                classes["narrow"] = pass_roofline(fam["eta_basis"][0], nb_n, sum(narrow),
+                                                  "filters of <= 24 taps", {"pass_taps": sorted(narrow)})
+            if nb_w:
+                classes["wide"] = pass_roofline(fam["eta_basis_wide"][0], nb_w, sum(wide_t),
+                                                "filters of > 24 taps", {"pass_taps": sorted(wide_t)})
+            rooflines["eta_basis"]["classes"] = classes
     if fam["eta_mix"][1]:
-        n_terms = fam["eta_basis"][1] // 3
+        n_terms = n_terms_basis or (fam["eta_basis"][1] + fam["eta_basis_wide"][1]) // 3
         # reads b and every shared term once, forms every member candidate
         nbytes = 4.0 * nvox * (n_terms + 1)
         t = fam["eta_mix"][0] / 1e3
@@ -410,16 +434,20 @@ def cert_workload(args, rank, world, dev):
             "share_of_step": fam["eta_mix"][0] / step_ms if step_ms else None}
     # measured DRAM bytes per launch (ncu capture of the same workload,
     # profiles/round1/traffic_cert512.json) where available
-    tpath = ROOT / "profiles" / "round1" / "traffic_cert512.json"
-    if tpath.exists() and n == 512 and world == 1:
+    tpath = next((p for p in (ROOT / "profiles" / "round2" / "traffic_cert512.json",
+                              ROOT / "profiles" / "round1" / "traffic_cert512.json") if p.exists()), None)
+    if tpath is not None and n == 512 and world == 1:
         fams = json.loads(tpath.read_text())["families"]
         for f, rl in rooflines.items():
             if f in fams:
                 rl["traffic"] = fams[f]["dram_bytes_per_launch"]
-                rl["traffic_source"] = "profiles/round1/traffic_cert512.json (ncu dram__bytes_read+write)"
+                rl["traffic_source"] = f"{tpath.relative_to(ROOT)} (ncu dram__bytes_read+write)"
     roof = None
     if rooflines:
-        dom_fam = max(rooflines, key=lambda f: fam[f][0])
+        fam_ms = {f: fam[f][0] for f in rooflines}
+        if "eta_basis" in fam_ms:
+            fam_ms["eta_basis"] += fam["eta_basis_wide"][0]
+        dom_fam = max(rooflines, key=lambda f: fam_ms[f])
         roof = dict(rooflines[dom_fam])
         roof["dominant_family"] = dom_fam
         roof["all"] = rooflines

@@ -234,6 +234,13 @@ int sfw3d_table_candidate(const sfw3d_table* t, int dtype, int cand, int* uses_b
  *   "refine_cap" exactly re-evaluated voxels per call before members fall
  *                back to the direct kernel (default 65536). */
 int sfw3d_table_set_option(sfw3d_table* t, const char* name, double value);
+/* The 1-D passes of the shared separable basis (3 per term: x, y, z filter
+ * lengths), for the measurement's per-pass rooflines: a pass moves 2 volumes
+ * and executes 2 * taps FLOP per voxel; filters of more than 24 taps run the
+ * FP32-bound wide tiles (profile family "eta_basis_wide"), the others the
+ * HBM-bound narrow tiles ("eta_basis"). *n_out = 3 * terms. */
+int sfw3d_table_basis_passes(const sfw3d_table* t, int dtype, int cap, int32_t* taps_out,
+                             int* n_out);
 int sfw3d_table_destroy(sfw3d_table* t);
 /* Diagnostics: voxels the calling thread's last sfw3d_eta_argmax re-evaluated
  * exactly (refined basis members; > 65536 means it fell back to direct). */

@@ -35,7 +35,7 @@ EXPORTS = (
     "sfw3d_cost_grad_slab_dev", "sfw3d_render_slab", "sfw3d_atom_sums_slab",
     "sfw3d_volume_info", "sfw3d_volume_read", "sfw3d_volume_write",
     "sfw3d_lbfgsb_minimize", "sfw3d_refine_eta_max", "sfw3d_local_descent", "sfw3d_solve",
-    "sfw3d_residual_ranged",
+    "sfw3d_residual_ranged", "sfw3d_table_basis_passes",
 )
 
 
@@ -78,6 +78,7 @@ OBJECTIVE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER
                            C.POINTER(C.c_double))
 
 _SIGNATURES = {
+    "sfw3d_table_basis_passes": (C.c_int, [_vp, C.c_int, C.c_int, _i32p, _ip]),
     "sfw3d_residual_ranged": (C.c_int, [_vp, C.c_int, _ip, _vp, C.POINTER(_vp), _dp, _i32p, C.c_int,
                                         _vp, _dp]),
     "sfw3d_solve": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp, C.POINTER(SolveOptions), _vp, C.c_int, _dp,

@@ -107,7 +107,13 @@ class AtomTemplateTable:
                           "terms": nt.value,
                           "fit_err": fe.value, "direct_taps": cdt.value, "basis_taps": cbt.value,
                           "flops_per_voxel": fl.value})
+        npass = C.c_int()
+        N.check(N.lib().sfw3d_table_basis_passes(h, code, 0, None, C.byref(npass)))
+        ptaps = np.zeros(max(npass.value, 1), dtype=np.int32)
+        N.check(N.lib().sfw3d_table_basis_passes(h, code, npass.value, N.i32_ptr(ptaps),
+                                                 C.byref(npass)))
         return {"n_cand": nc.value, "n_direct": nd.value, "n_basis": nb.value,
+                "basis_pass_taps": [int(v) for v in ptaps[:npass.value]],
                 "direct_taps_per_voxel": dt.value, "basis_taps_per_voxel": bt.value,
                 "direct_flops_per_voxel": df.value, "basis_flops_per_voxel": bf.value,
                 "candidates": cands}

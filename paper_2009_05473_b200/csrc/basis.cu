@@ -1025,6 +1025,9 @@ double basis_set_ebound(const BasisSet* s, int cand) {
 int basis_set_n_terms(const BasisSet* s) { return s ? int(s->betas.size()) : 0; }
 int basis_set_n_members(const BasisSet* s) { return s ? int(s->members.size()) : 0; }
 long long basis_set_taps(const BasisSet* s) { return s ? s->taps_per_voxel : 0; }
+int basis_set_pass_taps(const BasisSet* s, int term, int axis) {
+  return (s && term >= 0 && term < int(s->betas.size())) ? s->tlen[axis][term] : 0;
+}
 double basis_set_member_flops(const BasisSet* s) {
   return s ? 2.0 * double(s->betas.size()) + 2.0 : 0.0;
 }
@@ -1963,12 +1966,15 @@ int basis_set_eval(sfw3d_ctx* ctx, const BasisSet* s, int dtype, const int dims[
                                se->win, se->H, t1, se->link, "eta_basis"));
       continue;
     }
+    // (profile families by the bound of the pass: filters of more than
+    // kBasisNarrowTaps taps are FP32-bound, the others HBM-bound)
+    auto fam = [](int l) { return l > kBasisNarrowTaps ? "eta_basis_wide" : "eta_basis"; };
     SFW3D_TRY(corr_pass_impl(ctx, dtype, src, t1, dims, 2, tp + es * (l0 + l1), s->tlo[2][t], l2,
-                             nullptr, 0.0, 1.0, "eta_basis"));
+                             nullptr, 0.0, 1.0, fam(l2)));
     SFW3D_TRY(corr_pass_impl(ctx, dtype, t1, t2, dims, 1, tp + es * l0, s->tlo[1][t], l1,
-                             nullptr, 0.0, 1.0, "eta_basis"));
+                             nullptr, 0.0, 1.0, fam(l1)));
     SFW3D_TRY(corr_pass_impl(ctx, dtype, t2, terms + size_t(t) * n * es, dims, 0, tp, s->tlo[0][t],
-                             l0, nullptr, 0.0, 1.0, "eta_basis"));
+                             l0, nullptr, 0.0, 1.0, fam(l0)));
   }
   if (!fields && ring2_all_ok(s, dtype, dims)) {
     double* ap = abs_dev ? absparts : nullptr;  // |b| statistics ride along with the mix

@@ -68,6 +68,10 @@ double basis_set_ebound(const BasisSet* s, int cand);
 int basis_set_n_terms(const BasisSet* s);
 int basis_set_n_members(const BasisSet* s);
 long long basis_set_taps(const BasisSet* s);        // per voxel, all shared terms
+int basis_set_pass_taps(const BasisSet* s, int term, int axis);  // taps of one 1-D pass
+// 1-D filters longer than this are FP32-bound (wide tiles), the others HBM-bound
+// (psf.cu: kNarrowTaps; the profile families "eta_basis_wide" / "eta_basis")
+constexpr int kBasisNarrowTaps = 24;
 double basis_set_flops(const BasisSet* s);          // executed flops per voxel (all members)
 double basis_set_member_flops(const BasisSet* s);   // mix flops per voxel per member
 

@@ -950,6 +950,19 @@ extern "C" int sfw3d_table_info(const sfw3d_table* t, int dtype, int* n_cand, in
   return SFW3D_OK;
 }
 
+extern "C" int sfw3d_table_basis_passes(const sfw3d_table* t, int dtype, int cap, int32_t* taps_out,
+                                        int* n_out) {
+  SFW3D_CHECK_ARG(t && n_out, "NULL argument");
+  SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
+  SFW3D_TRY(ensure_basis(t, dtype));
+  const int nt = basis_set_n_terms(t->set(dtype));
+  *n_out = 3 * nt;
+  if (taps_out)
+    for (int k = 0; k < nt && 3 * k + 2 < cap; ++k)
+      for (int a = 0; a < 3; ++a) taps_out[3 * k + a] = basis_set_pass_taps(t->set(dtype), k, a);
+  return SFW3D_OK;
+}
+
 extern "C" int sfw3d_table_candidate(const sfw3d_table* t, int dtype, int cand, int* uses_basis,
                                      int* n_terms, double* fit_err, int64_t* direct_taps,
                                      int64_t* basis_taps, double* flops) {

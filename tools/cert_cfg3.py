@@ -27,7 +27,7 @@ torch.cuda.synchronize()
 ctx = N.context()
 ctx.profile(True)
 eta_argmax_dev(r, 1.0, table, win)
-fam = {f: ctx.profile_read(f) for f in ("eta_direct", "eta_basis", "eta_mix", "eta_refine", "psf_pass", "pad", "argmax")}
+fam = {f: ctx.profile_read(f) for f in ("eta_direct", "eta_basis", "eta_basis_wide", "eta_mix", "eta_refine", "psf_pass", "pad", "argmax")}
 ctx.profile(False)
 info = table.info()
 print({k: (round(v[0], 3), v[1]) for k, v in fam.items() if v[1]}, "refined", N.last_refine_count(),

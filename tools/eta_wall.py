@@ -34,7 +34,7 @@ wall = (time.perf_counter() - t0) / reps
 ctx.profile(True)
 for _ in range(reps):
     eta_argmax_dev(r, 1.0, table, win)
-fam = {f: ctx.profile_read(f) for f in ("eta_direct", "eta_basis", "eta_mix", "eta_refine",
+fam = {f: ctx.profile_read(f) for f in ("eta_direct", "eta_basis", "eta_basis_wide", "eta_mix", "eta_refine",
                                        "psf_pass", "pad", "argmax")}
 ctx.profile(False)
 dev = sum(v[0] for v in fam.values()) / reps

@@ -46,7 +46,7 @@ def ef(*a, **k):
     ctx = N.context()
     ctx.profile(True)
     out = _ef(*a, **k)
-    for f in ("eta_direct", "eta_basis", "eta_mix", "eta_refine", "psf_pass", "pad", "argmax"):
+    for f in ("eta_direct", "eta_basis", "eta_basis_wide", "eta_mix", "eta_refine", "psf_pass", "pad", "argmax"):
         FAM[f] += ctx.profile_read(f)[0]
     ctx.profile(False)
     REF.append(N.last_refine_count())
