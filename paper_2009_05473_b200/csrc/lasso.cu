@@ -95,9 +95,12 @@ __global__ void __launch_bounds__(256) residual_kernel(const T* __restrict__ y,
       jb = plane_ptr[x];
       je = plane_ptr[x + 1];
     }
-    T r[V];
+    // the running residual is kept in fp64 across the atoms (one conversion
+    // per phi value; fp32 storage rounds once, at the end) — the conversion
+    // pipe, not HBM, bounded the per-atom fp32 round trip
+    double r[V];
 #pragma unroll
-    for (int u = 0; u < V; ++u) r[u] = y[i + u];
+    for (int u = 0; u < V; ++u) r[u] = double(y[i + u]);
     int jj = jb;
     for (; jj + 4 <= je; jj += 4) {
       T ph[4][V];
@@ -117,34 +120,26 @@ __global__ void __launch_bounds__(256) residual_kernel(const T* __restrict__ y,
       for (int a = 0; a < 4; ++a) {
         const double wj = w[ja[a]];
 #pragma unroll
-        for (int u = 0; u < V; ++u) {
-          if constexpr (sizeof(T) == 8)
-            r[u] = __dsub_rn(r[u], __dmul_rn(wj, ph[a][u]));  // data -= w * phi
-          else
-            r[u] = T(double(r[u]) - wj * double(ph[a][u]));
-        }
+        for (int u = 0; u < V; ++u)
+          r[u] = __dsub_rn(r[u], __dmul_rn(wj, double(ph[a][u])));  // data -= w * phi
       }
     }
     for (; jj < je; ++jj) {
       const int j = plane_atoms ? plane_atoms[jj] : jj;
       const double wj = w[j];
 #pragma unroll
-      for (int u = 0; u < V; ++u) {
-        if constexpr (sizeof(T) == 8)
-          r[u] = __dsub_rn(r[u], __dmul_rn(wj, phis[j][i + u]));
-        else
-          r[u] = T(double(r[u]) - wj * double(phis[j][i + u]));
-      }
+      for (int u = 0; u < V; ++u) r[u] = __dsub_rn(r[u], __dmul_rn(wj, double(phis[j][i + u])));
     }
 #pragma unroll
     for (int u = 0; u < V; ++u) {
-      if (out) out[i + u] = r[u];
-      s += double(r[u]) * double(r[u]);
+      const T rt = T(r[u]);
+      if (out) out[i + u] = rt;
+      s += double(rt) * double(rt);
     }
   }
   // (tail voxels when n is not a multiple of V)
   for (long long i = nv * V + blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
-    T r = y[i];
+    double rd = double(y[i]);
     int jb = 0, je = k;
     if (plane_ptr) {
       const int x = int(i / plane);
@@ -153,11 +148,9 @@ __global__ void __launch_bounds__(256) residual_kernel(const T* __restrict__ y,
     }
     for (int jj = jb; jj < je; ++jj) {
       const int j2 = plane_atoms ? plane_atoms[jj] : jj;
-      if constexpr (sizeof(T) == 8)
-        r = __dsub_rn(r, __dmul_rn(w[j2], phis[j2][i]));
-      else
-        r = T(double(r) - w[j2] * double(phis[j2][i]));
+      rd = __dsub_rn(rd, __dmul_rn(w[j2], double(phis[j2][i])));
     }
+    const T r = T(rd);
     if (out) out[i] = r;
     s += double(r) * double(r);
   }
