@@ -326,15 +326,46 @@ class _Layout:
     def layout(self, n: int):
         self.n = int(n)
         self.bounds = [slab_bounds(self.n, self.size, r) for r in range(self.size)]
+        self._plans = {}
         return self
+
+    def _exchange_plan(self, lo: int, hi: int):
+        """(sends [(peer, own_row, count)] in each receiver's plan order, recvs
+        [(owner, window_row, count)], local copies [(window_row, own_row, count)])
+        of one exchange; computed once per (lo, hi) — a certificate repeats
+        the same dozen halo shapes every step."""
+        key = (lo, hi)
+        plan = self._plans.get(key)
+        if plan is None:
+            sends, recvs, local = [], [], []
+            for q in range(self.size):
+                if q == self.rank:
+                    continue
+                for owner, _, orow, cnt in halo_plan(self.bounds, self.n, q, lo, hi):
+                    if owner == self.rank:
+                        sends.append((q, orow, cnt))
+            for owner, row, orow, cnt in halo_plan(self.bounds, self.n, self.rank, lo, hi):
+                if owner == self.rank:
+                    local.append((row, orow, cnt))
+                else:
+                    recvs.append((owner, row, cnt))
+            plan = self._plans[key] = (sends, recvs, local)
+        return plan
 
 
 def _fill_halo_self(win, own: int, lo: int, hi: int) -> None:
     """Periodic halos from the rank's own planes (a ring of one)."""
-    for i in range(lo):  # plane x0 - lo + i  ==  owned plane (own - lo + i) mod own
-        win[i] = win[lo + (own - lo + i) % own]
-    for i in range(hi):
-        win[lo + own + i] = win[lo + i % own]
+    # plane x0 - lo + i  ==  owned plane (own - lo + i) mod own; copied in
+    # contiguous runs (one copy per run, not per plane)
+    def runs(dst0, count, src_of):
+        i = 0
+        while i < count:
+            s0 = src_of(i)
+            m = min(count - i, own - s0)  # run until the source wraps
+            win[dst0 + i:dst0 + i + m] = win[lo + s0:lo + s0 + m]
+            i += m
+    runs(0, lo, lambda i: (own - lo + i) % own)
+    runs(lo + own, hi, lambda i: i % own)
 
 
 class TorchComm(_Layout):
@@ -358,18 +389,11 @@ class TorchComm(_Layout):
             return
         if self.n is None:
             raise RuntimeError("TorchComm.layout(n) must be called before halo exchanges")
-        ops, local = [], []
-        for q in range(self.size):  # my sends, in each receiver's plan order
-            if q == self.rank:
-                continue
-            for owner, _, orow, cnt in halo_plan(self.bounds, self.n, q, lo, hi):
-                if owner == self.rank:
-                    ops.append(dist.P2POp(dist.isend, win[lo + orow:lo + orow + cnt], q, self.group))
-        for owner, row, orow, cnt in halo_plan(self.bounds, self.n, self.rank, lo, hi):
-            if owner == self.rank:
-                local.append((row, orow, cnt))
-            else:
-                ops.append(dist.P2POp(dist.irecv, win[row:row + cnt], owner, self.group))
+        sends, recvs, local = self._exchange_plan(lo, hi)
+        ops = [dist.P2POp(dist.isend, win[lo + orow:lo + orow + cnt], q, self.group)
+               for q, orow, cnt in sends]
+        ops += [dist.P2POp(dist.irecv, win[row:row + cnt], owner, self.group)
+                for owner, row, cnt in recvs]
         for row, orow, cnt in local:
             win[row:row + cnt] = win[lo + orow:lo + orow + cnt]
         if ops:
