@@ -417,8 +417,9 @@ enum { SFW3D_TERM_CERTIFICATE = 0, SFW3D_TERM_ITERATION_CAP = 1, SFW3D_TERM_STAL
  * new atom, Gram rows (cached), non-negative LASSO, residual + criterion,
  * prune, duplicate guard, slide(s), final re-check — driven by a C++
  * controller on the calling thread. arena_dev: caller-owned device memory of
- * arena_volumes >= max_outer_iterations + 3 volumes of `dtype` (residual,
- * scratch, one phi per atom). rows_out: max_outer_iterations x 6 doubles
+ * arena_volumes volumes of `dtype` (residual, scratch, one phi per atom:
+ * max_outer_iterations + 2 always suffice; SFW3D_ENOMEM if the atoms outgrow a
+ * smaller arena). rows_out: max_outer_iterations x 6 doubles
  * (w, m, sigma, d); records: max_outer_iterations entries. */
 int sfw3d_solve(sfw3d_ctx* ctx, const sfw3d_psf* psf, const sfw3d_table* table, int dtype,
                 const void* y_dev, const sfw3d_solve_options* opts, void* arena_dev,

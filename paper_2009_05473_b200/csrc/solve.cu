@@ -295,7 +295,7 @@ extern "C" int sfw3d_solve(sfw3d_ctx* ctx, const sfw3d_psf* psf, const sfw3d_tab
   SFW3D_CHECK_ARG(dtype == SFW3D_F32 || dtype == SFW3D_F64, "dtype");
   SFW3D_CHECK_ARG(opts->lam > 0.0, "lam must be > 0");
   SFW3D_CHECK_ARG(opts->max_outer_iterations >= 1, "max_outer_iterations must be >= 1");
-  SFW3D_CHECK_ARG(arena_volumes >= opts->max_outer_iterations + 3, "arena too small");
+  SFW3D_CHECK_ARG(arena_volumes >= 3, "arena too small");  // (SFW3D_ENOMEM when atoms outgrow it)
   SFW3D_CHECK_ARG(opts->sigma_grid && opts->shape_grid && opts->n_sigma > 0 && opts->n_shape > 0, "grids");
   Loop L{ctx, psf, table, dtype, y_dev, opts};
   for (int a = 0; a < 3; ++a) L.dims[a] = psf->dims[a];

@@ -91,3 +91,11 @@ def test_objective_exception_propagates():
         raise FloatingPointError("non-finite certificate value")
     with pytest.raises(FloatingPointError):
         O.minimize(bad, [0.0, 0.0], [(-1, 1)] * 2)
+
+
+def test_invalid_arguments_raise_value_error():
+    f = lambda x: (float(x @ x), 2 * x)
+    with pytest.raises(ValueError):
+        O.minimize(f, [0.0, 0.0], [(1.0, -1.0), (0.0, 1.0)])  # lower bound above upper
+    with pytest.raises(ValueError):
+        O.minimize(f, [0.0], [(0.0, 1.0)], gtol=-1.0)
