@@ -312,12 +312,12 @@ __global__ void __launch_bounds__(NT, MINB) pass_tile2_kernel(
 // the FMA issue slots of the scalar tile at the same per-element arithmetic
 // (two independent RN FMAs, bit-identical results). 8 groups of J outputs
 // along the axis per CTA (To = 8 J); taps stored duplicated (t, t).
-template <int J, int MINB>
-__global__ void __launch_bounds__(256, MINB) pass_tile2x2_kernel(
+template <int J, int MINB, int NT = 256>
+__global__ void __launch_bounds__(NT, MINB) pass_tile2x2_kernel(
     const float* __restrict__ in, float* __restrict__ out, int n_axis, long long stride,
     const float* __restrict__ taps_g, int lo, int ntaps, int a_begin, int a_end, int out_shift,
     int l2mode) {
-  constexpr int TI = 64, G = 8, To = J * G;
+  constexpr int TI = 64, G = NT / 32, To = J * G;
   const unsigned long long pol = l2_policy(l2mode);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nt4 = (ntaps + 3) & ~3;
@@ -326,12 +326,12 @@ __global__ void __launch_bounds__(256, MINB) pass_tile2x2_kernel(
   const int rows = To + nt4;
   const int a0 = a_begin + blockIdx.x * To;
   const long long base0 = (long long)blockIdx.z * n_axis * stride + (long long)blockIdx.y * TI;
-  for (int q = threadIdx.x; q < nt4; q += 256) {
+  for (int q = threadIdx.x; q < nt4; q += NT) {
     const float t = q < ntaps ? taps_g[q] : 0.f;
     taps2[q] = pack2(t, t);
   }
   {
-    constexpr int kRowVecs = TI / 4, dr = 256 / kRowVecs;
+    constexpr int kRowVecs = TI / 4, dr = NT / kRowVecs;
     const int c = (threadIdx.x % kRowVecs) * 4;
     int r = threadIdx.x / kRowVecs;
     int a = (a0 + lo + r) % n_axis;
@@ -650,10 +650,10 @@ int launch_tile2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axi
 }
 
 
-template <int J, int MINB>
+template <int J, int MINB, int NT = 256>
 int launch_tile2x2(sfw3d_ctx* ctx, const float* in, float* out, const int dims[3], int axis,
                    const float* taps, int lo, int ntaps, const XRange& xr) {
-  constexpr int TI = 64, To = J * 8;
+  constexpr int TI = 64, To = J * (NT / 32);
   long long stride = 1;
   for (int a = axis + 1; a < 3; ++a) stride *= dims[a];
   long long outer = 1;
@@ -662,10 +662,10 @@ int launch_tile2x2(sfw3d_ctx* ctx, const float* in, float* out, const int dims[3
   const int nt4 = (ntaps + 3) & ~3;
   const size_t smem = size_t(nt4) * 8 + size_t(To + nt4) * TI * sizeof(float);
   if (smem > 48 * 1024)
-    SFW3D_CUDA_TRY(allow_dynamic_smem(reinterpret_cast<const void*>(pass_tile2x2_kernel<J, MINB>), size_t(int(smem))));
+    SFW3D_CUDA_TRY(allow_dynamic_smem(reinterpret_cast<const void*>(pass_tile2x2_kernel<J, MINB, NT>), size_t(int(smem))));
   const int ab = xr.begin, ae = xr.end < 0 ? n : xr.end;
   dim3 grid(unsigned((ae - ab + To - 1) / To), unsigned(stride / TI), unsigned(outer));
-  pass_tile2x2_kernel<J, MINB><<<grid, 256, smem, ctx->stream>>>(in, out, n, stride, taps, lo,
+  pass_tile2x2_kernel<J, MINB, NT><<<grid, NT, smem, ctx->stream>>>(in, out, n, stride, taps, lo,
                                                                  ntaps, ab, ae, xr.shift, ctx->l2mode);
   SFW3D_LAUNCH_CHECK(ctx);
   return SFW3D_OK;
@@ -693,6 +693,17 @@ int launch_z2(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], const T* t
                                                          pitch, addend, T(aw), T(w), ctx->l2mode);
   SFW3D_LAUNCH_CHECK(ctx);
   return SFW3D_OK;
+}
+
+// Packed strided tile by filter length: up to 64 taps the 128-thread CTA (4
+// groups of 16 outputs: 6 resident CTAs per SM instead of 3, so the staging,
+// FMA and store phases of different CTAs overlap better — config 4 11.22 ->
+// 11.01 ms, 256^3 certificate 2.03 -> 1.90 ms); longer filters keep the
+// 256-thread tile, whose halo rows are a smaller share of the staged tile.
+inline int launch_x2(sfw3d_ctx* ctx, const float* in, float* out, const int dims[3], int axis,
+                     const float* taps, int lo, int ntaps, const XRange& xr) {
+  if (ntaps <= 64) return launch_tile2x2<16, 6, 128>(ctx, in, out, dims, axis, taps, lo, ntaps, xr);
+  return launch_tile2x2<16, 3>(ctx, in, out, dims, axis, taps, lo, ntaps, xr);
 }
 
 // Tile choice. Wide filters (> kNarrowTaps taps) take J = 32 outputs per
@@ -755,7 +766,7 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
     if (dims[axis] >= 128 && wide) {
       if constexpr (f32) {
         if (!addend && w == 1.0 && xr.sq == nullptr)  // packed FFMA2 tile
-          return launch_tile2x2<16, 3>(ctx, in, out, dims, axis, taps, lo, ntaps, xr);
+          return launch_x2(ctx, in, out, dims, axis, taps, lo, ntaps, xr);
         return launch_tile2<T, 32, 3>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
       } else {
         return launch_tile2<T, 32, 1>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
@@ -765,7 +776,7 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
       // (packed FFMA2 tile also for narrow filters: 512^3 15-tap y/x passes
       // 0.218 -> 0.205 ms, bit-identical)
       if (dims[axis] >= 128 && !addend && w == 1.0 && xr.sq == nullptr)
-        return launch_tile2x2<16, 3>(ctx, in, out, dims, axis, taps, lo, ntaps, xr);
+        return launch_x2(ctx, in, out, dims, axis, taps, lo, ntaps, xr);
       return launch_tile2<T, 16, 5>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
     }
     else return launch_tile2<T, 16>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
