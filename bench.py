@@ -721,7 +721,8 @@ def solve_workload(dev, algo: str = "bsfw", cpu: bool = True):
            "split_s": {"certificate": res.trace.step_time("certificate"),
                        "lasso": res.trace.step_time("lasso"),
                        "descent": res.trace.step_time("descent"),
-                       "table": res.trace.t_table}}
+                       "table": res.trace.t_table},
+           "path": "sfw3d_solve (outer loop, L-BFGS-B ascent and slide inside the library)"}
     if algo == "bsfw":
         out.update({"reference_atoms": int(g["rows"].shape[0]), "reference_criterion": float(g["C"]),
                     "reference_cpu_s_build_container": float(g["t_total"])})
@@ -754,6 +755,7 @@ def solve_recipe_workload(config: int, algo: str):
     desc = {2: "128^3 f64, N=20, 30 candidates", 3: "256^3 fp32, N=100, 48 candidates"}[config]
     return {"metric": f"{algo.upper()} solve time, config {config} ({desc})",
             "value": r["solve_s"], "unit": "s", "higher_is_better": False,
+            "path": "sfw3d_solve (outer loop, L-BFGS-B ascent and slide inside the library)",
             **{k: r[k] for k in ("outer_iterations", "atoms", "termination", "criterion",
                                  "truth_atoms", "truth_matched_within_2vox", "split_s",
                                  "setup_s")}}
