@@ -760,6 +760,11 @@ int pass_typed(sfw3d_ctx* ctx, const T* in, T* out, const int dims[3], int axis,
     // the 64-plane tile: 2 groups of 32 instead of 4)
     const int range = (xr.end < 0 ? dims[axis] : xr.end) - xr.begin;
     if (dims[axis] >= 128 && wide && range <= 64) {
+      if constexpr (f32) {
+        // (the 64-output packed tile is exactly an 8-rank slab of 512 planes)
+        if (!addend && w == 1.0 && xr.sq == nullptr && ntaps <= 64)
+          return launch_tile2x2<16, 6, 128>(ctx, in, out, dims, axis, taps, lo, ntaps, xr);
+      }
       if constexpr (f32) return launch_tile2<T, 32, 5, 128>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
       else return launch_tile2<T, 32, 1, 128>(ctx, in, out, dims, axis, taps, lo, ntaps, addend, aw, w, xr);
     }
