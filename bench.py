@@ -65,6 +65,16 @@ def parse():
     return ap.parse_args()
 
 
+def workload_config(n: int, n_cand: int) -> dict:
+    """The workload both arms run (BASELINE.json config 4), identical in both lines."""
+    return {"workload": f"cfg4 certificate: {n}^3 fp32 residual (N(0,1) + 200 blurred "
+                        f"generalized Gaussians) x {n_cand} (sigma,d) candidates, PSF sigma_h=3 "
+                        "31^3, eta at every voxel + global argmax",
+            "grid": n, "candidates": n_cand,
+            "l2": f"inputs larger than L2 ({4 * n ** 3 / 2 ** 20:.0f} MiB residual per step)"
+                  if 4 * n ** 3 > 126e6 else "residual smaller than L2 (reduced-size run)"}
+
+
 # ----------------------------------------------------------------- clocks
 class Clocks:
     """SM clock + throttle-reason sampling during the timed region
@@ -257,9 +267,9 @@ def reference_arm(args):
         "unit": "voxel-candidates/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"cfg4 certificate {args.n}^3 x {n_cand} candidates (FFT "
-                               "eta_field, oracle port of sfw3d certificate.py:140-184) on the "
-                               "host residual configs.cfg4_residual_host (same array as the GPU arm)"},
+        "config": workload_config(args.n, n_cand),
+        "reference_impl": "FFT eta_field, oracle port of sfw3d certificate.py:140-184, on the host "
+                          "residual configs.cfg4_residual_host (the same array as the GPU arm)",
         "cpu_baseline": {"value": value, "unit": "voxel-candidates/s", "cores": threads,
                          "kind": "port",
                          "sample": f"all {n_cand} candidates x {args.n}^3 per step (threads over "
@@ -827,16 +837,12 @@ def main():
             "unit": "voxel-candidates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"cfg4 certificate: {args.n}^3 fp32 residual (N(0,1) + 200 "
-                                   "blurred generalized Gaussians) x 16 (sigma,d) candidates, "
-                                   "PSF sigma_h=3 31^3, eta at every voxel + global argmax",
-                       "grid": args.n, "candidates": res["table"]["n_cand"],
-                       "tap_tol": args.tap_tol, "mode": args.mode,
-                       "parallelism": (f"x-slabs x{world}: each rank holds its own planes; halos "
-                                       "exchanged (NCCL P2P) before every x pass, refinement "
-                                       "thresholds all-reduced, per-candidate records all-gathered")
-                       if world > 1 else "single GPU",
-                       "l2": "inputs larger than L2 (512 MiB residual, 0.9 GiB padded copy)"},
+            "config": workload_config(args.n, res["table"]["n_cand"]),
+            "run": {"tap_tol": args.tap_tol, "mode": args.mode,
+                    "parallelism": (f"x-slabs x{world}: each rank holds its own planes; halos "
+                                    "exchanged (NCCL P2P) before every x pass, refinement "
+                                    "thresholds all-reduced, per-candidate records all-gathered")
+                    if world > 1 else "single GPU"},
             "gpu_launches": res["launches"], "clocks": res["clocks"], "roofline": res["roofline"],
             "cpu_baseline": cpu, "e2e": res["e2e"], "kernel_ms_per_step": res["kernel_ms"],
             "table": res["table"], "argmax": res["best"], "parity": parity,
