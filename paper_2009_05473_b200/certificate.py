@@ -295,6 +295,53 @@ def refine_eta_max_dev(residual, lam: float, psf: Psf, start: AtomParams, bounds
     return clamp_to_domain(AtomParams.from_array(theta), bounds), float(eta.value)
 
 
+def refine_eta_max_multistart(residual, lam: float, psf: Psf, starts, bounds: DomainBounds,
+                              max_iter: int = 200, gtol: float = 1e-8, back=None):
+    """Batched multi-start ascent: every start runs its own
+    in-library L-BFGS-B on its own CUDA stream / library context from a host
+    thread (the C calls release the GIL), all against ONE back-projection
+    H^T r; the best refined (theta, eta) wins, ties to the earlier start. Not
+    the reference's semantics — it refines only the grid argmax
+    (certificate.py:227-236) — so the solvers do not use it by default; it is
+    the tool for callers who want the ascent to escape a poor grid seed."""
+    import threading
+    import torch
+    if lam <= 0.0:
+        raise ValueError(f"lam must be > 0, got {lam}")
+    starts = list(starts)
+    if not starts:
+        raise ValueError("at least one start is required")
+    if back is None:
+        back = psf_apply_dev(psf, residual, True)
+    dev = back.device
+    ready = torch.cuda.Event()
+    ready.record(torch.cuda.current_stream(dev))
+    out, err = [None] * len(starts), []
+
+    def run(i):
+        try:
+            stream = torch.cuda.Stream(dev)
+            with torch.cuda.stream(stream):
+                stream.wait_event(ready)
+                out[i] = refine_eta_max_dev(residual, lam, psf, starts[i], bounds, max_iter, gtol,
+                                            back=back)
+        except BaseException as exc:
+            err.append(exc)
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(len(starts))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if err:
+        raise err[0]
+    best = 0
+    for i in range(1, len(out)):
+        if out[i][1] > out[best][1]:
+            best = i
+    return out[best]
+
+
 def _refine_scipy(ctx, back, lam, start, bounds, max_iter, gtol):
     """certificate.py:201-224 with scipy's L-BFGS-B driving the device evaluations."""
     from .forward import code_of
@@ -334,6 +381,20 @@ def certificate_max(residual: Volume, lam: float, table: AtomTemplateTable, psf:
     if residual.dims != table.dims:
         raise ValueError(f"dims mismatch: residual {residual.dims} vs table {table.dims}")
     return certificate_max_dev(to_dev(residual), lam, table, psf, bounds)
+
+
+def certificate_max_multistart_dev(residual, lam, table, psf, bounds, n_starts: int = 4):
+    """Grid scan, then the batched multi-start ascent from the n_starts best
+    per-candidate grid maxima (the reference's single start is the first)."""
+    window = _position_window(bounds, table.dims)
+    best, per, _ = eta_argmax_dev(residual, lam, table, window)
+    nd = len(table.shape_grid)
+    order = sorted(range(len(per)), key=lambda c: (-per[c].value, c))
+    order = [int(best.cand)] + [c for c in order if c != int(best.cand)]
+    starts = [AtomParams(m=tuple(float(v) for v in per[c].pos),
+                         sigma=float(table.sigma_grid[c // nd]), d=float(table.shape_grid[c % nd]))
+              for c in order[:max(1, n_starts)]]
+    return refine_eta_max_multistart(residual, lam, psf, starts, bounds)
 
 
 def certificate_max_dev(residual, lam, table, psf, bounds, info: dict | None = None):

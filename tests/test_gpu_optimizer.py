@@ -189,3 +189,21 @@ def test_residual_with_supports_is_bit_identical(P, case, prec):
         assert ss.value == ss_ref
     finally:
         P.set_precision("f64")
+
+
+def test_multistart_refine_at_least_the_single_start(P, case):
+    """Batched multi-start ascent: concurrent in-library L-BFGS-B runs (one
+    stream / context per start) against one back-projection; the first start
+    is the reference's grid argmax, so the result can only be >= its ascent."""
+    from paper_2009_05473_b200.certificate import (certificate_max_dev,
+                                                   certificate_max_multistart_dev)
+    from paper_2009_05473_b200.forward import to_dev
+    table = P.build_template_table(case["psf"], *case["grids"])
+    y = to_dev(P.Volume(case["y"]))
+    th1, eta1 = certificate_max_dev(y, case["lam"], table, case["psf"], case["bounds"])
+    thm, etam = certificate_max_multistart_dev(y, case["lam"], table, case["psf"], case["bounds"], 6)
+    assert etam >= eta1 * (1 - 1e-12)
+    th_one, eta_one = certificate_max_multistart_dev(y, case["lam"], table, case["psf"],
+                                                     case["bounds"], 1)
+    np.testing.assert_allclose(th_one.to_array(), th1.to_array(), rtol=0, atol=1e-12)
+    assert eta_one == eta1
