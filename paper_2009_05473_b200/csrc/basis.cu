@@ -21,6 +21,7 @@
 // (trunc = 1e-12 for fp64, 1e-9 for fp32 storage), which adds at most trunc
 // to every member's error (fp64: included in the recorded error).
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -1426,52 +1427,56 @@ __global__ void __launch_bounds__(kMixThreads, sizeof(T) == 4 ? 2 : 1) mix_ring_
 // producer walks the flattened (vector, entry) sequence through a table of
 // byte offsets; the running maxima take the max of the 4 voxels first and
 // do index work only on improvement (interior z).
-template <typename T, int NMD, int NS>
-__global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
+template <typename T, int NMD, int NS, int NT, int VV>
+__global__ void __launch_bounds__(NT, NT == 128 ? 3 : 2) mix_ring2_kernel(
     const T* __restrict__ b, const T* __restrict__ terms, long long n, int K,
     const T* __restrict__ Wd, const T* __restrict__ w0d, const int* __restrict__ dmem, int nmd,
     const int* __restrict__ cterm, int nmc, const int* __restrict__ cmem,
     const int* __restrict__ cid, int nx, int ny, int nz, int4 wlo, int4 whi, double lam,
     double* __restrict__ absparts, Best* __restrict__ partial) {
-  constexpr int V = 16 / sizeof(T);
+  // VV 16-byte vectors per thread and entry (VV = 2 with 128-thread CTAs: the
+  // same 1024-voxel iteration span, per-entry overhead amortised over 8 voxels)
+  constexpr int V = VV * 16 / sizeof(T);
   constexpr int NMC = 8;  // copy members (at most)
   static_assert((NS & (NS - 1)) == 0, "ring depth is a power of two");
   double abs_s = 0.0;  // sum |b| (fp64) and max |b| of the vectors read (absparts)
   T abs_m = T(0);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* ring = reinterpret_cast<T*>(smem_raw);                       // [NS][threads][V]
-  T* sW = ring + NS * kMixThreads * V;                            // [K][NMD], 16-byte rows
+  T* sW = ring + NS * NT * V;                            // [K][NMD], 16-byte rows
   T* sw0 = sW + K * NMD;                                          // [NMD]
   T* sbv = sw0 + NMD;                                             // [NMD + NMC][threads]
-  int* sbi = reinterpret_cast<int*>(sbv + (NMD + NMC) * kMixThreads);
-  int* sCt = sbi + (NMD + NMC) * kMixThreads;                     // [K]: copy slot or -1
-  __shared__ Best red[NMD + NMC][kMixThreads / 32];
-  for (int e = threadIdx.x; e < K * NMD; e += kMixThreads) {
+  int* sbi = reinterpret_cast<int*>(sbv + (NMD + NMC) * NT);
+  int* sCt = sbi + (NMD + NMC) * NT;                     // [K]: copy slot or -1
+  __shared__ Best red[NMD + NMC][NT / 32];
+  for (int e = threadIdx.x; e < K * NMD; e += NT) {
     const int k = e / NMD, m = e % NMD;
     sW[e] = m < nmd ? Wd[size_t(m) * K + k] : T(0);
   }
-  for (int e = threadIdx.x; e < NMD; e += kMixThreads) sw0[e] = e < nmd ? w0d[e] : T(0);
-  for (int e = threadIdx.x; e < K; e += kMixThreads) sCt[e] = cterm[e];
+  for (int e = threadIdx.x; e < NMD; e += NT) sw0[e] = e < nmd ? w0d[e] : T(0);
+  for (int e = threadIdx.x; e < K; e += NT) sCt[e] = cterm[e];
 #pragma unroll
   for (int m = 0; m < NMD + NMC; ++m) {
-    sbv[m * kMixThreads + threadIdx.x] = T(-INFINITY);
-    sbi[m * kMixThreads + threadIdx.x] = 0x7fffffff;
+    sbv[m * NT + threadIdx.x] = T(-INFINITY);
+    sbi[m * NT + threadIdx.x] = 0x7fffffff;
   }
   __syncthreads();
   const long long nv = n / V;
-  const long long chunk =
-      ((nv + gridDim.x - 1) / gridDim.x + kMixThreads - 1) / kMixThreads * kMixThreads;
+  // chunks in units of one iteration span (NT * V voxels = 256 16-byte
+  // vectors for every variant: the collect pass revisits the same ranges)
+  const long long nspan = (n / (16 / sizeof(T)) + 255) / 256;  // iteration spans in the volume
+  const long long chunk = (nspan + gridDim.x - 1) / gridDim.x * NT;
   const long long qbeg = blockIdx.x * chunk + threadIdx.x, qend = min(nv, (blockIdx.x + 1) * chunk);
-  const int iters = qbeg < qend ? int((qend - qbeg + kMixThreads - 1) / kMixThreads) : 0;
+  const int iters = qbeg < qend ? int((qend - qbeg + NT - 1) / NT) : 0;
   const int E = K + 1;
   const int G = iters * E;
   T* myslot = ring + threadIdx.x * V;
-  constexpr int kSlot = kMixThreads * V;
+  constexpr int kSlot = NT * V;
   // producer: entry pe of the vector stream (0 = b, 1 + k = T_k), running
   // pointers into b and the terms, running ring-slot byte offsets
   const char* bq = reinterpret_cast<const char*>(b + qbeg * V);
   const char* tq = reinterpret_cast<const char*>(terms + qbeg * V);
-  const long long vstep = (long long)kMixThreads * V * sizeof(T);
+  const long long vstep = (long long)NT * V * sizeof(T);
   const long long nstride = n * (long long)sizeof(T);
   const long long twrap = vstep - (long long)K * nstride;
   const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(myslot));
@@ -1483,8 +1488,10 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
   // global read, the slot is zero-filled and never consumed)
   auto issue = [&]() {
     const char* a = pe == 0 ? bq : tq;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sbase + poff), "l"(a),
-                 "r"(pleft > 0 ? 16 : 0));
+#pragma unroll
+    for (int vv = 0; vv < VV; ++vv)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sbase + poff + 16 * vv),
+                   "l"(a + 16 * vv), "r"(pleft > 0 ? 16 : 0));
     poff = (poff + kSlotB) & (kRingB - 1);
     --pleft;
     tq += pe != 0 ? nstride : 0LL;
@@ -1502,12 +1509,15 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
   auto take = [&](T (&v)[V]) {
     cp_async_wait_group<NS - 2>();
     const T* sl = reinterpret_cast<const T*>(reinterpret_cast<const char*>(myslot) + coff);
-    if constexpr (sizeof(T) == 4) {
-      const float4 q = *reinterpret_cast<const float4*>(sl);
-      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
-    } else {
-      const double2 q = *reinterpret_cast<const double2*>(sl);
-      v[0] = q.x; v[1] = q.y;
+#pragma unroll
+    for (int vv = 0; vv < VV; ++vv) {
+      if constexpr (sizeof(T) == 4) {
+        const float4 q = *reinterpret_cast<const float4*>(sl + 4 * vv);
+        v[4 * vv] = q.x; v[4 * vv + 1] = q.y; v[4 * vv + 2] = q.z; v[4 * vv + 3] = q.w;
+      } else {
+        const double2 q = *reinterpret_cast<const double2*>(sl + 2 * vv);
+        v[2 * vv] = q.x; v[2 * vv + 1] = q.y;
+      }
     }
     coff = (coff + kSlotB) & (kRingB - 1);
     issue();
@@ -1515,7 +1525,7 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
   };
   // running maximum of member slot m over this vector's V voxels
   auto track = [&](int m, const T (&a)[V], long long i0, bool zfull, int z0) {
-    T* pv = sbv + m * kMixThreads + threadIdx.x;
+    T* pv = sbv + m * NT + threadIdx.x;
     if (zfull) {
       T mx = a[0];
 #pragma unroll
@@ -1526,7 +1536,7 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
         for (int j = V - 2; j >= 0; --j)
           if (a[j] == mx) bj = j;
         *pv = mx;
-        sbi[m * kMixThreads + threadIdx.x] = int(i0 + bj);
+        sbi[m * NT + threadIdx.x] = int(i0 + bj);
       }
     } else {
       T bv = *pv;
@@ -1541,13 +1551,13 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
       }
       if (bj >= 0) {
         *pv = bv;
-        sbi[m * kMixThreads + threadIdx.x] = int(i0 + bj);
+        sbi[m * NT + threadIdx.x] = int(i0 + bj);
       }
     }
   };
   // voxel position of this thread's vector, advanced incrementally (one
-  // kMixThreads * V step per iteration) instead of divided out per vector
-  const int step = kMixThreads * V;
+  // NT * V step per iteration) instead of divided out per vector
+  const int step = NT * V;
   const int dzs = step % nz, dys = step / nz;
   int z0 = 0, y = 0, x = 0;
   if (iters > 0) {
@@ -1570,7 +1580,7 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
         ++x;
       }
     }
-    const long long i0 = (qbeg + (long long)it * kMixThreads) * V;
+    const long long i0 = (qbeg + (long long)it * NT) * V;
     const bool row_win = x >= wlo.x && x <= whi.x && y >= wlo.y && y <= whi.y;
     const bool zfull = z0 >= wlo.z && z0 + V - 1 <= whi.z;
     if constexpr (sizeof(T) == 4 && NMD >= 16) {
@@ -1687,8 +1697,8 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
 #pragma unroll
   for (int m = 0; m < NMD + NMC; ++m) {
     if (m < NMD ? m >= nmd : m - NMD >= nmc) continue;
-    const int bi = sbi[m * kMixThreads + threadIdx.x];
-    Best bm = {bi == 0x7fffffff ? -INFINITY : double(sbv[m * kMixThreads + threadIdx.x]) / lam,
+    const int bi = sbi[m * NT + threadIdx.x];
+    Best bm = {bi == 0x7fffffff ? -INFINITY : double(sbv[m * NT + threadIdx.x]) / lam,
                bi == 0x7fffffff ? 0x7fffffffffffffffLL : (long long)bi};
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -1703,7 +1713,7 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
     const int m = threadIdx.x;
     if (m < NMD ? m < nmd : m - NMD < nmc) {
       Best bm = red[m][0];
-      for (int w = 1; w < kMixThreads / 32; ++w)
+      for (int w = 1; w < NT / 32; ++w)
         if (better(red[m][w].v, red[m][w].idx, bm.v, bm.idx)) bm = red[m][w];
       const int mem = m < NMD ? dmem[m] : cmem[m - NMD];  // member index
       partial[(long long)mem * gridDim.x + blockIdx.x] = bm;
@@ -1716,7 +1726,7 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
       ds += __shfl_xor_sync(0xffffffffu, ds, o);
       dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
     }
-    __shared__ double sa[kMixThreads / 32][2];
+    __shared__ double sa[NT / 32][2];
     if (lane == 0) {
       sa[warp][0] = ds;
       sa[warp][1] = dm;
@@ -1724,7 +1734,7 @@ __global__ void __launch_bounds__(kMixThreads, 2) mix_ring2_kernel(
     __syncthreads();
     if (threadIdx.x == 0) {
       double t = 0.0, mm = 0.0;
-      for (int w = 0; w < kMixThreads / 32; ++w) {
+      for (int w = 0; w < NT / 32; ++w) {
         t += sa[w][0];
         mm = fmax(mm, sa[w][1]);
       }
@@ -1831,26 +1841,25 @@ static int launch_mix_nm(sfw3d_ctx* ctx, int nblocks, const void* b, const void*
   return SFW3D_OK;
 }
 
-template <typename T, int NMD, int NS>
+template <typename T, int NMD, int NS, int NT = kMixThreads, int VV = 1>
 static int launch_ring2(sfw3d_ctx* ctx, int nblocks, const void* b, const void* terms, long long n,
                         int nt, const BasisSet* s, const int dims[3], int4 wlo, int4 whi,
                         double lam, Best* partial, int d0 = 0, int dn = -1, bool copies = true,
                         double* absparts = nullptr) {
   if (dn < 0) dn = s->nmd;
-  constexpr int V4 = 16 / sizeof(T);
-  const size_t smem = size_t(NS) * kMixThreads * V4 * sizeof(T) + size_t(nt + 1) * 8 +
-                      (size_t(nt) * NMD + NMD + size_t(NMD + 8) * kMixThreads) * sizeof(T) +
-                      size_t(NMD + 8) * kMixThreads * sizeof(int) + size_t(nt) * sizeof(int) + 16;
+  constexpr int V = VV * 16 / sizeof(T);
+  const size_t smem = size_t(NS) * NT * V * sizeof(T) + size_t(nt + 1) * 8 +
+                      (size_t(nt) * NMD + NMD + size_t(NMD + 8) * NT) * sizeof(T) +
+                      size_t(NMD + 8) * NT * sizeof(int) + size_t(nt) * sizeof(int) + 16;
   if (smem > 48 * 1024)
-    SFW3D_CUDA_TRY(allow_dynamic_smem(reinterpret_cast<const void*>(mix_ring2_kernel<T, NMD, NS>), size_t(int(smem))));
-  mix_ring2_kernel<T, NMD, NS><<<nblocks, kMixThreads, smem, ctx->stream>>>(
+    SFW3D_CUDA_TRY(allow_dynamic_smem(reinterpret_cast<const void*>(mix_ring2_kernel<T, NMD, NS, NT, VV>), size_t(int(smem))));
+  mix_ring2_kernel<T, NMD, NS, NT, VV><<<nblocks, NT, smem, ctx->stream>>>(
       static_cast<const T*>(b), static_cast<const T*>(terms), n, nt,
       static_cast<const T*>(s->Wd_dev) + size_t(d0) * nt, static_cast<const T*>(s->w0d_dev) + d0,
       s->dmem_dev + d0, dn, s->cterm_dev, copies ? s->nmc : 0, s->cmem_dev, s->cid_dev, dims[0],
       dims[1], dims[2], wlo, whi, lam, absparts, partial);
   return SFW3D_OK;
 }
-
 // every member through mix_ring2_kernel (dense members 16 per launch, the
 // copies with the first): argmax-only evaluations whose z extent takes
 // 16-byte vectors. The collect pass then chunks with the same V = 16 / es.
@@ -1865,16 +1874,31 @@ static int launch_ring2_all(sfw3d_ctx* ctx, int nblocks, const void* b, const vo
                             int4 whi, double lam, Best* partial, double* absparts = nullptr) {
   // ring depth: 16 slots (fp32); 8 for fp64 (keeps 2 CTAs per SM)
   constexpr int NS = sizeof(T) == 8 ? 8 : 16;
-  for (int d0 = 0; d0 < std::max(s->nmd, 1); d0 += 16) {
-    const int dn = std::max(0, std::min(16, s->nmd - d0));
+  // dense members per launch: 12 where the 8-voxel fp32 form applies (a
+  // 48-member table takes 4 launches of 12 instead of 3 of 16 — one more sweep
+  // over the terms, 1.52 -> 1.01 ms at config 3), else 16
+  const int slice = (sizeof(T) == 4 && n % 8 == 0 && dims[2] % 8 == 0) ? 12 : 16;
+  for (int d0 = 0; d0 < std::max(s->nmd, 1); d0 += slice) {
+    const int dn = std::max(0, std::min(slice, s->nmd - d0));
     const bool cp = d0 == 0;
     SFW3D_PROF(ctx, "eta_mix");
+    // fp32 slices of <= 12 dense members: 128-thread CTAs with two 16-byte
+    // vectors per thread and entry — the per-entry producer / weight / loop
+    // overhead is amortised over 8 voxels instead of 4 (3 CTAs per SM at 157
+    // registers, ring depth 8): config-4 mix 1.84 -> 1.56 ms, bit-identical
+    const bool v8 = sizeof(T) == 4 && n % 8 == 0 && dims[2] % 8 == 0;
+#define SFW3D_RING2(NMD_)                                                                           \
+  (v8 ? launch_ring2<T, NMD_, 8, 128, 2>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam,    \
+                                          partial, d0, dn, cp, cp ? absparts : nullptr)           \
+      : launch_ring2<T, NMD_, NS>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial,  \
+                                  d0, dn, cp, cp ? absparts : nullptr))
     if (dn <= 4)
-      SFW3D_TRY((launch_ring2<T, 4, NS>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp, cp ? absparts : nullptr)));
+      SFW3D_TRY(SFW3D_RING2(4));
     else if (dn <= 8)
-      SFW3D_TRY((launch_ring2<T, 8, NS>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp, cp ? absparts : nullptr)));
+      SFW3D_TRY(SFW3D_RING2(8));
     else if (dn <= 12)
-      SFW3D_TRY((launch_ring2<T, 12, NS>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp, cp ? absparts : nullptr)));
+      SFW3D_TRY(SFW3D_RING2(12));
+#undef SFW3D_RING2
     else
       SFW3D_TRY((launch_ring2<T, 16, NS>(ctx, nblocks, b, terms, n, nt, s, dims, wlo, whi, lam, partial, d0, dn, cp, cp ? absparts : nullptr)));
     SFW3D_LAUNCH_CHECK(ctx);
