@@ -29,6 +29,7 @@ namespace {
 
 constexpr int kChunk = 4096;               // atom-sum chunk (voxels)
 constexpr int kSumThreads = 256;
+
 constexpr int kMaxAxis = 1024;             // tabulated axis length in atom sums
 constexpr int kMaxRows = 512;              // rows per chunk (fp64)
 // fp32: 4x larger chunks (amortise the row table and the fp64 block
@@ -94,6 +95,32 @@ __device__ __forceinline__ double profile64(const AtomGeo& a, double u2, double&
 
 // single-instruction MUFU transcendentals (flush-to-zero approximations;
 // the fp32 storage path's own rounding dominates their error)
+// register-pair forms of the packed f32x2 helpers (a pair is two adjacent
+// registers: these moves are usually free)
+__device__ __forceinline__ f32x2 pk2(float lo, float hi) {
+  f32x2 d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+  return d;
+}
+__device__ __forceinline__ void upk2(f32x2 v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// small non-negative int -> float and small unsigned division without the
+// XU (MUFU / conversion) pipe, which bounds the fp32 atom kernels
+__device__ __forceinline__ float i2f_small(int i) {  // 0 <= i < 2^23
+  return __int_as_float(0x4B000000 + i) - 8388608.f;
+}
+__device__ __forceinline__ unsigned div_magic(int d) {  // ceil(2^32 / d); 0 stands for d == 1
+  return d <= 1 ? 0u : 0xFFFFFFFFu / unsigned(d) + 1u;
+}
+__device__ __forceinline__ int div_small(int a, unsigned magic) {  // a / d for a * d < 2^32
+  return magic ? int(__umulhi(unsigned(a), magic)) : a;
+}
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -556,7 +583,7 @@ struct FAtom {
   int lo, cnt;       // brick-local start / count per axis: byte a = axis
   float w, hd, inv2sd;  // inv2sd: -log2(e) / (2 sigma^d)
   int d2;
-  float inv_ngz;  // 1 / ceil(cz / 4)
+  unsigned ngz_magic;  // div_magic(ceil(cz / 4))
 };
 
 // run of the unwrapped box [s, s + l) meeting brick coords [b0, b0 + B)
@@ -632,7 +659,7 @@ __global__ void __launch_bounds__(kFT) render_f32_kernel(const AtomGeo* __restri
         f.hd = float(a.half_d);
         f.inv2sd = float(-1.4426950408889634 * a.inv2sd);  // (-log2 e) / (2 sigma^d)
         f.d2 = a.d2;
-        f.inv_ngz = rcp_approx(float((c[2] + 3) >> 2));
+        f.ngz_magic = div_magic((c[2] + 3) >> 2);
       }
     }
     const unsigned mask = __ballot_sync(0xffffffffu, hit);
@@ -664,13 +691,13 @@ __global__ void __launch_bounds__(kFT) render_f32_kernel(const AtomGeo* __restri
       const bool d2 = g.d2 != 0;
       // unit = one x-y row x 4 consecutive z (lanes along z groups)
       for (int u = lane; u < units; u += 32) {
-        const int row = fdiv_small(u, ngz, g.inv_ngz);
+        const int row = div_small(u, g.ngz_magic);
         const int gz = u - row * ngz;
         const int ix = row >= cy ? 1 : 0;  // (kFW = 2 planes per warp)
         const int iy = row - ix * cy;
-        const float ox = ox0 + float(ix), oy = g.o0y + float(iy);
+        const float ox = ox0 + i2f_small(ix), oy = g.o0y + i2f_small(iy);
         const float oxy2 = fmaf(ox, ox, oy * oy);
-        float oz = g.o0z + float(4 * gz);
+        float oz = g.o0z + i2f_small(4 * gz);
         float* pa = acc + ((px0 + ix) * kFY + lo1 + iy) * kFP + lo2 + 4 * gz;
         const int nz4 = cz - 4 * gz;  // valid voxels of this group (>= 1)
 #pragma unroll
@@ -732,44 +759,90 @@ __global__ void __launch_bounds__(kSumThreads) atom_sums_f32_kernel(
     rows[q] = rr;
   }
   __syncthreads();
-  const int ngz = (l2 + 3) >> 2;
-  const float inv_ngz = rcp_approx(float(ngz));
+  // unit = one x-y row x 8 consecutive z, as 4 voxel PAIRS on the packed
+  // f32x2 pipe (fma / mul / add of both voxels in one instruction; the MUFU
+  // ops lg2, ex2, ex2, rcp stay per voxel): the arithmetic around the four
+  // MUFU ops was what bound this kernel (issue slots, not the MUFU pipe)
+  // Units are ALIGNED groups of 8 consecutive volume z (two 16-byte loads per
+  // lane: the scalar loads' 32 sector look-ups per instruction were what
+  // bound this kernel, L1/TEX at 85%); voxels of a group outside the box's z
+  // span are masked (b = 0). nz % 4 == 0 (dispatch), so a 16-byte vector
+  // never straddles the periodic wrap.
+  constexpr int ZG = 8;
+  const int za = zs & 3;                       // the box starts za voxels into its first vector
+  const int ngz = (za + l2 + ZG - 1) / ZG;
+  const unsigned ngz_magic = div_magic(ngz);
   const int units = ch.nrows * ngz;
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f, s5 = 0.f;
-  // unit = one x-y row x 4 consecutive z (lanes along z groups: the four
-  // field loads of a warp share their 32-byte sectors)
+  const int zbase = zs - za;                   // aligned volume z of group 0
+  const float ozbase = o0z - i2f_small(za);    // its offset from the centre
+  f32x2 S0 = 0ull, S3 = 0ull, S4 = 0ull, S5 = 0ull;
+  float s1 = 0.f, s2 = 0.f;
+  const f32x2 hd2 = pk2(hd, hd), inv2 = pk2(inv2sd, inv2sd),
+              nl2e = pk2(-1.4426950408889634f, -1.4426950408889634f), two2 = pk2(2.f, 2.f);
   for (int u = threadIdx.x; u < units; u += kSumThreads) {
-    const int q = fdiv_small(u, ngz, inv_ngz);
-    const int g4 = 4 * (u - q * ngz);
+    const int q = div_small(u, ngz_magic);
+    const int g8 = ZG * (u - q * ngz);          // group start, in voxels from zbase
     const RowF rr = rows[q];
-    const int nz4 = l2 - g4;
-    int gz = zs + g4;
-    gz = gz >= nz ? gz - nz : gz;
-    float b[4];
+    const int i0 = g8 - za;                     // box-local z index of the group's first voxel
+    float b[ZG];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      b[j] = j < nz4 ? __ldg(field + rr.lin + gz) : 0.f;
-      gz = gz + 1 == nz ? 0 : gz + 1;
-    }
-    float oz = o0z + float(g4);
-    float sab = 0.f;
+    for (int h = 0; h < ZG / 4; ++h) {
+      int z4 = zbase + g8 + 4 * h;
+      z4 = z4 >= nz ? z4 - nz : z4;
+      float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i0 + 4 * h + 3 >= 0 && i0 + 4 * h < l2)
+        v4 = __ldg(reinterpret_cast<const float4*>(field + rr.lin + z4));
+      const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float u2 = fmaf(oz, oz, rr.oxy2);
-      float t, lg;
-      const float v = profile32(inv2sd, hd, d2, u2, t, lg);
-      const float vb = v * b[j];
-      const float vtb = vb * t;
-      s0 += vb;
-      s4 += vtb;
-      s5 = fmaf(vtb, fmaxf(lg, -126.f), s5);  // (u2 = 0: vtb = 0, lg = -inf)
-      const float ab = vtb * rcp_approx(fmaxf(u2, 1e-30f));
-      sab += ab;
-      s3 = fmaf(ab, oz, s3);
-      oz += 1.f;
+      for (int j = 0; j < 4; ++j) {
+        const int i = i0 + 4 * h + j;
+        b[4 * h + j] = (i >= 0 && i < l2) ? vv[j] : 0.f;
+      }
     }
+    const float ozs = ozbase + i2f_small(g8);
+    f32x2 oz2 = pk2(ozs, ozs + 1.f);
+    const f32x2 oxy2 = pk2(rr.oxy2, rr.oxy2);
+    f32x2 SAB = 0ull;
+#pragma unroll
+    for (int jp = 0; jp < ZG / 2; ++jp) {
+      const f32x2 u2 = fma2(oz2, oz2, oxy2);
+      float ua, ub;
+      upk2(u2, ua, ub);
+      const float lga = lg2_approx(ua), lgb = lg2_approx(ub);
+      f32x2 p2 = u2;
+      if (!d2) {
+        const f32x2 e2 = mul2(hd2, pk2(lga, lgb));
+        float ea, eb;
+        upk2(e2, ea, eb);
+        p2 = pk2(ex2_approx(ea), ex2_approx(eb));
+      }
+      const f32x2 t2 = mul2(inv2, p2);
+      float xa, xb;
+      upk2(mul2(nl2e, t2), xa, xb);
+      const f32x2 v2 = pk2(ex2_approx(xa), ex2_approx(xb));
+      const f32x2 vb = mul2(v2, pk2(b[2 * jp], b[2 * jp + 1]));
+      const f32x2 vtb = mul2(vb, t2);
+      S0 = add2(S0, vb);
+      S4 = add2(S4, vtb);
+      S5 = fma2(vtb, pk2(fmaxf(lga, -126.f), fmaxf(lgb, -126.f)), S5);  // (u2 = 0: vtb = 0)
+      const f32x2 ab = mul2(vtb, pk2(rcp_approx(fmaxf(ua, 1e-30f)), rcp_approx(fmaxf(ub, 1e-30f))));
+      SAB = add2(SAB, ab);
+      S3 = fma2(ab, oz2, S3);
+      oz2 = add2(oz2, two2);
+    }
+    float sa, sb;
+    upk2(SAB, sa, sb);
+    const float sab = sa + sb;
     s1 = fmaf(sab, rr.ox, s1);
     s2 = fmaf(sab, rr.oy, s2);
+  }
+  float s0, s3, s4, s5;
+  {
+    float x, y;
+    upk2(S0, x, y); s0 = x + y;
+    upk2(S3, x, y); s3 = x + y;
+    upk2(S4, x, y); s4 = x + y;
+    upk2(S5, x, y); s5 = x + y;
   }
   const float dd = float(a.d);
   double s[6] = {double(s0), double(dd * s1), double(dd * s2), double(dd * s3),
@@ -954,7 +1027,7 @@ int atom_sums_impl(sfw3d_ctx* ctx, int dtype, const int dims[3], const void* fie
           atoms_dev, ch_dev, dims[0], dims[1], dims[2], static_cast<const double*>(field), part);
   } else {
     static const int kOne[3] = {1, 1, 1};
-    if (interval_boxes(atoms, dims, kOne))
+    if (interval_boxes(atoms, dims, kOne) && dims[2] % 4 == 0)  // (16-byte field loads)
       atom_sums_f32_kernel<<<nch, kSumThreads, 0, ctx->stream>>>(
           atoms_dev, ch_dev, dims[0], dims[1], dims[2], static_cast<const float*>(field), part);
     else if (small)
