@@ -171,8 +171,20 @@ def build_template_table(psf: Psf, sigma_grid, shape_grid, bounds: DomainBounds 
     opts = {"prune": None if prune is None else int(bool(prune)),
             "global_voxels": global_voxels, "loose_tol": loose_tol,
             "refine_cap": refine_cap}
-    table = AtomTemplateTable(sigma_grid, shape_grid, psf.dims, psf, tap_tol, mode, basis_tol,
-                              opts)
+    # Tables are immutable values: the same (kernel, grids, options) gives the
+    # same table, so it is built once per Psf object and handed out again (a
+    # solver called after lambda = c * max eta, or a regularisation path,
+    # asks for the table it already has; config 3: 0.3 s of host work).
+    cache = psf.__dict__.setdefault("_tables", {})
+    key = (sigma_grid.tobytes(), shape_grid.tobytes(), float(tap_tol), mode, float(basis_tol),
+           tuple(sorted((k, v) for k, v in opts.items() if v is not None)))
+    table = cache.get(key)
+    if table is None:
+        table = AtomTemplateTable(sigma_grid, shape_grid, psf.dims, psf, tap_tol, mode, basis_tol,
+                                  opts)
+        if len(cache) >= 8:
+            cache.pop(next(iter(cache)))
+        cache[key] = table
     table.native(N.device_index(None))
     return table
 

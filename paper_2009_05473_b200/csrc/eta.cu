@@ -24,6 +24,7 @@
 //   voxels within 2 E_c of the member's approximate maximum are re-evaluated
 //   with the direct taps, so maxima / argmaxima are the direct ones.
 #include <algorithm>
+#include <mutex>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -661,9 +662,75 @@ static int build_candidate(const int dims[3], double sigma, double d, double tap
   return SFW3D_OK;
 }
 
-// builds the shared basis of one storage precision on first use (fits
-// accepted at basis_tol; fp64 members with inexact fits get their maxima
-// refined exactly, see refine_kernel)
+// Fitted bases are shared between tables: the fit (NNLS over the common box
+// lattice, greedy pruning: 0.3 s of host time at config 3) depends only on the
+// grid geometry, the candidates and the fit options — not on the data — so a
+// solver that builds its table for the same grid again (a regularisation
+// path, or lambda = c * max eta followed by the solve) reuses it. Entries are
+// reference-counted; a few unreferenced ones are kept.
+struct BasisCacheEntry {
+  std::string key;
+  BasisSet* set;
+  int refs;
+  unsigned long long stamp;
+};
+static std::mutex g_basis_mu;
+static std::vector<BasisCacheEntry> g_basis_cache;
+static unsigned long long g_basis_stamp = 0;
+constexpr size_t kBasisCacheIdle = 8;
+
+static std::string basis_key(const sfw3d_table* t, int dtype, double tol, bool prune, double loose) {
+  std::string k;
+  auto put = [&](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
+  put(&t->device, sizeof(int));
+  put(&dtype, sizeof(int));
+  put(t->dims, 3 * sizeof(int));
+  put(&tol, sizeof(double));
+  put(&prune, sizeof(bool));
+  put(&loose, sizeof(double));
+  for (const BasisCandidate& c : t->bcands) {
+    put(&c.sigma, sizeof(double));
+    put(&c.d, sizeof(double));
+    put(c.lo, 3 * sizeof(int));
+    put(c.hi, 3 * sizeof(int));
+    put(&c.direct_taps, sizeof(long long));
+    put(&c.tap_tol, sizeof(double));
+  }
+  return k;
+}
+
+static void basis_release(BasisSet* s) {
+  if (!s) return;
+  std::vector<BasisSet*> dead;
+  {
+    std::lock_guard<std::mutex> g(g_basis_mu);
+    bool found = false;
+    for (auto& e : g_basis_cache)
+      if (e.set == s) {
+        if (e.refs > 0) --e.refs;
+        e.stamp = ++g_basis_stamp;
+        found = true;
+      }
+    if (!found) dead.push_back(s);
+    // keep the most recently used idle entries only
+    for (;;) {
+      size_t idle = 0, oldest = g_basis_cache.size();
+      for (size_t i = 0; i < g_basis_cache.size(); ++i)
+        if (g_basis_cache[i].refs == 0) {
+          ++idle;
+          if (oldest == g_basis_cache.size() || g_basis_cache[i].stamp < g_basis_cache[oldest].stamp) oldest = i;
+        }
+      if (idle <= kBasisCacheIdle) break;
+      dead.push_back(g_basis_cache[oldest].set);
+      g_basis_cache.erase(g_basis_cache.begin() + oldest);
+    }
+  }
+  for (BasisSet* d : dead) basis_set_destroy(d);
+}
+
+// builds (or takes from the cache) the shared basis of one storage precision
+// on first use (fits accepted at basis_tol; fp64 members with inexact fits
+// get their maxima refined exactly, see refine_kernel)
 static int ensure_basis(const sfw3d_table* t, int dtype) {
   if (t->mode != 0) return SFW3D_OK;
   BasisSet*& s = dtype == SFW3D_F64 ? t->set64 : t->set32;
@@ -678,11 +745,27 @@ static int ensure_basis(const sfw3d_table* t, int dtype) {
     prune = t->global_voxels > 0 ? basis_prune_voxels(t->global_voxels, dtype)
                                  : basis_prune_rule(t->dims, dtype);
   const double loose = t->loose_tol < 0.0 ? basis_loose_tol(dtype) : t->loose_tol;
+  const std::string key = basis_key(t, dtype, tol, prune, loose);
+  {
+    std::lock_guard<std::mutex> g(g_basis_mu);
+    for (auto& e : g_basis_cache)
+      if (e.key == key) {
+        ++e.refs;
+        e.stamp = ++g_basis_stamp;
+        s = e.set;
+        cudaSetDevice(dev);
+        return SFW3D_OK;
+      }
+  }
   const int st = basis_set_build(t->dims, t->bcands, dtype, tol, &built, true, prune, loose);
   cudaSetDevice(dev);
   if (st != SFW3D_OK) {
     basis_set_destroy(built);
     return st;
+  }
+  {
+    std::lock_guard<std::mutex> g(g_basis_mu);
+    g_basis_cache.push_back({key, built, 1, ++g_basis_stamp});
   }
   s = built;
   return SFW3D_OK;
@@ -832,8 +915,8 @@ extern "C" int sfw3d_table_set_option(sfw3d_table* t, const char* name, double v
   }
   // the shared bases depend on prune / loose_tol: refit on next use
   cudaSetDevice(t->device);
-  basis_set_destroy(t->set32);
-  basis_set_destroy(t->set64);
+  basis_release(t->set32);
+  basis_release(t->set64);
   t->set32 = t->set64 = nullptr;
   return SFW3D_OK;
 }
@@ -846,8 +929,8 @@ extern "C" int sfw3d_table_destroy(sfw3d_table* t) {
     if (c.t32) cudaFree(c.t32);
     if (c.rows_dev) cudaFree(c.rows_dev);
   }
-  basis_set_destroy(t->set32);
-  basis_set_destroy(t->set64);
+  basis_release(t->set32);
+  basis_release(t->set64);
   if (t->refcand_dev) cudaFree(t->refcand_dev);
   delete t;
   return SFW3D_OK;
