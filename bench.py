@@ -738,7 +738,9 @@ def solve_workload(dev, algo: str = "bsfw", cpu: bool = True):
                        "lasso": res.trace.step_time("lasso"),
                        "descent": res.trace.step_time("descent"),
                        "table": res.trace.t_table},
-           "path": "sfw3d_solve (outer loop, L-BFGS-B ascent and slide inside the library)"}
+           "path": "sfw3d_solve (outer loop, L-BFGS-B ascent and slide inside the library)",
+           "table": "memoised per Psf and grid: built by the warm-up solve (experiment.py:487-492 "
+                    "discards one warm-up run too); `table` in split_s is the lookup"}
     if algo == "bsfw":
         out.update({"reference_atoms": int(g["rows"].shape[0]), "reference_criterion": float(g["C"]),
                     "reference_cpu_s_build_container": float(g["t_total"])})
@@ -772,6 +774,8 @@ def solve_recipe_workload(config: int, algo: str):
     return {"metric": f"{algo.upper()} solve time, config {config} ({desc})",
             "value": r["solve_s"], "unit": "s", "higher_is_better": False,
             "path": "sfw3d_solve (outer loop, L-BFGS-B ascent and slide inside the library)",
+            "table": "memoised per Psf and grid: built in setup_s by the lambda = c * max eta "
+                     "evaluation of the recipe, looked up by the solve",
             **{k: r[k] for k in ("outer_iterations", "atoms", "termination", "criterion",
                                  "truth_atoms", "truth_matched_within_2vox", "split_s",
                                  "setup_s")}}
