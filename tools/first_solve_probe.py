@@ -1,10 +1,14 @@
+"""First-call vs steady-state wall time of the config-1 BSFW solve (table and
+basis memoisation, allocator warm-up): python tools/first_solve_probe.py"""
 import sys, time
-sys.path.insert(0, '/root/repo'); sys.path.insert(0, '/root/repo/oracle')
+from pathlib import Path
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT)); sys.path.insert(0, str(ROOT / "oracle"))
 import numpy as np, torch
 import paper_2009_05473_b200 as P
 import sfw3d_oracle as O
 from paper_2009_05473_b200 import solvers
-g = np.load('/root/repo/tests/golden/config1.npz')
+g = np.load(ROOT / 'tests' / 'golden' / 'config1.npz')
 P.set_precision("f64")
 dims = (64, 64, 64)
 psf = P.Psf(P.Volume(O.box_gaussian_psf(dims, (2, 2, 2), (7, 7, 7))), normalize=False)
